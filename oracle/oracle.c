@@ -1,0 +1,187 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct sequential CPU implementation of what the
+ * hot path computes, written from the paper (arXiv 2205.11659, R. Levien,
+ * "Fast GPU bounding boxes on tree-structured scenes").  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load this library.  It shares no code, headers, tables or helpers with
+ * the CUDA path (paper_2205_11659_b200/csrc), and the CUDA path never loads it.
+ *
+ * Citations: P:n = PAPER.md line n (section in brackets).
+ * Readings of silent / ambiguous points are numbered as in DESIGN.md §3.
+ *
+ * Element tags (one byte per element of the flattened tree):
+ *   1 = open of a clip node, 2 = open of a blend node, 3 = close,
+ *   anything else (0 canonical) = leaf                     [DESIGN R2]
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { TAG_OPEN_CLIP = 1, TAG_OPEN_BLEND = 2, TAG_CLOSE = 3 };
+
+/* ------------------------------------------------------------------------ */
+/* oracle_paren_match                                                        */
+/*                                                                           */
+/* Fig. 1 (§2) run literally:                                       */
+/*     stack = [-1]                                                          */
+/*     for i in range(len(s)):                                               */
+/*         out[i] = stack[len(stack) - 1]                                    */
+/*         if inp[i] == '(':  stack.push(i)                                  */
+/*         elif inp[i] == ')': stack.pop()                                   */
+/* parent[i] := out[i]  (the "stronger" problem).                      */
+/* match[i]  := classical partner ("traditional version"), -1 if none. */
+/* A close that finds only the -1 sentinel (Fig. 1 would pop the sentinel;   */
+/* undefined in the paper) leaves the stack unchanged and gets match = -1:   */
+/* the stack-monoid semantics of §4, DESIGN R3.                  */
+/* Leaves read the top and neither push nor pop (DESIGN R2).                */
+/* Returns 0, or -1 on allocation failure.                                   */
+/* ------------------------------------------------------------------------ */
+int oracle_paren_match(const uint8_t *tags, int64_t n, int32_t *match, int32_t *parent)
+{
+    int64_t *stack = (int64_t *)malloc((size_t)(n + 1) * sizeof(int64_t));
+    if (!stack) return -1;
+    int64_t sp = 0;
+    stack[sp++] = -1;
+    for (int64_t i = 0; i < n; i++) {
+        parent[i] = (int32_t)stack[sp - 1];
+        match[i] = -1;
+        uint8_t t = tags[i];
+        if (t == TAG_OPEN_CLIP || t == TAG_OPEN_BLEND) {
+            stack[sp++] = i;
+        } else if (t == TAG_CLOSE) {
+            if (stack[sp - 1] != -1) {
+                int64_t o = stack[--sp];
+                match[i] = (int32_t)o;                  /* P:74 partner */
+                match[o] = (int32_t)i;
+            }                                            /* else: R3 */
+        }
+    }
+    free(stack);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Bounding-box algebra (§6).                                   */
+/* Boxes are (x0, y0, x1, y1) fp32.  Intersection = (max x0, max y0, min x1, */
+/* min y1); union = (min x0, min y0, max x1, max y1) — raw, never            */
+/* canonicalised (DESIGN R9).  min/max are taken in the IEEE 754-2019        */
+/* totalOrder (-NaN < -inf < ... < -0 < +0 < ... < +inf < +NaN), so every    */
+/* result is a unique bit pattern (DESIGN R12).                              */
+/* ------------------------------------------------------------------------ */
+typedef struct { float x0, y0, x1, y1; } box_t;
+
+static uint32_t f32_bits(float x) { uint32_t u; memcpy(&u, &x, 4); return u; }
+
+/* totalOrder(x, y): x is ordered at or below y.  Written from the standard's
+ * definition: a negative-signed value lies below every positive-signed one;
+ * among equal signs, larger magnitude (bit pattern without the sign, which
+ * orders finite < inf < NaN payloads) lies further from zero. */
+static int total_le(float x, float y)
+{
+    uint32_t bx = f32_bits(x), by = f32_bits(y);
+    int neg_x = (bx >> 31) != 0, neg_y = (by >> 31) != 0;
+    uint32_t mx = bx & 0x7fffffffu, my = by & 0x7fffffffu;
+    if (neg_x != neg_y) return neg_x;          /* -anything <= +anything */
+    if (!neg_x) return mx <= my;               /* both positive-signed */
+    return mx >= my;                           /* both negative-signed */
+}
+static float tmin(float x, float y) { return total_le(x, y) ? x : y; }
+static float tmax(float x, float y) { return total_le(x, y) ? y : x; }
+
+static box_t isect(box_t p, box_t q)
+{
+    box_t r = { tmax(p.x0, q.x0), tmax(p.y0, q.y0), tmin(p.x1, q.x1), tmin(p.y1, q.y1) };
+    return r;
+}
+static box_t unite(box_t p, box_t q)
+{
+    box_t r = { tmin(p.x0, q.x0), tmin(p.y0, q.y0), tmax(p.x1, q.x1), tmax(p.y1, q.y1) };
+    return r;
+}
+
+enum { KIND_ROOT = 0, KIND_CLIP = 1, KIND_BLEND = 2 };
+typedef struct { box_t clip; box_t uni; int64_t open; int kind; } entry_t;
+
+/* ------------------------------------------------------------------------ */
+/* oracle_tree_bbox                                                          */
+/*                                                                           */
+/* The sequential algorithm of the introduction (§1): walk the tree    */
+/* keeping a stack; each entry holds a clip box and a blend (union) box.     */
+/*   leaf box      = own box ∩ every clip node on the root path      */
+/*   clip open     = own box ∩ clip of the enclosing entry       (R6) */
+/*   blend node    = union of its descendant leaves' clipped boxes (P:24,    */
+/*                   P:196); a blend node has no box of its own  (R7, R8)    */
+/*   result of every node is produced at its close, and for blend    */
+/*   nodes scattered to the open as well                 (R10)       */
+/*   unmatched close -> EMPTY, stack unchanged                   (R3)        */
+/*   opens still on the stack at the end are closed implicitly    (R4)       */
+/* INF = (-inf,-inf,+inf,+inf) and EMPTY = (+inf,+inf,-inf,-inf) are the     */
+/* identities of ∩ and ∪ (R11).                                              */
+/* boxes: n*4 floats in, n*4 floats out (AoS, x0 y0 x1 y1).                  */
+/* Returns 0, or -1 on allocation failure.                                   */
+/* ------------------------------------------------------------------------ */
+int oracle_tree_bbox(const uint8_t *tags, const float *leaf_bbox, int64_t n, float *node_bbox)
+{
+    const float inf = __builtin_inff();
+    const box_t INF = { -inf, -inf, inf, inf };
+    const box_t EMPTY = { inf, inf, -inf, -inf };
+    const box_t *in = (const box_t *)leaf_bbox;
+    box_t *out = (box_t *)node_bbox;
+
+    entry_t *stack = (entry_t *)malloc((size_t)(n + 1) * sizeof(entry_t));
+    if (!stack) return -1;
+    int64_t sp = 0;
+    stack[sp].clip = INF; stack[sp].uni = EMPTY; stack[sp].open = -1; stack[sp].kind = KIND_ROOT;
+    sp++;
+
+    for (int64_t i = 0; i < n; i++) {
+        entry_t *top = &stack[sp - 1];
+        uint8_t t = tags[i];
+        if (t == TAG_OPEN_CLIP) {
+            box_t c = isect(in[i], top->clip);
+            out[i] = c;
+            entry_t e = { c, EMPTY, i, KIND_CLIP };
+            stack[sp++] = e;
+        } else if (t == TAG_OPEN_BLEND) {
+            entry_t e = { top->clip, EMPTY, i, KIND_BLEND };
+            out[i] = EMPTY;           /* overwritten when the node is closed */
+            stack[sp++] = e;
+        } else if (t == TAG_CLOSE) {
+            if (top->kind == KIND_ROOT) {
+                out[i] = EMPTY;       /* R3 */
+            } else {
+                entry_t e = stack[--sp];
+                out[i] = e.uni;
+                if (e.kind == KIND_BLEND) out[e.open] = e.uni;
+                stack[sp - 1].uni = unite(stack[sp - 1].uni, e.uni);
+            }
+        } else {                      /* leaf */
+            box_t c = isect(in[i], top->clip);
+            out[i] = c;
+            top->uni = unite(top->uni, c);
+        }
+    }
+    while (stack[sp - 1].kind != KIND_ROOT) {      /* R4: implicit closes */
+        entry_t e = stack[--sp];
+        if (e.kind == KIND_BLEND) out[e.open] = e.uni;
+        stack[sp - 1].uni = unite(stack[sp - 1].uni, e.uni);
+    }
+    free(stack);
+    return 0;
+}
+
+/* Global Bic of the whole stream (a = unmatched closes, b = unmatched opens),
+ * by the same stack walk (used by tests and the bench report only). */
+int oracle_count_unmatched(const uint8_t *tags, int64_t n, int64_t *a, int64_t *b)
+{
+    int64_t depth = 0, under = 0;
+    for (int64_t i = 0; i < n; i++) {
+        uint8_t t = tags[i];
+        if (t == TAG_OPEN_CLIP || t == TAG_OPEN_BLEND) depth++;
+        else if (t == TAG_CLOSE) { if (depth > 0) depth--; else under++; }
+    }
+    *a = under; *b = depth;
+    return 0;
+}
