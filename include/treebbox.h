@@ -1,0 +1,136 @@
+/*
+ * treebbox.h — C ABI of the B200 (sm_100a) hot path of
+ *   R. Levien, "Fast GPU bounding boxes on tree-structured scenes",
+ *   arXiv 2205.11659.
+ * Citations: P:n = PAPER.md line n (section in brackets); R<k> = reading k of
+ * DESIGN.md §3 (points the paper leaves open).
+ *
+ * Input model (§1.1): a flattened tree, one byte per element:
+ *     1 = open of a clip node, 2 = open of a blend node, 3 = close,
+ *     every other byte value = leaf (R2).
+ *
+ * Conventions shared by every entry point
+ *   - Pointers named d_* are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *     on the current CUDA device; h_* are HOST pointers.  All arrays are
+ *     caller-owned; the library never frees them.  Inputs must stay alive and
+ *     unmodified until `stream` has passed the call.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *     Everything is enqueued on it; device entry points never synchronise the
+ *     host.  Outputs are valid once the stream has reached the call.
+ *   - Return value: 0 on success, otherwise a negative TB_ERR_* code; the
+ *     message is available from tb_last_error() (thread-local).  Only
+ *     host-checkable conditions are errors.  Data-dependent situations
+ *     (unmatched closes, opens left open at the end) are NOT errors and have
+ *     defined outputs (R3, R4).
+ *   - n == 0 is a successful no-op.  n must be <= 2^31 - 1 (int32 indices,
+ *     -1 sentinel; R5).
+ *   - Alignment: d_tags, d_match, d_parent, d_leaf_bbox, d_node_bbox must be
+ *     16-byte aligned (TB_ERR_ALIGN otherwise).  Outputs must not overlap
+ *     inputs or each other (TB_ERR_ALIAS).
+ *   - Workspace: the library keeps a per-(device, stream) scratch cache grown
+ *     on demand (the growth itself synchronises the device once).  The *_ws
+ *     variants take caller-provided scratch instead (no allocation; suitable
+ *     for CUDA-graph capture); size it with *_workspace_bytes(n).
+ *   - Results are deterministic and bit-identical to the sequential
+ *     definitions (Fig. 1), whatever the tiling.
+ */
+#ifndef TREEBBOX_H
+#define TREEBBOX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TB_OK 0
+#define TB_ERR_ARG -1    /* n < 0, n > 2^31-1, null pointer with n > 0, bad size */
+#define TB_ERR_ALIGN -2  /* a pointer is not 16-byte aligned */
+#define TB_ERR_ALIAS -3  /* an output overlaps an input or another output */
+#define TB_ERR_CUDA -4   /* CUDA launch / allocation / copy error */
+#define TB_ERR_NCCL -5   /* NCCL error (sharded entry points) */
+
+/* Tag byte values (R2). */
+#define TB_LEAF 0
+#define TB_OPEN_CLIP 1
+#define TB_OPEN_BLEND 2
+#define TB_CLOSE 3
+
+/* Message for the last nonzero return on this host thread ("" if none). */
+const char *tb_last_error(void);
+
+/* Library version string. */
+const char *tb_version(void);
+
+/* ------------------------------------------------------------------------
+ * paren_match — parentheses matching (§2; §3; §4)
+ *
+ * d_tags   : device uint8[n], tag bytes as above.
+ * d_parent : device int32[n] out.  parent[i] = Fig. 1's out[i]: the
+ *            index of the innermost open enclosing element i, -1 at the root.
+ *            For a matched close this is its matching open ("stronger
+ *            version").
+ * d_match  : device int32[n] out.  Classical partner: matched opens and
+ *            closes point at each other; leaves, opens never closed (R4) and
+ *            closes with nothing to close (R3) get -1.
+ * Computation: one pass over the tags — a decoupled-look-back scan of the
+ * bicyclic monoid with stack-monoid slices per tile (P:229-233,
+ * §7.1), in-tile resolution, and cross-tile lookup by the suffix relation
+ * (P:131-138).  HBM traffic ~9 bytes/element (+ tile slices).
+ * ------------------------------------------------------------------------ */
+int paren_match(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *d_parent,
+                void *stream);
+
+size_t paren_match_workspace_bytes(int64_t n);
+/* d_workspace: device scratch of >= paren_match_workspace_bytes(n) bytes,
+ * 256-byte aligned, not used concurrently by another call. */
+int paren_match_ws(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *d_parent,
+                   void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
+ * tree_bbox — clip intersections and blend unions (§6; §9)
+ *
+ * d_tags      : device uint8[n] as above.
+ * d_leaf_bbox : device float32[n][4] (x0, y0, x1, y1).  Read for leaves and
+ *               clip opens only (blend opens and closes are ignored, R7).
+ * d_node_bbox : device float32[n][4] out:
+ *     leaf          own box ∩ every clip node on its root path
+ *     clip open     own box ∩ every clip ancestor (effective clip)   (R6)
+ *     close         raw union of the clipped leaves strictly inside
+ *                   the node, for clip and blend nodes alike          (R8, R10)
+ *     blend open    the same union, scattered to the open
+ *     unmatched     close -> EMPTY; an open never closed spans to the end (R3, R4)
+ * INF = (-inf,-inf,+inf,+inf), EMPTY = (+inf,+inf,-inf,-inf) (R11).  min/max
+ * follow IEEE 754 totalOrder (-0 < +0), so results are unique bit patterns
+ * (R12).  Boxes are never canonicalised (R9).
+ * Matching is recomputed internally (no match/parent arguments).
+ * ------------------------------------------------------------------------ */
+int tree_bbox(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, float *d_node_bbox,
+              void *stream);
+
+size_t tree_bbox_workspace_bytes(int64_t n);
+int tree_bbox_ws(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, float *d_node_bbox,
+                 void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Host-buffer variants (end-to-end API): h_* are host pointers (pinned or
+ * pageable).  Inputs are copied to library-owned device buffers on `stream`,
+ * the device call runs, outputs are copied back, and the call synchronises
+ * `stream` before returning.
+ * ------------------------------------------------------------------------ */
+int paren_match_host(const uint8_t *h_tags, int64_t n, int32_t *h_match, int32_t *h_parent,
+                     void *stream);
+int tree_bbox_host(const uint8_t *h_tags, const float *h_leaf_bbox, int64_t n, float *h_node_bbox,
+                   void *stream);
+
+/* ------------------------------------------------------------------------
+ * Validation helper: the global Bic of the stream: a = closes with
+ * nothing to close, b = opens left open at the end.  Synchronises `stream`.
+ * ------------------------------------------------------------------------ */
+int tb_count_unmatched(const uint8_t *d_tags, int64_t n, int64_t *h_a, int64_t *h_b, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TREEBBOX_H */

@@ -1,0 +1,160 @@
+"""paper_2205_11659_b200 — B200 (sm_100a) hot path of Levien's tree bounding boxes.
+
+Thin Python binding over the C ABI in ``include/treebbox.h``
+(``libtreebbox.so``, built in-tree from ``csrc/``).  This module only
+marshals arguments (torch CUDA tensors -> device pointers + current stream);
+every step of the computation runs in the CUDA kernels.  There is no CPU or
+PyTorch fallback: if the extension cannot be loaded, calls raise.
+
+    match, parent = paren_match(tags)               # §2-§8 of the paper
+    node_bbox     = tree_bbox(tags, leaf_bbox)      # §6, §9
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from . import build as _build
+
+__all__ = ["paren_match", "tree_bbox", "paren_match_host", "tree_bbox_host", "count_unmatched",
+           "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes"]
+
+LIB_PATH = _build.LIB
+_lock = threading.Lock()
+_lib = None
+
+
+class TreeBBoxError(RuntimeError):
+    pass
+
+
+def load():
+    """Load (building first if the sources are newer) libtreebbox.so."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if _build.needs_build():
+                _build.build()
+            lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+            P, I64, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t
+            sigs = {
+                "tb_last_error": ([], ctypes.c_char_p),
+                "tb_version": ([], ctypes.c_char_p),
+                "paren_match": ([P, I64, P, P, P], ctypes.c_int),
+                "paren_match_ws": ([P, I64, P, P, P, SZ, P], ctypes.c_int),
+                "paren_match_workspace_bytes": ([I64], SZ),
+                "paren_match_host": ([P, I64, P, P, P], ctypes.c_int),
+                "tree_bbox": ([P, P, I64, P, P], ctypes.c_int),
+                "tree_bbox_ws": ([P, P, I64, P, P, SZ, P], ctypes.c_int),
+                "tree_bbox_workspace_bytes": ([I64], SZ),
+                "tree_bbox_host": ([P, P, I64, P, P], ctypes.c_int),
+                "tb_count_unmatched": ([P, I64, P, P, P], ctypes.c_int),
+            }
+            for name, (args, res) in sigs.items():
+                fn = getattr(lib, name, None)
+                if fn is None:
+                    continue
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = load().tb_last_error().decode(errors="replace")
+        raise TreeBBoxError(f"treebbox error {rc}: {msg}")
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _need_cuda(t: torch.Tensor, name: str, dtype):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def paren_match(tags: torch.Tensor, match: torch.Tensor | None = None,
+                parent: torch.Tensor | None = None):
+    """Parentheses matching on the GPU.  tags: uint8 CUDA [n].
+
+    Returns (match, parent), int32 CUDA [n] (see include/treebbox.h)."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    n = tags.numel()
+    if match is None:
+        match = torch.empty(n, dtype=torch.int32, device=tags.device)
+    if parent is None:
+        parent = torch.empty(n, dtype=torch.int32, device=tags.device)
+    _need_cuda(match, "match", torch.int32)
+    _need_cuda(parent, "parent", torch.int32)
+    with torch.cuda.device(tags.device):
+        _check(lib.paren_match(tags.data_ptr(), n, match.data_ptr(), parent.data_ptr(),
+                               _stream(tags.device)))
+    return match, parent
+
+
+def tree_bbox(tags: torch.Tensor, leaf_bbox: torch.Tensor, node_bbox: torch.Tensor | None = None):
+    """Clip intersections + blend unions on the GPU.
+
+    tags: uint8 CUDA [n]; leaf_bbox: float32 CUDA [n, 4].  Returns float32 [n, 4]."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    _need_cuda(leaf_bbox, "leaf_bbox", torch.float32)
+    n = tags.numel()
+    if leaf_bbox.numel() != 4 * n:
+        raise ValueError("leaf_bbox must be [n, 4]")
+    if node_bbox is None:
+        node_bbox = torch.empty((n, 4), dtype=torch.float32, device=tags.device)
+    _need_cuda(node_bbox, "node_bbox", torch.float32)
+    with torch.cuda.device(tags.device):
+        _check(lib.tree_bbox(tags.data_ptr(), leaf_bbox.data_ptr(), n, node_bbox.data_ptr(),
+                             _stream(tags.device)))
+    return node_bbox
+
+
+def workspace_bytes(n: int) -> dict:
+    lib = load()
+    return {"paren_match": int(lib.paren_match_workspace_bytes(n)),
+            "tree_bbox": int(lib.tree_bbox_workspace_bytes(n))}
+
+
+def paren_match_host(tags: torch.Tensor, match: torch.Tensor, parent: torch.Tensor,
+                     device=None):
+    """End-to-end host-buffer call (copies in, computes, copies out, syncs)."""
+    lib = load()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    with torch.cuda.device(dev):
+        _check(lib.paren_match_host(tags.data_ptr(), tags.numel(), match.data_ptr(),
+                                    parent.data_ptr(), _stream(dev)))
+    return match, parent
+
+
+def tree_bbox_host(tags: torch.Tensor, leaf_bbox: torch.Tensor, node_bbox: torch.Tensor,
+                   device=None):
+    lib = load()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    with torch.cuda.device(dev):
+        _check(lib.tree_bbox_host(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(),
+                                  node_bbox.data_ptr(), _stream(dev)))
+    return node_bbox
+
+
+def count_unmatched(tags: torch.Tensor):
+    """Global Bic (a, b) of the stream, computed on the GPU (synchronises)."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    a = ctypes.c_int64(0)
+    b = ctypes.c_int64(0)
+    with torch.cuda.device(tags.device):
+        _check(lib.tb_count_unmatched(tags.data_ptr(), tags.numel(), ctypes.byref(a), ctypes.byref(b),
+                                      _stream(tags.device)))
+    return a.value, b.value

@@ -1,0 +1,165 @@
+// C ABI (include/treebbox.h): argument validation, workspace cache, launches.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "kernels.h"
+#include "treebbox.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(TB_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+constexpr int64_t kMaxN = 2147483647LL;
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + nb && y < x + na;
+}
+
+int check_n(int64_t n) {
+  if (n < 0 || n > kMaxN) return fail(TB_ERR_ARG, "n = %lld out of range [0, 2^31-1]", (long long)n);
+  return TB_OK;
+}
+
+// ---- per-(device, stream) scratch cache ---------------------------------
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_mu;
+std::map<std::pair<int, void*>, Buf> g_ws;
+
+int get_ws(void* stream, int slot, size_t need, void** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_mu);
+  Buf& b = g_ws[{dev * 16 + slot, stream}];
+  if (b.bytes < need) {
+    if (b.p) {
+      e = cudaStreamSynchronize((cudaStream_t)stream);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+      cudaFree(b.p);
+      b.p = nullptr;
+      b.bytes = 0;
+    }
+    size_t sz = need + need / 8 + 4096;
+    e = cudaMalloc(&b.p, sz);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(workspace)");
+    b.bytes = sz;
+  }
+  *out = b.p;
+  return TB_OK;
+}
+
+int pm_checks(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent) {
+  int r = check_n(n);
+  if (r) return r;
+  if (n == 0) return TB_OK;
+  if (!tags || !match || !parent) return fail(TB_ERR_ARG, "null pointer with n > 0");
+  if (!aligned16(tags) || !aligned16(match) || !aligned16(parent))
+    return fail(TB_ERR_ALIGN, "tags, match and parent must be 16-byte aligned");
+  const size_t n4 = (size_t)n * 4;
+  if (overlap(match, n4, parent, n4) || overlap(match, n4, tags, (size_t)n) ||
+      overlap(parent, n4, tags, (size_t)n))
+    return fail(TB_ERR_ALIAS, "outputs overlap each other or the input");
+  return TB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tb_last_error(void) { return g_err; }
+const char* tb_version(void) { return "treebbox-b200 0.1 (sm_100a)"; }
+
+size_t paren_match_workspace_bytes(int64_t n) { return n > 0 ? tb::pm_workspace_bytes(n) : 0; }
+
+int paren_match_ws(const uint8_t* d_tags, int64_t n, int32_t* d_match, int32_t* d_parent,
+                   void* d_workspace, size_t workspace_bytes, void* stream) {
+  g_err[0] = 0;
+  int r = pm_checks(d_tags, n, d_match, d_parent);
+  if (r || n == 0) return r;
+  if (!d_workspace || workspace_bytes < tb::pm_workspace_bytes(n))
+    return fail(TB_ERR_ARG, "workspace too small: need %zu bytes", tb::pm_workspace_bytes(n));
+  cudaError_t e = tb::pm_launch(d_tags, n, d_match, d_parent, d_workspace, nullptr, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "paren_match launch");
+  return TB_OK;
+}
+
+int paren_match(const uint8_t* d_tags, int64_t n, int32_t* d_match, int32_t* d_parent, void* stream) {
+  g_err[0] = 0;
+  int r = pm_checks(d_tags, n, d_match, d_parent);
+  if (r || n == 0) return r;
+  void* ws = nullptr;
+  const size_t need = tb::pm_workspace_bytes(n);
+  r = get_ws(stream, 0, need, &ws);
+  if (r) return r;
+  return paren_match_ws(d_tags, n, d_match, d_parent, ws, need, stream);
+}
+
+int paren_match_host(const uint8_t* h_tags, int64_t n, int32_t* h_match, int32_t* h_parent,
+                     void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r || n == 0) return r;
+  if (!h_tags || !h_match || !h_parent) return fail(TB_ERR_ARG, "null pointer with n > 0");
+  const size_t nb_t = ((size_t)n + 255) & ~(size_t)255;
+  const size_t nb_i = ((size_t)n * 4 + 255) & ~(size_t)255;
+  void* io = nullptr;
+  r = get_ws(stream, 1, nb_t + 2 * nb_i, &io);
+  if (r) return r;
+  uint8_t* d_tags = (uint8_t*)io;
+  int32_t* d_match = (int32_t*)((char*)io + nb_t);
+  int32_t* d_parent = (int32_t*)((char*)io + nb_t + nb_i);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D tags");
+  r = paren_match(d_tags, n, d_match, d_parent, stream);
+  if (r) return r;
+  e = cudaMemcpyAsync(h_match, d_match, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_parent, d_parent, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H results");
+  return TB_OK;
+}
+
+int tb_count_unmatched(const uint8_t* d_tags, int64_t n, int64_t* h_a, int64_t* h_b, void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r) return r;
+  if (!h_a || !h_b || (n > 0 && !d_tags)) return fail(TB_ERR_ARG, "null pointer");
+  void* ws = nullptr;
+  r = get_ws(stream, 2, tb::bic_count_workspace_bytes(n) + 256, &ws);
+  if (r) return r;
+  int64_t* d_out = (int64_t*)((char*)ws + tb::bic_count_workspace_bytes(n));
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = tb::bic_count_launch(d_tags, n, ws, d_out, s);
+  if (e != cudaSuccess) return cuda_fail(e, "bic_count launch");
+  int64_t h[2];
+  e = cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "bic_count readback");
+  *h_a = h[0];
+  *h_b = h[1];
+  return TB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Device helpers shared by the sm_100a kernels (NOT shared with oracle/).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tb {
+
+// ---------------------------------------------------------------------------
+// Bicyclic monoid (§3): (a,b) = (unmatched closes, unmatched opens)
+//   (a,b) ⊕ (c,d) = (a + c - min(b,c), b + d - min(b,c))
+// ---------------------------------------------------------------------------
+struct Bic {
+  int a, b;
+};
+__device__ __forceinline__ Bic bic_combine(Bic x, Bic y) {
+  int m = min(x.b, y.a);
+  return Bic{x.a + y.a - m, x.b + y.b - m};
+}
+
+// Packed look-back descriptor: [63:62] flag, [61:31] a, [30:0] b.
+enum : uint32_t { DESC_NONE = 0, DESC_AGG = 1, DESC_INC = 2 };
+__device__ __forceinline__ uint64_t desc_pack(uint32_t flag, Bic v) {
+  return ((uint64_t)flag << 62) | ((uint64_t)(uint32_t)v.a << 31) | (uint64_t)(uint32_t)v.b;
+}
+__device__ __forceinline__ uint32_t desc_flag(uint64_t d) { return (uint32_t)(d >> 62); }
+__device__ __forceinline__ Bic desc_val(uint64_t d) {
+  return Bic{(int)((d >> 31) & 0x7fffffffu), (int)(d & 0x7fffffffu)};
+}
+
+// ---------------------------------------------------------------------------
+// Memory-model helpers (PTX, gpu scope).  Cross-CTA data is published with
+// st.release after the payload is written and read with ld.acquire; payload
+// reads after an acquire use ld.relaxed.gpu / .cg so no stale L1 line is hit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_cg_s32(const int32_t* p) { return __ldcg(p); }
+
+// Spin until a published u32 slot is nonzero (values are stored +1).
+__device__ __forceinline__ uint32_t wait_u32(const uint32_t* p) {
+  uint32_t v = ld_acquire_u32(p);
+  while (v == 0) {
+    __nanosleep(32);
+    v = ld_acquire_u32(p);
+  }
+  return v;
+}
+
+// Streaming 16-byte load that does not allocate in L1.
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Per-byte classification of 4 tag bytes into a 4-bit mask (bit i <-> byte i).
+__device__ __forceinline__ uint32_t byte_mask4(uint32_t cmp /* 0xff per hit */) {
+  uint32_t m = cmp & 0x01010101u;
+  return (m * 0x01020408u) >> 24;
+}
+// 16 tag bytes -> (open mask, close mask), bit i <-> element i.
+__device__ __forceinline__ void classify16(uint4 w, uint32_t& om, uint32_t& cm) {
+  uint32_t o = 0, c = 0;
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    uint32_t x = ws[q];
+    uint32_t op = __vcmpeq4(x, 0x01010101u) | __vcmpeq4(x, 0x02020202u);
+    uint32_t cl = __vcmpeq4(x, 0x03030303u);
+    o |= byte_mask4(op) << (4 * q);
+    c |= byte_mask4(cl) << (4 * q);
+  }
+  om = o;
+  cm = c;
+}
+
+// Index of the j-th (0-based) lowest set bit of m (m has > j bits set).
+__device__ __forceinline__ int select_bit(uint32_t m, int j) {
+  for (; j > 0; --j) m &= m - 1;
+  return __ffs(m) - 1;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_bcast(T v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+}  // namespace tb

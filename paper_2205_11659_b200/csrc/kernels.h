@@ -1,0 +1,27 @@
+// Internal launch interface between the C ABI (api.cu) and the kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tb {
+
+// Stack live before the first element of a (shard) launch: Bic prefix (a, h)
+// and the entries at heights [lo, h) (global indices), device memory.
+struct ShardInit {
+  int a;
+  int h;
+  const int32_t* stack;
+  int lo;
+};
+
+size_t pm_workspace_bytes(int64_t n);
+size_t pm_ctrl_bytes(int64_t n);
+cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
+                      const ShardInit* init, cudaStream_t stream);
+
+size_t bic_count_workspace_bytes(int64_t n);
+cudaError_t bic_count_launch(const uint8_t* tags, int64_t n, void* ws, int64_t* d_out2,
+                             cudaStream_t stream);
+
+}  // namespace tb
