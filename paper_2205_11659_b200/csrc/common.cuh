@@ -48,13 +48,26 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_acqrel_u32(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ int ld_cg_s32(const int32_t* p) { return __ldcg(p); }
 
 // Spin until a published u32 slot is nonzero (values are stored +1).
 __device__ __forceinline__ uint32_t wait_u32(const uint32_t* p) {
   uint32_t v = ld_acquire_u32(p);
   while (v == 0) {
-    __nanosleep(32);
+    // pure spin (nanosleep granularity is too coarse here)
     v = ld_acquire_u32(p);
   }
   return v;
@@ -90,10 +103,27 @@ __device__ __forceinline__ void classify16(uint4 w, uint32_t& om, uint32_t& cm) 
   cm = c;
 }
 
-// Index of the j-th (0-based) lowest set bit of m (m has > j bits set).
+// Index of the j-th (0-based) lowest set bit of a 16-bit mask m (m has > j
+// bits set): branch-free binary search on popcounts.
 __device__ __forceinline__ int select_bit(uint32_t m, int j) {
-  for (; j > 0; --j) m &= m - 1;
-  return __ffs(m) - 1;
+  int pos = 0, c;
+  c = __popc(m & 0xffu);
+  if (j >= c) { j -= c; pos += 8; m >>= 8; }
+  c = __popc(m & 0xfu);
+  if (j >= c) { j -= c; pos += 4; m >>= 4; }
+  c = __popc(m & 0x3u);
+  if (j >= c) { j -= c; pos += 2; m >>= 2; }
+  c = (int)(m & 1u);
+  if (j >= c) pos += 1;
+  return pos;
+}
+
+// Named barriers (ids 1..15; 0 is __syncthreads), `n` threads participate.
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 template <typename T>

@@ -59,39 +59,48 @@ struct CtrlLayout {
 // ---------------------------------------------------------------------------
 // Decoupled look-back (one warp).  Returns the exclusive Bic prefix of tile T
 // (T >= 1).  Tile 0 publishes an inclusive descriptor straight away, so the
-// walk always terminates.
+// walk always terminates.  Each round trip inspects LBW = 128 predecessors
+// (4 independent loads per lane): with many tiles in flight the newest
+// inclusive descriptor typically lies a few hundred tiles back.
 // ---------------------------------------------------------------------------
+constexpr int LBG = 4;  // groups of 32 descriptors per round trip
+
+__device__ __forceinline__ Bic warp_fold_desc(uint64_t d, bool valid, int lane, int stop) {
+  // lane k holds tile (j - k); fold lanes [0, stop] with earlier tiles first
+  Bic v = (valid && lane <= stop) ? desc_val(d) : Bic{0, 0};
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Bic o;
+    o.a = __shfl_down_sync(0xffffffffu, v.a, off);
+    o.b = __shfl_down_sync(0xffffffffu, v.b, off);
+    if (lane + off < 32) v = bic_combine(o, v);
+  }
+  return Bic{__shfl_sync(0xffffffffu, v.a, 0), __shfl_sync(0xffffffffu, v.b, 0)};
+}
+
 __device__ __forceinline__ Bic lookback_warp(const Ctrl& c, int T) {
   const int lane = threadIdx.x & 31;
   Bic acc{0, 0};
   int j = T - 1;
   while (true) {
-    const int t = j - lane;
-    uint64_t d = 0;
-    if (t >= 0) {
-      d = ld_acquire_u64(c.desc + t);
-      while (desc_flag(d) == DESC_NONE) {
-        __nanosleep(20);
-        d = ld_acquire_u64(c.desc + t);
-      }
-    }
-    const unsigned inc = __ballot_sync(0xffffffffu, t >= 0 && desc_flag(d) == DESC_INC);
-    const int stop = inc ? (__ffs(inc) - 1) : 31;
-    Bic v = (t >= 0 && lane <= stop) ? desc_val(d) : Bic{0, 0};
-    // lane k holds tile j-k; combine earlier (higher lane) first.
+    uint64_t d[LBG];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      Bic o;
-      o.a = __shfl_down_sync(0xffffffffu, v.a, off);
-      o.b = __shfl_down_sync(0xffffffffu, v.b, off);
-      if (lane + off < 32) v = bic_combine(o, v);
+    for (int g = 0; g < LBG; g++) {
+      const int t = j - 32 * g - lane;
+      d[g] = t >= 0 ? ld_relaxed_u64(c.desc + t) : desc_pack(DESC_INC, Bic{0, 0});
     }
-    Bic win{__shfl_sync(0xffffffffu, v.a, 0), __shfl_sync(0xffffffffu, v.b, 0)};
-    acc = bic_combine(win, acc);
-    if (inc) break;
-    j -= 32;
+#pragma unroll
+    for (int g = 0; g < LBG; g++) {
+      const int t = j - 32 * g - lane;
+      // descriptors carry their own payload: relaxed (strong) loads suffice
+      while (desc_flag(d[g]) == DESC_NONE) d[g] = ld_relaxed_u64(c.desc + t);
+      const unsigned inc = __ballot_sync(0xffffffffu, desc_flag(d[g]) == DESC_INC);
+      const int stop = inc ? (__ffs(inc) - 1) : 31;
+      acc = bic_combine(warp_fold_desc(d[g], t >= 0, lane, stop), acc);
+      if (inc) return acc;
+    }
+    j -= 32 * LBG;
   }
-  return acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -131,29 +140,79 @@ __device__ __forceinline__ int owner_search(const Ctrl& c, int from, int X, int&
   return -1;
 }
 
-// ---------------------------------------------------------------------------
-// Publish tile T's low-water mark and fold it into the hierarchy (warp 0,
-// after every thread's slice writes were fenced and the block synchronised).
-// The last of 32 siblings to arrive publishes the parent entry.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void publish_lowwater(const Ctrl& c, int T, int L) {
+// Low-water marks of the 32 tiles before `base` (lane j <-> tile base-1-j),
+// read once and kept in a register; 0 = not yet published.  Searches from
+// any `from` in (base-32, base] are answered from it while it covers them,
+// waiting only for the tiles that are actually needed (closest first).
+struct LwWindow {
+  int base;
+  uint32_t v;  // lw + 1 as published, 0 = unknown
+};
+
+__device__ __forceinline__ LwWindow lw_window_load(const Ctrl& c, int base) {
   const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-    __threadfence();
-    st_release_u32(c.lw + T, (uint32_t)L + 1u);
+  const int t = base - 1 - lane;
+  LwWindow w;
+  w.base = base;
+  w.v = t >= 0 ? ld_acquire_u32(c.lw + t) : 0xffffffffu;  // 0xffffffff: no tile
+  return w;
+}
+
+// Search via the window first; falls back to the hierarchy if the answer is
+// older than the window.
+__device__ __forceinline__ int owner_search_win(const Ctrl& c, LwWindow& w, int from, int X, int& Lout) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t ux = (uint32_t)X;
+  const int t = w.base - 1 - lane;
+  const bool cand = t < from && t >= 0;
+  while (true) {
+    // closest candidate lane whose value is known and qualifies, with all
+    // closer candidates known (and not qualifying)
+    const bool known = w.v != 0u;
+    const bool q = cand && known && (w.v - 1u) <= ux;
+    const unsigned mq = __ballot_sync(0xffffffffu, q);
+    const unsigned mu = __ballot_sync(0xffffffffu, cand && !known);
+    const unsigned first_q = mq & (~mq + 1u);          // lowest qualifying lane
+    const unsigned before = first_q ? (first_q - 1u) : 0xffffffffu;
+    if (mq && (mu & before) == 0u) {
+      const int k = __ffs(mq) - 1;
+      Lout = (int)(__shfl_sync(0xffffffffu, w.v, k) - 1u);
+      return w.base - 1 - k;
+    }
+    if (!mq && !mu) break;  // nothing in the window qualifies
+    // wait for the unknown candidates that matter (closer than any hit)
+    if (cand && !known && (mq == 0u || ((1u << lane) & before))) w.v = wait_u32(c.lw + t);
   }
+  if (w.base - 32 <= 0) return -1;
+  return owner_search(c, min(from, w.base - 32), X, Lout);
+}
+
+// ---------------------------------------------------------------------------
+// Publish tile T's inclusive descriptor and low-water mark (one thread, after
+// the block synchronised on its slice writes).  The release store orders all
+// of the CTA's earlier writes (bar.sync + gpu-scope release, as in CUTLASS's
+// semaphores) before both stores; the relaxed low-water store after the
+// release fence forms a release pattern for readers that acquire it.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void publish_inclusive(const Ctrl& c, int T, Bic incl, int L, bool desc_too) {
+  if (desc_too) st_release_u64(c.desc + T, desc_pack(DESC_INC, incl));
+  else __threadfence();
+  st_relaxed_u32(c.lw + T, (uint32_t)L + 1u);
+}
+
+// Fold tile T's published low-water mark into the 32-ary hierarchy (warp;
+// off the critical path).  The last of 32 siblings to arrive publishes the
+// parent entry.
+__device__ __forceinline__ void hierarchy_arrive(const Ctrl& c, int T) {
+  const int lane = threadIdx.x & 31;
   int idx = T;
 #pragma unroll 1
   for (int k = 1; k < HLEVELS; k++) {
     const int g = idx >> 5;
     unsigned old = 0;
-    if (lane == 0) {
-      __threadfence();
-      old = atomicAdd(c.cnt[k] + g, 1u);
-    }
+    if (lane == 0) old = atom_add_acqrel_u32(c.cnt[k] + g, 1u);
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != 31u) return;
-    __threadfence();
     uint32_t v = wait_u32(c.lv[k - 1] + ((size_t)g << 5) + lane);
     v = __reduce_min_sync(0xffffffffu, v);
     if (lane == 0) st_release_u32(c.lv[k] + g, v);
