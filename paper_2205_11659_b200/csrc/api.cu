@@ -141,21 +141,6 @@ int paren_match_host(const uint8_t* h_tags, int64_t n, int32_t* h_match, int32_t
   return TB_OK;
 }
 
-/* Debug: paren_match with per-tile phase timestamps (globaltimer ns) written
- * to d_trace[tile * 16 + slot].  Not part of the public header. */
-int tb_debug_paren_match_trace(const uint8_t* d_tags, int64_t n, int32_t* d_match, int32_t* d_parent,
-                               uint64_t* d_trace, void* stream) {
-  g_err[0] = 0;
-  int r = pm_checks(d_tags, n, d_match, d_parent);
-  if (r || n == 0) return r;
-  void* ws = nullptr;
-  r = get_ws(stream, 0, tb::pm_workspace_bytes(n), &ws);
-  if (r) return r;
-  cudaError_t e = tb::pm_launch(d_tags, n, d_match, d_parent, ws, nullptr, (cudaStream_t)stream, d_trace);
-  if (e != cudaSuccess) return cuda_fail(e, "paren_match launch");
-  return TB_OK;
-}
-
 int tb_count_unmatched(const uint8_t* d_tags, int64_t n, int64_t* h_a, int64_t* h_b, void* stream) {
   g_err[0] = 0;
   int r = check_n(n);

@@ -18,7 +18,7 @@ struct ShardInit {
 size_t pm_workspace_bytes(int64_t n);
 size_t pm_ctrl_bytes(int64_t n);
 cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
-                      const ShardInit* init, cudaStream_t stream, uint64_t* trace = nullptr);
+                      const ShardInit* init, cudaStream_t stream);
 
 size_t bic_count_workspace_bytes(int64_t n);
 cudaError_t bic_count_launch(const uint8_t* tags, int64_t n, void* ws, int64_t* d_out2,

@@ -18,19 +18,21 @@ struct Ctrl {
   uint32_t* counter;         // dynamic tile ids
   uint64_t* desc;            // [ntiles] Bic look-back descriptors
   uint32_t* lw;              // [ntiles] low-water mark L_T + 1 (0 = not yet)
+  int32_t* hstart;           // [ntiles] stack height at the tile start (written with lw)
   uint32_t* lv[HLEVELS];     // lv[k][g] = 1 + min L over tiles [g*32^k, (g+1)*32^k)
   uint32_t* cnt[HLEVELS];    // arrival counters for lv[k]
 };
 
 // Sizes (in elements) of the control arrays for `ntiles` tiles.
 struct CtrlLayout {
-  size_t off_counter, off_desc, off_lw, off_lv[HLEVELS], off_cnt[HLEVELS], bytes;
+  size_t off_counter, off_desc, off_lw, off_h, off_lv[HLEVELS], off_cnt[HLEVELS], bytes;
   __host__ __device__ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
   __host__ __device__ explicit CtrlLayout(int64_t ntiles) {
     size_t o = 0;
     off_counter = o; o = align256(o + 16);
     off_desc = o; o = align256(o + 8 * (size_t)ntiles);
     off_lw = o; o = align256(o + 4 * (size_t)ntiles);
+    off_h = o; o = align256(o + 4 * (size_t)ntiles);
     int64_t m = ntiles;
     off_lv[0] = off_cnt[0] = 0;
     for (int k = 1; k < HLEVELS; k++) {
@@ -46,6 +48,7 @@ struct CtrlLayout {
     c.counter = (uint32_t*)(b + off_counter);
     c.desc = (uint64_t*)(b + off_desc);
     c.lw = (uint32_t*)(b + off_lw);
+    c.hstart = (int32_t*)(b + off_h);
     c.lv[0] = c.lw;
     c.cnt[0] = nullptr;
     for (int k = 1; k < HLEVELS; k++) {
@@ -185,6 +188,53 @@ __device__ __forceinline__ int owner_search_win(const Ctrl& c, LwWindow& w, int 
   }
   if (w.base - 32 <= 0) return -1;
   return owner_search(c, min(from, w.base - 32), X, Lout);
+}
+
+// ---------------------------------------------------------------------------
+// Owner search over a COMPLETE hierarchy (finish pass: the reduce pass has
+// ended, every value is published, plain loads suffice).  Same contract as
+// owner_search.  The first 32 predecessors of `from` are tested in one
+// ballot; older owners are found through the 32-ary levels.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int owner_search_done(const Ctrl& c, int from, int X, int& Lout) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t ux = (uint32_t)X;
+  {
+    const int t = from - 1 - lane;
+    const uint32_t v = t >= 0 ? __ldg(c.lw + t) - 1u : 0xffffffffu;
+    const unsigned m = __ballot_sync(0xffffffffu, t >= 0 && v <= ux);
+    if (m) {
+      const int k = __ffs(m) - 1;
+      Lout = (int)__shfl_sync(0xffffffffu, v, k);
+      return from - 1 - k;
+    }
+    if (from <= 32) return -1;
+    from -= 32;
+  }
+  int idx = from;
+#pragma unroll 1
+  for (int k = 0; k < HLEVELS; k++) {
+    const int g = idx >> 5, r = idx & 31;
+    const uint32_t v = lane < r ? __ldg(c.lv[k] + ((size_t)g << 5) + lane) - 1u : 0xffffffffu;
+    const unsigned m = __ballot_sync(0xffffffffu, lane < r && v <= ux);
+    if (m) {
+      int E = (g << 5) + (31 - __clz(m));
+      uint32_t L = __shfl_sync(0xffffffffu, v, 31 - __clz(m));
+#pragma unroll 1
+      for (int j = k - 1; j >= 0; j--) {
+        const uint32_t v2 = __ldg(c.lv[j] + ((size_t)E << 5) + lane) - 1u;
+        const unsigned m2 = __ballot_sync(0xffffffffu, v2 <= ux);
+        const int top = 31 - __clz(m2);
+        L = __shfl_sync(0xffffffffu, v2, top);
+        E = (E << 5) + top;
+      }
+      Lout = (int)L;
+      return E;
+    }
+    idx = g;
+    if (idx == 0) break;
+  }
+  return -1;
 }
 
 // ---------------------------------------------------------------------------
