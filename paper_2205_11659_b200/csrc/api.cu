@@ -83,6 +83,19 @@ int pm_checks(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent) {
   return TB_OK;
 }
 
+int bb_checks(const uint8_t* tags, const float* leaf, int64_t n, float* out) {
+  int r = check_n(n);
+  if (r) return r;
+  if (n == 0) return TB_OK;
+  if (!tags || !leaf || !out) return fail(TB_ERR_ARG, "null pointer with n > 0");
+  if (!aligned16(tags) || !aligned16(leaf) || !aligned16(out))
+    return fail(TB_ERR_ALIGN, "tags, leaf_bbox and node_bbox must be 16-byte aligned");
+  const size_t nb = (size_t)n * 16;
+  if (overlap(out, nb, leaf, nb) || overlap(out, nb, tags, (size_t)n))
+    return fail(TB_ERR_ALIAS, "node_bbox overlaps an input");
+  return TB_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -136,6 +149,57 @@ int paren_match_host(const uint8_t* h_tags, int64_t n, int32_t* h_match, int32_t
   if (r) return r;
   e = cudaMemcpyAsync(h_match, d_match, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(h_parent, d_parent, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H results");
+  return TB_OK;
+}
+
+size_t tree_bbox_workspace_bytes(int64_t n) { return n > 0 ? tb::bb_workspace_bytes(n) : 0; }
+
+int tree_bbox_ws(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox,
+                 void* d_workspace, size_t workspace_bytes, void* stream) {
+  g_err[0] = 0;
+  int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
+  if (r || n == 0) return r;
+  if (!d_workspace || workspace_bytes < tb::bb_workspace_bytes(n))
+    return fail(TB_ERR_ARG, "workspace too small: need %zu bytes", tb::bb_workspace_bytes(n));
+  cudaError_t e = tb::bb_launch(d_tags, d_leaf_bbox, n, d_node_bbox, d_workspace, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_bbox launch");
+  return TB_OK;
+}
+
+int tree_bbox(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox, void* stream) {
+  g_err[0] = 0;
+  int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
+  if (r || n == 0) return r;
+  void* ws = nullptr;
+  const size_t need = tb::bb_workspace_bytes(n);
+  r = get_ws(stream, 3, need, &ws);
+  if (r) return r;
+  return tree_bbox_ws(d_tags, d_leaf_bbox, n, d_node_bbox, ws, need, stream);
+}
+
+int tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, float* h_node_bbox,
+                   void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r || n == 0) return r;
+  if (!h_tags || !h_leaf_bbox || !h_node_bbox) return fail(TB_ERR_ARG, "null pointer with n > 0");
+  const size_t nb_t = ((size_t)n + 255) & ~(size_t)255;
+  const size_t nb_b = ((size_t)n * 16 + 255) & ~(size_t)255;
+  void* io = nullptr;
+  r = get_ws(stream, 4, nb_t + 2 * nb_b, &io);
+  if (r) return r;
+  uint8_t* d_tags = (uint8_t*)io;
+  float* d_in = (float*)((char*)io + nb_t);
+  float* d_out = (float*)((char*)io + nb_t + nb_b);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, h_leaf_bbox, (size_t)n * 16, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D inputs");
+  r = tree_bbox(d_tags, d_in, n, d_out, stream);
+  if (r) return r;
+  e = cudaMemcpyAsync(h_node_bbox, d_out, (size_t)n * 16, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "D2H results");
   return TB_OK;

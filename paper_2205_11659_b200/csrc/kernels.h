@@ -20,6 +20,10 @@ size_t pm_ctrl_bytes(int64_t n);
 cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
                       const ShardInit* init, cudaStream_t stream);
 
+size_t bb_workspace_bytes(int64_t n);
+cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
+                      cudaStream_t stream);
+
 size_t bic_count_workspace_bytes(int64_t n);
 cudaError_t bic_count_launch(const uint8_t* tags, int64_t n, void* ws, int64_t* d_out2,
                              cudaStream_t stream);

@@ -1,0 +1,894 @@
+// tree_bbox for sm_100a: clip intersections and blend unions (§6 P:192-221,
+// §9) on top of the same tile machinery as paren_match.
+//
+// Tile = 256 threads x 8 contiguous elements = 2048 elements.  Boxes are
+// carried as totalOrder integer keys (boxes.cuh).
+//
+// bb_reduce (pass 1; reads the tags and, gathered, the boxes of each tile's
+//   unmatched opens): per-thread register walk -> Bic; block scans; the
+//   tile's stack slice with, per entry, its original index, kind and the
+//   tile-local cumulative clip lc = ∩ of the clip boxes of slice entries 0..p
+//   (the "inclusive intersection scan" the paper's first bbox dispatch puts
+//   in its slices); decoupled look-back -> stack height at the tile
+//   start; low-water mark + 32-ary hierarchy (as paren_match).
+// bb_finish (pass 2; persistent CTAs, reads tags + boxes, writes node_bbox):
+//   1. incoming stack top (a_T + 1 entries) copied from predecessors' slices
+//      (owner rule); its TRUE clips = lc ∩ TC(owner), where TC(U) is the true
+//      clip just below tile U's low-water mark.  TC of the deepest owner is
+//      found by a warp-parallel look-back along the owner chain that stops at
+//      the first tile that already published its TC; this tile then publishes
+//      its own TC.  (The paper rebuilds the snapshot by an exclusive scan of
+//      per-partition top boxes; this is the single-pass equivalent.)
+//   2. thread-level chains (a thread's outermost external entry lives in an
+//      earlier thread) are resolved by pointer jumping over the 256 threads.
+//   3. each thread runs the sequential two-box stack algorithm of the
+//      introduction over its 8 elements, starting from its resolved
+//      external stack: leaf = box ∩ clip(top), clip open pushes
+//      box ∩ clip(top), blend open pushes clip(top), a close yields the
+//      union of its node's clipped leaves at the close and, for
+//      blend nodes, at the open.
+//   4. nodes opened in an earlier thread or tile get their unions from
+//      suffix unions (published per slice entry) ∪ range unions over whole
+//      threads (sparse table) / whole tiles (32-ary hierarchy of per-tile
+//      unions, published as tiles finish step 3) ∪ this thread's prefix union.
+// bb_final: blend nodes still open at the end of the stream (R4) get the
+//   union of everything after them.
+#include <algorithm>
+#include <climits>
+#include "boxes.cuh"
+#include "kernels.h"
+#include "stackscan.cuh"
+#include "tile_common.cuh"
+
+namespace tb {
+namespace bb {
+
+constexpr int NT = 256;
+constexpr int K = 8;
+constexpr int TILE = NT * K;
+constexpr int NW = NT / 32;
+constexpr int LOGNT = 8;
+constexpr int SREC = TILE + 1;  // slice records per tile
+
+struct SliceRec {
+  int4 lc;   // tile-local cumulative clip (keys)
+  int idx;   // original element index
+  int kind;  // 1 = blend open, 0 = clip open
+  int pad0, pad1;
+};
+
+// Finish-pass state published by tiles (flags zeroed per call).
+struct FState {
+  uint32_t* counter;        // dynamic tile ids of the finish pass
+  uint32_t* tcf;            // [ntiles] TC published
+  uint32_t* suf;            // [ntiles] suffix unions published
+  uint32_t* uf[HLEVELS];    // [k][g] union hierarchy published (k = 0: per tile)
+  uint32_t* ucnt[HLEVELS];  // arrival counters (k >= 1)
+  int4* tc;                 // [ntiles] true clip just below the tile's low-water mark
+  int4* u[HLEVELS];         // [k][g] union of true-clipped leaves (k = 0: per tile)
+  int4* su;                 // [ntiles * TILE] true union of leaves after each slice entry
+  int32_t* bcount;          // [ntiles] slice length (written by pass 1)
+};
+
+// Per-CTA scratch of the persistent finish pass (global, L2-resident).
+struct Scratch {
+  int4* cin;    // [TILE+1] clip of the incoming entry at depth d (lc, then true)
+  int4* meta;   // [TILE+1] {index, kind, run, slice position}
+  int4* accin;  // [TILE+1] union of leaves from the entry's open to the tile start
+  int4* uoc;    // [TILE]   thread-local cumulative clip of each thread-unmatched open
+  int4* uosu;   // [TILE]   union of the thread's leaves after each thread-unmatched open
+  int4* run;    // [TILE+1] {tile, L, lo, hi}
+  int4* runtc;  // [TILE+1] TC of the run's tile
+  int4* runr;   // [TILE+1] union over the tiles between the run's tile and this tile
+};
+constexpr size_t SCRATCH_BYTES = 16 * (size_t)(7 * (TILE + 1) + TILE) + 1024;
+
+struct Params {
+  const uint8_t* tags;
+  const float4* boxes;
+  float4* out;
+  int64_t n;
+  int ntiles;
+  Ctrl ctrl;
+  SliceRec* slice;  // [ntiles * SREC]
+  FState f;
+  char* scratch;
+};
+
+// ----------------------------------------------------------------------------
+// small helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void classify8(uint2 raw, uint32_t& om, uint32_t& cm, uint32_t& bm) {
+  uint32_t o = 0, c = 0, b = 0;
+  const uint32_t ws[2] = {raw.x, raw.y};
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t bl = __vcmpeq4(x, 0x02020202u);
+    o |= byte_mask4(__vcmpeq4(x, 0x01010101u) | bl) << (4 * q);
+    c |= byte_mask4(__vcmpeq4(x, 0x03030303u)) << (4 * q);
+    b |= byte_mask4(bl) << (4 * q);
+  }
+  om = o;
+  cm = c;
+  bm = b;
+}
+
+__device__ __forceinline__ uint2 load_tags8(const uint8_t* tags, int64_t n, int64_t tbase, bool full) {
+  if (full) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(tags + tbase));
+    return r;
+  }
+  uint32_t wv[2] = {0, 0};
+  for (int i = 0; i < 8; i++) {
+    const int64_t g = tbase + i;
+    const uint32_t v = g < n ? tags[g] : 0u;
+    wv[i >> 2] |= v << (8 * (i & 3));
+  }
+  return make_uint2(wv[0], wv[1]);
+}
+
+// Bic walk over 8 elements: S = opens left on the thread stack, ucm = closes
+// that pop the stack at thread start.
+__device__ __forceinline__ void walk8(uint32_t om, uint32_t cm, uint32_t& S_out, uint32_t& ucm_out) {
+  uint32_t S = 0, ucm = 0;
+#pragma unroll
+  for (int i = 0; i < K; i++) {
+    const uint32_t bit = 1u << i;
+    const int top = 31 - __clz(S);
+    const bool pop = (cm & bit) && S;
+    ucm |= ((cm & bit) && !S) ? bit : 0u;
+    S = (om & bit) ? (S | bit) : (pop ? (S ^ (1u << top)) : S);
+  }
+  S_out = S;
+  ucm_out = ucm;
+}
+
+__device__ __forceinline__ KBox ld_kbox_cg(const int4* p) { return from_int4(__ldcg(p)); }
+
+// Exclusive block scan of an int (sum).
+template <int NW_>
+__device__ __forceinline__ int block_excl_sum(int v, int* wsum, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += o;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < NW_; w++) {
+    const int s = wsum[w];
+    if (w < warp) pre += s;
+    tot += s;
+  }
+  total = tot;
+  return pre + x - v;
+}
+
+// Exclusive block ∩-scan of a box (thread order).
+template <int NW_>
+__device__ __forceinline__ KBox block_excl_isect(KBox v, KBox* wbox) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  KBox x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const KBox o = shfl_up_box(x, off);
+    if (lane >= off) x = isect(x, o);
+  }
+  if (lane == 31) wbox[warp] = x;
+  __syncthreads();
+  KBox pre = kINF();
+#pragma unroll
+  for (int w = 0; w < NW_; w++)
+    if (w < warp) pre = isect(pre, wbox[w]);
+  KBox e = shfl_up_box(x, 1);
+  if (lane == 0) e = kINF();
+  return isect(pre, e);
+}
+
+// ----------------------------------------------------------------------------
+// pass 1
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) bb_reduce(Params p) {
+  __shared__ Bic wtot[NW];
+  __shared__ KBox wbox[NW];
+  __shared__ int s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = (int)atomicAdd(p.ctrl.counter, 1u);
+  __syncthreads();
+  const int T = s_tile;
+  const int64_t base = (int64_t)T * TILE;
+  const int64_t tbase = base + (int64_t)tid * K;
+  const bool full = base + TILE <= p.n;
+
+  uint32_t om, cm, bm, S, ucm;
+  classify8(load_tags8(p.tags, p.n, tbase, full), om, cm, bm);
+  walk8(om, cm, S, ucm);
+  const int a_t = __popc(ucm), b_t = __popc(S);
+  Bic ex, sx, tot;
+  block_bic_scans<NW>(Bic{a_t, b_t}, wtot, ex, sx, tot, true);
+  if (tid == 0) {
+    if (T == 0) st_release_u64(p.ctrl.desc, desc_pack(DESC_INC, tot));
+    else st_release_u64(p.ctrl.desc + T, desc_pack(DESC_AGG, tot));
+    p.f.bcount[T] = tot.b;
+  }
+  // surviving unmatched opens of this thread: the s_t lowest bits of S
+  const int s_t = max(b_t - sx.a, 0);
+  uint32_t surv = 0;
+  {
+    uint32_t m = S;
+    for (int k = 0; k < s_t; k++) {
+      surv |= m & (~m + 1u);
+      m &= m - 1;
+    }
+  }
+  KBox bx[K];
+  KBox own = kINF();
+#pragma unroll
+  for (int i = 0; i < K; i++) {
+    bx[i] = kINF();
+    if (((surv & ~bm) >> i) & 1u) bx[i] = to_kbox(__ldg(p.boxes + tbase + i));
+    own = isect(own, bx[i]);
+  }
+  KBox acc = block_excl_isect<NW>(own, wbox);
+  {
+    const int l_t = ex.b - ex.a - a_t;
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      if ((surv >> i) & 1u) {
+        acc = isect(acc, bx[i]);
+        SliceRec r;
+        r.lc = to_int4(acc);
+        r.idx = (int)(tbase + i);
+        r.kind = (int)((bm >> i) & 1u);
+        r.pad0 = r.pad1 = 0;
+        p.slice[(int64_t)T * SREC + (l_t + k + tot.a)] = r;
+        k++;
+      }
+    }
+  }
+  if (warp == 0) {
+    const Bic excl = (T == 0) ? Bic{0, 0} : lookback_warp(p.ctrl, T);
+    if (lane == 0) {
+      p.ctrl.hstart[T] = excl.b;
+      publish_inclusive(p.ctrl, T, bic_combine(excl, tot), max(excl.b - tot.a, 0), T > 0);
+    }
+    hierarchy_arrive(p.ctrl, T);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// hierarchy of per-tile unions (finish pass)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ KBox wait_box(const uint32_t* flag, const int4* val) {
+  while (ld_acquire_u32(flag) == 0u) {
+  }
+  return ld_kbox_cg(val);
+}
+
+// Union over tiles [a, b] (warp-cooperative; waits for unpublished entries).
+__device__ __forceinline__ KBox range_union_tiles(const FState& f, int a, int b) {
+  const int lane = threadIdx.x & 31;
+  KBox acc = kEMPTY();
+  int k = 0;
+  while (a <= b) {
+    const uint32_t* fl = f.uf[k];
+    const int4* val = f.u[k];
+    if ((a >> 5) == (b >> 5) || k == HLEVELS - 1) {
+      for (int i = a + lane; i <= b; i += 32) acc = unite(acc, wait_box(fl + i, val + i));
+      break;
+    }
+    if (a & 31) {
+      const int e = a | 31;
+      const int i = a + lane;
+      if (i <= e) acc = unite(acc, wait_box(fl + i, val + i));
+      a = e + 1;
+    }
+    if ((b & 31) != 31) {
+      const int s = b & ~31;
+      const int i = s + lane;
+      if (i <= b) acc = unite(acc, wait_box(fl + i, val + i));
+      b = s - 1;
+    }
+    if (a > b) break;
+    a >>= 5;
+    b = ((b + 1) >> 5) - 1;
+    k++;
+  }
+  return warp_unite_all(acc);
+}
+
+// Publish the tile's union and fold it into the hierarchy (warp; the last of
+// 32 siblings publishes the parent).
+__device__ __forceinline__ void publish_union(const FState& f, int T, KBox tu) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    f.u[0][T] = to_int4(tu);
+    __threadfence();
+    st_release_u32(f.uf[0] + T, 1u);
+  }
+  int idx = T;
+#pragma unroll 1
+  for (int k = 1; k < HLEVELS; k++) {
+    const int g = idx >> 5;
+    unsigned old = 0;
+    if (lane == 0) old = atom_add_acqrel_u32(f.ucnt[k] + g, 1u);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != 31u) return;
+    const int c = (g << 5) + lane;
+    KBox v = wait_box(f.uf[k - 1] + c, f.u[k - 1] + c);
+    v = warp_unite_all(v);
+    if (lane == 0) {
+      f.u[k][g] = to_int4(v);
+      __threadfence();
+      st_release_u32(f.uf[k] + g, 1u);
+    }
+    idx = g;
+  }
+}
+
+// True clip just below tile u's low-water mark Lu, i.e. the clip of the
+// entry at height Lu - 1 of the stack at u's start (INF at the root).  Walks
+// the owner chain (warp-parallel over 32 predecessors at a time), combining
+// the chain tiles' tile-local clips, until a tile that already published its
+// own TC.
+__device__ KBox chain_tc(const Params& p, int u, int Lu) {
+  const int lane = threadIdx.x & 31;
+  KBox acc = kINF();
+  int h = Lu - 1;
+  while (h >= 0) {
+    if (ld_acquire_u32(p.f.tcf + u)) return isect(acc, ld_kbox_cg(p.f.tc + u));
+    const int t = u - 1 - lane;
+    const int L = t >= 0 ? (int)(__ldg(p.ctrl.lw + t) - 1u) : INT_MAX;
+    const uint32_t fl = t >= 0 ? ld_acquire_u32(p.f.tcf + t) : 0u;
+    // min L over closer tiles (exclusive prefix-min in lane order)
+    int m = L;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, m, off);
+      if (lane >= off) m = min(m, o);
+    }
+    int mex = __shfl_up_sync(0xffffffffu, m, 1);
+    if (lane == 0) mex = INT_MAX;
+    const int thr = min(h, mex == INT_MAX ? INT_MAX : mex - 1);
+    const bool on = t >= 0 && L <= thr;
+    const unsigned mon = __ballot_sync(0xffffffffu, on);
+    const unsigned mres = __ballot_sync(0xffffffffu, on && fl);
+    if (mon == 0u) {
+      // no owner among the 32 predecessors: jump through the hierarchy
+      if (u <= 32) return acc;  // nothing older: the root
+      int LW = 0;
+      const int W = owner_search_done(p.ctrl, u - 32, h, LW);
+      if (W < 0) return acc;
+      acc = isect(acc, from_int4(__ldg(&p.slice[(int64_t)W * SREC + (h - LW)].lc)));
+      u = W;
+      h = LW - 1;
+      continue;
+    }
+    const int klim = mres ? (__ffs(mres) - 1) : 31;
+    KBox c = kINF();
+    if (on && lane <= klim) c = from_int4(__ldg(&p.slice[(int64_t)t * SREC + (thr - L)].lc));
+    acc = isect(acc, warp_isect_all(c));
+    if (mres) {
+      const KBox tcr = shfl_box(t >= 0 ? ld_kbox_cg(p.f.tc + max(t, 0)) : kINF(), klim);
+      return isect(acc, tcr);
+    }
+    const int last = 31 - __clz(mon);
+    const int Llast = __shfl_sync(0xffffffffu, L, last);
+    u = u - 1 - last;
+    h = Llast - 1;
+  }
+  return acc;
+}
+
+// ----------------------------------------------------------------------------
+// pass 2 (persistent)
+// ----------------------------------------------------------------------------
+struct Smem {
+  int win[NW][5][32];
+  int wmin[NW];
+  int l[NT];
+  uint32_t uo[NT];
+  uint32_t bmk[NT];
+  int uoff[NT];
+  int link[NT];
+  int4 pjacc[2][NT];
+  int pjptr[2][NT];
+  int pjesc[2][NT];
+  int4 tl[NT];
+  int4 sp[LOGNT][NT];  // sparse table of per-thread unions of true-clipped leaves
+  Bic wtot[NW];
+  int wsum[NW];
+  int tile, nruns;
+};
+
+__device__ __forceinline__ int rank_in(uint32_t m, int bit) { return __popc(m & ((1u << bit) - 1u)); }
+
+__device__ __forceinline__ KBox range_union_threads(const Smem& s, int a, int b) {
+  if (a > b) return kEMPTY();
+  const int len = b - a + 1;
+  const int k = min(31 - __clz(len), LOGNT - 1);  // two windows of 2^k cover len <= 2^LOGNT
+  return unite(from_int4(s.sp[k][b]), from_int4(s.sp[k][a + (1 << k) - 1]));
+}
+
+__global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Scratch sc;
+  {
+    int4* b = reinterpret_cast<int4*>(p.scratch + (size_t)blockIdx.x * SCRATCH_BYTES);
+    sc.cin = b;
+    sc.meta = sc.cin + (TILE + 1);
+    sc.accin = sc.meta + (TILE + 1);
+    sc.run = sc.accin + (TILE + 1);
+    sc.runtc = sc.run + (TILE + 1);
+    sc.runr = sc.runtc + (TILE + 1);
+    sc.uoc = sc.runr + (TILE + 1);
+    sc.uosu = sc.uoc + TILE;
+  }
+
+  while (true) {
+    if (tid == 0) s.tile = (int)atomicAdd(p.f.counter, 1u);
+    __syncthreads();
+    const int T = s.tile;
+    if (T >= p.ntiles) break;
+    const int64_t base = (int64_t)T * TILE;
+    const int64_t tbase = base + (int64_t)tid * K;
+    const bool full = base + TILE <= p.n;
+
+    // ---- A. load ------------------------------------------------------------
+    uint32_t om, cm, bm, S, ucm;
+    classify8(load_tags8(p.tags, p.n, tbase, full), om, cm, bm);
+    KBox bx[K];
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      const bool need = ((~cm & ~bm) >> i) & 1u;  // leaves and clip opens carry boxes
+      bx[i] = (need && (full || tbase + i < p.n)) ? to_kbox(__ldg(p.boxes + tbase + i)) : kINF();
+    }
+    walk8(om, cm, S, ucm);
+    const int a_t = __popc(ucm), b_t = __popc(S);
+
+    // ---- B. scans, thread references ----------------------------------------
+    Bic ex, sx, tot;
+    block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, true);
+    const int aT = tot.a;
+    const int r_t = ex.b - ex.a;
+    const int l_t = r_t - a_t;
+    int tot_uo;
+    const int uoff = block_excl_sum<NW>(b_t, s.wsum, tot_uo);
+    int wl[5];
+    lane_windows(l_t, wl);
+#pragma unroll
+    for (int k = 0; k < 5; k++) s.win[warp][k][lane] = wl[k];
+    {
+      const int o = __shfl_sync(0xffffffffu, wl[4], 15);
+      if (lane == 31) s.wmin[warp] = min(wl[4], o);
+    }
+    s.l[tid] = l_t;
+    s.uo[tid] = S;
+    s.bmk[tid] = bm;
+    s.uoff[tid] = uoff;
+    // thread-local cumulative clip of each thread-unmatched open
+    {
+      KBox acc = kINF();
+      int k = 0;
+#pragma unroll
+      for (int i = 0; i < K; i++) {
+        if ((S >> i) & 1u) {
+          if (!((bm >> i) & 1u)) acc = isect(acc, bx[i]);
+          sc.uoc[uoff + k] = to_int4(acc);
+          k++;
+        }
+      }
+    }
+    const int H = __ldg(p.ctrl.hstart + T);
+    const int lo = max(H - 1 - aT, 0);
+    for (int d = H + tid; d <= aT; d += NT) {
+      sc.cin[d] = to_int4(kINF());
+      sc.meta[d] = make_int4(-1, 0, -1, 0);
+    }
+    __syncthreads();
+    const int top_ref = thread_ref<NW, K>(wl, l_t, S, r_t - 1, s.win, s.wmin, s.l, s.uo);
+    const int link_ref = thread_ref<NW, K>(wl, l_t, S, l_t - 1, s.win, s.wmin, s.l, s.uo);
+
+    // ---- C. incoming stack: runs of predecessors' slices ------------------
+    if (warp == 0) {
+      int cur = H - 1, from = T, nr = 0;
+      while (cur >= lo) {
+        int LU = 0;
+        const int U = owner_search_done(p.ctrl, from, cur, LU);
+        const int rlo = max(LU, lo);
+        if (lane == 0) sc.run[nr] = make_int4(U, LU, rlo, cur);
+        nr++;
+        cur = LU - 1;
+        from = U;
+      }
+      if (lane == 0) s.nruns = nr;
+    }
+    __syncthreads();
+    const int nr = s.nruns;
+    for (int r = warp; r < nr; r += NW) {
+      const int4 rr = __ldcg(sc.run + r);
+      const int cnt = rr.w - rr.z + 1;
+      for (int i = lane; i < cnt; i += 32) {
+        const int h = rr.w - i;
+        const SliceRec rec = p.slice[(int64_t)rr.x * SREC + (h - rr.y)];
+        const int d = H - 1 - h;
+        sc.cin[d] = rec.lc;
+        sc.meta[d] = make_int4(rec.idx, rec.kind, r, h - rr.y);
+      }
+    }
+    __syncthreads();
+    // TC of each run's tile: deepest by look-back, the others from the run below
+    if (warp == 0 && nr > 0) {
+      const int4 rb = __ldcg(sc.run + nr - 1);
+      KBox tc = chain_tc(p, rb.x, rb.y);
+      if (lane == 0) sc.runtc[nr - 1] = to_int4(tc);
+      for (int r = nr - 2; r >= 0; r--) {
+        const int4 rbelow = __ldcg(sc.run + r + 1);
+        tc = isect(from_int4(__ldcg(sc.cin + (H - 1 - rbelow.w))), tc);
+        if (lane == 0) sc.runtc[r] = to_int4(tc);
+      }
+    }
+    __syncthreads();
+    for (int d = tid; d < min(aT + 1, H); d += NT) {
+      const int run = __ldcg(sc.meta + d).z;
+      sc.cin[d] = to_int4(isect(from_int4(__ldcg(sc.cin + d)), from_int4(__ldcg(sc.runtc + run))));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      p.f.tc[T] = __ldcg(sc.cin + aT);  // true clip just below this tile's low-water mark
+      __threadfence();
+      st_release_u32(p.f.tcf + T, 1u);
+    }
+
+    // ---- D. thread chains: clip of each thread's link entry ---------------
+    {
+      int ptr = -1, esc = 0;
+      KBox acc = kINF();
+      if (link_ref >= 0) {
+        const int W = link_ref / K;
+        ptr = W;
+        acc = from_int4(__ldcg(sc.uoc + s.uoff[W] + rank_in(s.uo[W], link_ref % K)));
+      } else {
+        esc = link_ref;
+      }
+      int cb = 0;
+      s.pjacc[0][tid] = to_int4(acc);
+      s.pjptr[0][tid] = ptr;
+      s.pjesc[0][tid] = esc;
+      __syncthreads();
+      for (int round = 0; round < LOGNT; round++) {
+        if (ptr >= 0) {
+          acc = isect(acc, from_int4(s.pjacc[cb][ptr]));
+          esc = s.pjesc[cb][ptr];
+          ptr = s.pjptr[cb][ptr];
+        }
+        s.pjacc[cb ^ 1][tid] = to_int4(acc);
+        s.pjptr[cb ^ 1][tid] = ptr;
+        s.pjesc[cb ^ 1][tid] = esc;
+        cb ^= 1;
+        __syncthreads();
+      }
+      s.tl[tid] = to_int4(isect(acc, from_int4(__ldcg(sc.cin + (-esc - 1)))));
+    }
+    __syncthreads();
+
+    // true clip of an entry of this thread's start stack
+    auto entry_clip = [&](int ref) -> KBox {
+      if (ref >= 0) {
+        const int V = ref / K;
+        return isect(from_int4(__ldcg(sc.uoc + s.uoff[V] + rank_in(s.uo[V], ref % K))), from_int4(s.tl[V]));
+      }
+      return from_int4(__ldcg(sc.cin + (-ref - 1)));
+    };
+    auto next_down = [&](int ref) -> int {
+      if (ref >= 0) {
+        const int V = ref / K;
+        const uint32_t below = s.uo[V] & ((1u << (ref % K)) - 1u);
+        return below ? V * K + (31 - __clz(below)) : s.link[V];
+      }
+      return ref - 1;
+    };
+    s.link[tid] = link_ref;
+    __syncthreads();
+
+    // ---- E. per-thread two-box stack walk ----------------------------
+    KBox lclip[K], luni[K], pu_at[K];
+    KBox pu = kEMPTY();  // union of this thread's clipped leaves so far
+    {
+      int ref = top_ref;
+      KBox cext = entry_clip(ref);
+      uint32_t St = 0;
+      int dcur = 0;
+#pragma unroll
+      for (int i = 0; i < K; i++) {
+        const uint32_t bit = 1u << i;
+        const int top = 31 - __clz(St);
+        const KBox ctop = St ? lclip[top] : cext;
+        const int64_t g = tbase + i;
+        const bool live = full || g < p.n;
+        if (om & bit) {
+          const bool blend = bm & bit;
+          const KBox c = blend ? ctop : isect(bx[i], ctop);
+          lclip[i] = c;
+          luni[i] = kEMPTY();
+          if (!blend && live) p.out[g] = to_float4(c);
+          St |= bit;
+        } else if (cm & bit) {
+          if (St) {
+            const KBox U = luni[top];
+            if (live) p.out[g] = to_float4(U);
+            if ((bm >> top) & 1u) p.out[tbase + top] = to_float4(U);
+            St ^= 1u << top;
+            if (St) {
+              const int nt = 31 - __clz(St);
+              luni[nt] = unite(luni[nt], U);
+            }
+          } else {
+            pu_at[dcur] = pu;
+            dcur++;
+            ref = next_down(ref);
+            cext = entry_clip(ref);
+          }
+        } else if (live) {
+          const KBox c = isect(bx[i], ctop);
+          p.out[g] = to_float4(c);
+          pu = unite(pu, c);
+          if (St) luni[top] = unite(luni[top], c);
+        }
+      }
+      // suffix unions of the thread-unmatched opens (deepest first)
+      KBox acc = kEMPTY();
+      int k = b_t;
+#pragma unroll
+      for (int i = K - 1; i >= 0; i--) {
+        if ((St >> i) & 1u) {
+          acc = unite(acc, luni[i]);
+          k--;
+          sc.uosu[uoff + k] = to_int4(acc);
+        }
+      }
+    }
+    s.sp[0][tid] = to_int4(pu);
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 1; k < LOGNT; k++) {
+      const int h = 1 << (k - 1);
+      KBox v = from_int4(s.sp[k - 1][tid]);
+      if (tid >= h) v = unite(v, from_int4(s.sp[k - 1][tid - h]));
+      s.sp[k][tid] = to_int4(v);
+      __syncthreads();
+    }
+
+    // ---- F. publish the tile union and slice-entry suffix unions ---------
+    {
+      const int s_t = max(b_t - sx.a, 0);
+      if (s_t > 0) {
+        const KBox after = range_union_threads(s, tid + 1, NT - 1);
+        for (int k = 0; k < s_t; k++) {
+          const KBox v = unite(from_int4(__ldcg(sc.uosu + uoff + k)), after);
+          p.f.su[(int64_t)T * TILE + (l_t + k + aT)] = to_int4(v);
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      if (lane == 0) {
+        __threadfence();
+        st_release_u32(p.f.suf + T, 1u);
+      }
+      publish_union(p.f, T, range_union_threads(s, 0, NT - 1));
+    }
+
+    // ---- G. unions reaching back into earlier tiles -------------------------
+    for (int r = warp; r < nr; r += NW) {
+      const int4 rr = __ldcg(sc.run + r);
+      const KBox mid = range_union_tiles(p.f, rr.x + 1, T - 1);
+      if (lane == 0) sc.runr[r] = to_int4(mid);
+    }
+    __syncthreads();
+    for (int d = tid; d < min(aT, H); d += NT) {
+      const int4 m = __ldcg(sc.meta + d);
+      const int U = __ldcg(sc.run + m.z).x;
+      while (ld_acquire_u32(p.f.suf + U) == 0u) {
+      }
+      const KBox v = unite(ld_kbox_cg(p.f.su + (int64_t)U * TILE + m.w), from_int4(__ldcg(sc.runr + m.z)));
+      sc.accin[d] = to_int4(v);
+    }
+    __syncthreads();
+
+    // ---- H. closes that pop entries of earlier threads / tiles -------------
+    {
+      int ref = top_ref;
+      int j = 0;
+#pragma unroll
+      for (int i = 0; i < K; i++) {
+        if ((ucm >> i) & 1u) {
+          const int64_t g = tbase + i;
+          KBox U;
+          bool blend = false;
+          int64_t oidx = -1;
+          if (ref >= 0) {
+            const int V = ref / K;
+            const KBox su = from_int4(__ldcg(sc.uosu + s.uoff[V] + rank_in(s.uo[V], ref % K)));
+            U = unite(unite(su, range_union_threads(s, V + 1, tid - 1)), pu_at[j]);
+            blend = (s.bmk[V] >> (ref % K)) & 1u;
+            oidx = base + ref;
+          } else {
+            const int dd = -ref - 1;
+            if (dd >= H) {
+              U = kEMPTY();  // nothing to close (R3)
+            } else {
+              const int4 m = __ldcg(sc.meta + dd);
+              U = unite(unite(from_int4(__ldcg(sc.accin + dd)), range_union_threads(s, 0, tid - 1)), pu_at[j]);
+              blend = m.y != 0;
+              oidx = m.x;
+            }
+          }
+          if (full || g < p.n) p.out[g] = to_float4(U);
+          if (blend) p.out[oidx] = to_float4(U);
+          ref = next_down(ref);
+          j++;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// pass 3: blend nodes still open at the end of the stream (R4)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ int range_min_L(const Ctrl& c, int a, int b) {
+  const int lane = threadIdx.x & 31;
+  int acc = INT_MAX;
+  int k = 0;
+  while (a <= b) {
+    const uint32_t* v = c.lv[k];
+    if ((a >> 5) == (b >> 5) || k == HLEVELS - 1) {
+      for (int i = a + lane; i <= b; i += 32) acc = min(acc, (int)(__ldg(v + i) - 1u));
+      break;
+    }
+    if (a & 31) {
+      const int e = a | 31, i = a + lane;
+      if (i <= e) acc = min(acc, (int)(__ldg(v + i) - 1u));
+      a = e + 1;
+    }
+    if ((b & 31) != 31) {
+      const int s0 = b & ~31, i = s0 + lane;
+      if (i <= b) acc = min(acc, (int)(__ldg(v + i) - 1u));
+      b = s0 - 1;
+    }
+    if (a > b) break;
+    a >>= 5;
+    b = ((b + 1) >> 5) - 1;
+    k++;
+  }
+  return __reduce_min_sync(0xffffffffu, acc);
+}
+
+__global__ void __launch_bounds__(128) bb_final(Params p) {
+  const int lane = threadIdx.x & 31;
+  const int W = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (W >= p.ntiles) return;
+  const int bW = __ldg(p.f.bcount + W);
+  if (bW == 0) return;
+  const int LW = (int)(__ldg(p.ctrl.lw + W) - 1u);
+  const int minL = (W + 1 < p.ntiles) ? range_min_L(p.ctrl, W + 1, p.ntiles - 1) : INT_MAX;
+  const int nsurv = min(bW, max(minL - LW, 0));  // entries at heights < minL survive
+  if (nsurv == 0) return;
+  const KBox after = (W + 1 < p.ntiles) ? range_union_tiles(p.f, W + 1, p.ntiles - 1) : kEMPTY();
+  for (int q = lane; q < nsurv; q += 32) {
+    const SliceRec rec = p.slice[(int64_t)W * SREC + q];
+    if (rec.kind) {
+      const KBox v = unite(ld_kbox_cg(p.f.su + (int64_t)W * TILE + q), after);
+      p.out[rec.idx] = to_float4(v);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// workspace
+// ----------------------------------------------------------------------------
+struct Layout {
+  size_t ctrl_bytes, fzero_off, fzero_bytes, data_off, bytes;
+  size_t off_counter, off_tcf, off_suf, off_uf[HLEVELS], off_ucnt[HLEVELS];
+  size_t off_tc, off_u[HLEVELS], off_su, off_bcount, off_slice, off_scratch;
+  int64_t ntiles;
+  int nblocks;
+  static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+  Layout(int64_t n, int nblocks_) : nblocks(nblocks_) {
+    ntiles = (n + TILE - 1) / TILE;
+    ctrl_bytes = CtrlLayout(ntiles).bytes;
+    size_t o = al(ctrl_bytes);
+    fzero_off = o;
+    off_counter = o; o = al(o + 16);
+    off_tcf = o; o = al(o + 4 * (size_t)ntiles);
+    off_suf = o; o = al(o + 4 * (size_t)ntiles);
+    int64_t m = ntiles;
+    for (int k = 0; k < HLEVELS; k++) {
+      off_uf[k] = o; o = al(o + 4 * (size_t)m);
+      off_ucnt[k] = o; o = al(o + 4 * (size_t)m);
+      m = (m + 31) / 32;
+    }
+    fzero_bytes = o - fzero_off;
+    data_off = o;
+    off_tc = o; o = al(o + 16 * (size_t)ntiles);
+    m = ntiles;
+    for (int k = 0; k < HLEVELS; k++) {
+      off_u[k] = o; o = al(o + 16 * (size_t)m);
+      m = (m + 31) / 32;
+    }
+    off_bcount = o; o = al(o + 4 * (size_t)ntiles);
+    off_su = o; o = al(o + 16 * (size_t)ntiles * TILE);
+    off_slice = o; o = al(o + sizeof(SliceRec) * (size_t)ntiles * SREC);
+    off_scratch = o; o = al(o + SCRATCH_BYTES * (size_t)nblocks);
+    bytes = o;
+  }
+};
+
+int finish_blocks() {
+  static int nb = 0;
+  if (nb == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(bb_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bb_finish, NT, sizeof(Smem));
+    nb = sms * (occ > 0 ? occ : 1);
+  }
+  return nb;
+}
+
+}  // namespace bb
+
+size_t bb_workspace_bytes(int64_t n) {
+  if (n <= 0) return 0;
+  return bb::Layout(n, bb::finish_blocks()).bytes;
+}
+
+cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
+                      cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int nb_max = bb::finish_blocks();
+  bb::Layout L(n, nb_max);
+  cudaError_t err = cudaMemsetAsync(ws, 0, L.ctrl_bytes, stream);
+  if (err == cudaSuccess) err = cudaMemsetAsync((char*)ws + L.fzero_off, 0, L.fzero_bytes, stream);
+  if (err != cudaSuccess) return err;
+  char* b = (char*)ws;
+  bb::Params p;
+  p.tags = tags;
+  p.boxes = reinterpret_cast<const float4*>(leaf_bbox);
+  p.out = reinterpret_cast<float4*>(node_bbox);
+  p.n = n;
+  p.ntiles = (int)L.ntiles;
+  p.ctrl = CtrlLayout(L.ntiles).bind(ws);
+  p.slice = (bb::SliceRec*)(b + L.off_slice);
+  p.f.counter = (uint32_t*)(b + L.off_counter);
+  p.f.tcf = (uint32_t*)(b + L.off_tcf);
+  p.f.suf = (uint32_t*)(b + L.off_suf);
+  for (int k = 0; k < HLEVELS; k++) {
+    p.f.uf[k] = (uint32_t*)(b + L.off_uf[k]);
+    p.f.ucnt[k] = (uint32_t*)(b + L.off_ucnt[k]);
+    p.f.u[k] = (int4*)(b + L.off_u[k]);
+  }
+  p.f.tc = (int4*)(b + L.off_tc);
+  p.f.su = (int4*)(b + L.off_su);
+  p.f.bcount = (int32_t*)(b + L.off_bcount);
+  p.scratch = b + L.off_scratch;
+  const int nfin = (int)std::min<int64_t>(L.ntiles, (int64_t)nb_max);
+  bb::bb_reduce<<<(unsigned)L.ntiles, bb::NT, 0, stream>>>(p);
+  bb::bb_finish<<<(unsigned)nfin, bb::NT, sizeof(bb::Smem), stream>>>(p);
+  bb::bb_final<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace tb
