@@ -69,8 +69,8 @@ size_t bic_count_workspace_bytes(int64_t n) {
 cudaError_t bic_count_launch(const uint8_t* tags, int64_t n, void* ws, int64_t* d_out2,
                              cudaStream_t stream) {
   const int64_t m = (n + bc::TILE - 1) / bc::TILE;
-  if (m > 0) bc::block_bic<<<(unsigned)m, bc::NT, 0, stream>>>(tags, n, (int2*)ws);
-  bc::fold_parts<<<1, 32, 0, stream>>>((const int2*)ws, m, d_out2);
+  if (m > 0) TB_LAUNCH(stream, "bic_block", (bc::block_bic<<<(unsigned)m, bc::NT, 0, stream>>>(tags, n, (int2*)ws)));
+  TB_LAUNCH(stream, "bic_fold", (bc::fold_parts<<<1, 32, 0, stream>>>((const int2*)ws, m, d_out2)));
   return cudaGetLastError();
 }
 

@@ -15,6 +15,17 @@ struct ShardInit {
   int lo;
 };
 
+// Launch accounting / optional event timing around each kernel (prof.cu).
+void prof_begin(cudaStream_t s, const char* name, void** token);
+void prof_end(cudaStream_t s, void* token);
+#define TB_LAUNCH(stream, name, ...)             \
+  do {                                           \
+    void* tb_tok_;                               \
+    ::tb::prof_begin((stream), (name), &tb_tok_); \
+    __VA_ARGS__;                                 \
+    ::tb::prof_end((stream), tb_tok_);           \
+  } while (0)
+
 size_t pm_workspace_bytes(int64_t n);
 size_t pm_ctrl_bytes(int64_t n);
 cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,

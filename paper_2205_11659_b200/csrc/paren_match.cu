@@ -298,8 +298,8 @@ cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* p
     if (err != cudaSuccess) return err;
     configured = true;
   }
-  pm::pm_reduce<<<(unsigned)ntiles, pm::NT, 0, stream>>>(p);
-  pm::pm_finish<<<(unsigned)ntiles, pm::NT, smem, stream>>>(p);
+  TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)ntiles, pm::NT, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "pm_finish", (pm::pm_finish<<<(unsigned)ntiles, pm::NT, smem, stream>>>(p)));
   return cudaGetLastError();
 }
 

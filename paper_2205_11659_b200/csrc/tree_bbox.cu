@@ -885,9 +885,9 @@ cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, fl
   p.f.bcount = (int32_t*)(b + L.off_bcount);
   p.scratch = b + L.off_scratch;
   const int nfin = (int)std::min<int64_t>(L.ntiles, (int64_t)nb_max);
-  bb::bb_reduce<<<(unsigned)L.ntiles, bb::NT, 0, stream>>>(p);
-  bb::bb_finish<<<(unsigned)nfin, bb::NT, sizeof(bb::Smem), stream>>>(p);
-  bb::bb_final<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p);
+  TB_LAUNCH(stream, "bb_reduce", (bb::bb_reduce<<<(unsigned)L.ntiles, bb::NT, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "bb_finish", (bb::bb_finish<<<(unsigned)nfin, bb::NT, sizeof(bb::Smem), stream>>>(p)));
+  TB_LAUNCH(stream, "bb_final", (bb::bb_final<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p)));
   return cudaGetLastError();
 }
 
