@@ -66,29 +66,40 @@ int oracle_paren_match(const uint8_t *tags, int64_t n, int32_t *match, int32_t *
 /* Bounding-box algebra (§6).                                   */
 /* Boxes are (x0, y0, x1, y1) fp32.  Intersection = (max x0, max y0, min x1, */
 /* min y1); union = (min x0, min y0, max x1, max y1) — raw, never            */
-/* canonicalised (DESIGN R9).  min/max are taken in the IEEE 754-2019        */
-/* totalOrder (-NaN < -inf < ... < -0 < +0 < ... < +inf < +NaN), so every    */
-/* result is a unique bit pattern (DESIGN R12).                              */
+/* canonicalised (DESIGN R9).  min/max (DESIGN R12): ordinary order with     */
+/* -0 below +0; a NaN operand is ignored (the other operand is returned),    */
+/* and two NaNs give the canonical NaN 0x7fffffff — IEEE 754-2008 minNum /   */
+/* maxNum with signed zeros ordered.  NaN is outside the input domain; the   */
+/* rule only makes every result a unique bit pattern.                        */
 /* ------------------------------------------------------------------------ */
 typedef struct { float x0, y0, x1, y1; } box_t;
 
 static uint32_t f32_bits(float x) { uint32_t u; memcpy(&u, &x, 4); return u; }
+static float bits_f32(uint32_t u) { float x; memcpy(&x, &u, 4); return x; }
+static int is_nan(float x) { return (f32_bits(x) & 0x7fffffffu) > 0x7f800000u; }
 
-/* totalOrder(x, y): x is ordered at or below y.  Written from the standard's
- * definition: a negative-signed value lies below every positive-signed one;
- * among equal signs, larger magnitude (bit pattern without the sign, which
- * orders finite < inf < NaN payloads) lies further from zero. */
-static int total_le(float x, float y)
+/* x ordered at or below y, for non-NaN x, y: numeric order, and -0 < +0. */
+static int ordered_le(float x, float y)
 {
-    uint32_t bx = f32_bits(x), by = f32_bits(y);
-    int neg_x = (bx >> 31) != 0, neg_y = (by >> 31) != 0;
-    uint32_t mx = bx & 0x7fffffffu, my = by & 0x7fffffffu;
-    if (neg_x != neg_y) return neg_x;          /* -anything <= +anything */
-    if (!neg_x) return mx <= my;               /* both positive-signed */
-    return mx >= my;                           /* both negative-signed */
+    if (x < y) return 1;
+    if (x > y) return 0;
+    /* equal: only the zeros can differ in bits */
+    return (f32_bits(x) >> 31) >= (f32_bits(y) >> 31);   /* -0 <= +0, x == x */
 }
-static float tmin(float x, float y) { return total_le(x, y) ? x : y; }
-static float tmax(float x, float y) { return total_le(x, y) ? y : x; }
+static float tmin(float x, float y)
+{
+    if (is_nan(x) && is_nan(y)) return bits_f32(0x7fffffffu);
+    if (is_nan(x)) return y;
+    if (is_nan(y)) return x;
+    return ordered_le(x, y) ? x : y;
+}
+static float tmax(float x, float y)
+{
+    if (is_nan(x) && is_nan(y)) return bits_f32(0x7fffffffu);
+    if (is_nan(x)) return y;
+    if (is_nan(y)) return x;
+    return ordered_le(x, y) ? y : x;
+}
 
 static box_t isect(box_t p, box_t q)
 {

@@ -108,9 +108,10 @@ def match_from_parent(tags, parent):
 
 
 # ----------------------------------------------------------------------------
-# Boxes.  Coordinates are handled as fp32 bit patterns; min/max use IEEE
-# totalOrder, implemented here through an unsigned key (a different mapping
-# from the oracle's case analysis and from the kernels' signed key).
+# Boxes.  Coordinates are handled as fp32 bit patterns; min/max order -0
+# below +0 through an unsigned totalOrder key (a different mechanism from the
+# oracle's comparisons and from the kernels' FMNMX); NaN operands are ignored
+# (DESIGN R12).
 # ----------------------------------------------------------------------------
 
 def f2u(x: float) -> int:
@@ -125,11 +126,30 @@ def _key(u: int) -> int:
     return (~u) & 0xFFFFFFFF if u & 0x80000000 else u | 0x80000000
 
 
+def _isnan(u: int) -> bool:
+    return (u & 0x7FFFFFFF) > 0x7F800000
+
+
+QNAN = 0x7FFFFFFF  # canonical NaN when both operands are NaN (DESIGN R12)
+
+
 def umin(p: int, q: int) -> int:
+    if _isnan(p) and _isnan(q):
+        return QNAN
+    if _isnan(p):
+        return q
+    if _isnan(q):
+        return p
     return p if _key(p) <= _key(q) else q
 
 
 def umax(p: int, q: int) -> int:
+    if _isnan(p) and _isnan(q):
+        return QNAN
+    if _isnan(p):
+        return q
+    if _isnan(q):
+        return p
     return q if _key(p) <= _key(q) else p
 
 
