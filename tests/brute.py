@@ -183,7 +183,7 @@ def bbox_by_ancestors(tags, boxes_u):
         t = tags[i]
         if t == CLOSE or t == 2:
             continue
-        c = boxes_u[i]
+        c = isect_u(boxes_u[i], INF_U)  # ∩ over an empty ancestor set = INF (R11)
         p = parent[i]
         while p != -1:
             if tags[p] == 1:
