@@ -205,6 +205,21 @@ int tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, f
   return TB_OK;
 }
 
+/* Debug (not in the public header): tree_bbox with per-tile phase timestamps
+ * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
+int tb_debug_tree_bbox_trace(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox,
+                             uint64_t* d_trace, void* stream) {
+  g_err[0] = 0;
+  int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
+  if (r || n == 0) return r;
+  void* ws = nullptr;
+  r = get_ws(stream, 3, tb::bb_workspace_bytes(n), &ws);
+  if (r) return r;
+  cudaError_t e = tb::bb_launch(d_tags, d_leaf_bbox, n, d_node_bbox, ws, (cudaStream_t)stream, d_trace);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_bbox launch");
+  return TB_OK;
+}
+
 int tb_count_unmatched(const uint8_t* d_tags, int64_t n, int64_t* h_a, int64_t* h_b, void* stream) {
   g_err[0] = 0;
   int r = check_n(n);

@@ -33,7 +33,7 @@ cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* p
 
 size_t bb_workspace_bytes(int64_t n);
 cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
-                      cudaStream_t stream);
+                      cudaStream_t stream, uint64_t* trace = nullptr);
 
 size_t bic_count_workspace_bytes(int64_t n);
 cudaError_t bic_count_launch(const uint8_t* tags, int64_t n, void* ws, int64_t* d_out2,

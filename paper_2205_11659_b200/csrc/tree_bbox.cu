@@ -51,7 +51,7 @@ constexpr int LOGNT = 8;
 constexpr int SREC = TILE + 1;  // slice records per tile
 
 struct SliceRec {
-  int4 lc;   // tile-local cumulative clip (keys)
+  float4 lc; // tile-local cumulative clip
   int idx;   // original element index
   int kind;  // 1 = blend open, 0 = clip open
   int pad0, pad1;
@@ -64,22 +64,22 @@ struct FState {
   uint32_t* suf;            // [ntiles] suffix unions published
   uint32_t* uf[HLEVELS];    // [k][g] union hierarchy published (k = 0: per tile)
   uint32_t* ucnt[HLEVELS];  // arrival counters (k >= 1)
-  int4* tc;                 // [ntiles] true clip just below the tile's low-water mark
-  int4* u[HLEVELS];         // [k][g] union of true-clipped leaves (k = 0: per tile)
-  int4* su;                 // [ntiles * TILE] true union of leaves after each slice entry
+  float4* tc;               // [ntiles] true clip just below the tile's low-water mark
+  float4* u[HLEVELS];       // [k][g] union of true-clipped leaves (k = 0: per tile)
+  float4* su;               // [ntiles * TILE] true union of leaves after each slice entry
   int32_t* bcount;          // [ntiles] slice length (written by pass 1)
 };
 
 // Per-CTA scratch of the persistent finish pass (global, L2-resident).
 struct Scratch {
-  int4* cin;    // [TILE+1] clip of the incoming entry at depth d (lc, then true)
-  int4* meta;   // [TILE+1] {index, kind, run, slice position}
-  int4* accin;  // [TILE+1] union of leaves from the entry's open to the tile start
-  int4* uoc;    // [TILE]   thread-local cumulative clip of each thread-unmatched open
-  int4* uosu;   // [TILE]   union of the thread's leaves after each thread-unmatched open
-  int4* run;    // [TILE+1] {tile, L, lo, hi}
-  int4* runtc;  // [TILE+1] TC of the run's tile
-  int4* runr;   // [TILE+1] union over the tiles between the run's tile and this tile
+  float4* cin;    // [TILE+1] clip of the incoming entry at depth d (lc, then true)
+  int4* meta;     // [TILE+1] {index, kind, run, slice position}
+  float4* accin;  // [TILE+1] union of leaves from the entry's open to the tile start
+  float4* uoc;    // [TILE]   thread-local cumulative clip of each thread-unmatched open
+  float4* uosu;   // [TILE]   union of the thread's leaves after each thread-unmatched open
+  int4* run;      // [TILE+1] {tile, L, lo, hi}
+  float4* runtc;  // [TILE+1] TC of the run's tile
+  float4* runr;   // [TILE+1] union over the tiles between the run's tile and this tile
 };
 constexpr size_t SCRATCH_BYTES = 16 * (size_t)(7 * (TILE + 1) + TILE) + 1024;
 
@@ -93,7 +93,18 @@ struct Params {
   SliceRec* slice;  // [ntiles * SREC]
   FState f;
   char* scratch;
+  uint64_t* trace;  // optional per-tile phase timestamps (debug)
 };
+
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define BB_TRACE(T, slot)                                                           \
+  do {                                                                              \
+    if (p.trace && threadIdx.x == 0) p.trace[(size_t)(T) * 16 + (slot)] = gtime();  \
+  } while (0)
 
 // ----------------------------------------------------------------------------
 // small helpers
@@ -145,7 +156,7 @@ __device__ __forceinline__ void walk8(uint32_t om, uint32_t cm, uint32_t& S_out,
   ucm_out = ucm;
 }
 
-__device__ __forceinline__ KBox ld_kbox_cg(const int4* p) { return from_int4(__ldcg(p)); }
+__device__ __forceinline__ float4 ld_box_cg(const float4* p) { return __ldcg(p); }
 
 // Exclusive block scan of an int (sum).
 template <int NW_>
@@ -172,22 +183,22 @@ __device__ __forceinline__ int block_excl_sum(int v, int* wsum, int& total) {
 
 // Exclusive block ∩-scan of a box (thread order).
 template <int NW_>
-__device__ __forceinline__ KBox block_excl_isect(KBox v, KBox* wbox) {
+__device__ __forceinline__ float4 block_excl_isect(float4 v, float4* wbox) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  KBox x = v;
+  float4 x = v;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const KBox o = shfl_up_box(x, off);
+    const float4 o = shfl_up_box(x, off);
     if (lane >= off) x = isect(x, o);
   }
   if (lane == 31) wbox[warp] = x;
   __syncthreads();
-  KBox pre = kINF();
+  float4 pre = bINF();
 #pragma unroll
   for (int w = 0; w < NW_; w++)
     if (w < warp) pre = isect(pre, wbox[w]);
-  KBox e = shfl_up_box(x, 1);
-  if (lane == 0) e = kINF();
+  float4 e = shfl_up_box(x, 1);
+  if (lane == 0) e = bINF();
   return isect(pre, e);
 }
 
@@ -196,7 +207,7 @@ __device__ __forceinline__ KBox block_excl_isect(KBox v, KBox* wbox) {
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
   __shared__ Bic wtot[NW];
-  __shared__ KBox wbox[NW];
+  __shared__ float4 wbox[NW];
   __shared__ int s_tile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_tile = (int)atomicAdd(p.ctrl.counter, 1u);
@@ -227,15 +238,15 @@ __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
       m &= m - 1;
     }
   }
-  KBox bx[K];
-  KBox own = kINF();
+  float4 bx[K];
+  float4 own = bINF();
 #pragma unroll
   for (int i = 0; i < K; i++) {
-    bx[i] = kINF();
-    if (((surv & ~bm) >> i) & 1u) bx[i] = to_kbox(__ldg(p.boxes + tbase + i));
+    bx[i] = bINF();
+    if (((surv & ~bm) >> i) & 1u) bx[i] = (__ldg(p.boxes + tbase + i));
     own = isect(own, bx[i]);
   }
-  KBox acc = block_excl_isect<NW>(own, wbox);
+  float4 acc = block_excl_isect<NW>(own, wbox);
   {
     const int l_t = ex.b - ex.a - a_t;
     int k = 0;
@@ -244,7 +255,7 @@ __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
       if ((surv >> i) & 1u) {
         acc = isect(acc, bx[i]);
         SliceRec r;
-        r.lc = to_int4(acc);
+        r.lc = (acc);
         r.idx = (int)(tbase + i);
         r.kind = (int)((bm >> i) & 1u);
         r.pad0 = r.pad1 = 0;
@@ -266,20 +277,20 @@ __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
 // ----------------------------------------------------------------------------
 // hierarchy of per-tile unions (finish pass)
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ KBox wait_box(const uint32_t* flag, const int4* val) {
+__device__ __forceinline__ float4 wait_box(const uint32_t* flag, const float4* val) {
   while (ld_acquire_u32(flag) == 0u) {
   }
-  return ld_kbox_cg(val);
+  return ld_box_cg(val);
 }
 
 // Union over tiles [a, b] (warp-cooperative; waits for unpublished entries).
-__device__ __forceinline__ KBox range_union_tiles(const FState& f, int a, int b) {
+__device__ __forceinline__ float4 range_union_tiles(const FState& f, int a, int b) {
   const int lane = threadIdx.x & 31;
-  KBox acc = kEMPTY();
+  float4 acc = bEMPTY();
   int k = 0;
   while (a <= b) {
     const uint32_t* fl = f.uf[k];
-    const int4* val = f.u[k];
+    const float4* val = f.u[k];
     if ((a >> 5) == (b >> 5) || k == HLEVELS - 1) {
       for (int i = a + lane; i <= b; i += 32) acc = unite(acc, wait_box(fl + i, val + i));
       break;
@@ -306,10 +317,10 @@ __device__ __forceinline__ KBox range_union_tiles(const FState& f, int a, int b)
 
 // Publish the tile's union and fold it into the hierarchy (warp; the last of
 // 32 siblings publishes the parent).
-__device__ __forceinline__ void publish_union(const FState& f, int T, KBox tu) {
+__device__ __forceinline__ void publish_union(const FState& f, int T, float4 tu) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
-    f.u[0][T] = to_int4(tu);
+    f.u[0][T] = (tu);
     __threadfence();
     st_release_u32(f.uf[0] + T, 1u);
   }
@@ -322,10 +333,10 @@ __device__ __forceinline__ void publish_union(const FState& f, int T, KBox tu) {
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != 31u) return;
     const int c = (g << 5) + lane;
-    KBox v = wait_box(f.uf[k - 1] + c, f.u[k - 1] + c);
+    float4 v = wait_box(f.uf[k - 1] + c, f.u[k - 1] + c);
     v = warp_unite_all(v);
     if (lane == 0) {
-      f.u[k][g] = to_int4(v);
+      f.u[k][g] = (v);
       __threadfence();
       st_release_u32(f.uf[k] + g, 1u);
     }
@@ -338,12 +349,12 @@ __device__ __forceinline__ void publish_union(const FState& f, int T, KBox tu) {
 // the owner chain (warp-parallel over 32 predecessors at a time), combining
 // the chain tiles' tile-local clips, until a tile that already published its
 // own TC.
-__device__ KBox chain_tc(const Params& p, int u, int Lu) {
+__device__ float4 chain_tc(const Params& p, int u, int Lu) {
   const int lane = threadIdx.x & 31;
-  KBox acc = kINF();
+  float4 acc = bINF();
   int h = Lu - 1;
   while (h >= 0) {
-    if (ld_acquire_u32(p.f.tcf + u)) return isect(acc, ld_kbox_cg(p.f.tc + u));
+    if (ld_acquire_u32(p.f.tcf + u)) return isect(acc, ld_box_cg(p.f.tc + u));
     const int t = u - 1 - lane;
     const int L = t >= 0 ? (int)(__ldg(p.ctrl.lw + t) - 1u) : INT_MAX;
     const uint32_t fl = t >= 0 ? ld_acquire_u32(p.f.tcf + t) : 0u;
@@ -366,17 +377,17 @@ __device__ KBox chain_tc(const Params& p, int u, int Lu) {
       int LW = 0;
       const int W = owner_search_done(p.ctrl, u - 32, h, LW);
       if (W < 0) return acc;
-      acc = isect(acc, from_int4(__ldg(&p.slice[(int64_t)W * SREC + (h - LW)].lc)));
+      acc = isect(acc, (__ldg(&p.slice[(int64_t)W * SREC + (h - LW)].lc)));
       u = W;
       h = LW - 1;
       continue;
     }
     const int klim = mres ? (__ffs(mres) - 1) : 31;
-    KBox c = kINF();
-    if (on && lane <= klim) c = from_int4(__ldg(&p.slice[(int64_t)t * SREC + (thr - L)].lc));
+    float4 c = bINF();
+    if (on && lane <= klim) c = (__ldg(&p.slice[(int64_t)t * SREC + (thr - L)].lc));
     acc = isect(acc, warp_isect_all(c));
     if (mres) {
-      const KBox tcr = shfl_box(t >= 0 ? ld_kbox_cg(p.f.tc + max(t, 0)) : kINF(), klim);
+      const float4 tcr = shfl_box(t >= 0 ? ld_box_cg(p.f.tc + max(t, 0)) : bINF(), klim);
       return isect(acc, tcr);
     }
     const int last = 31 - __clz(mon);
@@ -398,11 +409,11 @@ struct Smem {
   uint32_t bmk[NT];
   int uoff[NT];
   int link[NT];
-  int4 pjacc[2][NT];
+  float4 pjacc[2][NT];
   int pjptr[2][NT];
   int pjesc[2][NT];
-  int4 tl[NT];
-  int4 sp[LOGNT][NT];  // sparse table of per-thread unions of true-clipped leaves
+  float4 tl[NT];
+  float4 sp[LOGNT][NT];  // sparse table of per-thread unions of true-clipped leaves
   Bic wtot[NW];
   int wsum[NW];
   int tile, nruns;
@@ -410,11 +421,11 @@ struct Smem {
 
 __device__ __forceinline__ int rank_in(uint32_t m, int bit) { return __popc(m & ((1u << bit) - 1u)); }
 
-__device__ __forceinline__ KBox range_union_threads(const Smem& s, int a, int b) {
-  if (a > b) return kEMPTY();
+__device__ __forceinline__ float4 range_union_threads(const Smem& s, int a, int b) {
+  if (a > b) return bEMPTY();
   const int len = b - a + 1;
   const int k = min(31 - __clz(len), LOGNT - 1);  // two windows of 2^k cover len <= 2^LOGNT
-  return unite(from_int4(s.sp[k][b]), from_int4(s.sp[k][a + (1 << k) - 1]));
+  return unite((s.sp[k][b]), (s.sp[k][a + (1 << k) - 1]));
 }
 
 __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
@@ -423,12 +434,12 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Scratch sc;
   {
-    int4* b = reinterpret_cast<int4*>(p.scratch + (size_t)blockIdx.x * SCRATCH_BYTES);
+    float4* b = reinterpret_cast<float4*>(p.scratch + (size_t)blockIdx.x * SCRATCH_BYTES);
     sc.cin = b;
-    sc.meta = sc.cin + (TILE + 1);
-    sc.accin = sc.meta + (TILE + 1);
-    sc.run = sc.accin + (TILE + 1);
-    sc.runtc = sc.run + (TILE + 1);
+    sc.meta = reinterpret_cast<int4*>(sc.cin + (TILE + 1));
+    sc.accin = reinterpret_cast<float4*>(sc.meta + (TILE + 1));
+    sc.run = reinterpret_cast<int4*>(sc.accin + (TILE + 1));
+    sc.runtc = reinterpret_cast<float4*>(sc.run + (TILE + 1));
     sc.runr = sc.runtc + (TILE + 1);
     sc.uoc = sc.runr + (TILE + 1);
     sc.uosu = sc.uoc + TILE;
@@ -443,14 +454,15 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     const int64_t tbase = base + (int64_t)tid * K;
     const bool full = base + TILE <= p.n;
 
+    BB_TRACE(T, 0);
     // ---- A. load ------------------------------------------------------------
     uint32_t om, cm, bm, S, ucm;
     classify8(load_tags8(p.tags, p.n, tbase, full), om, cm, bm);
-    KBox bx[K];
+    float4 bx[K];
 #pragma unroll
     for (int i = 0; i < K; i++) {
       const bool need = ((~cm & ~bm) >> i) & 1u;  // leaves and clip opens carry boxes
-      bx[i] = (need && (full || tbase + i < p.n)) ? to_kbox(__ldg(p.boxes + tbase + i)) : kINF();
+      bx[i] = (need && (full || tbase + i < p.n)) ? (__ldg(p.boxes + tbase + i)) : bINF();
     }
     walk8(om, cm, S, ucm);
     const int a_t = __popc(ucm), b_t = __popc(S);
@@ -477,13 +489,13 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     s.uoff[tid] = uoff;
     // thread-local cumulative clip of each thread-unmatched open
     {
-      KBox acc = kINF();
+      float4 acc = bINF();
       int k = 0;
 #pragma unroll
       for (int i = 0; i < K; i++) {
         if ((S >> i) & 1u) {
           if (!((bm >> i) & 1u)) acc = isect(acc, bx[i]);
-          sc.uoc[uoff + k] = to_int4(acc);
+          sc.uoc[uoff + k] = (acc);
           k++;
         }
       }
@@ -491,13 +503,14 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     const int H = __ldg(p.ctrl.hstart + T);
     const int lo = max(H - 1 - aT, 0);
     for (int d = H + tid; d <= aT; d += NT) {
-      sc.cin[d] = to_int4(kINF());
+      sc.cin[d] = (bINF());
       sc.meta[d] = make_int4(-1, 0, -1, 0);
     }
     __syncthreads();
     const int top_ref = thread_ref<NW, K>(wl, l_t, S, r_t - 1, s.win, s.wmin, s.l, s.uo);
     const int link_ref = thread_ref<NW, K>(wl, l_t, S, l_t - 1, s.win, s.wmin, s.l, s.uo);
 
+    BB_TRACE(T, 1);
     // ---- C. incoming stack: runs of predecessors' slices ------------------
     if (warp == 0) {
       int cur = H - 1, from = T, nr = 0;
@@ -526,21 +539,22 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
       }
     }
     __syncthreads();
+    BB_TRACE(T, 2);
     // TC of each run's tile: deepest by look-back, the others from the run below
     if (warp == 0 && nr > 0) {
       const int4 rb = __ldcg(sc.run + nr - 1);
-      KBox tc = chain_tc(p, rb.x, rb.y);
-      if (lane == 0) sc.runtc[nr - 1] = to_int4(tc);
+      float4 tc = chain_tc(p, rb.x, rb.y);
+      if (lane == 0) sc.runtc[nr - 1] = (tc);
       for (int r = nr - 2; r >= 0; r--) {
         const int4 rbelow = __ldcg(sc.run + r + 1);
-        tc = isect(from_int4(__ldcg(sc.cin + (H - 1 - rbelow.w))), tc);
-        if (lane == 0) sc.runtc[r] = to_int4(tc);
+        tc = isect((__ldcg(sc.cin + (H - 1 - rbelow.w))), tc);
+        if (lane == 0) sc.runtc[r] = (tc);
       }
     }
     __syncthreads();
     for (int d = tid; d < min(aT + 1, H); d += NT) {
       const int run = __ldcg(sc.meta + d).z;
-      sc.cin[d] = to_int4(isect(from_int4(__ldcg(sc.cin + d)), from_int4(__ldcg(sc.runtc + run))));
+      sc.cin[d] = (isect((__ldcg(sc.cin + d)), (__ldcg(sc.runtc + run))));
     }
     __syncthreads();
     if (tid == 0) {
@@ -549,45 +563,46 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
       st_release_u32(p.f.tcf + T, 1u);
     }
 
+    BB_TRACE(T, 3);
     // ---- D. thread chains: clip of each thread's link entry ---------------
     {
       int ptr = -1, esc = 0;
-      KBox acc = kINF();
+      float4 acc = bINF();
       if (link_ref >= 0) {
         const int W = link_ref / K;
         ptr = W;
-        acc = from_int4(__ldcg(sc.uoc + s.uoff[W] + rank_in(s.uo[W], link_ref % K)));
+        acc = (__ldcg(sc.uoc + s.uoff[W] + rank_in(s.uo[W], link_ref % K)));
       } else {
         esc = link_ref;
       }
       int cb = 0;
-      s.pjacc[0][tid] = to_int4(acc);
+      s.pjacc[0][tid] = (acc);
       s.pjptr[0][tid] = ptr;
       s.pjesc[0][tid] = esc;
       __syncthreads();
       for (int round = 0; round < LOGNT; round++) {
         if (ptr >= 0) {
-          acc = isect(acc, from_int4(s.pjacc[cb][ptr]));
+          acc = isect(acc, (s.pjacc[cb][ptr]));
           esc = s.pjesc[cb][ptr];
           ptr = s.pjptr[cb][ptr];
         }
-        s.pjacc[cb ^ 1][tid] = to_int4(acc);
+        s.pjacc[cb ^ 1][tid] = (acc);
         s.pjptr[cb ^ 1][tid] = ptr;
         s.pjesc[cb ^ 1][tid] = esc;
         cb ^= 1;
         __syncthreads();
       }
-      s.tl[tid] = to_int4(isect(acc, from_int4(__ldcg(sc.cin + (-esc - 1)))));
+      s.tl[tid] = (isect(acc, (__ldcg(sc.cin + (-esc - 1)))));
     }
     __syncthreads();
 
     // true clip of an entry of this thread's start stack
-    auto entry_clip = [&](int ref) -> KBox {
+    auto entry_clip = [&](int ref) -> float4 {
       if (ref >= 0) {
         const int V = ref / K;
-        return isect(from_int4(__ldcg(sc.uoc + s.uoff[V] + rank_in(s.uo[V], ref % K))), from_int4(s.tl[V]));
+        return isect((__ldcg(sc.uoc + s.uoff[V] + rank_in(s.uo[V], ref % K))), (s.tl[V]));
       }
-      return from_int4(__ldcg(sc.cin + (-ref - 1)));
+      return (__ldcg(sc.cin + (-ref - 1)));
     };
     auto next_down = [&](int ref) -> int {
       if (ref >= 0) {
@@ -600,82 +615,89 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     s.link[tid] = link_ref;
     __syncthreads();
 
+    BB_TRACE(T, 4);
     // ---- E. per-thread two-box stack walk ----------------------------
-    KBox lclip[K], luni[K], pu_at[K];
-    KBox pu = kEMPTY();  // union of this thread's clipped leaves so far
+    // The thread's stack is the bitmask St of its open positions; the clip of
+    // the top is the effective clip of the deepest clip open on it (a blend
+    // passes its parent's clip through), else the clip of the external top.
+    // A node closed inside the thread gets the union of the clipped leaves
+    // strictly inside it (predicated loop over the thread's 8 values).
+    uint32_t lm = ~om & ~cm & 0xffu;  // leaves
+    if (!full) {
+      const int64_t rem = p.n - tbase;
+      lm &= rem >= K ? 0xffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+    }
+    const uint32_t clipm = om & ~bm;
+    float4 suf = bEMPTY();  // union of all this thread's clipped leaves (filled below)
     {
       int ref = top_ref;
-      KBox cext = entry_clip(ref);
+      float4 cext = entry_clip(ref);
+      float4 ctop = cext;
       uint32_t St = 0;
-      int dcur = 0;
 #pragma unroll
       for (int i = 0; i < K; i++) {
         const uint32_t bit = 1u << i;
-        const int top = 31 - __clz(St);
-        const KBox ctop = St ? lclip[top] : cext;
         const int64_t g = tbase + i;
-        const bool live = full || g < p.n;
         if (om & bit) {
-          const bool blend = bm & bit;
-          const KBox c = blend ? ctop : isect(bx[i], ctop);
-          lclip[i] = c;
-          luni[i] = kEMPTY();
-          if (!blend && live) p.out[g] = to_float4(c);
+          if (!(bm & bit)) {
+            bx[i] = isect(bx[i], ctop);
+            ctop = bx[i];
+            p.out[g] = bx[i];
+          }
           St |= bit;
         } else if (cm & bit) {
           if (St) {
-            const KBox U = luni[top];
-            if (live) p.out[g] = to_float4(U);
-            if ((bm >> top) & 1u) p.out[tbase + top] = to_float4(U);
-            St ^= 1u << top;
-            if (St) {
-              const int nt = 31 - __clz(St);
-              luni[nt] = unite(luni[nt], U);
-            }
+            const int o = 31 - __clz(St);
+            float4 U = bEMPTY();
+#pragma unroll
+            for (int j = 0; j < i; j++)
+              if (((lm >> j) & 1u) && j > o) U = unite(U, bx[j]);
+            p.out[g] = U;
+            if ((bm >> o) & 1u) p.out[tbase + o] = U;
+            St ^= 1u << o;
+            const uint32_t cs = St & clipm;
+            const int jt = cs ? 31 - __clz(cs) : -1;
+            ctop = cext;
+#pragma unroll
+            for (int j = 0; j < i; j++)
+              if (j == jt) ctop = bx[j];
           } else {
-            pu_at[dcur] = pu;
-            dcur++;
             ref = next_down(ref);
             cext = entry_clip(ref);
+            ctop = cext;
           }
-        } else if (live) {
-          const KBox c = isect(bx[i], ctop);
-          p.out[g] = to_float4(c);
-          pu = unite(pu, c);
-          if (St) luni[top] = unite(luni[top], c);
+        } else if ((lm >> i) & 1u) {
+          bx[i] = isect(bx[i], ctop);
+          p.out[g] = bx[i];
         }
       }
-      // suffix unions of the thread-unmatched opens (deepest first)
-      KBox acc = kEMPTY();
-      int k = b_t;
+      // suffix unions after each thread-unmatched open (St = those opens)
 #pragma unroll
-      for (int i = K - 1; i >= 0; i--) {
-        if ((St >> i) & 1u) {
-          acc = unite(acc, luni[i]);
-          k--;
-          sc.uosu[uoff + k] = to_int4(acc);
-        }
+      for (int j = K - 1; j >= 0; j--) {
+        if ((St >> j) & 1u) sc.uosu[uoff + __popc(St & ((1u << j) - 1u))] = suf;
+        if ((lm >> j) & 1u) suf = unite(suf, bx[j]);
       }
     }
-    s.sp[0][tid] = to_int4(pu);
+    s.sp[0][tid] = suf;
     __syncthreads();
 #pragma unroll 1
     for (int k = 1; k < LOGNT; k++) {
       const int h = 1 << (k - 1);
-      KBox v = from_int4(s.sp[k - 1][tid]);
-      if (tid >= h) v = unite(v, from_int4(s.sp[k - 1][tid - h]));
-      s.sp[k][tid] = to_int4(v);
+      float4 v = (s.sp[k - 1][tid]);
+      if (tid >= h) v = unite(v, (s.sp[k - 1][tid - h]));
+      s.sp[k][tid] = (v);
       __syncthreads();
     }
 
+    BB_TRACE(T, 5);
     // ---- F. publish the tile union and slice-entry suffix unions ---------
     {
       const int s_t = max(b_t - sx.a, 0);
       if (s_t > 0) {
-        const KBox after = range_union_threads(s, tid + 1, NT - 1);
+        const float4 after = range_union_threads(s, tid + 1, NT - 1);
         for (int k = 0; k < s_t; k++) {
-          const KBox v = unite(from_int4(__ldcg(sc.uosu + uoff + k)), after);
-          p.f.su[(int64_t)T * TILE + (l_t + k + aT)] = to_int4(v);
+          const float4 v = unite((__ldcg(sc.uosu + uoff + k)), after);
+          p.f.su[(int64_t)T * TILE + (l_t + k + aT)] = (v);
         }
       }
     }
@@ -688,11 +710,12 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
       publish_union(p.f, T, range_union_threads(s, 0, NT - 1));
     }
 
+    BB_TRACE(T, 6);
     // ---- G. unions reaching back into earlier tiles -------------------------
     for (int r = warp; r < nr; r += NW) {
       const int4 rr = __ldcg(sc.run + r);
-      const KBox mid = range_union_tiles(p.f, rr.x + 1, T - 1);
-      if (lane == 0) sc.runr[r] = to_int4(mid);
+      const float4 mid = range_union_tiles(p.f, rr.x + 1, T - 1);
+      if (lane == 0) sc.runr[r] = (mid);
     }
     __syncthreads();
     for (int d = tid; d < min(aT, H); d += NT) {
@@ -700,46 +723,50 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
       const int U = __ldcg(sc.run + m.z).x;
       while (ld_acquire_u32(p.f.suf + U) == 0u) {
       }
-      const KBox v = unite(ld_kbox_cg(p.f.su + (int64_t)U * TILE + m.w), from_int4(__ldcg(sc.runr + m.z)));
-      sc.accin[d] = to_int4(v);
+      const float4 v = unite(ld_box_cg(p.f.su + (int64_t)U * TILE + m.w), (__ldcg(sc.runr + m.z)));
+      sc.accin[d] = (v);
     }
     __syncthreads();
 
+    BB_TRACE(T, 7);
     // ---- H. closes that pop entries of earlier threads / tiles -------------
     {
       int ref = top_ref;
-      int j = 0;
 #pragma unroll
       for (int i = 0; i < K; i++) {
         if ((ucm >> i) & 1u) {
           const int64_t g = tbase + i;
-          KBox U;
+          float4 PU = bEMPTY();  // this thread's clipped leaves before the close
+#pragma unroll
+          for (int j = 0; j < i; j++)
+            if ((lm >> j) & 1u) PU = unite(PU, bx[j]);
+          float4 U;
           bool blend = false;
           int64_t oidx = -1;
           if (ref >= 0) {
             const int V = ref / K;
-            const KBox su = from_int4(__ldcg(sc.uosu + s.uoff[V] + rank_in(s.uo[V], ref % K)));
-            U = unite(unite(su, range_union_threads(s, V + 1, tid - 1)), pu_at[j]);
+            const float4 su = __ldcg(sc.uosu + s.uoff[V] + rank_in(s.uo[V], ref % K));
+            U = unite(unite(su, range_union_threads(s, V + 1, tid - 1)), PU);
             blend = (s.bmk[V] >> (ref % K)) & 1u;
             oidx = base + ref;
           } else {
             const int dd = -ref - 1;
             if (dd >= H) {
-              U = kEMPTY();  // nothing to close (R3)
+              U = bEMPTY();  // nothing to close (R3)
             } else {
               const int4 m = __ldcg(sc.meta + dd);
-              U = unite(unite(from_int4(__ldcg(sc.accin + dd)), range_union_threads(s, 0, tid - 1)), pu_at[j]);
+              U = unite(unite(__ldcg(sc.accin + dd), range_union_threads(s, 0, tid - 1)), PU);
               blend = m.y != 0;
               oidx = m.x;
             }
           }
-          if (full || g < p.n) p.out[g] = to_float4(U);
-          if (blend) p.out[oidx] = to_float4(U);
+          p.out[g] = U;
+          if (blend) p.out[oidx] = U;
           ref = next_down(ref);
-          j++;
         }
       }
     }
+    BB_TRACE(T, 8);
     __syncthreads();
   }
 }
@@ -785,12 +812,12 @@ __global__ void __launch_bounds__(128) bb_final(Params p) {
   const int minL = (W + 1 < p.ntiles) ? range_min_L(p.ctrl, W + 1, p.ntiles - 1) : INT_MAX;
   const int nsurv = min(bW, max(minL - LW, 0));  // entries at heights < minL survive
   if (nsurv == 0) return;
-  const KBox after = (W + 1 < p.ntiles) ? range_union_tiles(p.f, W + 1, p.ntiles - 1) : kEMPTY();
+  const float4 after = (W + 1 < p.ntiles) ? range_union_tiles(p.f, W + 1, p.ntiles - 1) : bEMPTY();
   for (int q = lane; q < nsurv; q += 32) {
     const SliceRec rec = p.slice[(int64_t)W * SREC + q];
     if (rec.kind) {
-      const KBox v = unite(ld_kbox_cg(p.f.su + (int64_t)W * TILE + q), after);
-      p.out[rec.idx] = to_float4(v);
+      const float4 v = unite(ld_box_cg(p.f.su + (int64_t)W * TILE + q), after);
+      p.out[rec.idx] = (v);
     }
   }
 }
@@ -856,7 +883,7 @@ size_t bb_workspace_bytes(int64_t n) {
 }
 
 cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, uint64_t* trace) {
   if (n <= 0) return cudaSuccess;
   const int nb_max = bb::finish_blocks();
   bb::Layout L(n, nb_max);
@@ -878,12 +905,13 @@ cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, fl
   for (int k = 0; k < HLEVELS; k++) {
     p.f.uf[k] = (uint32_t*)(b + L.off_uf[k]);
     p.f.ucnt[k] = (uint32_t*)(b + L.off_ucnt[k]);
-    p.f.u[k] = (int4*)(b + L.off_u[k]);
+    p.f.u[k] = (float4*)(b + L.off_u[k]);
   }
-  p.f.tc = (int4*)(b + L.off_tc);
-  p.f.su = (int4*)(b + L.off_su);
+  p.f.tc = (float4*)(b + L.off_tc);
+  p.f.su = (float4*)(b + L.off_su);
   p.f.bcount = (int32_t*)(b + L.off_bcount);
   p.scratch = b + L.off_scratch;
+  p.trace = trace;
   const int nfin = (int)std::min<int64_t>(L.ntiles, (int64_t)nb_max);
   TB_LAUNCH(stream, "bb_reduce", (bb::bb_reduce<<<(unsigned)L.ntiles, bb::NT, 0, stream>>>(p)));
   TB_LAUNCH(stream, "bb_finish", (bb::bb_finish<<<(unsigned)nfin, bb::NT, sizeof(bb::Smem), stream>>>(p)));

@@ -107,10 +107,11 @@ def test_underflow_heavy_random():
 
 
 SPECIALS = torch.tensor([0.0, -0.0, INF, -INF, 1e-45, -1e-45, 1.1754942e-38, 3.4028235e38,
-                         -3.4028235e38, 1.0, -1.0, 0.5])
+                         -3.4028235e38, 1.0, -1.0, 0.5, float("nan"), -float("nan")])
 
 
 def test_special_values():
+    """±0, ±inf, subnormals, extremes and NaN (outside the domain; R12 rule)."""
     g = torch.Generator().manual_seed(9)
     n = 200_000
     t = scenegen.walk_tags(n, 9, p_leaf=0.4)
