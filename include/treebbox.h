@@ -74,10 +74,10 @@ const char *tb_version(void);
  * d_match  : device int32[n] out.  Classical partner: matched opens and
  *            closes point at each other; leaves, opens never closed (R4) and
  *            closes with nothing to close (R3) get -1.
- * Computation: one pass over the tags — a decoupled-look-back scan of the
- * bicyclic monoid with stack-monoid slices per tile (P:229-233,
- * §7.1), in-tile resolution, and cross-tile lookup by the suffix relation
- * (P:131-138).  HBM traffic ~9 bytes/element (+ tile slices).
+ * Computation: a reduce pass over the tags (decoupled-look-back scan of the
+ * bicyclic monoid, publishing each tile's stack slice,
+ * P:229-233) and a finish pass (in-tile resolution, cross-tile lookup by the
+ * suffix relation).  HBM traffic ~10 bytes/element (+ slices).
  * ------------------------------------------------------------------------ */
 int paren_match(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *d_parent,
                 void *stream);
@@ -102,8 +102,9 @@ int paren_match_ws(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *
  *     blend open    the same union, scattered to the open
  *     unmatched     close -> EMPTY; an open never closed spans to the end (R3, R4)
  * INF = (-inf,-inf,+inf,+inf), EMPTY = (+inf,+inf,-inf,-inf) (R11).  min/max
- * follow IEEE 754 totalOrder (-0 < +0), so results are unique bit patterns
- * (R12).  Boxes are never canonicalised (R9).
+ * order -0 below +0 and ignore NaN operands (R12; the measured semantics of
+ * PTX min/max.f32), so results are unique bit patterns.  Boxes are never
+ * canonicalised (R9).
  * Matching is recomputed internally (no match/parent arguments).
  * ------------------------------------------------------------------------ */
 int tree_bbox(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, float *d_node_bbox,
@@ -123,6 +124,28 @@ int paren_match_host(const uint8_t *h_tags, int64_t n, int32_t *h_match, int32_t
                      void *stream);
 int tree_bbox_host(const uint8_t *h_tags, const float *h_leaf_bbox, int64_t n, float *h_node_bbox,
                    void *stream);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU sharding: one process per GPU, the global stream
+ * split into contiguous chunks in rank order.  Each rank passes its chunk:
+ * d_tags / d_match / d_parent hold n_local elements whose global indices are
+ * [offset, offset + n_local); outputs hold GLOBAL indices and are identical
+ * to the single-GPU call on the whole stream.  The chunks are summarised by
+ * their Bic value and unmatched-open list (§3-§4), exchanged with
+ * NCCL all-gathers on `comm`, and each rank finishes locally; a close whose
+ * open lies in an earlier chunk is reported to that chunk in a second small
+ * all-gather.  `comm` is an ncclComm_t (from tb_comm_init).  Collective: all
+ * ranks must call with their chunks.  The call synchronises `stream` (the
+ * exchange sizes are read on the host).
+ * ------------------------------------------------------------------------ */
+#define TB_UNIQUE_ID_BYTES 128
+/* Rank 0 creates an id; broadcast its 128 bytes to the other ranks. */
+int tb_get_unique_id(uint8_t *out);
+/* Create / destroy the library's NCCL communicator (*comm = ncclComm_t). */
+int tb_comm_init(const uint8_t *id, int nranks, int rank, void **comm);
+int tb_comm_destroy(void *comm);
+int paren_match_shard(const uint8_t *d_tags, int64_t n_local, int64_t offset, int32_t *d_match,
+                      int32_t *d_parent, void *comm, void *stream);
 
 /* ------------------------------------------------------------------------
  * Validation helper: the global Bic of the stream: a = closes with

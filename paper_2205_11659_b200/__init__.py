@@ -20,7 +20,7 @@ import torch
 from . import build as _build
 
 __all__ = ["paren_match", "tree_bbox", "paren_match_host", "tree_bbox_host", "count_unmatched",
-           "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes"]
+           "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard"]
 
 LIB_PATH = _build.LIB
 _lock = threading.Lock()
@@ -52,6 +52,14 @@ def load():
                 "tree_bbox_workspace_bytes": ([I64], SZ),
                 "tree_bbox_host": ([P, P, I64, P, P], ctypes.c_int),
                 "tb_count_unmatched": ([P, I64, P, P, P], ctypes.c_int),
+                "tb_get_unique_id": ([P], ctypes.c_int),
+                "tb_comm_init": ([P, ctypes.c_int, ctypes.c_int, P], ctypes.c_int),
+                "tb_comm_destroy": ([P], ctypes.c_int),
+                "paren_match_shard": ([P, I64, I64, P, P, P, P], ctypes.c_int),
+                "tb_debug_paren_match_vshard": ([P, I64, ctypes.c_int, P, P, P], ctypes.c_int),
+                "tb_launch_count": ([], ctypes.c_longlong),
+                "tb_profile_enable": ([ctypes.c_int], ctypes.c_int),
+                "tb_profile_read": ([ctypes.c_char_p, SZ], ctypes.c_int),
             }
             for name, (args, res) in sigs.items():
                 fn = getattr(lib, name, None)
@@ -158,3 +166,69 @@ def count_unmatched(tags: torch.Tensor):
         _check(lib.tb_count_unmatched(tags.data_ptr(), tags.numel(), ctypes.byref(a), ctypes.byref(b),
                                       _stream(tags.device)))
     return a.value, b.value
+
+
+def paren_match_vshard(tags: torch.Tensor, nshards: int):
+    """Test hook: the multi-GPU shard protocol run with `nshards` virtual shards
+    of one device buffer on one GPU (device copies stand in for NCCL)."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    n = tags.numel()
+    match = torch.empty(n, dtype=torch.int32, device=tags.device)
+    parent = torch.empty(n, dtype=torch.int32, device=tags.device)
+    with torch.cuda.device(tags.device):
+        _check(lib.tb_debug_paren_match_vshard(tags.data_ptr(), n, nshards, match.data_ptr(), parent.data_ptr(),
+                                               _stream(tags.device)))
+    return match, parent
+
+
+class ShardContext:
+    """One rank of a sharded run (one process per GPU, contiguous chunks in
+    rank order).  Bootstraps the library's own NCCL communicator through the
+    caller's torch.distributed process group (the 128-byte NCCL id is
+    broadcast from rank 0), then exposes the sharded calls for this rank's
+    chunk [offset, offset + n_local) of the global stream."""
+
+    def __init__(self, world: int, rank: int, offset: int, n_local: int, device=None):
+        import torch.distributed as dist
+        lib = load()
+        self.world, self.rank, self.offset, self.n = world, rank, offset, n_local
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        buf = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib.tb_get_unique_id(buf))
+        backend = dist.get_backend()
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8,
+                         device=self.device if backend == "nccl" else "cpu")
+        dist.broadcast(t, 0)
+        ident = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        comm = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib.tb_comm_init(ident, world, rank, ctypes.byref(comm)))
+        self.comm = comm
+
+    def paren_match(self, tags: torch.Tensor, match: torch.Tensor, parent: torch.Tensor):
+        lib = load()
+        _need_cuda(tags, "tags", torch.uint8)
+        with torch.cuda.device(tags.device):
+            _check(lib.paren_match_shard(tags.data_ptr(), tags.numel(), self.offset, match.data_ptr(),
+                                         parent.data_ptr(), self.comm, _stream(tags.device)))
+        return match, parent
+
+    def tree_bbox(self, tags: torch.Tensor, leaf_bbox: torch.Tensor, node_bbox: torch.Tensor):
+        lib = load()
+        fn = getattr(lib, "tree_bbox_shard", None)
+        if fn is None:
+            raise TreeBBoxError("tree_bbox_shard is not available in this build")
+        fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                       ctypes.c_void_p, ctypes.c_void_p]
+        fn.restype = ctypes.c_int
+        with torch.cuda.device(tags.device):
+            _check(fn(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), self.offset, node_bbox.data_ptr(),
+                      self.comm, _stream(tags.device)))
+        return node_bbox
+
+    def close(self):
+        if self.comm:
+            load().tb_comm_destroy(self.comm)
+            self.comm = None

@@ -8,6 +8,13 @@
 
 #include "kernels.h"
 #include "treebbox.h"
+#ifdef TB_WITH_NCCL
+#include <nccl.h>
+namespace tb {
+cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* match, int32_t* parent,
+                          ncclComm_t comm, cudaStream_t s, int* nccl_err);
+}
+#endif
 
 namespace {
 
@@ -217,6 +224,81 @@ int tb_debug_tree_bbox_trace(const uint8_t* d_tags, const float* d_leaf_bbox, in
   if (r) return r;
   cudaError_t e = tb::bb_launch(d_tags, d_leaf_bbox, n, d_node_bbox, ws, (cudaStream_t)stream, d_trace);
   if (e != cudaSuccess) return cuda_fail(e, "tree_bbox launch");
+  return TB_OK;
+}
+
+/* ---- sharding ------------------------------------------------------------ */
+
+int tb_get_unique_id(uint8_t* out) {
+  g_err[0] = 0;
+  if (!out) return fail(TB_ERR_ARG, "null pointer");
+#ifdef TB_WITH_NCCL
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(TB_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(id) == TB_UNIQUE_ID_BYTES, "NCCL unique id size");
+  memcpy(out, &id, sizeof(id));
+  return TB_OK;
+#else
+  return fail(TB_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+int tb_comm_init(const uint8_t* id, int nranks, int rank, void** comm) {
+  g_err[0] = 0;
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(TB_ERR_ARG, "bad communicator arguments");
+#ifdef TB_WITH_NCCL
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c = nullptr;
+  ncclResult_t r = ncclCommInitRank(&c, nranks, uid, rank);
+  if (r != ncclSuccess) return fail(TB_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  *comm = c;
+  return TB_OK;
+#else
+  return fail(TB_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+int tb_comm_destroy(void* comm) {
+  g_err[0] = 0;
+#ifdef TB_WITH_NCCL
+  if (comm) ncclCommDestroy((ncclComm_t)comm);
+  return TB_OK;
+#else
+  return fail(TB_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+int paren_match_shard(const uint8_t* d_tags, int64_t n_local, int64_t offset, int32_t* d_match, int32_t* d_parent,
+                      void* comm, void* stream) {
+  g_err[0] = 0;
+  int r = pm_checks(d_tags, n_local, d_match, d_parent);
+  if (r) return r;
+  if (offset < 0 || offset + n_local > kMaxN) return fail(TB_ERR_ARG, "offset + n_local out of range");
+  if (!comm) return fail(TB_ERR_ARG, "null communicator");
+#ifdef TB_WITH_NCCL
+  int nerr = 0;
+  cudaError_t e = tb::pm_nccl_shard(d_tags, n_local, offset, d_match, d_parent, (ncclComm_t)comm,
+                                    (cudaStream_t)stream, &nerr);
+  if (nerr) return fail(TB_ERR_NCCL, "NCCL error %d", nerr);
+  if (e != cudaSuccess) return cuda_fail(e, "paren_match_shard");
+  return TB_OK;
+#else
+  return fail(TB_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+/* Debug / test (not in the public header): the shard protocol with G virtual
+ * shards of one device buffer on one GPU; must equal paren_match. */
+int tb_debug_paren_match_vshard(const uint8_t* d_tags, int64_t n, int nshards, int32_t* d_match, int32_t* d_parent,
+                                void* stream) {
+  g_err[0] = 0;
+  int r = pm_checks(d_tags, n, d_match, d_parent);
+  if (r || n == 0) return r;
+  if (nshards < 1 || nshards > n) return fail(TB_ERR_ARG, "bad shard count");
+  cudaError_t e = tb::pm_vshard(d_tags, n, nshards, d_match, d_parent, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "paren_match vshard");
   return TB_OK;
 }
 

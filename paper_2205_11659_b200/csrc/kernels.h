@@ -13,6 +13,8 @@ struct ShardInit {
   int h;
   const int32_t* stack;
   int lo;
+  int64_t offset;  // global index of the chunk's first element
+  int2* pairs;     // paren_match: (open, close) for closes that pop stack entries
 };
 
 // Launch accounting / optional event timing around each kernel (prof.cu).
@@ -30,10 +32,18 @@ size_t pm_workspace_bytes(int64_t n);
 size_t pm_ctrl_bytes(int64_t n);
 cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
                       const ShardInit* init, cudaStream_t stream);
+cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
+                             cudaStream_t stream);
+cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
+                             const ShardInit* init, cudaStream_t stream);
+cudaError_t pm_summary_launch(const uint8_t* tags, int64_t n, void* ws, int32_t* hdr, int32_t* opens,
+                              cudaStream_t stream);
 
 size_t bb_workspace_bytes(int64_t n);
 cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
                       cudaStream_t stream, uint64_t* trace = nullptr);
+
+cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int32_t* parent, cudaStream_t s);
 
 size_t bic_count_workspace_bytes(int64_t n);
 cudaError_t bic_count_launch(const uint8_t* tags, int64_t n, void* ws, int64_t* d_out2,

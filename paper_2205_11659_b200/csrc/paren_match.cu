@@ -21,7 +21,6 @@
 //   written into the earlier tile's match[] slot (overwriting pass 1's -1).
 // No inter-CTA waiting in pass 2: pass 1's results are complete at launch.
 #include <climits>
-#include <cstdlib>
 #include "kernels.h"
 #include "stackscan.cuh"
 #include "tile_common.cuh"
@@ -44,9 +43,10 @@ struct Params {
   int32_t* slice;  // [ntiles * TILE]
   Ctrl ctrl;
   Bic init;                   // prefix before the first element (shard mode)
-  const int32_t* init_stack;  // entries at heights [init_lo, init.b)
+  const int32_t* init_stack;  // entries at heights [init_lo, init.b) (global indices)
   int init_lo;
-  int dbg;                    // debug: bit0 skip look-back, bit1 skip hierarchy, bit2 skip slice
+  int64_t offset;             // global index of element 0 (shard mode)
+  int2* pairs;                // shard mode: (open, close) for closes that pop init_stack entries
 };
 
 // ----------------------------------------------------------------------------
@@ -77,21 +77,20 @@ __global__ void __launch_bounds__(NT) pm_reduce(Params p) {
     const int l_t = ex.b - ex.a - a_t;
     const int s_t = max(b_t - sx.a, 0);
     uint32_t m = w.S;
-    for (int k = 0; k < ((p.dbg & 4) ? 0 : s_t); k++) {
+    for (int k = 0; k < s_t; k++) {
       const int bit = __ffs(m) - 1;
       m &= m - 1;
-      const int gi = (int)(tbase + bit);
-      p.slice[base + (l_t + k + tot.a)] = gi;
-      p.match[gi] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
+      p.slice[base + (l_t + k + tot.a)] = (int)(p.offset + tbase + bit);
+      p.match[tbase + bit] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
     }
   }
   if (warp == 0) {
-    const Bic excl = (T == 0 || (p.dbg & 1)) ? p.init : lookback_warp(p.ctrl, T);
+    const Bic excl = (T == 0) ? p.init : lookback_warp(p.ctrl, T);
     if (lane == 0) {
       p.ctrl.hstart[T] = excl.b;
       publish_inclusive(p.ctrl, T, bic_combine(excl, tot), max(excl.b - tot.a, 0), T > 0);
     }
-    if (!(p.dbg & 2)) hierarchy_arrive(p.ctrl, T);
+    hierarchy_arrive(p.ctrl, T);
   }
 }
 
@@ -188,7 +187,8 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
       const int32_t* src = U >= 0 ? p.slice + (int64_t)U * TILE : p.init_stack;
       for (int i = tid; i < cnt; i += NT) {
         const int h = hhi - i;
-        s.inc[H - 1 - h] = __ldg(src + (h - LU));
+        const int v = __ldg(src + (h - LU));
+        s.inc[H - 1 - h] = U >= 0 ? v : -(v + 2);  // init-stack entries are tagged (<= -2)
       }
     }
     const int more = s.more;
@@ -198,11 +198,12 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
     __syncthreads();
   }
 
-  // entries of the stack at this thread's start that it pops (depths 0..a_t)
+  // entries of the stack at this thread's start that it pops (depths 0..a_t),
+  // kept as references: >= 0 in-tile element, < 0 incoming depth -ref-1
   {
     int ref = top_ref;
     for (int d = 0; d <= a_t; d++) {
-      s.extv[d][tid] = ref >= 0 ? (int)(base + ref) : s.inc[-ref - 1];
+      s.extv[d][tid] = ref;
       if (ref >= 0) {
         const int V = ref >> 4;
         const uint32_t below = s.uo[V] & ((1u << (ref & 15)) - 1u);
@@ -215,9 +216,23 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
 
   // parent / match
   const uint32_t mo = w.om & ~w.S;
-  const int tb32 = (int)tbase;
+  const int tb32 = (int)(p.offset + tbase);  // global indices fit in int32 (N <= 2^31 - 1)
+  const int gbase = (int)(p.offset + base);
+  // value of a reference: global index, -1 for the root, or an init-stack entry
+  auto resolve = [&](int ref, bool& from_init) -> int {
+    from_init = false;
+    if (ref >= 0) return gbase + ref;
+    const int e = s.inc[-ref - 1];
+    if (e <= -2) {
+      from_init = true;
+      return -e - 2;
+    }
+    return e;
+  };
   int dcur = 0;
-  int val = s.extv[0][tid];
+  int ref = s.extv[0][tid];
+  bool vinit;
+  int val = resolve(ref, vinit);
 #pragma unroll
   for (int q = 0; q < K / 4; q++) {
     int pv[4], mv[4];
@@ -230,9 +245,20 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
       int m = (w.om & bit) ? ((mo & bit) ? tb32 + nib(w.mlo, w.mhi, i) : SKIP) : -1;
       const bool uc = (w.ucm & bit) != 0u;
       m = (w.cm & bit) ? (uc ? val : local_par) : m;
-      if (uc && val >= 0) p.match[val] = tb32 + i;  // partner opened in an earlier thread / tile
+      if (uc && val >= 0) {
+        if (!vinit) {
+          p.match[val - p.offset] = tb32 + i;  // partner opened in an earlier thread / tile
+        } else {
+          // partner lives in an earlier shard: record (open, close) for the exchange
+          const int k = p.init.b - H + (-ref - 1);
+          p.pairs[k] = make_int2(val, tb32 + i);
+        }
+      }
       dcur += uc;
-      if (uc) val = s.extv[dcur][tid];
+      if (uc) {
+        ref = s.extv[dcur][tid];
+        val = resolve(ref, vinit);
+      }
       mv[j] = m;
     }
     if (full) {
@@ -257,6 +283,32 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
   }
 }
 
+// Chunk summary for sharding: the chunk's final stack (its unmatched opens,
+// bottom to top, global indices) = heights [0, b) of the stack after the last
+// tile, found by the owner rule from a virtual tile `ntiles`.
+__global__ void __launch_bounds__(NT) pm_summary(Params p, int ntiles, int32_t* hdr, int32_t* opens) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const Bic tot = desc_val(__ldcg(p.ctrl.desc + ntiles - 1));  // inclusive prefix of the last tile
+  if (tid == 0) {
+    hdr[0] = tot.a;
+    hdr[1] = tot.b;
+  }
+  int cur = tot.b - 1, from = ntiles;
+  while (cur >= 0) {
+    if (warp == 0) cur = find_runs(s, p.ctrl, cur, from, 0, 0);
+    __syncthreads();
+    const int nr = s.nruns;
+    for (int r = 0; r < nr; r++) {
+      const int U = s.runU[r], LU = s.runL[r], hlo = s.runLo[r], hhi = s.runHi[r];
+      for (int h = hlo + tid; h <= hhi; h += NT) opens[h] = __ldcg(p.slice + (int64_t)U * TILE + (h - LU));
+    }
+    cur = s.more;
+    __syncthreads();
+  }
+}
+
 }  // namespace pm
 
 size_t pm_workspace_bytes(int64_t n) {
@@ -270,13 +322,10 @@ size_t pm_ctrl_bytes(int64_t n) {
   return CtrlLayout(ntiles).bytes;
 }
 
-cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
-                      const ShardInit* init, cudaStream_t stream) {
-  if (n <= 0) return cudaSuccess;
+static pm::Params pm_params(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
+                            const ShardInit* init) {
   const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
   CtrlLayout L(ntiles);
-  cudaError_t err = cudaMemsetAsync(ws, 0, L.bytes, stream);
-  if (err != cudaSuccess) return err;
   pm::Params p;
   p.tags = tags;
   p.n = n;
@@ -287,20 +336,63 @@ cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* p
   p.init = init ? Bic{init->a, init->h} : Bic{0, 0};
   p.init_stack = init ? init->stack : nullptr;
   p.init_lo = init ? init->lo : 0;
-  {
-    const char* e = getenv("TB_DEBUG_PM");
-    p.dbg = e ? atoi(e) : 0;
-  }
+  p.offset = init ? init->offset : 0;
+  p.pairs = init ? init->pairs : nullptr;
+  return p;
+}
+
+static cudaError_t pm_configure() {
   static bool configured = false;
-  const int smem = (int)sizeof(pm::Smem);
   if (!configured) {
-    err = cudaFuncSetAttribute(pm::pm_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t err = cudaFuncSetAttribute(pm::pm_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)sizeof(pm::Smem));
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(pm::pm_summary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(pm::Smem));
     if (err != cudaSuccess) return err;
     configured = true;
   }
+  return cudaSuccess;
+}
+
+cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
+                             cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
+  cudaError_t err = cudaMemsetAsync(ws, 0, CtrlLayout(ntiles).bytes, stream);
+  if (err != cudaSuccess) return err;
+  pm::Params p = pm_params(tags, n, match, nullptr, ws, init);
   TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)ntiles, pm::NT, 0, stream>>>(p)));
-  TB_LAUNCH(stream, "pm_finish", (pm::pm_finish<<<(unsigned)ntiles, pm::NT, smem, stream>>>(p)));
   return cudaGetLastError();
+}
+
+cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
+                             const ShardInit* init, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t err = pm_configure();
+  if (err != cudaSuccess) return err;
+  const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
+  pm::Params p = pm_params(tags, n, match, parent, ws, init);
+  TB_LAUNCH(stream, "pm_finish", (pm::pm_finish<<<(unsigned)ntiles, pm::NT, sizeof(pm::Smem), stream>>>(p)));
+  return cudaGetLastError();
+}
+
+cudaError_t pm_summary_launch(const uint8_t* tags, int64_t n, void* ws, int32_t* hdr, int32_t* opens,
+                              cudaStream_t stream) {
+  cudaError_t err = pm_configure();
+  if (err != cudaSuccess) return err;
+  const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
+  if (ntiles == 0) return cudaMemsetAsync(hdr, 0, 8, stream);
+  pm::Params p = pm_params(tags, n, nullptr, nullptr, ws, nullptr);
+  TB_LAUNCH(stream, "pm_summary",
+            (pm::pm_summary<<<1, pm::NT, sizeof(pm::Smem), stream>>>(p, (int)ntiles, hdr, opens)));
+  return cudaGetLastError();
+}
+
+cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
+                      const ShardInit* init, cudaStream_t stream) {
+  cudaError_t err = pm_reduce_launch(tags, n, match, ws, init, stream);
+  if (err == cudaSuccess) err = pm_finish_launch(tags, n, match, parent, ws, init, stream);
+  return err;
 }
 
 }  // namespace tb

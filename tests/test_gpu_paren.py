@@ -174,3 +174,26 @@ def test_errors():
     assert rc == -1
     rc = lib.paren_match(0, 10, m.data_ptr(), m.data_ptr(), 0)
     assert rc == -1
+
+
+@pytest.mark.parametrize("nshards", [1, 2, 3, 5, 8])
+def test_virtual_shards_equal_oracle(nshards):
+    """The multi-GPU protocol (chunk summaries, composed incoming stacks,
+    (open, close) pairs across chunks) run with virtual shards on one GPU."""
+    tb = gpu()
+    cases = [scenegen.walk_tags(1_000_003, 7, p_leaf=0.5),
+             scenegen.walk_tags(200_000, 8, p_leaf=0.0),
+             scenegen.deep_chain_tags(300_000, 3),
+             torch.full((50_000,), 3, dtype=torch.uint8),
+             torch.full((50_000,), 1, dtype=torch.uint8),
+             torch.cat([torch.full((30_000,), 1, dtype=torch.uint8), torch.full((45_000,), 3, dtype=torch.uint8),
+                        torch.full((20_000,), 2, dtype=torch.uint8)])]
+    g = torch.Generator().manual_seed(nshards)
+    cases.append(torch.multinomial(torch.tensor([0.2, 0.2, 0.1, 0.5]), 400_000, replacement=True,
+                                   generator=g).to(torch.uint8))
+    for t in cases:
+        m_ref, p_ref = oracle.paren_match(t.numpy())
+        m, p = tb.paren_match_vshard(t.cuda(), nshards)
+        torch.cuda.synchronize()
+        assert np.array_equal(p.cpu().numpy(), p_ref)
+        assert np.array_equal(m.cpu().numpy(), m_ref)
