@@ -20,7 +20,8 @@ import torch
 from . import build as _build
 
 __all__ = ["paren_match", "tree_bbox", "paren_match_host", "tree_bbox_host", "count_unmatched",
-           "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard"]
+           "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
+           "tree_bbox_vshard"]
 
 LIB_PATH = _build.LIB
 _lock = threading.Lock()
@@ -57,6 +58,8 @@ def load():
                 "tb_comm_destroy": ([P], ctypes.c_int),
                 "paren_match_shard": ([P, I64, I64, P, P, P, P], ctypes.c_int),
                 "tb_debug_paren_match_vshard": ([P, I64, ctypes.c_int, P, P, P], ctypes.c_int),
+                "tb_debug_tree_bbox_vshard": ([P, P, I64, ctypes.c_int, P, P], ctypes.c_int),
+                "tree_bbox_shard": ([P, P, I64, I64, P, P, P], ctypes.c_int),
                 "tb_launch_count": ([], ctypes.c_longlong),
                 "tb_profile_enable": ([ctypes.c_int], ctypes.c_int),
                 "tb_profile_read": ([ctypes.c_char_p, SZ], ctypes.c_int),
@@ -182,6 +185,18 @@ def paren_match_vshard(tags: torch.Tensor, nshards: int):
     return match, parent
 
 
+def tree_bbox_vshard(tags: torch.Tensor, leaf_bbox: torch.Tensor, nshards: int):
+    """Test hook: the tree_bbox shard protocol with `nshards` virtual shards."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    _need_cuda(leaf_bbox, "leaf_bbox", torch.float32)
+    out = torch.empty_like(leaf_bbox)
+    with torch.cuda.device(tags.device):
+        _check(lib.tb_debug_tree_bbox_vshard(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), nshards,
+                                             out.data_ptr(), _stream(tags.device)))
+    return out
+
+
 class ShardContext:
     """One rank of a sharded run (one process per GPU, contiguous chunks in
     rank order).  Bootstraps the library's own NCCL communicator through the
@@ -217,15 +232,10 @@ class ShardContext:
 
     def tree_bbox(self, tags: torch.Tensor, leaf_bbox: torch.Tensor, node_bbox: torch.Tensor):
         lib = load()
-        fn = getattr(lib, "tree_bbox_shard", None)
-        if fn is None:
-            raise TreeBBoxError("tree_bbox_shard is not available in this build")
-        fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
-                       ctypes.c_void_p, ctypes.c_void_p]
-        fn.restype = ctypes.c_int
+        _need_cuda(tags, "tags", torch.uint8)
         with torch.cuda.device(tags.device):
-            _check(fn(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), self.offset, node_bbox.data_ptr(),
-                      self.comm, _stream(tags.device)))
+            _check(lib.tree_bbox_shard(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), self.offset,
+                                       node_bbox.data_ptr(), self.comm, _stream(tags.device)))
         return node_bbox
 
     def close(self):

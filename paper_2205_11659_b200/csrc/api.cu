@@ -13,6 +13,8 @@
 namespace tb {
 cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* match, int32_t* parent,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err);
+cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, float* out,
+                          ncclComm_t comm, cudaStream_t s, int* nccl_err);
 }
 #endif
 
@@ -287,6 +289,36 @@ int paren_match_shard(const uint8_t* d_tags, int64_t n_local, int64_t offset, in
 #else
   return fail(TB_ERR_NCCL, "built without NCCL");
 #endif
+}
+
+int tree_bbox_shard(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n_local, int64_t offset,
+                    float* d_node_bbox, void* comm, void* stream) {
+  g_err[0] = 0;
+  int r = bb_checks(d_tags, d_leaf_bbox, n_local, d_node_bbox);
+  if (r) return r;
+  if (offset < 0 || offset + n_local > kMaxN) return fail(TB_ERR_ARG, "offset + n_local out of range");
+  if (!comm) return fail(TB_ERR_ARG, "null communicator");
+#ifdef TB_WITH_NCCL
+  int nerr = 0;
+  cudaError_t e = tb::bb_nccl_shard(d_tags, d_leaf_bbox, n_local, offset, d_node_bbox, (ncclComm_t)comm,
+                                    (cudaStream_t)stream, &nerr);
+  if (nerr) return fail(TB_ERR_NCCL, "NCCL error %d", nerr);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_bbox_shard");
+  return TB_OK;
+#else
+  return fail(TB_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+int tb_debug_tree_bbox_vshard(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, int nshards,
+                              float* d_node_bbox, void* stream) {
+  g_err[0] = 0;
+  int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
+  if (r || n == 0) return r;
+  if (nshards < 1 || nshards > n) return fail(TB_ERR_ARG, "bad shard count");
+  cudaError_t e = tb::bb_vshard(d_tags, d_leaf_bbox, n, nshards, d_node_bbox, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_bbox vshard");
+  return TB_OK;
 }
 
 /* Debug / test (not in the public header): the shard protocol with G virtual

@@ -43,6 +43,32 @@ size_t bb_workspace_bytes(int64_t n);
 cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
                       cudaStream_t stream, uint64_t* trace = nullptr);
 
+// tree_bbox shard mode: the stack live before the chunk, with true clips.
+struct BbShard {
+  int64_t offset;  // global index of the chunk's first element
+  int H0;          // stack height at the chunk start
+  int init_lo;     // entries provided for heights [init_lo, H0)
+  const float4* init_clip;
+  const int4* init_meta;  // {global index, kind, source chunk, slice position}
+  void* pops;             // BbPop records of closes popping provided entries
+};
+size_t bb_sumrec_bytes();
+size_t bb_pop_bytes();
+cudaError_t bb_reduce_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, const BbShard* sh,
+                             cudaStream_t stream);
+cudaError_t bb_finish_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
+                             const BbShard* sh, cudaStream_t stream, uint64_t* trace = nullptr);
+cudaError_t bb_summary_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, int32_t* hdr,
+                              void* recs, int4* runs, cudaStream_t stream);
+cudaError_t bb_export_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, const void* recs,
+                             int b, float4* suf_tiles, float4* out_tu, float4* out_su, cudaStream_t stream);
+cudaError_t bb_compose_launch(const void* allrecs, int maxb, const int* L, int g, int lo, int H, float4* init_clip,
+                              int4* init_meta, cudaStream_t stream);
+cudaError_t bb_fixup_launch(int G, int g, int64_t off, int b_g, int min_L_after, int L_g, const float4* tu,
+                            const float4* allsu, int maxb, const void* allpops, int maxp, const int* npops,
+                            const void* myrecs, float4* out, cudaStream_t stream);
+
+cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, float* out, cudaStream_t s);
 cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int32_t* parent, cudaStream_t s);
 
 size_t bic_count_workspace_bytes(int64_t n);

@@ -83,6 +83,13 @@ struct Scratch {
 };
 constexpr size_t SCRATCH_BYTES = 16 * (size_t)(7 * (TILE + 1) + TILE) + 1024;
 
+// A close that pops an entry of an earlier chunk (shard mode).
+struct BbPop {
+  int4 a;     // {close global index, open global index, open kind, source chunk}
+  int4 b;     // {position in the source chunk's slice, 0, 0, 0}
+  float4 pu;  // union of this chunk's clipped leaves before the close
+};
+
 struct Params {
   const uint8_t* tags;
   const float4* boxes;
@@ -94,6 +101,13 @@ struct Params {
   FState f;
   char* scratch;
   uint64_t* trace;  // optional per-tile phase timestamps (debug)
+  // shard mode (zero / null when unsharded): the stack live before the chunk
+  int64_t offset;           // global index of element 0
+  int H0;                   // stack height at the chunk start
+  int init_lo;              // entries provided for heights [init_lo, H0)
+  const float4* init_clip;  // their true clips
+  const int4* init_meta;    // {global index, kind, source chunk, position in its slice}
+  BbPop* pops;              // closes popping a provided entry (finished by the shard fix-up)
 };
 
 __device__ __forceinline__ uint64_t gtime() {
@@ -224,7 +238,7 @@ __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
   Bic ex, sx, tot;
   block_bic_scans<NW>(Bic{a_t, b_t}, wtot, ex, sx, tot, true);
   if (tid == 0) {
-    if (T == 0) st_release_u64(p.ctrl.desc, desc_pack(DESC_INC, tot));
+    if (T == 0) st_release_u64(p.ctrl.desc, desc_pack(DESC_INC, bic_combine(Bic{0, p.H0}, tot)));
     else st_release_u64(p.ctrl.desc + T, desc_pack(DESC_AGG, tot));
     p.f.bcount[T] = tot.b;
   }
@@ -256,7 +270,7 @@ __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
         acc = isect(acc, bx[i]);
         SliceRec r;
         r.lc = (acc);
-        r.idx = (int)(tbase + i);
+        r.idx = (int)(p.offset + tbase + i);
         r.kind = (int)((bm >> i) & 1u);
         r.pad0 = r.pad1 = 0;
         p.slice[(int64_t)T * SREC + (l_t + k + tot.a)] = r;
@@ -265,7 +279,7 @@ __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
     }
   }
   if (warp == 0) {
-    const Bic excl = (T == 0) ? Bic{0, 0} : lookback_warp(p.ctrl, T);
+    const Bic excl = (T == 0) ? Bic{0, p.H0} : lookback_warp(p.ctrl, T);
     if (lane == 0) {
       p.ctrl.hstart[T] = excl.b;
       publish_inclusive(p.ctrl, T, bic_combine(excl, tot), max(excl.b - tot.a, 0), T > 0);
@@ -372,11 +386,11 @@ __device__ float4 chain_tc(const Params& p, int u, int Lu) {
     const unsigned mon = __ballot_sync(0xffffffffu, on);
     const unsigned mres = __ballot_sync(0xffffffffu, on && fl);
     if (mon == 0u) {
-      // no owner among the 32 predecessors: jump through the hierarchy
-      if (u <= 32) return acc;  // nothing older: the root
+      // no owner among the 32 predecessors: jump through the hierarchy; with
+      // no owning tile at all the entry was live before the chunk (shard mode)
       int LW = 0;
-      const int W = owner_search_done(p.ctrl, u - 32, h, LW);
-      if (W < 0) return acc;
+      const int W = u > 32 ? owner_search_done(p.ctrl, u - 32, h, LW) : -1;
+      if (W < 0) return (h < p.H0 && h >= p.init_lo) ? isect(acc, __ldg(p.init_clip + (h - p.init_lo))) : acc;
       acc = isect(acc, (__ldg(&p.slice[(int64_t)W * SREC + (h - LW)].lc)));
       u = W;
       h = LW - 1;
@@ -518,8 +532,9 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
         int LU = 0;
         const int U = owner_search_done(p.ctrl, from, cur, LU);
         const int rlo = max(LU, lo);
-        if (lane == 0) sc.run[nr] = make_int4(U, LU, rlo, cur);
+        if (lane == 0) sc.run[nr] = make_int4(U, U >= 0 ? LU : p.init_lo, U >= 0 ? rlo : lo, cur);
         nr++;
+        if (U < 0) break;  // the rest lies in the stack provided by the shard exchange
         cur = LU - 1;
         from = U;
       }
@@ -532,10 +547,16 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
       const int cnt = rr.w - rr.z + 1;
       for (int i = lane; i < cnt; i += 32) {
         const int h = rr.w - i;
-        const SliceRec rec = p.slice[(int64_t)rr.x * SREC + (h - rr.y)];
         const int d = H - 1 - h;
-        sc.cin[d] = rec.lc;
-        sc.meta[d] = make_int4(rec.idx, rec.kind, r, h - rr.y);
+        if (rr.x >= 0) {
+          const SliceRec rec = p.slice[(int64_t)rr.x * SREC + (h - rr.y)];
+          sc.cin[d] = rec.lc;
+          sc.meta[d] = make_int4(rec.idx, rec.kind, r, h - rr.y);
+        } else {  // live before the chunk: true clip provided by the shard exchange
+          const int q = h - p.init_lo;
+          sc.cin[d] = __ldg(p.init_clip + q);
+          sc.meta[d] = make_int4(__ldg(p.init_meta + q).x, __ldg(p.init_meta + q).y, r, q);
+        }
       }
     }
     __syncthreads();
@@ -543,7 +564,7 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     // TC of each run's tile: deepest by look-back, the others from the run below
     if (warp == 0 && nr > 0) {
       const int4 rb = __ldcg(sc.run + nr - 1);
-      float4 tc = chain_tc(p, rb.x, rb.y);
+      float4 tc = rb.x >= 0 ? chain_tc(p, rb.x, rb.y) : bINF();
       if (lane == 0) sc.runtc[nr - 1] = (tc);
       for (int r = nr - 2; r >= 0; r--) {
         const int4 rbelow = __ldcg(sc.run + r + 1);
@@ -721,10 +742,13 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     for (int d = tid; d < min(aT, H); d += NT) {
       const int4 m = __ldcg(sc.meta + d);
       const int U = __ldcg(sc.run + m.z).x;
-      while (ld_acquire_u32(p.f.suf + U) == 0u) {
+      float4 v = __ldcg(sc.runr + m.z);
+      if (U >= 0) {
+        while (ld_acquire_u32(p.f.suf + U) == 0u) {
+        }
+        v = unite(ld_box_cg(p.f.su + (int64_t)U * TILE + m.w), v);
       }
-      const float4 v = unite(ld_box_cg(p.f.su + (int64_t)U * TILE + m.w), (__ldcg(sc.runr + m.z)));
-      sc.accin[d] = (v);
+      sc.accin[d] = v;
     }
     __syncthreads();
 
@@ -742,7 +766,7 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
             if ((lm >> j) & 1u) PU = unite(PU, bx[j]);
           float4 U;
           bool blend = false;
-          int64_t oidx = -1;
+          int64_t oidx = -1;  // chunk-local index of the open to scatter to
           if (ref >= 0) {
             const int V = ref / K;
             const float4 su = __ldcg(sc.uosu + s.uoff[V] + rank_in(s.uo[V], ref % K));
@@ -756,8 +780,19 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
             } else {
               const int4 m = __ldcg(sc.meta + dd);
               U = unite(unite(__ldcg(sc.accin + dd), range_union_threads(s, 0, tid - 1)), PU);
-              blend = m.y != 0;
-              oidx = m.x;
+              if (__ldcg(sc.run + m.z).x >= 0) {
+                blend = m.y != 0;
+                oidx = m.x - p.offset;
+              } else {
+                // the open lives in an earlier chunk: U so far is this chunk's part
+                const int k = p.H0 - H + dd;
+                const int4 im = __ldg(p.init_meta + m.w);
+                BbPop rec;
+                rec.a = make_int4((int)(p.offset + g), im.x, im.y, im.z);
+                rec.b = make_int4(im.w, 0, 0, 0);
+                rec.pu = U;
+                p.pops[k] = rec;
+              }
             }
           }
           p.out[g] = U;
@@ -823,6 +858,172 @@ __global__ void __launch_bounds__(128) bb_final(Params p) {
 }
 
 // ----------------------------------------------------------------------------
+// shard support: chunk summary, chunk export, composition of
+// the incoming stack, fix-up of nodes that span chunks
+// ----------------------------------------------------------------------------
+// One entry of a chunk's final stack (its unmatched opens, bottom to top).
+struct SumRec {
+  float4 clip;  // chunk-local cumulative clip (true clip if the chunk began at the root)
+  int idx;      // global index
+  int kind;     // 1 = blend
+  int tile;     // owning tile in the chunk
+  int pos;      // position in that tile's slice
+};
+
+// After bb_reduce (chunk-local frame): header (a, b) and the chunk's final
+// stack; the clip of an entry = its tile-local cumulative clip ∩ the clip of
+// the entry just below its run (runs are processed bottom-up).
+__global__ void __launch_bounds__(NT) bb_summary(Params p, int32_t* hdr, SumRec* recs, int4* runs) {
+  __shared__ int s_nr;
+  __shared__ float4 s_tc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Bic tot = desc_val(__ldcg(p.ctrl.desc + p.ntiles - 1));
+  if (tid == 0) {
+    hdr[0] = tot.a;
+    hdr[1] = tot.b;
+  }
+  if (warp == 0) {
+    int cur = tot.b - 1, from = p.ntiles, nr = 0;
+    while (cur >= 0) {
+      int LU = 0;
+      const int U = owner_search_done(p.ctrl, from, cur, LU);
+      if (lane == 0) runs[nr] = make_int4(U, LU, LU, cur);
+      nr++;
+      cur = LU - 1;
+      from = U;
+    }
+    if (lane == 0) s_nr = nr;
+  }
+  __syncthreads();
+  const int nr = s_nr;
+  float4 tc = bINF();
+  for (int r = nr - 1; r >= 0; r--) {
+    const int4 rr = __ldcg(runs + r);
+    for (int h = rr.z + tid; h <= rr.w; h += NT) {
+      const SliceRec rec = p.slice[(int64_t)rr.x * SREC + (h - rr.y)];
+      SumRec o;
+      o.clip = isect(rec.lc, tc);
+      o.idx = rec.idx;
+      o.kind = rec.kind;
+      o.tile = rr.x;
+      o.pos = h - rr.y;
+      recs[h] = o;
+    }
+    __syncthreads();
+    if (tid == 0) s_tc = __ldcg(&recs[rr.w].clip);
+    __syncthreads();
+    tc = s_tc;
+  }
+}
+
+// After bb_finish (chunk-local frame): the chunk's union of clipped leaves and,
+// per final-stack entry, the union of the chunk's leaves after it:
+//   su(entry) = su_tile(entry) ∪ (union of the tiles after its tile).
+__global__ void __launch_bounds__(1024) bb_export(Params p, const SumRec* recs, int b, float4* suf_tiles,
+                                                  float4* out_tu, float4* out_su) {
+  __shared__ float4 wtot[32];
+  __shared__ float4 carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry = bEMPTY();
+  __syncthreads();
+  // suffix unions over tiles: suf_tiles[t] = union of tiles (t, ntiles)
+  for (int hi = p.ntiles - 1; hi >= 0; hi -= 1024) {
+    const int t = hi - tid;
+    float4 v = t >= 0 ? ld_box_cg(p.f.u[0] + t) : bEMPTY();
+    // inclusive scan from high t to low t (tid order)
+    float4 x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float4 o = shfl_up_box(x, off);
+      if (lane >= off) x = unite(x, o);
+    }
+    if (lane == 31) wtot[warp] = x;
+    __syncthreads();
+    float4 pre = carry;
+    for (int w = 0; w < warp; w++) pre = unite(pre, wtot[w]);
+    float4 ex = shfl_up_box(x, 1);
+    if (lane == 0) ex = bEMPTY();
+    if (t >= 0) suf_tiles[t] = unite(pre, ex);
+    __syncthreads();
+    if (tid == 0) {
+      float4 c = carry;
+      for (int w = 0; w < 32; w++) c = unite(c, wtot[w]);
+      carry = c;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *out_tu = carry;
+  __syncthreads();
+  for (int q = tid; q < b; q += 1024) {
+    const SumRec r = recs[q];
+    out_su[q] = unite(ld_box_cg(p.f.su + (int64_t)r.tile * TILE + r.pos), __ldcg(suf_tiles + r.tile));
+  }
+}
+
+// Rank g: true clips TC of every earlier chunk (just below its low-water
+// mark, owner rule over chunks), then the provided stack entries for
+// heights [lo, H): clip = chunk-local clip ∩ TC(owner chunk).
+__global__ void __launch_bounds__(256) bb_compose(const SumRec* allrecs, int maxb, const int* L, int g, int lo,
+                                                  int H, float4* init_clip, int4* init_meta) {
+  __shared__ float4 tc[64];
+  if (threadIdx.x == 0) {
+    for (int h = 0; h < g; h++) {
+      const int X = L[h] - 1;
+      float4 v = bINF();
+      if (X >= 0) {
+        int o = h - 1;
+        while (o > 0 && L[o] > X) o--;
+        v = isect(allrecs[(int64_t)o * maxb + (X - L[o])].clip, tc[o]);
+      }
+      tc[h] = v;
+    }
+  }
+  __syncthreads();
+  for (int X = lo + threadIdx.x; X < H; X += blockDim.x) {
+    int o = g - 1;
+    while (o > 0 && L[o] > X) o--;
+    const int q = X - L[o];
+    const SumRec r = allrecs[(int64_t)o * maxb + q];
+    init_clip[X - lo] = isect(r.clip, tc[o]);
+    init_meta[X - lo] = make_int4(r.idx, r.kind, o, q);
+  }
+}
+
+// Rank g: finish the nodes that span chunks.
+//   own pops:           out[close] = su_h(open) ∪ TU(h+1..g-1) ∪ pu
+//   later chunks' pops of own blend opens: out[open] = the same union
+//   own blend opens open at the end of the stream: su_g ∪ TU(g+1..G-1)
+__global__ void bb_fixup(int G, int g, int64_t off, int b_g, int min_L_after, int L_g, const float4* tu,
+                         const float4* allsu, int maxb, const BbPop* allpops, int maxp, const int* npops,
+                         const SumRec* myrecs, float4* out) {
+  auto turange = [&](int a, int bb) {
+    float4 v = bEMPTY();
+    for (int k = a; k <= bb; k++) v = unite(v, tu[k]);
+    return v;
+  };
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int k = g; k < G; k++) {
+    for (int64_t i = i0; i < npops[k]; i += stride) {
+      const BbPop r = allpops[(int64_t)k * maxp + i];
+      const int h = r.a.w, q = r.b.x;
+      if (k == g) {
+        const float4 U = unite(unite(allsu[(int64_t)h * maxb + q], turange(h + 1, g - 1)), r.pu);
+        out[r.a.x - off] = U;
+      } else if (h == g && r.a.z) {
+        const float4 U = unite(unite(allsu[(int64_t)g * maxb + q], turange(g + 1, k - 1)), r.pu);
+        out[r.a.y - off] = U;
+      }
+    }
+  }
+  for (int64_t q = i0; q < b_g; q += stride) {
+    if ((int64_t)L_g + q < (int64_t)min_L_after && myrecs[q].kind) {
+      out[myrecs[q].idx - off] = unite(allsu[(int64_t)g * maxb + q], turange(g + 1, G - 1));
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
 // workspace
 // ----------------------------------------------------------------------------
 struct Layout {
@@ -882,14 +1083,9 @@ size_t bb_workspace_bytes(int64_t n) {
   return bb::Layout(n, bb::finish_blocks()).bytes;
 }
 
-cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
-                      cudaStream_t stream, uint64_t* trace) {
-  if (n <= 0) return cudaSuccess;
-  const int nb_max = bb::finish_blocks();
-  bb::Layout L(n, nb_max);
-  cudaError_t err = cudaMemsetAsync(ws, 0, L.ctrl_bytes, stream);
-  if (err == cudaSuccess) err = cudaMemsetAsync((char*)ws + L.fzero_off, 0, L.fzero_bytes, stream);
-  if (err != cudaSuccess) return err;
+static bb::Params bb_params(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
+                           const BbShard* sh, uint64_t* trace) {
+  bb::Layout L(n, bb::finish_blocks());
   char* b = (char*)ws;
   bb::Params p;
   p.tags = tags;
@@ -912,10 +1108,86 @@ cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, fl
   p.f.bcount = (int32_t*)(b + L.off_bcount);
   p.scratch = b + L.off_scratch;
   p.trace = trace;
-  const int nfin = (int)std::min<int64_t>(L.ntiles, (int64_t)nb_max);
+  p.offset = sh ? sh->offset : 0;
+  p.H0 = sh ? sh->H0 : 0;
+  p.init_lo = sh ? sh->init_lo : 0;
+  p.init_clip = sh ? (const float4*)sh->init_clip : nullptr;
+  p.init_meta = sh ? (const int4*)sh->init_meta : nullptr;
+  p.pops = sh ? (bb::BbPop*)sh->pops : nullptr;
+  return p;
+}
+
+cudaError_t bb_reduce_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, const BbShard* sh,
+                             cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  bb::Layout L(n, bb::finish_blocks());
+  cudaError_t err = cudaMemsetAsync(ws, 0, L.ctrl_bytes, stream);
+  if (err == cudaSuccess) err = cudaMemsetAsync((char*)ws + L.fzero_off, 0, L.fzero_bytes, stream);
+  if (err != cudaSuccess) return err;
+  bb::Params p = bb_params(tags, leaf_bbox, n, nullptr, ws, sh, nullptr);
   TB_LAUNCH(stream, "bb_reduce", (bb::bb_reduce<<<(unsigned)L.ntiles, bb::NT, 0, stream>>>(p)));
+  return cudaGetLastError();
+}
+
+cudaError_t bb_finish_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
+                             const BbShard* sh, cudaStream_t stream, uint64_t* trace) {
+  if (n <= 0) return cudaSuccess;
+  const int nb_max = bb::finish_blocks();
+  bb::Layout L(n, nb_max);
+  bb::Params p = bb_params(tags, leaf_bbox, n, node_bbox, ws, sh, trace);
+  const int nfin = (int)std::min<int64_t>(L.ntiles, (int64_t)nb_max);
   TB_LAUNCH(stream, "bb_finish", (bb::bb_finish<<<(unsigned)nfin, bb::NT, sizeof(bb::Smem), stream>>>(p)));
-  TB_LAUNCH(stream, "bb_final", (bb::bb_final<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p)));
+  if (!sh)
+    TB_LAUNCH(stream, "bb_final", (bb::bb_final<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p)));
+  return cudaGetLastError();
+}
+
+cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
+                      cudaStream_t stream, uint64_t* trace) {
+  cudaError_t err = bb_reduce_launch(tags, leaf_bbox, n, ws, nullptr, stream);
+  if (err == cudaSuccess) err = bb_finish_launch(tags, leaf_bbox, n, node_bbox, ws, nullptr, stream, trace);
+  return err;
+}
+
+size_t bb_sumrec_bytes() { return sizeof(bb::SumRec); }
+size_t bb_pop_bytes() { return sizeof(bb::BbPop); }
+
+cudaError_t bb_summary_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, int32_t* hdr,
+                              void* recs, int4* runs, cudaStream_t stream) {
+  if (n <= 0) return cudaMemsetAsync(hdr, 0, 8, stream);
+  bb::Params p = bb_params(tags, leaf_bbox, n, nullptr, ws, nullptr, nullptr);
+  TB_LAUNCH(stream, "bb_summary", (bb::bb_summary<<<1, bb::NT, 0, stream>>>(p, hdr, (bb::SumRec*)recs, runs)));
+  return cudaGetLastError();
+}
+
+cudaError_t bb_export_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, const void* recs,
+                             int b, float4* suf_tiles, float4* out_tu, float4* out_su, cudaStream_t stream) {
+  if (n <= 0) {
+    const float inf = __builtin_inff();
+    float4 e = make_float4(inf, inf, -inf, -inf);
+    return cudaMemcpyAsync(out_tu, &e, sizeof(e), cudaMemcpyHostToDevice, stream);
+  }
+  bb::Params p = bb_params(tags, leaf_bbox, n, nullptr, ws, nullptr, nullptr);
+  TB_LAUNCH(stream, "bb_export",
+            (bb::bb_export<<<1, 1024, 0, stream>>>(p, (const bb::SumRec*)recs, b, suf_tiles, out_tu, out_su)));
+  return cudaGetLastError();
+}
+
+cudaError_t bb_compose_launch(const void* allrecs, int maxb, const int* L, int g, int lo, int H, float4* init_clip,
+                              int4* init_meta, cudaStream_t stream) {
+  TB_LAUNCH(stream, "bb_compose",
+            (bb::bb_compose<<<1, 256, 0, stream>>>((const bb::SumRec*)allrecs, maxb, L, g, lo, H, init_clip,
+                                                   init_meta)));
+  return cudaGetLastError();
+}
+
+cudaError_t bb_fixup_launch(int G, int g, int64_t off, int b_g, int min_L_after, int L_g, const float4* tu,
+                            const float4* allsu, int maxb, const void* allpops, int maxp, const int* npops,
+                            const void* myrecs, float4* out, cudaStream_t stream) {
+  TB_LAUNCH(stream, "bb_fixup",
+            (bb::bb_fixup<<<256, 256, 0, stream>>>(G, g, off, b_g, min_L_after, L_g, tu, allsu, maxb,
+                                                   (const bb::BbPop*)allpops, maxp, npops,
+                                                   (const bb::SumRec*)myrecs, out)));
   return cudaGetLastError();
 }
 

@@ -169,3 +169,29 @@ def test_host_api():
     tb.tree_bbox_host(t, b, out)
     ref = oracle.tree_bbox(t.numpy(), b.numpy())
     assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("nshards", [1, 2, 3, 5, 8])
+def test_virtual_shards_equal_oracle(nshards):
+    """tree_bbox shard protocol (clip chain over chunks, exchanged unions and
+    pops, fix-up of nodes spanning chunks) with virtual shards on one GPU."""
+    tb = gpu()
+    g = torch.Generator().manual_seed(nshards)
+    cases = [scenegen.walk_tags(1_000_003, 7, p_leaf=0.5),
+             scenegen.walk_tags(200_000, 8, p_leaf=0.3, p_clip=0.5),
+             scenegen.deep_chain_tags(300_000, 3, leaves_mid=True),
+             torch.full((50_000,), 3, dtype=torch.uint8),
+             torch.full((50_000,), 2, dtype=torch.uint8),
+             torch.multinomial(torch.tensor([0.3, 0.15, 0.1, 0.45]), 400_000, replacement=True,
+                               generator=g).to(torch.uint8)]
+    chain = torch.stack([torch.where(torch.rand(60_000, generator=g) < 0.6, 1, 2).to(torch.uint8),
+                         torch.zeros(60_000, dtype=torch.uint8)], 1).reshape(-1)
+    cases.append(torch.cat([chain, torch.full((50_000,), 3, dtype=torch.uint8)]))
+    for i, t in enumerate(cases):
+        b = scenegen.boxes(t.numel(), 100 + i, t)
+        ref = oracle.tree_bbox(t.numpy(), b.numpy())
+        out = tb.tree_bbox_vshard(t.cuda(), b.cuda(), nshards)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        bad = np.nonzero((got.view(np.uint32) != ref.view(np.uint32)).any(1))[0]
+        assert len(bad) == 0, (i, bad[:10], len(bad), t[bad[:5]].tolist(), got[bad[:3]].tolist(), ref[bad[:3]].tolist())
