@@ -28,6 +28,9 @@ void prof_end(cudaStream_t s, void* token);
     ::tb::prof_end((stream), tb_tok_);           \
   } while (0)
 
+struct Ctrl;
+cudaError_t tile_scan_launch(const Ctrl& c, int64_t ntiles, int init_a, int init_h, cudaStream_t stream);
+
 size_t pm_workspace_bytes(int64_t n);
 size_t pm_ctrl_bytes(int64_t n);
 cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,

@@ -54,11 +54,8 @@ struct Params {
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) pm_reduce(Params p) {
   __shared__ Bic wtot[NW];
-  __shared__ int s_tile;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = (int)atomicAdd(p.ctrl.counter, 1u);  // issue order = tile order
-  __syncthreads();
-  const int T = s_tile;
+  const int tid = threadIdx.x;
+  const int T = blockIdx.x;
   const int64_t base = (int64_t)T * TILE;
   const int64_t tbase = base + (int64_t)tid * K;
   const bool full = base + TILE <= p.n;
@@ -67,30 +64,17 @@ __global__ void __launch_bounds__(NT) pm_reduce(Params p) {
   const int a_t = __popc(w.ucm), b_t = __popc(w.S);
   Bic ex, sx, tot;
   block_bic_scans<NW>(Bic{a_t, b_t}, wtot, ex, sx, tot, true);
-  if (tid == 0) {
-    if (T == 0) st_release_u64(p.ctrl.desc, desc_pack(DESC_INC, bic_combine(p.init, tot)));
-    else st_release_u64(p.ctrl.desc + T, desc_pack(DESC_AGG, tot));
-  }
+  if (tid == 0) p.ctrl.agg[T] = make_int2(tot.a, tot.b);  // the tile scan turns these into heights
   // slice: this thread's unmatched opens that survive to the tile end sit at
   // relative heights l_t + k, slice position l_t + k + a_T.
-  {
-    const int l_t = ex.b - ex.a - a_t;
-    const int s_t = max(b_t - sx.a, 0);
-    uint32_t m = w.S;
-    for (int k = 0; k < s_t; k++) {
-      const int bit = __ffs(m) - 1;
-      m &= m - 1;
-      p.slice[base + (l_t + k + tot.a)] = (int)(p.offset + tbase + bit);
-      p.match[tbase + bit] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
-    }
-  }
-  if (warp == 0) {
-    const Bic excl = (T == 0) ? p.init : lookback_warp(p.ctrl, T);
-    if (lane == 0) {
-      p.ctrl.hstart[T] = excl.b;
-      publish_inclusive(p.ctrl, T, bic_combine(excl, tot), max(excl.b - tot.a, 0), T > 0);
-    }
-    hierarchy_arrive(p.ctrl, T);
+  const int l_t = ex.b - ex.a - a_t;
+  const int s_t = max(b_t - sx.a, 0);
+  uint32_t m = w.S;
+  for (int k = 0; k < s_t; k++) {
+    const int bit = __ffs(m) - 1;
+    m &= m - 1;
+    p.slice[base + (l_t + k + tot.a)] = (int)(p.offset + tbase + bit);
+    p.match[tbase + bit] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
   }
 }
 
@@ -290,7 +274,8 @@ __global__ void __launch_bounds__(NT) pm_summary(Params p, int ntiles, int32_t* 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
-  const Bic tot = desc_val(__ldcg(p.ctrl.desc + ntiles - 1));  // inclusive prefix of the last tile
+  const int2 t2 = __ldcg(p.ctrl.total);  // Bic value of the chunk (tile scan)
+  const Bic tot{t2.x, t2.y};
   if (tid == 0) {
     hdr[0] = tot.a;
     hdr[1] = tot.b;
@@ -358,11 +343,11 @@ cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, voi
                              cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
-  cudaError_t err = cudaMemsetAsync(ws, 0, CtrlLayout(ntiles).bytes, stream);
-  if (err != cudaSuccess) return err;
   pm::Params p = pm_params(tags, n, match, nullptr, ws, init);
   TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)ntiles, pm::NT, 0, stream>>>(p)));
-  return cudaGetLastError();
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return tile_scan_launch(p.ctrl, ntiles, p.init.a, p.init.b, stream);
 }
 
 cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,

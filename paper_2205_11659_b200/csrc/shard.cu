@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "stackscan.cuh"
 #include "treebbox.h"
 #ifdef TB_WITH_NCCL
 #include <nccl.h>
@@ -256,12 +257,12 @@ cudaError_t read_bb_header(BbChunk& c) {
     c.a = c.b = 0;
     return cudaSuccess;
   }
-  // descriptor array follows the tile counter in the control block (stackscan.cuh CtrlLayout)
-  uint64_t d = 0;
-  cudaError_t e = cudaMemcpyAsync(&d, (char*)c.ws + 256 + 8 * (ntiles - 1), 8, cudaMemcpyDeviceToHost, c.s);
+  // Bic value of the chunk, written by the tile scan into the control block
+  int2 t{0, 0};
+  cudaError_t e = cudaMemcpyAsync(&t, (char*)c.ws + CtrlLayout(ntiles).off_total, 8, cudaMemcpyDeviceToHost, c.s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c.s);
-  c.a = (int64_t)((d >> 31) & 0x7fffffffu);
-  c.b = (int64_t)(d & 0x7fffffffu);
+  c.a = t.x;
+  c.b = t.y;
   return e;
 }
 

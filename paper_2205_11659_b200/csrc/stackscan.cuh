@@ -19,13 +19,15 @@ struct Ctrl {
   uint64_t* desc;            // [ntiles] Bic look-back descriptors
   uint32_t* lw;              // [ntiles] low-water mark L_T + 1 (0 = not yet)
   int32_t* hstart;           // [ntiles] stack height at the tile start (written with lw)
+  int2* agg;                 // [ntiles] Bic value (a, b) of each tile (reduce pass)
+  int2* total;               // [1] Bic value of the whole stream (after the tile scan)
   uint32_t* lv[HLEVELS];     // lv[k][g] = 1 + min L over tiles [g*32^k, (g+1)*32^k)
   uint32_t* cnt[HLEVELS];    // arrival counters for lv[k]
 };
 
 // Sizes (in elements) of the control arrays for `ntiles` tiles.
 struct CtrlLayout {
-  size_t off_counter, off_desc, off_lw, off_h, off_lv[HLEVELS], off_cnt[HLEVELS], bytes;
+  size_t off_counter, off_desc, off_lw, off_h, off_agg, off_total, off_lv[HLEVELS], off_cnt[HLEVELS], bytes;
   __host__ __device__ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
   __host__ __device__ explicit CtrlLayout(int64_t ntiles) {
     size_t o = 0;
@@ -33,6 +35,8 @@ struct CtrlLayout {
     off_desc = o; o = align256(o + 8 * (size_t)ntiles);
     off_lw = o; o = align256(o + 4 * (size_t)ntiles);
     off_h = o; o = align256(o + 4 * (size_t)ntiles);
+    off_agg = o; o = align256(o + 8 * (size_t)ntiles);
+    off_total = o; o = align256(o + 8);
     int64_t m = ntiles;
     off_lv[0] = off_cnt[0] = 0;
     for (int k = 1; k < HLEVELS; k++) {
@@ -49,6 +53,8 @@ struct CtrlLayout {
     c.desc = (uint64_t*)(b + off_desc);
     c.lw = (uint32_t*)(b + off_lw);
     c.hstart = (int32_t*)(b + off_h);
+    c.agg = (int2*)(b + off_agg);
+    c.total = (int2*)(b + off_total);
     c.lv[0] = c.lw;
     c.cnt[0] = nullptr;
     for (int k = 1; k < HLEVELS; k++) {

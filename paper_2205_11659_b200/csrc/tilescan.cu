@@ -1,0 +1,87 @@
+// Tile-level scan of the bicyclic monoid (§3) between the reduce and
+// finish passes.  Each tile's reduce pass only publishes its Bic value (no
+// inter-tile waiting); this single-CTA kernel turns them into, per tile, the
+// stack height at its start H_T (exclusive prefix .b), its low-water mark
+// L_T = max(H_T - a_T, 0), and the 32-ary min hierarchy over L used by the
+// owner search (F1).  Two warp-shuffle passes over each warp's contiguous
+// range of tiles with a block-level exclusive scan of the warp totals in
+// between — a reduce-then-scan at tile granularity.
+#include "kernels.h"
+#include "stackscan.cuh"
+
+namespace tb {
+namespace ts {
+
+constexpr int NT = 1024, NW = NT / 32;
+
+__device__ __forceinline__ Bic warp_incl_scan(Bic v, int lane) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Bic o{__shfl_up_sync(0xffffffffu, v.a, off), __shfl_up_sync(0xffffffffu, v.b, off)};
+    if (lane >= off) v = bic_combine(o, v);
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(NT) tile_scan(Ctrl c, int ntiles, Bic init) {
+  __shared__ Bic wt[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int span = ((ntiles + NW - 1) / NW + 31) & ~31;
+  const int t0 = warp * span, t1 = min(t0 + span, ntiles);
+  // pass A: total of this warp's range
+  Bic carry{0, 0};
+  for (int t = t0; t < t1; t += 32) {
+    const int i = t + lane;
+    const int2 g = i < t1 ? __ldcg(c.agg + i) : make_int2(0, 0);
+    const Bic x = warp_incl_scan(Bic{g.x, g.y}, lane);
+    const Bic last{__shfl_sync(0xffffffffu, x.a, 31), __shfl_sync(0xffffffffu, x.b, 31)};
+    carry = bic_combine(carry, last);
+  }
+  if (lane == 0) wt[warp] = carry;
+  __syncthreads();
+  Bic pre = init;
+  for (int w = 0; w < warp; w++) pre = bic_combine(pre, wt[w]);
+  if (warp == NW - 1 && lane == 0) {
+    Bic tot = init;
+    for (int w = 0; w < NW; w++) tot = bic_combine(tot, wt[w]);
+    *c.total = make_int2(tot.a, tot.b);
+  }
+  // pass B: exclusive prefix of every tile -> start height, low-water mark
+  for (int t = t0; t < t1; t += 32) {
+    const int i = t + lane;
+    const int2 g = i < t1 ? __ldcg(c.agg + i) : make_int2(0, 0);
+    const Bic x = warp_incl_scan(Bic{g.x, g.y}, lane);
+    Bic ex{__shfl_up_sync(0xffffffffu, x.a, 1), __shfl_up_sync(0xffffffffu, x.b, 1)};
+    if (lane == 0) ex = Bic{0, 0};
+    const Bic e = bic_combine(pre, ex);
+    if (i < t1) {
+      c.hstart[i] = e.b;
+      c.lw[i] = (uint32_t)max(e.b - g.x, 0) + 1u;
+    }
+    const Bic last{__shfl_sync(0xffffffffu, x.a, 31), __shfl_sync(0xffffffffu, x.b, 31)};
+    pre = bic_combine(pre, last);
+  }
+  // 32-ary min hierarchy over the low-water marks (full groups are complete)
+  int m = ntiles;
+  for (int k = 1; k < HLEVELS; k++) {
+    __syncthreads();
+    const int groups = (m + 31) / 32;
+    for (int g = warp; g < groups; g += NW) {
+      const int i = g * 32 + lane;
+      uint32_t v = i < m ? __ldcg(c.lv[k - 1] + i) : 0xffffffffu;
+      v = __reduce_min_sync(0xffffffffu, v);
+      if (lane == 0) c.lv[k][g] = v;
+    }
+    m = groups;
+  }
+}
+
+}  // namespace ts
+
+cudaError_t tile_scan_launch(const Ctrl& c, int64_t ntiles, int init_a, int init_h, cudaStream_t stream) {
+  if (ntiles <= 0) return cudaSuccess;
+  TB_LAUNCH(stream, "tile_scan", (ts::tile_scan<<<1, ts::NT, 0, stream>>>(c, (int)ntiles, Bic{init_a, init_h})));
+  return cudaGetLastError();
+}
+
+}  // namespace tb

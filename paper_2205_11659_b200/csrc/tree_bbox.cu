@@ -222,11 +222,8 @@ __device__ __forceinline__ float4 block_excl_isect(float4 v, float4* wbox) {
 __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
   __shared__ Bic wtot[NW];
   __shared__ float4 wbox[NW];
-  __shared__ int s_tile;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = (int)atomicAdd(p.ctrl.counter, 1u);
-  __syncthreads();
-  const int T = s_tile;
+  const int tid = threadIdx.x;
+  const int T = blockIdx.x;
   const int64_t base = (int64_t)T * TILE;
   const int64_t tbase = base + (int64_t)tid * K;
   const bool full = base + TILE <= p.n;
@@ -238,8 +235,7 @@ __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
   Bic ex, sx, tot;
   block_bic_scans<NW>(Bic{a_t, b_t}, wtot, ex, sx, tot, true);
   if (tid == 0) {
-    if (T == 0) st_release_u64(p.ctrl.desc, desc_pack(DESC_INC, bic_combine(Bic{0, p.H0}, tot)));
-    else st_release_u64(p.ctrl.desc + T, desc_pack(DESC_AGG, tot));
+    p.ctrl.agg[T] = make_int2(tot.a, tot.b);  // the tile scan turns these into heights
     p.f.bcount[T] = tot.b;
   }
   // surviving unmatched opens of this thread: the s_t lowest bits of S
@@ -277,14 +273,6 @@ __global__ void __launch_bounds__(NT) bb_reduce(Params p) {
         k++;
       }
     }
-  }
-  if (warp == 0) {
-    const Bic excl = (T == 0) ? Bic{0, p.H0} : lookback_warp(p.ctrl, T);
-    if (lane == 0) {
-      p.ctrl.hstart[T] = excl.b;
-      publish_inclusive(p.ctrl, T, bic_combine(excl, tot), max(excl.b - tot.a, 0), T > 0);
-    }
-    hierarchy_arrive(p.ctrl, T);
   }
 }
 
@@ -877,7 +865,8 @@ __global__ void __launch_bounds__(NT) bb_summary(Params p, int32_t* hdr, SumRec*
   __shared__ int s_nr;
   __shared__ float4 s_tc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const Bic tot = desc_val(__ldcg(p.ctrl.desc + p.ntiles - 1));
+  const int2 t2 = __ldcg(p.ctrl.total);  // Bic value of the chunk (tile scan)
+  const Bic tot{t2.x, t2.y};
   if (tid == 0) {
     hdr[0] = tot.a;
     hdr[1] = tot.b;
@@ -1121,12 +1110,13 @@ cudaError_t bb_reduce_launch(const uint8_t* tags, const float* leaf_bbox, int64_
                              cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   bb::Layout L(n, bb::finish_blocks());
-  cudaError_t err = cudaMemsetAsync(ws, 0, L.ctrl_bytes, stream);
-  if (err == cudaSuccess) err = cudaMemsetAsync((char*)ws + L.fzero_off, 0, L.fzero_bytes, stream);
+  cudaError_t err = cudaMemsetAsync((char*)ws + L.fzero_off, 0, L.fzero_bytes, stream);
   if (err != cudaSuccess) return err;
   bb::Params p = bb_params(tags, leaf_bbox, n, nullptr, ws, sh, nullptr);
   TB_LAUNCH(stream, "bb_reduce", (bb::bb_reduce<<<(unsigned)L.ntiles, bb::NT, 0, stream>>>(p)));
-  return cudaGetLastError();
+  err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return tile_scan_launch(p.ctrl, L.ntiles, 0, p.H0, stream);
 }
 
 cudaError_t bb_finish_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
