@@ -105,7 +105,8 @@ int paren_match_ws(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *
  * order -0 below +0 and ignore NaN operands (R12; the measured semantics of
  * PTX min/max.f32), so results are unique bit patterns.  Boxes are never
  * canonicalised (R9).
- * Matching is recomputed internally (no match/parent arguments).
+ * Matching is computed internally (paren_match into the workspace), then
+ * the boxes follow from it as in tree_bbox_matched below.
  * ------------------------------------------------------------------------ */
 int tree_bbox(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, float *d_node_bbox,
               void *stream);
@@ -113,6 +114,26 @@ int tree_bbox(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, float 
 size_t tree_bbox_workspace_bytes(int64_t n);
 int tree_bbox_ws(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, float *d_node_bbox,
                  void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
+ * tree_bbox_matched — the same boxes from a matching already computed
+ *
+ * d_match, d_parent: device int32[n], exactly paren_match's outputs for
+ * d_tags (16-byte aligned; not checked for consistency — other values give
+ * undefined node_bbox but never out-of-bounds accesses only if they are
+ * paren_match's).  tree_bbox(...) is paren_match into its workspace followed
+ * by this call.  With the parent of every element known, an element's clip is
+ * box ∩ clip(parent) and a node's union is the union of the clipped
+ * leaves strictly between its open and its close; both are
+ * evaluated per tile with the cross-tile parts taken from the tiles' slices
+ * (tile-unmatched opens) and a hierarchy of tile unions.
+ * ------------------------------------------------------------------------ */
+int tree_bbox_matched(const uint8_t *d_tags, const float *d_leaf_bbox, const int32_t *d_match,
+                      const int32_t *d_parent, int64_t n, float *d_node_bbox, void *stream);
+size_t tree_bbox_matched_workspace_bytes(int64_t n);
+int tree_bbox_matched_ws(const uint8_t *d_tags, const float *d_leaf_bbox, const int32_t *d_match,
+                         const int32_t *d_parent, int64_t n, float *d_node_bbox, void *d_workspace,
+                         size_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
  * Host-buffer variants (end-to-end API): h_* are host pointers (pinned or

@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["paren_match", "tree_bbox", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["paren_match", "tree_bbox", "tree_bbox_matched", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard"]
 
@@ -52,6 +52,9 @@ def load():
                 "tree_bbox_ws": ([P, P, I64, P, P, SZ, P], ctypes.c_int),
                 "tree_bbox_workspace_bytes": ([I64], SZ),
                 "tree_bbox_host": ([P, P, I64, P, P], ctypes.c_int),
+                "tree_bbox_matched": ([P, P, P, P, I64, P, P], ctypes.c_int),
+                "tree_bbox_matched_ws": ([P, P, P, P, I64, P, P, SZ, P], ctypes.c_int),
+                "tree_bbox_matched_workspace_bytes": ([I64], SZ),
                 "tb_count_unmatched": ([P, I64, P, P, P], ctypes.c_int),
                 "tb_get_unique_id": ([P], ctypes.c_int),
                 "tb_comm_init": ([P, ctypes.c_int, ctypes.c_int, P], ctypes.c_int),
@@ -132,10 +135,31 @@ def tree_bbox(tags: torch.Tensor, leaf_bbox: torch.Tensor, node_bbox: torch.Tens
     return node_bbox
 
 
+def tree_bbox_matched(tags: torch.Tensor, leaf_bbox: torch.Tensor, match: torch.Tensor, parent: torch.Tensor,
+                      node_bbox: torch.Tensor | None = None):
+    """tree_bbox from paren_match's outputs (match, parent) for the same tags."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    _need_cuda(leaf_bbox, "leaf_bbox", torch.float32)
+    _need_cuda(match, "match", torch.int32)
+    _need_cuda(parent, "parent", torch.int32)
+    n = tags.numel()
+    if leaf_bbox.numel() != 4 * n or match.numel() != n or parent.numel() != n:
+        raise ValueError("leaf_bbox must be [n, 4], match and parent [n]")
+    if node_bbox is None:
+        node_bbox = torch.empty((n, 4), dtype=torch.float32, device=tags.device)
+    _need_cuda(node_bbox, "node_bbox", torch.float32)
+    with torch.cuda.device(tags.device):
+        _check(lib.tree_bbox_matched(tags.data_ptr(), leaf_bbox.data_ptr(), match.data_ptr(), parent.data_ptr(), n,
+                                     node_bbox.data_ptr(), _stream(tags.device)))
+    return node_bbox
+
+
 def workspace_bytes(n: int) -> dict:
     lib = load()
     return {"paren_match": int(lib.paren_match_workspace_bytes(n)),
-            "tree_bbox": int(lib.tree_bbox_workspace_bytes(n))}
+            "tree_bbox": int(lib.tree_bbox_workspace_bytes(n)),
+            "tree_bbox_matched": int(lib.tree_bbox_matched_workspace_bytes(n))}
 
 
 def paren_match_host(tags: torch.Tensor, match: torch.Tensor, parent: torch.Tensor,

@@ -163,18 +163,56 @@ int paren_match_host(const uint8_t* h_tags, int64_t n, int32_t* h_match, int32_t
   return TB_OK;
 }
 
-size_t tree_bbox_workspace_bytes(int64_t n) { return n > 0 ? tb::bb_workspace_bytes(n) : 0; }
+// tree_bbox = paren_match into the workspace, then the boxes from the matching
+struct BbWs {
+  size_t pm_off, match_off, parent_off, bbm_off, bytes;
+  explicit BbWs(int64_t n) {
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    size_t o = 0;
+    pm_off = o; o = al(o + tb::pm_workspace_bytes(n));
+    match_off = o; o = al(o + 4 * (size_t)n);
+    parent_off = o; o = al(o + 4 * (size_t)n);
+    bbm_off = o; o = al(o + tb::bbm_workspace_bytes(n));
+    bytes = o;
+  }
+};
 
-int tree_bbox_ws(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox,
-                 void* d_workspace, size_t workspace_bytes, void* stream) {
+static int bbm_checks(const uint8_t* tags, const float* leaf, const int32_t* match, const int32_t* parent, int64_t n,
+               float* out) {
+  int r = bb_checks(tags, leaf, n, out);
+  if (r || n == 0) return r;
+  if (!match || !parent) return fail(TB_ERR_ARG, "null pointer with n > 0");
+  if (!aligned16(match) || !aligned16(parent)) return fail(TB_ERR_ALIGN, "match and parent must be 16-byte aligned");
+  const size_t nb = (size_t)n * 16, n4 = (size_t)n * 4;
+  if (overlap(out, nb, match, n4) || overlap(out, nb, parent, n4))
+    return fail(TB_ERR_ALIAS, "node_bbox overlaps an input");
+  return TB_OK;
+}
+
+size_t tree_bbox_workspace_bytes(int64_t n) { return n > 0 ? BbWs(n).bytes : 0; }
+
+static int tree_bbox_ws_impl(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox,
+                             void* d_workspace, size_t workspace_bytes, void* stream, uint64_t* trace) {
   g_err[0] = 0;
   int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
   if (r || n == 0) return r;
-  if (!d_workspace || workspace_bytes < tb::bb_workspace_bytes(n))
-    return fail(TB_ERR_ARG, "workspace too small: need %zu bytes", tb::bb_workspace_bytes(n));
-  cudaError_t e = tb::bb_launch(d_tags, d_leaf_bbox, n, d_node_bbox, d_workspace, (cudaStream_t)stream);
+  const BbWs L(n);
+  if (!d_workspace || workspace_bytes < L.bytes)
+    return fail(TB_ERR_ARG, "workspace too small: need %zu bytes", L.bytes);
+  char* w = (char*)d_workspace;
+  int32_t* match = (int32_t*)(w + L.match_off);
+  int32_t* parent = (int32_t*)(w + L.parent_off);
+  cudaError_t e = tb::pm_launch(d_tags, n, match, parent, w + L.pm_off, nullptr, (cudaStream_t)stream);
+  if (e == cudaSuccess)
+    e = tb::bbm_launch(d_tags, d_leaf_bbox, match, parent, n, d_node_bbox, w + L.bbm_off, (cudaStream_t)stream,
+                       trace);
   if (e != cudaSuccess) return cuda_fail(e, "tree_bbox launch");
   return TB_OK;
+}
+
+int tree_bbox_ws(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox,
+                 void* d_workspace, size_t workspace_bytes, void* stream) {
+  return tree_bbox_ws_impl(d_tags, d_leaf_bbox, n, d_node_bbox, d_workspace, workspace_bytes, stream, nullptr);
 }
 
 int tree_bbox(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox, void* stream) {
@@ -182,10 +220,38 @@ int tree_bbox(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float*
   int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
   if (r || n == 0) return r;
   void* ws = nullptr;
-  const size_t need = tb::bb_workspace_bytes(n);
+  const size_t need = tree_bbox_workspace_bytes(n);
   r = get_ws(stream, 3, need, &ws);
   if (r) return r;
   return tree_bbox_ws(d_tags, d_leaf_bbox, n, d_node_bbox, ws, need, stream);
+}
+
+size_t tree_bbox_matched_workspace_bytes(int64_t n) { return n > 0 ? tb::bbm_workspace_bytes(n) : 0; }
+
+int tree_bbox_matched_ws(const uint8_t* d_tags, const float* d_leaf_bbox, const int32_t* d_match,
+                         const int32_t* d_parent, int64_t n, float* d_node_bbox, void* d_workspace,
+                         size_t workspace_bytes, void* stream) {
+  g_err[0] = 0;
+  int r = bbm_checks(d_tags, d_leaf_bbox, d_match, d_parent, n, d_node_bbox);
+  if (r || n == 0) return r;
+  if (!d_workspace || workspace_bytes < tb::bbm_workspace_bytes(n))
+    return fail(TB_ERR_ARG, "workspace too small: need %zu bytes", tb::bbm_workspace_bytes(n));
+  cudaError_t e = tb::bbm_launch(d_tags, d_leaf_bbox, d_match, d_parent, n, d_node_bbox, d_workspace,
+                                 (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_bbox_matched launch");
+  return TB_OK;
+}
+
+int tree_bbox_matched(const uint8_t* d_tags, const float* d_leaf_bbox, const int32_t* d_match,
+                      const int32_t* d_parent, int64_t n, float* d_node_bbox, void* stream) {
+  g_err[0] = 0;
+  int r = bbm_checks(d_tags, d_leaf_bbox, d_match, d_parent, n, d_node_bbox);
+  if (r || n == 0) return r;
+  void* ws = nullptr;
+  const size_t need = tb::bbm_workspace_bytes(n);
+  r = get_ws(stream, 5, need, &ws);
+  if (r) return r;
+  return tree_bbox_matched_ws(d_tags, d_leaf_bbox, d_match, d_parent, n, d_node_bbox, ws, need, stream);
 }
 
 int tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, float* h_node_bbox,
@@ -216,17 +282,18 @@ int tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, f
 
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
+int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }
+
 int tb_debug_tree_bbox_trace(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox,
                              uint64_t* d_trace, void* stream) {
   g_err[0] = 0;
   int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
   if (r || n == 0) return r;
   void* ws = nullptr;
-  r = get_ws(stream, 3, tb::bb_workspace_bytes(n), &ws);
+  const size_t need = tree_bbox_workspace_bytes(n);
+  r = get_ws(stream, 3, need, &ws);
   if (r) return r;
-  cudaError_t e = tb::bb_launch(d_tags, d_leaf_bbox, n, d_node_bbox, ws, (cudaStream_t)stream, d_trace);
-  if (e != cudaSuccess) return cuda_fail(e, "tree_bbox launch");
-  return TB_OK;
+  return tree_bbox_ws_impl(d_tags, d_leaf_bbox, n, d_node_bbox, ws, need, stream, d_trace);
 }
 
 /* ---- sharding ------------------------------------------------------------ */

@@ -42,6 +42,13 @@ cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int
 cudaError_t pm_summary_launch(const uint8_t* tags, int64_t n, void* ws, int32_t* hdr, int32_t* opens,
                               cudaStream_t stream);
 
+// tree_bbox from matching (tree_bbox_m.cu): the single-device path
+size_t bbm_workspace_bytes(int64_t n);
+int bbm_tile_elems();
+cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                       int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace = nullptr);
+
+// tree_bbox by stack slices (tree_bbox.cu): the shard path
 size_t bb_workspace_bytes(int64_t n);
 cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
                       cudaStream_t stream, uint64_t* trace = nullptr);
@@ -55,6 +62,7 @@ struct BbShard {
   const int4* init_meta;  // {global index, kind, source chunk, slice position}
   void* pops;             // BbPop records of closes popping provided entries
 };
+int bb_tile_elems();
 size_t bb_sumrec_bytes();
 size_t bb_pop_bytes();
 cudaError_t bb_reduce_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, const BbShard* sh,

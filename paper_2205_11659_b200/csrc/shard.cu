@@ -185,7 +185,7 @@ struct BbChunk {
   }
   cudaError_t alloc_buffers(int G) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const int64_t ntiles = (n + 2047) / 2048 + 1;
+    const int64_t ntiles = (n + bb_tile_elems() - 1) / bb_tile_elems() + 1;
     const size_t bb1 = (size_t)std::max<int64_t>(b, 1), ab1 = (size_t)std::max<int64_t>(a, 1);
     const size_t bytes = al(bb_sumrec_bytes() * bb1) + al(16 * (bb1 + 1)) + al(16 * (size_t)ntiles) + al(16) +
                          al(16 * bb1) + al(16 * (ab1 + 1)) + al(16 * (ab1 + 1)) + al(bb_pop_bytes() * ab1) +
@@ -252,7 +252,7 @@ struct BbChunk {
 cudaError_t read_bb_header(BbChunk& c) {
   const size_t ctrl = 0;
   (void)ctrl;
-  const int64_t ntiles = (c.n + 2047) / 2048;
+  const int64_t ntiles = (c.n + bb_tile_elems() - 1) / bb_tile_elems();
   if (ntiles == 0) {
     c.a = c.b = 0;
     return cudaSuccess;

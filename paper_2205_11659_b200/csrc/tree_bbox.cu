@@ -35,6 +35,7 @@
 //   union of everything after them.
 #include <algorithm>
 #include <climits>
+#include <cooperative_groups.h>
 #include "boxes.cuh"
 #include "kernels.h"
 #include "stackscan.cuh"
@@ -43,11 +44,10 @@
 namespace tb {
 namespace bb {
 
-constexpr int NT = 256;
+constexpr int NT = 128;
 constexpr int K = 8;
 constexpr int TILE = NT * K;
 constexpr int NW = NT / 32;
-constexpr int LOGNT = 8;
 constexpr int SREC = TILE + 1;  // slice records per tile
 
 struct SliceRec {
@@ -346,64 +346,76 @@ __device__ __forceinline__ void publish_union(const FState& f, int T, float4 tu)
   }
 }
 
-// True clip just below tile u's low-water mark Lu, i.e. the clip of the
-// entry at height Lu - 1 of the stack at u's start (INF at the root).  Walks
-// the owner chain (warp-parallel over 32 predecessors at a time), combining
-// the chain tiles' tile-local clips, until a tile that already published its
-// own TC.
-__device__ float4 chain_tc(const Params& p, int u, int Lu) {
+// ----------------------------------------------------------------------------
+// tile clip chain: TC(V) = true clip of the entry just below tile V's
+// low-water mark (height L_V - 1 of the stack at V's start; INF at the root).
+// TC(V) = lc_W(X - L_W) ∩ TC(W) with W the owner of height X = L_V - 1 (F1),
+// a forest over tiles; resolved by pointer jumping (cooperative grid, one
+// grid-wide barrier per doubling round).  Replaces the per-partition
+// "exclusive scan of top boxes" of the paper's second bbox dispatch.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bb_tc(Params p, float4* acc2, int* ptr2, int* flag) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
-  float4 acc = bINF();
-  int h = Lu - 1;
-  while (h >= 0) {
-    if (ld_acquire_u32(p.f.tcf + u)) return isect(acc, ld_box_cg(p.f.tc + u));
-    const int t = u - 1 - lane;
-    const int L = t >= 0 ? (int)(__ldg(p.ctrl.lw + t) - 1u) : INT_MAX;
-    const uint32_t fl = t >= 0 ? ld_acquire_u32(p.f.tcf + t) : 0u;
-    // min L over closer tiles (exclusive prefix-min in lane order)
-    int m = L;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int o = __shfl_up_sync(0xffffffffu, m, off);
-      if (lane >= off) m = min(m, o);
-    }
-    int mex = __shfl_up_sync(0xffffffffu, m, 1);
-    if (lane == 0) mex = INT_MAX;
-    const int thr = min(h, mex == INT_MAX ? INT_MAX : mex - 1);
-    const bool on = t >= 0 && L <= thr;
-    const unsigned mon = __ballot_sync(0xffffffffu, on);
-    const unsigned mres = __ballot_sync(0xffffffffu, on && fl);
-    if (mon == 0u) {
-      // no owner among the 32 predecessors: jump through the hierarchy; with
-      // no owning tile at all the entry was live before the chunk (shard mode)
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+  const int nt = p.ntiles;
+  float4* acc[2] = {acc2, acc2 + nt};
+  int* ptr[2] = {ptr2, ptr2 + nt};
+  // links (one warp per tile: the owner search is warp-cooperative)
+  for (int V = gw; V < nt; V += nwarps) {
+    const int X = (int)(__ldg(p.ctrl.lw + V) - 1u) - 1;
+    float4 a = bINF();
+    int q = -1;
+    if (X >= 0) {
       int LW = 0;
-      const int W = u > 32 ? owner_search_done(p.ctrl, u - 32, h, LW) : -1;
-      if (W < 0) return (h < p.H0 && h >= p.init_lo) ? isect(acc, __ldg(p.init_clip + (h - p.init_lo))) : acc;
-      acc = isect(acc, (__ldg(&p.slice[(int64_t)W * SREC + (h - LW)].lc)));
-      u = W;
-      h = LW - 1;
-      continue;
+      const int W = owner_search_done(p.ctrl, V, X, LW);
+      if (W >= 0) {
+        a = __ldg(&p.slice[(int64_t)W * SREC + (X - LW)].lc);
+        q = W;
+      } else if (X < p.H0 && X >= p.init_lo) {
+        a = __ldg(p.init_clip + (X - p.init_lo));
+      }
     }
-    const int klim = mres ? (__ffs(mres) - 1) : 31;
-    float4 c = bINF();
-    if (on && lane <= klim) c = (__ldg(&p.slice[(int64_t)t * SREC + (thr - L)].lc));
-    acc = isect(acc, warp_isect_all(c));
-    if (mres) {
-      const float4 tcr = shfl_box(t >= 0 ? ld_box_cg(p.f.tc + max(t, 0)) : bINF(), klim);
-      return isect(acc, tcr);
+    if (lane == 0) {
+      acc[0][V] = a;
+      ptr[0][V] = q;
     }
-    const int last = 31 - __clz(mon);
-    const int Llast = __shfl_sync(0xffffffffu, L, last);
-    u = u - 1 - last;
-    h = Llast - 1;
   }
-  return acc;
+  const int gt = (int)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  const int nthr = (int)(gridDim.x * (int64_t)blockDim.x);
+  int cb = 0;
+  for (int round = 0; round < 32; round++) {
+    if (gt == 0) flag[round & 1] = 0;
+    grid.sync();
+    int any = 0;
+    for (int V = gt; V < nt; V += nthr) {
+      float4 a = __ldcg(acc[cb] + V);
+      int q = __ldcg(ptr[cb] + V);
+      if (q >= 0) {
+        a = isect(a, __ldcg(acc[cb] + q));
+        q = __ldcg(ptr[cb] + q);
+        any |= q >= 0;
+      }
+      acc[cb ^ 1][V] = a;
+      ptr[cb ^ 1][V] = q;
+    }
+    any = __syncthreads_or(any);
+    if (any && threadIdx.x == 0) atomicOr(flag + (round & 1), 1);
+    cb ^= 1;
+    grid.sync();
+    if (__ldcg(flag + (round & 1)) == 0) break;
+  }
+  for (int V = gt; V < nt; V += nthr) p.f.tc[V] = __ldcg(acc[cb] + V);
 }
 
 // ----------------------------------------------------------------------------
 // pass 2 (persistent)
 // ----------------------------------------------------------------------------
 struct Smem {
+  float4 box[TILE];  // the tile's boxes (swizzled), replaced in place by its outputs
+  float4 tl[NT];     // true clip of each thread's link entry
   int win[NW][5][32];
   int wmin[NW];
   int l[NT];
@@ -411,26 +423,46 @@ struct Smem {
   uint32_t bmk[NT];
   int uoff[NT];
   int link[NT];
-  float4 pjacc[2][NT];
-  int pjptr[2][NT];
-  int pjesc[2][NT];
-  float4 tl[NT];
-  float4 sp[LOGNT][NT];  // sparse table of per-thread unions of true-clipped leaves
+  uint32_t skip[NT];  // tile-unmatched blend opens: written by a later tile or bb_final
+  union {
+    struct {  // phase D: pointer jumping over threads
+      float4 acc[2][NT];
+      int ptr[2][NT];
+      int esc[2][NT];
+    } pj;
+    struct {  // phases F-H: unions over whole threads
+      float4 win[6][NT];  // union of thread unions over lanes [lane-2^k+1, lane] (clipped to the warp)
+      float4 suf[NT];     // inclusive suffix within the warp
+    } un;
+  } u;
+  float4 wtu[NW];    // per-warp unions
   Bic wtot[NW];
   int wsum[NW];
   int tile, nruns;
 };
 
+// element i of thread t lives at slot 8t + (i ^ (t & 7)): conflict-free both
+// for the coalesced copies (8 consecutive elements = one row) and for the
+// per-thread accesses (8 consecutive threads hit 8 distinct 16-byte columns)
+__device__ __forceinline__ int slot(int t, int i) { return (t << 3) | (i ^ (t & 7)); }
+__device__ __forceinline__ int slot_of(int e) { return slot(e >> 3, e & 7); }
+
 __device__ __forceinline__ int rank_in(uint32_t m, int bit) { return __popc(m & ((1u << bit) - 1u)); }
 
+// Union of the clipped leaves of whole threads [a, b] (a <= b + 1).
 __device__ __forceinline__ float4 range_union_threads(const Smem& s, int a, int b) {
   if (a > b) return bEMPTY();
-  const int len = b - a + 1;
-  const int k = min(31 - __clz(len), LOGNT - 1);  // two windows of 2^k cover len <= 2^LOGNT
-  return unite((s.sp[k][b]), (s.sp[k][a + (1 << k) - 1]));
+  const int wa = a >> 5, wb = b >> 5;
+  if (wa == wb) {
+    const int k = 31 - __clz(b - a + 1);
+    return unite(s.u.un.win[k][b], s.u.un.win[k][a + (1 << k) - 1]);
+  }
+  float4 v = unite(s.u.un.suf[a], s.u.un.win[5][b]);
+  for (int w = wa + 1; w < wb; w++) v = unite(v, s.wtu[w]);
+  return v;
 }
 
-__global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
+__global__ void __launch_bounds__(NT, 6) bb_finish(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -455,23 +487,23 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     const int64_t base = (int64_t)T * TILE;
     const int64_t tbase = base + (int64_t)tid * K;
     const bool full = base + TILE <= p.n;
+    const int nvalid = full ? TILE : (int)(p.n - base);
 
     BB_TRACE(T, 0);
-    // ---- A. load ------------------------------------------------------------
+    // ---- A. load: tags to registers, boxes to shared memory (coalesced) --
     uint32_t om, cm, bm, S, ucm;
     classify8(load_tags8(p.tags, p.n, tbase, full), om, cm, bm);
-    float4 bx[K];
 #pragma unroll
-    for (int i = 0; i < K; i++) {
-      const bool need = ((~cm & ~bm) >> i) & 1u;  // leaves and clip opens carry boxes
-      bx[i] = (need && (full || tbase + i < p.n)) ? (__ldg(p.boxes + tbase + i)) : bINF();
+    for (int j = 0; j < K; j++) {
+      const int e = j * NT + tid;
+      s.box[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bINF();
     }
     walk8(om, cm, S, ucm);
     const int a_t = __popc(ucm), b_t = __popc(S);
 
     // ---- B. scans, thread references ----------------------------------------
     Bic ex, sx, tot;
-    block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, true);
+    block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, true);  // (barrier: boxes staged)
     const int aT = tot.a;
     const int r_t = ex.b - ex.a;
     const int l_t = r_t - a_t;
@@ -489,6 +521,15 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     s.uo[tid] = S;
     s.bmk[tid] = bm;
     s.uoff[tid] = uoff;
+    const int s_t = max(b_t - sx.a, 0);  // this thread's opens that survive the tile
+    {
+      uint32_t surv = 0, m = S;
+      for (int k = 0; k < s_t; k++) {
+        surv |= m & (~m + 1u);
+        m &= m - 1;
+      }
+      s.skip[tid] = surv & bm;
+    }
     // thread-local cumulative clip of each thread-unmatched open
     {
       float4 acc = bINF();
@@ -496,8 +537,8 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
 #pragma unroll
       for (int i = 0; i < K; i++) {
         if ((S >> i) & 1u) {
-          if (!((bm >> i) & 1u)) acc = isect(acc, bx[i]);
-          sc.uoc[uoff + k] = (acc);
+          if (!((bm >> i) & 1u)) acc = isect(acc, s.box[slot(tid, i)]);
+          sc.uoc[uoff + k] = acc;
           k++;
         }
       }
@@ -505,12 +546,13 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     const int H = __ldg(p.ctrl.hstart + T);
     const int lo = max(H - 1 - aT, 0);
     for (int d = H + tid; d <= aT; d += NT) {
-      sc.cin[d] = (bINF());
+      sc.cin[d] = bINF();
       sc.meta[d] = make_int4(-1, 0, -1, 0);
     }
     __syncthreads();
     const int top_ref = thread_ref<NW, K>(wl, l_t, S, r_t - 1, s.win, s.wmin, s.l, s.uo);
     const int link_ref = thread_ref<NW, K>(wl, l_t, S, l_t - 1, s.win, s.wmin, s.l, s.uo);
+    s.link[tid] = link_ref;
 
     BB_TRACE(T, 1);
     // ---- C. incoming stack: runs of predecessors' slices ------------------
@@ -549,28 +591,23 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     }
     __syncthreads();
     BB_TRACE(T, 2);
-    // TC of each run's tile: deepest by look-back, the others from the run below
+    // TC of each run's tile: deepest precomputed (bb_tc), the others from the run below
     if (warp == 0 && nr > 0) {
       const int4 rb = __ldcg(sc.run + nr - 1);
-      float4 tc = rb.x >= 0 ? chain_tc(p, rb.x, rb.y) : bINF();
-      if (lane == 0) sc.runtc[nr - 1] = (tc);
+      float4 tc = rb.x >= 0 ? __ldg(p.f.tc + rb.x) : bINF();
+      if (lane == 0) sc.runtc[nr - 1] = tc;
       for (int r = nr - 2; r >= 0; r--) {
         const int4 rbelow = __ldcg(sc.run + r + 1);
-        tc = isect((__ldcg(sc.cin + (H - 1 - rbelow.w))), tc);
-        if (lane == 0) sc.runtc[r] = (tc);
+        tc = isect(__ldcg(sc.cin + (H - 1 - rbelow.w)), tc);
+        if (lane == 0) sc.runtc[r] = tc;
       }
     }
     __syncthreads();
     for (int d = tid; d < min(aT + 1, H); d += NT) {
       const int run = __ldcg(sc.meta + d).z;
-      sc.cin[d] = (isect((__ldcg(sc.cin + d)), (__ldcg(sc.runtc + run))));
+      sc.cin[d] = isect(__ldcg(sc.cin + d), __ldcg(sc.runtc + run));
     }
     __syncthreads();
-    if (tid == 0) {
-      p.f.tc[T] = __ldcg(sc.cin + aT);  // true clip just below this tile's low-water mark
-      __threadfence();
-      st_release_u32(p.f.tcf + T, 1u);
-    }
 
     BB_TRACE(T, 3);
     // ---- D. thread chains: clip of each thread's link entry ---------------
@@ -580,28 +617,28 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
       if (link_ref >= 0) {
         const int W = link_ref / K;
         ptr = W;
-        acc = (__ldcg(sc.uoc + s.uoff[W] + rank_in(s.uo[W], link_ref % K)));
+        acc = __ldcg(sc.uoc + s.uoff[W] + rank_in(s.uo[W], link_ref % K));
       } else {
         esc = link_ref;
       }
       int cb = 0;
-      s.pjacc[0][tid] = (acc);
-      s.pjptr[0][tid] = ptr;
-      s.pjesc[0][tid] = esc;
-      __syncthreads();
-      for (int round = 0; round < LOGNT; round++) {
+      s.u.pj.acc[0][tid] = acc;
+      s.u.pj.ptr[0][tid] = ptr;
+      s.u.pj.esc[0][tid] = esc;
+      int any = __syncthreads_or(ptr >= 0);
+      while (any) {
         if (ptr >= 0) {
-          acc = isect(acc, (s.pjacc[cb][ptr]));
-          esc = s.pjesc[cb][ptr];
-          ptr = s.pjptr[cb][ptr];
+          acc = isect(acc, s.u.pj.acc[cb][ptr]);
+          esc = s.u.pj.esc[cb][ptr];
+          ptr = s.u.pj.ptr[cb][ptr];
         }
-        s.pjacc[cb ^ 1][tid] = (acc);
-        s.pjptr[cb ^ 1][tid] = ptr;
-        s.pjesc[cb ^ 1][tid] = esc;
+        s.u.pj.acc[cb ^ 1][tid] = acc;
+        s.u.pj.ptr[cb ^ 1][tid] = ptr;
+        s.u.pj.esc[cb ^ 1][tid] = esc;
         cb ^= 1;
-        __syncthreads();
+        any = __syncthreads_or(ptr >= 0);
       }
-      s.tl[tid] = (isect(acc, (__ldcg(sc.cin + (-esc - 1)))));
+      s.tl[tid] = isect(acc, __ldcg(sc.cin + (-esc - 1)));
     }
     __syncthreads();
 
@@ -609,9 +646,9 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     auto entry_clip = [&](int ref) -> float4 {
       if (ref >= 0) {
         const int V = ref / K;
-        return isect((__ldcg(sc.uoc + s.uoff[V] + rank_in(s.uo[V], ref % K))), (s.tl[V]));
+        return isect(__ldcg(sc.uoc + s.uoff[V] + rank_in(s.uo[V], ref % K)), s.tl[V]);
       }
-      return (__ldcg(sc.cin + (-ref - 1)));
+      return __ldcg(sc.cin + (-ref - 1));
     };
     auto next_down = [&](int ref) -> int {
       if (ref >= 0) {
@@ -621,8 +658,6 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
       }
       return ref - 1;
     };
-    s.link[tid] = link_ref;
-    __syncthreads();
 
     BB_TRACE(T, 4);
     // ---- E. per-thread two-box stack walk ----------------------------
@@ -630,14 +665,15 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
     // the top is the effective clip of the deepest clip open on it (a blend
     // passes its parent's clip through), else the clip of the external top.
     // A node closed inside the thread gets the union of the clipped leaves
-    // strictly inside it (predicated loop over the thread's 8 values).
+    // strictly inside it.  Results replace the boxes in shared memory; a
+    // close that pops an external entry records the thread's prefix union.
     uint32_t lm = ~om & ~cm & 0xffu;  // leaves
     if (!full) {
       const int64_t rem = p.n - tbase;
       lm &= rem >= K ? 0xffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
     }
     const uint32_t clipm = om & ~bm;
-    float4 suf = bEMPTY();  // union of all this thread's clipped leaves (filled below)
+    float4 tu_thr = bEMPTY();  // union of this thread's clipped leaves
     {
       int ref = top_ref;
       float4 cext = entry_clip(ref);
@@ -646,12 +682,11 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
 #pragma unroll
       for (int i = 0; i < K; i++) {
         const uint32_t bit = 1u << i;
-        const int64_t g = tbase + i;
+        float4& me = s.box[slot(tid, i)];
         if (om & bit) {
           if (!(bm & bit)) {
-            bx[i] = isect(bx[i], ctop);
-            ctop = bx[i];
-            p.out[g] = bx[i];
+            ctop = isect(me, ctop);
+            me = ctop;
           }
           St |= bit;
         } else if (cm & bit) {
@@ -660,55 +695,60 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
             float4 U = bEMPTY();
 #pragma unroll
             for (int j = 0; j < i; j++)
-              if (((lm >> j) & 1u) && j > o) U = unite(U, bx[j]);
-            p.out[g] = U;
-            if ((bm >> o) & 1u) p.out[tbase + o] = U;
+              if (((lm >> j) & 1u) && j > o) U = unite(U, s.box[slot(tid, j)]);
+            me = U;
+            if ((bm >> o) & 1u) s.box[slot(tid, o)] = U;
             St ^= 1u << o;
             const uint32_t cs = St & clipm;
-            const int jt = cs ? 31 - __clz(cs) : -1;
-            ctop = cext;
-#pragma unroll
-            for (int j = 0; j < i; j++)
-              if (j == jt) ctop = bx[j];
+            ctop = cs ? s.box[slot(tid, 31 - __clz(cs))] : cext;
           } else {
+            me = tu_thr;  // prefix union; completed in H
             ref = next_down(ref);
             cext = entry_clip(ref);
             ctop = cext;
           }
         } else if ((lm >> i) & 1u) {
-          bx[i] = isect(bx[i], ctop);
-          p.out[g] = bx[i];
+          const float4 v = isect(me, ctop);
+          me = v;
+          tu_thr = unite(tu_thr, v);
         }
       }
-      // suffix unions after each thread-unmatched open (St = those opens)
+      // unions after each thread-unmatched open (St = those opens)
+      float4 suf = bEMPTY();
 #pragma unroll
       for (int j = K - 1; j >= 0; j--) {
         if ((St >> j) & 1u) sc.uosu[uoff + __popc(St & ((1u << j) - 1u))] = suf;
-        if ((lm >> j) & 1u) suf = unite(suf, bx[j]);
+        if ((lm >> j) & 1u) suf = unite(suf, s.box[slot(tid, j)]);
       }
-    }
-    s.sp[0][tid] = suf;
-    __syncthreads();
-#pragma unroll 1
-    for (int k = 1; k < LOGNT; k++) {
-      const int h = 1 << (k - 1);
-      float4 v = (s.sp[k - 1][tid]);
-      if (tid >= h) v = unite(v, (s.sp[k - 1][tid - h]));
-      s.sp[k][tid] = (v);
-      __syncthreads();
     }
 
-    BB_TRACE(T, 5);
-    // ---- F. publish the tile union and slice-entry suffix unions ---------
+    // ---- F. unions over whole threads; publish tile union and suffix unions --
     {
-      const int s_t = max(b_t - sx.a, 0);
-      if (s_t > 0) {
-        const float4 after = range_union_threads(s, tid + 1, NT - 1);
-        for (int k = 0; k < s_t; k++) {
-          const float4 v = unite((__ldcg(sc.uosu + uoff + k)), after);
-          p.f.su[(int64_t)T * TILE + (l_t + k + aT)] = (v);
-        }
+      // windows of 2^k lanes ending at each lane (k = 0..5, clipped at lane 0;
+      // level 5 is the inclusive in-warp prefix)
+      float4 w = tu_thr, suf = tu_thr;
+      s.u.un.win[0][tid] = w;
+#pragma unroll
+      for (int k = 1; k <= 5; k++) {
+        const int off = 1 << (k - 1);
+        const float4 a = shfl_up_box(w, off);
+        if (lane >= off) w = unite(w, a);
+        s.u.un.win[k][tid] = w;
+        const float4 b = make_float4(__shfl_down_sync(0xffffffffu, suf.x, off),
+                                     __shfl_down_sync(0xffffffffu, suf.y, off),
+                                     __shfl_down_sync(0xffffffffu, suf.z, off),
+                                     __shfl_down_sync(0xffffffffu, suf.w, off));
+        if (lane + off < 32) suf = unite(suf, b);
       }
+      s.u.un.suf[tid] = suf;
+      if (lane == 31) s.wtu[warp] = w;  // w = inclusive prefix over the whole warp
+    }
+    __syncthreads();
+    BB_TRACE(T, 5);
+    if (s_t > 0) {
+      const float4 after = range_union_threads(s, tid + 1, NT - 1);
+      for (int k = 0; k < s_t; k++)
+        p.f.su[(int64_t)T * TILE + (l_t + k + aT)] = unite(__ldcg(sc.uosu + uoff + k), after);
     }
     __syncthreads();
     if (warp == 0) {
@@ -716,15 +756,16 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
         __threadfence();
         st_release_u32(p.f.suf + T, 1u);
       }
-      publish_union(p.f, T, range_union_threads(s, 0, NT - 1));
+      float4 tu = lane < NW ? s.wtu[lane] : bEMPTY();
+      publish_union(p.f, T, warp_unite_all(tu));
     }
 
-    BB_TRACE(T, 6);
     // ---- G. unions reaching back into earlier tiles -------------------------
+    BB_TRACE(T, 6);
     for (int r = warp; r < nr; r += NW) {
       const int4 rr = __ldcg(sc.run + r);
       const float4 mid = range_union_tiles(p.f, rr.x + 1, T - 1);
-      if (lane == 0) sc.runr[r] = (mid);
+      if (lane == 0) sc.runr[r] = mid;
     }
     __syncthreads();
     for (int d = tid; d < min(aT, H); d += NT) {
@@ -742,35 +783,28 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
 
     BB_TRACE(T, 7);
     // ---- H. closes that pop entries of earlier threads / tiles -------------
-    {
+    if (ucm) {
       int ref = top_ref;
 #pragma unroll
       for (int i = 0; i < K; i++) {
         if ((ucm >> i) & 1u) {
           const int64_t g = tbase + i;
-          float4 PU = bEMPTY();  // this thread's clipped leaves before the close
-#pragma unroll
-          for (int j = 0; j < i; j++)
-            if ((lm >> j) & 1u) PU = unite(PU, bx[j]);
+          float4& me = s.box[slot(tid, i)];
           float4 U;
-          bool blend = false;
-          int64_t oidx = -1;  // chunk-local index of the open to scatter to
           if (ref >= 0) {
             const int V = ref / K;
             const float4 su = __ldcg(sc.uosu + s.uoff[V] + rank_in(s.uo[V], ref % K));
-            U = unite(unite(su, range_union_threads(s, V + 1, tid - 1)), PU);
-            blend = (s.bmk[V] >> (ref % K)) & 1u;
-            oidx = base + ref;
+            U = unite(unite(su, range_union_threads(s, V + 1, tid - 1)), me);
+            if ((s.bmk[V] >> (ref % K)) & 1u) s.box[slot(V, ref % K)] = U;
           } else {
             const int dd = -ref - 1;
             if (dd >= H) {
               U = bEMPTY();  // nothing to close (R3)
             } else {
               const int4 m = __ldcg(sc.meta + dd);
-              U = unite(unite(__ldcg(sc.accin + dd), range_union_threads(s, 0, tid - 1)), PU);
+              U = unite(unite(__ldcg(sc.accin + dd), range_union_threads(s, 0, tid - 1)), me);
               if (__ldcg(sc.run + m.z).x >= 0) {
-                blend = m.y != 0;
-                oidx = m.x - p.offset;
+                if (m.y) p.out[m.x - p.offset] = U;  // blend open of an earlier tile
               } else {
                 // the open lives in an earlier chunk: U so far is this chunk's part
                 const int k = p.H0 - H + dd;
@@ -783,11 +817,18 @@ __global__ void __launch_bounds__(NT, 2) bb_finish(Params p) {
               }
             }
           }
-          p.out[g] = U;
-          if (blend) p.out[oidx] = U;
+          me = U;
           ref = next_down(ref);
         }
       }
+    }
+    __syncthreads();
+
+    // ---- copy-out (coalesced), skipping tile-unmatched blend opens --------
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      const int e = j * NT + tid;
+      if (e < nvalid && !((s.skip[e >> 3] >> (e & 7)) & 1u)) __stcs(p.out + base + e, s.box[slot_of(e)]);
     }
     BB_TRACE(T, 8);
     __syncthreads();
@@ -1018,7 +1059,7 @@ __global__ void bb_fixup(int G, int g, int64_t off, int b_g, int min_L_after, in
 struct Layout {
   size_t ctrl_bytes, fzero_off, fzero_bytes, data_off, bytes;
   size_t off_counter, off_tcf, off_suf, off_uf[HLEVELS], off_ucnt[HLEVELS];
-  size_t off_tc, off_u[HLEVELS], off_su, off_bcount, off_slice, off_scratch;
+  size_t off_tc, off_u[HLEVELS], off_su, off_bcount, off_slice, off_scratch, off_tcacc, off_tcptr, off_tcflag;
   int64_t ntiles;
   int nblocks;
   static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -1045,6 +1086,9 @@ struct Layout {
       m = (m + 31) / 32;
     }
     off_bcount = o; o = al(o + 4 * (size_t)ntiles);
+    off_tcacc = o; o = al(o + 32 * (size_t)ntiles);
+    off_tcptr = o; o = al(o + 8 * (size_t)ntiles);
+    off_tcflag = o; o = al(o + 16);
     off_su = o; o = al(o + 16 * (size_t)ntiles * TILE);
     off_slice = o; o = al(o + sizeof(SliceRec) * (size_t)ntiles * SREC);
     off_scratch = o; o = al(o + SCRATCH_BYTES * (size_t)nblocks);
@@ -1125,6 +1169,29 @@ cudaError_t bb_finish_launch(const uint8_t* tags, const float* leaf_bbox, int64_
   const int nb_max = bb::finish_blocks();
   bb::Layout L(n, nb_max);
   bb::Params p = bb_params(tags, leaf_bbox, n, node_bbox, ws, sh, trace);
+  {
+    // tile clip chains (cooperative: one grid-wide barrier per doubling round)
+    static int tc_blocks = 0;
+    if (tc_blocks == 0) {
+      int dev = 0, sms = 0, occ = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bb::bb_tc, 256, 0);
+      tc_blocks = sms * std::max(occ, 1);
+    }
+    char* b = (char*)ws;
+    float4* acc2 = (float4*)(b + L.off_tcacc);
+    int* ptr2 = (int*)(b + L.off_tcptr);
+    int* flag = (int*)(b + L.off_tcflag);
+    const int64_t need = (L.ntiles * 32 + 255) / 256;  // one warp per tile in the link phase
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(need, tc_blocks));
+    void* args[] = {(void*)&p, (void*)&acc2, (void*)&ptr2, (void*)&flag};
+    void* tok;
+    prof_begin(stream, "bb_tc", &tok);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)bb::bb_tc, dim3(blocks), dim3(256), args, 0, stream);
+    prof_end(stream, tok);
+    if (e != cudaSuccess) return e;
+  }
   const int nfin = (int)std::min<int64_t>(L.ntiles, (int64_t)nb_max);
   TB_LAUNCH(stream, "bb_finish", (bb::bb_finish<<<(unsigned)nfin, bb::NT, sizeof(bb::Smem), stream>>>(p)));
   if (!sh)
@@ -1139,6 +1206,7 @@ cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, fl
   return err;
 }
 
+int bb_tile_elems() { return bb::TILE; }
 size_t bb_sumrec_bytes() { return sizeof(bb::SumRec); }
 size_t bb_pop_bytes() { return sizeof(bb::BbPop); }
 

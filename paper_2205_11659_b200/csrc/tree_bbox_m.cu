@@ -1,0 +1,849 @@
+// tree_bbox from matching (sm_100a): clip intersections and blend unions
+// (§6, §9) computed from the parent / match arrays that
+// paren_match produces (§2: parent = Fig. 1's out, match = the
+// classical partner).
+//
+// With the parent of every element known, the clip of an element is
+//     ctx(e) = box(e) ∩ ctx(parent(e))        (clip opens and leaves)
+//     ctx(b) = ctx(parent(b))                  (blend opens carry no box, R7)
+// and the union of a node (o, c = match(o)) is the union of the clipped leaves
+// strictly between o and c (R8).  Both are evaluated tile by tile:
+//
+// bbm_reduce   one CTA per tile.  The tile's opens whose close lies beyond the
+//              tile ("tile-unmatched": the slice of P:229-233) get their
+//              tile-local cumulative clip lc = ∩ of the clip boxes of the
+//              slice entries below and at them, written in place into
+//              node_bbox[o] (a placeholder the later passes read), and the tile
+//              records its link = the parent of its bottom slice entry.
+// bbm_tc       TC(T) = ctx(link_T) = lc(link_T) ∩ TC(tile of link_T): a forest
+//              over tiles resolved by pointer jumping (cooperative grid).  This
+//              replaces the paper's exclusive scan of per-partition top boxes
+//              (P:292).
+// bbm_main     persistent CTAs, tiles in order (atomic ticket):
+//   B  per-thread walk over its 8 elements: the clip relative to the
+//      thread's external ancestor X (the parent of the current outermost
+//      in-thread group), in place in shared memory;
+//   C  the context of each thread's link (X of its last outermost group) by
+//      pointer jumping over the tile's threads;
+//   D  pending elements: ctx(X) = rel(X) ∩ TL[thread of X] inside the tile,
+//      lc(X) ∩ TC(tile of X) outside it (componentwise idempotent, so reading
+//      a slot while its owner finalises it is harmless);
+//   E  per-thread union walk (sequential stack algorithm) over the
+//      thread's elements: in-thread nodes are finished, closes of outer nodes
+//      record the thread's prefix union, opens left open record the union of
+//      the thread's leaves after them;
+//   F  window unions over threads (warp shuffles), the tile's union published
+//      into a 32-ary hierarchy, and for every slice entry the union of the
+//      tile's leaves after it;
+//   G  closes of outer nodes: suffix union of the open's thread (or tile) ∪
+//      whole threads / whole tiles in between ∪ this thread's prefix (F4);
+//      blend opens receive the union (in shared memory, or in node_bbox when
+//      the open lies in an earlier tile);
+//   H  coalesced copy-out (slice blend opens are left to their closing tile).
+// bbm_final    blend opens never closed (R4): union of everything after them.
+#include <algorithm>
+#include <climits>
+#include <cooperative_groups.h>
+#include "boxes.cuh"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tb {
+namespace bbm {
+
+constexpr int NT = 128;
+constexpr int K = 8;
+constexpr int TILE = NT * K;
+constexpr int NW = NT / 32;
+constexpr int LV = 5;    // 32-ary levels of the tile-union hierarchy (32^5 tiles > 2^31 / TILE)
+constexpr int QCAP = 32; // distinct earlier tiles whose range union a tile resolves cooperatively
+
+struct Params {
+  const uint8_t* tags;
+  const float4* boxes;
+  const int32_t* match;
+  const int32_t* parent;
+  float4* out;
+  int64_t n;
+  int ntiles;
+  uint32_t* counter;     // tile tickets of bbm_main
+  uint32_t* uf[LV];      // published flags of the union hierarchy
+  uint32_t* ucnt[LV];    // arrival counters (k >= 1)
+  float4* u[LV];         // u[0][T] = union of tile T's clipped leaves; u[k] over 32^k tiles
+  int32_t* link;         // [ntiles] parent of the tile's bottom slice entry (-1: root / none)
+  float4* tc;            // [ntiles] ctx(link)
+  float4* tsuf;          // [ntiles + 1] union of tiles [T, ntiles) (after bbm_main)
+  float4* su;            // [n] union of the tile's clipped leaves after each slice entry
+  int32_t* never;        // [n] blend opens never closed (R4)
+  uint32_t* nnever;      // their count
+  uint64_t* trace;       // optional per-tile phase timestamps (debug)
+};
+
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define BBM_TRACE(T, s)                                                          \
+  do {                                                                           \
+    if (p.trace && threadIdx.x == 0) p.trace[(size_t)(T) * 16 + (s)] = gtime();  \
+  } while (0)
+
+// tag byte classes of 8 elements: om = opens (clip or blend), bm = blend
+// opens, cm = closes; everything else is a leaf (R2)
+__device__ __forceinline__ void classify8(uint2 raw, uint32_t& om, uint32_t& cm, uint32_t& bm) {
+  uint32_t o = 0, c = 0, b = 0;
+  const uint32_t ws[2] = {raw.x, raw.y};
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t bl = __vcmpeq4(x, 0x02020202u);
+    o |= byte_mask4(__vcmpeq4(x, 0x01010101u) | bl) << (4 * q);
+    c |= byte_mask4(__vcmpeq4(x, 0x03030303u)) << (4 * q);
+    b |= byte_mask4(bl) << (4 * q);
+  }
+  om = o;
+  cm = c;
+  bm = b;
+}
+
+__device__ __forceinline__ uint2 load_tags8(const uint8_t* tags, int64_t n, int64_t tbase) {
+  if (tbase + 8 <= n) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(tags + tbase));
+    return r;
+  }
+  uint32_t wv[2] = {0, 0};
+  for (int i = 0; i < 8; i++) {
+    const int64_t g = tbase + i;
+    const uint32_t v = g < n ? tags[g] : 0u;
+    wv[i >> 2] |= v << (8 * (i & 3));
+  }
+  return make_uint2(wv[0], wv[1]);
+}
+
+// 8 consecutive int32 (16-byte aligned when full); -1 past the end
+__device__ __forceinline__ void load_i8(const int32_t* a, int64_t n, int64_t tbase, int (&v)[K]) {
+  if (tbase + 8 <= n) {
+    const int4 x = __ldg(reinterpret_cast<const int4*>(a + tbase));
+    const int4 y = __ldg(reinterpret_cast<const int4*>(a + tbase) + 1);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < K; i++) v[i] = (tbase + i < n) ? __ldg(a + tbase + i) : -1;
+  }
+}
+
+__device__ __forceinline__ float4 wait_box(const uint32_t* flag, const float4* val) {
+  while (ld_acquire_u32(flag) == 0u) {
+  }
+  return __ldcg(val);
+}
+
+// Union over tiles [a, b] by one warp (a, b warp-uniform): per hierarchy
+// level, the lanes load the partial groups at both ends in parallel.
+__device__ float4 range_union_tiles_warp(const Params& p, int a, int b) {
+  const int lane = threadIdx.x & 31;
+  float4 acc = bEMPTY();
+  int k = 0;
+  while (a <= b) {
+    const uint32_t* fl = p.uf[k];
+    const float4* val = p.u[k];
+    if ((a >> 5) == (b >> 5) || k == LV - 1) {
+      for (int i = a + lane; i <= b; i += 32) acc = unite(acc, wait_box(fl + i, val + i));
+      break;
+    }
+    if (a & 31) {
+      const int e = a | 31;
+      const int i = a + lane;
+      if (i <= e) acc = unite(acc, wait_box(fl + i, val + i));
+      a = e + 1;
+    }
+    if ((b & 31) != 31) {
+      const int s0 = b & ~31;
+      const int i = s0 + lane;
+      if (i <= b) acc = unite(acc, wait_box(fl + i, val + i));
+      b = s0 - 1;
+    }
+    if (a > b) break;
+    a >>= 5;
+    b = ((b + 1) >> 5) - 1;
+    k++;
+  }
+  return warp_unite_all(acc);
+}
+
+// The same by one thread (fallback when a tile needs more than QCAP ranges).
+__device__ float4 range_union_tiles_seq(const Params& p, int a, int b) {
+  float4 acc = bEMPTY();
+  int k = 0;
+  while (a <= b) {
+    if (k == LV - 1 || (a >> 5) == (b >> 5)) {
+      for (int i = a; i <= b; i++) acc = unite(acc, wait_box(p.uf[k] + i, p.u[k] + i));
+      break;
+    }
+    for (; a & 31; a++) acc = unite(acc, wait_box(p.uf[k] + a, p.u[k] + a));
+    for (; (b & 31) != 31; b--) acc = unite(acc, wait_box(p.uf[k] + b, p.u[k] + b));
+    a >>= 5;
+    b = ((b + 1) >> 5) - 1;
+    k++;
+  }
+  return acc;
+}
+
+// Publish the tile's union and fold it into the hierarchy (one warp; the last
+// of 32 siblings to arrive publishes the parent).
+__device__ __forceinline__ void publish_union(const Params& p, int T, float4 tu) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    p.u[0][T] = tu;
+    __threadfence();
+    st_release_u32(p.uf[0] + T, 1u);
+  }
+  int idx = T;
+#pragma unroll 1
+  for (int k = 1; k < LV; k++) {
+    const int g = idx >> 5;
+    unsigned old = 0;
+    if (lane == 0) old = atom_add_acqrel_u32(p.ucnt[k] + g, 1u);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    // a partial last group never completes: ranges reaching the end of the
+    // stream are served by tsuf
+    if (old != 31u) return;
+    const int c = (g << 5) + lane;
+    float4 v = wait_box(p.uf[k - 1] + c, p.u[k - 1] + c);
+    v = warp_unite_all(v);
+    if (lane == 0) {
+      p.u[k][g] = v;
+      __threadfence();
+      st_release_u32(p.uf[k] + g, 1u);
+    }
+    idx = g;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// bbm_reduce: slice clips (lc) in place, tile links
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) bbm_reduce(Params p) {
+  __shared__ float4 wbox[NW];
+  __shared__ int wmin[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockIdx.x;
+  const int64_t base = (int64_t)T * TILE, tbase = base + (int64_t)tid * K;
+  const int64_t tend = base + TILE;
+  uint32_t om, cm, bm;
+  classify8(load_tags8(p.tags, p.n, tbase), om, cm, bm);
+  int mt[K];
+  load_i8(p.match, p.n, tbase, mt);
+  uint32_t sm = 0;  // slice entries (opens closed beyond the tile or never)
+#pragma unroll
+  for (int i = 0; i < K; i++)
+    if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= tend)) sm |= 1u << i;
+  // thread aggregate of the slice clips, then exclusive ∩-scan over threads
+  float4 agg = bINF();
+#pragma unroll
+  for (int i = 0; i < K; i++)
+    if (((sm & ~bm) >> i) & 1u) agg = isect(agg, __ldg(p.boxes + tbase + i));
+  float4 x = agg;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float4 o = shfl_up_box(x, off);
+    if (lane >= off) x = isect(x, o);
+  }
+  const int first = sm ? (tid * K + __ffs(sm) - 1) : INT_MAX;
+  const int wf = __reduce_min_sync(0xffffffffu, first);
+  if (lane == 31) wbox[warp] = x;
+  if (lane == 0) wmin[warp] = wf;
+  __syncthreads();
+  float4 pre = bINF();
+  int tf = INT_MAX;
+#pragma unroll
+  for (int w = 0; w < NW; w++) {
+    if (w < warp) pre = isect(pre, wbox[w]);
+    tf = min(tf, wmin[w]);
+  }
+  float4 e = shfl_up_box(x, 1);
+  if (lane == 0) e = bINF();
+  float4 acc = isect(pre, e);
+#pragma unroll
+  for (int i = 0; i < K; i++) {
+    if ((sm >> i) & 1u) {
+      if (!((bm >> i) & 1u)) acc = isect(acc, __ldg(p.boxes + tbase + i));
+      p.out[tbase + i] = acc;
+    }
+  }
+  if (tid == 0) p.link[T] = (tf == INT_MAX) ? -1 : __ldg(p.parent + base + tf);
+}
+
+// ----------------------------------------------------------------------------
+// bbm_tc: TC(T) = ctx(link_T) by pointer jumping over tiles (cooperative)
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2, int* flag) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int nt = p.ntiles;
+  const int gt = (int)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  const int nthr = (int)(gridDim.x * (int64_t)blockDim.x);
+  float4* acc[2] = {acc2, acc2 + nt};
+  int* ptr[2] = {ptr2, ptr2 + nt};
+  for (int V = gt; V < nt; V += nthr) {
+    const int X = __ldg(p.link + V);
+    acc[0][V] = X >= 0 ? __ldg(p.out + X) : bINF();  // lc(X), written by bbm_reduce
+    ptr[0][V] = X >= 0 ? X / TILE : -1;
+  }
+  int cb = 0;
+  for (int round = 0; round < 40; round++) {
+    if (gt == 0) flag[round & 1] = 0;
+    grid.sync();
+    int any = 0;
+    for (int V = gt; V < nt; V += nthr) {
+      float4 a = __ldcg(acc[cb] + V);
+      int q = __ldcg(ptr[cb] + V);
+      if (q >= 0) {
+        a = isect(a, __ldcg(acc[cb] + q));
+        q = __ldcg(ptr[cb] + q);
+        any |= q >= 0;
+      }
+      acc[cb ^ 1][V] = a;
+      ptr[cb ^ 1][V] = q;
+    }
+    any = __syncthreads_or(any);
+    if (any && threadIdx.x == 0) atomicOr(flag + (round & 1), 1);
+    cb ^= 1;
+    grid.sync();
+    if (__ldcg(flag + (round & 1)) == 0) break;
+  }
+  for (int V = gt; V < nt; V += nthr) p.tc[V] = __ldcg(acc[cb] + V);
+}
+
+// ----------------------------------------------------------------------------
+// bbm_main
+// ----------------------------------------------------------------------------
+struct Smem {
+  float4 val[TILE];  // boxes -> clips -> outputs (swizzled slots)
+  float4 ua[TILE];   // union accumulators of opens; prefix unions of outer closes
+  float4 tl[NT];     // ctx of each thread's link
+  union {
+    struct {
+      float4 acc[2][NT];
+      int ptr[2][NT];
+    } pj;
+    struct {
+      float4 win[6][NT];  // union of thread unions over lanes [lane - 2^k + 1, lane] (clipped to the warp)
+      float4 suf[NT];     // inclusive suffix within the warp
+    } un;
+  } u;
+  float4 wtu[NW];
+  uint32_t bmk[NT];
+  int qkey[QCAP];     // earlier tiles To whose range union (To, T) this tile needs
+  float4 qval[QCAP];
+  int qn;
+  int tile;
+};
+
+__device__ __forceinline__ int qslot(int To) { return (int)(((uint32_t)To * 2654435761u) >> 27) & (QCAP - 1); }
+
+// element i of thread t lives at slot 8t + (i ^ (t & 7)): conflict-free both for
+// the coalesced copies and for the per-thread accesses
+__device__ __forceinline__ int slot(int t, int i) { return (t << 3) | (i ^ (t & 7)); }
+__device__ __forceinline__ int slot_of(int e) { return slot(e >> 3, e & 7); }
+
+// union of the clipped leaves of whole threads [a, b]
+__device__ __forceinline__ float4 range_union_threads(const Smem& s, int a, int b) {
+  if (a > b) return bEMPTY();
+  const int wa = a >> 5, wb = b >> 5;
+  if (wa == wb) {
+    const int k = 31 - __clz(b - a + 1);
+    return unite(s.u.un.win[k][b], s.u.un.win[k][a + (1 << k) - 1]);
+  }
+  float4 v = unite(s.u.un.suf[a], s.u.un.win[5][b]);
+#pragma unroll 1
+  for (int w = wa + 1; w < wb; w++) v = unite(v, s.wtu[w]);
+  return v;
+}
+
+__global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  while (true) {
+    if (tid == 0) s.tile = (int)atomicAdd(p.counter, 1u);
+    __syncthreads();
+    const int T = s.tile;
+    if (T >= p.ntiles) break;
+    const int64_t base = (int64_t)T * TILE;
+    const int64_t tstart = base + (int64_t)tid * K;
+    const int64_t tend = base + TILE;
+    const int nvalid = (int)(p.n - base < TILE ? p.n - base : TILE);
+    BBM_TRACE(T, 0);
+
+    // ---- A. load -----------------------------------------------------------
+    uint32_t om, cm, bm;
+    classify8(load_tags8(p.tags, p.n, tstart), om, cm, bm);
+    uint32_t lm = ~om & ~cm & 0xffu;
+    {
+      const int64_t rem = p.n - tstart;
+      if (rem < K) lm &= rem <= 0 ? 0u : ((1u << rem) - 1u);
+    }
+    int mt[K], pr[K];
+    load_i8(p.match, p.n, tstart, mt);
+    load_i8(p.parent, p.n, tstart, pr);
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      const int e = j * NT + tid;
+      s.val[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bINF();
+    }
+    s.bmk[tid] = bm;
+    if (tid < QCAP) s.qkey[tid] = -1;
+    if (tid == 0) s.qn = 0;
+    uint32_t thr_un = 0;  // opens closed beyond this thread (or never)
+#pragma unroll
+    for (int i = 0; i < K; i++)
+      if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= tstart + K)) thr_un |= 1u << i;
+    __syncthreads();
+
+    // ---- B. clips relative to the thread's external ancestor -----------------
+    int curX = -1;
+    uint32_t pend = 0;
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      if (((om | lm) >> i) & 1u) {
+        const int par = pr[i];
+        float4 b = bINF();
+        if (par < tstart) {
+          curX = par;
+        } else {
+          b = s.val[slot(tid, par - (int)tstart)];
+        }
+        float4& me = s.val[slot(tid, i)];
+        me = ((bm >> i) & 1u) ? b : isect(me, b);
+        if (curX >= 0) pend |= 1u << i;
+      }
+    }
+    __syncthreads();
+    BBM_TRACE(T, 1);
+
+    // ---- C. ctx of each thread's link (pointer jumping over threads) ----------
+    {
+      float4 acc = bINF();
+      int ptr = -1;
+      if (thr_un && curX >= 0) {
+        if (curX < base) {
+          acc = isect(__ldcg(p.out + curX), __ldg(p.tc + curX / TILE));
+        } else {
+          const int x = curX - (int)base;
+          acc = s.val[slot_of(x)];
+          ptr = x / K;
+        }
+      }
+      int cb = 0;
+      s.u.pj.acc[0][tid] = acc;
+      s.u.pj.ptr[0][tid] = ptr;
+      int any = __syncthreads_or(ptr >= 0);
+      while (any) {
+        if (ptr >= 0) {
+          acc = isect(acc, s.u.pj.acc[cb][ptr]);
+          ptr = s.u.pj.ptr[cb][ptr];
+        }
+        s.u.pj.acc[cb ^ 1][tid] = acc;
+        s.u.pj.ptr[cb ^ 1][tid] = ptr;
+        cb ^= 1;
+        any = __syncthreads_or(ptr >= 0);
+      }
+      s.tl[tid] = acc;
+    }
+    __syncthreads();
+    BBM_TRACE(T, 2);
+
+    // ---- D. finish pending clips: rel ∩ ctx(X) ----------------------------------
+    if (pend) {
+      int X = -1, cx = INT_MIN;
+      float4 g = bINF();
+#pragma unroll
+      for (int i = 0; i < K; i++) {
+        if (((om | lm) >> i) & 1u) {
+          if (pr[i] < tstart) X = pr[i];
+          if ((pend >> i) & 1u) {
+            if (X != cx) {
+              cx = X;
+              if (X < base) {
+                g = isect(__ldcg(p.out + X), __ldg(p.tc + X / TILE));
+              } else {
+                const int x = X - (int)base;
+                g = isect(s.val[slot_of(x)], s.tl[x / K]);
+              }
+            }
+            float4& me = s.val[slot(tid, i)];
+            me = isect(me, g);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    BBM_TRACE(T, 3);
+
+    // ---- E. union walk ------------------------------------------------------------
+    float4 PT = bEMPTY();  // union of this thread's clipped leaves so far
+    uint32_t S = 0, ecm = 0;
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      const uint32_t bit = 1u << i;
+      if (lm & bit) {
+        const float4 v = s.val[slot(tid, i)];
+        PT = unite(PT, v);
+        if (S) {
+          float4& a = s.ua[slot(tid, 31 - __clz(S))];
+          a = unite(a, v);
+        }
+      } else if (om & bit) {
+        S |= bit;
+        s.ua[slot(tid, i)] = bEMPTY();
+      } else if ((cm & bit) && i < nvalid - tid * K) {
+        const int m = mt[i];
+        if (m >= tstart) {
+          const int o = m - (int)tstart;  // the top of S
+          const float4 U = s.ua[slot(tid, o)];
+          s.val[slot(tid, i)] = U;
+          if ((bm >> o) & 1u) s.val[slot(tid, o)] = U;
+          S ^= 1u << o;
+          if (S) {
+            float4& a = s.ua[slot(tid, 31 - __clz(S))];
+            a = unite(a, U);
+          }
+        } else if (m >= 0) {
+          s.ua[slot(tid, i)] = PT;
+          s.val[slot(tid, i)].x = __int_as_float(m);  // the open, until G writes the union here
+          ecm |= bit;
+        } else {
+          s.val[slot(tid, i)] = bEMPTY();  // R3
+        }
+      }
+    }
+    {
+      // suffix unions of the opens left open: union of the thread's leaves after them
+      float4 R = bEMPTY();
+      uint32_t q = S;
+      while (q) {
+        const int o = 31 - __clz(q);
+        q ^= 1u << o;
+        float4& a = s.ua[slot(tid, o)];
+        R = unite(R, a);
+        a = R;
+      }
+    }
+    BBM_TRACE(T, 4);
+
+    // ---- F. unions over threads; publication ------------------------------------------
+    {
+      float4 w = PT, suf = PT;
+      s.u.un.win[0][tid] = w;
+#pragma unroll
+      for (int k = 1; k <= 5; k++) {
+        const int off = 1 << (k - 1);
+        const float4 a = shfl_up_box(w, off);
+        if (lane >= off) w = unite(w, a);
+        s.u.un.win[k][tid] = w;
+        const float4 b = make_float4(__shfl_down_sync(0xffffffffu, suf.x, off),
+                                     __shfl_down_sync(0xffffffffu, suf.y, off),
+                                     __shfl_down_sync(0xffffffffu, suf.z, off),
+                                     __shfl_down_sync(0xffffffffu, suf.w, off));
+        if (lane + off < 32) suf = unite(suf, b);
+      }
+      s.u.un.suf[tid] = suf;
+      if (lane == 31) s.wtu[warp] = w;
+    }
+    __syncthreads();
+    {
+      uint32_t q = 0, nvm = 0;  // slice entries of this thread; blend opens never closed
+#pragma unroll
+      for (int i = 0; i < K; i++) {
+        if (((thr_un >> i) & 1u) && (mt[i] < 0 || mt[i] >= tend)) q |= 1u << i;
+        if (((bm >> i) & 1u) && mt[i] < 0) nvm |= 1u << i;
+      }
+      if (q) {
+        const float4 after = range_union_threads(s, tid + 1, NT - 1);
+#pragma unroll 1
+        while (q) {
+          const int o = __ffs(q) - 1;
+          q &= q - 1;
+          p.su[tstart + o] = unite(s.ua[slot(tid, o)], after);
+          if ((nvm >> o) & 1u) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + o);
+        }
+      }
+    }
+    if (ecm) {
+      // register the earlier tiles this thread needs a range union to
+      int last = -1;
+      uint32_t q = ecm;
+#pragma unroll 1
+      while (q) {
+        const int i = __ffs(q) - 1;
+        q &= q - 1;
+        const int o = __float_as_int(s.val[slot(tid, i)].x);
+        if (o >= base) continue;
+        const int To = o / TILE;
+        if (To < T - 1 && To != last) {
+          last = To;
+          int h = qslot(To);
+#pragma unroll 1
+          for (int probe = 0; probe < QCAP; probe++) {
+            const int old = atomicCAS(&s.qkey[h], -1, To);
+            if (old == -1 || old == To) {
+              if (old == -1) atomicAdd(&s.qn, 1);
+              break;
+            }
+            h = (h + 1) & (QCAP - 1);
+          }
+        }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (warp == 0) {
+      float4 tu = lane < NW ? s.wtu[lane] : bEMPTY();
+      tu = warp_unite_all(tu);
+      publish_union(p, T, tu);
+    }
+    BBM_TRACE(T, 5);
+
+    // ---- G. closes of nodes opened in an earlier thread or tile -------------------------
+    if (s.qn) {  // range unions over whole earlier tiles, one warp per distinct range
+      for (int r = warp; r < QCAP; r += NW) {
+        const int To = s.qkey[r];
+        if (To >= 0) {
+          const float4 R = range_union_tiles_warp(p, To + 1, T - 1);
+          if (lane == 0) s.qval[r] = R;
+        }
+      }
+      __syncthreads();
+    }
+    if (ecm) {
+      int cto = -1;
+      float4 cR = bEMPTY(), pre_thr = bEMPTY();
+      bool have_pre = false;
+      uint32_t q = ecm;
+#pragma unroll 1
+      while (q) {
+        const int i = __ffs(q) - 1;
+        q &= q - 1;
+        float4& me = s.val[slot(tid, i)];
+        const int o = __float_as_int(me.x);
+        float4 U = s.ua[slot(tid, i)];  // this thread's prefix before the close
+        if (o >= base) {
+          const int x = o - (int)base;
+          const int V = x / K;
+          U = unite(U, unite(s.ua[slot_of(x)], range_union_threads(s, V + 1, tid - 1)));
+          if ((s.bmk[V] >> (x % K)) & 1u) s.val[slot_of(x)] = U;
+        } else {
+          const int To = o / TILE;
+          const float4 su = wait_box(p.uf[0] + To, p.su + o);
+          if (To != cto) {
+            cto = To;
+            cR = bEMPTY();
+            if (To < T - 1) {
+              int h = qslot(To), probe = 0;
+#pragma unroll 1
+              while (probe < QCAP && s.qkey[h] != To) {
+                h = (h + 1) & (QCAP - 1);
+                probe++;
+              }
+              cR = probe < QCAP ? s.qval[h] : range_union_tiles_seq(p, To + 1, T - 1);
+            }
+          }
+          if (!have_pre) {
+            pre_thr = range_union_threads(s, 0, tid - 1);
+            have_pre = true;
+          }
+          U = unite(unite(U, su), unite(cR, pre_thr));
+          if (__ldg(p.tags + o) == 2) p.out[o] = U;
+        }
+        me = U;
+      }
+    }
+    __syncthreads();
+    BBM_TRACE(T, 6);
+
+    // ---- H. copy-out (slice blend opens belong to their closing tile) ---------------------
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      const int e = j * NT + tid;
+      if (e < nvalid) {
+        const int t = e >> 3, i = e & 7;
+        // a slice blend open: blend, and not closed inside this tile
+        bool skip = false;
+        if ((s.bmk[t] >> i) & 1u) {
+          const int m = __ldg(p.match + base + e);
+          skip = m < 0 || m >= tend;
+        }
+        if (!skip) __stcs(p.out + base + e, s.val[slot_of(e)]);
+      }
+    }
+    BBM_TRACE(T, 7);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// blend opens never closed (R4)
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) bbm_tsuf(Params p) {
+  // one CTA: tsuf[T] = ∪ u[0][T..ntiles-1], reverse scan in chunks of 1024
+  __shared__ float4 wb[32];
+  __shared__ float4 carry_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float4 carry = bEMPTY();
+  if (tid == 0) p.tsuf[p.ntiles] = carry;
+  for (int hi = p.ntiles - 1; hi >= 0; hi -= 1024) {
+    const int T = hi - tid;
+    float4 v = T >= 0 ? __ldcg(p.u[0] + T) : bEMPTY();
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float4 o = shfl_up_box(v, off);
+      if (lane >= off) v = unite(v, o);
+    }
+    if (lane == 31) wb[warp] = v;
+    __syncthreads();
+    float4 pre = carry;
+    for (int w = 0; w < warp; w++) pre = unite(pre, wb[w]);
+    v = unite(v, pre);
+    if (T >= 0) p.tsuf[T] = v;
+    if (tid == 1023) carry_s = v;
+    __syncthreads();
+    carry = carry_s;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) bbm_final(Params p) {
+  const uint32_t cnt = __ldcg(p.nnever);
+  for (uint32_t q = blockIdx.x * 256 + threadIdx.x; q < cnt; q += gridDim.x * 256) {
+    const int o = __ldcg(p.never + q);
+    const int To = o / TILE;
+    p.out[o] = unite(__ldcg(p.su + o), __ldcg(p.tsuf + To + 1));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// workspace
+// ----------------------------------------------------------------------------
+struct Layout {
+  int64_t ntiles;
+  size_t zero_off, zero_bytes;
+  size_t off_counter, off_nnever, off_uf[LV], off_ucnt[LV];
+  size_t off_u[LV], off_link, off_tc, off_tsuf, off_su, off_never, off_tcacc, off_tcptr, off_tcflag, bytes;
+  explicit Layout(int64_t n) {
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    ntiles = (n + TILE - 1) / TILE;
+    size_t o = 0;
+    zero_off = o;
+    off_counter = o; o = al(o + 4);
+    off_nnever = o; o = al(o + 4);
+    int64_t m = ntiles;
+    for (int k = 0; k < LV; k++) {
+      off_uf[k] = o; o = al(o + 4 * (size_t)m);
+      off_ucnt[k] = o; o = al(o + 4 * (size_t)m);
+      m = (m + 31) / 32;
+    }
+    zero_bytes = o - zero_off;
+    m = ntiles;
+    for (int k = 0; k < LV; k++) {
+      off_u[k] = o; o = al(o + 16 * (size_t)m);
+      m = (m + 31) / 32;
+    }
+    off_link = o; o = al(o + 4 * (size_t)ntiles);
+    off_tc = o; o = al(o + 16 * (size_t)ntiles);
+    off_tsuf = o; o = al(o + 16 * (size_t)(ntiles + 1));
+    off_tcacc = o; o = al(o + 32 * (size_t)ntiles);
+    off_tcptr = o; o = al(o + 8 * (size_t)ntiles);
+    off_tcflag = o; o = al(o + 16);
+    off_su = o; o = al(o + 16 * (size_t)n);
+    off_never = o; o = al(o + 4 * (size_t)n);
+    bytes = o;
+  }
+};
+
+int main_blocks() {
+  static int nb = 0;
+  if (nb == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(bbm_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbm_main, NT, sizeof(Smem));
+    nb = sms * (occ > 0 ? occ : 1);
+  }
+  return nb;
+}
+
+int tc_blocks() {
+  static int nb = 0;
+  if (nb == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbm_tc, 256, 0);
+    nb = sms * std::max(occ, 1);
+  }
+  return nb;
+}
+
+}  // namespace bbm
+
+size_t bbm_workspace_bytes(int64_t n) {
+  if (n <= 0) return 0;
+  return bbm::Layout(n).bytes;
+}
+
+int bbm_tile_elems() { return bbm::TILE; }
+
+cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                       int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace) {
+  if (n <= 0) return cudaSuccess;
+  bbm::Layout L(n);
+  char* b = (char*)ws;
+  bbm::Params p;
+  p.tags = tags;
+  p.boxes = reinterpret_cast<const float4*>(leaf_bbox);
+  p.match = match;
+  p.parent = parent;
+  p.out = reinterpret_cast<float4*>(node_bbox);
+  p.n = n;
+  p.ntiles = (int)L.ntiles;
+  p.counter = (uint32_t*)(b + L.off_counter);
+  p.nnever = (uint32_t*)(b + L.off_nnever);
+  for (int k = 0; k < bbm::LV; k++) {
+    p.uf[k] = (uint32_t*)(b + L.off_uf[k]);
+    p.ucnt[k] = (uint32_t*)(b + L.off_ucnt[k]);
+    p.u[k] = (float4*)(b + L.off_u[k]);
+  }
+  p.tsuf = (float4*)(b + L.off_tsuf);
+  p.link = (int32_t*)(b + L.off_link);
+  p.tc = (float4*)(b + L.off_tc);
+  p.su = (float4*)(b + L.off_su);
+  p.never = (int32_t*)(b + L.off_never);
+  p.trace = trace;
+  cudaError_t err = cudaMemsetAsync(b + L.zero_off, 0, L.zero_bytes, stream);
+  if (err != cudaSuccess) return err;
+  TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<(unsigned)L.ntiles, bbm::NT, 0, stream>>>(p)));
+  {
+    float4* acc2 = (float4*)(b + L.off_tcacc);
+    int* ptr2 = (int*)(b + L.off_tcptr);
+    int* flag = (int*)(b + L.off_tcflag);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((L.ntiles + 255) / 256, bbm::tc_blocks()));
+    void* args[] = {(void*)&p, (void*)&acc2, (void*)&ptr2, (void*)&flag};
+    void* tok;
+    prof_begin(stream, "bbm_tc", &tok);
+    err = cudaLaunchCooperativeKernel((const void*)bbm::bbm_tc, dim3(blocks), dim3(256), args, 0, stream);
+    prof_end(stream, tok);
+    if (err != cudaSuccess) return err;
+  }
+  const int nmain = (int)std::min<int64_t>(L.ntiles, (int64_t)bbm::main_blocks());
+  TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<<<(unsigned)nmain, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_tsuf", (bbm::bbm_tsuf<<<1, 1024, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
+  return cudaGetLastError();
+}
+
+}  // namespace tb

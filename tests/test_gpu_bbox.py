@@ -2,7 +2,7 @@
 
 Boxes are compared as raw fp32 bit patterns (0 ULP): min/max are
 exact and totalOrder makes every result unique, including signed zeros.
-Sizes span many tiles (2048 elements each) with ragged tails; edge corpora
+Sizes span many tiles (1024 elements each) with ragged tails; edge corpora
 hit tile boundaries, deep chains (C3/C3L), bursts (C4), unmatched closes
 (R3), unmatched trailing opens (R4) and special fp32 values.
 """
@@ -17,7 +17,7 @@ import oracle
 import scenegen
 
 pytestmark = pytest.mark.gpu
-TILE = 2048
+TILE = 1024
 INF = float("inf")
 
 
@@ -26,7 +26,7 @@ def gpu():
     return tb
 
 
-def check(tags_cpu: torch.Tensor, boxes_cpu: torch.Tensor | None = None, seed: int = 0):
+def check(tags_cpu: torch.Tensor, boxes_cpu: torch.Tensor | None = None, seed: int = 0, matched: bool = False):
     tb = gpu()
     t = tags_cpu.to(torch.uint8).contiguous()
     n = t.numel()
@@ -35,7 +35,17 @@ def check(tags_cpu: torch.Tensor, boxes_cpu: torch.Tensor | None = None, seed: i
     ref = oracle.tree_bbox(t.numpy(), b.numpy())
     out = tb.tree_bbox(t.cuda(), b.cuda())
     torch.cuda.synchronize()
+    same_bits(out, ref, t)
+    if matched and n > 0:
+        m, p = tb.paren_match(t.cuda())
+        out2 = tb.tree_bbox_matched(t.cuda(), b.cuda(), m, p)
+        torch.cuda.synchronize()
+        same_bits(out2, ref, t)
+
+
+def same_bits(out, ref, t):
     got = out.cpu().numpy()
+    n = len(got)
     gb, rb = got.view(np.uint32), ref.view(np.uint32)
     if not np.array_equal(gb, rb):
         bad = np.nonzero((gb != rb).any(1))[0]
@@ -60,7 +70,7 @@ def test_empty_and_single():
         check(torch.tensor([v], dtype=torch.uint8), torch.tensor([[1.0, 2.0, 3.0, 4.0]]))
 
 
-@pytest.mark.parametrize("n", [7, 8, 9, 2047, 2048, 2049, 4095, 4096, 4097, 3 * 2048 + 5, 65 * 2048 - 1,
+@pytest.mark.parametrize("n", [7, 8, 9, 1023, 1024, 1025, 2047, 2048, 2049, 4095, 4096, 4097, 3 * 2048 + 5, 65 * 2048 - 1,
                                65 * 2048 + 3])
 def test_tile_boundaries_random(n):
     for seed in range(3):
@@ -131,7 +141,7 @@ def test_inverted_boxes():
 @pytest.mark.parametrize("seed", range(4))
 def test_random_walks(seed):
     for n in (1 << 16, (1 << 20) + 12345):
-        check(scenegen.walk_tags(n, seed, p_leaf=0.5 if seed % 2 else 0.25), seed=seed)
+        check(scenegen.walk_tags(n, seed, p_leaf=0.5 if seed % 2 else 0.25), seed=seed, matched=True)
 
 
 def test_configs_c1_c2():
@@ -150,6 +160,18 @@ def test_config_c4_full():
 
 def test_config_c5_bench_size():
     check(scenegen.config("C5")[0], seed=4)
+
+
+def test_matched_entry_point():
+    """tree_bbox_matched on paren_match's outputs: every corpus shape."""
+    g = torch.Generator().manual_seed(21)
+    cases = [scenegen.walk_tags(300_007, 21, p_leaf=0.5), scenegen.deep_chain_tags(50_000, 1),
+             scenegen.deep_chain_tags(70_001, 2, leaves_mid=True), torch.full((5000,), 2, dtype=torch.uint8),
+             torch.full((5000,), 3, dtype=torch.uint8),
+             torch.multinomial(torch.tensor([0.3, 0.15, 0.1, 0.45]), 100_000, replacement=True,
+                               generator=g).to(torch.uint8)]
+    for i, t in enumerate(cases):
+        check(t, seed=i, matched=True)
 
 
 def test_deterministic_repeat():
