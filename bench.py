@@ -8,7 +8,8 @@ Workload (BASELINE.json metric "G elements/s for paren_match+tree_bbox"): the
 paper's random push/pop stream (configs[4], "random-depth stream"),
 synthetic, 2^27 elements per GPU (weak scaling; N = 8 is the 1B-element
 stream), 50 % leaves, 75 % of opens are clips, unbalanced tail kept.  One
-step = paren_match then tree_bbox over the resident stream.  Inputs (2.2 GB
+step = paren_match, then tree_bbox_matched on its match/parent outputs (the
+boxes computed from that matching), over the resident stream.  Inputs (2.2 GB
 per GPU) exceed the 126 MB L2, so no flush between steps.
 
 Printed (rank 0, one JSON line): value = elements x steps / max-over-ranks
@@ -37,7 +38,8 @@ import torch  # noqa: E402
 METRIC = "G elements/s for paren_match+tree_bbox"
 UNIT = "Gelem/s"
 BYTES_PM = 9     # 1 B tag in, 4 B match + 4 B parent out
-BYTES_TB = 33    # 1 B tag + 16 B box in, 16 B box out
+BYTES_TB = 41    # tree_bbox_matched: 1 B tag + 16 B box + 4 B match + 4 B parent in, 16 B box out
+BYTES_PAIR = 41  # the step's own inputs and outputs: 1 B tag + 16 B box in; 4 + 4 + 16 B out
 
 
 def parse():
@@ -210,7 +212,7 @@ def main():
     def step():
         if shard is None:
             tb.paren_match(tags, match, parent)
-            tb.tree_bbox(tags, boxes, out)
+            tb.tree_bbox_matched(tags, boxes, match, parent, out)
         else:
             shard.paren_match(tags, match, parent)
             shard.tree_bbox(tags, boxes, out)
@@ -257,8 +259,9 @@ def main():
     lib.tb_profile_read(buf, len(buf))
     lib.tb_profile_enable(0)
     per_kernel = json.loads(buf.value.decode() or "{}")
-    alg_bytes = {"pm_finish": BYTES_PM * n, "pm_reduce": 1 * n, "bb_finish": BYTES_TB * n, "bb_reduce": 1 * n}
-    dom = max(per_kernel.items(), key=lambda kv: kv[1][1])[0] if per_kernel else "bb_finish"
+    alg_bytes = {"pm_finish": BYTES_PM * n, "pm_reduce": 1 * n, "bbm_main": BYTES_TB * n, "bbm_reduce": 5 * n,
+                 "bb_finish": 33 * n, "bb_reduce": 1 * n}
+    dom = max(per_kernel.items(), key=lambda kv: kv[1][1])[0] if per_kernel else "bbm_main"
     cnt, tot_ms = per_kernel.get(dom, [1, float("nan")])
     avg_ms = tot_ms / max(cnt, 1)
     peak, peak_src = measured_peak()
@@ -281,8 +284,16 @@ def main():
         e_steps = max(1, min(args.steps, 3))
 
         def estep():
-            tb.paren_match_host(h_tags, h_match, h_parent, device=dev)
-            tb.tree_bbox_host(h_tags, h_boxes, h_out, device=dev)
+            if shard is None:
+                tb.paren_match_tree_bbox_host(h_tags, h_boxes, h_match, h_parent, h_out, device=dev)
+            else:
+                tags.copy_(h_tags, non_blocking=True)
+                boxes.copy_(h_boxes, non_blocking=True)
+                step()
+                h_match.copy_(match, non_blocking=True)
+                h_parent.copy_(parent, non_blocking=True)
+                h_out.copy_(out, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
         estep()
         torch.cuda.synchronize()
         barrier()
@@ -300,8 +311,10 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": world * n * e_steps / (ems / 1e3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * n + 16 * n, "d2h_bytes_per_step": 8 * n + 16 * n,
-               "steps": e_steps, "api": "paren_match_host + tree_bbox_host (pinned host buffers)"}
+               "h2d_bytes_per_step": 17 * n, "d2h_bytes_per_step": 24 * n,
+               "steps": e_steps,
+               "api": ("paren_match_tree_bbox_host (pinned host buffers)" if shard is None else
+                       "pinned H2D + ShardContext.paren_match/tree_bbox + D2H")}
 
     # --- oracle on the host (rank 0, N = 1 only)
     cpu = None
@@ -336,8 +349,8 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
-            "pair_bytes_per_elem": BYTES_PM + BYTES_TB,
-            "pair_hbm_frac": (BYTES_PM + BYTES_TB) * n * world / (ms_per_step / 1e3) / 1e9 / (peak * world),
+            "pair_bytes_per_elem": BYTES_PAIR,
+            "pair_hbm_frac": BYTES_PAIR * n * world / (ms_per_step / 1e3) / 1e9 / (peak * world),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

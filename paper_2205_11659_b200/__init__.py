@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["paren_match", "tree_bbox", "tree_bbox_matched", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["paren_match", "tree_bbox", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard"]
 
@@ -53,6 +53,7 @@ def load():
                 "tree_bbox_workspace_bytes": ([I64], SZ),
                 "tree_bbox_host": ([P, P, I64, P, P], ctypes.c_int),
                 "tree_bbox_matched": ([P, P, P, P, I64, P, P], ctypes.c_int),
+                "paren_match_tree_bbox_host": ([P, P, I64, P, P, P, P], ctypes.c_int),
                 "tree_bbox_matched_ws": ([P, P, P, P, I64, P, P, SZ, P], ctypes.c_int),
                 "tree_bbox_matched_workspace_bytes": ([I64], SZ),
                 "tb_count_unmatched": ([P, I64, P, P, P], ctypes.c_int),
@@ -181,6 +182,18 @@ def tree_bbox_host(tags: torch.Tensor, leaf_bbox: torch.Tensor, node_bbox: torch
         _check(lib.tree_bbox_host(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(),
                                   node_bbox.data_ptr(), _stream(dev)))
     return node_bbox
+
+
+def paren_match_tree_bbox_host(tags: torch.Tensor, leaf_bbox: torch.Tensor, match: torch.Tensor,
+                               parent: torch.Tensor, node_bbox: torch.Tensor, device=None):
+    """The whole hot path from (pinned) host tensors: copies in, paren_match,
+    tree_bbox_matched, copies out, synchronises."""
+    lib = load()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    with torch.cuda.device(dev):
+        _check(lib.paren_match_tree_bbox_host(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), match.data_ptr(),
+                                              parent.data_ptr(), node_bbox.data_ptr(), _stream(dev)))
+    return match, parent, node_bbox
 
 
 def count_unmatched(tags: torch.Tensor):

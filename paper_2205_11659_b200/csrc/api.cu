@@ -280,6 +280,41 @@ int tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, f
   return TB_OK;
 }
 
+int paren_match_tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, int32_t* h_match,
+                               int32_t* h_parent, float* h_node_bbox, void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r || n == 0) return r;
+  if (!h_tags || !h_leaf_bbox || !h_match || !h_parent || !h_node_bbox)
+    return fail(TB_ERR_ARG, "null pointer with n > 0");
+  const size_t nb_t = ((size_t)n + 255) & ~(size_t)255;
+  const size_t nb_i = ((size_t)n * 4 + 255) & ~(size_t)255;
+  const size_t nb_b = ((size_t)n * 16 + 255) & ~(size_t)255;
+  void* io = nullptr;
+  r = get_ws(stream, 6, nb_t + 2 * nb_i + 2 * nb_b, &io);
+  if (r) return r;
+  char* c = (char*)io;
+  uint8_t* d_tags = (uint8_t*)c;
+  int32_t* d_match = (int32_t*)(c + nb_t);
+  int32_t* d_parent = (int32_t*)(c + nb_t + nb_i);
+  float* d_in = (float*)(c + nb_t + 2 * nb_i);
+  float* d_out = (float*)(c + nb_t + 2 * nb_i + nb_b);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, h_leaf_bbox, (size_t)n * 16, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D inputs");
+  r = paren_match(d_tags, n, d_match, d_parent, stream);
+  if (r) return r;
+  r = tree_bbox_matched(d_tags, d_in, d_match, d_parent, n, d_out, stream);
+  if (r) return r;
+  e = cudaMemcpyAsync(h_match, d_match, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_parent, d_parent, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_node_bbox, d_out, (size_t)n * 16, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H results");
+  return TB_OK;
+}
+
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }

@@ -40,7 +40,8 @@
 //      blend opens receive the union (in shared memory, or in node_bbox when
 //      the open lies in an earlier tile);
 //   H  coalesced copy-out (slice blend opens are left to their closing tile).
-// bbm_final    blend opens never closed (R4): union of everything after them.
+// bbm_final    blend opens never closed (R4): union of everything after them
+//              (the open's tile suffix ∪ the hierarchy over all later tiles).
 #include <algorithm>
 #include <climits>
 #include <cooperative_groups.h>
@@ -72,7 +73,6 @@ struct Params {
   float4* u[LV];         // u[0][T] = union of tile T's clipped leaves; u[k] over 32^k tiles
   int32_t* link;         // [ntiles] parent of the tile's bottom slice entry (-1: root / none)
   float4* tc;            // [ntiles] ctx(link)
-  float4* tsuf;          // [ntiles + 1] union of tiles [T, ntiles) (after bbm_main)
   float4* su;            // [n] union of the tile's clipped leaves after each slice entry
   int32_t* never;        // [n] blend opens never closed (R4)
   uint32_t* nnever;      // their count
@@ -201,18 +201,17 @@ __device__ __forceinline__ void publish_union(const Params& p, int T, float4 tu)
     __threadfence();
     st_release_u32(p.uf[0] + T, 1u);
   }
-  int idx = T;
+  int idx = T, m = p.ntiles;  // m = nodes at level k - 1
 #pragma unroll 1
   for (int k = 1; k < LV; k++) {
     const int g = idx >> 5;
+    const int kids = min(32, m - (g << 5));
     unsigned old = 0;
     if (lane == 0) old = atom_add_acqrel_u32(p.ucnt[k] + g, 1u);
     old = __shfl_sync(0xffffffffu, old, 0);
-    // a partial last group never completes: ranges reaching the end of the
-    // stream are served by tsuf
-    if (old != 31u) return;
+    if (old != (unsigned)(kids - 1)) return;
     const int c = (g << 5) + lane;
-    float4 v = wait_box(p.uf[k - 1] + c, p.u[k - 1] + c);
+    float4 v = lane < kids ? wait_box(p.uf[k - 1] + c, p.u[k - 1] + c) : bEMPTY();
     v = warp_unite_all(v);
     if (lane == 0) {
       p.u[k][g] = v;
@@ -220,6 +219,7 @@ __device__ __forceinline__ void publish_union(const Params& p, int T, float4 tu)
       st_release_u32(p.uf[k] + g, 1u);
     }
     idx = g;
+    m = (m + 31) >> 5;
   }
 }
 
@@ -337,6 +337,7 @@ struct Smem {
   } u;
   float4 wtu[NW];
   uint32_t bmk[NT];
+  uint32_t skip[NT];  // slice blend opens (their output belongs to the closing tile)
   int qkey[QCAP];     // earlier tiles To whose range union (To, T) this tile needs
   float4 qval[QCAP];
   int qn;
@@ -391,19 +392,33 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
     int mt[K], pr[K];
     load_i8(p.match, p.n, tstart, mt);
     load_i8(p.parent, p.n, tstart, pr);
+    // contexts of out-of-tile parents (lc in node_bbox ∩ TC of their tile):
+    // the last two distinct ones are fetched now, used in C/D
+    int xa = -1, xb = -1;
 #pragma unroll
-    for (int j = 0; j < K; j++) {
-      const int e = j * NT + tid;
-      s.val[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bINF();
+    for (int i = 0; i < K; i++) {
+      if ((((om | lm) >> i) & 1u) && pr[i] >= 0 && pr[i] < base && pr[i] != xa) {
+        xb = xa;
+        xa = pr[i];
+      }
     }
+    float4 ga = bINF(), gb = bINF();
+    if (xa >= 0) ga = isect(__ldcg(p.out + xa), __ldg(p.tc + xa / TILE));
+    if (xb >= 0) gb = isect(__ldcg(p.out + xb), __ldg(p.tc + xb / TILE));
+    // own boxes into own slots (each warp's 4 KB is one L1-resident span)
+#pragma unroll
+    for (int i = 0; i < K; i++)
+      s.val[slot(tid, i)] = (tstart + i < p.n) ? __ldg(p.boxes + tstart + i) : bINF();
     s.bmk[tid] = bm;
     if (tid < QCAP) s.qkey[tid] = -1;
     if (tid == 0) s.qn = 0;
-    uint32_t thr_un = 0;  // opens closed beyond this thread (or never)
+    uint32_t thr_un = 0, skipm = 0;  // opens closed beyond this thread (or never); slice blend opens
 #pragma unroll
-    for (int i = 0; i < K; i++)
+    for (int i = 0; i < K; i++) {
       if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= tstart + K)) thr_un |= 1u << i;
-    __syncthreads();
+      if (((bm >> i) & 1u) && (mt[i] < 0 || mt[i] >= tend)) skipm |= 1u << i;
+    }
+    s.skip[tid] = skipm;
 
     // ---- B. clips relative to the thread's external ancestor -----------------
     int curX = -1;
@@ -432,7 +447,7 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
       int ptr = -1;
       if (thr_un && curX >= 0) {
         if (curX < base) {
-          acc = isect(__ldcg(p.out + curX), __ldg(p.tc + curX / TILE));
+          acc = curX == xa ? ga : (curX == xb ? gb : isect(__ldcg(p.out + curX), __ldg(p.tc + curX / TILE)));
         } else {
           const int x = curX - (int)base;
           acc = s.val[slot_of(x)];
@@ -470,7 +485,7 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
             if (X != cx) {
               cx = X;
               if (X < base) {
-                g = isect(__ldcg(p.out + X), __ldg(p.tc + X / TILE));
+                g = X == xa ? ga : (X == xb ? gb : isect(__ldcg(p.out + X), __ldg(p.tc + X / TILE)));
               } else {
                 const int x = X - (int)base;
                 g = isect(s.val[slot_of(x)], s.tl[x / K]);
@@ -572,6 +587,7 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
           p.su[tstart + o] = unite(s.ua[slot(tid, o)], after);
           if ((nvm >> o) & 1u) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + o);
         }
+        __threadfence();
       }
     }
     if (ecm) {
@@ -600,7 +616,6 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
         }
       }
     }
-    __threadfence();
     __syncthreads();
     if (warp == 0) {
       float4 tu = lane < NW ? s.wtu[lane] : bEMPTY();
@@ -671,14 +686,7 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
     for (int j = 0; j < K; j++) {
       const int e = j * NT + tid;
       if (e < nvalid) {
-        const int t = e >> 3, i = e & 7;
-        // a slice blend open: blend, and not closed inside this tile
-        bool skip = false;
-        if ((s.bmk[t] >> i) & 1u) {
-          const int m = __ldg(p.match + base + e);
-          skip = m < 0 || m >= tend;
-        }
-        if (!skip) __stcs(p.out + base + e, s.val[slot_of(e)]);
+        if (!((s.skip[e >> 3] >> (e & 7)) & 1u)) __stcs(p.out + base + e, s.val[slot_of(e)]);
       }
     }
     BBM_TRACE(T, 7);
@@ -688,40 +696,16 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
 // ----------------------------------------------------------------------------
 // blend opens never closed (R4)
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) bbm_tsuf(Params p) {
-  // one CTA: tsuf[T] = ∪ u[0][T..ntiles-1], reverse scan in chunks of 1024
-  __shared__ float4 wb[32];
-  __shared__ float4 carry_s;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  float4 carry = bEMPTY();
-  if (tid == 0) p.tsuf[p.ntiles] = carry;
-  for (int hi = p.ntiles - 1; hi >= 0; hi -= 1024) {
-    const int T = hi - tid;
-    float4 v = T >= 0 ? __ldcg(p.u[0] + T) : bEMPTY();
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const float4 o = shfl_up_box(v, off);
-      if (lane >= off) v = unite(v, o);
-    }
-    if (lane == 31) wb[warp] = v;
-    __syncthreads();
-    float4 pre = carry;
-    for (int w = 0; w < warp; w++) pre = unite(pre, wb[w]);
-    v = unite(v, pre);
-    if (T >= 0) p.tsuf[T] = v;
-    if (tid == 1023) carry_s = v;
-    __syncthreads();
-    carry = carry_s;
-    __syncthreads();
-  }
-}
-
 __global__ void __launch_bounds__(256) bbm_final(Params p) {
+  // one warp per open: its tile's suffix after it ∪ every later tile
   const uint32_t cnt = __ldcg(p.nnever);
-  for (uint32_t q = blockIdx.x * 256 + threadIdx.x; q < cnt; q += gridDim.x * 256) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * 8;
+  for (uint32_t q = blockIdx.x * 8 + (threadIdx.x >> 5); q < cnt; q += nwarps) {
     const int o = __ldcg(p.never + q);
     const int To = o / TILE;
-    p.out[o] = unite(__ldcg(p.su + o), __ldcg(p.tsuf + To + 1));
+    const float4 after = To + 1 < p.ntiles ? range_union_tiles_warp(p, To + 1, p.ntiles - 1) : bEMPTY();
+    if (lane == 0) p.out[o] = unite(__ldcg(p.su + o), after);
   }
 }
 
@@ -732,7 +716,7 @@ struct Layout {
   int64_t ntiles;
   size_t zero_off, zero_bytes;
   size_t off_counter, off_nnever, off_uf[LV], off_ucnt[LV];
-  size_t off_u[LV], off_link, off_tc, off_tsuf, off_su, off_never, off_tcacc, off_tcptr, off_tcflag, bytes;
+  size_t off_u[LV], off_link, off_tc, off_su, off_never, off_tcacc, off_tcptr, off_tcflag, bytes;
   explicit Layout(int64_t n) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     ntiles = (n + TILE - 1) / TILE;
@@ -754,7 +738,6 @@ struct Layout {
     }
     off_link = o; o = al(o + 4 * (size_t)ntiles);
     off_tc = o; o = al(o + 16 * (size_t)ntiles);
-    off_tsuf = o; o = al(o + 16 * (size_t)(ntiles + 1));
     off_tcacc = o; o = al(o + 32 * (size_t)ntiles);
     off_tcptr = o; o = al(o + 8 * (size_t)ntiles);
     off_tcflag = o; o = al(o + 16);
@@ -818,7 +801,6 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
     p.ucnt[k] = (uint32_t*)(b + L.off_ucnt[k]);
     p.u[k] = (float4*)(b + L.off_u[k]);
   }
-  p.tsuf = (float4*)(b + L.off_tsuf);
   p.link = (int32_t*)(b + L.off_link);
   p.tc = (float4*)(b + L.off_tc);
   p.su = (float4*)(b + L.off_su);
@@ -841,7 +823,6 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   }
   const int nmain = (int)std::min<int64_t>(L.ntiles, (int64_t)bbm::main_blocks());
   TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<<<(unsigned)nmain, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
-  TB_LAUNCH(stream, "bbm_tsuf", (bbm::bbm_tsuf<<<1, 1024, 0, stream>>>(p)));
   TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
   return cudaGetLastError();
 }

@@ -193,6 +193,20 @@ def test_host_api():
     assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
 
 
+def test_pipeline_host_api():
+    tb = gpu()
+    t = scenegen.walk_tags(300_001, 5).pin_memory()
+    b = scenegen.boxes(t.numel(), 5, t).pin_memory()
+    m = torch.empty(t.numel(), dtype=torch.int32).pin_memory()
+    p = torch.empty_like(m).pin_memory()
+    out = torch.empty_like(b).pin_memory()
+    tb.paren_match_tree_bbox_host(t, b, m, p, out)
+    m_ref, p_ref = oracle.paren_match(t.numpy())
+    ref = oracle.tree_bbox(t.numpy(), b.numpy())
+    assert np.array_equal(m.numpy(), m_ref) and np.array_equal(p.numpy(), p_ref)
+    assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
+
+
 @pytest.mark.parametrize("nshards", [1, 2, 3, 5, 8])
 def test_virtual_shards_equal_oracle(nshards):
     """tree_bbox shard protocol (clip chain over chunks, exchanged unions and
