@@ -19,7 +19,7 @@
 //              over tiles resolved by pointer jumping (cooperative grid).  This
 //              replaces the paper's exclusive scan of per-partition top boxes
 //              (P:292).
-// bbm_main     persistent CTAs, tiles in order (atomic ticket):
+// bbm_main     one CTA per tile, no waiting on other tiles:
 //   B  per-thread walk over its 8 elements: the clip relative to the
 //      thread's external ancestor X (the parent of the current outermost
 //      in-thread group), in place in shared memory;
@@ -32,14 +32,16 @@
 //      thread's elements: in-thread nodes are finished, closes of outer nodes
 //      record the thread's prefix union, opens left open record the union of
 //      the thread's leaves after them;
-//   F  window unions over threads (warp shuffles), the tile's union published
-//      into a 32-ary hierarchy, and for every slice entry the union of the
-//      tile's leaves after it;
-//   G  closes of outer nodes: suffix union of the open's thread (or tile) ∪
-//      whole threads / whole tiles in between ∪ this thread's prefix (F4);
-//      blend opens receive the union (in shared memory, or in node_bbox when
-//      the open lies in an earlier tile);
+//   F  window unions over threads (warp shuffles); for every slice entry the
+//      union of the tile's leaves after it (su); the tile's union folded into
+//      a 32-ary hierarchy (last arriver computes the parent);
+//   G  closes of nodes opened in an earlier thread: suffix union of the open's
+//      thread ∪ whole threads in between ∪ this thread's prefix (F4); closes
+//      of nodes opened in an earlier tile: the tile prefix before the close,
+//      listed for bbm_close;
 //   H  coalesced copy-out (slice blend opens are left to their closing tile).
+// bbm_close    one warp per tile, its listed closes: prefix ∪ su(open) ∪ the
+//              whole tiles in between (hierarchy); blend opens receive it.
 // bbm_final    blend opens never closed (R4): union of everything after them
 //              (the open's tile suffix ∪ the hierarchy over all later tiles).
 #include <algorithm>
@@ -57,7 +59,6 @@ constexpr int K = 8;
 constexpr int TILE = NT * K;
 constexpr int NW = NT / 32;
 constexpr int LV = 5;    // 32-ary levels of the tile-union hierarchy (32^5 tiles > 2^31 / TILE)
-constexpr int QCAP = 32; // distinct earlier tiles whose range union a tile resolves cooperatively
 
 struct Params {
   const uint8_t* tags;
@@ -67,13 +68,13 @@ struct Params {
   float4* out;
   int64_t n;
   int ntiles;
-  uint32_t* counter;     // tile tickets of bbm_main
-  uint32_t* uf[LV];      // published flags of the union hierarchy
-  uint32_t* ucnt[LV];    // arrival counters (k >= 1)
+  uint32_t* ucnt[LV];    // arrival counters of the union hierarchy (k >= 1)
   float4* u[LV];         // u[0][T] = union of tile T's clipped leaves; u[k] over 32^k tiles
   int32_t* link;         // [ntiles] parent of the tile's bottom slice entry (-1: root / none)
   float4* tc;            // [ntiles] ctx(link)
   float4* su;            // [n] union of the tile's clipped leaves after each slice entry
+  int32_t* xc;           // [ntiles][TILE] closes of nodes opened in an earlier tile
+  int32_t* xcnt;         // [ntiles] their count
   int32_t* never;        // [n] blend opens never closed (R4)
   uint32_t* nnever;      // their count
   uint64_t* trace;       // optional per-tile phase timestamps (debug)
@@ -135,35 +136,28 @@ __device__ __forceinline__ void load_i8(const int32_t* a, int64_t n, int64_t tba
   }
 }
 
-__device__ __forceinline__ float4 wait_box(const uint32_t* flag, const float4* val) {
-  while (ld_acquire_u32(flag) == 0u) {
-  }
-  return __ldcg(val);
-}
-
-// Union over tiles [a, b] by one warp (a, b warp-uniform): per hierarchy
-// level, the lanes load the partial groups at both ends in parallel.
+// Union over tiles [a, b] by one warp (a, b warp-uniform; the hierarchy is
+// complete): per level the lanes load the partial groups at both ends.
 __device__ float4 range_union_tiles_warp(const Params& p, int a, int b) {
   const int lane = threadIdx.x & 31;
   float4 acc = bEMPTY();
   int k = 0;
   while (a <= b) {
-    const uint32_t* fl = p.uf[k];
     const float4* val = p.u[k];
     if ((a >> 5) == (b >> 5) || k == LV - 1) {
-      for (int i = a + lane; i <= b; i += 32) acc = unite(acc, wait_box(fl + i, val + i));
+      for (int i = a + lane; i <= b; i += 32) acc = unite(acc, __ldcg(val + i));
       break;
     }
     if (a & 31) {
       const int e = a | 31;
       const int i = a + lane;
-      if (i <= e) acc = unite(acc, wait_box(fl + i, val + i));
+      if (i <= e) acc = unite(acc, __ldcg(val + i));
       a = e + 1;
     }
     if ((b & 31) != 31) {
       const int s0 = b & ~31;
       const int i = s0 + lane;
-      if (i <= b) acc = unite(acc, wait_box(fl + i, val + i));
+      if (i <= b) acc = unite(acc, __ldcg(val + i));
       b = s0 - 1;
     }
     if (a > b) break;
@@ -174,32 +168,13 @@ __device__ float4 range_union_tiles_warp(const Params& p, int a, int b) {
   return warp_unite_all(acc);
 }
 
-// The same by one thread (fallback when a tile needs more than QCAP ranges).
-__device__ float4 range_union_tiles_seq(const Params& p, int a, int b) {
-  float4 acc = bEMPTY();
-  int k = 0;
-  while (a <= b) {
-    if (k == LV - 1 || (a >> 5) == (b >> 5)) {
-      for (int i = a; i <= b; i++) acc = unite(acc, wait_box(p.uf[k] + i, p.u[k] + i));
-      break;
-    }
-    for (; a & 31; a++) acc = unite(acc, wait_box(p.uf[k] + a, p.u[k] + a));
-    for (; (b & 31) != 31; b--) acc = unite(acc, wait_box(p.uf[k] + b, p.u[k] + b));
-    a >>= 5;
-    b = ((b + 1) >> 5) - 1;
-    k++;
-  }
-  return acc;
-}
-
-// Publish the tile's union and fold it into the hierarchy (one warp; the last
-// of 32 siblings to arrive publishes the parent).
+// Store the tile's union and fold it into the 32-ary hierarchy (one warp; the
+// last of a group's children to arrive computes the parent; nobody waits).
 __device__ __forceinline__ void publish_union(const Params& p, int T, float4 tu) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
     p.u[0][T] = tu;
     __threadfence();
-    st_release_u32(p.uf[0] + T, 1u);
   }
   int idx = T, m = p.ntiles;  // m = nodes at level k - 1
 #pragma unroll 1
@@ -211,12 +186,11 @@ __device__ __forceinline__ void publish_union(const Params& p, int T, float4 tu)
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != (unsigned)(kids - 1)) return;
     const int c = (g << 5) + lane;
-    float4 v = lane < kids ? wait_box(p.uf[k - 1] + c, p.u[k - 1] + c) : bEMPTY();
+    float4 v = lane < kids ? __ldcg(p.u[k - 1] + c) : bEMPTY();
     v = warp_unite_all(v);
     if (lane == 0) {
       p.u[k][g] = v;
       __threadfence();
-      st_release_u32(p.uf[k] + g, 1u);
     }
     idx = g;
     m = (m + 31) >> 5;
@@ -338,13 +312,8 @@ struct Smem {
   float4 wtu[NW];
   uint32_t bmk[NT];
   uint32_t skip[NT];  // slice blend opens (their output belongs to the closing tile)
-  int qkey[QCAP];     // earlier tiles To whose range union (To, T) this tile needs
-  float4 qval[QCAP];
-  int qn;
-  int tile;
+  int nx;             // closes of earlier tiles' nodes listed for bbm_close
 };
-
-__device__ __forceinline__ int qslot(int To) { return (int)(((uint32_t)To * 2654435761u) >> 27) & (QCAP - 1); }
 
 // element i of thread t lives at slot 8t + (i ^ (t & 7)): conflict-free both for
 // the coalesced copies and for the per-thread accesses
@@ -369,12 +338,8 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  while (true) {
-    if (tid == 0) s.tile = (int)atomicAdd(p.counter, 1u);
-    __syncthreads();
-    const int T = s.tile;
-    if (T >= p.ntiles) break;
+  {
+    const int T = blockIdx.x;
     const int64_t base = (int64_t)T * TILE;
     const int64_t tstart = base + (int64_t)tid * K;
     const int64_t tend = base + TILE;
@@ -410,8 +375,7 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
     for (int i = 0; i < K; i++)
       s.val[slot(tid, i)] = (tstart + i < p.n) ? __ldg(p.boxes + tstart + i) : bINF();
     s.bmk[tid] = bm;
-    if (tid < QCAP) s.qkey[tid] = -1;
-    if (tid == 0) s.qn = 0;
+    if (tid == 0) s.nx = 0;
     uint32_t thr_un = 0, skipm = 0;  // opens closed beyond this thread (or never); slice blend opens
 #pragma unroll
     for (int i = 0; i < K; i++) {
@@ -587,33 +551,6 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
           p.su[tstart + o] = unite(s.ua[slot(tid, o)], after);
           if ((nvm >> o) & 1u) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + o);
         }
-        __threadfence();
-      }
-    }
-    if (ecm) {
-      // register the earlier tiles this thread needs a range union to
-      int last = -1;
-      uint32_t q = ecm;
-#pragma unroll 1
-      while (q) {
-        const int i = __ffs(q) - 1;
-        q &= q - 1;
-        const int o = __float_as_int(s.val[slot(tid, i)].x);
-        if (o >= base) continue;
-        const int To = o / TILE;
-        if (To < T - 1 && To != last) {
-          last = To;
-          int h = qslot(To);
-#pragma unroll 1
-          for (int probe = 0; probe < QCAP; probe++) {
-            const int old = atomicCAS(&s.qkey[h], -1, To);
-            if (old == -1 || old == To) {
-              if (old == -1) atomicAdd(&s.qn, 1);
-              break;
-            }
-            h = (h + 1) & (QCAP - 1);
-          }
-        }
       }
     }
     __syncthreads();
@@ -624,20 +561,11 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
     }
     BBM_TRACE(T, 5);
 
-    // ---- G. closes of nodes opened in an earlier thread or tile -------------------------
-    if (s.qn) {  // range unions over whole earlier tiles, one warp per distinct range
-      for (int r = warp; r < QCAP; r += NW) {
-        const int To = s.qkey[r];
-        if (To >= 0) {
-          const float4 R = range_union_tiles_warp(p, To + 1, T - 1);
-          if (lane == 0) s.qval[r] = R;
-        }
-      }
-      __syncthreads();
-    }
+    // ---- G. closes of nodes opened in an earlier thread (finished here) or an
+    //      earlier tile (prefix union of this tile before the close stored,
+    //      the close listed for bbm_close) -----------------------------------------------
     if (ecm) {
-      int cto = -1;
-      float4 cR = bEMPTY(), pre_thr = bEMPTY();
+      float4 pre_thr = bEMPTY();
       bool have_pre = false;
       uint32_t q = ecm;
 #pragma unroll 1
@@ -653,32 +581,18 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
           U = unite(U, unite(s.ua[slot_of(x)], range_union_threads(s, V + 1, tid - 1)));
           if ((s.bmk[V] >> (x % K)) & 1u) s.val[slot_of(x)] = U;
         } else {
-          const int To = o / TILE;
-          const float4 su = wait_box(p.uf[0] + To, p.su + o);
-          if (To != cto) {
-            cto = To;
-            cR = bEMPTY();
-            if (To < T - 1) {
-              int h = qslot(To), probe = 0;
-#pragma unroll 1
-              while (probe < QCAP && s.qkey[h] != To) {
-                h = (h + 1) & (QCAP - 1);
-                probe++;
-              }
-              cR = probe < QCAP ? s.qval[h] : range_union_tiles_seq(p, To + 1, T - 1);
-            }
-          }
           if (!have_pre) {
             pre_thr = range_union_threads(s, 0, tid - 1);
             have_pre = true;
           }
-          U = unite(unite(U, su), unite(cR, pre_thr));
-          if (__ldg(p.tags + o) == 2) p.out[o] = U;
+          U = unite(U, pre_thr);
+          p.xc[(int64_t)T * TILE + atomicAdd(&s.nx, 1)] = (int)(tstart + i);
         }
         me = U;
       }
     }
     __syncthreads();
+    if (tid == 0) p.xcnt[T] = s.nx;
     BBM_TRACE(T, 6);
 
     // ---- H. copy-out (slice blend opens belong to their closing tile) ---------------------
@@ -690,6 +604,58 @@ __global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
       }
     }
     BBM_TRACE(T, 7);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// bbm_close: closes of nodes opened in an earlier tile (one warp per tile):
+// union = prefix of the close's tile (stored by bbm_main) ∪ the open's tile
+// suffix after it ∪ the whole tiles in between (F4); blend opens get it too.
+// Lanes sharing the open's tile share one warp-cooperative range union.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bbm_close(Params p) {
+  const int lane = threadIdx.x & 31;
+  const int T = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (T >= p.ntiles) return;
+  const int cnt = __ldg(p.xcnt + T);
+  int cto = -1;  // warp cache: the last range resolved (deep chains repeat one open tile)
+  float4 cR = bEMPTY();
+  for (int j0 = 0; j0 < cnt; j0 += 32) {
+    const int j = j0 + lane;
+    const bool valid = j < cnt;
+    int c = 0, o = 0, To = 0;
+    float4 P = bEMPTY(), su = bEMPTY();
+    uint8_t kind = 0;
+    if (valid) {
+      c = __ldg(p.xc + (int64_t)T * TILE + j);
+      o = __ldg(p.match + c);
+      To = o / TILE;
+      P = __ldcg(p.out + c);
+      su = __ldcg(p.su + o);
+      kind = __ldg(p.tags + o);
+    }
+    float4 R = bEMPTY();
+    bool pending = valid && To < T - 1;
+    if (pending && To == cto) {
+      R = cR;
+      pending = false;
+    }
+    uint32_t mask;
+    while ((mask = __ballot_sync(0xffffffffu, pending)) != 0u) {
+      const int tl = __shfl_sync(0xffffffffu, To, __ffs(mask) - 1);
+      const float4 Rl = range_union_tiles_warp(p, tl + 1, T - 1);
+      if (pending && To == tl) {
+        R = Rl;
+        pending = false;
+      }
+      cto = tl;
+      cR = Rl;
+    }
+    if (valid) {
+      const float4 U = unite(unite(P, su), R);
+      p.out[c] = U;
+      if (kind == 2) p.out[o] = U;  // blend open
+    }
   }
 }
 
@@ -715,18 +681,16 @@ __global__ void __launch_bounds__(256) bbm_final(Params p) {
 struct Layout {
   int64_t ntiles;
   size_t zero_off, zero_bytes;
-  size_t off_counter, off_nnever, off_uf[LV], off_ucnt[LV];
-  size_t off_u[LV], off_link, off_tc, off_su, off_never, off_tcacc, off_tcptr, off_tcflag, bytes;
+  size_t off_nnever, off_ucnt[LV];
+  size_t off_u[LV], off_link, off_tc, off_su, off_xc, off_xcnt, off_never, off_tcacc, off_tcptr, off_tcflag, bytes;
   explicit Layout(int64_t n) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     ntiles = (n + TILE - 1) / TILE;
     size_t o = 0;
     zero_off = o;
-    off_counter = o; o = al(o + 4);
     off_nnever = o; o = al(o + 4);
     int64_t m = ntiles;
     for (int k = 0; k < LV; k++) {
-      off_uf[k] = o; o = al(o + 4 * (size_t)m);
       off_ucnt[k] = o; o = al(o + 4 * (size_t)m);
       m = (m + 31) / 32;
     }
@@ -738,26 +702,23 @@ struct Layout {
     }
     off_link = o; o = al(o + 4 * (size_t)ntiles);
     off_tc = o; o = al(o + 16 * (size_t)ntiles);
+    off_xcnt = o; o = al(o + 4 * (size_t)ntiles);
     off_tcacc = o; o = al(o + 32 * (size_t)ntiles);
     off_tcptr = o; o = al(o + 8 * (size_t)ntiles);
     off_tcflag = o; o = al(o + 16);
     off_su = o; o = al(o + 16 * (size_t)n);
+    off_xc = o; o = al(o + 4 * (size_t)ntiles * TILE);
     off_never = o; o = al(o + 4 * (size_t)n);
     bytes = o;
   }
 };
 
-int main_blocks() {
-  static int nb = 0;
-  if (nb == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+void main_setup() {
+  static bool done = false;
+  if (!done) {
     cudaFuncSetAttribute(bbm_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbm_main, NT, sizeof(Smem));
-    nb = sms * (occ > 0 ? occ : 1);
+    done = true;
   }
-  return nb;
 }
 
 int tc_blocks() {
@@ -794,10 +755,8 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   p.out = reinterpret_cast<float4*>(node_bbox);
   p.n = n;
   p.ntiles = (int)L.ntiles;
-  p.counter = (uint32_t*)(b + L.off_counter);
   p.nnever = (uint32_t*)(b + L.off_nnever);
   for (int k = 0; k < bbm::LV; k++) {
-    p.uf[k] = (uint32_t*)(b + L.off_uf[k]);
     p.ucnt[k] = (uint32_t*)(b + L.off_ucnt[k]);
     p.u[k] = (float4*)(b + L.off_u[k]);
   }
@@ -805,6 +764,8 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   p.tc = (float4*)(b + L.off_tc);
   p.su = (float4*)(b + L.off_su);
   p.never = (int32_t*)(b + L.off_never);
+  p.xc = (int32_t*)(b + L.off_xc);
+  p.xcnt = (int32_t*)(b + L.off_xcnt);
   p.trace = trace;
   cudaError_t err = cudaMemsetAsync(b + L.zero_off, 0, L.zero_bytes, stream);
   if (err != cudaSuccess) return err;
@@ -821,8 +782,10 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
     prof_end(stream, tok);
     if (err != cudaSuccess) return err;
   }
-  const int nmain = (int)std::min<int64_t>(L.ntiles, (int64_t)bbm::main_blocks());
-  TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<<<(unsigned)nmain, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
+  bbm::main_setup();
+  TB_LAUNCH(stream, "bbm_main",
+            (bbm::bbm_main<<<(unsigned)L.ntiles, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<(unsigned)((L.ntiles + 7) / 8), 256, 0, stream>>>(p)));
   TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
   return cudaGetLastError();
 }
