@@ -33,14 +33,14 @@
 //      record the thread's prefix union, opens left open record the union of
 //      the thread's leaves after them;
 //   F  window unions over threads (warp shuffles); for every slice entry the
-//      union of the tile's leaves after it (su); the tile's union folded into
-//      a 32-ary hierarchy (last arriver computes the parent);
+//      union of the tile's leaves after it (su); the tile's union (a 32-ary
+//      hierarchy over tile unions is built by bbm_hier afterwards);
 //   G  closes of nodes opened in an earlier thread: suffix union of the open's
 //      thread ∪ whole threads in between ∪ this thread's prefix (F4); closes
 //      of nodes opened in an earlier tile: the tile prefix before the close,
 //      listed for bbm_close;
-//   H  coalesced copy-out (slice blend opens are left to their closing tile).
-// bbm_close    one warp per tile, its listed closes: prefix ∪ su(open) ∪ the
+//   H  coalesced copy-out.
+// bbm_close    one CTA per tile (warps take 32 listed closes at a time): prefix ∪ su(open) ∪ the
 //              whole tiles in between (hierarchy); blend opens receive it.
 // bbm_final    blend opens never closed (R4): union of everything after them
 //              (the open's tile suffix ∪ the hierarchy over all later tiles).
@@ -68,7 +68,6 @@ struct Params {
   float4* out;
   int64_t n;
   int ntiles;
-  uint32_t* ucnt[LV];    // arrival counters of the union hierarchy (k >= 1)
   float4* u[LV];         // u[0][T] = union of tile T's clipped leaves; u[k] over 32^k tiles
   int32_t* link;         // [ntiles] parent of the tile's bottom slice entry (-1: root / none)
   float4* tc;            // [ntiles] ctx(link)
@@ -166,35 +165,6 @@ __device__ float4 range_union_tiles_warp(const Params& p, int a, int b) {
     k++;
   }
   return warp_unite_all(acc);
-}
-
-// Store the tile's union and fold it into the 32-ary hierarchy (one warp; the
-// last of a group's children to arrive computes the parent; nobody waits).
-__device__ __forceinline__ void publish_union(const Params& p, int T, float4 tu) {
-  const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-    p.u[0][T] = tu;
-    __threadfence();
-  }
-  int idx = T, m = p.ntiles;  // m = nodes at level k - 1
-#pragma unroll 1
-  for (int k = 1; k < LV; k++) {
-    const int g = idx >> 5;
-    const int kids = min(32, m - (g << 5));
-    unsigned old = 0;
-    if (lane == 0) old = atom_add_acqrel_u32(p.ucnt[k] + g, 1u);
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old != (unsigned)(kids - 1)) return;
-    const int c = (g << 5) + lane;
-    float4 v = lane < kids ? __ldcg(p.u[k - 1] + c) : bEMPTY();
-    v = warp_unite_all(v);
-    if (lane == 0) {
-      p.u[k][g] = v;
-      __threadfence();
-    }
-    idx = g;
-    m = (m + 31) >> 5;
-  }
 }
 
 // ----------------------------------------------------------------------------
@@ -297,22 +267,22 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
 // ----------------------------------------------------------------------------
 struct Smem {
   float4 val[TILE];  // boxes -> clips -> outputs (swizzled slots)
-  float4 ua[TILE];   // union accumulators of opens; prefix unions of outer closes
-  float4 tl[NT];     // ctx of each thread's link
+  int xo[TILE];      // the open of each outer close (phase G)
   union {
-    struct {
+    struct {         // C: pointer jumping over threads
       float4 acc[2][NT];
       int ptr[2][NT];
     } pj;
-    struct {
-      float4 win[6][NT];  // union of thread unions over lanes [lane - 2^k + 1, lane] (clipped to the warp)
+    float4 tl[NT];   // D: ctx of each thread's link
+    struct {         // F-G
+      float4 win[5][NT];  // union of thread unions over lanes [lane - 2^k + 1, lane] (clipped to the warp)
       float4 suf[NT];     // inclusive suffix within the warp
     } un;
   } u;
   float4 wtu[NW];
-  uint32_t bmk[NT];
-  uint32_t skip[NT];  // slice blend opens (their output belongs to the closing tile)
-  int nx;             // closes of earlier tiles' nodes listed for bbm_close
+  uint32_t bmk[NT];  // blend opens of each thread
+  uint32_t lmk[NT];  // leaves of each thread
+  int nx;            // closes of earlier tiles' nodes listed for bbm_close
 };
 
 // element i of thread t lives at slot 8t + (i ^ (t & 7)): conflict-free both for
@@ -320,307 +290,318 @@ struct Smem {
 __device__ __forceinline__ int slot(int t, int i) { return (t << 3) | (i ^ (t & 7)); }
 __device__ __forceinline__ int slot_of(int e) { return slot(e >> 3, e & 7); }
 
+// union of the clipped leaves of thread V after its position j
+__device__ __forceinline__ float4 thread_suffix(const Smem& s, int V, int j) {
+  float4 u = bEMPTY();
+  uint32_t m = s.lmk[V] & ~((2u << j) - 1u);
+  while (m) {
+    const int i = __ffs(m) - 1;
+    m &= m - 1;
+    u = unite(u, s.val[slot(V, i)]);
+  }
+  return u;
+}
+
+// union of whole threads [a, b] inside one warp
+__device__ __forceinline__ float4 warp_range(const Smem& s, int a, int b) {
+  const int len = b - a + 1;
+  if (len == 32) return s.wtu[a >> 5];
+  const int k = 31 - __clz(len);
+  return unite(s.u.un.win[k][b], s.u.un.win[k][a + (1 << k) - 1]);
+}
+
 // union of the clipped leaves of whole threads [a, b]
 __device__ __forceinline__ float4 range_union_threads(const Smem& s, int a, int b) {
   if (a > b) return bEMPTY();
   const int wa = a >> 5, wb = b >> 5;
-  if (wa == wb) {
-    const int k = 31 - __clz(b - a + 1);
-    return unite(s.u.un.win[k][b], s.u.un.win[k][a + (1 << k) - 1]);
-  }
-  float4 v = unite(s.u.un.suf[a], s.u.un.win[5][b]);
+  if (wa == wb) return warp_range(s, a, b);
+  float4 v = unite(s.u.un.suf[a], warp_range(s, wb << 5, b));
 #pragma unroll 1
   for (int w = wa + 1; w < wb; w++) v = unite(v, s.wtu[w]);
   return v;
 }
 
-__global__ void __launch_bounds__(NT, 4) bbm_main(Params p) {
+__global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {
-    const int T = blockIdx.x;
-    const int64_t base = (int64_t)T * TILE;
-    const int64_t tstart = base + (int64_t)tid * K;
-    const int64_t tend = base + TILE;
-    const int nvalid = (int)(p.n - base < TILE ? p.n - base : TILE);
-    BBM_TRACE(T, 0);
+  const int T = blockIdx.x;
+  const int64_t base = (int64_t)T * TILE;
+  const int64_t tstart = base + (int64_t)tid * K;
+  const int64_t tend = base + TILE;
+  const int nvalid = (int)(p.n - base < TILE ? p.n - base : TILE);
+  BBM_TRACE(T, 0);
 
-    // ---- A. load -----------------------------------------------------------
-    uint32_t om, cm, bm;
-    classify8(load_tags8(p.tags, p.n, tstart), om, cm, bm);
-    uint32_t lm = ~om & ~cm & 0xffu;
-    {
-      const int64_t rem = p.n - tstart;
-      if (rem < K) lm &= rem <= 0 ? 0u : ((1u << rem) - 1u);
-    }
-    int mt[K], pr[K];
-    load_i8(p.match, p.n, tstart, mt);
-    load_i8(p.parent, p.n, tstart, pr);
-    // contexts of out-of-tile parents (lc in node_bbox ∩ TC of their tile):
-    // the last two distinct ones are fetched now, used in C/D
-    int xa = -1, xb = -1;
+  // ---- A. load -------------------------------------------------------------
+  uint32_t om, cm, bm;
+  classify8(load_tags8(p.tags, p.n, tstart), om, cm, bm);
+  uint32_t lm = ~om & ~cm & 0xffu;
+  {
+    const int64_t rem = p.n - tstart;
+    if (rem < K) lm &= rem <= 0 ? 0u : ((1u << rem) - 1u);
+  }
+  int mt[K], pr[K];
+  load_i8(p.match, p.n, tstart, mt);
+  load_i8(p.parent, p.n, tstart, pr);
+  // contexts of out-of-tile parents (lc in node_bbox ∩ TC of their tile):
+  // the last two distinct ones are fetched now, used in C/D
+  int xa = -1, xb = -1;
 #pragma unroll
-    for (int i = 0; i < K; i++) {
-      if ((((om | lm) >> i) & 1u) && pr[i] >= 0 && pr[i] < base && pr[i] != xa) {
-        xb = xa;
-        xa = pr[i];
+  for (int i = 0; i < K; i++) {
+    if ((((om | lm) >> i) & 1u) && pr[i] >= 0 && pr[i] < base && pr[i] != xa) {
+      xb = xa;
+      xa = pr[i];
+    }
+  }
+  float4 ga = bINF(), gb = bINF();
+  if (xa >= 0) ga = isect(__ldcg(p.out + xa), __ldg(p.tc + xa / TILE));
+  if (xb >= 0) gb = isect(__ldcg(p.out + xb), __ldg(p.tc + xb / TILE));
+  // own boxes into own slots (each warp's 4 KB is one L1-resident span)
+#pragma unroll
+  for (int i = 0; i < K; i++)
+    s.val[slot(tid, i)] = (tstart + i < p.n) ? __ldg(p.boxes + tstart + i) : bINF();
+  s.bmk[tid] = bm;
+  s.lmk[tid] = lm;
+  if (tid == 0) s.nx = 0;
+  uint32_t thr_un = 0;  // opens closed beyond this thread (or never)
+#pragma unroll
+  for (int i = 0; i < K; i++)
+    if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= tstart + K)) thr_un |= 1u << i;
+
+  // ---- B. clips relative to the thread's external ancestor -------------------
+  int curX = -1;
+  uint32_t pend = 0;
+#pragma unroll
+  for (int i = 0; i < K; i++) {
+    if (((om | lm) >> i) & 1u) {
+      const int par = pr[i];
+      float4 b = bINF();
+      if (par < tstart) {
+        curX = par;
+      } else {
+        b = s.val[slot(tid, par - (int)tstart)];
+      }
+      float4& me = s.val[slot(tid, i)];
+      me = ((bm >> i) & 1u) ? b : isect(me, b);
+      if (curX >= 0) pend |= 1u << i;
+    }
+  }
+  __syncthreads();
+  BBM_TRACE(T, 1);
+
+  // ---- C. ctx of each thread's link (pointer jumping over threads) ------------
+  {
+    float4 acc = bINF();
+    int ptr = -1;
+    if (thr_un && curX >= 0) {
+      if (curX < base) {
+        acc = curX == xa ? ga : (curX == xb ? gb : isect(__ldcg(p.out + curX), __ldg(p.tc + curX / TILE)));
+      } else {
+        const int x = curX - (int)base;
+        acc = s.val[slot_of(x)];
+        ptr = x / K;
       }
     }
-    float4 ga = bINF(), gb = bINF();
-    if (xa >= 0) ga = isect(__ldcg(p.out + xa), __ldg(p.tc + xa / TILE));
-    if (xb >= 0) gb = isect(__ldcg(p.out + xb), __ldg(p.tc + xb / TILE));
-    // own boxes into own slots (each warp's 4 KB is one L1-resident span)
-#pragma unroll
-    for (int i = 0; i < K; i++)
-      s.val[slot(tid, i)] = (tstart + i < p.n) ? __ldg(p.boxes + tstart + i) : bINF();
-    s.bmk[tid] = bm;
-    if (tid == 0) s.nx = 0;
-    uint32_t thr_un = 0, skipm = 0;  // opens closed beyond this thread (or never); slice blend opens
-#pragma unroll
-    for (int i = 0; i < K; i++) {
-      if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= tstart + K)) thr_un |= 1u << i;
-      if (((bm >> i) & 1u) && (mt[i] < 0 || mt[i] >= tend)) skipm |= 1u << i;
+    int cb = 0;
+    s.u.pj.acc[0][tid] = acc;
+    s.u.pj.ptr[0][tid] = ptr;
+    int any = __syncthreads_or(ptr >= 0);
+    while (any) {
+      if (ptr >= 0) {
+        acc = isect(acc, s.u.pj.acc[cb][ptr]);
+        ptr = s.u.pj.ptr[cb][ptr];
+      }
+      s.u.pj.acc[cb ^ 1][tid] = acc;
+      s.u.pj.ptr[cb ^ 1][tid] = ptr;
+      cb ^= 1;
+      any = __syncthreads_or(ptr >= 0);
     }
-    s.skip[tid] = skipm;
+    s.u.tl[tid] = acc;  // every read of pj happened before the last barrier
+  }
+  __syncthreads();
+  BBM_TRACE(T, 2);
 
-    // ---- B. clips relative to the thread's external ancestor -----------------
-    int curX = -1;
-    uint32_t pend = 0;
+  // ---- D. finish pending clips: rel ∩ ctx(X) ------------------------------------
+  if (pend) {
+    int X = -1, cx = INT_MIN;
+    float4 g = bINF();
 #pragma unroll
     for (int i = 0; i < K; i++) {
       if (((om | lm) >> i) & 1u) {
-        const int par = pr[i];
-        float4 b = bINF();
-        if (par < tstart) {
-          curX = par;
-        } else {
-          b = s.val[slot(tid, par - (int)tstart)];
-        }
-        float4& me = s.val[slot(tid, i)];
-        me = ((bm >> i) & 1u) ? b : isect(me, b);
-        if (curX >= 0) pend |= 1u << i;
-      }
-    }
-    __syncthreads();
-    BBM_TRACE(T, 1);
-
-    // ---- C. ctx of each thread's link (pointer jumping over threads) ----------
-    {
-      float4 acc = bINF();
-      int ptr = -1;
-      if (thr_un && curX >= 0) {
-        if (curX < base) {
-          acc = curX == xa ? ga : (curX == xb ? gb : isect(__ldcg(p.out + curX), __ldg(p.tc + curX / TILE)));
-        } else {
-          const int x = curX - (int)base;
-          acc = s.val[slot_of(x)];
-          ptr = x / K;
-        }
-      }
-      int cb = 0;
-      s.u.pj.acc[0][tid] = acc;
-      s.u.pj.ptr[0][tid] = ptr;
-      int any = __syncthreads_or(ptr >= 0);
-      while (any) {
-        if (ptr >= 0) {
-          acc = isect(acc, s.u.pj.acc[cb][ptr]);
-          ptr = s.u.pj.ptr[cb][ptr];
-        }
-        s.u.pj.acc[cb ^ 1][tid] = acc;
-        s.u.pj.ptr[cb ^ 1][tid] = ptr;
-        cb ^= 1;
-        any = __syncthreads_or(ptr >= 0);
-      }
-      s.tl[tid] = acc;
-    }
-    __syncthreads();
-    BBM_TRACE(T, 2);
-
-    // ---- D. finish pending clips: rel ∩ ctx(X) ----------------------------------
-    if (pend) {
-      int X = -1, cx = INT_MIN;
-      float4 g = bINF();
-#pragma unroll
-      for (int i = 0; i < K; i++) {
-        if (((om | lm) >> i) & 1u) {
-          if (pr[i] < tstart) X = pr[i];
-          if ((pend >> i) & 1u) {
-            if (X != cx) {
-              cx = X;
-              if (X < base) {
-                g = X == xa ? ga : (X == xb ? gb : isect(__ldcg(p.out + X), __ldg(p.tc + X / TILE)));
-              } else {
-                const int x = X - (int)base;
-                g = isect(s.val[slot_of(x)], s.tl[x / K]);
-              }
+        if (pr[i] < tstart) X = pr[i];
+        if ((pend >> i) & 1u) {
+          if (X != cx) {
+            cx = X;
+            if (X < base) {
+              g = X == xa ? ga : (X == xb ? gb : isect(__ldcg(p.out + X), __ldg(p.tc + X / TILE)));
+            } else {
+              const int x = X - (int)base;
+              g = isect(s.val[slot_of(x)], s.u.tl[x / K]);
             }
-            float4& me = s.val[slot(tid, i)];
-            me = isect(me, g);
           }
+          float4& me = s.val[slot(tid, i)];
+          me = isect(me, g);
         }
       }
     }
-    __syncthreads();
-    BBM_TRACE(T, 3);
+  }
+  __syncthreads();
+  BBM_TRACE(T, 3);
 
-    // ---- E. union walk ------------------------------------------------------------
-    float4 PT = bEMPTY();  // union of this thread's clipped leaves so far
-    uint32_t S = 0, ecm = 0;
+  // ---- E. unions inside the thread ---------------------------------------------------
+  // A node opened and closed in this thread gets the union of the leaves between
+  // (the slots hold final clips now); a close of an outer node records the
+  // thread's prefix union (completed in G).
+  float4 PT = bEMPTY();  // union of this thread's clipped leaves so far
+  uint32_t ecm = 0;
+#pragma unroll
+  for (int i = 0; i < K; i++) {
+    const uint32_t bit = 1u << i;
+    if (lm & bit) {
+      PT = unite(PT, s.val[slot(tid, i)]);
+    } else if (cm & bit) {
+      const int m = mt[i];
+      if (m >= tstart) {
+        const int o = m - (int)tstart;
+        float4 U = bEMPTY();
+        uint32_t lb = lm & (bit - 1u) & ~((2u << o) - 1u);  // leaves strictly between
+        while (lb) {
+          const int j = __ffs(lb) - 1;
+          lb &= lb - 1;
+          U = unite(U, s.val[slot(tid, j)]);
+        }
+        s.val[slot(tid, i)] = U;
+        if ((bm >> o) & 1u) s.val[slot(tid, o)] = U;
+      } else if (m >= 0) {
+        s.val[slot(tid, i)] = PT;
+        s.xo[slot(tid, i)] = m;
+        ecm |= bit;
+      } else {
+        s.val[slot(tid, i)] = bEMPTY();  // R3
+      }
+    }
+  }
+  BBM_TRACE(T, 4);
+
+  // ---- F. unions over threads; slice suffix unions; tile union ----------------------
+  {
+    float4 w = PT, suf = PT;
+    s.u.un.win[0][tid] = w;
+#pragma unroll
+    for (int k = 1; k <= 5; k++) {
+      const int off = 1 << (k - 1);
+      const float4 a = shfl_up_box(w, off);
+      if (lane >= off) w = unite(w, a);
+      if (k < 5) s.u.un.win[k][tid] = w;
+      const float4 b = make_float4(__shfl_down_sync(0xffffffffu, suf.x, off),
+                                   __shfl_down_sync(0xffffffffu, suf.y, off),
+                                   __shfl_down_sync(0xffffffffu, suf.z, off),
+                                   __shfl_down_sync(0xffffffffu, suf.w, off));
+      if (lane + off < 32) suf = unite(suf, b);
+    }
+    s.u.un.suf[tid] = suf;
+    if (lane == 31) s.wtu[warp] = w;
+  }
+  __syncthreads();
+  {
+    uint32_t q = 0, nvm = 0;  // slice entries of this thread; blend opens never closed
 #pragma unroll
     for (int i = 0; i < K; i++) {
-      const uint32_t bit = 1u << i;
-      if (lm & bit) {
-        const float4 v = s.val[slot(tid, i)];
-        PT = unite(PT, v);
-        if (S) {
-          float4& a = s.ua[slot(tid, 31 - __clz(S))];
-          a = unite(a, v);
-        }
-      } else if (om & bit) {
-        S |= bit;
-        s.ua[slot(tid, i)] = bEMPTY();
-      } else if ((cm & bit) && i < nvalid - tid * K) {
-        const int m = mt[i];
-        if (m >= tstart) {
-          const int o = m - (int)tstart;  // the top of S
-          const float4 U = s.ua[slot(tid, o)];
-          s.val[slot(tid, i)] = U;
-          if ((bm >> o) & 1u) s.val[slot(tid, o)] = U;
-          S ^= 1u << o;
-          if (S) {
-            float4& a = s.ua[slot(tid, 31 - __clz(S))];
-            a = unite(a, U);
-          }
-        } else if (m >= 0) {
-          s.ua[slot(tid, i)] = PT;
-          s.val[slot(tid, i)].x = __int_as_float(m);  // the open, until G writes the union here
-          ecm |= bit;
-        } else {
-          s.val[slot(tid, i)] = bEMPTY();  // R3
-        }
-      }
+      if (((thr_un >> i) & 1u) && (mt[i] < 0 || mt[i] >= tend)) q |= 1u << i;
+      if (((bm >> i) & 1u) && mt[i] < 0) nvm |= 1u << i;
     }
-    {
-      // suffix unions of the opens left open: union of the thread's leaves after them
-      float4 R = bEMPTY();
-      uint32_t q = S;
-      while (q) {
-        const int o = 31 - __clz(q);
-        q ^= 1u << o;
-        float4& a = s.ua[slot(tid, o)];
-        R = unite(R, a);
-        a = R;
-      }
-    }
-    BBM_TRACE(T, 4);
-
-    // ---- F. unions over threads; publication ------------------------------------------
-    {
-      float4 w = PT, suf = PT;
-      s.u.un.win[0][tid] = w;
-#pragma unroll
-      for (int k = 1; k <= 5; k++) {
-        const int off = 1 << (k - 1);
-        const float4 a = shfl_up_box(w, off);
-        if (lane >= off) w = unite(w, a);
-        s.u.un.win[k][tid] = w;
-        const float4 b = make_float4(__shfl_down_sync(0xffffffffu, suf.x, off),
-                                     __shfl_down_sync(0xffffffffu, suf.y, off),
-                                     __shfl_down_sync(0xffffffffu, suf.z, off),
-                                     __shfl_down_sync(0xffffffffu, suf.w, off));
-        if (lane + off < 32) suf = unite(suf, b);
-      }
-      s.u.un.suf[tid] = suf;
-      if (lane == 31) s.wtu[warp] = w;
-    }
-    __syncthreads();
-    {
-      uint32_t q = 0, nvm = 0;  // slice entries of this thread; blend opens never closed
-#pragma unroll
-      for (int i = 0; i < K; i++) {
-        if (((thr_un >> i) & 1u) && (mt[i] < 0 || mt[i] >= tend)) q |= 1u << i;
-        if (((bm >> i) & 1u) && mt[i] < 0) nvm |= 1u << i;
-      }
-      if (q) {
-        const float4 after = range_union_threads(s, tid + 1, NT - 1);
-#pragma unroll 1
-        while (q) {
-          const int o = __ffs(q) - 1;
-          q &= q - 1;
-          p.su[tstart + o] = unite(s.ua[slot(tid, o)], after);
-          if ((nvm >> o) & 1u) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + o);
-        }
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      float4 tu = lane < NW ? s.wtu[lane] : bEMPTY();
-      tu = warp_unite_all(tu);
-      publish_union(p, T, tu);
-    }
-    BBM_TRACE(T, 5);
-
-    // ---- G. closes of nodes opened in an earlier thread (finished here) or an
-    //      earlier tile (prefix union of this tile before the close stored,
-    //      the close listed for bbm_close) -----------------------------------------------
-    if (ecm) {
-      float4 pre_thr = bEMPTY();
-      bool have_pre = false;
-      uint32_t q = ecm;
+    if (q) {
+      const float4 after = range_union_threads(s, tid + 1, NT - 1);
 #pragma unroll 1
       while (q) {
-        const int i = __ffs(q) - 1;
+        const int o = __ffs(q) - 1;
         q &= q - 1;
-        float4& me = s.val[slot(tid, i)];
-        const int o = __float_as_int(me.x);
-        float4 U = s.ua[slot(tid, i)];  // this thread's prefix before the close
-        if (o >= base) {
-          const int x = o - (int)base;
-          const int V = x / K;
-          U = unite(U, unite(s.ua[slot_of(x)], range_union_threads(s, V + 1, tid - 1)));
-          if ((s.bmk[V] >> (x % K)) & 1u) s.val[slot_of(x)] = U;
-        } else {
-          if (!have_pre) {
-            pre_thr = range_union_threads(s, 0, tid - 1);
-            have_pre = true;
-          }
-          U = unite(U, pre_thr);
-          p.xc[(int64_t)T * TILE + atomicAdd(&s.nx, 1)] = (int)(tstart + i);
-        }
-        me = U;
+        p.su[tstart + o] = unite(thread_suffix(s, tid, o), after);
+        if ((nvm >> o) & 1u) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + o);
       }
     }
-    __syncthreads();
-    if (tid == 0) p.xcnt[T] = s.nx;
-    BBM_TRACE(T, 6);
-
-    // ---- H. copy-out (slice blend opens belong to their closing tile) ---------------------
-#pragma unroll
-    for (int j = 0; j < K; j++) {
-      const int e = j * NT + tid;
-      if (e < nvalid) {
-        if (!((s.skip[e >> 3] >> (e & 7)) & 1u)) __stcs(p.out + base + e, s.val[slot_of(e)]);
-      }
-    }
-    BBM_TRACE(T, 7);
   }
+  if (tid == 0) {
+    float4 tu = s.wtu[0];
+#pragma unroll
+    for (int w = 1; w < NW; w++) tu = unite(tu, s.wtu[w]);
+    p.u[0][T] = tu;
+  }
+  BBM_TRACE(T, 5);
+
+  // ---- G. closes of nodes opened in an earlier thread (finished here) or an
+  //      earlier tile (the tile's prefix before the close stored, the close
+  //      listed for bbm_close) --------------------------------------------------------
+  if (ecm) {
+    float4 pre_thr = bEMPTY();
+    bool have_pre = false;
+    uint32_t q = ecm;
+#pragma unroll 1
+    while (q) {
+      const int i = __ffs(q) - 1;
+      q &= q - 1;
+      float4& me = s.val[slot(tid, i)];
+      const int o = s.xo[slot(tid, i)];
+      float4 U = me;  // this thread's prefix before the close
+      if (o >= base) {
+        const int x = o - (int)base;
+        const int V = x / K;
+        U = unite(U, unite(thread_suffix(s, V, x % K), range_union_threads(s, V + 1, tid - 1)));
+        if ((s.bmk[V] >> (x % K)) & 1u) s.val[slot_of(x)] = U;
+      } else {
+        if (!have_pre) {
+          pre_thr = range_union_threads(s, 0, tid - 1);
+          have_pre = true;
+        }
+        U = unite(U, pre_thr);
+        p.xc[(int64_t)T * TILE + atomicAdd(&s.nx, 1)] = (int)(tstart + i);
+      }
+      me = U;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) p.xcnt[T] = s.nx;
+  BBM_TRACE(T, 6);
+
+  // ---- H. copy-out.  A slice blend open is stored with its true context: later
+  //      tiles read ctx = node_bbox[o] ∩ TC(tile of o), the same whether they see
+  //      lc (bbm_reduce) or the context (∩ is idempotent per component); its
+  //      union replaces it in bbm_close / bbm_final. ------------------------------------
+#pragma unroll
+  for (int j = 0; j < K; j++) {
+    const int e = j * NT + tid;
+    if (e < nvalid) __stcs(p.out + base + e, s.val[slot_of(e)]);
+  }
+  BBM_TRACE(T, 7);
 }
 
 // ----------------------------------------------------------------------------
-// bbm_close: closes of nodes opened in an earlier tile (one warp per tile):
+// bbm_hier: level k of the 32-ary hierarchy of tile unions from level k - 1
+// (one warp per group; launched once per level)
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bbm_hier(Params p, int k, int m /* nodes at level k - 1 */) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if ((g << 5) >= m) return;
+  const int c = (g << 5) + lane;
+  float4 v = c < m ? __ldcg(p.u[k - 1] + c) : bEMPTY();
+  v = warp_unite_all(v);
+  if (lane == 0) p.u[k][g] = v;
+}
+
+// ----------------------------------------------------------------------------
+// bbm_close: closes of nodes opened in an earlier tile (one CTA per tile):
 // union = prefix of the close's tile (stored by bbm_main) ∪ the open's tile
 // suffix after it ∪ the whole tiles in between (F4); blend opens get it too.
 // Lanes sharing the open's tile share one warp-cooperative range union.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) bbm_close(Params p) {
-  const int lane = threadIdx.x & 31;
-  const int T = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (T >= p.ntiles) return;
+__global__ void __launch_bounds__(128) bbm_close(Params p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int T = blockIdx.x;
   const int cnt = __ldg(p.xcnt + T);
   int cto = -1;  // warp cache: the last range resolved (deep chains repeat one open tile)
   float4 cR = bEMPTY();
-  for (int j0 = 0; j0 < cnt; j0 += 32) {
+  for (int j0 = warp * 32; j0 < cnt; j0 += 128) {
     const int j = j0 + lane;
     const bool valid = j < cnt;
     int c = 0, o = 0, To = 0;
@@ -681,7 +662,7 @@ __global__ void __launch_bounds__(256) bbm_final(Params p) {
 struct Layout {
   int64_t ntiles;
   size_t zero_off, zero_bytes;
-  size_t off_nnever, off_ucnt[LV];
+  size_t off_nnever;
   size_t off_u[LV], off_link, off_tc, off_su, off_xc, off_xcnt, off_never, off_tcacc, off_tcptr, off_tcflag, bytes;
   explicit Layout(int64_t n) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -689,13 +670,8 @@ struct Layout {
     size_t o = 0;
     zero_off = o;
     off_nnever = o; o = al(o + 4);
-    int64_t m = ntiles;
-    for (int k = 0; k < LV; k++) {
-      off_ucnt[k] = o; o = al(o + 4 * (size_t)m);
-      m = (m + 31) / 32;
-    }
     zero_bytes = o - zero_off;
-    m = ntiles;
+    int64_t m = ntiles;
     for (int k = 0; k < LV; k++) {
       off_u[k] = o; o = al(o + 16 * (size_t)m);
       m = (m + 31) / 32;
@@ -757,7 +733,6 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   p.ntiles = (int)L.ntiles;
   p.nnever = (uint32_t*)(b + L.off_nnever);
   for (int k = 0; k < bbm::LV; k++) {
-    p.ucnt[k] = (uint32_t*)(b + L.off_ucnt[k]);
     p.u[k] = (float4*)(b + L.off_u[k]);
   }
   p.link = (int32_t*)(b + L.off_link);
@@ -785,7 +760,16 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   bbm::main_setup();
   TB_LAUNCH(stream, "bbm_main",
             (bbm::bbm_main<<<(unsigned)L.ntiles, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
-  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<(unsigned)((L.ntiles + 7) / 8), 256, 0, stream>>>(p)));
+  {
+    int64_t m = L.ntiles;
+    for (int k = 1; k < bbm::LV && m > 1; k++) {
+      const int64_t groups = (m + 31) / 32;
+      TB_LAUNCH(stream, "bbm_hier",
+                (bbm::bbm_hier<<<(unsigned)((groups + 7) / 8), 256, 0, stream>>>(p, k, (int)m)));
+      m = groups;
+    }
+  }
+  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<(unsigned)L.ntiles, 128, 0, stream>>>(p)));
   TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
   return cudaGetLastError();
 }
