@@ -54,27 +54,55 @@ struct Params {
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) pm_reduce(Params p) {
   __shared__ Bic wtot[NW];
+  __shared__ uint8_t bic4[256];  // Bic of 4 elements: index = open nibble | close nibble << 4; a | b << 4
   const int tid = threadIdx.x;
   const int T = blockIdx.x;
   const int64_t base = (int64_t)T * TILE;
   const int64_t tbase = base + (int64_t)tid * K;
   const bool full = base + TILE <= p.n;
-
-  const Walk16 w = walk16(load_tags16(p.tags, p.n, tbase, full));
-  const int a_t = __popc(w.ucm), b_t = __popc(w.S);
+  static_assert(NT >= 256, "bic4 is filled one entry per thread");
+  {
+    Bic v{0, 0};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const Bic e{(tid >> (4 + j)) & 1, (tid >> j) & 1};  // close -> (1, 0), open -> (0, 1)
+      v = bic_combine(v, e);
+    }
+    bic4[tid] = (uint8_t)(v.a | (v.b << 4));
+  }
+  uint32_t om, cm;
+  classify16(load_tags16(p.tags, p.n, tbase, full), om, cm);
+  __syncthreads();
+  Bic tb{0, 0};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t e = bic4[((om >> (4 * q)) & 15u) | (((cm >> (4 * q)) & 15u) << 4)];
+    tb = bic_combine(tb, Bic{(int)(e & 15u), (int)(e >> 4)});
+  }
+  const int a_t = tb.a, b_t = tb.b;
   Bic ex, sx, tot;
   block_bic_scans<NW>(Bic{a_t, b_t}, wtot, ex, sx, tot, true);
   if (tid == 0) p.ctrl.agg[T] = make_int2(tot.a, tot.b);  // the tile scan turns these into heights
   // slice: this thread's unmatched opens that survive to the tile end sit at
-  // relative heights l_t + k, slice position l_t + k + a_T.
+  // relative heights l_t + k, slice position l_t + k + a_T (the bottom s_t of
+  // the thread's stack; only those threads walk their elements).
   const int l_t = ex.b - ex.a - a_t;
   const int s_t = max(b_t - sx.a, 0);
-  uint32_t m = w.S;
-  for (int k = 0; k < s_t; k++) {
-    const int bit = __ffs(m) - 1;
-    m &= m - 1;
-    p.slice[base + (l_t + k + tot.a)] = (int)(p.offset + tbase + bit);
-    p.match[tbase + bit] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
+  if (s_t > 0) {
+    uint32_t S = 0;
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      const uint32_t bit = 1u << i;
+      if (om & bit) S |= bit;
+      else if ((cm & bit) && S) S ^= 1u << (31 - __clz(S));
+    }
+    uint32_t m = S;
+    for (int k = 0; k < s_t; k++) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      p.slice[base + (l_t + k + tot.a)] = (int)(p.offset + tbase + bit);
+      p.match[tbase + bit] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
+    }
   }
 }
 

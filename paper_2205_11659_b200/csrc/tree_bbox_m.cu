@@ -170,55 +170,63 @@ __device__ float4 range_union_tiles_warp(const Params& p, int a, int b) {
 // ----------------------------------------------------------------------------
 // bbm_reduce: slice clips (lc) in place, tile links
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) bbm_reduce(Params p) {
-  __shared__ float4 wbox[NW];
-  __shared__ int wmin[NW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int T = blockIdx.x;
-  const int64_t base = (int64_t)T * TILE, tbase = base + (int64_t)tid * K;
+// One warp per tile, 32 consecutive elements per lane (10 independent 16-byte
+// loads in flight per lane, warp-level scans only).
+constexpr int RK = TILE / 32;  // elements per lane in bbm_reduce
+__global__ void __launch_bounds__(128) bbm_reduce(Params p) {
+  const int lane = threadIdx.x & 31;
+  const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (T >= p.ntiles) return;
+  const int64_t base = (int64_t)T * TILE, lbase = base + (int64_t)lane * RK;
   const int64_t tend = base + TILE;
-  uint32_t om, cm, bm;
-  classify8(load_tags8(p.tags, p.n, tbase), om, cm, bm);
-  int mt[K];
-  load_i8(p.match, p.n, tbase, mt);
-  uint32_t sm = 0;  // slice entries (opens closed beyond the tile or never)
+  uint32_t sm = 0, bmask = 0;  // slice entries (opens closed beyond the tile or never); blend opens
+  if (lbase + RK <= p.n) {
+    const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase));
+    const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase) + 1);
+    const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+    int4 mv[RK / 4];
 #pragma unroll
-  for (int i = 0; i < K; i++)
-    if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= tend)) sm |= 1u << i;
-  // thread aggregate of the slice clips, then exclusive ∩-scan over threads
+    for (int q = 0; q < RK / 4; q++) mv[q] = __ldg(reinterpret_cast<const int4*>(p.match + lbase) + q);
+#pragma unroll
+    for (int q = 0; q < RK / 4; q++) {
+      uint32_t om, cm, bm;
+      classify8(make_uint2(tw[q], 0u), om, cm, bm);
+      const int ms[4] = {mv[q].x, mv[q].y, mv[q].z, mv[q].w};
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (((om >> j) & 1u) && (ms[j] < 0 || ms[j] >= tend)) sm |= 1u << (4 * q + j);
+      bmask |= (bm & 15u) << (4 * q);
+    }
+  } else {
+    for (int i = 0; i < RK; i++) {
+      const int64_t g = lbase + i;
+      if (g >= p.n) break;
+      const uint8_t t = p.tags[g];
+      if (t == 1 || t == 2) {
+        const int m = __ldg(p.match + g);
+        if (m < 0 || m >= tend) sm |= 1u << i;
+        if (t == 2) bmask |= 1u << i;
+      }
+    }
+  }
+  // lane aggregate of the slice clips, exclusive ∩-scan over lanes
   float4 agg = bINF();
-#pragma unroll
-  for (int i = 0; i < K; i++)
-    if (((sm & ~bm) >> i) & 1u) agg = isect(agg, __ldg(p.boxes + tbase + i));
+  for (uint32_t q = sm & ~bmask; q; q &= q - 1) agg = isect(agg, __ldg(p.boxes + lbase + __ffs(q) - 1));
   float4 x = agg;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const float4 o = shfl_up_box(x, off);
     if (lane >= off) x = isect(x, o);
   }
-  const int first = sm ? (tid * K + __ffs(sm) - 1) : INT_MAX;
-  const int wf = __reduce_min_sync(0xffffffffu, first);
-  if (lane == 31) wbox[warp] = x;
-  if (lane == 0) wmin[warp] = wf;
-  __syncthreads();
-  float4 pre = bINF();
-  int tf = INT_MAX;
-#pragma unroll
-  for (int w = 0; w < NW; w++) {
-    if (w < warp) pre = isect(pre, wbox[w]);
-    tf = min(tf, wmin[w]);
+  float4 acc = shfl_up_box(x, 1);
+  if (lane == 0) acc = bINF();
+  for (uint32_t q = sm; q; q &= q - 1) {
+    const int i = __ffs(q) - 1;
+    if (!((bmask >> i) & 1u)) acc = isect(acc, __ldg(p.boxes + lbase + i));
+    p.out[lbase + i] = acc;
   }
-  float4 e = shfl_up_box(x, 1);
-  if (lane == 0) e = bINF();
-  float4 acc = isect(pre, e);
-#pragma unroll
-  for (int i = 0; i < K; i++) {
-    if ((sm >> i) & 1u) {
-      if (!((bm >> i) & 1u)) acc = isect(acc, __ldg(p.boxes + tbase + i));
-      p.out[tbase + i] = acc;
-    }
-  }
-  if (tid == 0) p.link[T] = (tf == INT_MAX) ? -1 : __ldg(p.parent + base + tf);
+  const int first = __reduce_min_sync(0xffffffffu, sm ? (lane * RK + __ffs(sm) - 1) : INT_MAX);
+  if (lane == 0) p.link[T] = (first == INT_MAX) ? -1 : __ldg(p.parent + base + first);
 }
 
 // ----------------------------------------------------------------------------
@@ -744,7 +752,7 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   p.trace = trace;
   cudaError_t err = cudaMemsetAsync(b + L.zero_off, 0, L.zero_bytes, stream);
   if (err != cudaSuccess) return err;
-  TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<(unsigned)L.ntiles, bbm::NT, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p)));
   {
     float4* acc2 = (float4*)(b + L.off_tcacc);
     int* ptr2 = (int*)(b + L.off_tcptr);
