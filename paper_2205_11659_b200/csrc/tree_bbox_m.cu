@@ -364,10 +364,12 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
   float4 ga = bINF(), gb = bINF();
   if (xa >= 0) ga = isect(__ldcg(p.out + xa), __ldg(p.tc + xa / TILE));
   if (xb >= 0) gb = isect(__ldcg(p.out + xb), __ldg(p.tc + xb / TILE));
-  // own boxes into own slots (each warp's 4 KB is one L1-resident span)
+  // boxes into the slots, coalesced (512 contiguous bytes per warp instruction)
 #pragma unroll
-  for (int i = 0; i < K; i++)
-    s.val[slot(tid, i)] = (tstart + i < p.n) ? __ldg(p.boxes + tstart + i) : bINF();
+  for (int j = 0; j < K; j++) {
+    const int e = j * NT + tid;
+    s.val[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bINF();
+  }
   s.bmk[tid] = bm;
   s.lmk[tid] = lm;
   if (tid == 0) s.nx = 0;
@@ -375,6 +377,7 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
 #pragma unroll
   for (int i = 0; i < K; i++)
     if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= tstart + K)) thr_un |= 1u << i;
+  __syncthreads();
 
   // ---- B. clips relative to the thread's external ancestor -------------------
   int curX = -1;
