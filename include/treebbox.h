@@ -146,7 +146,9 @@ int paren_match_host(const uint8_t *h_tags, int64_t n, int32_t *h_match, int32_t
 int tree_bbox_host(const uint8_t *h_tags, const float *h_leaf_bbox, int64_t n, float *h_node_bbox,
                    void *stream);
 /* The whole hot path from host buffers: copy tags and boxes in, paren_match,
- * tree_bbox_matched on its outputs, copy match, parent and node_bbox out. */
+ * tree_bbox_matched on its outputs, copy match, parent and node_bbox out.  The
+ * box upload and the match/parent download run on library side streams,
+ * overlapped with the kernels (pass pinned host memory for real overlap). */
 int paren_match_tree_bbox_host(const uint8_t *h_tags, const float *h_leaf_bbox, int64_t n, int32_t *h_match,
                                int32_t *h_parent, float *h_node_bbox, void *stream);
 

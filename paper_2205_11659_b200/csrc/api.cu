@@ -78,6 +78,35 @@ int get_ws(void* stream, int slot, size_t need, void** out) {
   return TB_OK;
 }
 
+// Side streams / events of the host pipeline, one set per device (never freed).
+struct AuxStreams {
+  cudaStream_t in = nullptr, out = nullptr;
+  cudaEvent_t start = nullptr, in_done = nullptr, pm_done = nullptr, out_done = nullptr;
+};
+std::map<int, AuxStreams> g_aux;
+
+int get_aux(AuxStreams** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_mu);
+  AuxStreams& a = g_aux[dev];
+  if (!a.in) {
+    e = cudaStreamCreateWithFlags(&a.in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a.out, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.start, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.in_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.pm_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.out_done, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      a = AuxStreams{};
+      return cuda_fail(e, "side streams");
+    }
+  }
+  *out = &a;
+  return TB_OK;
+}
+
 int pm_checks(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent) {
   int r = check_n(n);
   if (r) return r;
@@ -299,17 +328,32 @@ int paren_match_tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, 
   int32_t* d_parent = (int32_t*)(c + nb_t + nb_i);
   float* d_in = (float*)(c + nb_t + 2 * nb_i);
   float* d_out = (float*)(c + nb_t + 2 * nb_i + nb_b);
+  // Copies overlap the kernels and each other (PCIe is full duplex): the boxes
+  // go in on a side stream while paren_match runs, match/parent come out on a
+  // second side stream while the boxes are still going in.
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, h_leaf_bbox, (size_t)n * 16, cudaMemcpyHostToDevice, s);
+  AuxStreams* ax = nullptr;
+  r = get_aux(&ax);
+  if (r) return r;
+  cudaError_t e = cudaEventRecord(ax->start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->in, ax->start, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, h_leaf_bbox, (size_t)n * 16, cudaMemcpyHostToDevice, ax->in);
+  if (e == cudaSuccess) e = cudaEventRecord(ax->in_done, ax->in);
   if (e != cudaSuccess) return cuda_fail(e, "H2D inputs");
   r = paren_match(d_tags, n, d_match, d_parent, stream);
   if (r) return r;
+  e = cudaEventRecord(ax->pm_done, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->out, ax->pm_done, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_match, d_match, (size_t)n * 4, cudaMemcpyDeviceToHost, ax->out);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_parent, d_parent, (size_t)n * 4, cudaMemcpyDeviceToHost, ax->out);
+  if (e == cudaSuccess) e = cudaEventRecord(ax->out_done, ax->out);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ax->in_done, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H match/parent");
   r = tree_bbox_matched(d_tags, d_in, d_match, d_parent, n, d_out, stream);
   if (r) return r;
-  e = cudaMemcpyAsync(h_match, d_match, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(h_parent, d_parent, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(h_node_bbox, d_out, (size_t)n * 16, cudaMemcpyDeviceToHost, s);
+  e = cudaMemcpyAsync(h_node_bbox, d_out, (size_t)n * 16, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ax->out_done, 0);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "D2H results");
   return TB_OK;
