@@ -275,7 +275,6 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
 // ----------------------------------------------------------------------------
 struct Smem {
   float4 val[TILE];  // boxes -> clips -> outputs (swizzled slots)
-  int xo[TILE];      // the open of each outer close (phase G)
   union {
     struct {         // C: pointer jumping over threads
       float4 acc[2][NT];
@@ -288,6 +287,7 @@ struct Smem {
     } un;
   } u;
   float4 wtu[NW];
+  float4 wmid[NW][NW];  // union of the warps strictly between two warps
   uint32_t bmk[NT];  // blend opens of each thread
   uint32_t lmk[NT];  // leaves of each thread
   int nx;            // closes of earlier tiles' nodes listed for bbm_close
@@ -298,35 +298,18 @@ struct Smem {
 __device__ __forceinline__ int slot(int t, int i) { return (t << 3) | (i ^ (t & 7)); }
 __device__ __forceinline__ int slot_of(int e) { return slot(e >> 3, e & 7); }
 
-// union of the clipped leaves of thread V after its position j
-__device__ __forceinline__ float4 thread_suffix(const Smem& s, int V, int j) {
-  float4 u = bEMPTY();
-  uint32_t m = s.lmk[V] & ~((2u << j) - 1u);
-  while (m) {
-    const int i = __ffs(m) - 1;
-    m &= m - 1;
-    u = unite(u, s.val[slot(V, i)]);
-  }
-  return u;
-}
-
-// union of whole threads [a, b] inside one warp
-__device__ __forceinline__ float4 warp_range(const Smem& s, int a, int b) {
-  const int len = b - a + 1;
-  if (len == 32) return s.wtu[a >> 5];
-  const int k = 31 - __clz(len);
-  return unite(s.u.un.win[k][b], s.u.un.win[k][a + (1 << k) - 1]);
-}
-
-// union of the clipped leaves of whole threads [a, b]
+// union of the clipped leaves of whole threads [a, b]: the suffix of a's warp,
+// the warps strictly between (table), the window part of b's warp ending at
+// b — selects rather than branches, since every lane asks a different range
 __device__ __forceinline__ float4 range_union_threads(const Smem& s, int a, int b) {
   if (a > b) return bEMPTY();
   const int wa = a >> 5, wb = b >> 5;
-  if (wa == wb) return warp_range(s, a, b);
-  float4 v = unite(s.u.un.suf[a], warp_range(s, wb << 5, b));
-#pragma unroll 1
-  for (int w = wa + 1; w < wb; w++) v = unite(v, s.wtu[w]);
-  return v;
+  const int a2 = (wa == wb) ? a : (wb << 5);  // start of the part inside b's warp
+  const int len = b - a2 + 1;
+  const int k = min(31 - __clz(len), 4);
+  const float4 right = (len == 32) ? s.wtu[wb] : unite(s.u.un.win[k][b], s.u.un.win[k][a2 + (1 << k) - 1]);
+  if (wa == wb) return right;
+  return unite(unite(s.u.un.suf[a], right), s.wmid[wa][wb]);
 }
 
 __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
@@ -484,9 +467,8 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
         s.val[slot(tid, i)] = U;
         if ((bm >> o) & 1u) s.val[slot(tid, o)] = U;
       } else if (m >= 0) {
-        s.val[slot(tid, i)] = PT;
-        s.xo[slot(tid, i)] = m;
-        ecm |= bit;
+        s.val[slot(tid, i)] = PT;  // completed by the open's thread (F) or in G
+        if (m < base) ecm |= bit;
       } else {
         s.val[slot(tid, i)] = bEMPTY();  // R3
       }
@@ -514,24 +496,50 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
     if (lane == 31) s.wtu[warp] = w;
   }
   __syncthreads();
+  BBM_TRACE(T, 8);
+  if (tid < NW * NW) {
+    const int x = tid / NW, y = tid % NW;
+    float4 m = bEMPTY();
+    for (int w = x + 1; w < y; w++) m = unite(m, s.wtu[w]);
+    s.wmid[x][y] = m;
+  }
+  __syncthreads();
+  BBM_TRACE(T, 9);
   {
-    uint32_t q = 0, nvm = 0;  // slice entries of this thread; blend opens never closed
+    // Opens left open at this thread's end, from the top down with R = union of
+    // this thread's leaves after them: a slice entry publishes su = R ∪ the
+    // threads after this one; an open closed by a later thread of the tile
+    // finishes that close: R ∪ the threads in between ∪ the closer's prefix.
+    uint32_t qt = 0, qi = 0, nvm = 0;
 #pragma unroll
     for (int i = 0; i < K; i++) {
-      if (((thr_un >> i) & 1u) && (mt[i] < 0 || mt[i] >= tend)) q |= 1u << i;
+      if ((thr_un >> i) & 1u) {
+        if (mt[i] < 0 || mt[i] >= tend) qt |= 1u << i;
+        else qi |= 1u << i;
+      }
       if (((bm >> i) & 1u) && mt[i] < 0) nvm |= 1u << i;
     }
-    if (q) {
-      const float4 after = range_union_threads(s, tid + 1, NT - 1);
-#pragma unroll 1
-      while (q) {
-        const int o = __ffs(q) - 1;
-        q &= q - 1;
-        p.su[tstart + o] = unite(thread_suffix(s, tid, o), after);
-        if ((nvm >> o) & 1u) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + o);
+    if (qt | qi) {
+      const float4 after = qt ? range_union_threads(s, tid + 1, NT - 1) : bEMPTY();
+      float4 R = bEMPTY();
+#pragma unroll
+      for (int i = K - 1; i >= 0; i--) {
+        const uint32_t bit = 1u << i;
+        if (qt & bit) {
+          p.su[tstart + i] = unite(R, after);
+          if (nvm & bit) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + i);
+        } else if (qi & bit) {
+          const int c = mt[i] - (int)base;
+          float4& cv = s.val[slot_of(c)];
+          const float4 U = unite(unite(R, range_union_threads(s, tid + 1, c / K - 1)), cv);
+          cv = U;
+          if ((bm >> i) & 1u) s.val[slot(tid, i)] = U;
+        }
+        if ((lm & bit) && ((qt | qi) & (bit - 1u))) R = unite(R, s.val[slot(tid, i)]);
       }
     }
   }
+  BBM_TRACE(T, 10);
   if (tid == 0) {
     float4 tu = s.wtu[0];
 #pragma unroll
@@ -544,30 +552,15 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
   //      earlier tile (the tile's prefix before the close stored, the close
   //      listed for bbm_close) --------------------------------------------------------
   if (ecm) {
-    float4 pre_thr = bEMPTY();
-    bool have_pre = false;
+    const float4 pre = range_union_threads(s, 0, tid - 1);
     uint32_t q = ecm;
 #pragma unroll 1
     while (q) {
       const int i = __ffs(q) - 1;
       q &= q - 1;
       float4& me = s.val[slot(tid, i)];
-      const int o = s.xo[slot(tid, i)];
-      float4 U = me;  // this thread's prefix before the close
-      if (o >= base) {
-        const int x = o - (int)base;
-        const int V = x / K;
-        U = unite(U, unite(thread_suffix(s, V, x % K), range_union_threads(s, V + 1, tid - 1)));
-        if ((s.bmk[V] >> (x % K)) & 1u) s.val[slot_of(x)] = U;
-      } else {
-        if (!have_pre) {
-          pre_thr = range_union_threads(s, 0, tid - 1);
-          have_pre = true;
-        }
-        U = unite(U, pre_thr);
-        p.xc[(int64_t)T * TILE + atomicAdd(&s.nx, 1)] = (int)(tstart + i);
-      }
-      me = U;
+      me = unite(me, pre);
+      p.xc[(int64_t)T * TILE + atomicAdd(&s.nx, 1)] = (int)(tstart + i);
     }
   }
   __syncthreads();

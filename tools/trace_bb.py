@@ -21,5 +21,10 @@ for cfg in sys.argv[1:] or ["C5"]:
     for a in range(7):
         d = (t[:, a + 1] - t[:, a]) / 1e3
         print(f"  {names[a]:>10} -> {names[a+1]:<10} med {np.median(d):7.2f} p90 {np.percentile(d,90):7.2f} max {d.max():8.2f} us")
+    full = tr.view(nt, 16).cpu().numpy().astype(np.float64)
+    for a, b, nm in ((4, 8, "F windows+bar"), (8, 9, "F wmid+bar"), (9, 10, "F backward"), (10, 5, "F tile union")):
+        if full[:, b].max() > 0:
+            d = (full[:, b] - full[:, a]) / 1e3
+            print(f"  {nm:>24} med {np.median(d):7.2f} p90 {np.percentile(d,90):7.2f} us")
     d = (t[:, 7] - t[:, 0]) / 1e3
     print(f"  tile total med {np.median(d):.2f} p90 {np.percentile(d,90):.2f}")
