@@ -170,43 +170,81 @@ __device__ float4 range_union_tiles_warp(const Params& p, int a, int b) {
 // ----------------------------------------------------------------------------
 // bbm_reduce: slice clips (lc) in place, tile links
 // ----------------------------------------------------------------------------
-// One warp per tile, 32 consecutive elements per lane (10 independent 16-byte
-// loads in flight per lane, warp-level scans only).
+// One warp per tile, 32 consecutive elements per lane, tags only: the lane's
+// Bic from a 4-element table, warp scans give how many of the lane's unmatched
+// opens survive to the tile end (the bottom ones of its stack, §3-§4
+// P:96-138); only lanes owning survivors walk their elements.
 constexpr int RK = TILE / 32;  // elements per lane in bbm_reduce
 __global__ void __launch_bounds__(128) bbm_reduce(Params p) {
+  __shared__ uint8_t bic4[256];  // Bic of 4 elements: index = open nibble | close nibble << 4; a | b << 4
   const int lane = threadIdx.x & 31;
+  {
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      const int idx = t + 128 * r;
+      Bic v{0, 0};
+#pragma unroll
+      for (int j = 0; j < 4; j++) v = bic_combine(v, Bic{(idx >> (4 + j)) & 1, (idx >> j) & 1});
+      bic4[idx] = (uint8_t)(v.a | (v.b << 4));
+    }
+  }
+  __syncthreads();
   const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (T >= p.ntiles) return;
   const int64_t base = (int64_t)T * TILE, lbase = base + (int64_t)lane * RK;
-  const int64_t tend = base + TILE;
-  uint32_t sm = 0, bmask = 0;  // slice entries (opens closed beyond the tile or never); blend opens
+  uint32_t om = 0, cm = 0, bmask = 0;  // opens, closes, blend opens of the lane's 32 elements
   if (lbase + RK <= p.n) {
     const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase));
     const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase) + 1);
     const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-    int4 mv[RK / 4];
 #pragma unroll
-    for (int q = 0; q < RK / 4; q++) mv[q] = __ldg(reinterpret_cast<const int4*>(p.match + lbase) + q);
-#pragma unroll
-    for (int q = 0; q < RK / 4; q++) {
-      uint32_t om, cm, bm;
-      classify8(make_uint2(tw[q], 0u), om, cm, bm);
-      const int ms[4] = {mv[q].x, mv[q].y, mv[q].z, mv[q].w};
-#pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (((om >> j) & 1u) && (ms[j] < 0 || ms[j] >= tend)) sm |= 1u << (4 * q + j);
-      bmask |= (bm & 15u) << (4 * q);
+    for (int q = 0; q < 8; q++) {
+      const uint32_t x = tw[q];
+      const uint32_t bl = __vcmpeq4(x, 0x02020202u);
+      om |= byte_mask4(__vcmpeq4(x, 0x01010101u) | bl) << (4 * q);
+      cm |= byte_mask4(__vcmpeq4(x, 0x03030303u)) << (4 * q);
+      bmask |= byte_mask4(bl) << (4 * q);
     }
   } else {
     for (int i = 0; i < RK; i++) {
       const int64_t g = lbase + i;
       if (g >= p.n) break;
       const uint8_t t = p.tags[g];
-      if (t == 1 || t == 2) {
-        const int m = __ldg(p.match + g);
-        if (m < 0 || m >= tend) sm |= 1u << i;
-        if (t == 2) bmask |= 1u << i;
-      }
+      if (t == 1 || t == 2) om |= 1u << i;
+      if (t == 2) bmask |= 1u << i;
+      if (t == 3) cm |= 1u << i;
+    }
+  }
+  Bic lb{0, 0};
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    const uint32_t e = bic4[((om >> (4 * q)) & 15u) | (((cm >> (4 * q)) & 15u) << 4)];
+    lb = bic_combine(lb, Bic{(int)(e & 15u), (int)(e >> 4)});
+  }
+  // exclusive suffix over lanes: Bic of the tile's elements after this lane
+  Bic suf = lb;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Bic o{__shfl_down_sync(0xffffffffu, suf.a, off), __shfl_down_sync(0xffffffffu, suf.b, off)};
+    if (lane + off < 32) suf = bic_combine(suf, o);
+  }
+  Bic sx{__shfl_down_sync(0xffffffffu, suf.a, 1), __shfl_down_sync(0xffffffffu, suf.b, 1)};
+  if (lane == 31) sx = Bic{0, 0};
+  const int s_l = max(lb.b - sx.a, 0);  // survivors: the bottom s_l opens of the lane's stack
+  uint32_t sm = 0;
+  if (s_l > 0) {
+    uint32_t S = 0;
+#pragma unroll
+    for (int i = 0; i < RK; i++) {
+      const uint32_t bit = 1u << i;
+      if (om & bit) S |= bit;
+      else if ((cm & bit) && S) S ^= 1u << (31 - __clz(S));
+    }
+    for (int k = 0; k < s_l; k++) {
+      const uint32_t low = S & (~S + 1u);
+      sm |= low;
+      S ^= low;
     }
   }
   // lane aggregate of the slice clips, exclusive ∩-scan over lanes
