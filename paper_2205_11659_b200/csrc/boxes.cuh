@@ -24,10 +24,6 @@ __device__ __forceinline__ float4 unite(float4 a, float4 b) {
   return make_float4(fminf(a.x, b.x), fminf(a.y, b.y), fmaxf(a.z, b.z), fmaxf(a.w, b.w));
 }
 
-__device__ __forceinline__ float4 shfl_box(float4 v, int src) {
-  return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
-                     __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
-}
 __device__ __forceinline__ float4 shfl_up_box(float4 v, int d) {
   return make_float4(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d),
                      __shfl_up_sync(0xffffffffu, v.z, d), __shfl_up_sync(0xffffffffu, v.w, d));
@@ -35,11 +31,6 @@ __device__ __forceinline__ float4 shfl_up_box(float4 v, int d) {
 __device__ __forceinline__ float4 shfl_xor_box(float4 v, int m) {
   return make_float4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
                      __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
-}
-__device__ __forceinline__ float4 warp_isect_all(float4 v) {
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) v = isect(v, shfl_xor_box(v, m));
-  return v;
 }
 __device__ __forceinline__ float4 warp_unite_all(float4 v) {
 #pragma unroll

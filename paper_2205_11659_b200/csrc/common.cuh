@@ -17,51 +17,14 @@ __device__ __forceinline__ Bic bic_combine(Bic x, Bic y) {
   return Bic{x.a + y.a - m, x.b + y.b - m};
 }
 
-// Packed look-back descriptor: [63:62] flag, [61:31] a, [30:0] b.
-enum : uint32_t { DESC_NONE = 0, DESC_AGG = 1, DESC_INC = 2 };
-__device__ __forceinline__ uint64_t desc_pack(uint32_t flag, Bic v) {
-  return ((uint64_t)flag << 62) | ((uint64_t)(uint32_t)v.a << 31) | (uint64_t)(uint32_t)v.b;
-}
-__device__ __forceinline__ uint32_t desc_flag(uint64_t d) { return (uint32_t)(d >> 62); }
-__device__ __forceinline__ Bic desc_val(uint64_t d) {
-  return Bic{(int)((d >> 31) & 0x7fffffffu), (int)(d & 0x7fffffffu)};
-}
-
 // ---------------------------------------------------------------------------
-// Memory-model helpers (PTX, gpu scope).  Cross-CTA data is published with
-// st.release after the payload is written and read with ld.acquire; payload
-// reads after an acquire use ld.relaxed.gpu / .cg so no stale L1 line is hit.
+// Memory-model helper (PTX, gpu scope): acquire loads of published slots.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t atom_add_acqrel_u32(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ int ld_cg_s32(const int32_t* p) { return __ldcg(p); }
 
 // Spin until a published u32 slot is nonzero (values are stored +1).
 __device__ __forceinline__ uint32_t wait_u32(const uint32_t* p) {
@@ -118,17 +81,5 @@ __device__ __forceinline__ int select_bit(uint32_t m, int j) {
   return pos;
 }
 
-// Named barriers (ids 1..15; 0 is __syncthreads), `n` threads participate.
-__device__ __forceinline__ void named_bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_bcast(T v, int src) {
-  return __shfl_sync(0xffffffffu, v, src);
-}
 
 }  // namespace tb

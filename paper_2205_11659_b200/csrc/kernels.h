@@ -42,42 +42,52 @@ cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int
 cudaError_t pm_summary_launch(const uint8_t* tags, int64_t n, void* ws, int32_t* hdr, int32_t* opens,
                               cudaStream_t stream);
 
+// A close whose node was opened in an earlier chunk (shard mode): its global
+// index, the open's global index and the union of this chunk's clipped leaves
+// before the close.
+struct ShardPop {
+  float4 pre;
+  int c, o, pad0, pad1;
+};
+// One open of a chunk's final stack: global index and a box (its chunk-local
+// cumulative clip in exchange 1, the union of the chunk's leaves after it in
+// exchange 2).
+struct ShardOpen {
+  float4 v;
+  int idx, pad0, pad1, pad2;
+};
+
 // tree_bbox from matching (tree_bbox_m.cu): the single-device path
 size_t bbm_workspace_bytes(int64_t n);
 int bbm_tile_elems();
 cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
                        int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace = nullptr);
 
-// tree_bbox by stack slices (tree_bbox.cu): the shard path
-size_t bb_workspace_bytes(int64_t n);
-cudaError_t bb_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
-                      cudaStream_t stream, uint64_t* trace = nullptr);
-
-// tree_bbox shard mode: the stack live before the chunk, with true clips.
-struct BbShard {
-  int64_t offset;  // global index of the chunk's first element
-  int H0;          // stack height at the chunk start
-  int init_lo;     // entries provided for heights [init_lo, H0)
-  const float4* init_clip;
-  const int4* init_meta;  // {global index, kind, source chunk, slice position}
-  void* pops;             // BbPop records of closes popping provided entries
+// Shard mode of the same kernels: match / parent hold global indices, the
+// chunk's element 0 is global index `off`; contexts of earlier chunks' opens
+// come from an imported table; closes of earlier chunks' nodes are reported.
+struct BbmShard {
+  int64_t off;
+  const int32_t* ext_idx;  // ascending global indices
+  const float4* ext_ctx;   // true contexts
+  int n_ext;
+  ShardPop* pops;
+  uint32_t* npops;
 };
-int bb_tile_elems();
-size_t bb_sumrec_bytes();
-size_t bb_pop_bytes();
-cudaError_t bb_reduce_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, const BbShard* sh,
-                             cudaStream_t stream);
-cudaError_t bb_finish_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
-                             const BbShard* sh, cudaStream_t stream, uint64_t* trace = nullptr);
-cudaError_t bb_summary_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, int32_t* hdr,
-                              void* recs, int4* runs, cudaStream_t stream);
-cudaError_t bb_export_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, void* ws, const void* recs,
-                             int b, float4* suf_tiles, float4* out_tu, float4* out_su, cudaStream_t stream);
-cudaError_t bb_compose_launch(const void* allrecs, int maxb, const int* L, int g, int lo, int H, float4* init_clip,
-                              int4* init_meta, cudaStream_t stream);
-cudaError_t bb_fixup_launch(int G, int g, int64_t off, int b_g, int min_L_after, int L_g, const float4* tu,
-                            const float4* allsu, int maxb, const void* allpops, int maxp, const int* npops,
-                            const void* myrecs, float4* out, cudaStream_t stream);
+cudaError_t bbm_shard_phase1(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                             int64_t n, int64_t off, float* node_bbox, void* ws, ShardOpen* fs, int** b_dev,
+                             int* link_dev, cudaStream_t stream);
+cudaError_t bbm_compose_launch(const int4* hdr, int G, int g, const ShardOpen* allfs, int maxb, int n_ext,
+                               int32_t* ext_idx, float4* ext_ctx, cudaStream_t stream);
+cudaError_t bbm_shard_phase2(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                             int64_t n, float* node_bbox, void* ws, const BbmShard* sh, cudaStream_t stream);
+cudaError_t bbm_export_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match,
+                              const int32_t* parent, int64_t n, float* node_bbox, void* ws, const BbmShard* sh,
+                              const ShardOpen* fs, int b, ShardOpen* suc, float4* tu, cudaStream_t stream);
+cudaError_t bbm_fixup_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                             int64_t n, float* node_bbox, void* ws, const BbmShard* sh, const int4* hdr, int G, int g,
+                             const ShardOpen* allsuc, int maxb, const float4* alltu, const ShardPop* allpops,
+                             const int* npops, int maxp, cudaStream_t stream);
 
 cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, float* out, cudaStream_t s);
 cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int32_t* parent, cudaStream_t s);

@@ -14,7 +14,7 @@
 //            record (open, close) pairs instead of writing into another GPU.
 //   exchange 2: all-gather the pair lists; each rank writes match[open] for
 //            its own opens.
-// Two drivers share the protocol: NCCL (one chunk per process; the
+// Two drivers share each protocol: NCCL (one chunk per process; the
 // `*_shard` C entry points) and an in-process "virtual" driver that runs G
 // chunks of one buffer on one GPU in lockstep (tests; no peer traffic).
 #include <algorithm>
@@ -142,200 +142,209 @@ struct PmChunk {
   }
 };
 
-// ---- tree_bbox --------------------------------------------------------------
-// Same protocol with box payloads:
-//   phase 1: chunk-local reduce; header (a_g, b_g) read back; summary = the
-//            chunk's final stack with chunk-local cumulative clips.
-//   exchange 1: headers, summaries.
-//   phase 2: true clips of the provided stack entries (clip chain over
-//            chunks); reduce + finish with them; closes popping an entry of an
-//            earlier chunk record their partial union; export the chunk's
-//            union and the union after each final-stack entry.
-//   exchange 2: chunk unions, suffix unions, pop records.
-//   phase 3: fix-up of nodes spanning chunks and of blend nodes open at the
-//            end of the stream.
-struct BbChunk {
+}  // namespace
+
+// ---- tree_bbox ----------------------------------------------------------------
+// The boxes from the matching (tree_bbox_m.cu) over contiguous chunks.  Each
+// chunk has paren_match's GLOBAL match / parent for its elements.
+//   phase 1: chunk-local slice clips and tile chains (contexts of earlier
+//            chunks unknown = INF); the chunk's final stack (its opens closed
+//            after it or never) with chunk-local cumulative clips, and its link
+//            (the parent of its bottom entry, in an earlier chunk or the root).
+//   exchange 1: {off, n, b, link} per chunk, then the final-stack lists.
+//   compose: TCc(h) = ctx(link_h) chained over chunks in order; the import
+//            table of chunk g = the final-stack opens of chunks h < g with their
+//            true contexts (lcc ∩ TCc(h)).
+//   phase 2: the full local passes with the import table; closes of nodes
+//            opened in an earlier chunk report (close, open, this chunk's prefix).
+//   exchange 2: chunk unions, the union after each final-stack open, reports.
+//   fix-up: those closes, blend opens closed in a later chunk, blend opens
+//            never closed (F4 over chunks).
+namespace {
+
+struct BbmChunk {
   const uint8_t* tags;
   const float* leaf;
+  const int32_t* match;
+  const int32_t* parent;
   int64_t n, off;
   float* out;
   cudaStream_t s;
-  void* ws = nullptr;  // tree_bbox workspace (owned)
-  void* buf = nullptr;  // summary / exchange buffers (owned)
-  int32_t* hdr = nullptr;
-  void* recs = nullptr;     // [b] SumRec
-  int4* runs = nullptr;     // [b + 1]
-  float4* suf_tiles = nullptr;
-  float4* tu = nullptr;     // [1]
-  float4* su = nullptr;     // [b]
-  float4* init_clip = nullptr;
-  int4* init_meta = nullptr;
-  void* pops = nullptr;     // [a] BbPop
-  int* Ldev = nullptr;
-  int64_t a = 0, b = 0;
+  void* mem = nullptr;
+  void* ws = nullptr;
+  ShardOpen* fs = nullptr;   // [n] final stack (send 1)
+  ShardOpen* suc = nullptr;  // [n] union after each final-stack open (send 2)
+  ShardPop* pops = nullptr;  // [n] closes of earlier chunks' nodes (send 2)
+  uint32_t* npops = nullptr;
+  int* link = nullptr;
+  float4* tu = nullptr;      // chunk union (send 2)
+  int* bdev = nullptr;
+  void* extmem = nullptr;
+  int32_t* ext_idx = nullptr;
+  float4* ext_ctx = nullptr;
+  int b = 0, linkh = -1, np = 0, n_ext = 0;
 
-  cudaError_t alloc_ws() {
-    cudaError_t e = cudaMalloc(&ws, bb_workspace_bytes(std::max<int64_t>(n, 1)));
-    if (e == cudaSuccess) e = cudaMalloc(&hdr, 256);
-    return e;
-  }
-  cudaError_t phase1a() {  // chunk-local reduce; header into hdr (device)
-    BbShard local{off, 0, 0, nullptr, nullptr, nullptr};
-    return bb_reduce_launch(tags, leaf, n, ws, &local, s);
-  }
-  cudaError_t alloc_buffers(int G) {
+  BbmShard sh() const { return BbmShard{off, ext_idx, ext_ctx, n_ext, pops, npops}; }
+
+  cudaError_t alloc() {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const int64_t ntiles = (n + bb_tile_elems() - 1) / bb_tile_elems() + 1;
-    const size_t bb1 = (size_t)std::max<int64_t>(b, 1), ab1 = (size_t)std::max<int64_t>(a, 1);
-    const size_t bytes = al(bb_sumrec_bytes() * bb1) + al(16 * (bb1 + 1)) + al(16 * (size_t)ntiles) + al(16) +
-                         al(16 * bb1) + al(16 * (ab1 + 1)) + al(16 * (ab1 + 1)) + al(bb_pop_bytes() * ab1) +
-                         al(4 * (size_t)G);
-    cudaError_t e = cudaMalloc(&buf, bytes);
+    const size_t nn = (size_t)std::max<int64_t>(n, 1);
+    const size_t wsb = bbm_workspace_bytes((int64_t)nn);
+    const size_t bytes = al(wsb) + 3 * al(32 * nn) + al(64);
+    cudaError_t e = cudaMalloc(&mem, bytes);
     if (e != cudaSuccess) return e;
-    char* c = (char*)buf;
-    recs = c; c += al(bb_sumrec_bytes() * bb1);
-    runs = (int4*)c; c += al(16 * (bb1 + 1));
-    suf_tiles = (float4*)c; c += al(16 * (size_t)ntiles);
-    tu = (float4*)c; c += al(16);
-    su = (float4*)c; c += al(16 * bb1);
-    init_clip = (float4*)c; c += al(16 * (ab1 + 1));
-    init_meta = (int4*)c; c += al(16 * (ab1 + 1));
-    pops = c; c += al(bb_pop_bytes() * ab1);
-    Ldev = (int*)c;
-    return cudaSuccess;
+    char* c = (char*)mem;
+    ws = c; c += al(wsb);
+    fs = (ShardOpen*)c; c += al(32 * nn);
+    suc = (ShardOpen*)c; c += al(32 * nn);
+    pops = (ShardPop*)c; c += al(32 * nn);
+    tu = (float4*)c;
+    npops = (uint32_t*)(c + 16);
+    link = (int*)(c + 20);
+    return cudaMemsetAsync(npops, 0, 4, s);
   }
-  cudaError_t phase1b() { return bb_summary_launch(tags, leaf, n, ws, hdr, recs, runs, s); }
-  cudaError_t phase2(int g, const std::vector<Bic2>& hdrs, const void* allrecs, int maxb) {
-    const int G = (int)hdrs.size();
-    std::vector<int> L(G);
-    Bic2 pre{0, 0}, mine{0, 0};
-    for (int h = 0; h < G; h++) {
-      if (h == g) mine = pre;
-      L[h] = (int)std::max<int64_t>(pre.b - hdrs[h].a, 0);
-      pre = combine(pre, hdrs[h]);
-    }
-    const int H = (int)mine.b;
-    const int lo = std::max(H - 1 - (int)a, 0);
-    cudaError_t e = cudaMemcpyAsync(Ldev, L.data(), sizeof(int) * G, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && H > lo) e = bb_compose_launch(allrecs, maxb, Ldev, g, lo, H, init_clip, init_meta, s);
-    if (e != cudaSuccess) return e;
-    BbShard sh{off, H, lo, init_clip, init_meta, pops};
-    e = bb_reduce_launch(tags, leaf, n, ws, &sh, s);
-    if (e == cudaSuccess) e = bb_finish_launch(tags, leaf, n, out, ws, &sh, s);
-    if (e == cudaSuccess) e = bb_export_launch(tags, leaf, n, ws, recs, (int)b, suf_tiles, tu, su, s);
+  cudaError_t phase1() { return bbm_shard_phase1(tags, leaf, match, parent, n, off, out, ws, fs, &bdev, link, s); }
+  cudaError_t read_header() {
+    cudaError_t e = cudaMemcpyAsync(&b, bdev, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&linkh, link, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     return e;
   }
-  cudaError_t phase3(int g, const std::vector<Bic2>& hdrs, const float4* alltu, const float4* allsu, int maxb,
-                     const void* allpops, int maxp, const int* npops_dev) {
-    const int G = (int)hdrs.size();
-    std::vector<int> L(G);
-    Bic2 pre{0, 0};
-    for (int h = 0; h < G; h++) {
-      L[h] = (int)std::max<int64_t>(pre.b - hdrs[h].a, 0);
-      pre = combine(pre, hdrs[h]);
-    }
-    int min_after = 0x7fffffff;
-    for (int h = g + 1; h < G; h++) min_after = std::min(min_after, L[h]);
-    return bb_fixup_launch(G, g, off, (int)b, min_after, L[g], alltu, allsu, maxb, allpops, maxp, npops_dev, recs,
-                           reinterpret_cast<float4*>(out), s);
+  cudaError_t compose(const int4* hdr, int G, int g, const ShardOpen* allfs, int maxb, int cnt) {
+    n_ext = cnt;
+    const size_t c1 = (size_t)std::max(cnt, 1);
+    cudaError_t e = cudaMalloc(&extmem, 16 * c1 + 4 * c1 + 256);
+    if (e != cudaSuccess) return e;
+    ext_ctx = (float4*)extmem;
+    ext_idx = (int32_t*)((char*)extmem + 16 * c1);
+    if (cnt == 0) return cudaSuccess;
+    return bbm_compose_launch(hdr, G, g, allfs, maxb, cnt, ext_idx, ext_ctx, s);
+  }
+  cudaError_t phase2() {
+    const BbmShard x = sh();
+    return bbm_shard_phase2(tags, leaf, match, parent, n, out, ws, &x, s);
+  }
+  cudaError_t read_npops() {
+    cudaError_t e = cudaMemcpyAsync(&np, npops, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return e;
+  }
+  cudaError_t export_unions() {
+    const BbmShard x = sh();
+    return bbm_export_launch(tags, leaf, match, parent, n, out, ws, &x, fs, b, suc, tu, s);
+  }
+  cudaError_t fixup(const int4* hdr, int G, int g, const ShardOpen* allsuc, int maxb, const float4* alltu,
+                    const ShardPop* allpops, const int* npops_all, int maxp) {
+    const BbmShard x = sh();
+    return bbm_fixup_launch(tags, leaf, match, parent, n, out, ws, &x, hdr, G, g, allsuc, maxb, alltu, allpops,
+                            npops_all, maxp, s);
   }
   void release() {
-    if (ws) cudaFree(ws);
-    if (buf) cudaFree(buf);
-    if (hdr) cudaFree(hdr);
-    ws = buf = nullptr;
-    hdr = nullptr;
+    if (mem) cudaFree(mem);
+    if (extmem) cudaFree(extmem);
+    mem = extmem = nullptr;
   }
 };
 
-// header (a, b) of a chunk after phase 1a: the inclusive descriptor of its last tile
-cudaError_t read_bb_header(BbChunk& c) {
-  const size_t ctrl = 0;
-  (void)ctrl;
-  const int64_t ntiles = (c.n + bb_tile_elems() - 1) / bb_tile_elems();
-  if (ntiles == 0) {
-    c.a = c.b = 0;
-    return cudaSuccess;
-  }
-  // Bic value of the chunk, written by the tile scan into the control block
-  int2 t{0, 0};
-  cudaError_t e = cudaMemcpyAsync(&t, (char*)c.ws + CtrlLayout(ntiles).off_total, 8, cudaMemcpyDeviceToHost, c.s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(c.s);
-  c.a = t.x;
-  c.b = t.y;
-  return e;
-}
-
 }  // namespace
 
+// Virtual shards of one buffer (tests): the matching of the whole buffer comes
+// from the single-device paren_match (its sharded protocol is tested apart).
 cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, float* out, cudaStream_t s) {
-  std::vector<BbChunk> ch(G);
-  cudaError_t e = cudaSuccess;
+  int32_t* mp = nullptr;
+  void* pmws = nullptr;
+  const int64_t n64 = (n + 63) & ~int64_t(63);  // keeps parent 16-byte aligned
+  cudaError_t e = cudaMalloc(&mp, 8 * (size_t)n64);
+  if (e == cudaSuccess) e = cudaMalloc(&pmws, pm_workspace_bytes(n));
+  int32_t* match = mp;
+  int32_t* parent = mp + n64;
+  if (e == cudaSuccess) e = pm_launch(tags, n, match, parent, pmws, nullptr, s);
+  std::vector<BbmChunk> ch(G);
   for (int g = 0; g < G && e == cudaSuccess; g++) {
     const int64_t a = (g == 0) ? 0 : (n * g / G) & ~int64_t(63);
     const int64_t b = (g == G - 1) ? n : (n * (g + 1) / G) & ~int64_t(63);
-    ch[g].tags = tags + a;
-    ch[g].leaf = leaf + 4 * a;
-    ch[g].n = b - a;
-    ch[g].off = a;
-    ch[g].out = out + 4 * a;
-    ch[g].s = s;
-    e = ch[g].alloc_ws();
+    BbmChunk& c = ch[g];
+    c.tags = tags + a;
+    c.leaf = leaf + 4 * a;
+    c.match = match + a;
+    c.parent = parent + a;
+    c.n = b - a;
+    c.off = a;
+    c.out = out + 4 * a;
+    c.s = s;
+    e = c.alloc();
   }
-  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].phase1a();
-  for (int g = 0; g < G && e == cudaSuccess; g++) e = read_bb_header(ch[g]);
-  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].alloc_buffers(G);
-  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].phase1b();
-  std::vector<Bic2> hdrs(G);
-  int maxb = 1, maxp = 1;
+  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].phase1();
+  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].read_header();
+  // exchange 1
+  std::vector<int4> hdr(G);
+  int maxb = 1;
   for (int g = 0; g < G; g++) {
-    hdrs[g] = Bic2{ch[g].a, ch[g].b};
-    maxb = std::max<int>(maxb, (int)ch[g].b);
+    hdr[g] = make_int4((int)ch[g].off, (int)ch[g].n, ch[g].b, ch[g].linkh);
+    maxb = std::max(maxb, ch[g].b);
   }
-  std::vector<int> np(G);
-  {
-    Bic2 pre{0, 0};
-    for (int g = 0; g < G; g++) {
-      np[g] = (int)std::min<int64_t>(hdrs[g].a, pre.b);
-      maxp = std::max(maxp, np[g]);
-      pre = combine(pre, hdrs[g]);
-    }
-  }
-  const size_t rs = bb_sumrec_bytes(), ps = bb_pop_bytes();
-  char* allrecs = nullptr;
-  float4 *alltu = nullptr, *allsu = nullptr;
-  char* allpops = nullptr;
-  int* npops_dev = nullptr;
-  if (e == cudaSuccess) e = cudaMalloc(&allrecs, rs * (size_t)maxb * G);
-  if (e == cudaSuccess) e = cudaMalloc(&alltu, 16 * (size_t)G);
-  if (e == cudaSuccess) e = cudaMalloc(&allsu, 16 * (size_t)maxb * G);
-  if (e == cudaSuccess) e = cudaMalloc(&allpops, ps * (size_t)maxp * G);
-  if (e == cudaSuccess) e = cudaMalloc(&npops_dev, 4 * (size_t)G);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(npops_dev, np.data(), 4 * (size_t)G, cudaMemcpyHostToDevice, s);
+  int4* hdr_dev = nullptr;
+  ShardOpen *allfs = nullptr, *allsuc = nullptr;
+  float4* alltu = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&hdr_dev, sizeof(int4) * G);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hdr_dev, hdr.data(), sizeof(int4) * G, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMalloc(&allfs, sizeof(ShardOpen) * (size_t)maxb * G);
+  if (e == cudaSuccess) e = cudaMalloc(&allsuc, sizeof(ShardOpen) * (size_t)maxb * G);
+  if (e == cudaSuccess) e = cudaMalloc(&alltu, sizeof(float4) * G);
   for (int g = 0; g < G && e == cudaSuccess; g++)
-    if (ch[g].b > 0) e = cudaMemcpyAsync(allrecs + rs * (size_t)maxb * g, ch[g].recs, rs * ch[g].b, cudaMemcpyDeviceToDevice, s);
-  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].phase2(g, hdrs, allrecs, maxb);
+    if (ch[g].b > 0)
+      e = cudaMemcpyAsync(allfs + (size_t)g * maxb, ch[g].fs, sizeof(ShardOpen) * ch[g].b, cudaMemcpyDeviceToDevice,
+                          s);
+  // compose + phase 2
+  int before = 0;
   for (int g = 0; g < G && e == cudaSuccess; g++) {
-    e = cudaMemcpyAsync(alltu + g, ch[g].tu, 16, cudaMemcpyDeviceToDevice, s);
-    if (e == cudaSuccess && ch[g].b > 0)
-      e = cudaMemcpyAsync(allsu + (size_t)maxb * g, ch[g].su, 16 * ch[g].b, cudaMemcpyDeviceToDevice, s);
-    if (e == cudaSuccess && np[g] > 0)
-      e = cudaMemcpyAsync(allpops + ps * (size_t)maxp * g, ch[g].pops, ps * np[g], cudaMemcpyDeviceToDevice, s);
+    e = ch[g].compose(hdr_dev, G, g, allfs, maxb, before);
+    if (e == cudaSuccess) e = ch[g].phase2();
+    before += ch[g].b;
   }
-  for (int g = 0; g < G && e == cudaSuccess; g++)
-    e = ch[g].phase3(g, hdrs, alltu, allsu, maxb, allpops, maxp, npops_dev);
+  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].read_npops();
+  // exchange 2
+  int maxp = 1;
+  std::vector<int> np(G);
+  for (int g = 0; g < G; g++) {
+    np[g] = ch[g].np;
+    maxp = std::max(maxp, np[g]);
+  }
+  ShardPop* allpops = nullptr;
+  int* np_dev = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&allpops, sizeof(ShardPop) * (size_t)maxp * G);
+  if (e == cudaSuccess) e = cudaMalloc(&np_dev, sizeof(int) * G);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(np_dev, np.data(), sizeof(int) * G, cudaMemcpyHostToDevice, s);
+  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].export_unions();
+  for (int g = 0; g < G && e == cudaSuccess; g++) {
+    if (np[g] > 0)
+      e = cudaMemcpyAsync(allpops + (size_t)g * maxp, ch[g].pops, sizeof(ShardPop) * np[g], cudaMemcpyDeviceToDevice,
+                          s);
+    if (e == cudaSuccess && ch[g].b > 0)
+      e = cudaMemcpyAsync(allsuc + (size_t)g * maxb, ch[g].suc, sizeof(ShardOpen) * ch[g].b,
+                          cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(alltu + g, ch[g].tu, sizeof(float4), cudaMemcpyDeviceToDevice, s);
+  }
+  for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].fixup(hdr_dev, G, g, allsuc, maxb, alltu, allpops, np_dev, maxp);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = e2;
-  cudaFree(allrecs);
-  cudaFree(alltu);
-  cudaFree(allsu);
-  cudaFree(allpops);
-  cudaFree(npops_dev);
   for (auto& c : ch) c.release();
+  cudaFree(hdr_dev);
+  cudaFree(allfs);
+  cudaFree(allsuc);
+  cudaFree(alltu);
+  cudaFree(allpops);
+  cudaFree(np_dev);
+  cudaFree(mp);
+  cudaFree(pmws);
   return e;
 }
 
 #ifdef TB_WITH_NCCL
+cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* match, int32_t* parent,
+                          ncclComm_t comm, cudaStream_t s, int* nccl_err);
+
+// One rank: paren_match over the shards (global match / parent), then the boxes.
 cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, float* out,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err) {
   *nccl_err = 0;
@@ -348,77 +357,90 @@ cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int
     if (r != ncclSuccess) *nccl_err = (int)r;
     return r == ncclSuccess;
   };
-  BbChunk c;
+  int32_t* mp = nullptr;
+  const int64_t n64 = (std::max<int64_t>(n, 1) + 63) & ~int64_t(63);  // keeps parent 16-byte aligned
+  cudaError_t e = cudaMalloc(&mp, 8 * (size_t)n64);
+  int32_t* match = mp;
+  int32_t* parent = mp + n64;
+  if (e == cudaSuccess) e = pm_nccl_shard(tags, n, off, match, parent, comm, s, nccl_err);
+  BbmChunk c;
   c.tags = tags;
   c.leaf = leaf;
+  c.match = match;
+  c.parent = parent;
   c.n = n;
   c.off = off;
   c.out = out;
   c.s = s;
-  cudaError_t e = c.alloc_ws();
-  if (e == cudaSuccess) e = c.phase1a();
-  if (e == cudaSuccess) e = read_bb_header(c);
-  if (e == cudaSuccess) e = c.alloc_buffers(G);
-  if (e == cudaSuccess) e = c.phase1b();
-  // exchange 1: headers then summaries
-  int32_t* dh = nullptr;
-  std::vector<Bic2> hdrs(G);
-  int maxb = 1, maxp = 1;
-  std::vector<int> np(G);
-  if (e == cudaSuccess) e = cudaMalloc(&dh, 16 * (size_t)G);
-  if (e == cudaSuccess) {
-    int32_t mine[2] = {(int32_t)c.a, (int32_t)c.b};
-    e = cudaMemcpyAsync(dh + 2 * G, mine, 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && !*nccl_err) e = c.alloc();
+  if (e == cudaSuccess && !*nccl_err) e = c.phase1();
+  if (e == cudaSuccess && !*nccl_err) e = c.read_header();
+  // exchange 1: headers, then final-stack lists padded to the largest
+  int4* hdr_dev = nullptr;
+  std::vector<int4> hdr(G);
+  int maxb = 1, before = 0;
+  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&hdr_dev, sizeof(int4) * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) {
+    const int4 mine = make_int4((int)off, (int)n, c.b, c.linkh);
+    e = cudaMemcpyAsync(hdr_dev + G, &mine, sizeof(int4), cudaMemcpyHostToDevice, s);
   }
-  if (e == cudaSuccess && ok(ncclAllGather(dh + 2 * G, dh, 2, ncclInt32, comm, s))) {
-    std::vector<int32_t> h(2 * G);
-    e = cudaMemcpyAsync(h.data(), dh, 8 * (size_t)G, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && !*nccl_err && ok(ncclAllGather(hdr_dev + G, hdr_dev, 4, ncclInt32, comm, s))) {
+    e = cudaMemcpyAsync(hdr.data(), hdr_dev, sizeof(int4) * G, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    Bic2 pre{0, 0};
     for (int r = 0; r < G; r++) {
-      hdrs[r] = Bic2{h[2 * r], h[2 * r + 1]};
-      maxb = std::max(maxb, h[2 * r + 1]);
-      np[r] = (int)std::min<int64_t>(hdrs[r].a, pre.b);
-      maxp = std::max(maxp, np[r]);
-      pre = combine(pre, hdrs[r]);
+      maxb = std::max(maxb, hdr[r].z);
+      if (r < g) before += hdr[r].z;
     }
   }
-  const size_t rs = bb_sumrec_bytes(), ps = bb_pop_bytes();
-  char *allrecs = nullptr, *allpops = nullptr;
-  float4 *alltu = nullptr, *allsu = nullptr;
-  int* npops_dev = nullptr;
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allrecs, rs * (size_t)maxb * (G + 1));
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&alltu, 16 * (size_t)(G + 1));
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allsu, 16 * (size_t)maxb * (G + 1));
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allpops, ps * (size_t)maxp * (G + 1));
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&npops_dev, 4 * (size_t)G);
+  ShardOpen *allfs = nullptr, *allsuc = nullptr;
+  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allfs, sizeof(ShardOpen) * (size_t)maxb * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allsuc, sizeof(ShardOpen) * (size_t)maxb * (G + 1));
+  ShardOpen* sendfs = allfs + (size_t)maxb * G;
+  if (e == cudaSuccess && !*nccl_err && c.b > 0)
+    e = cudaMemcpyAsync(sendfs, c.fs, sizeof(ShardOpen) * c.b, cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess && !*nccl_err)
-    e = cudaMemcpyAsync(npops_dev, np.data(), 4 * (size_t)G, cudaMemcpyHostToDevice, s);
-  char* sendrecs = allrecs + rs * (size_t)maxb * G;
-  if (e == cudaSuccess && !*nccl_err && c.b > 0)
-    e = cudaMemcpyAsync(sendrecs, c.recs, rs * c.b, cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess && !*nccl_err) ok(ncclAllGather(sendrecs, allrecs, rs * (size_t)maxb, ncclUint8, comm, s));
-  if (e == cudaSuccess && !*nccl_err) e = c.phase2(g, hdrs, allrecs, maxb);
+    ok(ncclAllGather(sendfs, allfs, sizeof(ShardOpen) * (size_t)maxb, ncclUint8, comm, s));
+  if (e == cudaSuccess && !*nccl_err) e = c.compose(hdr_dev, G, g, allfs, maxb, before);
+  if (e == cudaSuccess && !*nccl_err) e = c.phase2();
+  if (e == cudaSuccess && !*nccl_err) e = c.read_npops();
   // exchange 2
-  float4* sendsu = allsu + (size_t)maxb * G;
-  char* sendpops = allpops + ps * (size_t)maxp * G;
+  int* np_dev = nullptr;
+  std::vector<int> np(G, 0);
+  int maxp = 1;
+  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&np_dev, sizeof(int) * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) e = cudaMemcpyAsync(np_dev + G, &c.np, sizeof(int), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && !*nccl_err && ok(ncclAllGather(np_dev + G, np_dev, 1, ncclInt32, comm, s))) {
+    e = cudaMemcpyAsync(np.data(), np_dev, sizeof(int) * G, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    for (int r = 0; r < G; r++) maxp = std::max(maxp, np[r]);
+  }
+  ShardPop* allpops = nullptr;
+  float4* alltu = nullptr;
+  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allpops, sizeof(ShardPop) * (size_t)maxp * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&alltu, sizeof(float4) * G);
+  if (e == cudaSuccess && !*nccl_err) e = c.export_unions();
+  ShardPop* sendpops = allpops + (size_t)maxp * G;
+  ShardOpen* sendsuc = allsuc + (size_t)maxb * G;
+  if (e == cudaSuccess && !*nccl_err && c.np > 0)
+    e = cudaMemcpyAsync(sendpops, c.pops, sizeof(ShardPop) * c.np, cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess && !*nccl_err && c.b > 0)
-    e = cudaMemcpyAsync(sendsu, c.su, 16 * c.b, cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess && !*nccl_err && np[g] > 0)
-    e = cudaMemcpyAsync(sendpops, c.pops, ps * np[g], cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess && !*nccl_err) ok(ncclAllGather(c.tu, alltu, 16, ncclUint8, comm, s));
-  if (e == cudaSuccess && !*nccl_err) ok(ncclAllGather(sendsu, allsu, 16 * (size_t)maxb, ncclUint8, comm, s));
-  if (e == cudaSuccess && !*nccl_err) ok(ncclAllGather(sendpops, allpops, ps * (size_t)maxp, ncclUint8, comm, s));
-  if (e == cudaSuccess && !*nccl_err) e = c.phase3(g, hdrs, alltu, allsu, maxb, allpops, maxp, npops_dev);
+    e = cudaMemcpyAsync(sendsuc, c.suc, sizeof(ShardOpen) * c.b, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && !*nccl_err) ok(ncclAllGather(c.tu, alltu, sizeof(float4), ncclUint8, comm, s));
+  if (e == cudaSuccess && !*nccl_err)
+    ok(ncclAllGather(sendsuc, allsuc, sizeof(ShardOpen) * (size_t)maxb, ncclUint8, comm, s));
+  if (e == cudaSuccess && !*nccl_err)
+    ok(ncclAllGather(sendpops, allpops, sizeof(ShardPop) * (size_t)maxp, ncclUint8, comm, s));
+  if (e == cudaSuccess && !*nccl_err) e = c.fixup(hdr_dev, G, g, allsuc, maxb, alltu, allpops, np_dev, maxp);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = e2;
-  cudaFree(dh);
-  cudaFree(allrecs);
-  cudaFree(alltu);
-  cudaFree(allsu);
-  cudaFree(allpops);
-  cudaFree(npops_dev);
   c.release();
+  cudaFree(hdr_dev);
+  cudaFree(allfs);
+  cudaFree(allsuc);
+  cudaFree(allpops);
+  cudaFree(alltu);
+  cudaFree(np_dev);
+  cudaFree(mp);
   return e;
 }
 #endif

@@ -1,11 +1,9 @@
-// Cross-tile machinery shared by paren_match and tree_bbox kernels:
-//   * decoupled look-back over the bicyclic monoid (§3; look-back is
-//     the paper's own future-work item, P:381 [Mer16]);
-//   * low-water-mark hierarchy used to find, for a height X of the stack at
-//     the start of tile `from`, the tile that pushed that entry (owner rule:
-//     the last tile U < from whose low-water mark L_U <= X).
-//     This is the "binary search over published slice prefixes" of the
-//     north star, done as a 32-ary search with warp ballots.
+// Cross-tile machinery of paren_match: the control block the tile scan fills
+// (tile start heights, low-water marks, their 32-ary min hierarchy), and the
+// owner search: for a height X of the stack at the start of tile `from`, the
+// tile that pushed that entry (owner rule F1: the last tile U < from whose
+// low-water mark L_U <= X).  This is the "binary search over published slice
+// prefixes" of the north star, done as a 32-ary search with warp ballots.
 #pragma once
 #include "common.cuh"
 
@@ -15,102 +13,45 @@ constexpr int HLEVELS = 4;  // 32^4 tiles >= 2^31 / 4096
 
 // Global control block of one call (zeroed by the host before each launch).
 struct Ctrl {
-  uint32_t* counter;         // dynamic tile ids
-  uint64_t* desc;            // [ntiles] Bic look-back descriptors
   uint32_t* lw;              // [ntiles] low-water mark L_T + 1 (0 = not yet)
   int32_t* hstart;           // [ntiles] stack height at the tile start (written with lw)
   int2* agg;                 // [ntiles] Bic value (a, b) of each tile (reduce pass)
   int2* total;               // [1] Bic value of the whole stream (after the tile scan)
   uint32_t* lv[HLEVELS];     // lv[k][g] = 1 + min L over tiles [g*32^k, (g+1)*32^k)
-  uint32_t* cnt[HLEVELS];    // arrival counters for lv[k]
 };
 
 // Sizes (in elements) of the control arrays for `ntiles` tiles.
 struct CtrlLayout {
-  size_t off_counter, off_desc, off_lw, off_h, off_agg, off_total, off_lv[HLEVELS], off_cnt[HLEVELS], bytes;
+  size_t off_lw, off_h, off_agg, off_total, off_lv[HLEVELS], bytes;
   __host__ __device__ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
   __host__ __device__ explicit CtrlLayout(int64_t ntiles) {
     size_t o = 0;
-    off_counter = o; o = align256(o + 16);
-    off_desc = o; o = align256(o + 8 * (size_t)ntiles);
     off_lw = o; o = align256(o + 4 * (size_t)ntiles);
     off_h = o; o = align256(o + 4 * (size_t)ntiles);
     off_agg = o; o = align256(o + 8 * (size_t)ntiles);
     off_total = o; o = align256(o + 8);
     int64_t m = ntiles;
-    off_lv[0] = off_cnt[0] = 0;
+    off_lv[0] = 0;
     for (int k = 1; k < HLEVELS; k++) {
       m = (m + 31) / 32;
       off_lv[k] = o; o = align256(o + 4 * (size_t)m);
-      off_cnt[k] = o; o = align256(o + 4 * (size_t)m);
     }
     bytes = o;
   }
   __host__ __device__ Ctrl bind(void* base) const {
     char* b = (char*)base;
     Ctrl c;
-    c.counter = (uint32_t*)(b + off_counter);
-    c.desc = (uint64_t*)(b + off_desc);
     c.lw = (uint32_t*)(b + off_lw);
     c.hstart = (int32_t*)(b + off_h);
     c.agg = (int2*)(b + off_agg);
     c.total = (int2*)(b + off_total);
     c.lv[0] = c.lw;
-    c.cnt[0] = nullptr;
     for (int k = 1; k < HLEVELS; k++) {
       c.lv[k] = (uint32_t*)(b + off_lv[k]);
-      c.cnt[k] = (uint32_t*)(b + off_cnt[k]);
     }
     return c;
   }
 };
-
-// ---------------------------------------------------------------------------
-// Decoupled look-back (one warp).  Returns the exclusive Bic prefix of tile T
-// (T >= 1).  Tile 0 publishes an inclusive descriptor straight away, so the
-// walk always terminates.  Each round trip inspects LBW = 128 predecessors
-// (4 independent loads per lane): with many tiles in flight the newest
-// inclusive descriptor typically lies a few hundred tiles back.
-// ---------------------------------------------------------------------------
-constexpr int LBG = 4;  // groups of 32 descriptors per round trip
-
-__device__ __forceinline__ Bic warp_fold_desc(uint64_t d, bool valid, int lane, int stop) {
-  // lane k holds tile (j - k); fold lanes [0, stop] with earlier tiles first
-  Bic v = (valid && lane <= stop) ? desc_val(d) : Bic{0, 0};
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    Bic o;
-    o.a = __shfl_down_sync(0xffffffffu, v.a, off);
-    o.b = __shfl_down_sync(0xffffffffu, v.b, off);
-    if (lane + off < 32) v = bic_combine(o, v);
-  }
-  return Bic{__shfl_sync(0xffffffffu, v.a, 0), __shfl_sync(0xffffffffu, v.b, 0)};
-}
-
-__device__ __forceinline__ Bic lookback_warp(const Ctrl& c, int T) {
-  const int lane = threadIdx.x & 31;
-  Bic acc{0, 0};
-  int j = T - 1;
-  while (true) {
-    uint64_t d[LBG];
-#pragma unroll
-    for (int g = 0; g < LBG; g++) {
-      const int t = j - 32 * g - lane;
-      d[g] = t >= 0 ? ld_relaxed_u64(c.desc + t) : desc_pack(DESC_INC, Bic{0, 0});
-    }
-#pragma unroll
-    for (int g = 0; g < LBG; g++) {
-      const int t = j - 32 * g - lane;
-      // descriptors carry their own payload: relaxed (strong) loads suffice
-      while (desc_flag(d[g]) == DESC_NONE) d[g] = ld_relaxed_u64(c.desc + t);
-      const unsigned inc = __ballot_sync(0xffffffffu, desc_flag(d[g]) == DESC_INC);
-      const int stop = inc ? (__ffs(inc) - 1) : 31;
-      acc = bic_combine(warp_fold_desc(d[g], t >= 0, lane, stop), acc);
-      if (inc) return acc;
-    }
-    j -= 32 * LBG;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Owner search (one warp): the last tile U < from with L_U <= X (X >= 0).
@@ -241,39 +182,6 @@ __device__ __forceinline__ int owner_search_done(const Ctrl& c, int from, int X,
     if (idx == 0) break;
   }
   return -1;
-}
-
-// ---------------------------------------------------------------------------
-// Publish tile T's inclusive descriptor and low-water mark (one thread, after
-// the block synchronised on its slice writes).  The release store orders all
-// of the CTA's earlier writes (bar.sync + gpu-scope release, as in CUTLASS's
-// semaphores) before both stores; the relaxed low-water store after the
-// release fence forms a release pattern for readers that acquire it.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void publish_inclusive(const Ctrl& c, int T, Bic incl, int L, bool desc_too) {
-  if (desc_too) st_release_u64(c.desc + T, desc_pack(DESC_INC, incl));
-  else __threadfence();
-  st_relaxed_u32(c.lw + T, (uint32_t)L + 1u);
-}
-
-// Fold tile T's published low-water mark into the 32-ary hierarchy (warp;
-// off the critical path).  The last of 32 siblings to arrive publishes the
-// parent entry.
-__device__ __forceinline__ void hierarchy_arrive(const Ctrl& c, int T) {
-  const int lane = threadIdx.x & 31;
-  int idx = T;
-#pragma unroll 1
-  for (int k = 1; k < HLEVELS; k++) {
-    const int g = idx >> 5;
-    unsigned old = 0;
-    if (lane == 0) old = atom_add_acqrel_u32(c.cnt[k] + g, 1u);
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old != 31u) return;
-    uint32_t v = wait_u32(c.lv[k - 1] + ((size_t)g << 5) + lane);
-    v = __reduce_min_sync(0xffffffffu, v);
-    if (lane == 0) st_release_u32(c.lv[k] + g, v);
-    idx = g;
-  }
 }
 
 }  // namespace tb

@@ -52,6 +52,7 @@
 #include "kernels.h"
 
 namespace tb {
+static const int kMinus1 = -1;
 namespace bbm {
 
 constexpr int NT = 128;
@@ -77,7 +78,41 @@ struct Params {
   int32_t* never;        // [n] blend opens never closed (R4)
   uint32_t* nnever;      // their count
   uint64_t* trace;       // optional per-tile phase timestamps (debug)
+  // shard mode; zero / null for one device.  match / parent hold
+  // GLOBAL indices; arrays are indexed locally (global - off).
+  int64_t off;             // global index of element 0
+  const int32_t* ext_idx;  // [n_ext] open entries of earlier chunks, ascending
+  const float4* ext_ctx;   // their true contexts
+  int n_ext;
+  ShardPop* pops;          // closes of nodes opened in an earlier chunk (for the exchange)
+  uint32_t* npops;
 };
+
+// True context of an open X of an earlier chunk (binary search in the
+// imported table; INF when there is none, i.e. the chunk-local frame).  Not
+// inlined: only shard mode takes it, for elements whose parent lies in an
+// earlier chunk.
+__device__ __noinline__ float4 ext_lookup(const int32_t* idx, const float4* ctx, int cnt, int X) {
+  int lo = 0, hi = cnt;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(idx + mid) < X) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < cnt && __ldg(idx + lo) == X) ? __ldg(ctx + lo) : bINF();
+}
+__device__ __forceinline__ float4 ext_ctx(const Params& p, int X) {
+  return ext_lookup(p.ext_idx, p.ext_ctx, p.n_ext, X);
+}
+
+// Context of an open X outside the current tile: node_bbox[X] holds lc(X) or
+// its true context (F6), completed by TC of X's tile; earlier chunks: imported.
+template <bool SHARD>
+__device__ __forceinline__ float4 outer_ctx(const Params& p, int X) {
+  if (SHARD && X < p.off) return ext_ctx(p, X);
+  const int64_t x = SHARD ? X - p.off : X;
+  return isect(__ldcg(p.out + x), __ldg(p.tc + x / TILE));
+}
 
 __device__ __forceinline__ uint64_t gtime() {
   uint64_t t;
@@ -279,9 +314,10 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
   float4* acc[2] = {acc2, acc2 + nt};
   int* ptr[2] = {ptr2, ptr2 + nt};
   for (int V = gt; V < nt; V += nthr) {
-    const int X = __ldg(p.link + V);
-    acc[0][V] = X >= 0 ? __ldg(p.out + X) : bINF();  // lc(X), written by bbm_reduce
-    ptr[0][V] = X >= 0 ? X / TILE : -1;
+    const int X = __ldg(p.link + V);  // global index
+    // lc(X), written by bbm_reduce; an open of an earlier chunk: imported context
+    acc[0][V] = X >= p.off ? __ldg(p.out + (X - p.off)) : (X >= 0 ? ext_ctx(p, X) : bINF());
+    ptr[0][V] = X >= p.off ? (int)((X - p.off) / TILE) : -1;
   }
   int cb = 0;
   for (int round = 0; round < 40; round++) {
@@ -350,15 +386,22 @@ __device__ __forceinline__ float4 range_union_threads(const Smem& s, int a, int 
   return unite(unite(s.u.un.suf[a], right), s.wmid[wa][wb]);
 }
 
+template <bool SHARD>
 __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = blockIdx.x;
-  const int64_t base = (int64_t)T * TILE;
+  const int64_t base = (int64_t)T * TILE;  // local indices (arrays)
   const int64_t tstart = base + (int64_t)tid * K;
-  const int64_t tend = base + TILE;
   const int nvalid = (int)(p.n - base < TILE ? p.n - base : TILE);
+  // global indices (compared with match / parent values)
+  // (the last tile of a shard chunk ends at the chunk end: a partner beyond it
+  // is in the next chunk, not in this tile or thread)
+  const int64_t gend = p.off + p.n;
+  const int64_t gbase = p.off + base, gtstart = p.off + tstart;
+  const int64_t gtend = SHARD ? min(gbase + TILE, gend) : gbase + TILE;
+  const int64_t gthr_end = SHARD ? min(gtstart + K, gend) : gtstart + K;
   BBM_TRACE(T, 0);
 
   // ---- A. load -------------------------------------------------------------
@@ -377,14 +420,14 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
   int xa = -1, xb = -1;
 #pragma unroll
   for (int i = 0; i < K; i++) {
-    if ((((om | lm) >> i) & 1u) && pr[i] >= 0 && pr[i] < base && pr[i] != xa) {
+    if ((((om | lm) >> i) & 1u) && pr[i] >= 0 && pr[i] < gbase && pr[i] != xa) {
       xb = xa;
       xa = pr[i];
     }
   }
   float4 ga = bINF(), gb = bINF();
-  if (xa >= 0) ga = isect(__ldcg(p.out + xa), __ldg(p.tc + xa / TILE));
-  if (xb >= 0) gb = isect(__ldcg(p.out + xb), __ldg(p.tc + xb / TILE));
+  if (xa >= 0) ga = outer_ctx<SHARD>(p, xa);
+  if (xb >= 0) gb = outer_ctx<SHARD>(p, xb);
   // boxes into the slots, coalesced (512 contiguous bytes per warp instruction)
 #pragma unroll
   for (int j = 0; j < K; j++) {
@@ -397,7 +440,7 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
   uint32_t thr_un = 0;  // opens closed beyond this thread (or never)
 #pragma unroll
   for (int i = 0; i < K; i++)
-    if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= tstart + K)) thr_un |= 1u << i;
+    if (((om >> i) & 1u) && (mt[i] < 0 || mt[i] >= gthr_end)) thr_un |= 1u << i;
   __syncthreads();
 
   // ---- B. clips relative to the thread's external ancestor -------------------
@@ -408,10 +451,10 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
     if (((om | lm) >> i) & 1u) {
       const int par = pr[i];
       float4 b = bINF();
-      if (par < tstart) {
+      if (par < gtstart) {
         curX = par;
       } else {
-        b = s.val[slot(tid, par - (int)tstart)];
+        b = s.val[slot(tid, (int)(par - gtstart))];
       }
       float4& me = s.val[slot(tid, i)];
       me = ((bm >> i) & 1u) ? b : isect(me, b);
@@ -426,10 +469,10 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
     float4 acc = bINF();
     int ptr = -1;
     if (thr_un && curX >= 0) {
-      if (curX < base) {
-        acc = curX == xa ? ga : (curX == xb ? gb : isect(__ldcg(p.out + curX), __ldg(p.tc + curX / TILE)));
+      if (curX < gbase) {
+        acc = curX == xa ? ga : (curX == xb ? gb : outer_ctx<SHARD>(p, curX));
       } else {
-        const int x = curX - (int)base;
+        const int x = (int)(curX - gbase);
         acc = s.val[slot_of(x)];
         ptr = x / K;
       }
@@ -460,14 +503,14 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
 #pragma unroll
     for (int i = 0; i < K; i++) {
       if (((om | lm) >> i) & 1u) {
-        if (pr[i] < tstart) X = pr[i];
+        if (pr[i] < gtstart) X = pr[i];
         if ((pend >> i) & 1u) {
           if (X != cx) {
             cx = X;
-            if (X < base) {
-              g = X == xa ? ga : (X == xb ? gb : isect(__ldcg(p.out + X), __ldg(p.tc + X / TILE)));
+            if (X < gbase) {
+              g = X == xa ? ga : (X == xb ? gb : outer_ctx<SHARD>(p, X));
             } else {
-              const int x = X - (int)base;
+              const int x = (int)(X - gbase);
               g = isect(s.val[slot_of(x)], s.u.tl[x / K]);
             }
           }
@@ -493,8 +536,8 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
       PT = unite(PT, s.val[slot(tid, i)]);
     } else if (cm & bit) {
       const int m = mt[i];
-      if (m >= tstart) {
-        const int o = m - (int)tstart;
+      if (m >= gtstart) {
+        const int o = (int)(m - gtstart);
         float4 U = bEMPTY();
         uint32_t lb = lm & (bit - 1u) & ~((2u << o) - 1u);  // leaves strictly between
         while (lb) {
@@ -506,7 +549,7 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
         if ((bm >> o) & 1u) s.val[slot(tid, o)] = U;
       } else if (m >= 0) {
         s.val[slot(tid, i)] = PT;  // completed by the open's thread (F) or in G
-        if (m < base) ecm |= bit;
+        if (m < gbase) ecm |= bit;
       } else {
         s.val[slot(tid, i)] = bEMPTY();  // R3
       }
@@ -552,7 +595,7 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
 #pragma unroll
     for (int i = 0; i < K; i++) {
       if ((thr_un >> i) & 1u) {
-        if (mt[i] < 0 || mt[i] >= tend) qt |= 1u << i;
+        if (mt[i] < 0 || mt[i] >= gtend) qt |= 1u << i;
         else qi |= 1u << i;
       }
       if (((bm >> i) & 1u) && mt[i] < 0) nvm |= 1u << i;
@@ -567,7 +610,7 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
           p.su[tstart + i] = unite(R, after);
           if (nvm & bit) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + i);
         } else if (qi & bit) {
-          const int c = mt[i] - (int)base;
+          const int c = (int)(mt[i] - gbase);
           float4& cv = s.val[slot_of(c)];
           const float4 U = unite(unite(R, range_union_threads(s, tid + 1, c / K - 1)), cv);
           cv = U;
@@ -641,7 +684,7 @@ __global__ void __launch_bounds__(128) bbm_close(Params p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int T = blockIdx.x;
   const int cnt = __ldg(p.xcnt + T);
-  int cto = -1;  // warp cache: the last range resolved (deep chains repeat one open tile)
+  int cto = INT_MIN;  // warp cache: the last range resolved (deep chains repeat one open tile); To = -1 is a key
   float4 cR = bEMPTY();
   for (int j0 = warp * 32; j0 < cnt; j0 += 128) {
     const int j = j0 + lane;
@@ -650,12 +693,17 @@ __global__ void __launch_bounds__(128) bbm_close(Params p) {
     float4 P = bEMPTY(), su = bEMPTY();
     uint8_t kind = 0;
     if (valid) {
-      c = __ldg(p.xc + (int64_t)T * TILE + j);
-      o = __ldg(p.match + c);
-      To = o / TILE;
+      c = __ldg(p.xc + (int64_t)T * TILE + j);  // local
+      o = __ldg(p.match + c);                   // global
       P = __ldcg(p.out + c);
-      su = __ldcg(p.su + o);
-      kind = __ldg(p.tags + o);
+      if (o >= p.off) {
+        const int64_t ol = o - p.off;
+        To = (int)(ol / TILE);
+        su = __ldcg(p.su + ol);
+        kind = __ldg(p.tags + ol);
+      } else {
+        To = -1;  // opened in an earlier chunk: this chunk's part is every tile before
+      }
     }
     float4 R = bEMPTY();
     bool pending = valid && To < T - 1;
@@ -676,8 +724,18 @@ __global__ void __launch_bounds__(128) bbm_close(Params p) {
     }
     if (valid) {
       const float4 U = unite(unite(P, su), R);
-      p.out[c] = U;
-      if (kind == 2) p.out[o] = U;  // blend open
+      if (o >= p.off) {
+        p.out[c] = U;
+        if (kind == 2) p.out[o - p.off] = U;  // blend open
+      } else {  // shard mode: finished after the exchange
+        const uint32_t q = atomicAdd(p.npops, 1u);
+        ShardPop r;
+        r.pre = U;
+        r.c = (int)(p.off + c);
+        r.o = o;
+        r.pad0 = r.pad1 = 0;
+        p.pops[q] = r;
+      }
     }
   }
 }
@@ -699,6 +757,215 @@ __global__ void __launch_bounds__(256) bbm_final(Params p) {
 }
 
 // ----------------------------------------------------------------------------
+// shard mode: a chunk's final stack, the chunk context chain,
+// exported unions, fix-up of nodes that span chunks
+// ----------------------------------------------------------------------------
+// The chunk's final stack = its opens closed after the chunk or never (§3-§4,
+// P:96-138), ascending.  Counted per tile (one warp per tile), positioned by an
+// exclusive scan, written with the chunk-local cumulative clip lc ∩ TC_local.
+__device__ __forceinline__ uint32_t fs_mask(const Params& p, int64_t lbase) {
+  uint32_t m = 0;
+  for (int i = 0; i < 32; i++) {
+    const int64_t x = lbase + i;
+    if (x >= p.n) break;
+    const uint8_t t = p.tags[x];
+    if (t == 1 || t == 2) {
+      const int mm = __ldg(p.match + x);
+      if (mm < 0 || mm >= p.off + p.n) m |= 1u << i;
+    }
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(128) bbm_fs_count(Params p, int* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (T >= p.ntiles) return;
+  const uint32_t m = fs_mask(p, (int64_t)T * TILE + lane * 32);
+  const int c = __reduce_add_sync(0xffffffffu, __popc(m));
+  if (lane == 0) cnt[T] = c;
+}
+
+// exclusive scan of cnt[0..nt) into offs (one CTA); offs[nt] = total
+__global__ void __launch_bounds__(1024) bbm_scan_counts(const int* cnt, int nt, int* offs) {
+  __shared__ int ws[32];
+  __shared__ int carry_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int carry = 0;
+  for (int b0 = 0; b0 < nt; b0 += 1024) {
+    const int i = b0 + tid;
+    const int v = i < nt ? cnt[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    int pre = carry;
+    for (int w = 0; w < warp; w++) pre += ws[w];
+    if (i < nt) offs[i] = pre + x - v;
+    if (tid == 1023) carry_s = pre + x;
+    __syncthreads();
+    carry = carry_s;
+    __syncthreads();
+  }
+  if (tid == 0) offs[nt] = carry;
+}
+
+__global__ void __launch_bounds__(128) bbm_fs_write(Params p, const int* offs, ShardOpen* fs, int* link_out) {
+  const int lane = threadIdx.x & 31;
+  const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (T >= p.ntiles) return;
+  const int64_t lbase = (int64_t)T * TILE + lane * 32;
+  uint32_t m = fs_mask(p, lbase);
+  int x = __popc(m);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  int pos = offs[T] + x - __popc(m);
+  const float4 tcT = __ldg(p.tc + T);
+  while (m) {
+    const int i = __ffs(m) - 1;
+    m &= m - 1;
+    ShardOpen r;
+    r.v = isect(__ldcg(p.out + lbase + i), tcT);  // lc ∩ TC_local
+    r.idx = (int)(p.off + lbase + i);
+    r.pad0 = r.pad1 = r.pad2 = 0;
+    fs[pos] = r;
+    if (pos == 0) *link_out = __ldg(p.parent + lbase + i);  // the chunk's link (earlier chunk or root)
+    pos++;
+  }
+}
+
+// position of global index X in a chunk's ascending list (-1 if absent)
+__device__ __forceinline__ int find_open(const ShardOpen* l, int cnt, int X) {
+  int lo = 0, hi = cnt;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (l[mid].idx < X) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < cnt && l[lo].idx == X) ? lo : -1;
+}
+
+__device__ __forceinline__ int chunk_of(const int4* hdr, int G, int X) {
+  int h = 0;
+  while (h + 1 < G && hdr[h + 1].x <= X) h++;
+  return h;
+}
+
+// TCc(h) = ctx(link_h) = lcc(link_h) ∩ TCc(chunk of link_h): the clip chain over
+// chunks (in order); then the import table of chunk g: every final-stack open
+// of chunks h < g with its true context lcc ∩ TCc(h).  hdr[h] = {off, n, b, link}.
+__global__ void __launch_bounds__(256) bbm_compose(const int4* hdr, int G, int g, const ShardOpen* allfs, int maxb,
+                                                   int32_t* ext_idx, float4* ext_ctx) {
+  __shared__ float4 tcc[64];
+  __shared__ int start[65];
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int h = 0; h < G; h++) {
+      const int4 hd = hdr[h];
+      float4 t = bINF();
+      if (hd.w >= 0) {
+        const int h2 = chunk_of(hdr, G, hd.w);
+        const int q = find_open(allfs + (size_t)h2 * maxb, hdr[h2].z, hd.w);
+        if (q >= 0) t = isect(allfs[(size_t)h2 * maxb + q].v, tcc[h2]);
+      }
+      tcc[h] = t;
+      start[h] = acc;
+      acc += hd.z;
+    }
+    start[G] = acc;
+  }
+  __syncthreads();
+  const int total = start[g];
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < total; i += gridDim.x * 256) {
+    int h = 0;
+    while (start[h + 1] <= i) h++;
+    const ShardOpen r = allfs[(size_t)h * maxb + (i - start[h])];
+    ext_idx[i] = r.idx;
+    ext_ctx[i] = isect(r.v, tcc[h]);
+  }
+}
+
+// Export after the local passes: for each final-stack open the union of the
+// chunk's clipped leaves after it (one warp per open), and the chunk's union.
+__global__ void __launch_bounds__(256) bbm_export(Params p, const ShardOpen* fs, int b, ShardOpen* suc, float4* tu) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (w == b) {
+    const float4 t = p.ntiles > 0 ? range_union_tiles_warp(p, 0, p.ntiles - 1) : bEMPTY();
+    if (lane == 0) *tu = t;
+    return;
+  }
+  if (w > b) return;
+  const int o = fs[w].idx;
+  const int64_t ol = o - p.off;
+  const int To = (int)(ol / TILE);
+  const float4 after = To + 1 < p.ntiles ? range_union_tiles_warp(p, To + 1, p.ntiles - 1) : bEMPTY();
+  if (lane == 0) {
+    ShardOpen r;
+    r.v = unite(__ldcg(p.su + ol), after);
+    r.idx = o;
+    r.pad0 = r.pad1 = r.pad2 = 0;
+    suc[w] = r;
+  }
+}
+
+__device__ __forceinline__ float4 chunk_range(const float4* alltu, int a, int b) {
+  float4 v = bEMPTY();
+  for (int h = a; h <= b; h++) v = unite(v, alltu[h]);
+  return v;
+}
+
+// Fix-up of nodes spanning chunks (chunk g), after exchange 2:
+//   own closes of earlier chunks' nodes: suffix of the open's chunk ∪ chunks
+//     between ∪ this chunk's prefix (F4 over chunks);
+//   own blend opens closed in a later chunk: the same union, from that chunk's
+//     record;
+//   own blend opens never closed (R4): ∪ every later chunk.
+__global__ void __launch_bounds__(256) bbm_fixup(Params p, const int4* hdr, int G, int g, const ShardOpen* allsuc,
+                                                 int maxb, const float4* alltu, const ShardPop* allpops,
+                                                 const int* npops, int maxp) {
+  const int64_t tid = blockIdx.x * (int64_t)256 + threadIdx.x, nthr = (int64_t)gridDim.x * 256;
+  // own pops
+  for (int64_t i = tid; i < npops[g]; i += nthr) {
+    const ShardPop r = allpops[(size_t)g * maxp + i];
+    const int h = chunk_of(hdr, G, r.o);
+    const int q = find_open(allsuc + (size_t)h * maxb, hdr[h].z, r.o);
+    float4 U = unite(r.pre, chunk_range(alltu, h + 1, g - 1));
+    if (q >= 0) U = unite(U, allsuc[(size_t)h * maxb + q].v);
+    p.out[r.c - p.off] = U;
+  }
+  // later chunks' pops of this chunk's blend opens
+  for (int k = g + 1; k < G; k++) {
+    for (int64_t i = tid; i < npops[k]; i += nthr) {
+      const ShardPop r = allpops[(size_t)k * maxp + i];
+      if (r.o < p.off || r.o >= p.off + p.n) continue;
+      const int64_t ol = r.o - p.off;
+      if (p.tags[ol] != 2) continue;
+      const int q = find_open(allsuc + (size_t)g * maxb, hdr[g].z, r.o);
+      float4 U = unite(r.pre, chunk_range(alltu, g + 1, k - 1));
+      if (q >= 0) U = unite(U, allsuc[(size_t)g * maxb + q].v);
+      p.out[ol] = U;
+    }
+  }
+  // blend opens never closed: the chunk-local part is in node_bbox (bbm_final)
+  if (g + 1 < G) {
+    const float4 later = chunk_range(alltu, g + 1, G - 1);
+    const uint32_t cnt = __ldcg(p.nnever);
+    for (int64_t i = tid; i < cnt; i += nthr) {
+      const int o = __ldcg(p.never + i);
+      p.out[o] = unite(__ldcg(p.out + o), later);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
 // workspace
 // ----------------------------------------------------------------------------
 struct Layout {
@@ -706,6 +973,7 @@ struct Layout {
   size_t zero_off, zero_bytes;
   size_t off_nnever;
   size_t off_u[LV], off_link, off_tc, off_su, off_xc, off_xcnt, off_never, off_tcacc, off_tcptr, off_tcflag, bytes;
+  size_t off_fscnt, off_fsoff;
   explicit Layout(int64_t n) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     ntiles = (n + TILE - 1) / TILE;
@@ -721,6 +989,8 @@ struct Layout {
     off_link = o; o = al(o + 4 * (size_t)ntiles);
     off_tc = o; o = al(o + 16 * (size_t)ntiles);
     off_xcnt = o; o = al(o + 4 * (size_t)ntiles);
+    off_fscnt = o; o = al(o + 4 * (size_t)ntiles);
+    off_fsoff = o; o = al(o + 4 * (size_t)(ntiles + 1));
     off_tcacc = o; o = al(o + 32 * (size_t)ntiles);
     off_tcptr = o; o = al(o + 8 * (size_t)ntiles);
     off_tcflag = o; o = al(o + 16);
@@ -734,7 +1004,8 @@ struct Layout {
 void main_setup() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(bbm_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    cudaFuncSetAttribute(bbm_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    cudaFuncSetAttribute(bbm_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
     done = true;
   }
 }
@@ -760,9 +1031,10 @@ size_t bbm_workspace_bytes(int64_t n) {
 
 int bbm_tile_elems() { return bbm::TILE; }
 
-cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
-                       int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace) {
-  if (n <= 0) return cudaSuccess;
+namespace {
+
+bbm::Params make_params(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                        int64_t n, float* node_bbox, void* ws, const BbmShard* sh, uint64_t* trace) {
   bbm::Layout L(n);
   char* b = (char*)ws;
   bbm::Params p;
@@ -774,9 +1046,7 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   p.n = n;
   p.ntiles = (int)L.ntiles;
   p.nnever = (uint32_t*)(b + L.off_nnever);
-  for (int k = 0; k < bbm::LV; k++) {
-    p.u[k] = (float4*)(b + L.off_u[k]);
-  }
+  for (int k = 0; k < bbm::LV; k++) p.u[k] = (float4*)(b + L.off_u[k]);
   p.link = (int32_t*)(b + L.off_link);
   p.tc = (float4*)(b + L.off_tc);
   p.su = (float4*)(b + L.off_su);
@@ -784,26 +1054,41 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   p.xc = (int32_t*)(b + L.off_xc);
   p.xcnt = (int32_t*)(b + L.off_xcnt);
   p.trace = trace;
-  cudaError_t err = cudaMemsetAsync(b + L.zero_off, 0, L.zero_bytes, stream);
-  if (err != cudaSuccess) return err;
-  TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p)));
-  {
-    float4* acc2 = (float4*)(b + L.off_tcacc);
-    int* ptr2 = (int*)(b + L.off_tcptr);
-    int* flag = (int*)(b + L.off_tcflag);
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((L.ntiles + 255) / 256, bbm::tc_blocks()));
-    void* args[] = {(void*)&p, (void*)&acc2, (void*)&ptr2, (void*)&flag};
-    void* tok;
-    prof_begin(stream, "bbm_tc", &tok);
-    err = cudaLaunchCooperativeKernel((const void*)bbm::bbm_tc, dim3(blocks), dim3(256), args, 0, stream);
-    prof_end(stream, tok);
-    if (err != cudaSuccess) return err;
-  }
+  p.off = sh ? sh->off : 0;
+  p.ext_idx = sh ? sh->ext_idx : nullptr;
+  p.ext_ctx = sh ? sh->ext_ctx : nullptr;
+  p.n_ext = sh ? sh->n_ext : 0;
+  p.pops = sh ? sh->pops : nullptr;
+  p.npops = sh ? sh->npops : nullptr;
+  return p;
+}
+
+cudaError_t launch_tc(const bbm::Params& p, void* ws, cudaStream_t stream) {
+  bbm::Layout L(p.n);
+  char* b = (char*)ws;
+  float4* acc2 = (float4*)(b + L.off_tcacc);
+  int* ptr2 = (int*)(b + L.off_tcptr);
+  int* flag = (int*)(b + L.off_tcflag);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((L.ntiles + 255) / 256, bbm::tc_blocks()));
+  bbm::Params pc = p;
+  void* args[] = {(void*)&pc, (void*)&acc2, (void*)&ptr2, (void*)&flag};
+  void* tok;
+  prof_begin(stream, "bbm_tc", &tok);
+  cudaError_t err = cudaLaunchCooperativeKernel((const void*)bbm::bbm_tc, dim3(blocks), dim3(256), args, 0, stream);
+  prof_end(stream, tok);
+  return err;
+}
+
+// bbm_main, the union hierarchy, bbm_close, bbm_final
+cudaError_t launch_rest(const bbm::Params& p, cudaStream_t stream) {
+  const int64_t nt = p.ntiles;
   bbm::main_setup();
-  TB_LAUNCH(stream, "bbm_main",
-            (bbm::bbm_main<<<(unsigned)L.ntiles, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
+  if (p.off == 0 && p.n_ext == 0 && p.pops == nullptr)
+    TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<false><<<(unsigned)nt, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
+  else
+    TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<true><<<(unsigned)nt, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
   {
-    int64_t m = L.ntiles;
+    int64_t m = nt;
     for (int k = 1; k < bbm::LV && m > 1; k++) {
       const int64_t groups = (m + 31) / 32;
       TB_LAUNCH(stream, "bbm_hier",
@@ -811,8 +1096,94 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
       m = groups;
     }
   }
-  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<(unsigned)L.ntiles, 128, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<(unsigned)nt, 128, 0, stream>>>(p)));
   TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                       int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace) {
+  if (n <= 0) return cudaSuccess;
+  bbm::Layout L(n);
+  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, nullptr, trace);
+  cudaError_t err = cudaMemsetAsync((char*)ws + L.zero_off, 0, L.zero_bytes, stream);
+  if (err != cudaSuccess) return err;
+  TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p)));
+  err = launch_tc(p, ws, stream);
+  if (err != cudaSuccess) return err;
+  return launch_rest(p, stream);
+}
+
+cudaError_t bbm_shard_phase1(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                             int64_t n, int64_t off, float* node_bbox, void* ws, ShardOpen* fs, int** b_dev,
+                             int* link_dev, cudaStream_t stream) {
+  bbm::Layout L(std::max<int64_t>(n, 1));
+  char* b = (char*)ws;
+  int* cnt = (int*)(b + L.off_fscnt);
+  int* offs = (int*)(b + L.off_fsoff);
+  *b_dev = offs + L.ntiles;
+  if (n <= 0) {
+    cudaError_t e = cudaMemsetAsync(offs + L.ntiles, 0, 4, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(link_dev, &kMinus1, 4, cudaMemcpyHostToDevice, stream);
+    return e;
+  }
+  BbmShard sh{off, nullptr, nullptr, 0, nullptr, nullptr};
+  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, &sh, nullptr);
+  cudaError_t err = cudaMemsetAsync((char*)ws + L.zero_off, 0, L.zero_bytes, stream);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(link_dev, &kMinus1, 4, cudaMemcpyHostToDevice, stream);
+  if (err != cudaSuccess) return err;
+  const unsigned g4 = (unsigned)((L.ntiles + 3) / 4);
+  TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<g4, 128, 0, stream>>>(p)));
+  err = launch_tc(p, ws, stream);  // no imported contexts yet: chunk-local TC
+  if (err != cudaSuccess) return err;
+  TB_LAUNCH(stream, "bbm_fs_count", (bbm::bbm_fs_count<<<g4, 128, 0, stream>>>(p, cnt)));
+  TB_LAUNCH(stream, "bbm_scan_counts", (bbm::bbm_scan_counts<<<1, 1024, 0, stream>>>(cnt, (int)L.ntiles, offs)));
+  TB_LAUNCH(stream, "bbm_fs_write", (bbm::bbm_fs_write<<<g4, 128, 0, stream>>>(p, offs, fs, link_dev)));
+  return cudaGetLastError();
+}
+
+cudaError_t bbm_compose_launch(const int4* hdr, int G, int g, const ShardOpen* allfs, int maxb, int n_ext,
+                               int32_t* ext_idx, float4* ext_ctx, cudaStream_t stream) {
+  const int blocks = std::max(1, std::min((n_ext + 255) / 256, 1024));
+  TB_LAUNCH(stream, "bbm_compose",
+            (bbm::bbm_compose<<<blocks, 256, 0, stream>>>(hdr, G, g, allfs, maxb, ext_idx, ext_ctx)));
+  return cudaGetLastError();
+}
+
+cudaError_t bbm_shard_phase2(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                             int64_t n, float* node_bbox, void* ws, const BbmShard* sh, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  bbm::Layout L(n);
+  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, sh, nullptr);
+  cudaError_t err = cudaMemsetAsync((char*)ws + L.zero_off, 0, L.zero_bytes, stream);  // R4 list count
+  if (err == cudaSuccess) err = launch_tc(p, ws, stream);
+  if (err != cudaSuccess) return err;
+  return launch_rest(p, stream);
+}
+
+cudaError_t bbm_export_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match,
+                              const int32_t* parent, int64_t n, float* node_bbox, void* ws, const BbmShard* sh,
+                              const ShardOpen* fs, int b, ShardOpen* suc, float4* tu, cudaStream_t stream) {
+  if (n <= 0) {
+    const float inf = __builtin_inff();
+    const float4 e = make_float4(inf, inf, -inf, -inf);
+    return cudaMemcpyAsync(tu, &e, sizeof(e), cudaMemcpyHostToDevice, stream);
+  }
+  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, sh, nullptr);
+  TB_LAUNCH(stream, "bbm_export", (bbm::bbm_export<<<(unsigned)(b / 8 + 1), 256, 0, stream>>>(p, fs, b, suc, tu)));
+  return cudaGetLastError();
+}
+
+cudaError_t bbm_fixup_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                             int64_t n, float* node_bbox, void* ws, const BbmShard* sh, const int4* hdr, int G, int g,
+                             const ShardOpen* allsuc, int maxb, const float4* alltu, const ShardPop* allpops,
+                             const int* npops, int maxp, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, sh, nullptr);
+  TB_LAUNCH(stream, "bbm_fixup", (bbm::bbm_fixup<<<148, 256, 0, stream>>>(p, hdr, G, g, allsuc, maxb, alltu,
+                                                                         allpops, npops, maxp)));
   return cudaGetLastError();
 }
 
