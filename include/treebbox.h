@@ -174,11 +174,13 @@ int tb_comm_destroy(void *comm);
 int paren_match_shard(const uint8_t *d_tags, int64_t n_local, int64_t offset, int32_t *d_match,
                       int32_t *d_parent, void *comm, void *stream);
 /* tree_bbox over contiguous chunks: d_leaf_bbox / d_node_bbox hold the chunk's
- * n_local boxes.  Exchange 1 carries each chunk's final stack with chunk-local
- * cumulative clips (true clips then follow by a clip chain over chunks);
- * exchange 2 carries each chunk's union, the union after each of its
- * final-stack entries and its closes of earlier chunks' nodes, from which
- * every rank finishes the nodes that span chunks (F4). */
+ * n_local boxes.  Runs paren_match_shard (global matching) first, then the
+ * boxes from the matching: exchange 1 carries each chunk's final stack (opens
+ * closed after it or never) with chunk-local cumulative clips, from which every
+ * rank derives the true contexts of earlier chunks' opens; exchange 2 carries
+ * chunk unions, the union after each final-stack open and the closes of
+ * earlier chunks' nodes with their prefix unions, from which every rank
+ * finishes the nodes that span chunks (F4). */
 int tree_bbox_shard(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n_local, int64_t offset,
                     float *d_node_bbox, void *comm, void *stream);
 
