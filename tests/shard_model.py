@@ -101,3 +101,139 @@ def protocol(tags_chunk, off, rank, allgather):
     all_pairs = [p for lst in allgather(pairs) for p in lst]
     apply_pairs(match, off, all_pairs)
     return parent, match
+
+
+# ---------------------------------------------------------------------------
+# tree_bbox shard protocol (mirrors the bbm shard path of csrc/shard.cu):
+# inputs are the chunk's tags / boxes and paren_match's GLOBAL parent / match
+# for the chunk's elements.  Boxes are (x0, y0, x1, y1) tuples of floats;
+# intersection = max/max/min/min, union = min/min/max/max (DESIGN R9-R11).
+# ---------------------------------------------------------------------------
+INF_BOX = (-float("inf"), -float("inf"), float("inf"), float("inf"))
+EMPTY_BOX = (float("inf"), float("inf"), -float("inf"), -float("inf"))
+
+
+def isect(a, b):
+    return (max(a[0], b[0]), max(a[1], b[1]), min(a[2], b[2]), min(a[3], b[3]))
+
+
+def unite(a, b):
+    return (min(a[0], b[0]), min(a[1], b[1]), max(a[2], b[2]), max(a[3], b[3]))
+
+
+def _contexts(tags, boxes, parent, off, ext):
+    """Clip context of every element: box ∩ ctx(parent) (clip opens and leaves),
+    ctx(parent) for blend opens; a parent in an earlier chunk takes ext[parent]
+    (INF when ext is None: the chunk-local frame)."""
+    n = len(tags)
+    ctx = [None] * n
+    for i in range(n):
+        t = tags[i]
+        if t == CLOSE:
+            continue
+        p = parent[i]
+        if p < 0:
+            pc = INF_BOX
+        elif p < off:
+            pc = ext.get(p, INF_BOX) if ext is not None else INF_BOX
+        else:
+            pc = ctx[p - off]
+        ctx[i] = pc if t == 2 else isect(tuple(boxes[i]), pc)
+    return ctx
+
+
+def bbox_phase1(tags, boxes, parent, match, off):
+    """Final stack of the chunk (opens closed after it or never) with chunk-local
+    cumulative clips, and the chunk's link."""
+    n = len(tags)
+    lctx = _contexts(tags, boxes, parent, off, None)
+    fs = [(off + i, lctx[i]) for i in range(n) if tags[i] in OPEN and (match[i] < 0 or match[i] >= off + n)]
+    link = parent[fs[0][0] - off] if fs else -1
+    return {"off": off, "n": n, "link": link, "fs": fs}
+
+
+def bbox_compose(summaries, g):
+    """True contexts of the final-stack opens of chunks before g (chain over chunks)."""
+    tcc = []
+    for h, sm in enumerate(summaries):
+        t = INF_BOX
+        if sm["link"] >= 0:
+            h2 = max(k for k in range(h) if summaries[k]["off"] <= sm["link"])
+            t = isect(dict(summaries[h2]["fs"])[sm["link"]], tcc[h2])
+        tcc.append(t)
+    ext = {}
+    for h in range(g):
+        for idx, v in summaries[h]["fs"]:
+            ext[idx] = isect(v, tcc[h])
+    return ext
+
+
+def bbox_phase2(tags, boxes, parent, match, off, ext):
+    """Local outputs, the chunk's exports (union, union after each final-stack
+    open) and the closes of earlier chunks' nodes with their prefix unions."""
+    n = len(tags)
+    ctx = _contexts(tags, boxes, parent, off, ext)
+    out = [None] * n
+    leaf = [tags[i] not in OPEN and tags[i] != CLOSE for i in range(n)]
+    for i in range(n):
+        if leaf[i] or tags[i] == 1:
+            out[i] = ctx[i]
+
+    def seg(a, b):  # union of clipped leaves in [a, b) (local)
+        u = EMPTY_BOX
+        for j in range(a, b):
+            if leaf[j]:
+                u = unite(u, out[j])
+        return u
+
+    reports = []
+    for i in range(n):
+        if tags[i] != CLOSE:
+            continue
+        o = match[i]
+        if o < 0:
+            out[i] = EMPTY_BOX
+        elif o >= off:
+            u = seg(o - off + 1, i)
+            out[i] = u
+            if tags[o - off] == 2:
+                out[o - off] = u
+        else:
+            reports.append((off + i, o, seg(0, i)))
+    suc = [(idx, seg(idx - off + 1, n)) for idx, _ in bbox_phase1(tags, boxes, parent, match, off)["fs"]]
+    never = [i for i in range(n) if tags[i] == 2 and match[i] < 0]
+    for i in never:
+        out[i] = seg(i + 1, n)
+    return out, {"tu": seg(0, n), "suc": suc, "reports": reports}, never
+
+
+def bbox_fixup(out, tags, off, g, summaries, exports, never):
+    G = len(exports)
+
+    def chunks(a, b):
+        u = EMPTY_BOX
+        for h in range(a, b + 1):
+            u = unite(u, exports[h]["tu"])
+        return u
+
+    for c, o, pre in exports[g]["reports"]:
+        h = max(k for k in range(G) if summaries[k]["off"] <= o)
+        u = unite(unite(pre, chunks(h + 1, g - 1)), dict(exports[h]["suc"]).get(o, EMPTY_BOX))
+        out[c - off] = u
+    mine = dict(exports[g]["suc"])
+    for k in range(g + 1, G):
+        for c, o, pre in exports[k]["reports"]:
+            if off <= o < off + len(tags) and tags[o - off] == 2:
+                out[o - off] = unite(unite(pre, chunks(g + 1, k - 1)), mine.get(o, EMPTY_BOX))
+    later = chunks(g + 1, G - 1)
+    for i in never:
+        out[i] = unite(out[i], later)
+    return out
+
+
+def bbox_protocol(tags, boxes, parent, match, off, rank, allgather):
+    summaries = allgather(bbox_phase1(tags, boxes, parent, match, off))
+    ext = bbox_compose(summaries, rank)
+    out, exp, never = bbox_phase2(tags, boxes, parent, match, off, ext)
+    exports = allgather(exp)
+    return bbox_fixup(out, tags, off, rank, summaries, exports, never)
