@@ -82,4 +82,41 @@ __device__ __forceinline__ int select_bit(uint32_t m, int j) {
 }
 
 
+// ---------------------------------------------------------------------------
+// Unmatched opens of a run of elements, 4 at a time.  Walking backwards with P
+// = closes to the right still waiting for a partner, an open is unmatched in
+// the run iff P == 0 when it is reached (§3-§4: exactly the opens of the run's
+// Bic b component).  Table entry for (open nibble o, close nibble c, min(P, 4)):
+// bits 0-3 = the nibble's unmatched opens, bits 4-7 = P_out - P_in + 4 (a P of 4
+// or more already matches every open of the nibble).  Index = o | c << 4 | pin << 8.
+// ---------------------------------------------------------------------------
+constexpr int UNM4_ENTRIES = 256 * 5;
+__device__ __forceinline__ uint8_t unm4_entry(int idx) {
+  const int o = idx & 15, c = (idx >> 4) & 15, pin = idx >> 8;
+  int P = pin, mask = 0;
+  for (int j = 3; j >= 0; j--) {
+    if ((c >> j) & 1) P++;
+    else if ((o >> j) & 1) {
+      if (P > 0) P--;
+      else mask |= 1 << j;
+    }
+  }
+  return (uint8_t)(mask | ((P - pin + 4) << 4));
+}
+__device__ __forceinline__ void unm4_fill(uint8_t* tab, int tid, int nthreads) {
+  for (int i = tid; i < UNM4_ENTRIES; i += nthreads) tab[i] = unm4_entry(i);
+}
+// unmatched opens among the 32 elements of (ow, cw), walking backwards from a
+// pending count P (updated)
+__device__ __forceinline__ uint32_t unm32(const uint8_t* tab, uint32_t ow, uint32_t cw, int& P) {
+  uint32_t um = 0;
+#pragma unroll
+  for (int q = 7; q >= 0; q--) {
+    const uint32_t e = tab[((ow >> (4 * q)) & 15u) | (((cw >> (4 * q)) & 15u) << 4) | ((uint32_t)min(P, 4) << 8)];
+    um |= (e & 15u) << (4 * q);
+    P += (int)(e >> 4) - 4;
+  }
+  return um;
+}
+
 }  // namespace tb

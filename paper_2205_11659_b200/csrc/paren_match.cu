@@ -52,56 +52,96 @@ struct Params {
 // ----------------------------------------------------------------------------
 // pass 1
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) pm_reduce(Params p) {
-  __shared__ Bic wtot[NW];
+// One warp per tile, 128 consecutive elements per lane: the lane's Bic from a
+// 4-element table, warp shuffles for the scans (no block barrier).  A lane
+// whose bottom s_l unmatched opens survive the tile finds them with a second
+// table, walking backwards 4 elements at a time (common.cuh unm32).
+constexpr int RL = TILE / 32;  // elements per lane in pm_reduce
+__global__ void __launch_bounds__(256) pm_reduce(Params p) {
   __shared__ uint8_t bic4[256];  // Bic of 4 elements: index = open nibble | close nibble << 4; a | b << 4
-  const int tid = threadIdx.x;
-  const int T = blockIdx.x;
-  const int64_t base = (int64_t)T * TILE;
-  const int64_t tbase = base + (int64_t)tid * K;
-  const bool full = base + TILE <= p.n;
-  static_assert(NT >= 256, "bic4 is filled one entry per thread");
+  __shared__ uint8_t unm4[UNM4_ENTRIES];
+  const int lane = threadIdx.x & 31;
   {
+    const int t = threadIdx.x;
     Bic v{0, 0};
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const Bic e{(tid >> (4 + j)) & 1, (tid >> j) & 1};  // close -> (1, 0), open -> (0, 1)
-      v = bic_combine(v, e);
-    }
-    bic4[tid] = (uint8_t)(v.a | (v.b << 4));
+    for (int j = 0; j < 4; j++) v = bic_combine(v, Bic{(t >> (4 + j)) & 1, (t >> j) & 1});
+    bic4[t] = (uint8_t)(v.a | (v.b << 4));
+    unm4_fill(unm4, t, 256);
   }
-  uint32_t om, cm;
-  classify16(load_tags16(p.tags, p.n, tbase, full), om, cm);
   __syncthreads();
-  Bic tb{0, 0};
+  const int ntiles = (int)((p.n + TILE - 1) / TILE);
+  const int T = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (T >= ntiles) return;
+  const int64_t base = (int64_t)T * TILE, lbase = base + (int64_t)lane * RL;
+  uint32_t om[RL / 32], cm[RL / 32];
+  {
+    uint4 raw[RL / 16];
+    // L1-allocating loads: the lane stride is 128 B, so the first load brings
+    // the warp's 4 KB into L1 and the other seven hit it
 #pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const uint32_t e = bic4[((om >> (4 * q)) & 15u) | (((cm >> (4 * q)) & 15u) << 4)];
-    tb = bic_combine(tb, Bic{(int)(e & 15u), (int)(e >> 4)});
-  }
-  const int a_t = tb.a, b_t = tb.b;
-  Bic ex, sx, tot;
-  block_bic_scans<NW>(Bic{a_t, b_t}, wtot, ex, sx, tot, true);
-  if (tid == 0) p.ctrl.agg[T] = make_int2(tot.a, tot.b);  // the tile scan turns these into heights
-  // slice: this thread's unmatched opens that survive to the tile end sit at
-  // relative heights l_t + k, slice position l_t + k + a_T (the bottom s_t of
-  // the thread's stack; only those threads walk their elements).
-  const int l_t = ex.b - ex.a - a_t;
-  const int s_t = max(b_t - sx.a, 0);
-  if (s_t > 0) {
-    uint32_t S = 0;
-#pragma unroll
-    for (int i = 0; i < K; i++) {
-      const uint32_t bit = 1u << i;
-      if (om & bit) S |= bit;
-      else if ((cm & bit) && S) S ^= 1u << (31 - __clz(S));
+    for (int q = 0; q < RL / 16; q++) {
+      const int64_t g = lbase + 16 * q;
+      raw[q] = g + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags + g)) : load_tags16(p.tags, p.n, g, false);
     }
-    uint32_t m = S;
-    for (int k = 0; k < s_t; k++) {
-      const int bit = __ffs(m) - 1;
-      m &= m - 1;
-      p.slice[base + (l_t + k + tot.a)] = (int)(p.offset + tbase + bit);
-      p.match[tbase + bit] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
+#pragma unroll
+    for (int q = 0; q < RL / 16; q++) {
+      uint32_t o, c;
+      classify16(raw[q], o, c);
+      if (q & 1) {
+        om[q >> 1] |= o << 16;
+        cm[q >> 1] |= c << 16;
+      } else {
+        om[q >> 1] = o;
+        cm[q >> 1] = c;
+      }
+    }
+  }
+  Bic lb{0, 0};
+#pragma unroll
+  for (int w = 0; w < RL / 32; w++) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint32_t e = bic4[((om[w] >> (4 * q)) & 15u) | (((cm[w] >> (4 * q)) & 15u) << 4)];
+      lb = bic_combine(lb, Bic{(int)(e & 15u), (int)(e >> 4)});
+    }
+  }
+  Bic incl = lb, suf = lb;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Bic a{__shfl_up_sync(0xffffffffu, incl.a, off), __shfl_up_sync(0xffffffffu, incl.b, off)};
+    if (lane >= off) incl = bic_combine(a, incl);
+    const Bic b{__shfl_down_sync(0xffffffffu, suf.a, off), __shfl_down_sync(0xffffffffu, suf.b, off)};
+    if (lane + off < 32) suf = bic_combine(suf, b);
+  }
+  const Bic tot{__shfl_sync(0xffffffffu, incl.a, 31), __shfl_sync(0xffffffffu, incl.b, 31)};
+  Bic ex{__shfl_up_sync(0xffffffffu, incl.a, 1), __shfl_up_sync(0xffffffffu, incl.b, 1)};
+  Bic sx{__shfl_down_sync(0xffffffffu, suf.a, 1), __shfl_down_sync(0xffffffffu, suf.b, 1)};
+  if (lane == 0) ex = Bic{0, 0};
+  if (lane == 31) sx = Bic{0, 0};
+  if (lane == 0) p.ctrl.agg[T] = make_int2(tot.a, tot.b);  // the tile scan turns these into heights
+  // slice: this lane's unmatched opens that survive to the tile end sit at
+  // relative heights l + k, slice position l + k + a_T (k = rank from the bottom)
+  const int l = ex.b - ex.a - lb.a;
+  const int s_l = max(lb.b - sx.a, 0);
+  if (s_l > 0) {
+    // the lane's unmatched opens (backward, 4 at a time); the bottom s_l survive
+    uint32_t um[RL / 32];
+    int P = 0;
+#pragma unroll
+    for (int w = RL / 32 - 1; w >= 0; w--) um[w] = unm32(unm4, om[w], cm[w], P);
+    int k = 0;
+#pragma unroll
+    for (int w = 0; w < RL / 32; w++) {
+      uint32_t m = um[w];
+      while (m && k < s_l) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t x = lbase + 32 * w + j;
+        p.slice[base + (l + k + tot.a)] = (int)(p.offset + x);
+        p.match[x] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
+        k++;
+      }
     }
   }
 }
@@ -372,7 +412,7 @@ cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, voi
   if (n <= 0) return cudaSuccess;
   const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
   pm::Params p = pm_params(tags, n, match, nullptr, ws, init);
-  TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)ntiles, pm::NT, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p)));
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   return tile_scan_launch(p.ctrl, ntiles, p.init.a, p.init.b, stream);
