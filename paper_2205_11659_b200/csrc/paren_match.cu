@@ -191,6 +191,7 @@ __device__ __forceinline__ int find_runs(Smem& s, const Ctrl& c, int cur, int& f
   return cur;
 }
 
+template <bool SHARD>
 __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -270,12 +271,13 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
   const uint32_t mo = w.om & ~w.S;
   const int tb32 = (int)(p.offset + tbase);  // global indices fit in int32 (N <= 2^31 - 1)
   const int gbase = (int)(p.offset + base);
-  // value of a reference: global index, -1 for the root, or an init-stack entry
+  // value of a reference: global index, -1 for the root, or (shard mode) an
+  // entry of the stack provided by the exchange
   auto resolve = [&](int ref, bool& from_init) -> int {
     from_init = false;
     if (ref >= 0) return gbase + ref;
     const int e = s.inc[-ref - 1];
-    if (e <= -2) {
+    if (SHARD && e <= -2) {
       from_init = true;
       return -e - 2;
     }
@@ -297,15 +299,6 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
       int m = (w.om & bit) ? ((mo & bit) ? tb32 + nib(w.mlo, w.mhi, i) : SKIP) : -1;
       const bool uc = (w.ucm & bit) != 0u;
       m = (w.cm & bit) ? (uc ? val : local_par) : m;
-      if (uc && val >= 0) {
-        if (!vinit) {
-          p.match[val - p.offset] = tb32 + i;  // partner opened in an earlier thread / tile
-        } else {
-          // partner lives in an earlier shard: record (open, close) for the exchange
-          const int k = p.init.b - H + (-ref - 1);
-          p.pairs[k] = make_int2(val, tb32 + i);
-        }
-      }
       dcur += uc;
       if (uc) {
         ref = s.extv[dcur][tid];
@@ -331,6 +324,29 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
           if (mv[j] != SKIP) p.match[g] = mv[j];
         }
       }
+    }
+  }
+  // closes whose partner opened in an earlier thread / tile write match[open]
+  // (the d-th such close pops the entry at depth d of the thread's start stack)
+  {
+    uint32_t q = w.ucm;
+    int d = 0;
+#pragma unroll 1
+    while (q) {
+      const int i = __ffs(q) - 1;
+      q &= q - 1;
+      const int r = s.extv[d][tid];
+      bool from_init;
+      const int v = resolve(r, from_init);
+      if (v >= 0) {
+        if (!SHARD || !from_init) {
+          p.match[v - p.offset] = tb32 + i;
+        } else {  // partner lives in an earlier shard: record (open, close) for the exchange
+          const int k = p.init.b - H + (-r - 1);
+          p.pairs[k] = make_int2(v, tb32 + i);
+        }
+      }
+      d++;
     }
   }
 }
@@ -397,8 +413,11 @@ static pm::Params pm_params(const uint8_t* tags, int64_t n, int32_t* match, int3
 static cudaError_t pm_configure() {
   static bool configured = false;
   if (!configured) {
-    cudaError_t err = cudaFuncSetAttribute(pm::pm_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t err = cudaFuncSetAttribute(pm::pm_finish<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)sizeof(pm::Smem));
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(pm::pm_finish<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(pm::Smem));
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(pm::pm_summary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(pm::Smem));
     if (err != cudaSuccess) return err;
@@ -425,7 +444,10 @@ cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int
   if (err != cudaSuccess) return err;
   const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
   pm::Params p = pm_params(tags, n, match, parent, ws, init);
-  TB_LAUNCH(stream, "pm_finish", (pm::pm_finish<<<(unsigned)ntiles, pm::NT, sizeof(pm::Smem), stream>>>(p)));
+  if (p.init_stack == nullptr && p.pairs == nullptr)  // no stack provided by a shard exchange
+    TB_LAUNCH(stream, "pm_finish", (pm::pm_finish<false><<<(unsigned)ntiles, pm::NT, sizeof(pm::Smem), stream>>>(p)));
+  else
+    TB_LAUNCH(stream, "pm_finish", (pm::pm_finish<true><<<(unsigned)ntiles, pm::NT, sizeof(pm::Smem), stream>>>(p)));
   return cudaGetLastError();
 }
 
