@@ -89,6 +89,20 @@ int paren_match_ws(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *
                    void *d_workspace, size_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
+ * paren_match_bytes — parenthesis matching over raw text (SURVEY §8(f) NEXT
+ * row 3; the parsing use of the method)
+ *
+ * d_bytes     : device uint8[n] text (16-byte aligned).
+ * h_class_map : HOST uint8[256]; byte value -> tag class (1 or 2 = open,
+ *               3 = close, anything else = leaf; e.g. '{' '[' -> 1,
+ *               '}' ']' -> 3 for JSON brackets).  Read during the call.
+ * d_match, d_parent: as paren_match, for the classified stream.  Brackets are
+ * classified per byte (string literals and escapes are not special).
+ * ------------------------------------------------------------------------ */
+int paren_match_bytes(const uint8_t *d_bytes, int64_t n, const uint8_t *h_class_map, int32_t *d_match,
+                      int32_t *d_parent, void *stream);
+
+/* ------------------------------------------------------------------------
  * tree_bbox — clip intersections and blend unions (§6; §9)
  *
  * d_tags      : device uint8[n] as above.

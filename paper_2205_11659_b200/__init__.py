@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["paren_match", "tree_bbox", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["paren_match", "paren_match_bytes", "tree_bbox", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard"]
 
@@ -54,6 +54,7 @@ def load():
                 "tree_bbox_host": ([P, P, I64, P, P], ctypes.c_int),
                 "tree_bbox_matched": ([P, P, P, P, I64, P, P], ctypes.c_int),
                 "paren_match_tree_bbox_host": ([P, P, I64, P, P, P, P], ctypes.c_int),
+                "paren_match_bytes": ([P, I64, P, P, P, P], ctypes.c_int),
                 "tree_bbox_matched_ws": ([P, P, P, P, I64, P, P, SZ, P], ctypes.c_int),
                 "tree_bbox_matched_workspace_bytes": ([I64], SZ),
                 "tb_count_unmatched": ([P, I64, P, P, P], ctypes.c_int),
@@ -114,6 +115,28 @@ def paren_match(tags: torch.Tensor, match: torch.Tensor | None = None,
     with torch.cuda.device(tags.device):
         _check(lib.paren_match(tags.data_ptr(), n, match.data_ptr(), parent.data_ptr(),
                                _stream(tags.device)))
+    return match, parent
+
+
+def paren_match_bytes(text: torch.Tensor, class_map: bytes, match: torch.Tensor | None = None,
+                      parent: torch.Tensor | None = None):
+    """Parenthesis matching over raw text bytes (uint8 CUDA [n]); class_map: 256
+    bytes mapping each byte value to a tag class (1/2 open, 3 close, else leaf)."""
+    lib = load()
+    _need_cuda(text, "text", torch.uint8)
+    if len(class_map) != 256:
+        raise ValueError("class_map must have 256 entries")
+    n = text.numel()
+    if match is None:
+        match = torch.empty(n, dtype=torch.int32, device=text.device)
+    if parent is None:
+        parent = torch.empty(n, dtype=torch.int32, device=text.device)
+    _need_cuda(match, "match", torch.int32)
+    _need_cuda(parent, "parent", torch.int32)
+    cm = (ctypes.c_uint8 * 256)(*bytes(class_map))
+    with torch.cuda.device(text.device):
+        _check(lib.paren_match_bytes(text.data_ptr(), n, cm, match.data_ptr(), parent.data_ptr(),
+                                     _stream(text.device)))
     return match, parent
 
 

@@ -359,6 +359,25 @@ int paren_match_tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, 
   return TB_OK;
 }
 
+int paren_match_bytes(const uint8_t* d_bytes, int64_t n, const uint8_t* h_class_map, int32_t* d_match,
+                      int32_t* d_parent, void* stream) {
+  g_err[0] = 0;
+  int r = pm_checks(d_bytes, n, d_match, d_parent);
+  if (r || n == 0) return r;
+  if (!h_class_map) return fail(TB_ERR_ARG, "null class map");
+  const size_t nb_t = ((size_t)n + 255) & ~(size_t)255;
+  const size_t need = nb_t + tb::pm_workspace_bytes(n);
+  void* ws = nullptr;
+  r = get_ws(stream, 7, need, &ws);
+  if (r) return r;
+  uint8_t* tags = (uint8_t*)ws;
+  cudaError_t e = tb::classify_bytes_launch(d_bytes, n, h_class_map, tags, (cudaStream_t)stream);
+  if (e == cudaSuccess)
+    e = tb::pm_launch(tags, n, d_match, d_parent, (char*)ws + nb_t, nullptr, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "paren_match_bytes launch");
+  return TB_OK;
+}
+
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }

@@ -92,6 +92,10 @@ cudaError_t bbm_fixup_launch(const uint8_t* tags, const float* leaf_bbox, const 
 cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, float* out, cudaStream_t s);
 cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int32_t* parent, cudaStream_t s);
 
+// raw bytes -> tag bytes through a 256-entry class map (host pointer)
+cudaError_t classify_bytes_launch(const uint8_t* in, int64_t n, const uint8_t* class_map, uint8_t* out,
+                                  cudaStream_t stream);
+
 size_t bic_count_workspace_bytes(int64_t n);
 cudaError_t bic_count_launch(const uint8_t* tags, int64_t n, void* ws, int64_t* d_out2,
                              cudaStream_t stream);

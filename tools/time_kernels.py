@@ -39,10 +39,13 @@ def main():
         n = tags.numel()
         m = torch.empty(n, dtype=torch.int32, device="cuda")
         p = torch.empty(n, dtype=torch.int32, device="cuda")
-        med, mn = time_fn(lambda: tb.paren_match(tags, m, p), flush=flush)
+        if name.upper() == "J1":  # raw text bytes through the JSON class map
+            med, mn = time_fn(lambda: tb.paren_match_bytes(tags, scenegen.JSON_CLASS_MAP, m, p), flush=flush)
+        else:
+            med, mn = time_fn(lambda: tb.paren_match(tags, m, p), flush=flush)
         row = {"config": name, "n": n, "pm_ms": med, "pm_min_ms": mn,
                "pm_Gelem_s": n / med / 1e6, "pm_GBs": 9 * n / med / 1e6}
-        if args.bbox:
+        if args.bbox and name.upper() != "J1":
             boxes = scenegen.boxes(n, 7, tags, device="cuda")
             out = torch.empty_like(boxes)
             med, mn = time_fn(lambda: tb.tree_bbox(tags, boxes, out), flush=flush)
