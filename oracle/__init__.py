@@ -53,6 +53,8 @@ def _load():
             lib.oracle_tree_bbox.restype = ctypes.c_int
             lib.oracle_count_unmatched.argtypes = [P, ctypes.c_int64, P, P]
             lib.oracle_count_unmatched.restype = ctypes.c_int
+            lib.oracle_tree_transform.argtypes = [P, P, ctypes.c_int64, P]
+            lib.oracle_tree_transform.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -83,6 +85,20 @@ def tree_bbox(tags: np.ndarray, leaf_bbox: np.ndarray, out: np.ndarray | None = 
     res = out if out is not None else np.empty((n, 4), np.float32)
     if _load().oracle_tree_bbox(_ptr(tags), _ptr(boxes), n, _ptr(res)) != 0:
         raise MemoryError("oracle_tree_bbox: allocation failed")
+    return res
+
+
+def tree_transform(tags: np.ndarray, local: np.ndarray):
+    """Affine transforms composed down the tree (R15), fp64.  local: float32
+    [n, 6] (a, b, c, d, tx, ty); returns float64 [n, 6]."""
+    tags = np.ascontiguousarray(tags, dtype=np.uint8)
+    loc = np.ascontiguousarray(local, dtype=np.float32).reshape(-1, 6)
+    n = tags.shape[0]
+    if loc.shape[0] != n:
+        raise ValueError("local must have n rows")
+    res = np.empty((n, 6), np.float64)
+    if _load().oracle_tree_transform(_ptr(tags), _ptr(loc), n, _ptr(res)) != 0:
+        raise MemoryError("oracle_tree_transform: allocation failed")
     return res
 
 

@@ -196,3 +196,57 @@ int oracle_count_unmatched(const uint8_t *tags, int64_t n, int64_t *a, int64_t *
     *a = under; *b = depth;
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* oracle_tree_transform — a generic monoid payload down the tree           */
+/* ("it can compute any monoid")      */
+/*                                                                           */
+/* The clip stack of P:26 with its intersection replaced by composition of  */
+/* 2D affine transforms (reading R15): every leaf and open gets             */
+/*     world = world(enclosing open) ∘ local        (root: identity)         */
+/* a close echoes the world transform of the node it closes (P:300's        */
+/* "result at the close"); an unmatched close gets the identity (R3).       */
+/* Transform layout: 6 floats (a, b, c, d, tx, ty) meaning                  */
+/*     p -> [[a, b], [c, d]] p + (tx, ty);   (A ∘ B)(p) = A(B(p)).           */
+/* Composition is neither commutative nor idempotent.  Computed in fp64.   */
+/* local: n*6 floats in; world: n*6 doubles out.  Returns 0, -1 on OOM.     */
+/* ------------------------------------------------------------------------ */
+typedef struct { double a, b, c, d, tx, ty; } xf_t;
+
+static xf_t xf_compose(xf_t A, xf_t B)
+{
+    xf_t r;
+    r.a = A.a * B.a + A.b * B.c;
+    r.b = A.a * B.b + A.b * B.d;
+    r.c = A.c * B.a + A.d * B.c;
+    r.d = A.c * B.b + A.d * B.d;
+    r.tx = A.a * B.tx + A.b * B.ty + A.tx;
+    r.ty = A.c * B.tx + A.d * B.ty + A.ty;
+    return r;
+}
+
+int oracle_tree_transform(const uint8_t *tags, const float *local, int64_t n, double *world)
+{
+    const xf_t I = { 1, 0, 0, 1, 0, 0 };
+    xf_t *stack = (xf_t *)malloc((size_t)(n + 1) * sizeof(xf_t));
+    if (!stack) return -1;
+    int64_t sp = 0;
+    stack[sp++] = I;                                  /* the root */
+    for (int64_t i = 0; i < n; i++) {
+        const uint8_t t = tags[i];
+        xf_t w;
+        if (t == TAG_CLOSE) {
+            if (sp > 1) w = stack[--sp];              /* the node it closes */
+            else w = I;                               /* R3 */
+        } else {
+            const float *l = local + 6 * i;
+            const xf_t L = { l[0], l[1], l[2], l[3], l[4], l[5] };
+            w = xf_compose(stack[sp - 1], L);
+            if (t == TAG_OPEN_CLIP || t == TAG_OPEN_BLEND) stack[sp++] = w;
+        }
+        double *o = world + 6 * i;
+        o[0] = w.a; o[1] = w.b; o[2] = w.c; o[3] = w.d; o[4] = w.tx; o[5] = w.ty;
+    }
+    free(stack);
+    return 0;
+}
