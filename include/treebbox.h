@@ -150,6 +150,24 @@ int tree_bbox_matched_ws(const uint8_t *d_tags, const float *d_leaf_bbox, const 
                          size_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
+ * tree_transform — a generic monoid payload down the tree (SURVEY §8(f) NEXT
+ * row 2; "it can compute any monoid"): 2D affine transforms,
+ * composition being neither commutative nor idempotent (reading R15).
+ *
+ * d_local : device float32[n][6] (a, b, c, d, tx, ty): p -> [[a,b],[c,d]] p + t.
+ *           Read for leaves and opens (clip and blend alike); ignored for closes.
+ * d_match, d_parent: paren_match's outputs for d_tags.
+ * d_world : device float32[n][6] out: leaf / open: world(enclosing open) ∘ local
+ *           (root: identity); close: the world of the node it closes;
+ *           unmatched close: identity.  fp32 with fused multiply-adds; the
+ *           association order differs from the sequential walk, so results
+ *           match it exactly only when every product is exact (DESIGN R15).
+ * All device pointers 16-byte aligned; world must not overlap an input.
+ * ------------------------------------------------------------------------ */
+int tree_transform(const uint8_t *d_tags, const float *d_local, const int32_t *d_match, const int32_t *d_parent,
+                   int64_t n, float *d_world, void *stream);
+
+/* ------------------------------------------------------------------------
  * Host-buffer variants (end-to-end API): h_* are host pointers (pinned or
  * pageable).  Inputs are copied to library-owned device buffers on `stream`,
  * the device call runs, outputs are copied back, and the call synchronises

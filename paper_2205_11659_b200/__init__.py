@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["paren_match", "paren_match_bytes", "tree_bbox", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard"]
 
@@ -55,6 +55,7 @@ def load():
                 "tree_bbox_matched": ([P, P, P, P, I64, P, P], ctypes.c_int),
                 "paren_match_tree_bbox_host": ([P, P, I64, P, P, P, P], ctypes.c_int),
                 "paren_match_bytes": ([P, I64, P, P, P, P], ctypes.c_int),
+                "tree_transform": ([P, P, P, P, I64, P, P], ctypes.c_int),
                 "tree_bbox_matched_ws": ([P, P, P, P, I64, P, P, SZ, P], ctypes.c_int),
                 "tree_bbox_matched_workspace_bytes": ([I64], SZ),
                 "tb_count_unmatched": ([P, I64, P, P, P], ctypes.c_int),
@@ -177,6 +178,26 @@ def tree_bbox_matched(tags: torch.Tensor, leaf_bbox: torch.Tensor, match: torch.
         _check(lib.tree_bbox_matched(tags.data_ptr(), leaf_bbox.data_ptr(), match.data_ptr(), parent.data_ptr(), n,
                                      node_bbox.data_ptr(), _stream(tags.device)))
     return node_bbox
+
+
+def tree_transform(tags: torch.Tensor, local: torch.Tensor, match: torch.Tensor, parent: torch.Tensor,
+                   world: torch.Tensor | None = None):
+    """2D affine transforms composed down the tree (local: float32 CUDA [n, 6])."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    _need_cuda(local, "local", torch.float32)
+    _need_cuda(match, "match", torch.int32)
+    _need_cuda(parent, "parent", torch.int32)
+    n = tags.numel()
+    if local.numel() != 6 * n:
+        raise ValueError("local must be [n, 6]")
+    if world is None:
+        world = torch.empty((n, 6), dtype=torch.float32, device=tags.device)
+    _need_cuda(world, "world", torch.float32)
+    with torch.cuda.device(tags.device):
+        _check(lib.tree_transform(tags.data_ptr(), local.data_ptr(), match.data_ptr(), parent.data_ptr(), n,
+                                  world.data_ptr(), _stream(tags.device)))
+    return world
 
 
 def workspace_bytes(n: int) -> dict:

@@ -378,6 +378,27 @@ int paren_match_bytes(const uint8_t* d_bytes, int64_t n, const uint8_t* h_class_
   return TB_OK;
 }
 
+int tree_transform(const uint8_t* d_tags, const float* d_local, const int32_t* d_match, const int32_t* d_parent,
+                   int64_t n, float* d_world, void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r || n == 0) return r;
+  if (!d_tags || !d_local || !d_match || !d_parent || !d_world) return fail(TB_ERR_ARG, "null pointer with n > 0");
+  if (!aligned16(d_tags) || !aligned16(d_local) || !aligned16(d_match) || !aligned16(d_parent) ||
+      !aligned16(d_world))
+    return fail(TB_ERR_ALIGN, "tags, local, match, parent and world must be 16-byte aligned");
+  const size_t nb = (size_t)n * 24, n4 = (size_t)n * 4;
+  if (overlap(d_world, nb, d_local, nb) || overlap(d_world, nb, d_tags, (size_t)n) ||
+      overlap(d_world, nb, d_match, n4) || overlap(d_world, nb, d_parent, n4))
+    return fail(TB_ERR_ALIAS, "world overlaps an input");
+  void* ws = nullptr;
+  r = get_ws(stream, 8, tb::tt_workspace_bytes(n), &ws);
+  if (r) return r;
+  cudaError_t e = tb::tt_launch(d_tags, d_local, d_match, d_parent, n, d_world, ws, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_transform launch");
+  return TB_OK;
+}
+
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }

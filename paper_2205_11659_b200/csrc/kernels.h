@@ -92,6 +92,11 @@ cudaError_t bbm_fixup_launch(const uint8_t* tags, const float* leaf_bbox, const 
 cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, float* out, cudaStream_t s);
 cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int32_t* parent, cudaStream_t s);
 
+// 2D affine transforms composed down the tree (tree_transform.cu)
+size_t tt_workspace_bytes(int64_t n);
+cudaError_t tt_launch(const uint8_t* tags, const float* local, const int32_t* match, const int32_t* parent,
+                      int64_t n, float* world, void* ws, cudaStream_t stream);
+
 // raw bytes -> tag bytes through a 256-entry class map (host pointer)
 cudaError_t classify_bytes_launch(const uint8_t* in, int64_t n, const uint8_t* class_map, uint8_t* out,
                                   cudaStream_t stream);

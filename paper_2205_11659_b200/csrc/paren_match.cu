@@ -139,7 +139,6 @@ __global__ void __launch_bounds__(256) pm_reduce(Params p) {
         m &= m - 1;
         const int64_t x = lbase + 32 * w + j;
         p.slice[base + (l + k + tot.a)] = (int)(p.offset + x);
-        p.match[x] = -1;  // placeholder: a later tile's close may overwrite it in pass 2
         k++;
       }
     }
@@ -378,6 +377,22 @@ __global__ void __launch_bounds__(NT) pm_summary(Params p, int ntiles, int32_t* 
   }
 }
 
+// Opens never closed (R4) get match = -1; every other open's match is written
+// by its close in pm_finish.  Entry k of tile U's slice sits at height L_U + k
+// and survives to the end iff it lies below the low-water mark of every later
+// tile (F1; smin from the tile scan): each tile marks its bottom
+// min(b_U, smin_U - L_U) entries (one warp per tile).
+__global__ void __launch_bounds__(256) pm_unmatched(Params p, int ntiles) {
+  const int lane = threadIdx.x & 31;
+  const int U = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (U >= ntiles) return;
+  const int L = (int)__ldg(p.ctrl.lw + U) - 1;
+  const int bU = __ldg(p.ctrl.agg + U).y;
+  const int sm = __ldg(p.ctrl.smin + U);
+  const int surv = min(bU, max(sm == INT_MAX ? bU : sm - L, 0));
+  for (int k = lane; k < surv; k += 32) p.match[__ldcg(p.slice + (int64_t)U * TILE + k) - p.offset] = -1;
+}
+
 }  // namespace pm
 
 size_t pm_workspace_bytes(int64_t n) {
@@ -420,6 +435,7 @@ static cudaError_t pm_configure() {
                                  (int)sizeof(pm::Smem));
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(pm::pm_summary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(pm::Smem));
+
     if (err != cudaSuccess) return err;
     configured = true;
   }
@@ -431,10 +447,15 @@ cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, voi
   if (n <= 0) return cudaSuccess;
   const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
   pm::Params p = pm_params(tags, n, match, nullptr, ws, init);
-  TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p)));
-  cudaError_t err = cudaGetLastError();
+  cudaError_t err = pm_configure();
   if (err != cudaSuccess) return err;
-  return tile_scan_launch(p.ctrl, ntiles, p.init.a, p.init.b, stream);
+  TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p)));
+  err = cudaGetLastError();
+  if (err == cudaSuccess) err = tile_scan_launch(p.ctrl, ntiles, p.init.a, p.init.b, stream);
+  if (err != cudaSuccess) return err;
+  TB_LAUNCH(stream, "pm_unmatched",
+            (pm::pm_unmatched<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p, (int)ntiles)));
+  return cudaGetLastError();
 }
 
 cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,

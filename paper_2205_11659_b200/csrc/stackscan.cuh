@@ -17,12 +17,13 @@ struct Ctrl {
   int32_t* hstart;           // [ntiles] stack height at the tile start (written with lw)
   int2* agg;                 // [ntiles] Bic value (a, b) of each tile (reduce pass)
   int2* total;               // [1] Bic value of the whole stream (after the tile scan)
+  int* smin;                 // [ntiles] min low-water mark over the later tiles (INT_MAX: none)
   uint32_t* lv[HLEVELS];     // lv[k][g] = 1 + min L over tiles [g*32^k, (g+1)*32^k)
 };
 
 // Sizes (in elements) of the control arrays for `ntiles` tiles.
 struct CtrlLayout {
-  size_t off_lw, off_h, off_agg, off_total, off_lv[HLEVELS], bytes;
+  size_t off_lw, off_h, off_agg, off_total, off_smin, off_lv[HLEVELS], bytes;
   __host__ __device__ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
   __host__ __device__ explicit CtrlLayout(int64_t ntiles) {
     size_t o = 0;
@@ -30,6 +31,7 @@ struct CtrlLayout {
     off_h = o; o = align256(o + 4 * (size_t)ntiles);
     off_agg = o; o = align256(o + 8 * (size_t)ntiles);
     off_total = o; o = align256(o + 8);
+    off_smin = o; o = align256(o + 4 * (size_t)ntiles);
     int64_t m = ntiles;
     off_lv[0] = 0;
     for (int k = 1; k < HLEVELS; k++) {
@@ -45,6 +47,7 @@ struct CtrlLayout {
     c.hstart = (int32_t*)(b + off_h);
     c.agg = (int2*)(b + off_agg);
     c.total = (int2*)(b + off_total);
+    c.smin = (int*)(b + off_smin);
     c.lv[0] = c.lw;
     for (int k = 1; k < HLEVELS; k++) {
       c.lv[k] = (uint32_t*)(b + off_lv[k]);

@@ -6,6 +6,7 @@
 // owner search (F1).  Two warp-shuffle passes over each warp's contiguous
 // range of tiles with a block-level exclusive scan of the warp totals in
 // between — a reduce-then-scan at tile granularity.
+#include <climits>
 #include "kernels.h"
 #include "stackscan.cuh"
 
@@ -25,6 +26,7 @@ __device__ __forceinline__ Bic warp_incl_scan(Bic v, int lane) {
 
 __global__ void __launch_bounds__(NT) tile_scan(Ctrl c, int ntiles, Bic init) {
   __shared__ Bic wt[NW];
+  __shared__ int wmin[NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int span = ((ntiles + NW - 1) / NW + 31) & ~31;
   const int t0 = warp * span, t1 = min(t0 + span, ntiles);
@@ -47,6 +49,7 @@ __global__ void __launch_bounds__(NT) tile_scan(Ctrl c, int ntiles, Bic init) {
     *c.total = make_int2(tot.a, tot.b);
   }
   // pass B: exclusive prefix of every tile -> start height, low-water mark
+  int lmin = INT_MAX;
   for (int t = t0; t < t1; t += 32) {
     const int i = t + lane;
     const int2 g = i < t1 ? __ldcg(c.agg + i) : make_int2(0, 0);
@@ -57,9 +60,31 @@ __global__ void __launch_bounds__(NT) tile_scan(Ctrl c, int ntiles, Bic init) {
     if (i < t1) {
       c.hstart[i] = e.b;
       c.lw[i] = (uint32_t)max(e.b - g.x, 0) + 1u;
+      lmin = min(lmin, max(e.b - g.x, 0));
     }
     const Bic last{__shfl_sync(0xffffffffu, x.a, 31), __shfl_sync(0xffffffffu, x.b, 31)};
     pre = bic_combine(pre, last);
+  }
+  // pass C: smin[i] = min L over tiles > i (which of a tile's slice entries
+  // survive to the end of the stream, F1), backwards over each warp's range
+  lmin = __reduce_min_sync(0xffffffffu, lmin);
+  if (lane == 0) wmin[warp] = lmin;
+  __syncthreads();
+  int after = INT_MAX;
+  for (int w = warp + 1; w < NW; w++) after = min(after, wmin[w]);
+  for (int t = t0 + ((t1 - t0 - 1) & ~31); t1 > t0 && t >= t0; t -= 32) {
+    const int i = t + lane;
+    const int v = i < t1 ? (int)__ldcg(c.lw + i) - 1 : INT_MAX;
+    int x = v;  // min over lanes >= lane
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_down_sync(0xffffffffu, x, off);
+      if (lane + off < 32) x = min(x, y);
+    }
+    int ex = __shfl_down_sync(0xffffffffu, x, 1);
+    if (lane == 31) ex = INT_MAX;
+    if (i < t1) c.smin[i] = min(ex, after);
+    after = min(after, __shfl_sync(0xffffffffu, x, 0));
   }
   // 32-ary min hierarchy over the low-water marks (full groups are complete)
   int m = ntiles;

@@ -32,6 +32,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C2,C3,C4,C5")
     ap.add_argument("--bbox", action="store_true")
+    ap.add_argument("--transform", action="store_true", help="also time tree_transform (57 B/element)")
     args = ap.parse_args()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for name in args.configs.split(","):
@@ -50,6 +51,15 @@ def main():
             out = torch.empty_like(boxes)
             med, mn = time_fn(lambda: tb.tree_bbox(tags, boxes, out), flush=flush)
             row.update({"tb_ms": med, "tb_Gelem_s": n / med / 1e6, "tb_GBs": 33 * n / med / 1e6})
+        if args.transform and name.upper() != "J1":
+            tb.paren_match(tags, m, p)
+            loc = torch.zeros((n, 6), dtype=torch.float32, device="cuda")
+            loc[:, 0] = 1
+            loc[:, 3] = 1
+            loc[:, 4:] = torch.rand((n, 2), device="cuda")
+            world = torch.empty_like(loc)
+            med, mn = time_fn(lambda: tb.tree_transform(tags, loc, m, p, world), flush=flush)
+            row.update({"tt_ms": med, "tt_Gelem_s": n / med / 1e6, "tt_GBs": 57 * n / med / 1e6})
         print(json.dumps(row), flush=True)
 
 
