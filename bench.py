@@ -215,7 +215,7 @@ def main():
             tb.tree_bbox_matched(tags, boxes, match, parent, out)
         else:
             shard.paren_match(tags, match, parent)
-            shard.tree_bbox(tags, boxes, out)
+            shard.tree_bbox_matched(tags, boxes, match, parent, out)
 
     def barrier():
         if world > 1:

@@ -215,6 +215,11 @@ int paren_match_shard(const uint8_t *d_tags, int64_t n_local, int64_t offset, in
  * finishes the nodes that span chunks (F4). */
 int tree_bbox_shard(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n_local, int64_t offset,
                     float *d_node_bbox, void *comm, void *stream);
+/* The same from a matching already computed by paren_match_shard (d_match /
+ * d_parent: the chunk's n_local entries, GLOBAL indices). */
+int tree_bbox_matched_shard(const uint8_t *d_tags, const float *d_leaf_bbox, const int32_t *d_match,
+                            const int32_t *d_parent, int64_t n_local, int64_t offset, float *d_node_bbox, void *comm,
+                            void *stream);
 
 /* ------------------------------------------------------------------------
  * Validation helper: the global Bic of the stream: a = closes with

@@ -66,6 +66,7 @@ def load():
                 "tb_debug_paren_match_vshard": ([P, I64, ctypes.c_int, P, P, P], ctypes.c_int),
                 "tb_debug_tree_bbox_vshard": ([P, P, I64, ctypes.c_int, P, P], ctypes.c_int),
                 "tree_bbox_shard": ([P, P, I64, I64, P, P, P], ctypes.c_int),
+                "tree_bbox_matched_shard": ([P, P, P, P, I64, I64, P, P, P], ctypes.c_int),
                 "tb_launch_count": ([], ctypes.c_longlong),
                 "tb_profile_enable": ([ctypes.c_int], ctypes.c_int),
                 "tb_profile_read": ([ctypes.c_char_p, SZ], ctypes.c_int),
@@ -317,6 +318,17 @@ class ShardContext:
         with torch.cuda.device(tags.device):
             _check(lib.tree_bbox_shard(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), self.offset,
                                        node_bbox.data_ptr(), self.comm, _stream(tags.device)))
+        return node_bbox
+
+    def tree_bbox_matched(self, tags: torch.Tensor, leaf_bbox: torch.Tensor, match: torch.Tensor,
+                          parent: torch.Tensor, node_bbox: torch.Tensor):
+        """Boxes from this rank's slice of the global matching (paren_match above)."""
+        lib = load()
+        _need_cuda(tags, "tags", torch.uint8)
+        with torch.cuda.device(tags.device):
+            _check(lib.tree_bbox_matched_shard(tags.data_ptr(), leaf_bbox.data_ptr(), match.data_ptr(),
+                                               parent.data_ptr(), tags.numel(), self.offset, node_bbox.data_ptr(),
+                                               self.comm, _stream(tags.device)))
         return node_bbox
 
     def close(self):

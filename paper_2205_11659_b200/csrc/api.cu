@@ -13,6 +13,8 @@
 namespace tb {
 cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* match, int32_t* parent,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err);
+cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t* match, const int32_t* parent,
+                           int64_t n, int64_t off, float* out, ncclComm_t comm, cudaStream_t s, int* nccl_err);
 cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, float* out,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err);
 }
@@ -490,6 +492,26 @@ int tree_bbox_shard(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n_l
                                     (cudaStream_t)stream, &nerr);
   if (nerr) return fail(TB_ERR_NCCL, "NCCL error %d", nerr);
   if (e != cudaSuccess) return cuda_fail(e, "tree_bbox_shard");
+  return TB_OK;
+#else
+  return fail(TB_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+int tree_bbox_matched_shard(const uint8_t* d_tags, const float* d_leaf_bbox, const int32_t* d_match,
+                            const int32_t* d_parent, int64_t n_local, int64_t offset, float* d_node_bbox, void* comm,
+                            void* stream) {
+  g_err[0] = 0;
+  int r = bbm_checks(d_tags, d_leaf_bbox, d_match, d_parent, n_local, d_node_bbox);
+  if (r) return r;
+  if (offset < 0 || offset + n_local > kMaxN) return fail(TB_ERR_ARG, "offset + n_local out of range");
+  if (!comm) return fail(TB_ERR_ARG, "null communicator");
+#ifdef TB_WITH_NCCL
+  int nerr = 0;
+  cudaError_t e = tb::bbm_nccl_shard(d_tags, d_leaf_bbox, d_match, d_parent, n_local, offset, d_node_bbox,
+                                     (ncclComm_t)comm, (cudaStream_t)stream, &nerr);
+  if (nerr) return fail(TB_ERR_NCCL, "NCCL error %d", nerr);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_bbox_matched_shard");
   return TB_OK;
 #else
   return fail(TB_ERR_NCCL, "built without NCCL");

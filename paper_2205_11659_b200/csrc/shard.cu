@@ -344,9 +344,9 @@ cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, 
 cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* match, int32_t* parent,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err);
 
-// One rank: paren_match over the shards (global match / parent), then the boxes.
-cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, float* out,
-                          ncclComm_t comm, cudaStream_t s, int* nccl_err) {
+// One rank: the boxes from the global matching (match / parent of the chunk).
+cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t* match, const int32_t* parent,
+                           int64_t n, int64_t off, float* out, ncclComm_t comm, cudaStream_t s, int* nccl_err) {
   *nccl_err = 0;
   int G = 0, g = 0;
   if (ncclCommCount(comm, &G) != ncclSuccess || ncclCommUserRank(comm, &g) != ncclSuccess) {
@@ -357,12 +357,7 @@ cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int
     if (r != ncclSuccess) *nccl_err = (int)r;
     return r == ncclSuccess;
   };
-  int32_t* mp = nullptr;
-  const int64_t n64 = (std::max<int64_t>(n, 1) + 63) & ~int64_t(63);  // keeps parent 16-byte aligned
-  cudaError_t e = cudaMalloc(&mp, 8 * (size_t)n64);
-  int32_t* match = mp;
-  int32_t* parent = mp + n64;
-  if (e == cudaSuccess) e = pm_nccl_shard(tags, n, off, match, parent, comm, s, nccl_err);
+  cudaError_t e = cudaSuccess;
   BbmChunk c;
   c.tags = tags;
   c.leaf = leaf;
@@ -440,6 +435,22 @@ cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int
   cudaFree(allpops);
   cudaFree(alltu);
   cudaFree(np_dev);
+  return e;
+}
+
+// One rank: paren_match over the shards (global match / parent), then the boxes.
+cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, float* out,
+                          ncclComm_t comm, cudaStream_t s, int* nccl_err) {
+  *nccl_err = 0;
+  int32_t* mp = nullptr;
+  const int64_t n64 = (std::max<int64_t>(n, 1) + 63) & ~int64_t(63);  // keeps parent 16-byte aligned
+  cudaError_t e = cudaMalloc(&mp, 8 * (size_t)n64);
+  int32_t* match = mp;
+  int32_t* parent = mp + n64;
+  if (e == cudaSuccess) e = pm_nccl_shard(tags, n, off, match, parent, comm, s, nccl_err);
+  if (e == cudaSuccess && !*nccl_err) e = bbm_nccl_shard(tags, leaf, match, parent, n, off, out, comm, s, nccl_err);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
   cudaFree(mp);
   return e;
 }

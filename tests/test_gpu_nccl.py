@@ -1,5 +1,5 @@
 """The NCCL-backed shard entry points (tb_get_unique_id, tb_comm_init,
-paren_match_shard, tree_bbox_shard) through ShardContext, with a world of one
+paren_match_shard, tree_bbox_shard, tree_bbox_matched_shard) through ShardContext, with a world of one
 rank (the GPU box has one GPU; multi-rank exchange logic is covered by the
 virtual-shard parity tests and the gloo protocol tests)."""
 import os
@@ -35,6 +35,10 @@ def test_nccl_shard_world1():
         o_ref = oracle.tree_bbox(t.numpy(), b.numpy())
         assert np.array_equal(m.cpu().numpy(), m_ref) and np.array_equal(p.cpu().numpy(), p_ref)
         assert np.array_equal(out.cpu().numpy().view(np.uint32), o_ref.view(np.uint32))
+        out2 = torch.empty_like(out)
+        ctx.tree_bbox_matched(t.cuda(), b.cuda(), m, p, out2)  # the bench's multi-GPU step
+        torch.cuda.synchronize()
+        assert np.array_equal(out2.cpu().numpy().view(np.uint32), o_ref.view(np.uint32))
         ctx.close()
     finally:
         dist.destroy_process_group()
