@@ -603,6 +603,8 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
     if (qt | qi) {
       const float4 after = qt ? range_union_threads(s, tid + 1, NT - 1) : bEMPTY();
       float4 R = bEMPTY();
+      uint64_t pk = 0;  // up to 4 pending (close, open position) entries, 16 bits each
+      int npk = 0;
 #pragma unroll
       for (int i = K - 1; i >= 0; i--) {
         const uint32_t bit = 1u << i;
@@ -612,11 +614,26 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
         } else if (qi & bit) {
           const int c = (int)(mt[i] - gbase);
           float4& cv = s.val[slot_of(c)];
-          const float4 U = unite(unite(R, range_union_threads(s, tid + 1, c / K - 1)), cv);
-          cv = U;
-          if ((bm >> i) & 1u) s.val[slot(tid, i)] = U;
+          if (npk < 4) {  // the thread range is added below, with the lanes in step
+            cv = unite(R, cv);
+            pk |= (uint64_t)(c | (i << 10)) << (16 * npk);
+            npk++;
+          } else {
+            const float4 U = unite(unite(R, range_union_threads(s, tid + 1, c / K - 1)), cv);
+            cv = U;
+            if ((bm >> i) & 1u) s.val[slot(tid, i)] = U;
+          }
         }
         if ((lm & bit) && ((qt | qi) & (bit - 1u))) R = unite(R, s.val[slot(tid, i)]);
+      }
+#pragma unroll 1
+      for (int k = 0; k < npk; k++) {
+        const int e = (int)(pk >> (16 * k)) & 0xffff;
+        const int c = e & 1023, i = e >> 10;
+        float4& cv = s.val[slot_of(c)];
+        const float4 U = unite(cv, range_union_threads(s, tid + 1, c / K - 1));
+        cv = U;
+        if ((bm >> i) & 1u) s.val[slot(tid, i)] = U;
       }
     }
   }
