@@ -36,7 +36,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so (gcc -O2, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -55,6 +55,9 @@ def _load():
             lib.oracle_count_unmatched.restype = ctypes.c_int
             lib.oracle_tree_transform.argtypes = [P, P, ctypes.c_int64, P]
             lib.oracle_tree_transform.restype = ctypes.c_int
+            lib.oracle_bin_leaves.argtypes = [P, P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_float,
+                                              P, P, P, ctypes.c_int64]
+            lib.oracle_bin_leaves.restype = ctypes.c_int64
             _lib = lib
     return _lib
 
@@ -100,6 +103,23 @@ def tree_transform(tags: np.ndarray, local: np.ndarray):
     if _load().oracle_tree_transform(_ptr(tags), _ptr(loc), n, _ptr(res)) != 0:
         raise MemoryError("oracle_tree_transform: allocation failed")
     return res
+
+
+def bin_leaves(tags: np.ndarray, node_bbox: np.ndarray, gw: int, gh: int, bs: float):
+    """Culling + binning of clipped leaf boxes (R16).  Returns (counts, offsets,
+    items) with items in leaf order inside each bin."""
+    tags = np.ascontiguousarray(tags, dtype=np.uint8)
+    box = np.ascontiguousarray(node_bbox, dtype=np.float32).reshape(-1, 4)
+    counts = np.zeros(gw * gh, np.int32)
+    offsets = np.zeros(gw * gh + 1, np.int32)
+    total = _load().oracle_bin_leaves(_ptr(tags), _ptr(box), tags.shape[0], gw, gh, bs, _ptr(counts),
+                                      _ptr(offsets), 0, 0)
+    if total < 0:
+        raise MemoryError("oracle_bin_leaves")
+    items = np.zeros(max(total, 1), np.int32)
+    _load().oracle_bin_leaves(_ptr(tags), _ptr(box), tags.shape[0], gw, gh, bs, _ptr(counts), _ptr(offsets),
+                              _ptr(items), total)
+    return counts, offsets, items[:total]
 
 
 def count_unmatched(tags: np.ndarray):

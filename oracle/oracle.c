@@ -15,6 +15,7 @@
  *   1 = open of a clip node, 2 = open of a blend node, 3 = close,
  *   anything else (0 canonical) = leaf                     [DESIGN R2]
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -249,4 +250,60 @@ int oracle_tree_transform(const uint8_t *tags, const float *local, int64_t n, do
     }
     free(stack);
     return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* oracle_bin_leaves — culling and binning of the clipped leaf boxes        */
+/* (the motivating use: "input to visibility       */
+/* culling and binning"; reading R16).                          */
+/* A leaf (tags not 1/2/3) whose clipped box (node_bbox) is non-empty        */
+/* (x0 < x1 and y0 < y1) and overlaps the viewport [0, gw*bs) x [0, gh*bs)   */
+/* is listed in every bin (bx, by) with [bx*bs, (bx+1)*bs) x [by*bs, ...)    */
+/* overlapping its box (open overlap: x0 < (bx+1)*bs and x1 > bx*bs).        */
+/* counts[gw*gh]; offsets[gw*gh+1] exclusive; items in leaf order per bin.   */
+/* Returns the number of items (items written only if <= capacity).          */
+/* ------------------------------------------------------------------------ */
+static void bin_range(float lo, float hi, float bs, int g, int *a, int *b)
+{
+    /* bins k with lo < (k+1)*bs and hi > k*bs */
+    double fa = floor((double)lo / bs), fb = ceil((double)hi / bs) - 1.0;
+    if (fa < 0) fa = 0;
+    if (fb > g - 1) fb = g - 1;
+    *a = (int)fa;
+    *b = (int)fb;
+}
+
+int64_t oracle_bin_leaves(const uint8_t *tags, const float *node_bbox, int64_t n, int gw, int gh, float bs,
+                          int32_t *counts, int32_t *offsets, int32_t *items, int64_t capacity)
+{
+    const int nb = gw * gh;
+    for (int i = 0; i < nb; i++) counts[i] = 0;
+    for (int pass = 0; pass < 2; pass++) {
+        int64_t *cur = NULL;
+        if (pass == 1) {
+            offsets[0] = 0;
+            for (int i = 0; i < nb; i++) offsets[i + 1] = offsets[i] + counts[i];
+            if (offsets[nb] > capacity) return offsets[nb];
+            cur = (int64_t *)calloc((size_t)nb, sizeof(int64_t));
+            if (!cur) return -1;
+        }
+        for (int64_t e = 0; e < n; e++) {
+            const uint8_t t = tags[e];
+            if (t == 1 || t == 2 || t == 3) continue;
+            const float *bx = node_bbox + 4 * e;
+            if (!(bx[0] < bx[2] && bx[1] < bx[3])) continue;                      /* empty: culled */
+            if (!(bx[2] > 0 && bx[3] > 0 && bx[0] < gw * bs && bx[1] < gh * bs)) continue;  /* off-screen */
+            int x0, x1, y0, y1;
+            bin_range(bx[0], bx[2], bs, gw, &x0, &x1);
+            bin_range(bx[1], bx[3], bs, gh, &y0, &y1);
+            for (int y = y0; y <= y1; y++)
+                for (int x = x0; x <= x1; x++) {
+                    const int k = y * gw + x;
+                    if (pass == 0) counts[k]++;
+                    else items[offsets[k] + cur[k]++] = (int32_t)e;
+                }
+        }
+        if (pass == 1) free(cur);
+    }
+    return offsets[nb];
 }
