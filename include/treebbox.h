@@ -168,6 +168,26 @@ int tree_transform(const uint8_t *d_tags, const float *d_local, const int32_t *d
                    int64_t n, float *d_world, void *stream);
 
 /* ------------------------------------------------------------------------
+ * bin_leaves — culling and binning of the clipped leaf boxes (SURVEY §8(f)
+ * NEXT row 4; "input to visibility culling and binning"; R16)
+ *
+ * d_node_bbox : tree_bbox's output (device float32[n][4], 16-byte aligned).
+ * A leaf whose box is non-empty (x0 < x1, y0 < y1) and overlaps the viewport
+ * [0, grid_w*bin_size) x [0, grid_h*bin_size) is listed in every bin (bx, by)
+ * whose square [bx*bin_size, (bx+1)*bin_size) x [...] overlaps its box.
+ * d_counts  : device int32[grid_w*grid_h] out (bin index = by*grid_w + bx).
+ * d_offsets : device int32[grid_w*grid_h + 1] out, exclusive prefix of counts.
+ * d_items   : device int32[capacity] out: leaf indices, bin after bin; the
+ *             order inside a bin is unspecified.  Filled only if the total
+ *             fits in capacity.
+ * *h_total  : HOST out, the number of (bin, leaf) items.  The call synchronises
+ * `stream` (the total is read on the host).
+ * ------------------------------------------------------------------------ */
+int bin_leaves(const uint8_t *d_tags, const float *d_node_bbox, int64_t n, int grid_w, int grid_h, float bin_size,
+               int32_t *d_counts, int32_t *d_offsets, int32_t *d_items, int64_t capacity, int64_t *h_total,
+               void *stream);
+
+/* ------------------------------------------------------------------------
  * Host-buffer variants (end-to-end API): h_* are host pointers (pinned or
  * pageable).  Inputs are copied to library-owned device buffers on `stream`,
  * the device call runs, outputs are copied back, and the call synchronises

@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "bin_leaves", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard"]
 
@@ -56,6 +56,8 @@ def load():
                 "paren_match_tree_bbox_host": ([P, P, I64, P, P, P, P], ctypes.c_int),
                 "paren_match_bytes": ([P, I64, P, P, P, P], ctypes.c_int),
                 "tree_transform": ([P, P, P, P, I64, P, P], ctypes.c_int),
+                "bin_leaves": ([P, P, I64, ctypes.c_int, ctypes.c_int, ctypes.c_float, P, P, P, I64, P, P],
+                               ctypes.c_int),
                 "tree_bbox_matched_ws": ([P, P, P, P, I64, P, P, SZ, P], ctypes.c_int),
                 "tree_bbox_matched_workspace_bytes": ([I64], SZ),
                 "tb_count_unmatched": ([P, I64, P, P, P], ctypes.c_int),
@@ -199,6 +201,29 @@ def tree_transform(tags: torch.Tensor, local: torch.Tensor, match: torch.Tensor,
         _check(lib.tree_transform(tags.data_ptr(), local.data_ptr(), match.data_ptr(), parent.data_ptr(), n,
                                   world.data_ptr(), _stream(tags.device)))
     return world
+
+
+def bin_leaves(tags: torch.Tensor, node_bbox: torch.Tensor, grid_w: int, grid_h: int, bin_size: float):
+    """Culling + binning of clipped leaf boxes.  Returns (counts, offsets, items),
+    int32 CUDA tensors; the order inside a bin is unspecified."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    _need_cuda(node_bbox, "node_bbox", torch.float32)
+    n = tags.numel()
+    nb = grid_w * grid_h
+    counts = torch.empty(nb, dtype=torch.int32, device=tags.device)
+    offsets = torch.empty(nb + 1, dtype=torch.int32, device=tags.device)
+    total = ctypes.c_int64(0)
+    items = torch.empty(max(n, 1), dtype=torch.int32, device=tags.device)
+    with torch.cuda.device(tags.device):
+        for _ in range(2):  # a second call when the first guess of the capacity was too small
+            _check(lib.bin_leaves(tags.data_ptr(), node_bbox.data_ptr(), n, grid_w, grid_h, float(bin_size),
+                                  counts.data_ptr(), offsets.data_ptr(), items.data_ptr(), items.numel(),
+                                  ctypes.byref(total), _stream(tags.device)))
+            if total.value <= items.numel():
+                break
+            items = torch.empty(total.value, dtype=torch.int32, device=tags.device)
+    return counts, offsets, items[:total.value]
 
 
 def workspace_bytes(n: int) -> dict:

@@ -401,6 +401,26 @@ int tree_transform(const uint8_t* d_tags, const float* d_local, const int32_t* d
   return TB_OK;
 }
 
+int bin_leaves(const uint8_t* d_tags, const float* d_node_bbox, int64_t n, int grid_w, int grid_h, float bin_size,
+               int32_t* d_counts, int32_t* d_offsets, int32_t* d_items, int64_t capacity, int64_t* h_total,
+               void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r) return r;
+  if (grid_w <= 0 || grid_h <= 0 || (int64_t)grid_w * grid_h > (1 << 26) || !(bin_size > 0.f))
+    return fail(TB_ERR_ARG, "bad bin grid");
+  if (!d_counts || !d_offsets || !h_total || (n > 0 && (!d_tags || !d_node_bbox)) || (capacity > 0 && !d_items))
+    return fail(TB_ERR_ARG, "null pointer");
+  if (n > 0 && !aligned16(d_node_bbox)) return fail(TB_ERR_ALIGN, "node_bbox must be 16-byte aligned");
+  void* ws = nullptr;
+  r = get_ws(stream, 9, sizeof(int32_t) * (size_t)grid_w * grid_h, &ws);
+  if (r) return r;
+  cudaError_t e = tb::bins_launch(d_tags, d_node_bbox, n, grid_w, grid_h, bin_size, d_counts, d_offsets,
+                                  (int32_t*)ws, d_items, capacity, h_total, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "bin_leaves");
+  return TB_OK;
+}
+
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }

@@ -97,6 +97,11 @@ size_t tt_workspace_bytes(int64_t n);
 cudaError_t tt_launch(const uint8_t* tags, const float* local, const int32_t* match, const int32_t* parent,
                       int64_t n, float* world, void* ws, cudaStream_t stream);
 
+// culling + binning of clipped leaf boxes (bins.cu); synchronises to read the total
+cudaError_t bins_launch(const uint8_t* tags, const float* node_bbox, int64_t n, int gw, int gh, float bs,
+                        int32_t* counts, int32_t* offsets, int32_t* cursor, int32_t* items, int64_t capacity,
+                        int64_t* total, cudaStream_t stream);
+
 // raw bytes -> tag bytes through a 256-entry class map (host pointer)
 cudaError_t classify_bytes_launch(const uint8_t* in, int64_t n, const uint8_t* class_map, uint8_t* out,
                                   cudaStream_t stream);
