@@ -188,6 +188,21 @@ int bin_leaves(const uint8_t *d_tags, const float *d_node_bbox, int64_t n, int g
                void *stream);
 
 /* ------------------------------------------------------------------------
+ * compact_scene — stream compaction front end (the
+ * step upstream of the path)
+ *
+ * d_tags      : device uint8[n] full scene stream (16-byte aligned).
+ * d_boxes     : device float32[n][4] or NULL (then no boxes are moved).
+ * h_keep_map  : HOST uint8[256]: nonzero = keep elements with that byte value.
+ * d_tags_out, d_boxes_out, d_index_out: device [n] out (capacity n); the kept
+ *               elements in stream order, their boxes, their index in the
+ *               full stream.
+ * *h_n_out    : HOST out, the number kept.  The call synchronises `stream`.
+ * ------------------------------------------------------------------------ */
+int compact_scene(const uint8_t *d_tags, const float *d_boxes, int64_t n, const uint8_t *h_keep_map,
+                  uint8_t *d_tags_out, float *d_boxes_out, int32_t *d_index_out, int64_t *h_n_out, void *stream);
+
+/* ------------------------------------------------------------------------
  * Host-buffer variants (end-to-end API): h_* are host pointers (pinned or
  * pageable).  Inputs are copied to library-owned device buffers on `stream`,
  * the device call runs, outputs are copied back, and the call synchronises

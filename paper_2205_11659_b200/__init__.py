@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "bin_leaves", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "bin_leaves", "compact_scene", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard"]
 
@@ -56,6 +56,7 @@ def load():
                 "paren_match_tree_bbox_host": ([P, P, I64, P, P, P, P], ctypes.c_int),
                 "paren_match_bytes": ([P, I64, P, P, P, P], ctypes.c_int),
                 "tree_transform": ([P, P, P, P, I64, P, P], ctypes.c_int),
+                "compact_scene": ([P, P, I64, P, P, P, P, P, P], ctypes.c_int),
                 "bin_leaves": ([P, P, I64, ctypes.c_int, ctypes.c_int, ctypes.c_float, P, P, P, I64, P, P],
                                ctypes.c_int),
                 "tree_bbox_matched_ws": ([P, P, P, P, I64, P, P, SZ, P], ctypes.c_int),
@@ -224,6 +225,30 @@ def bin_leaves(tags: torch.Tensor, node_bbox: torch.Tensor, grid_w: int, grid_h:
                 break
             items = torch.empty(total.value, dtype=torch.int32, device=tags.device)
     return counts, offsets, items[:total.value]
+
+
+def compact_scene(tags: torch.Tensor, boxes: torch.Tensor | None, keep_map: bytes):
+    """Keep the elements whose byte value has keep_map[byte] != 0, in order.
+    Returns (tags, boxes or None, index into the full stream)."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    if len(keep_map) != 256:
+        raise ValueError("keep_map must have 256 entries")
+    n = tags.numel()
+    t_out = torch.empty(max(n, 1), dtype=torch.uint8, device=tags.device)
+    idx = torch.empty(max(n, 1), dtype=torch.int32, device=tags.device)
+    b_out = None
+    if boxes is not None:
+        _need_cuda(boxes, "boxes", torch.float32)
+        b_out = torch.empty((max(n, 1), 4), dtype=torch.float32, device=tags.device)
+    km = (ctypes.c_uint8 * 256)(*bytes(keep_map))
+    cnt = ctypes.c_int64(0)
+    with torch.cuda.device(tags.device):
+        _check(lib.compact_scene(tags.data_ptr(), boxes.data_ptr() if boxes is not None else None, n, km,
+                                 t_out.data_ptr(), b_out.data_ptr() if b_out is not None else None, idx.data_ptr(),
+                                 ctypes.byref(cnt), _stream(tags.device)))
+    k = cnt.value
+    return t_out[:k], (b_out[:k] if b_out is not None else None), idx[:k]
 
 
 def workspace_bytes(n: int) -> dict:

@@ -421,6 +421,25 @@ int bin_leaves(const uint8_t* d_tags, const float* d_node_bbox, int64_t n, int g
   return TB_OK;
 }
 
+int compact_scene(const uint8_t* d_tags, const float* d_boxes, int64_t n, const uint8_t* h_keep_map,
+                  uint8_t* d_tags_out, float* d_boxes_out, int32_t* d_index_out, int64_t* h_n_out, void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r) return r;
+  if (!h_keep_map || !h_n_out) return fail(TB_ERR_ARG, "null pointer");
+  if (n > 0 && (!d_tags || !d_tags_out || !d_index_out || (d_boxes && !d_boxes_out)))
+    return fail(TB_ERR_ARG, "null pointer with n > 0");
+  if (n > 0 && (!aligned16(d_tags) || (d_boxes && (!aligned16(d_boxes) || !aligned16(d_boxes_out)))))
+    return fail(TB_ERR_ALIGN, "tags and boxes must be 16-byte aligned");
+  void* ws = nullptr;
+  r = get_ws(stream, 10, tb::compact_workspace_bytes(n), &ws);
+  if (r) return r;
+  cudaError_t e = tb::compact_launch(d_tags, d_boxes, n, h_keep_map, d_tags_out, d_boxes_out, d_index_out, h_n_out,
+                                     ws, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "compact_scene");
+  return TB_OK;
+}
+
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }

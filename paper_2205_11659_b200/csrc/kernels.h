@@ -102,6 +102,12 @@ cudaError_t bins_launch(const uint8_t* tags, const float* node_bbox, int64_t n, 
                         int32_t* counts, int32_t* offsets, int32_t* cursor, int32_t* items, int64_t capacity,
                         int64_t* total, cudaStream_t stream);
 
+// stream compaction front end (compact.cu); synchronises to read the count
+size_t compact_workspace_bytes(int64_t n);
+cudaError_t compact_launch(const uint8_t* tags, const float* boxes, int64_t n, const uint8_t* keep_map,
+                           uint8_t* tags_out, float* boxes_out, int32_t* index_out, int64_t* n_out, void* ws,
+                           cudaStream_t stream);
+
 // raw bytes -> tag bytes through a 256-entry class map (host pointer)
 cudaError_t classify_bytes_launch(const uint8_t* in, int64_t n, const uint8_t* class_map, uint8_t* out,
                                   cudaStream_t stream);
