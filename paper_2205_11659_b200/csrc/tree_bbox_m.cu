@@ -105,13 +105,29 @@ __device__ __forceinline__ float4 ext_ctx(const Params& p, int X) {
   return ext_lookup(p.ext_idx, p.ext_ctx, p.n_ext, X);
 }
 
+// node_bbox[X] of a slice entry X is read by later tiles while X's own tile may
+// be storing X's true context over lc(X) (F6): both values give the same
+// result, and the accesses are relaxed (morally strong) so they do not race.
+__device__ __forceinline__ float4 ld_relaxed_box(const float4* p) {
+  float4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_box(float4* p, float4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 // Context of an open X outside the current tile: node_bbox[X] holds lc(X) or
 // its true context (F6), completed by TC of X's tile; earlier chunks: imported.
 template <bool SHARD>
 __device__ __forceinline__ float4 outer_ctx(const Params& p, int X) {
   if (SHARD && X < p.off) return ext_ctx(p, X);
   const int64_t x = SHARD ? X - p.off : X;
-  return isect(__ldcg(p.out + x), __ldg(p.tc + x / TILE));
+  return isect(ld_relaxed_box(p.out + x), __ldg(p.tc + x / TILE));
 }
 
 __device__ __forceinline__ uint64_t gtime() {
@@ -496,15 +512,19 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
   __syncthreads();
   BBM_TRACE(T, 2);
 
-  // ---- D. finish pending clips: rel ∩ ctx(X) ------------------------------------
-  if (pend) {
+  // ---- D. finish pending clips: rel ∩ ctx(X).  Other threads read only this
+  //      thread's thread-unmatched opens (as their contexts); those all belong
+  //      to the thread's last external group (context tl[tid]) and are
+  //      finished after the barrier, so no slot is read while it is written.
+  const uint32_t pend_now = pend & ~thr_un;
+  if (pend_now) {
     int X = -1, cx = INT_MIN;
     float4 g = bINF();
 #pragma unroll
     for (int i = 0; i < K; i++) {
       if (((om | lm) >> i) & 1u) {
         if (pr[i] < gtstart) X = pr[i];
-        if ((pend >> i) & 1u) {
+        if ((pend_now >> i) & 1u) {
           if (X != cx) {
             cx = X;
             if (X < gbase) {
@@ -521,6 +541,17 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
     }
   }
   __syncthreads();
+  if (pend & thr_un) {
+    const float4 g = s.u.tl[tid];
+    uint32_t q = pend & thr_un;
+#pragma unroll 1
+    while (q) {
+      const int i = __ffs(q) - 1;
+      q &= q - 1;
+      float4& me = s.val[slot(tid, i)];
+      me = isect(me, g);
+    }
+  }
   BBM_TRACE(T, 3);
 
   // ---- E. unions inside the thread ---------------------------------------------------
@@ -672,7 +703,7 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
 #pragma unroll
   for (int j = 0; j < K; j++) {
     const int e = j * NT + tid;
-    if (e < nvalid) __stcs(p.out + base + e, s.val[slot_of(e)]);
+    if (e < nvalid) st_relaxed_box(p.out + base + e, s.val[slot_of(e)]);
   }
   BBM_TRACE(T, 7);
 }
