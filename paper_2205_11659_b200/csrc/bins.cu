@@ -50,35 +50,6 @@ __global__ void __launch_bounds__(256) bin_count_k(P p) {
   }
 }
 
-__global__ void __launch_bounds__(1024) bin_scan_k(P p) {  // one CTA: exclusive scan, offsets[nb] = total
-  __shared__ int ws[32];
-  __shared__ int carry_s;
-  const int nb = p.gw * p.gh, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int carry = 0;
-  for (int b0 = 0; b0 < nb; b0 += 1024) {
-    const int i = b0 + tid;
-    const int v = i < nb ? p.counts[i] : 0;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) ws[warp] = x;
-    __syncthreads();
-    int pre = carry;
-    for (int w = 0; w < warp; w++) pre += ws[w];
-    if (i < nb) {
-      p.offsets[i] = pre + x - v;
-      p.cursor[i] = 0;
-    }
-    if (tid == 1023) carry_s = pre + x;
-    __syncthreads();
-    carry = carry_s;
-    __syncthreads();
-  }
-  if (tid == 0) p.offsets[nb] = carry;
-}
 
 __global__ void __launch_bounds__(256) bin_fill_k(P p) {
   for (int64_t e = blockIdx.x * (int64_t)256 + threadIdx.x; e < p.n; e += (int64_t)gridDim.x * 256) {
@@ -102,7 +73,8 @@ cudaError_t bins_launch(const uint8_t* tags, const float* node_bbox, int64_t n, 
   cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)nb, stream);
   const unsigned grid = 148 * 8;
   if (e == cudaSuccess && n > 0) TB_LAUNCH(stream, "bin_count", (bins::bin_count_k<<<grid, 256, 0, stream>>>(p)));
-  if (e == cudaSuccess) TB_LAUNCH(stream, "bin_scan", (bins::bin_scan_k<<<1, 1024, 0, stream>>>(p)));
+  if (e == cudaSuccess) e = excl_scan_launch(counts, nb, offsets, "bin_scan", stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (size_t)nb, stream);
   int32_t t = 0;
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(&t, offsets + nb, 4, cudaMemcpyDeviceToHost, stream);

@@ -52,32 +52,6 @@ __global__ void __launch_bounds__(NT) count_k(const uint8_t* tags, int64_t n, Ke
   }
 }
 
-__global__ void __launch_bounds__(1024) scan_k(const int* cnt, int nb, int* offs) {  // one CTA, offs[nb] = total
-  __shared__ int ws[32];
-  __shared__ int carry_s;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int carry = 0;
-  for (int b0 = 0; b0 < nb; b0 += 1024) {
-    const int i = b0 + tid;
-    const int v = i < nb ? cnt[i] : 0;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) ws[warp] = x;
-    __syncthreads();
-    int pre = carry;
-    for (int w = 0; w < warp; w++) pre += ws[w];
-    if (i < nb) offs[i] = pre + x - v;
-    if (tid == 1023) carry_s = pre + x;
-    __syncthreads();
-    carry = carry_s;
-    __syncthreads();
-  }
-  if (tid == 0) offs[nb] = carry;
-}
 
 __global__ void __launch_bounds__(NT) scatter_k(const uint8_t* tags, const float4* boxes, int64_t n, KeepMap kmv,
                                                 const int* offs, uint8_t* tags_out, float4* boxes_out,
@@ -122,7 +96,8 @@ cudaError_t compact_launch(const uint8_t* tags, const float* boxes, int64_t n, c
   int* cnt = (int*)ws;
   int* offs = cnt + nb + 1;
   if (n > 0) TB_LAUNCH(stream, "compact_count", (cpt::count_k<<<nb, cpt::NT, 0, stream>>>(tags, n, km, cnt)));
-  TB_LAUNCH(stream, "compact_scan", (cpt::scan_k<<<1, 1024, 0, stream>>>(cnt, nb, offs)));
+  cudaError_t e0 = excl_scan_launch(cnt, nb, offs, "compact_scan", stream);
+  if (e0 != cudaSuccess) return e0;
   if (n > 0)
     TB_LAUNCH(stream, "compact_scatter",
               (cpt::scatter_k<<<nb, cpt::NT, 0, stream>>>(tags, reinterpret_cast<const float4*>(boxes), n, km,

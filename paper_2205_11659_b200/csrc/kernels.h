@@ -102,6 +102,9 @@ cudaError_t bins_launch(const uint8_t* tags, const float* node_bbox, int64_t n, 
                         int32_t* counts, int32_t* offsets, int32_t* cursor, int32_t* items, int64_t capacity,
                         int64_t* total, cudaStream_t stream);
 
+// exclusive prefix sum of a small int32 array in one CTA: out[0..n) and out[n] = total
+cudaError_t excl_scan_launch(const int* in, int n, int* out, const char* name, cudaStream_t stream);
+
 // stream compaction front end (compact.cu); synchronises to read the count
 size_t compact_workspace_bytes(int64_t n);
 cudaError_t compact_launch(const uint8_t* tags, const float* boxes, int64_t n, const uint8_t* keep_map,

@@ -834,34 +834,6 @@ __global__ void __launch_bounds__(128) bbm_fs_count(Params p, int* cnt) {
   if (lane == 0) cnt[T] = c;
 }
 
-// exclusive scan of cnt[0..nt) into offs (one CTA); offs[nt] = total
-__global__ void __launch_bounds__(1024) bbm_scan_counts(const int* cnt, int nt, int* offs) {
-  __shared__ int ws[32];
-  __shared__ int carry_s;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int carry = 0;
-  for (int b0 = 0; b0 < nt; b0 += 1024) {
-    const int i = b0 + tid;
-    const int v = i < nt ? cnt[i] : 0;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) ws[warp] = x;
-    __syncthreads();
-    int pre = carry;
-    for (int w = 0; w < warp; w++) pre += ws[w];
-    if (i < nt) offs[i] = pre + x - v;
-    if (tid == 1023) carry_s = pre + x;
-    __syncthreads();
-    carry = carry_s;
-    __syncthreads();
-  }
-  if (tid == 0) offs[nt] = carry;
-}
-
 __global__ void __launch_bounds__(128) bbm_fs_write(Params p, const int* offs, ShardOpen* fs, int* link_out) {
   const int lane = threadIdx.x & 31;
   const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
@@ -1187,7 +1159,8 @@ cudaError_t bbm_shard_phase1(const uint8_t* tags, const float* leaf_bbox, const 
   err = launch_tc(p, ws, stream);  // no imported contexts yet: chunk-local TC
   if (err != cudaSuccess) return err;
   TB_LAUNCH(stream, "bbm_fs_count", (bbm::bbm_fs_count<<<g4, 128, 0, stream>>>(p, cnt)));
-  TB_LAUNCH(stream, "bbm_scan_counts", (bbm::bbm_scan_counts<<<1, 1024, 0, stream>>>(cnt, (int)L.ntiles, offs)));
+  err = excl_scan_launch(cnt, (int)L.ntiles, offs, "bbm_scan_counts", stream);
+  if (err != cudaSuccess) return err;
   TB_LAUNCH(stream, "bbm_fs_write", (bbm::bbm_fs_write<<<g4, 128, 0, stream>>>(p, offs, fs, link_dev)));
   return cudaGetLastError();
 }
