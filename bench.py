@@ -135,6 +135,16 @@ def profile_traffic():
 # ----------------------------------------------------------------------------
 # reference arm: the oracle on host cores
 # ----------------------------------------------------------------------------
+def bench_config(args, world):
+    """The workload description shared by both arms (the reference arm times a
+    bounded sample of it, described in its cpu_baseline)."""
+    return {"workload": f"C5 random-depth walk stream, 2^{args.log2n} elements per GPU "
+                        f"(global stream {world} x 2^{args.log2n}); 50% leaves, 75% clips",
+            "n_per_gpu": 1 << args.log2n, "seed": args.seed,
+            "l2": "inputs (2.2 GB/GPU) larger than L2; no flush",
+            "parallelism": f"contiguous shards x{world}" if world > 1 else "single GPU"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -160,13 +170,14 @@ def run_reference(args, rank, world):
         step()
     dt = time.perf_counter() - t0
     value = ns * args.steps / dt / 1e9
-    sample = f"first 2^{log2s} elements of the bench stream per step (the oracle is sequential)"
+    sample = (f"first 2^{log2s} elements of the bench stream per step (the oracle, oracle/oracle.c -O2, "
+              f"is sequential; its time is linear in the elements)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32",
         "data": "synthetic",
-        "config": {"workload": f"C5 random-depth walk, sample of 2^{log2s} elements", "oracle": "oracle/oracle.c -O2"},
+        "config": bench_config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -339,11 +350,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32", "data": "synthetic",
-            "config": {"workload": f"C5 random-depth walk stream, 2^{args.log2n} elements per GPU "
-                                   f"(global stream {world} x 2^{args.log2n}); 50% leaves, 75% clips",
-                       "n_per_gpu": n, "seed": args.seed,
-                       "l2": "inputs (2.2 GB/GPU) larger than L2; no flush",
-                       "parallelism": f"contiguous shards x{world}" if world > 1 else "single GPU"},
+            "config": bench_config(args, world),
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
