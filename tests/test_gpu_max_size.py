@@ -1,0 +1,53 @@
+"""The largest stream of BASELINE.json's configs on ONE device: 2^30 elements
+(the 1B-element C5 stream), ~65 GB of device buffers.  Properties that hold at
+any size are checked on the GPU over the whole stream; the outputs a prefix
+determines (parents, closes' partners, clipped leaves and clip opens, unions of
+nodes closed inside it) are compared with the oracle on the first 2^24."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import scenegen
+
+pytestmark = pytest.mark.gpu
+
+
+def test_one_billion_elements():
+    import paper_2205_11659_b200 as tb
+    n = 1 << 30
+    free, _ = torch.cuda.mem_get_info()
+    if free < 90 << 30:
+        pytest.skip("needs ~90 GB of free device memory")
+    tags = scenegen.walk_tags(n, 4, device="cuda")
+    boxes = scenegen.boxes(n, 4, tags, device="cuda")
+    torch.cuda.empty_cache()  # the generators' temporaries; the library allocates its own workspace
+    m, p = tb.paren_match(tags)
+    out = tb.tree_bbox_matched(tags, boxes, m, p)
+    torch.cuda.synchronize()
+    # properties over the whole stream
+    idx = torch.arange(n, device="cuda", dtype=torch.int64)
+    ml = m.long()
+    has = ml >= 0
+    assert torch.equal(ml[ml[has]], idx[has])                      # match is an involution
+    assert bool((p.long() < idx).all())                             # parents precede
+    close = tags == 3
+    assert torch.equal(p[close & has], m[close & has])              # a close's parent is its open
+    a, b = tb.count_unmatched(tags)
+    assert int((close & ~has).sum()) == a                           # R3 closes
+    assert int(((tags == 1) | (tags == 2)).logical_and(~has).sum()) == b   # R4 opens
+    del idx, ml, has
+    # the prefix determines these outputs
+    k = 1 << 24
+    t_k = tags[:k].cpu().numpy()
+    m_ref, p_ref = oracle.paren_match(t_k)
+    assert np.array_equal(p[:k].cpu().numpy(), p_ref)
+    mk = m[:k].cpu().numpy()
+    opens = (t_k == 1) | (t_k == 2)
+    done = m_ref >= 0
+    assert np.array_equal(mk[done], m_ref[done])                   # partners found inside the prefix
+    assert ((mk[opens & ~done] == -1) | (mk[opens & ~done] >= k)).all()   # the others close later or never
+    ref = oracle.tree_bbox(t_k, boxes[:k].cpu().numpy())
+    got = out[:k].cpu().numpy()
+    det = (t_k == 1) | ~np.isin(t_k, [1, 2, 3]) | (t_k == 3) | ((t_k == 2) & done)
+    assert np.array_equal(got[det].view(np.uint32), ref[det].view(np.uint32))
