@@ -11,10 +11,11 @@
 //             the tile's link = the parent of its bottom slice entry.
 // tt_tc       TC(T) = world(link_T) = TC(tile of link_T) ∘ lc(link_T): pointer
 //             jumping over tiles, composing earlier contexts on the left.
-// tt_main     one CTA per tile: each thread composes its elements relative to
-//             its external ancestor X; thread links by pointer jumping; every
-//             element's world = ctx(X) ∘ rel, written straight to global so
-//             the shared relative products other threads read stay intact.
+// tt_main     one CTA per tile, transforms staged through shared memory (SoA,
+//             coalesced in and out): each thread composes its elements relative
+//             to its external ancestor X; thread links by pointer jumping; every
+//             element's world = ctx(X) ∘ rel in place — the only slots other
+//             threads read (thread-unmatched opens) are finished after a barrier.
 // tt_closes   a close takes its open's world.
 #include <algorithm>
 #include <climits>
@@ -148,12 +149,27 @@ __global__ void __launch_bounds__(256) tt_tc(Params p, Xf* acc2, int* ptr2, int*
   for (int V = gt; V < nt; V += nthr) p.tc[V] = acc[cb][V];
 }
 
+// Shared memory holds the tile's transforms as six float arrays (SoA); thread t's
+// element i sits at index 8t + (i ^ ((t >> 2) & 7)), so the 32 lanes of a warp
+// reading their i-th element hit 32 distinct banks.
 struct Smem {
-  Xf rel[TILE];  // local, then the product relative to the thread's external ancestor
-  Xf tl[NT];     // world of each thread's link
+  float v[6][TILE];  // local, then relative to the thread's external ancestor, then world
+  Xf tl[NT];         // world of each thread's link
   Xf acc[2][NT];
   int ptr[2][NT];
 };
+__device__ __forceinline__ int sidx(int t, int i) { return (t << 3) | (i ^ ((t >> 2) & 7)); }
+__device__ __forceinline__ Xf sget(const Smem& s, int j) {
+  return Xf{s.v[0][j], s.v[1][j], s.v[2][j], s.v[3][j], s.v[4][j], s.v[5][j]};
+}
+__device__ __forceinline__ void sput(Smem& s, int j, const Xf& x) {
+  s.v[0][j] = x.a;
+  s.v[1][j] = x.b;
+  s.v[2][j] = x.c;
+  s.v[3][j] = x.d;
+  s.v[4][j] = x.tx;
+  s.v[5][j] = x.ty;
+}
 
 __device__ __forceinline__ Xf outer_ctx(const Params& p, int X) {  // an open of an earlier tile
   return compose(p.tc[X / TILE], p.lcg[X]);
@@ -165,6 +181,28 @@ __global__ void __launch_bounds__(NT) tt_main(Params p) {
   const int tid = threadIdx.x;
   const int T = blockIdx.x;
   const int64_t base = (int64_t)T * TILE, tstart = base + (int64_t)tid * K;
+  const int nvalid = (int)(p.n - base < TILE ? p.n - base : TILE);
+  // the tile's transforms, coalesced: 6 * TILE floats as float4s (AoS in HBM)
+  {
+    const float* src = p.local + 6 * base;
+    const int nf = 6 * nvalid;
+    const bool vec = nvalid == TILE;  // 6*TILE*4 bytes from a 16-byte aligned base
+    for (int f4 = tid; f4 < (6 * TILE) / 4; f4 += NT) {
+      float w[4];
+      if (vec) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(src) + f4);
+        w[0] = q.x; w[1] = q.y; w[2] = q.z; w[3] = q.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) w[k] = (4 * f4 + k < nf) ? __ldg(src + 4 * f4 + k) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int f = 4 * f4 + k, e = f / 6, c = f - 6 * e;
+        s.v[c][sidx(e >> 3, e & 7)] = w[k];
+      }
+    }
+  }
   uint8_t tg[K];
   int pr[K], mt[K];
 #pragma unroll
@@ -174,7 +212,6 @@ __global__ void __launch_bounds__(NT) tt_main(Params p) {
     tg[i] = ok ? p.tags[g] : 0;
     pr[i] = ok ? __ldg(p.parent + g) : -1;
     mt[i] = ok ? __ldg(p.match + g) : -1;
-    s.rel[tid * K + i] = ok ? load_xf(p.local, g) : xf_id();
   }
   uint32_t valid = 0, thr_un = 0, pend = 0;
 #pragma unroll
@@ -182,17 +219,17 @@ __global__ void __launch_bounds__(NT) tt_main(Params p) {
     if (tstart + i < p.n) valid |= 1u << i;
     if (is_open(tg[i]) && (mt[i] < 0 || mt[i] >= tstart + K)) thr_un |= 1u << i;
   }
+  __syncthreads();
   // relative products, in place
   int curX = -1;
 #pragma unroll
   for (int i = 0; i < K; i++) {
     if (((valid >> i) & 1u) && tg[i] != 3) {
       const int par = pr[i];
-      Xf& me = s.rel[tid * K + i];
       if (par < tstart) {
         curX = par;
       } else {
-        me = compose(s.rel[tid * K + (par - (int)tstart)], me);
+        sput(s, sidx(tid, i), compose(sget(s, sidx(tid, par - (int)tstart)), sget(s, sidx(tid, i))));
       }
       if (curX >= 0) pend |= 1u << i;
     }
@@ -206,8 +243,9 @@ __global__ void __launch_bounds__(NT) tt_main(Params p) {
       if (curX < base) {
         acc = outer_ctx(p, curX);
       } else {
-        acc = s.rel[curX - (int)base];
-        ptr = (curX - (int)base) / K;
+        const int x = curX - (int)base;
+        acc = sget(s, sidx(x >> 3, x & 7));
+        ptr = x / K;
       }
     }
     int cb = 0;
@@ -227,22 +265,62 @@ __global__ void __launch_bounds__(NT) tt_main(Params p) {
     s.tl[tid] = acc;
   }
   __syncthreads();
-  // worlds, straight to global (the shared relative products stay intact)
-  int X = -1, cx = INT_MIN;
-  Xf g = xf_id();
+  // worlds in place.  Other threads read only this thread's thread-unmatched
+  // opens (their contexts); those belong to its last external group (context
+  // tl[tid]) and are finished after the barrier.
+  {
+    const uint32_t now = pend & ~thr_un;
+    int X = -1, cx = INT_MIN;
+    Xf g = xf_id();
 #pragma unroll
-  for (int i = 0; i < K; i++) {
-    if (!((valid >> i) & 1u) || tg[i] == 3) continue;
-    if (pr[i] < tstart) X = pr[i];
-    Xf w = s.rel[tid * K + i];
-    if ((pend >> i) & 1u) {
-      if (X != cx) {
-        cx = X;
-        g = X < base ? outer_ctx(p, X) : compose(s.tl[(X - (int)base) / K], s.rel[X - (int)base]);
+    for (int i = 0; i < K; i++) {
+      if (!((valid >> i) & 1u) || tg[i] == 3) continue;
+      if (pr[i] < tstart) X = pr[i];
+      if ((now >> i) & 1u) {
+        if (X != cx) {
+          cx = X;
+          if (X < base) {
+            g = outer_ctx(p, X);
+          } else {
+            const int x = X - (int)base;
+            g = compose(s.tl[x / K], sget(s, sidx(x >> 3, x & 7)));
+          }
+        }
+        sput(s, sidx(tid, i), compose(g, sget(s, sidx(tid, i))));
       }
-      w = compose(g, w);
     }
-    store_xf(p.out, tstart + i, w);
+  }
+  __syncthreads();
+  if (pend & thr_un) {
+    const Xf g = s.tl[tid];
+    uint32_t q = pend & thr_un;
+#pragma unroll 1
+    while (q) {
+      const int i = __ffs(q) - 1;
+      q &= q - 1;
+      sput(s, sidx(tid, i), compose(g, sget(s, sidx(tid, i))));
+    }
+  }
+  __syncthreads();
+  // coalesced copy-out (closes are filled by tt_closes)
+  {
+    float* dst = p.out + 6 * base;
+    const int nf = 6 * nvalid;
+    for (int f4 = tid; f4 < (6 * TILE) / 4; f4 += NT) {
+      float w[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int f = 4 * f4 + k, e = f / 6, c = f - 6 * e;
+        w[k] = s.v[c][sidx(e >> 3, e & 7)];
+      }
+      if (nvalid == TILE) {
+        reinterpret_cast<float4*>(dst)[f4] = make_float4(w[0], w[1], w[2], w[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (4 * f4 + k < nf) dst[4 * f4 + k] = w[k];
+      }
+    }
   }
 }
 
