@@ -17,6 +17,10 @@ struct ShardInit {
   int2* pairs;     // paren_match: (open, close) for closes that pop stack entries
 };
 
+// One-time per-device setup (kernel attributes, occupancy-derived grid sizes):
+// `slot` names the setup, the bit of the current device says it is done.
+bool once_per_device(int slot);
+
 // Launch accounting / optional event timing around each kernel (prof.cu).
 void prof_begin(cudaStream_t s, const char* name, void** token);
 void prof_end(cudaStream_t s, void* token);

@@ -426,8 +426,7 @@ static pm::Params pm_params(const uint8_t* tags, int64_t n, int32_t* match, int3
 }
 
 static cudaError_t pm_configure() {
-  static bool configured = false;
-  if (!configured) {
+  if (once_per_device(0)) {
     cudaError_t err = cudaFuncSetAttribute(pm::pm_finish<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)sizeof(pm::Smem));
     if (err == cudaSuccess)
@@ -437,7 +436,6 @@ static cudaError_t pm_configure() {
       err = cudaFuncSetAttribute(pm::pm_summary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(pm::Smem));
 
     if (err != cudaSuccess) return err;
-    configured = true;
   }
   return cudaSuccess;
 }

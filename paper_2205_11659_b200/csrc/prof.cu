@@ -53,6 +53,18 @@ void prof_end(cudaStream_t s, void* token) {
   delete r;
 }
 
+bool once_per_device(int slot) {
+  static std::mutex mu;
+  static uint64_t done[16] = {};  // [slot] bit d = done on device d (< 64)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done[slot & 15] & bit) return false;
+  done[slot & 15] |= bit;
+  return true;
+}
+
 }  // namespace tb
 
 extern "C" {

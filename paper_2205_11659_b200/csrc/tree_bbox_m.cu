@@ -1022,24 +1022,18 @@ struct Layout {
 };
 
 void main_setup() {
-  static bool done = false;
-  if (!done) {
+  if (once_per_device(1)) {
     cudaFuncSetAttribute(bbm_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
     cudaFuncSetAttribute(bbm_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-    done = true;
   }
 }
 
-int tc_blocks() {
-  static int nb = 0;
-  if (nb == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbm_tc, 256, 0);
-    nb = sms * std::max(occ, 1);
-  }
-  return nb;
+int tc_blocks() {  // co-resident CTAs of the cooperative kernel on the current device
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbm_tc, 256, 0);
+  return sms * std::max(occ, 1);
 }
 
 }  // namespace bbm

@@ -349,16 +349,12 @@ struct Layout {
   }
 };
 
-int tc_blocks() {
-  static int nb = 0;
-  if (nb == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tt_tc, 256, 0);
-    nb = sms * std::max(occ, 1);
-  }
-  return nb;
+int tc_blocks() {  // co-resident CTAs of the cooperative kernel on the current device
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tt_tc, 256, 0);
+  return sms * std::max(occ, 1);
 }
 
 }  // namespace tt
@@ -394,11 +390,8 @@ cudaError_t tt_launch(const uint8_t* tags, const float* local, const int32_t* ma
     prof_end(stream, tok);
     if (err != cudaSuccess) return err;
   }
-  static bool configured = false;
-  if (!configured) {
+  if (once_per_device(2))
     cudaFuncSetAttribute(tt::tt_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(tt::Smem));
-    configured = true;
-  }
   TB_LAUNCH(stream, "tt_main", (tt::tt_main<<<(unsigned)L.ntiles, tt::NT, sizeof(tt::Smem), stream>>>(p)));
   TB_LAUNCH(stream, "tt_closes", (tt::tt_closes<<<148 * 8, 256, 0, stream>>>(p)));
   return cudaGetLastError();
