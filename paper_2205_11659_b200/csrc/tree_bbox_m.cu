@@ -55,9 +55,17 @@ namespace tb {
 static const int kMinus1 = -1;
 namespace bbm {
 
-constexpr int NT = 128;
-constexpr int K = 8;
+#ifndef BBM_K
+#define BBM_K 8
+#endif
+constexpr int K = BBM_K;           // elements per thread of bbm_main
+constexpr int NT = 1024 / K;       // its threads per tile
+#ifndef BBM_MINB
+#define BBM_MINB (BBM_K == 16 ? 9 : 6)
+#endif
+constexpr int MINB = BBM_MINB;     // resident CTAs per SM (shared memory / registers)
 constexpr int TILE = NT * K;
+static_assert(TILE == 1024 && (K == 8 || K == 16), "bbm tiles are 1024 elements");
 constexpr int NW = NT / 32;
 constexpr int LV = 5;    // 32-ary levels of the tile-union hierarchy (32^5 tiles > 2^31 / TILE)
 
@@ -140,13 +148,12 @@ __device__ __forceinline__ uint64_t gtime() {
     if (p.trace && threadIdx.x == 0) p.trace[(size_t)(T) * 16 + (s)] = gtime();  \
   } while (0)
 
-// tag byte classes of 8 elements: om = opens (clip or blend), bm = blend
-// opens, cm = closes; everything else is a leaf (R2)
-__device__ __forceinline__ void classify8(uint2 raw, uint32_t& om, uint32_t& cm, uint32_t& bm) {
+// tag byte classes of K elements (K / 4 words): om = opens (clip or blend),
+// bm = blend opens, cm = closes; everything else is a leaf (R2)
+__device__ __forceinline__ void classifyK(const uint32_t (&ws)[K / 4], uint32_t& om, uint32_t& cm, uint32_t& bm) {
   uint32_t o = 0, c = 0, b = 0;
-  const uint32_t ws[2] = {raw.x, raw.y};
 #pragma unroll
-  for (int q = 0; q < 2; q++) {
+  for (int q = 0; q < K / 4; q++) {
     const uint32_t x = ws[q];
     const uint32_t bl = __vcmpeq4(x, 0x02020202u);
     o |= byte_mask4(__vcmpeq4(x, 0x01010101u) | bl) << (4 * q);
@@ -158,28 +165,34 @@ __device__ __forceinline__ void classify8(uint2 raw, uint32_t& om, uint32_t& cm,
   bm = b;
 }
 
-__device__ __forceinline__ uint2 load_tags8(const uint8_t* tags, int64_t n, int64_t tbase) {
-  if (tbase + 8 <= n) {
-    uint2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(tags + tbase));
-    return r;
+__device__ __forceinline__ void load_tagsK(const uint8_t* tags, int64_t n, int64_t tbase, uint32_t (&wv)[K / 4]) {
+  if (tbase + K <= n) {
+    if constexpr (K == 16) {
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(wv[0]), "=r"(wv[1]), "=r"(wv[2]), "=r"(wv[3])
+                   : "l"(tags + tbase));
+    } else {
+      asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(wv[0]), "=r"(wv[1]) : "l"(tags + tbase));
+    }
+    return;
   }
-  uint32_t wv[2] = {0, 0};
-  for (int i = 0; i < 8; i++) {
+#pragma unroll
+  for (int q = 0; q < K / 4; q++) wv[q] = 0;
+  for (int i = 0; i < K; i++) {
     const int64_t g = tbase + i;
     const uint32_t v = g < n ? tags[g] : 0u;
     wv[i >> 2] |= v << (8 * (i & 3));
   }
-  return make_uint2(wv[0], wv[1]);
 }
 
-// 8 consecutive int32 (16-byte aligned when full); -1 past the end
-__device__ __forceinline__ void load_i8(const int32_t* a, int64_t n, int64_t tbase, int (&v)[K]) {
-  if (tbase + 8 <= n) {
-    const int4 x = __ldg(reinterpret_cast<const int4*>(a + tbase));
-    const int4 y = __ldg(reinterpret_cast<const int4*>(a + tbase) + 1);
-    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+// K consecutive int32 (16-byte aligned when full); -1 past the end
+__device__ __forceinline__ void load_iK(const int32_t* a, int64_t n, int64_t tbase, int (&v)[K]) {
+  if (tbase + K <= n) {
+#pragma unroll
+    for (int q = 0; q < K / 4; q++) {
+      const int4 x = __ldg(reinterpret_cast<const int4*>(a + tbase) + q);
+      v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < K; i++) v[i] = (tbase + i < n) ? __ldg(a + tbase + i) : -1;
@@ -378,15 +391,14 @@ struct Smem {
   } u;
   float4 wtu[NW];
   float4 wmid[NW][NW];  // union of the warps strictly between two warps
-  uint32_t bmk[NT];  // blend opens of each thread
-  uint32_t lmk[NT];  // leaves of each thread
   int nx;            // closes of earlier tiles' nodes listed for bbm_close
 };
 
-// element i of thread t lives at slot 8t + (i ^ (t & 7)): conflict-free both for
-// the coalesced copies and for the per-thread accesses
-__device__ __forceinline__ int slot(int t, int i) { return (t << 3) | (i ^ (t & 7)); }
-__device__ __forceinline__ int slot_of(int e) { return slot(e >> 3, e & 7); }
+// element i of thread t lives at slot Kt + (i ^ (t & 7)): conflict-free both for
+// the coalesced copies (8 consecutive elements of one thread per 128-byte
+// wavefront) and for the per-thread accesses (8 threads, distinct slot & 7)
+__device__ __forceinline__ int slot(int t, int i) { return t * K + (i ^ (t & 7)); }
+__device__ __forceinline__ int slot_of(int e) { return slot(e / K, e % K); }
 
 // union of the clipped leaves of whole threads [a, b]: the suffix of a's warp,
 // the warps strictly between (table), the window part of b's warp ending at
@@ -403,7 +415,7 @@ __device__ __forceinline__ float4 range_union_threads(const Smem& s, int a, int 
 }
 
 template <bool SHARD>
-__global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
+__global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -422,15 +434,19 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
 
   // ---- A. load -------------------------------------------------------------
   uint32_t om, cm, bm;
-  classify8(load_tags8(p.tags, p.n, tstart), om, cm, bm);
-  uint32_t lm = ~om & ~cm & 0xffu;
+  {
+    uint32_t tw[K / 4];
+    load_tagsK(p.tags, p.n, tstart, tw);
+    classifyK(tw, om, cm, bm);
+  }
+  uint32_t lm = ~om & ~cm & ((1u << K) - 1u);
   {
     const int64_t rem = p.n - tstart;
     if (rem < K) lm &= rem <= 0 ? 0u : ((1u << rem) - 1u);
   }
   int mt[K], pr[K];
-  load_i8(p.match, p.n, tstart, mt);
-  load_i8(p.parent, p.n, tstart, pr);
+  load_iK(p.match, p.n, tstart, mt);
+  load_iK(p.parent, p.n, tstart, pr);
   // contexts of out-of-tile parents (lc in node_bbox ∩ TC of their tile):
   // the last two distinct ones are fetched now, used in C/D
   int xa = -1, xb = -1;
@@ -450,8 +466,6 @@ __global__ void __launch_bounds__(NT, 6) bbm_main(Params p) {
     const int e = j * NT + tid;
     s.val[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bINF();
   }
-  s.bmk[tid] = bm;
-  s.lmk[tid] = lm;
   if (tid == 0) s.nx = 0;
   uint32_t thr_un = 0;  // opens closed beyond this thread (or never)
 #pragma unroll
