@@ -215,7 +215,14 @@ int tree_bbox_host(const uint8_t *h_tags, const float *h_leaf_bbox, int64_t n, f
 /* The whole hot path from host buffers: copy tags and boxes in, paren_match,
  * tree_bbox_matched on its outputs, copy match, parent and node_bbox out.  The
  * box upload and the match/parent download run on library side streams,
- * overlapped with the kernels (pass pinned host memory for real overlap). */
+ * overlapped with the kernels (pass pinned host memory for real overlap).
+ * When h_node_bbox is pinned (device-mapped under unified addressing) the box
+ * passes run in up to 16 chunks of tiles as the boxes arrive (each pass reads
+ * only its own and earlier tiles, §6 P:192-221 clips top-down, unions of
+ * closed nodes), each chunk's node_bbox is copied out while later chunks
+ * compute, and the few entries finished later (blend opens closed in a later
+ * chunk or never, R4) are then stored into h_node_bbox by a kernel through
+ * the mapping.  Same results as the unchunked path, bit for bit. */
 int paren_match_tree_bbox_host(const uint8_t *h_tags, const float *h_leaf_bbox, int64_t n, int32_t *h_match,
                                int32_t *h_parent, float *h_node_bbox, void *stream);
 

@@ -1,4 +1,5 @@
 // C ABI (include/treebbox.h): argument validation, workspace cache, launches.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -81,9 +82,12 @@ int get_ws(void* stream, int slot, size_t need, void** out) {
 }
 
 // Side streams / events of the host pipeline, one set per device (never freed).
+constexpr int kMaxChunks = 16;  // chunks of the pipelined host path
+int g_chunk_shift = 23;         // at least 2^shift elements per chunk (tests lower it)
 struct AuxStreams {
   cudaStream_t in = nullptr, out = nullptr;
   cudaEvent_t start = nullptr, in_done = nullptr, pm_done = nullptr, out_done = nullptr;
+  cudaEvent_t chunk_in[kMaxChunks] = {}, chunk_done[kMaxChunks] = {};
 };
 std::map<int, AuxStreams> g_aux;
 
@@ -100,6 +104,10 @@ int get_aux(AuxStreams** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.in_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.pm_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.out_done, cudaEventDisableTiming);
+    for (int c = 0; c < kMaxChunks && e == cudaSuccess; c++) {
+      e = cudaEventCreateWithFlags(&a.chunk_in[c], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.chunk_done[c], cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) {
       a = AuxStreams{};
       return cuda_fail(e, "side streams");
@@ -311,6 +319,60 @@ int tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, f
   return TB_OK;
 }
 
+// The chunked schedule of paren_match_tree_bbox_host (host result mapped):
+// tags in, paren_match, match / parent out (side stream `out`); boxes in by
+// chunks of tiles (side stream `in`); per chunk, once its boxes are in, the box
+// passes over its tiles (they read only earlier tiles) and its result out;
+// finally the never-closed blend opens, and the entries written after their
+// chunk went out are stored into the mapped host result by a kernel.
+static int pm_tb_host_pipelined(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, int32_t* h_match,
+                                int32_t* h_parent, float* h_node_bbox, float* hmap, uint8_t* d_tags,
+                                int32_t* d_match, int32_t* d_parent, float* d_in, float* d_out, cudaStream_t s,
+                                AuxStreams* ax) {
+  const int nt = tb::bbm_tiles(n);
+  const int64_t tile = tb::bbm_tile_elems();
+  int C = (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, n >> g_chunk_shift));
+  const int ct = (nt + C - 1) / C;
+  C = (nt + ct - 1) / ct;
+  void* bws = nullptr;
+  int r = get_ws(s, 5, tb::bbm_workspace_bytes(n), &bws);
+  if (r) return r;
+  auto lo = [&](int c) { return std::min<int64_t>(n, (int64_t)c * ct * tile); };
+  cudaError_t e = cudaEventRecord(ax->start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->in, ax->start, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
+  for (int c = 0; c < C && e == cudaSuccess; c++) {
+    const int64_t a = lo(c), b = lo(c + 1);
+    e = cudaMemcpyAsync(d_in + 4 * a, h_leaf_bbox + 4 * a, (size_t)(b - a) * 16, cudaMemcpyHostToDevice, ax->in);
+    if (e == cudaSuccess) e = cudaEventRecord(ax->chunk_in[c], ax->in);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "H2D inputs");
+  r = paren_match(d_tags, n, d_match, d_parent, s);
+  if (r) return r;
+  e = cudaEventRecord(ax->pm_done, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->out, ax->pm_done, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_match, d_match, (size_t)n * 4, cudaMemcpyDeviceToHost, ax->out);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_parent, d_parent, (size_t)n * 4, cudaMemcpyDeviceToHost, ax->out);
+  if (e == cudaSuccess) e = tb::bbm_begin(bws, n, s);
+  for (int c = 0; c < C && e == cudaSuccess; c++) {
+    const int64_t a = lo(c), b = lo(c + 1);
+    e = cudaStreamWaitEvent(s, ax->chunk_in[c], 0);
+    if (e == cudaSuccess)
+      e = tb::bbm_tiles_launch(d_tags, d_in, d_match, d_parent, n, d_out, bws, c * ct, std::min(nt, (c + 1) * ct), s);
+    if (e == cudaSuccess) e = cudaEventRecord(ax->chunk_done[c], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->out, ax->chunk_done[c], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h_node_bbox + 4 * a, d_out + 4 * a, (size_t)(b - a) * 16, cudaMemcpyDeviceToHost, ax->out);
+  }
+  if (e == cudaSuccess) e = tb::bbm_end(d_tags, d_in, d_match, d_parent, n, d_out, bws, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ax->out_done, ax->out);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ax->out_done, 0);
+  if (e == cudaSuccess) e = tb::bbm_patch_host_launch(d_tags, d_match, n, d_out, bws, hmap, ct, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "pipelined host path");
+  return TB_OK;
+}
+
 int paren_match_tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, int32_t* h_match,
                                int32_t* h_parent, float* h_node_bbox, void* stream) {
   g_err[0] = 0;
@@ -337,6 +399,18 @@ int paren_match_tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, 
   AuxStreams* ax = nullptr;
   r = get_aux(&ax);
   if (r) return r;
+  // Pinned (device-mapped) result: the box passes run chunk by chunk as the
+  // boxes arrive and each chunk's result goes out while later chunks compute.
+  float* hmap = nullptr;
+  {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, h_node_bbox) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer)
+      hmap = (float*)pa.devicePointer;
+    (void)cudaGetLastError();
+  }
+  if (hmap) return pm_tb_host_pipelined(h_tags, h_leaf_bbox, n, h_match, h_parent, h_node_bbox, hmap, d_tags,
+                                        d_match, d_parent, d_in, d_out, s, ax);
   cudaError_t e = cudaEventRecord(ax->start, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->in, ax->start, 0);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
@@ -443,6 +517,14 @@ int compact_scene(const uint8_t* d_tags, const float* d_boxes, int64_t n, const 
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }
+
+/* Debug: minimum chunk size (log2 elements) of the pipelined host path;
+ * returns the previous value (tests use small chunks on small inputs). */
+int tb_debug_host_chunk_shift(int shift) {
+  const int old = g_chunk_shift;
+  if (shift >= 10 && shift <= 40) g_chunk_shift = shift;
+  return old;
+}
 
 int tb_debug_tree_bbox_trace(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox,
                              uint64_t* d_trace, void* stream) {

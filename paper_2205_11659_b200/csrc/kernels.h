@@ -66,6 +66,21 @@ size_t bbm_workspace_bytes(int64_t n);
 int bbm_tile_elems();
 cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
                        int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace = nullptr);
+// The same passes split over tile ranges in order (chunked host pipeline):
+// bbm_begin once, bbm_tiles_launch for [t0, t1) as each range's boxes arrive
+// (every pass reads only its own and earlier tiles), bbm_end (never-closed
+// blend opens), then bbm_patch_host stores the entries written after their
+// chunk was copied out (blend opens closed in a later chunk, never-closed
+// ones) into the mapped host result.
+int bbm_tiles(int64_t n);
+cudaError_t bbm_begin(void* ws, int64_t n, cudaStream_t stream);
+cudaError_t bbm_tiles_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match,
+                             const int32_t* parent, int64_t n, float* node_bbox, void* ws, int t0, int t1,
+                             cudaStream_t stream);
+cudaError_t bbm_end(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                    int64_t n, float* node_bbox, void* ws, cudaStream_t stream);
+cudaError_t bbm_patch_host_launch(const uint8_t* tags, const int32_t* match, int64_t n, const float* node_bbox,
+                                  void* ws, float* host_mapped, int chunk_tiles, cudaStream_t stream);
 
 // Shard mode of the same kernels: match / parent hold global indices, the
 // chunk's element 0 is global index `off`; contexts of earlier chunks' opens

@@ -77,6 +77,7 @@ struct Params {
   float4* out;
   int64_t n;
   int ntiles;
+  int t0, t1;            // tiles of this launch: [t0, t1) (chunked pipeline; else [0, ntiles))
   float4* u[LV];         // u[0][T] = union of tile T's clipped leaves; u[k] over 32^k tiles
   int32_t* link;         // [ntiles] parent of the tile's bottom slice entry (-1: root / none)
   float4* tc;            // [ntiles] ctx(link)
@@ -254,8 +255,8 @@ __global__ void __launch_bounds__(128) bbm_reduce(Params p) {
     }
   }
   __syncthreads();
-  const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (T >= p.ntiles) return;
+  const int T = p.t0 + blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (T >= p.t1) return;
   const int64_t base = (int64_t)T * TILE, lbase = base + (int64_t)lane * RK;
   uint32_t om = 0, cm = 0, bmask = 0;  // opens, closes, blend opens of the lane's 32 elements
   if (lbase + RK <= p.n) {
@@ -337,23 +338,38 @@ __global__ void __launch_bounds__(128) bbm_reduce(Params p) {
 __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2, int* flag) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  const int nt = p.ntiles;
+  // tiles [t0, t1); TC of every tile before t0 is final (earlier launches of
+  // the chunked pipeline), so chains stop there
+  const int nt = p.ntiles, t0 = p.t0, t1 = p.t1;
   const int gt = (int)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
   const int nthr = (int)(gridDim.x * (int64_t)blockDim.x);
   float4* acc[2] = {acc2, acc2 + nt};
   int* ptr[2] = {ptr2, ptr2 + nt};
-  for (int V = gt; V < nt; V += nthr) {
+  for (int V = t0 + gt; V < t1; V += nthr) {
     const int X = __ldg(p.link + V);  // global index
-    // lc(X), written by bbm_reduce; an open of an earlier chunk: imported context
-    acc[0][V] = X >= p.off ? __ldg(p.out + (X - p.off)) : (X >= 0 ? ext_ctx(p, X) : bINF());
-    ptr[0][V] = X >= p.off ? (int)((X - p.off) / TILE) : -1;
+    // lc(X), written by bbm_reduce (or X's context: F6); an open of an earlier
+    // chunk: imported context
+    float4 a = bINF();
+    int q = -1;
+    if (X >= p.off) {
+      a = ld_relaxed_box(p.out + (X - p.off));
+      q = (int)((X - p.off) / TILE);
+      if (q < t0) {
+        a = isect(a, __ldcg(p.tc + q));
+        q = -1;
+      }
+    } else if (X >= 0) {
+      a = ext_ctx(p, X);
+    }
+    acc[0][V] = a;
+    ptr[0][V] = q;
   }
   int cb = 0;
   for (int round = 0; round < 40; round++) {
     if (gt == 0) flag[round & 1] = 0;
     grid.sync();
     int any = 0;
-    for (int V = gt; V < nt; V += nthr) {
+    for (int V = t0 + gt; V < t1; V += nthr) {
       float4 a = __ldcg(acc[cb] + V);
       int q = __ldcg(ptr[cb] + V);
       if (q >= 0) {
@@ -370,7 +386,7 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
     grid.sync();
     if (__ldcg(flag + (round & 1)) == 0) break;
   }
-  for (int V = gt; V < nt; V += nthr) p.tc[V] = __ldcg(acc[cb] + V);
+  for (int V = t0 + gt; V < t1; V += nthr) p.tc[V] = __ldcg(acc[cb] + V);
 }
 
 // ----------------------------------------------------------------------------
@@ -419,7 +435,7 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int T = blockIdx.x;
+  const int T = p.t0 + blockIdx.x;
   const int64_t base = (int64_t)T * TILE;  // local indices (arrays)
   const int64_t tstart = base + (int64_t)tid * K;
   const int nvalid = (int)(p.n - base < TILE ? p.n - base : TILE);
@@ -724,12 +740,15 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
 
 // ----------------------------------------------------------------------------
 // bbm_hier: level k of the 32-ary hierarchy of tile unions from level k - 1
-// (one warp per group; launched once per level)
+// (one warp per group; launched once per level).  Groups [g0, g1) are the ones
+// touching the launch's tiles; a group still missing later tiles is rebuilt by
+// a later launch and never read before (range unions take whole groups inside
+// finished tiles only).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) bbm_hier(Params p, int k, int m /* nodes at level k - 1 */) {
+__global__ void __launch_bounds__(256) bbm_hier(Params p, int k, int m /* nodes at level k - 1 */, int g0, int g1) {
   const int lane = threadIdx.x & 31;
-  const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if ((g << 5) >= m) return;
+  const int g = g0 + blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (g >= g1 || (g << 5) >= m) return;
   const int c = (g << 5) + lane;
   float4 v = c < m ? __ldcg(p.u[k - 1] + c) : bEMPTY();
   v = warp_unite_all(v);
@@ -744,7 +763,7 @@ __global__ void __launch_bounds__(256) bbm_hier(Params p, int k, int m /* nodes 
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) bbm_close(Params p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int T = blockIdx.x;
+  const int T = p.t0 + blockIdx.x;
   const int cnt = __ldg(p.xcnt + T);
   int cto = INT_MIN;  // warp cache: the last range resolved (deep chains repeat one open tile); To = -1 is a key
   float4 cR = bEMPTY();
@@ -815,6 +834,31 @@ __global__ void __launch_bounds__(256) bbm_final(Params p) {
     const int To = o / TILE;
     const float4 after = To + 1 < p.ntiles ? range_union_tiles_warp(p, To + 1, p.ntiles - 1) : bEMPTY();
     if (lane == 0) p.out[o] = unite(__ldcg(p.su + o), after);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// bbm_patch_host (chunked host pipeline): node_bbox entries written after
+// their chunk was copied out -- blend opens that receive their union from a
+// close in a later chunk (bbm_close) or that are never closed (bbm_final) --
+// stored again straight into the (mapped, pinned) host result.  One warp per
+// tile over its listed closes; then the never-closed list.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bbm_patch_host(Params p, float4* hout, int ctiles) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * 8;
+  for (int T = blockIdx.x * 8 + (threadIdx.x >> 5); T < p.ntiles; T += nwarps) {
+    const int cnt = __ldg(p.xcnt + T);
+    for (int j = lane; j < cnt; j += 32) {
+      const int c = __ldg(p.xc + (int64_t)T * TILE + j);
+      const int o = __ldg(p.match + c);
+      if (o >= 0 && (o / TILE) / ctiles < T / ctiles && __ldg(p.tags + o) == 2) hout[o] = __ldcg(p.out + o);
+    }
+  }
+  const uint32_t nv = __ldcg(p.nnever);
+  for (uint32_t q = blockIdx.x * 256 + threadIdx.x; q < nv; q += gridDim.x * 256) {
+    const int o = __ldcg(p.never + q);
+    hout[o] = __ldcg(p.out + o);
   }
 }
 
@@ -1073,6 +1117,8 @@ bbm::Params make_params(const uint8_t* tags, const float* leaf_bbox, const int32
   p.out = reinterpret_cast<float4*>(node_bbox);
   p.n = n;
   p.ntiles = (int)L.ntiles;
+  p.t0 = 0;
+  p.t1 = (int)L.ntiles;
   p.nnever = (uint32_t*)(b + L.off_nnever);
   for (int k = 0; k < bbm::LV; k++) p.u[k] = (float4*)(b + L.off_u[k]);
   p.link = (int32_t*)(b + L.off_link);
@@ -1097,7 +1143,7 @@ cudaError_t launch_tc(const bbm::Params& p, void* ws, cudaStream_t stream) {
   float4* acc2 = (float4*)(b + L.off_tcacc);
   int* ptr2 = (int*)(b + L.off_tcptr);
   int* flag = (int*)(b + L.off_tcflag);
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((L.ntiles + 255) / 256, bbm::tc_blocks()));
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((p.t1 - p.t0 + 255) / 256, bbm::tc_blocks()));
   bbm::Params pc = p;
   void* args[] = {(void*)&pc, (void*)&acc2, (void*)&ptr2, (void*)&flag};
   void* tok;
@@ -1107,24 +1153,32 @@ cudaError_t launch_tc(const bbm::Params& p, void* ws, cudaStream_t stream) {
   return err;
 }
 
-// bbm_main, the union hierarchy, bbm_close, bbm_final
-cudaError_t launch_rest(const bbm::Params& p, cudaStream_t stream) {
-  const int64_t nt = p.ntiles;
+// bbm_main, the union hierarchy and bbm_close over tiles [p.t0, p.t1)
+cudaError_t launch_range(const bbm::Params& p, cudaStream_t stream) {
+  const unsigned nt = (unsigned)(p.t1 - p.t0);
   bbm::main_setup();
   if (p.off == 0 && p.n_ext == 0 && p.pops == nullptr)
-    TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<false><<<(unsigned)nt, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
+    TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<false><<<nt, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
   else
-    TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<true><<<(unsigned)nt, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
+    TB_LAUNCH(stream, "bbm_main", (bbm::bbm_main<true><<<nt, bbm::NT, sizeof(bbm::Smem), stream>>>(p)));
   {
-    int64_t m = nt;
+    int64_t m = p.ntiles;
     for (int k = 1; k < bbm::LV && m > 1; k++) {
-      const int64_t groups = (m + 31) / 32;
+      const int sh = 5 * k;
+      const int g0 = p.t0 >> sh, g1 = ((p.t1 - 1) >> sh) + 1;  // groups touching the range
       TB_LAUNCH(stream, "bbm_hier",
-                (bbm::bbm_hier<<<(unsigned)((groups + 7) / 8), 256, 0, stream>>>(p, k, (int)m)));
-      m = groups;
+                (bbm::bbm_hier<<<(unsigned)((g1 - g0 + 7) / 8), 256, 0, stream>>>(p, k, (int)m, g0, g1)));
+      m = (m + 31) / 32;
     }
   }
-  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<(unsigned)nt, 128, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<nt, 128, 0, stream>>>(p)));
+  return cudaGetLastError();
+}
+
+// bbm_main, the union hierarchy, bbm_close, bbm_final
+cudaError_t launch_rest(const bbm::Params& p, cudaStream_t stream) {
+  cudaError_t err = launch_range(p, stream);
+  if (err != cudaSuccess) return err;
   TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
   return cudaGetLastError();
 }
@@ -1142,6 +1196,45 @@ cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_
   err = launch_tc(p, ws, stream);
   if (err != cudaSuccess) return err;
   return launch_rest(p, stream);
+}
+
+int bbm_tiles(int64_t n) { return (int)((n + bbm::TILE - 1) / bbm::TILE); }
+
+cudaError_t bbm_begin(void* ws, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  bbm::Layout L(n);
+  return cudaMemsetAsync((char*)ws + L.zero_off, 0, L.zero_bytes, stream);
+}
+
+cudaError_t bbm_tiles_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match,
+                             const int32_t* parent, int64_t n, float* node_bbox, void* ws, int t0, int t1,
+                             cudaStream_t stream) {
+  if (n <= 0 || t0 >= t1) return cudaSuccess;
+  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, nullptr, nullptr);
+  p.t0 = t0;
+  p.t1 = t1;
+  TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<(unsigned)((t1 - t0 + 3) / 4), 128, 0, stream>>>(p)));
+  cudaError_t err = launch_tc(p, ws, stream);
+  if (err != cudaSuccess) return err;
+  return launch_range(p, stream);
+}
+
+cudaError_t bbm_end(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                    int64_t n, float* node_bbox, void* ws, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, nullptr, nullptr);
+  TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
+  return cudaGetLastError();
+}
+
+cudaError_t bbm_patch_host_launch(const uint8_t* tags, const int32_t* match, int64_t n, const float* node_bbox,
+                                  void* ws, float* host_mapped, int chunk_tiles, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  bbm::Params p = make_params(tags, nullptr, match, nullptr, n, const_cast<float*>(node_bbox), ws, nullptr, nullptr);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p.ntiles + 7) / 8, 148 * 8));
+  TB_LAUNCH(stream, "bbm_patch_host", (bbm::bbm_patch_host<<<blocks, 256, 0, stream>>>(
+                                          p, reinterpret_cast<float4*>(host_mapped), chunk_tiles)));
+  return cudaGetLastError();
 }
 
 cudaError_t bbm_shard_phase1(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,

@@ -231,3 +231,56 @@ def test_virtual_shards_equal_oracle(nshards):
         got = out.cpu().numpy()
         bad = np.nonzero((got.view(np.uint32) != ref.view(np.uint32)).any(1))[0]
         assert len(bad) == 0, (i, bad[:10], len(bad), t[bad[:5]].tolist(), got[bad[:3]].tolist(), ref[bad[:3]].tolist())
+
+
+def _pipeline_cases():
+    g = torch.Generator().manual_seed(77)
+    chain = torch.stack([torch.where(torch.rand(40_000, generator=g) < 0.6, 1, 2).to(torch.uint8),
+                         torch.zeros(40_000, dtype=torch.uint8)], 1).reshape(-1)
+    return [scenegen.walk_tags(300_001, 5),
+            scenegen.walk_tags(250_000, 8, p_leaf=0.3, p_clip=0.5),
+            scenegen.deep_chain_tags(200_000, 3, leaves_mid=True),
+            torch.cat([chain, torch.full((40_000,), 3, dtype=torch.uint8)]),  # blend opens closed chunks later
+            torch.full((60_000,), 2, dtype=torch.uint8),                       # blend opens never closed (R4)
+            torch.multinomial(torch.tensor([0.3, 0.15, 0.1, 0.45]), 300_000, replacement=True,
+                              generator=g).to(torch.uint8)]
+
+
+@pytest.mark.parametrize("shift", [12, 14])
+def test_pipeline_host_api_chunked(shift):
+    """The chunked schedule of paren_match_tree_bbox_host (pinned result): box
+    passes over tile ranges as the boxes arrive, per-chunk copies out, late
+    entries (blend opens closed in a later chunk, never-closed ones) stored
+    through the host mapping -- bit-exact against the oracle."""
+    tb = gpu()
+    lib = tb.load()
+    old = lib.tb_debug_host_chunk_shift(shift)
+    try:
+        for i, t in enumerate(_pipeline_cases()):
+            t = t.pin_memory()
+            b = scenegen.boxes(t.numel(), 40 + i, t).pin_memory()
+            m = torch.empty(t.numel(), dtype=torch.int32).pin_memory()
+            p = torch.empty_like(m).pin_memory()
+            out = torch.full_like(b, float("nan")).pin_memory()
+            tb.paren_match_tree_bbox_host(t, b, m, p, out)
+            m_ref, p_ref = oracle.paren_match(t.numpy())
+            ref = oracle.tree_bbox(t.numpy(), b.numpy())
+            assert np.array_equal(m.numpy(), m_ref) and np.array_equal(p.numpy(), p_ref), i
+            bad = np.nonzero((out.numpy().view(np.uint32) != ref.view(np.uint32)).any(1))[0]
+            assert len(bad) == 0, (i, bad[:10], len(bad))
+    finally:
+        lib.tb_debug_host_chunk_shift(old)
+
+
+def test_pipeline_host_api_pageable():
+    """Pageable result buffer: the unchunked schedule, same results."""
+    tb = gpu()
+    t = scenegen.walk_tags(200_003, 6)
+    b = scenegen.boxes(t.numel(), 6, t)
+    m = torch.empty(t.numel(), dtype=torch.int32)
+    p = torch.empty_like(m)
+    out = torch.empty_like(b)
+    tb.paren_match_tree_bbox_host(t, b, m, p, out)
+    ref = oracle.tree_bbox(t.numpy(), b.numpy())
+    assert np.array_equal(m.numpy(), oracle.paren_match(t.numpy())[0])
+    assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
