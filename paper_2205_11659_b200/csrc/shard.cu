@@ -19,6 +19,9 @@
 // chunks of one buffer on one GPU in lockstep (tests; no peer traffic).
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "kernels.h"
@@ -56,6 +59,70 @@ Bic2 combine(Bic2 x, Bic2 y) {
   return Bic2{x.a + y.a - m, x.b + y.b - m};
 }
 
+// Device scratch of the shard protocols, reused across calls per (device,
+// stream) so that a steady-state call allocates nothing: a bump arena.  A call
+// that outgrows it gets extra blocks, merged into one block at the start of
+// the next call.  Calls on one stream are issued by one host thread at a time.
+struct Arena {
+  std::vector<std::pair<char*, size_t>> blocks;
+  int cur = 0;      // block being filled
+  size_t used = 0;  // its fill
+};
+std::mutex g_arena_mu;
+std::map<std::pair<int, cudaStream_t>, Arena> g_arenas;
+
+class Scratch {
+ public:
+  // slot: one arena per protocol (a driver holding buffers calls others)
+  Scratch(cudaStream_t s, int slot) : s_(s), slot_(slot) {}
+  cudaError_t begin() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_arena_mu);
+    a_ = &g_arenas[{dev * 8 + slot_, s_}];
+    if (a_->blocks.size() > 1) {
+      size_t total = 0;
+      for (auto& b : a_->blocks) total += b.second;
+      e = cudaStreamSynchronize(s_);
+      for (auto& b : a_->blocks) cudaFree(b.first);
+      a_->blocks.clear();
+      char* q = nullptr;
+      if (e == cudaSuccess) e = cudaMalloc(&q, total);
+      if (e != cudaSuccess) return e;
+      a_->blocks.push_back({q, total});
+    }
+    a_->cur = 0;
+    a_->used = 0;
+    return cudaSuccess;
+  }
+  template <class T>
+  cudaError_t get(size_t bytes, T** out) {
+    bytes = std::max<size_t>((bytes + 255) & ~size_t(255), 256);
+    Arena& a = *a_;
+    while (a.cur < (int)a.blocks.size() && a.used + bytes > a.blocks[a.cur].second) {
+      a.cur++;
+      a.used = 0;
+    }
+    if (a.cur == (int)a.blocks.size()) {
+      char* q = nullptr;
+      const size_t sz = std::max(bytes, (size_t)64 << 20);
+      cudaError_t e = cudaMalloc(&q, sz);
+      if (e != cudaSuccess) return e;
+      a.blocks.push_back({q, sz});
+      a.used = 0;
+    }
+    *out = reinterpret_cast<T*>(a.blocks[a.cur].first + a.used);
+    a.used += bytes;
+    return cudaSuccess;
+  }
+
+ private:
+  cudaStream_t s_;
+  int slot_;
+  Arena* a_ = nullptr;
+};
+
 // Per-chunk state of the paren_match shard protocol.
 struct PmChunk {
   const uint8_t* tags;
@@ -63,35 +130,24 @@ struct PmChunk {
   int32_t* match;
   int32_t* parent;
   cudaStream_t s;
-  // device buffers (one allocation)
-  void* mem = nullptr;
+  // device buffers (shard scratch)
   void* ws;           // pm workspace
   int32_t* hdr;       // [2] a, b
   int32_t* opens;     // [n] unmatched opens (send)
   int32_t* stack;     // [n + 1] composed initial stack
   int2* pairs;        // [n] (open, close) send
   int* Ldev;          // [G]
-  size_t bytes = 0;
 
-  cudaError_t alloc(int G) {
+  cudaError_t alloc(int G, Scratch& sc) {
     const size_t wsb = pm_workspace_bytes(std::max<int64_t>(n, 1));
     const size_t nn = (size_t)std::max<int64_t>(n, 1);
-    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    bytes = al(wsb) + al(8) + al(4 * nn) + al(4 * (nn + 1)) + al(8 * nn) + al(4 * (size_t)G);
-    cudaError_t e = cudaMalloc(&mem, bytes);
-    if (e != cudaSuccess) return e;
-    char* b = (char*)mem;
-    ws = b; b += al(wsb);
-    hdr = (int32_t*)b; b += al(8);
-    opens = (int32_t*)b; b += al(4 * nn);
-    stack = (int32_t*)b; b += al(4 * (nn + 1));
-    pairs = (int2*)b; b += al(8 * nn);
-    Ldev = (int*)b;
-    return cudaSuccess;
-  }
-  void release() {
-    if (mem) cudaFree(mem);
-    mem = nullptr;
+    cudaError_t e = sc.get(wsb, &ws);
+    if (e == cudaSuccess) e = sc.get(8, &hdr);
+    if (e == cudaSuccess) e = sc.get(4 * nn, &opens);
+    if (e == cudaSuccess) e = sc.get(4 * (nn + 1), &stack);
+    if (e == cudaSuccess) e = sc.get(8 * nn, &pairs);
+    if (e == cudaSuccess) e = sc.get(4 * (size_t)G, &Ldev);
+    return e;
   }
 
   // phase 1: chunk-local reduce + summary
@@ -125,9 +181,11 @@ struct PmChunk {
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
-    *npairs = std::min<int64_t>(ag, H);
-    e = cudaMemsetAsync(pairs, 0xff, sizeof(int2) * (size_t)std::max<int64_t>(n, 1), s);
-    if (e != cudaSuccess) return e;
+    *npairs = std::min<int64_t>(ag, H);  // the d-th pop of the incoming stack writes pairs[d]
+    if (*npairs > 0) {
+      e = cudaMemsetAsync(pairs, 0xff, sizeof(int2) * (size_t)*npairs, s);
+      if (e != cudaSuccess) return e;
+    }
     ShardInit init{(int)mine.a, H, stack, lo, off, pairs};
     e = pm_reduce_launch(tags, n, match, ws, &init, s);
     if (e == cudaSuccess) e = pm_finish_launch(tags, n, match, parent, ws, &init, s);
@@ -170,7 +228,6 @@ struct BbmChunk {
   int64_t n, off;
   float* out;
   cudaStream_t s;
-  void* mem = nullptr;
   void* ws = nullptr;
   ShardOpen* fs = nullptr;   // [n] final stack (send 1)
   ShardOpen* suc = nullptr;  // [n] union after each final-stack open (send 2)
@@ -179,25 +236,21 @@ struct BbmChunk {
   int* link = nullptr;
   float4* tu = nullptr;      // chunk union (send 2)
   int* bdev = nullptr;
-  void* extmem = nullptr;
   int32_t* ext_idx = nullptr;
   float4* ext_ctx = nullptr;
   int b = 0, linkh = -1, np = 0, n_ext = 0;
 
   BbmShard sh() const { return BbmShard{off, ext_idx, ext_ctx, n_ext, pops, npops}; }
 
-  cudaError_t alloc() {
-    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  cudaError_t alloc(Scratch& sc) {
     const size_t nn = (size_t)std::max<int64_t>(n, 1);
-    const size_t wsb = bbm_workspace_bytes((int64_t)nn);
-    const size_t bytes = al(wsb) + 3 * al(32 * nn) + al(64);
-    cudaError_t e = cudaMalloc(&mem, bytes);
+    char* c = nullptr;
+    cudaError_t e = sc.get(bbm_workspace_bytes((int64_t)nn), &ws);
+    if (e == cudaSuccess) e = sc.get(32 * nn, &fs);
+    if (e == cudaSuccess) e = sc.get(32 * nn, &suc);
+    if (e == cudaSuccess) e = sc.get(32 * nn, &pops);
+    if (e == cudaSuccess) e = sc.get(64, &c);
     if (e != cudaSuccess) return e;
-    char* c = (char*)mem;
-    ws = c; c += al(wsb);
-    fs = (ShardOpen*)c; c += al(32 * nn);
-    suc = (ShardOpen*)c; c += al(32 * nn);
-    pops = (ShardPop*)c; c += al(32 * nn);
     tu = (float4*)c;
     npops = (uint32_t*)(c + 16);
     link = (int*)(c + 20);
@@ -210,13 +263,12 @@ struct BbmChunk {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     return e;
   }
-  cudaError_t compose(const int4* hdr, int G, int g, const ShardOpen* allfs, int maxb, int cnt) {
+  cudaError_t compose(const int4* hdr, int G, int g, const ShardOpen* allfs, int maxb, int cnt, Scratch& sc) {
     n_ext = cnt;
     const size_t c1 = (size_t)std::max(cnt, 1);
-    cudaError_t e = cudaMalloc(&extmem, 16 * c1 + 4 * c1 + 256);
+    cudaError_t e = sc.get(16 * c1, &ext_ctx);
+    if (e == cudaSuccess) e = sc.get(4 * c1, &ext_idx);
     if (e != cudaSuccess) return e;
-    ext_ctx = (float4*)extmem;
-    ext_idx = (int32_t*)((char*)extmem + 16 * c1);
     if (cnt == 0) return cudaSuccess;
     return bbm_compose_launch(hdr, G, g, allfs, maxb, cnt, ext_idx, ext_ctx, s);
   }
@@ -239,11 +291,6 @@ struct BbmChunk {
     return bbm_fixup_launch(tags, leaf, match, parent, n, out, ws, &x, hdr, G, g, allsuc, maxb, alltu, allpops,
                             npops_all, maxp, s);
   }
-  void release() {
-    if (mem) cudaFree(mem);
-    if (extmem) cudaFree(extmem);
-    mem = extmem = nullptr;
-  }
 };
 
 }  // namespace
@@ -251,11 +298,16 @@ struct BbmChunk {
 // Virtual shards of one buffer (tests): the matching of the whole buffer comes
 // from the single-device paren_match (its sharded protocol is tested apart).
 cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, float* out, cudaStream_t s) {
+  Scratch sc(s, 3);
+  {
+    const cudaError_t e0 = sc.begin();
+    if (e0 != cudaSuccess) return e0;
+  }
   int32_t* mp = nullptr;
   void* pmws = nullptr;
   const int64_t n64 = (n + 63) & ~int64_t(63);  // keeps parent 16-byte aligned
-  cudaError_t e = cudaMalloc(&mp, 8 * (size_t)n64);
-  if (e == cudaSuccess) e = cudaMalloc(&pmws, pm_workspace_bytes(n));
+  cudaError_t e = sc.get(8 * (size_t)n64, &mp);
+  if (e == cudaSuccess) e = sc.get(pm_workspace_bytes(n), &pmws);
   int32_t* match = mp;
   int32_t* parent = mp + n64;
   if (e == cudaSuccess) e = pm_launch(tags, n, match, parent, pmws, nullptr, s);
@@ -272,7 +324,7 @@ cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, 
     c.off = a;
     c.out = out + 4 * a;
     c.s = s;
-    e = c.alloc();
+    e = c.alloc(sc);
   }
   for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].phase1();
   for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].read_header();
@@ -286,11 +338,11 @@ cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, 
   int4* hdr_dev = nullptr;
   ShardOpen *allfs = nullptr, *allsuc = nullptr;
   float4* alltu = nullptr;
-  if (e == cudaSuccess) e = cudaMalloc(&hdr_dev, sizeof(int4) * G);
+  if (e == cudaSuccess) e = sc.get(sizeof(int4) * G, &hdr_dev);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hdr_dev, hdr.data(), sizeof(int4) * G, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMalloc(&allfs, sizeof(ShardOpen) * (size_t)maxb * G);
-  if (e == cudaSuccess) e = cudaMalloc(&allsuc, sizeof(ShardOpen) * (size_t)maxb * G);
-  if (e == cudaSuccess) e = cudaMalloc(&alltu, sizeof(float4) * G);
+  if (e == cudaSuccess) e = sc.get(sizeof(ShardOpen) * (size_t)maxb * G, &allfs);
+  if (e == cudaSuccess) e = sc.get(sizeof(ShardOpen) * (size_t)maxb * G, &allsuc);
+  if (e == cudaSuccess) e = sc.get(sizeof(float4) * G, &alltu);
   for (int g = 0; g < G && e == cudaSuccess; g++)
     if (ch[g].b > 0)
       e = cudaMemcpyAsync(allfs + (size_t)g * maxb, ch[g].fs, sizeof(ShardOpen) * ch[g].b, cudaMemcpyDeviceToDevice,
@@ -298,7 +350,7 @@ cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, 
   // compose + phase 2
   int before = 0;
   for (int g = 0; g < G && e == cudaSuccess; g++) {
-    e = ch[g].compose(hdr_dev, G, g, allfs, maxb, before);
+    e = ch[g].compose(hdr_dev, G, g, allfs, maxb, before, sc);
     if (e == cudaSuccess) e = ch[g].phase2();
     before += ch[g].b;
   }
@@ -312,8 +364,8 @@ cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, 
   }
   ShardPop* allpops = nullptr;
   int* np_dev = nullptr;
-  if (e == cudaSuccess) e = cudaMalloc(&allpops, sizeof(ShardPop) * (size_t)maxp * G);
-  if (e == cudaSuccess) e = cudaMalloc(&np_dev, sizeof(int) * G);
+  if (e == cudaSuccess) e = sc.get(sizeof(ShardPop) * (size_t)maxp * G, &allpops);
+  if (e == cudaSuccess) e = sc.get(sizeof(int) * G, &np_dev);
   if (e == cudaSuccess) e = cudaMemcpyAsync(np_dev, np.data(), sizeof(int) * G, cudaMemcpyHostToDevice, s);
   for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].export_unions();
   for (int g = 0; g < G && e == cudaSuccess; g++) {
@@ -328,15 +380,6 @@ cudaError_t bb_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, 
   for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].fixup(hdr_dev, G, g, allsuc, maxb, alltu, allpops, np_dev, maxp);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = e2;
-  for (auto& c : ch) c.release();
-  cudaFree(hdr_dev);
-  cudaFree(allfs);
-  cudaFree(allsuc);
-  cudaFree(alltu);
-  cudaFree(allpops);
-  cudaFree(np_dev);
-  cudaFree(mp);
-  cudaFree(pmws);
   return e;
 }
 
@@ -348,6 +391,11 @@ cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* 
 cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t* match, const int32_t* parent,
                            int64_t n, int64_t off, float* out, ncclComm_t comm, cudaStream_t s, int* nccl_err) {
   *nccl_err = 0;
+  Scratch sc(s, 1);
+  {
+    const cudaError_t e0 = sc.begin();
+    if (e0 != cudaSuccess) return e0;
+  }
   int G = 0, g = 0;
   if (ncclCommCount(comm, &G) != ncclSuccess || ncclCommUserRank(comm, &g) != ncclSuccess) {
     *nccl_err = 1;
@@ -367,14 +415,14 @@ cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t
   c.off = off;
   c.out = out;
   c.s = s;
-  if (e == cudaSuccess && !*nccl_err) e = c.alloc();
+  if (e == cudaSuccess && !*nccl_err) e = c.alloc(sc);
   if (e == cudaSuccess && !*nccl_err) e = c.phase1();
   if (e == cudaSuccess && !*nccl_err) e = c.read_header();
   // exchange 1: headers, then final-stack lists padded to the largest
   int4* hdr_dev = nullptr;
   std::vector<int4> hdr(G);
   int maxb = 1, before = 0;
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&hdr_dev, sizeof(int4) * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) e = sc.get(sizeof(int4) * (G + 1), &hdr_dev);
   if (e == cudaSuccess && !*nccl_err) {
     const int4 mine = make_int4((int)off, (int)n, c.b, c.linkh);
     e = cudaMemcpyAsync(hdr_dev + G, &mine, sizeof(int4), cudaMemcpyHostToDevice, s);
@@ -388,21 +436,21 @@ cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t
     }
   }
   ShardOpen *allfs = nullptr, *allsuc = nullptr;
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allfs, sizeof(ShardOpen) * (size_t)maxb * (G + 1));
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allsuc, sizeof(ShardOpen) * (size_t)maxb * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) e = sc.get(sizeof(ShardOpen) * (size_t)maxb * (G + 1), &allfs);
+  if (e == cudaSuccess && !*nccl_err) e = sc.get(sizeof(ShardOpen) * (size_t)maxb * (G + 1), &allsuc);
   ShardOpen* sendfs = allfs + (size_t)maxb * G;
   if (e == cudaSuccess && !*nccl_err && c.b > 0)
     e = cudaMemcpyAsync(sendfs, c.fs, sizeof(ShardOpen) * c.b, cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess && !*nccl_err)
     ok(ncclAllGather(sendfs, allfs, sizeof(ShardOpen) * (size_t)maxb, ncclUint8, comm, s));
-  if (e == cudaSuccess && !*nccl_err) e = c.compose(hdr_dev, G, g, allfs, maxb, before);
+  if (e == cudaSuccess && !*nccl_err) e = c.compose(hdr_dev, G, g, allfs, maxb, before, sc);
   if (e == cudaSuccess && !*nccl_err) e = c.phase2();
   if (e == cudaSuccess && !*nccl_err) e = c.read_npops();
   // exchange 2
   int* np_dev = nullptr;
   std::vector<int> np(G, 0);
   int maxp = 1;
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&np_dev, sizeof(int) * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) e = sc.get(sizeof(int) * (G + 1), &np_dev);
   if (e == cudaSuccess && !*nccl_err) e = cudaMemcpyAsync(np_dev + G, &c.np, sizeof(int), cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess && !*nccl_err && ok(ncclAllGather(np_dev + G, np_dev, 1, ncclInt32, comm, s))) {
     e = cudaMemcpyAsync(np.data(), np_dev, sizeof(int) * G, cudaMemcpyDeviceToHost, s);
@@ -411,8 +459,8 @@ cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t
   }
   ShardPop* allpops = nullptr;
   float4* alltu = nullptr;
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allpops, sizeof(ShardPop) * (size_t)maxp * (G + 1));
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&alltu, sizeof(float4) * G);
+  if (e == cudaSuccess && !*nccl_err) e = sc.get(sizeof(ShardPop) * (size_t)maxp * (G + 1), &allpops);
+  if (e == cudaSuccess && !*nccl_err) e = sc.get(sizeof(float4) * G, &alltu);
   if (e == cudaSuccess && !*nccl_err) e = c.export_unions();
   ShardPop* sendpops = allpops + (size_t)maxp * G;
   ShardOpen* sendsuc = allsuc + (size_t)maxb * G;
@@ -428,13 +476,6 @@ cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t
   if (e == cudaSuccess && !*nccl_err) e = c.fixup(hdr_dev, G, g, allsuc, maxb, alltu, allpops, np_dev, maxp);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = e2;
-  c.release();
-  cudaFree(hdr_dev);
-  cudaFree(allfs);
-  cudaFree(allsuc);
-  cudaFree(allpops);
-  cudaFree(alltu);
-  cudaFree(np_dev);
   return e;
 }
 
@@ -442,16 +483,20 @@ cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t
 cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, float* out,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err) {
   *nccl_err = 0;
+  Scratch sc(s, 2);
+  {
+    const cudaError_t e0 = sc.begin();
+    if (e0 != cudaSuccess) return e0;
+  }
   int32_t* mp = nullptr;
   const int64_t n64 = (std::max<int64_t>(n, 1) + 63) & ~int64_t(63);  // keeps parent 16-byte aligned
-  cudaError_t e = cudaMalloc(&mp, 8 * (size_t)n64);
+  cudaError_t e = sc.get(8 * (size_t)n64, &mp);
   int32_t* match = mp;
   int32_t* parent = mp + n64;
   if (e == cudaSuccess) e = pm_nccl_shard(tags, n, off, match, parent, comm, s, nccl_err);
   if (e == cudaSuccess && !*nccl_err) e = bbm_nccl_shard(tags, leaf, match, parent, n, off, out, comm, s, nccl_err);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = e2;
-  cudaFree(mp);
   return e;
 }
 #endif
@@ -460,6 +505,11 @@ cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int
 // stream; the all-gathers are device copies.  Results must equal the
 // unsharded call (tests).
 cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int32_t* parent, cudaStream_t s) {
+  Scratch sc(s, 4);
+  {
+    const cudaError_t e0 = sc.begin();
+    if (e0 != cudaSuccess) return e0;
+  }
   std::vector<PmChunk> ch(G);
   cudaError_t e = cudaSuccess;
   for (int g = 0; g < G && e == cudaSuccess; g++) {
@@ -472,7 +522,7 @@ cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int
     ch[g].match = match + a;
     ch[g].parent = parent + a;
     ch[g].s = s;
-    e = ch[g].alloc(G);
+    e = ch[g].alloc(G, sc);
   }
   for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].phase1();
   // exchange 1
@@ -489,7 +539,7 @@ cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int
     }
   }
   int32_t* allopens = nullptr;
-  if (e == cudaSuccess) e = cudaMalloc(&allopens, sizeof(int32_t) * (size_t)maxb * G);
+  if (e == cudaSuccess) e = sc.get(sizeof(int32_t) * (size_t)maxb * G, &allopens);
   for (int g = 0; g < G && e == cudaSuccess; g++)
     if (hdrs[g].b > 0)
       e = cudaMemcpyAsync(allopens + (size_t)g * maxb, ch[g].opens, 4 * (size_t)hdrs[g].b, cudaMemcpyDeviceToDevice,
@@ -500,7 +550,7 @@ cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int
   int64_t maxp = 1;
   for (int g = 0; g < G; g++) maxp = std::max(maxp, np[g]);
   int2* allpairs = nullptr;
-  if (e == cudaSuccess) e = cudaMalloc(&allpairs, sizeof(int2) * (size_t)maxp * G);
+  if (e == cudaSuccess) e = sc.get(sizeof(int2) * (size_t)maxp * G, &allpairs);
   if (e == cudaSuccess) e = cudaMemsetAsync(allpairs, 0xff, sizeof(int2) * (size_t)maxp * G, s);
   for (int g = 0; g < G && e == cudaSuccess; g++)
     if (np[g] > 0)
@@ -509,9 +559,6 @@ cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int
   for (int g = 0; g < G && e == cudaSuccess; g++) e = ch[g].phase3(allpairs, maxp * G);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = e2;
-  cudaFree(allopens);
-  cudaFree(allpairs);
-  for (auto& c : ch) c.release();
   return e;
 }
 
@@ -521,6 +568,11 @@ cudaError_t pm_vshard(const uint8_t* tags, int64_t n, int G, int32_t* match, int
 cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* match, int32_t* parent,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err) {
   *nccl_err = 0;
+  Scratch sc(s, 0);
+  {
+    const cudaError_t e0 = sc.begin();
+    if (e0 != cudaSuccess) return e0;
+  }
   int G = 0, g = 0;
   if (ncclCommCount(comm, &G) != ncclSuccess || ncclCommUserRank(comm, &g) != ncclSuccess) {
     *nccl_err = 1;
@@ -533,7 +585,7 @@ cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* 
   c.match = match;
   c.parent = parent;
   c.s = s;
-  cudaError_t e = c.alloc(G);
+  cudaError_t e = c.alloc(G, sc);
   if (e == cudaSuccess) e = c.phase1();
   int32_t* allhdr = nullptr;
   int32_t* allopens = nullptr;
@@ -544,7 +596,7 @@ cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* 
     if (r != ncclSuccess) *nccl_err = (int)r;
     return r == ncclSuccess;
   };
-  if (e == cudaSuccess) e = cudaMalloc(&allhdr, 8 * (size_t)G);
+  if (e == cudaSuccess) e = sc.get(8 * (size_t)G, &allhdr);
   if (e == cudaSuccess && nccl_ok(ncclAllGather(c.hdr, allhdr, 2, ncclInt32, comm, s))) {
     std::vector<int32_t> h(2 * G);
     e = cudaMemcpyAsync(h.data(), allhdr, 8 * (size_t)G, cudaMemcpyDeviceToHost, s);
@@ -557,7 +609,7 @@ cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* 
   // send buffers padded to the largest contribution (NCCL all-gather counts are uniform)
   int32_t* sendopens = nullptr;
   int2* sendpairs = nullptr;
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allopens, sizeof(int32_t) * (size_t)maxb * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) e = sc.get(sizeof(int32_t) * (size_t)maxb * (G + 1), &allopens);
   if (e == cudaSuccess && !*nccl_err) {
     sendopens = allopens + (size_t)maxb * G;
     if (hdrs[g].b > 0)
@@ -576,7 +628,7 @@ cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* 
       pre = combine(pre, hdrs[r]);
     }
   }
-  if (e == cudaSuccess && !*nccl_err) e = cudaMalloc(&allpairs, sizeof(int2) * (size_t)maxp * (G + 1));
+  if (e == cudaSuccess && !*nccl_err) e = sc.get(sizeof(int2) * (size_t)maxp * (G + 1), &allpairs);
   if (e == cudaSuccess && !*nccl_err) {
     sendpairs = allpairs + (size_t)maxp * G;
     e = cudaMemsetAsync(sendpairs, 0xff, sizeof(int2) * (size_t)maxp, s);
@@ -588,10 +640,6 @@ cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* 
   if (e == cudaSuccess && !*nccl_err) e = c.phase3(allpairs, maxp * G);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = e2;
-  cudaFree(allhdr);
-  cudaFree(allopens);
-  cudaFree(allpairs);
-  c.release();
   return e;
 }
 #endif

@@ -95,6 +95,7 @@ struct Params {
   int n_ext;
   ShardPop* pops;          // closes of nodes opened in an earlier chunk (for the exchange)
   uint32_t* npops;
+  int fs_list;             // shard phase 1: bbm_reduce lists the chunk's final-stack opens per tile in xc / xcnt
 };
 
 // True context of an open X of an earlier chunk (binary search in the
@@ -312,6 +313,27 @@ __global__ void __launch_bounds__(128) bbm_reduce(Params p) {
       S ^= low;
     }
   }
+  if (p.fs_list) {
+    // shard phase 1: the survivors closed after the chunk or never are the
+    // tile's part of the chunk's final stack (ascending; xc / xcnt are free
+    // until phase 2)
+    uint32_t fm = 0;
+    for (uint32_t q = sm; q; q &= q - 1) {
+      const int i = __ffs(q) - 1;
+      const int mm = __ldg(p.match + lbase + i);
+      if (mm < 0 || mm >= p.off + p.n) fm |= 1u << i;
+    }
+    const int c = __popc(fm);
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    int pos = x - c;
+    for (uint32_t q = fm; q; q &= q - 1) p.xc[base + pos++] = lane * RK + __ffs(q) - 1;
+    if (lane == 31) p.xcnt[T] = x;
+  }
   // lane aggregate of the slice clips, exclusive ∩-scan over lanes
   float4 agg = bINF();
   for (uint32_t q = sm & ~bmask; q; q &= q - 1) agg = isect(agg, __ldg(p.boxes + lbase + __ffs(q) - 1));
@@ -442,10 +464,12 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
   // global indices (compared with match / parent values)
   // (the last tile of a shard chunk ends at the chunk end: a partner beyond it
   // is in the next chunk, not in this tile or thread)
+  // (32-bit: global indices fit in int32, n <= 2^31 - 1; the ends are clamped
+  // to the chunk end, a no-op on one device)
   const int64_t gend = p.off + p.n;
-  const int64_t gbase = p.off + base, gtstart = p.off + tstart;
-  const int64_t gtend = SHARD ? min(gbase + TILE, gend) : gbase + TILE;
-  const int64_t gthr_end = SHARD ? min(gtstart + K, gend) : gtstart + K;
+  const int gbase = (int)(p.off + base), gtstart = (int)(p.off + tstart);
+  const int gtend = (int)min((int64_t)gbase + TILE, gend);
+  const int gthr_end = (int)min((int64_t)gtstart + K, gend);
   BBM_TRACE(T, 0);
 
   // ---- A. load -------------------------------------------------------------
@@ -867,55 +891,26 @@ __global__ void __launch_bounds__(256) bbm_patch_host(Params p, float4* hout, in
 // exported unions, fix-up of nodes that span chunks
 // ----------------------------------------------------------------------------
 // The chunk's final stack = its opens closed after the chunk or never (§3-§4,
-// P:96-138), ascending.  Counted per tile (one warp per tile), positioned by an
-// exclusive scan, written with the chunk-local cumulative clip lc ∩ TC_local.
-__device__ __forceinline__ uint32_t fs_mask(const Params& p, int64_t lbase) {
-  uint32_t m = 0;
-  for (int i = 0; i < 32; i++) {
-    const int64_t x = lbase + i;
-    if (x >= p.n) break;
-    const uint8_t t = p.tags[x];
-    if (t == 1 || t == 2) {
-      const int mm = __ldg(p.match + x);
-      if (mm < 0 || mm >= p.off + p.n) m |= 1u << i;
-    }
-  }
-  return m;
-}
-
-__global__ void __launch_bounds__(128) bbm_fs_count(Params p, int* cnt) {
-  const int lane = threadIdx.x & 31;
-  const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (T >= p.ntiles) return;
-  const uint32_t m = fs_mask(p, (int64_t)T * TILE + lane * 32);
-  const int c = __reduce_add_sync(0xffffffffu, __popc(m));
-  if (lane == 0) cnt[T] = c;
-}
-
+// P:96-138), ascending: listed per tile by bbm_reduce (xc / xcnt), positioned
+// by an exclusive scan of the counts, written with the chunk-local cumulative
+// clip lc ∩ TC_local (one warp per tile).
 __global__ void __launch_bounds__(128) bbm_fs_write(Params p, const int* offs, ShardOpen* fs, int* link_out) {
   const int lane = threadIdx.x & 31;
   const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (T >= p.ntiles) return;
-  const int64_t lbase = (int64_t)T * TILE + lane * 32;
-  uint32_t m = fs_mask(p, lbase);
-  int x = __popc(m);
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  int pos = offs[T] + x - __popc(m);
+  const int cnt = __ldg(p.xcnt + T);
+  if (cnt == 0) return;
+  const int64_t base = (int64_t)T * TILE;
+  const int o0 = __ldg(offs + T);
   const float4 tcT = __ldg(p.tc + T);
-  while (m) {
-    const int i = __ffs(m) - 1;
-    m &= m - 1;
+  for (int j = lane; j < cnt; j += 32) {
+    const int64_t x = base + __ldg(p.xc + base + j);
     ShardOpen r;
-    r.v = isect(__ldcg(p.out + lbase + i), tcT);  // lc ∩ TC_local
-    r.idx = (int)(p.off + lbase + i);
+    r.v = isect(__ldcg(p.out + x), tcT);  // lc ∩ TC_local
+    r.idx = (int)(p.off + x);
     r.pad0 = r.pad1 = r.pad2 = 0;
-    fs[pos] = r;
-    if (pos == 0) *link_out = __ldg(p.parent + lbase + i);  // the chunk's link (earlier chunk or root)
-    pos++;
+    fs[o0 + j] = r;
+    if (o0 + j == 0) *link_out = __ldg(p.parent + x);  // the chunk's link (earlier chunk or root)
   }
 }
 
@@ -1051,7 +1046,7 @@ struct Layout {
   size_t zero_off, zero_bytes;
   size_t off_nnever;
   size_t off_u[LV], off_link, off_tc, off_su, off_xc, off_xcnt, off_never, off_tcacc, off_tcptr, off_tcflag, bytes;
-  size_t off_fscnt, off_fsoff;
+  size_t off_fsoff;
   explicit Layout(int64_t n) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     ntiles = (n + TILE - 1) / TILE;
@@ -1067,7 +1062,6 @@ struct Layout {
     off_link = o; o = al(o + 4 * (size_t)ntiles);
     off_tc = o; o = al(o + 16 * (size_t)ntiles);
     off_xcnt = o; o = al(o + 4 * (size_t)ntiles);
-    off_fscnt = o; o = al(o + 4 * (size_t)ntiles);
     off_fsoff = o; o = al(o + 4 * (size_t)(ntiles + 1));
     off_tcacc = o; o = al(o + 32 * (size_t)ntiles);
     off_tcptr = o; o = al(o + 8 * (size_t)ntiles);
@@ -1134,6 +1128,7 @@ bbm::Params make_params(const uint8_t* tags, const float* leaf_bbox, const int32
   p.n_ext = sh ? sh->n_ext : 0;
   p.pops = sh ? sh->pops : nullptr;
   p.npops = sh ? sh->npops : nullptr;
+  p.fs_list = 0;
   return p;
 }
 
@@ -1242,7 +1237,6 @@ cudaError_t bbm_shard_phase1(const uint8_t* tags, const float* leaf_bbox, const 
                              int* link_dev, cudaStream_t stream) {
   bbm::Layout L(std::max<int64_t>(n, 1));
   char* b = (char*)ws;
-  int* cnt = (int*)(b + L.off_fscnt);
   int* offs = (int*)(b + L.off_fsoff);
   *b_dev = offs + L.ntiles;
   if (n <= 0) {
@@ -1252,6 +1246,7 @@ cudaError_t bbm_shard_phase1(const uint8_t* tags, const float* leaf_bbox, const 
   }
   BbmShard sh{off, nullptr, nullptr, 0, nullptr, nullptr};
   bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, &sh, nullptr);
+  p.fs_list = 1;
   cudaError_t err = cudaMemsetAsync((char*)ws + L.zero_off, 0, L.zero_bytes, stream);
   if (err == cudaSuccess) err = cudaMemcpyAsync(link_dev, &kMinus1, 4, cudaMemcpyHostToDevice, stream);
   if (err != cudaSuccess) return err;
@@ -1259,8 +1254,7 @@ cudaError_t bbm_shard_phase1(const uint8_t* tags, const float* leaf_bbox, const 
   TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<g4, 128, 0, stream>>>(p)));
   err = launch_tc(p, ws, stream);  // no imported contexts yet: chunk-local TC
   if (err != cudaSuccess) return err;
-  TB_LAUNCH(stream, "bbm_fs_count", (bbm::bbm_fs_count<<<g4, 128, 0, stream>>>(p, cnt)));
-  err = excl_scan_launch(cnt, (int)L.ntiles, offs, "bbm_scan_counts", stream);
+  err = excl_scan_launch(p.xcnt, (int)L.ntiles, offs, "bbm_scan_counts", stream);
   if (err != cudaSuccess) return err;
   TB_LAUNCH(stream, "bbm_fs_write", (bbm::bbm_fs_write<<<g4, 128, 0, stream>>>(p, offs, fs, link_dev)));
   return cudaGetLastError();

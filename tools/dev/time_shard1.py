@@ -1,0 +1,36 @@
+"""Dev: one step of the sharded path (NCCL world of one rank) against the
+unsharded step on the same 2^27 stream (CUDA events), to see the protocol's
+own overhead: extra passes, host syncs, exchange copies."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import torch, torch.distributed as dist
+import scenegen, paper_2205_11659_b200 as tb
+os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER_PORT", "29533")
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+n = 1 << int(sys.argv[1] if len(sys.argv) > 1 else 27)
+tags = scenegen.walk_tags(n, 4, device="cuda"); boxes = scenegen.boxes(n, 4, tags, device="cuda")
+m = torch.empty(n, dtype=torch.int32, device="cuda"); p = torch.empty_like(m); out = torch.empty_like(boxes)
+ctx = tb.ShardContext(1, 0, 0, n)
+def t(fn, k=10):
+    for _ in range(3): fn()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); a.record()
+    for _ in range(k): fn()
+    b.record(); torch.cuda.synchronize(); return a.elapsed_time(b) / k
+plain = t(lambda: (tb.paren_match(tags, m, p), tb.tree_bbox_matched(tags, boxes, m, p, out)))
+ref = out.clone()
+shard = t(lambda: (ctx.paren_match(tags, m, p), ctx.tree_bbox_matched(tags, boxes, m, p, out)))
+print(f"n=2^{n.bit_length()-1} plain {plain:.3f} ms  shard(world 1) {shard:.3f} ms  same={torch.equal(out.view(torch.int32), ref.view(torch.int32))}")
+import ctypes, json
+lib = tb.load()
+lib.tb_profile_read.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
+for name, fn in (("plain", lambda: (tb.paren_match(tags, m, p), tb.tree_bbox_matched(tags, boxes, m, p, out))),
+                 ("shard", lambda: (ctx.paren_match(tags, m, p), ctx.tree_bbox_matched(tags, boxes, m, p, out)))):
+    lib.tb_profile_enable(1); lib.tb_profile_read(None, 0)
+    for _ in range(5): fn()
+    torch.cuda.synchronize()
+    buf = ctypes.create_string_buffer(1 << 16); lib.tb_profile_read(buf, len(buf)); lib.tb_profile_enable(0)
+    pk = json.loads(buf.value.decode() or "{}")
+    tot = sum(v[1] for v in pk.values()) / 5
+    print(name, f"kernel sum {tot:.3f} ms/step", {k: round(v[1] / 5, 4) for k, v in sorted(pk.items(), key=lambda kv: -kv[1][1])})
+ctx.close(); dist.destroy_process_group()
