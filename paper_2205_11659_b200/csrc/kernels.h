@@ -40,6 +40,8 @@ size_t pm_ctrl_bytes(int64_t n);
 cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
                       const ShardInit* init, cudaStream_t stream);
 cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
+                             cudaStream_t stream, bool mark_unmatched = true);
+cudaError_t pm_rescan_launch(int64_t n, int32_t* match, void* ws, const ShardInit* init, bool mark_unmatched,
                              cudaStream_t stream);
 cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
                              const ShardInit* init, cudaStream_t stream);

@@ -440,8 +440,23 @@ static cudaError_t pm_configure() {
   return cudaSuccess;
 }
 
-cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
+// tile scan (heights from the prefix `init`) and never-closed opens; the
+// per-tile aggregates and slices of pm_reduce do not depend on `init`, so the
+// shard protocol's phase 2 reuses phase 1's
+cudaError_t pm_rescan_launch(int64_t n, int32_t* match, void* ws, const ShardInit* init, bool mark_unmatched,
                              cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
+  pm::Params p = pm_params(nullptr, n, match, nullptr, ws, init);
+  cudaError_t err = tile_scan_launch(p.ctrl, ntiles, p.init.a, p.init.b, stream);
+  if (err != cudaSuccess || !mark_unmatched) return err;
+  TB_LAUNCH(stream, "pm_unmatched",
+            (pm::pm_unmatched<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p, (int)ntiles)));
+  return cudaGetLastError();
+}
+
+cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
+                             cudaStream_t stream, bool mark_unmatched) {
   if (n <= 0) return cudaSuccess;
   const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
   pm::Params p = pm_params(tags, n, match, nullptr, ws, init);
@@ -449,11 +464,8 @@ cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, voi
   if (err != cudaSuccess) return err;
   TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p)));
   err = cudaGetLastError();
-  if (err == cudaSuccess) err = tile_scan_launch(p.ctrl, ntiles, p.init.a, p.init.b, stream);
   if (err != cudaSuccess) return err;
-  TB_LAUNCH(stream, "pm_unmatched",
-            (pm::pm_unmatched<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p, (int)ntiles)));
-  return cudaGetLastError();
+  return pm_rescan_launch(n, match, ws, init, mark_unmatched, stream);
 }
 
 cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
