@@ -352,29 +352,24 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
 
 // Chunk summary for sharding: the chunk's final stack (its unmatched opens,
 // bottom to top, global indices) = heights [0, b) of the stack after the last
-// tile, found by the owner rule from a virtual tile `ntiles`.
-__global__ void __launch_bounds__(NT) pm_summary(Params p, int ntiles, int32_t* hdr, int32_t* opens) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int2 t2 = __ldcg(p.ctrl.total);  // Bic value of the chunk (tile scan)
-  const Bic tot{t2.x, t2.y};
-  if (tid == 0) {
-    hdr[0] = tot.a;
-    hdr[1] = tot.b;
+// tile.  By the owner rule (F1) tile U's slice entries that survive to the end
+// are its bottom min(b_U, smin_U - L_U) ones, at heights L_U + k; the ranges of
+// different tiles are disjoint, so each tile copies its survivors into place
+// (one warp per tile, as pm_unmatched).
+__global__ void __launch_bounds__(256) pm_summary(Params p, int ntiles, int32_t* hdr, int32_t* opens) {
+  const int lane = threadIdx.x & 31;
+  const int U = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (U == 0 && lane == 0) {
+    const int2 t2 = __ldcg(p.ctrl.total);  // Bic value of the chunk (tile scan)
+    hdr[0] = t2.x;
+    hdr[1] = t2.y;
   }
-  int cur = tot.b - 1, from = ntiles;
-  while (cur >= 0) {
-    if (warp == 0) cur = find_runs(s, p.ctrl, cur, from, 0, 0);
-    __syncthreads();
-    const int nr = s.nruns;
-    for (int r = 0; r < nr; r++) {
-      const int U = s.runU[r], LU = s.runL[r], hlo = s.runLo[r], hhi = s.runHi[r];
-      for (int h = hlo + tid; h <= hhi; h += NT) opens[h] = __ldcg(p.slice + (int64_t)U * TILE + (h - LU));
-    }
-    cur = s.more;
-    __syncthreads();
-  }
+  if (U >= ntiles) return;
+  const int L = (int)__ldg(p.ctrl.lw + U) - 1;
+  const int bU = __ldg(p.ctrl.agg + U).y;
+  const int sm = __ldg(p.ctrl.smin + U);
+  const int surv = min(bU, max(sm == INT_MAX ? bU : sm - L, 0));
+  for (int k = lane; k < surv; k += 32) opens[L + k] = __ldcg(p.slice + (int64_t)U * TILE + k);
 }
 
 // Opens never closed (R4) get match = -1; every other open's match is written
@@ -432,8 +427,6 @@ static cudaError_t pm_configure() {
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(pm::pm_finish<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(pm::Smem));
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(pm::pm_summary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(pm::Smem));
 
     if (err != cudaSuccess) return err;
   }
@@ -490,7 +483,7 @@ cudaError_t pm_summary_launch(const uint8_t* tags, int64_t n, void* ws, int32_t*
   if (ntiles == 0) return cudaMemsetAsync(hdr, 0, 8, stream);
   pm::Params p = pm_params(tags, n, nullptr, nullptr, ws, nullptr);
   TB_LAUNCH(stream, "pm_summary",
-            (pm::pm_summary<<<1, pm::NT, sizeof(pm::Smem), stream>>>(p, (int)ntiles, hdr, opens)));
+            (pm::pm_summary<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p, (int)ntiles, hdr, opens)));
   return cudaGetLastError();
 }
 
