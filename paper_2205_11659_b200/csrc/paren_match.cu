@@ -250,12 +250,14 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
     __syncthreads();
   }
 
-  // entries of the stack at this thread's start that it pops (depths 0..a_t),
-  // kept as references: >= 0 in-tile element, < 0 incoming depth -ref-1
+  // entries of the stack at this thread's start that it pops (depths 0..a_t):
+  // one device, their global indices (-1: root); shard mode, references
+  // (>= 0 in-tile element, < 0 incoming depth -ref-1) resolved where used
+  const int gbase0 = (int)(p.offset + base);
   {
     int ref = top_ref;
     for (int d = 0; d <= a_t; d++) {
-      s.extv[d][tid] = ref;
+      s.extv[d][tid] = SHARD ? ref : (ref >= 0 ? gbase0 + ref : s.inc[-ref - 1]);
       if (ref >= 0) {
         const int V = ref >> 4;
         const uint32_t below = s.uo[V] & ((1u << (ref & 15)) - 1u);
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
   int dcur = 0;
   int ref = s.extv[0][tid];
   bool vinit;
-  int val = resolve(ref, vinit);
+  int val = SHARD ? resolve(ref, vinit) : ref;
 #pragma unroll
   for (int q = 0; q < K / 4; q++) {
     int pv[4], mv[4];
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
       dcur += uc;
       if (uc) {
         ref = s.extv[dcur][tid];
-        val = resolve(ref, vinit);
+        val = SHARD ? resolve(ref, vinit) : ref;
       }
       mv[j] = m;
     }
@@ -335,8 +337,8 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
       const int i = __ffs(q) - 1;
       q &= q - 1;
       const int r = s.extv[d][tid];
-      bool from_init;
-      const int v = resolve(r, from_init);
+      bool from_init = false;
+      const int v = SHARD ? resolve(r, from_init) : r;
       if (v >= 0) {
         if (!SHARD || !from_init) {
           p.match[v - p.offset] = tb32 + i;
