@@ -783,15 +783,17 @@ __global__ void __launch_bounds__(256) bbm_hier(Params p, int k, int m /* nodes 
 // bbm_close: closes of nodes opened in an earlier tile (one CTA per tile):
 // union = prefix of the close's tile (stored by bbm_main) ∪ the open's tile
 // suffix after it ∪ the whole tiles in between (F4); blend opens get it too.
-// Lanes sharing the open's tile share one warp-cooperative range union.
+// Lanes sharing the open's tile share one warp-cooperative range union.  One
+// warp per tile (a tile lists ~17 closes on C5), 32 closes at a time.
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) bbm_close(Params p) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int T = p.t0 + blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int T = p.t0 + blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (T >= p.t1) return;
   const int cnt = __ldg(p.xcnt + T);
   int cto = INT_MIN;  // warp cache: the last range resolved (deep chains repeat one open tile); To = -1 is a key
   float4 cR = bEMPTY();
-  for (int j0 = warp * 32; j0 < cnt; j0 += 128) {
+  for (int j0 = 0; j0 < cnt; j0 += 32) {
     const int j = j0 + lane;
     const bool valid = j < cnt;
     int c = 0, o = 0, To = 0;
@@ -1166,7 +1168,7 @@ cudaError_t launch_range(const bbm::Params& p, cudaStream_t stream) {
       m = (m + 31) / 32;
     }
   }
-  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<nt, 128, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_close", (bbm::bbm_close<<<(nt + 3) / 4, 128, 0, stream>>>(p)));
   return cudaGetLastError();
 }
 
