@@ -284,3 +284,26 @@ def test_pipeline_host_api_pageable():
     ref = oracle.tree_bbox(t.numpy(), b.numpy())
     assert np.array_equal(m.numpy(), oracle.paren_match(t.numpy())[0])
     assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [1, 7, 1023, 1024, 1025, 4097, 33_000])
+def test_pipeline_host_api_ragged(n):
+    """Chunked host path at the smallest chunk size on ragged sizes (one
+    element, under one tile, exactly one tile, one tile + 1, many chunks);
+    pageable inputs with a pinned result."""
+    tb = gpu()
+    lib = tb.load()
+    old = lib.tb_debug_host_chunk_shift(10)
+    try:
+        t = scenegen.walk_tags(n, 90 + n % 7)
+        b = scenegen.boxes(n, 91, t)
+        m = torch.empty(n, dtype=torch.int32)
+        p = torch.empty_like(m)
+        out = torch.full((n, 4), float("nan")).pin_memory()
+        tb.paren_match_tree_bbox_host(t, b, m, p, out)
+        m_ref, p_ref = oracle.paren_match(t.numpy())
+        ref = oracle.tree_bbox(t.numpy(), b.numpy())
+        assert np.array_equal(m.numpy(), m_ref) and np.array_equal(p.numpy(), p_ref)
+        assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
+    finally:
+        lib.tb_debug_host_chunk_shift(old)
