@@ -15,8 +15,9 @@
 //             coalesced in and out): each thread composes its elements relative
 //             to its external ancestor X; thread links by pointer jumping; every
 //             element's world = ctx(X) ∘ rel in place — the only slots other
-//             threads read (thread-unmatched opens) are finished after a barrier.
-// tt_closes   a close takes its open's world.
+//             threads read (thread-unmatched opens) are finished after a barrier;
+//             then each close takes its open's world (in the tile: its slot;
+//             in an earlier tile: TC ∘ lc of that slice entry).
 #include <algorithm>
 #include <climits>
 #include <cooperative_groups.h>
@@ -83,14 +84,23 @@ __global__ void __launch_bounds__(128) tt_reduce(Params p) {
   const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (T >= p.ntiles) return;
   const int64_t base = (int64_t)T * TILE, lbase = base + (int64_t)lane * RK, tend = base + TILE;
-  uint32_t sm = 0;
-  for (int i = 0; i < RK; i++) {
-    const int64_t g = lbase + i;
-    if (g >= p.n) break;
-    if (is_open(p.tags[g])) {
-      const int m = __ldg(p.match + g);
-      if (m < 0 || m >= tend) sm |= 1u << i;
-    }
+  uint32_t om = 0;  // the lane's opens (tags as two 16-byte loads)
+  if (lbase + RK <= p.n) {
+    const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase));
+    const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase) + 1);
+    const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+      om |= byte_mask4(__vcmpeq4(tw[q], 0x01010101u) | __vcmpeq4(tw[q], 0x02020202u)) << (4 * q);
+  } else {
+    for (int i = 0; i < RK && lbase + i < p.n; i++)
+      if (is_open(p.tags[lbase + i])) om |= 1u << i;
+  }
+  uint32_t sm = 0;  // opens closed beyond the tile or never
+  for (uint32_t q = om; q; q &= q - 1) {
+    const int i = __ffs(q) - 1;
+    const int m = __ldg(p.match + lbase + i);
+    if (m < 0 || m >= tend) sm |= 1u << i;
   }
   Xf agg = xf_id();
   for (uint32_t q = sm; q; q &= q - 1) agg = compose(agg, load_xf(p.local, lbase + __ffs(q) - 1));
@@ -205,13 +215,25 @@ __global__ void __launch_bounds__(NT) tt_main(Params p) {
   }
   uint8_t tg[K];
   int pr[K], mt[K];
+  if (tstart + K <= p.n) {  // 8 tags, 8 parents, 8 matches as vectors (16-byte aligned)
+    const uint2 t8 = __ldg(reinterpret_cast<const uint2*>(p.tags + tstart));
+    const int4 p0 = __ldg(reinterpret_cast<const int4*>(p.parent + tstart));
+    const int4 p1 = __ldg(reinterpret_cast<const int4*>(p.parent + tstart) + 1);
+    const int4 m0 = __ldg(reinterpret_cast<const int4*>(p.match + tstart));
+    const int4 m1 = __ldg(reinterpret_cast<const int4*>(p.match + tstart) + 1);
 #pragma unroll
-  for (int i = 0; i < K; i++) {
-    const int64_t g = tstart + i;
-    const bool ok = g < p.n;
-    tg[i] = ok ? p.tags[g] : 0;
-    pr[i] = ok ? __ldg(p.parent + g) : -1;
-    mt[i] = ok ? __ldg(p.match + g) : -1;
+    for (int i = 0; i < K; i++) tg[i] = (uint8_t)(((i < 4 ? t8.x : t8.y) >> (8 * (i & 3))) & 0xffu);
+    pr[0] = p0.x; pr[1] = p0.y; pr[2] = p0.z; pr[3] = p0.w; pr[4] = p1.x; pr[5] = p1.y; pr[6] = p1.z; pr[7] = p1.w;
+    mt[0] = m0.x; mt[1] = m0.y; mt[2] = m0.z; mt[3] = m0.w; mt[4] = m1.x; mt[5] = m1.y; mt[6] = m1.z; mt[7] = m1.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      const int64_t g = tstart + i;
+      const bool ok = g < p.n;
+      tg[i] = ok ? p.tags[g] : 0;
+      pr[i] = ok ? __ldg(p.parent + g) : -1;
+      mt[i] = ok ? __ldg(p.match + g) : -1;
+    }
   }
   uint32_t valid = 0, thr_un = 0, pend = 0;
 #pragma unroll
@@ -302,7 +324,27 @@ __global__ void __launch_bounds__(NT) tt_main(Params p) {
     }
   }
   __syncthreads();
-  // coalesced copy-out (closes are filled by tt_closes)
+  // closes take their open's world (R15; unmatched: I): an open of this tile
+  // from its (final) slot, an open of an earlier tile -- a slice entry there --
+  // as TC ∘ lc
+  {
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      if (((valid >> i) & 1u) && tg[i] == 3) {
+        const int o = mt[i];
+        Xf w = xf_id();
+        if (o >= base) {
+          const int x = o - (int)base;
+          w = sget(s, sidx(x >> 3, x & 7));
+        } else if (o >= 0) {
+          w = outer_ctx(p, o);
+        }
+        sput(s, sidx(tid, i), w);
+      }
+    }
+  }
+  __syncthreads();
+  // coalesced copy-out
   {
     float* dst = p.out + 6 * base;
     const int nf = 6 * nvalid;
@@ -321,14 +363,6 @@ __global__ void __launch_bounds__(NT) tt_main(Params p) {
           if (4 * f4 + k < nf) dst[4 * f4 + k] = w[k];
       }
     }
-  }
-}
-
-__global__ void __launch_bounds__(256) tt_closes(Params p) {
-  for (int64_t i = blockIdx.x * (int64_t)256 + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * 256) {
-    if (p.tags[i] != 3) continue;
-    const int o = __ldg(p.match + i);
-    store_xf(p.out, i, o >= 0 ? load_xf(p.out, o) : xf_id());
   }
 }
 
@@ -393,7 +427,6 @@ cudaError_t tt_launch(const uint8_t* tags, const float* local, const int32_t* ma
   if (once_per_device(2))
     cudaFuncSetAttribute(tt::tt_main, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(tt::Smem));
   TB_LAUNCH(stream, "tt_main", (tt::tt_main<<<(unsigned)L.ntiles, tt::NT, sizeof(tt::Smem), stream>>>(p)));
-  TB_LAUNCH(stream, "tt_closes", (tt::tt_closes<<<148 * 8, 256, 0, stream>>>(p)));
   return cudaGetLastError();
 }
 
