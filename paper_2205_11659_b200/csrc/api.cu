@@ -487,7 +487,7 @@ int bin_leaves(const uint8_t* d_tags, const float* d_node_bbox, int64_t n, int g
     return fail(TB_ERR_ARG, "null pointer");
   if (n > 0 && !aligned16(d_node_bbox)) return fail(TB_ERR_ALIGN, "node_bbox must be 16-byte aligned");
   void* ws = nullptr;
-  r = get_ws(stream, 9, sizeof(int32_t) * (size_t)grid_w * grid_h, &ws);
+  r = get_ws(stream, 9, tb::bins_workspace_bytes(grid_w * grid_h), &ws);
   if (r) return r;
   cudaError_t e = tb::bins_launch(d_tags, d_node_bbox, n, grid_w, grid_h, bin_size, d_counts, d_offsets,
                                   (int32_t*)ws, d_items, capacity, h_total, (cudaStream_t)stream);
@@ -517,6 +517,10 @@ int compact_scene(const uint8_t* d_tags, const float* d_boxes, int64_t n, const 
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }
+
+/* Debug: capacity of bin_leaves' list of binned leaves (returns the previous
+ * one); tests lower it to reach the streaming fill. */
+int64_t tb_debug_bins_cap(int64_t cap) { return tb::bins_debug_cap(cap); }
 
 /* Debug: minimum chunk size (log2 elements) of the pipelined host path;
  * returns the previous value (tests use small chunks on small inputs). */

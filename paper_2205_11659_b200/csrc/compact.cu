@@ -53,6 +53,10 @@ __global__ void __launch_bounds__(NT) count_k(const uint8_t* tags, int64_t n, Ke
 }
 
 
+// Warp-cooperative scatter: each warp owns 512 contiguous elements, counted
+// first (16 per lane), then walked in 16 rounds of 32 consecutive elements --
+// one per lane, a ballot gives each kept element its output slot -- so reads
+// and the compacted writes are both contiguous across the warp.
 __global__ void __launch_bounds__(NT) scatter_k(const uint8_t* tags, const float4* boxes, int64_t n, KeepMap kmv,
                                                 const int* offs, uint8_t* tags_out, float4* boxes_out,
                                                 int32_t* index_out) {
@@ -61,25 +65,27 @@ __global__ void __launch_bounds__(NT) scatter_k(const uint8_t* tags, const float
   km[threadIdx.x] = kmv.m[threadIdx.x];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t g = (int64_t)blockIdx.x * BLK + (int64_t)threadIdx.x * K;
-  const uint32_t f = kept16(tags, n, g, km);
-  const int c = __popc(f);
-  int x = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) ws[warp] = x;
+  const int64_t w0 = (int64_t)blockIdx.x * BLK + (int64_t)warp * (32 * K);
+  const uint32_t f = kept16(tags, n, w0 + lane * K, km);
+  const int c = __reduce_add_sync(0xffffffffu, __popc(f));
+  if (lane == 0) ws[warp] = c;
   __syncthreads();
-  int pos = offs[blockIdx.x] + x - c;
+  int pos = offs[blockIdx.x];
   for (int w = 0; w < warp; w++) pos += ws[w];
-  for (uint32_t q = f; q; q &= q - 1) {
-    const int64_t e = g + __ffs(q) - 1;
-    tags_out[pos] = tags[e];
-    if (boxes) boxes_out[pos] = __ldg(boxes + e);
-    index_out[pos] = (int32_t)e;
-    pos++;
+#pragma unroll 4
+  for (int r = 0; r < K; r++) {
+    const int64_t e = w0 + r * 32 + lane;
+    // element e is bit (lane & 15) of lane 2r + lane / 16's kept mask
+    const uint32_t fl = __shfl_sync(0xffffffffu, f, 2 * r + (lane >> 4));
+    const bool k = (fl >> (lane & 15)) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, k);
+    if (k) {
+      const int at = pos + __popc(bal & ((1u << lane) - 1u));
+      tags_out[at] = tags[e];
+      if (boxes) boxes_out[at] = __ldg(boxes + e);
+      index_out[at] = (int32_t)e;
+    }
+    pos += __popc(bal);
   }
 }
 

@@ -119,6 +119,8 @@ cudaError_t tt_launch(const uint8_t* tags, const float* local, const int32_t* ma
                       int64_t n, float* world, void* ws, cudaStream_t stream);
 
 // culling + binning of clipped leaf boxes (bins.cu); synchronises to read the total
+size_t bins_workspace_bytes(int nb);
+int64_t bins_debug_cap(int64_t cap);
 cudaError_t bins_launch(const uint8_t* tags, const float* node_bbox, int64_t n, int gw, int gh, float bs,
                         int32_t* counts, int32_t* offsets, int32_t* cursor, int32_t* items, int64_t capacity,
                         int64_t* total, cudaStream_t stream);

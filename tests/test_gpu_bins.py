@@ -24,6 +24,7 @@ def check(tags, boxes, gw, gh, bs):
     for k in range(gw * gh):
         seg = np.sort(it[o[k]:o[k + 1]])
         assert np.array_equal(seg, it_ref[o_ref[k]:o_ref[k + 1]]), k
+    return len(it)
 
 
 @pytest.mark.parametrize("n,gw,gh,bs", [(1, 4, 4, 64.0), (5000, 7, 5, 700.0), (300_001, 16, 16, 256.0),
@@ -41,3 +42,21 @@ def test_special_boxes():
                           [10, 10, 5, 20], [-100, -100, -1, -1], [500, 500, 600, 600], [0, 0, 0, 10],
                           [1e30, 0, inf, 1]], dtype=torch.float32)
     check(tags, boxes, 4, 4, 64.0)
+
+
+def test_grid_over_shared_histogram():
+    """More bins than the per-CTA shared histogram holds (global-atomic counts)."""
+    tags = scenegen.walk_tags(200_003, 3, p_leaf=0.6)
+    check(tags, scenegen.boxes(200_003, 2, tags), 100, 60, 50.0)
+
+
+def test_streaming_fill_fallback():
+    """The list of binned leaves overflowing its capacity: the streaming fill."""
+    import paper_2205_11659_b200 as tb
+    lib = tb.load()
+    old = lib.tb_debug_bins_cap(16)
+    try:
+        tags = scenegen.walk_tags(300_001, 4, p_leaf=0.6)
+        assert check(tags, scenegen.boxes(300_001, 3, tags), 16, 16, 256.0) > 16  # the list overflowed
+    finally:
+        lib.tb_debug_bins_cap(old)
