@@ -307,3 +307,20 @@ def test_pipeline_host_api_ragged(n):
         assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
     finally:
         lib.tb_debug_host_chunk_shift(old)
+
+
+def test_pipeline_host_api_c5_bench_size():
+    """The e2e call bench.py times (C5, 2^27, pinned buffers, the default 16
+    chunks) bit-exact against the oracle on the whole stream."""
+    tb = gpu()
+    t = scenegen.walk_tags(1 << 27, 4)
+    b = scenegen.boxes(t.numel(), 4, t)
+    tp, bp = t.pin_memory(), b.pin_memory()
+    m = torch.empty(t.numel(), dtype=torch.int32).pin_memory()
+    p = torch.empty_like(m).pin_memory()
+    out = torch.empty_like(bp).pin_memory()
+    tb.paren_match_tree_bbox_host(tp, bp, m, p, out)
+    m_ref, p_ref = oracle.paren_match(t.numpy())
+    assert np.array_equal(m.numpy(), m_ref) and np.array_equal(p.numpy(), p_ref)
+    ref = oracle.tree_bbox(t.numpy(), b.numpy())
+    assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
