@@ -8,8 +8,10 @@ Workload (BASELINE.json metric "G elements/s for paren_match+tree_bbox"): the
 paper's random push/pop stream (configs[4], "random-depth stream"),
 synthetic, 2^27 elements per GPU (weak scaling; N = 8 is the 1B-element
 stream), 50 % leaves, 75 % of opens are clips, unbalanced tail kept.  One
-step = paren_match, then tree_bbox_matched on its match/parent outputs (the
-boxes computed from that matching), over the resident stream.  Inputs (2.2 GB
+step = paren_match_tree_bbox over the resident stream: match / parent (as
+paren_match) and node_bbox (as tree_bbox_matched on them) in one device call,
+the box reduce pass overlapped with paren_match; N > 1: the sharded
+paren_match then tree_bbox_matched.  Inputs (2.2 GB
 per GPU) exceed the 126 MB L2, so no flush between steps.
 
 Printed (rank 0, one JSON line): value = elements x steps / max-over-ranks
@@ -222,8 +224,7 @@ def main():
 
     def step():
         if shard is None:
-            tb.paren_match(tags, match, parent)
-            tb.tree_bbox_matched(tags, boxes, match, parent, out)
+            tb.paren_match_tree_bbox(tags, boxes, match, parent, out)
         else:
             shard.paren_match(tags, match, parent)
             shard.tree_bbox_matched(tags, boxes, match, parent, out)

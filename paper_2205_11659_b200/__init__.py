@@ -60,6 +60,7 @@ def load():
                 "bin_leaves": ([P, P, I64, ctypes.c_int, ctypes.c_int, ctypes.c_float, P, P, P, I64, P, P],
                                ctypes.c_int),
                 "tree_bbox_matched_ws": ([P, P, P, P, I64, P, P, SZ, P], ctypes.c_int),
+                "paren_match_tree_bbox": ([P, P, I64, P, P, P, P], ctypes.c_int),
                 "tree_bbox_matched_workspace_bytes": ([I64], SZ),
                 "tb_count_unmatched": ([P, I64, P, P, P], ctypes.c_int),
                 "tb_get_unique_id": ([P], ctypes.c_int),
@@ -184,6 +185,29 @@ def tree_bbox_matched(tags: torch.Tensor, leaf_bbox: torch.Tensor, match: torch.
         _check(lib.tree_bbox_matched(tags.data_ptr(), leaf_bbox.data_ptr(), match.data_ptr(), parent.data_ptr(), n,
                                      node_bbox.data_ptr(), _stream(tags.device)))
     return node_bbox
+
+
+def paren_match_tree_bbox(tags: torch.Tensor, leaf_bbox: torch.Tensor, match: torch.Tensor | None = None,
+                          parent: torch.Tensor | None = None, node_bbox: torch.Tensor | None = None):
+    """The whole hot path in one device call: (match, parent, node_bbox), the
+    box reduce pass overlapped with paren_match inside the library."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    _need_cuda(leaf_bbox, "leaf_bbox", torch.float32)
+    n = tags.numel()
+    if leaf_bbox.numel() != 4 * n:
+        raise ValueError("leaf_bbox must be [n, 4]")
+    dev = tags.device
+    match = torch.empty(n, dtype=torch.int32, device=dev) if match is None else match
+    parent = torch.empty(n, dtype=torch.int32, device=dev) if parent is None else parent
+    node_bbox = torch.empty((n, 4), dtype=torch.float32, device=dev) if node_bbox is None else node_bbox
+    _need_cuda(match, "match", torch.int32)
+    _need_cuda(parent, "parent", torch.int32)
+    _need_cuda(node_bbox, "node_bbox", torch.float32)
+    with torch.cuda.device(dev):
+        _check(lib.paren_match_tree_bbox(tags.data_ptr(), leaf_bbox.data_ptr(), n, match.data_ptr(),
+                                         parent.data_ptr(), node_bbox.data_ptr(), _stream(dev)))
+    return match, parent, node_bbox
 
 
 def tree_transform(tags: torch.Tensor, local: torch.Tensor, match: torch.Tensor, parent: torch.Tensor,

@@ -88,6 +88,8 @@ struct AuxStreams {
   cudaStream_t in = nullptr, out = nullptr;
   cudaEvent_t start = nullptr, in_done = nullptr, pm_done = nullptr, out_done = nullptr;
   cudaEvent_t chunk_in[kMaxChunks] = {}, chunk_done[kMaxChunks] = {};
+  cudaStream_t side = nullptr;  // paren_match_tree_bbox: the box reduce pass beside paren_match
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 std::map<int, AuxStreams> g_aux;
 
@@ -104,6 +106,9 @@ int get_aux(AuxStreams** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.in_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.pm_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.out_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a.side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming);
     for (int c = 0; c < kMaxChunks && e == cudaSuccess; c++) {
       e = cudaEventCreateWithFlags(&a.chunk_in[c], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.chunk_done[c], cudaEventDisableTiming);
@@ -291,6 +296,43 @@ int tree_bbox_matched(const uint8_t* d_tags, const float* d_leaf_bbox, const int
   r = get_ws(stream, 5, need, &ws);
   if (r) return r;
   return tree_bbox_matched_ws(d_tags, d_leaf_bbox, d_match, d_parent, n, d_node_bbox, ws, need, stream);
+}
+
+int paren_match_tree_bbox(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, int32_t* d_match,
+                          int32_t* d_parent, float* d_node_bbox, void* stream) {
+  g_err[0] = 0;
+  int r = pm_checks(d_tags, n, d_match, d_parent);
+  if (r || n == 0) return r;
+  r = bbm_checks(d_tags, d_leaf_bbox, d_match, d_parent, n, d_node_bbox);
+  if (r) return r;
+  const size_t nb = (size_t)n * 16, n4 = (size_t)n * 4;
+  if (overlap(d_match, n4, d_leaf_bbox, nb) || overlap(d_parent, n4, d_leaf_bbox, nb))
+    return fail(TB_ERR_ALIAS, "match / parent overlap leaf_bbox");
+  void* pmws = nullptr;
+  void* bws = nullptr;
+  r = get_ws(stream, 0, tb::pm_workspace_bytes(n), &pmws);
+  if (r) return r;
+  r = get_ws(stream, 5, tb::bbm_workspace_bytes(n), &bws);
+  if (r) return r;
+  AuxStreams* ax = nullptr;
+  r = get_aux(&ax);
+  if (r) return r;
+  // The box path's reduce pass reads only tags and boxes: it runs on a side
+  // stream beside paren_match's tile scan (one CTA) and finish pass, forked
+  // after paren_match's reduce pass and joined before the passes that need
+  // match / parent.
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = tb::pm_reduce_only_launch(d_tags, n, d_match, pmws, nullptr, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ax->fork, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->side, ax->fork, 0);
+  if (e == cudaSuccess) e = tb::bbm_launch_reduce(d_tags, d_leaf_bbox, n, d_node_bbox, bws, ax->side);
+  if (e == cudaSuccess) e = cudaEventRecord(ax->join, ax->side);
+  if (e == cudaSuccess) e = tb::pm_rescan_launch(n, d_match, pmws, nullptr, true, s);
+  if (e == cudaSuccess) e = tb::pm_finish_launch(d_tags, n, d_match, d_parent, pmws, nullptr, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ax->join, 0);
+  if (e == cudaSuccess) e = tb::bbm_launch_rest(d_tags, d_leaf_bbox, d_match, d_parent, n, d_node_bbox, bws, s);
+  if (e != cudaSuccess) return cuda_fail(e, "paren_match_tree_bbox launch");
+  return TB_OK;
 }
 
 int tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, int64_t n, float* h_node_bbox,

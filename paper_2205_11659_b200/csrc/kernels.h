@@ -41,6 +41,8 @@ cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* p
                       const ShardInit* init, cudaStream_t stream);
 cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
                              cudaStream_t stream, bool mark_unmatched = true);
+cudaError_t pm_reduce_only_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
+                                  cudaStream_t stream);
 cudaError_t pm_rescan_launch(int64_t n, int32_t* match, void* ws, const ShardInit* init, bool mark_unmatched,
                              cudaStream_t stream);
 cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
@@ -68,6 +70,12 @@ size_t bbm_workspace_bytes(int64_t n);
 int bbm_tile_elems();
 cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
                        int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace = nullptr);
+// bbm_launch in two parts: the reduce pass reads only tags and boxes (it can
+// run while paren_match computes match / parent), the rest needs both.
+cudaError_t bbm_launch_reduce(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
+                              cudaStream_t stream);
+cudaError_t bbm_launch_rest(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                            int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace = nullptr);
 // The same passes split over tile ranges in order (chunked host pipeline):
 // bbm_begin once, bbm_tiles_launch for [t0, t1) as each range's boxes arrive
 // (every pass reads only its own and earlier tiles), bbm_end (never-closed

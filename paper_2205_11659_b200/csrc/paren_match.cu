@@ -450,15 +450,20 @@ cudaError_t pm_rescan_launch(int64_t n, int32_t* match, void* ws, const ShardIni
   return cudaGetLastError();
 }
 
-cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
-                             cudaStream_t stream, bool mark_unmatched) {
+cudaError_t pm_reduce_only_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
+                                  cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
   pm::Params p = pm_params(tags, n, match, nullptr, ws, init);
   cudaError_t err = pm_configure();
   if (err != cudaSuccess) return err;
   TB_LAUNCH(stream, "pm_reduce", (pm::pm_reduce<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p)));
-  err = cudaGetLastError();
+  return cudaGetLastError();
+}
+
+cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
+                             cudaStream_t stream, bool mark_unmatched) {
+  cudaError_t err = pm_reduce_only_launch(tags, n, match, ws, init, stream);
   if (err != cudaSuccess) return err;
   return pm_rescan_launch(n, match, ws, init, mark_unmatched, stream);
 }

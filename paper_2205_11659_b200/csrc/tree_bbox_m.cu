@@ -79,7 +79,7 @@ struct Params {
   int ntiles;
   int t0, t1;            // tiles of this launch: [t0, t1) (chunked pipeline; else [0, ntiles))
   float4* u[LV];         // u[0][T] = union of tile T's clipped leaves; u[k] over 32^k tiles
-  int32_t* link;         // [ntiles] parent of the tile's bottom slice entry (-1: root / none)
+  int32_t* link;         // [ntiles] the tile's bottom slice entry (tile-local, -1: none); its parent is the link
   float4* tc;            // [ntiles] ctx(link)
   float4* su;            // [n] union of the tile's clipped leaves after each slice entry
   int32_t* xc;           // [ntiles][TILE] closes of nodes opened in an earlier tile
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(128) bbm_reduce(Params p) {
     p.out[lbase + i] = acc;
   }
   const int first = __reduce_min_sync(0xffffffffu, sm ? (lane * RK + __ffs(sm) - 1) : INT_MAX);
-  if (lane == 0) p.link[T] = (first == INT_MAX) ? -1 : __ldg(p.parent + base + first);
+  if (lane == 0) p.link[T] = (first == INT_MAX) ? -1 : first;  // bbm_tc takes its parent (tags + boxes only here)
 }
 
 // ----------------------------------------------------------------------------
@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
   float4* acc[2] = {acc2, acc2 + nt};
   int* ptr[2] = {ptr2, ptr2 + nt};
   for (int V = t0 + gt; V < t1; V += nthr) {
-    const int X = __ldg(p.link + V);  // global index
+    const int f = __ldg(p.link + V);  // the tile's first slice entry (local), -1: none
+    const int X = f >= 0 ? __ldg(p.parent + (int64_t)V * TILE + f) : -1;  // its parent: global index
     // lc(X), written by bbm_reduce (or X's context: F6); an open of an earlier
     // chunk: imported context
     float4 a = bINF();
@@ -1182,17 +1183,31 @@ cudaError_t launch_rest(const bbm::Params& p, cudaStream_t stream) {
 
 }  // namespace
 
-cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
-                       int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace) {
+cudaError_t bbm_launch_reduce(const uint8_t* tags, const float* leaf_bbox, int64_t n, float* node_bbox, void* ws,
+                              cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   bbm::Layout L(n);
-  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, nullptr, trace);
+  bbm::Params p = make_params(tags, leaf_bbox, nullptr, nullptr, n, node_bbox, ws, nullptr, nullptr);
   cudaError_t err = cudaMemsetAsync((char*)ws + L.zero_off, 0, L.zero_bytes, stream);
   if (err != cudaSuccess) return err;
   TB_LAUNCH(stream, "bbm_reduce", (bbm::bbm_reduce<<<(unsigned)((L.ntiles + 3) / 4), 128, 0, stream>>>(p)));
-  err = launch_tc(p, ws, stream);
+  return cudaGetLastError();
+}
+
+cudaError_t bbm_launch_rest(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                            int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace) {
+  if (n <= 0) return cudaSuccess;
+  bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, nullptr, trace);
+  cudaError_t err = launch_tc(p, ws, stream);
   if (err != cudaSuccess) return err;
   return launch_rest(p, stream);
+}
+
+cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,
+                       int64_t n, float* node_bbox, void* ws, cudaStream_t stream, uint64_t* trace) {
+  cudaError_t err = bbm_launch_reduce(tags, leaf_bbox, n, node_bbox, ws, stream);
+  if (err != cudaSuccess) return err;
+  return bbm_launch_rest(tags, leaf_bbox, match, parent, n, node_bbox, ws, stream, trace);
 }
 
 int bbm_tiles(int64_t n) { return (int)((n + bbm::TILE - 1) / bbm::TILE); }

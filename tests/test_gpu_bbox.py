@@ -324,3 +324,18 @@ def test_pipeline_host_api_c5_bench_size():
     assert np.array_equal(m.numpy(), m_ref) and np.array_equal(p.numpy(), p_ref)
     ref = oracle.tree_bbox(t.numpy(), b.numpy())
     assert np.array_equal(out.numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3L", "C5"])
+def test_fused_device_call(cfg):
+    """paren_match_tree_bbox (the bench step: box reduce pass beside
+    paren_match on a side stream) equals the oracle on every output."""
+    tb = gpu()
+    t = scenegen.config(cfg)[0]
+    b = scenegen.boxes(t.numel(), 13, t)
+    m, p, out = tb.paren_match_tree_bbox(t.cuda(), b.cuda())
+    torch.cuda.synchronize()
+    m_ref, p_ref = oracle.paren_match(t.numpy())
+    assert np.array_equal(m.cpu().numpy(), m_ref) and np.array_equal(p.cpu().numpy(), p_ref)
+    ref = oracle.tree_bbox(t.numpy(), b.numpy())
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))

@@ -79,3 +79,32 @@ def test_error_codes_new_entry_points():
     # n == 0 is a successful no-op everywhere
     assert L.tree_bbox_matched(0, 0, 0, 0, 0, 0, 0) == 0
     assert L.tree_transform(0, 0, 0, 0, 0, 0, 0) == 0
+
+
+def test_graph_capture_fused_call():
+    """paren_match_tree_bbox forks a side stream and joins it back: capturable
+    (after one warm-up call on the same stream sized its workspace)."""
+    import paper_2205_11659_b200 as tb
+    n = 250_003
+    tags = scenegen.walk_tags(n, 23, p_leaf=0.5)
+    boxes = scenegen.boxes(n, 23, tags)
+    t, b = tags.cuda(), boxes.cuda()
+    m = torch.empty(n, dtype=torch.int32, device="cuda")
+    p = torch.empty_like(m)
+    out = torch.empty_like(b)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        tb.paren_match_tree_bbox(t, b, m, p, out)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        tb.paren_match_tree_bbox(t, b, m, p, out)
+    m.fill_(7)
+    p.fill_(7)
+    out.fill_(7)
+    g.replay()
+    torch.cuda.synchronize()
+    m_ref, p_ref = oracle.paren_match(tags.numpy())
+    ref = oracle.tree_bbox(tags.numpy(), boxes.numpy())
+    assert np.array_equal(m.cpu().numpy(), m_ref) and np.array_equal(p.cpu().numpy(), p_ref)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
