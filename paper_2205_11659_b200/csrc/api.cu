@@ -92,6 +92,9 @@ struct AuxStreams {
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 std::map<int, AuxStreams> g_aux;
+// Serialises the enqueue sequences that use the shared side streams and events
+// (a record / wait pair of one caller must not interleave with another's).
+std::mutex g_aux_enqueue_mu;
 
 int get_aux(AuxStreams** out) {
   int dev = 0;
@@ -322,6 +325,7 @@ int paren_match_tree_bbox(const uint8_t* d_tags, const float* d_leaf_bbox, int64
   // after paren_match's reduce pass and joined before the passes that need
   // match / parent.
   cudaStream_t s = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(g_aux_enqueue_mu);
   cudaError_t e = tb::pm_reduce_only_launch(d_tags, n, d_match, pmws, nullptr, s);
   if (e == cudaSuccess) e = cudaEventRecord(ax->fork, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->side, ax->fork, 0);
@@ -380,6 +384,7 @@ static int pm_tb_host_pipelined(const uint8_t* h_tags, const float* h_leaf_bbox,
   int r = get_ws(s, 5, tb::bbm_workspace_bytes(n), &bws);
   if (r) return r;
   auto lo = [&](int c) { return std::min<int64_t>(n, (int64_t)c * ct * tile); };
+  std::unique_lock<std::mutex> lk(g_aux_enqueue_mu);
   cudaError_t e = cudaEventRecord(ax->start, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->in, ax->start, 0);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
@@ -410,6 +415,7 @@ static int pm_tb_host_pipelined(const uint8_t* h_tags, const float* h_leaf_bbox,
   if (e == cudaSuccess) e = cudaEventRecord(ax->out_done, ax->out);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ax->out_done, 0);
   if (e == cudaSuccess) e = tb::bbm_patch_host_launch(d_tags, d_match, n, d_out, bws, hmap, ct, s);
+  lk.unlock();
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "pipelined host path");
   return TB_OK;
@@ -453,6 +459,7 @@ int paren_match_tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, 
   }
   if (hmap) return pm_tb_host_pipelined(h_tags, h_leaf_bbox, n, h_match, h_parent, h_node_bbox, hmap, d_tags,
                                         d_match, d_parent, d_in, d_out, s, ax);
+  std::unique_lock<std::mutex> lk(g_aux_enqueue_mu);
   cudaError_t e = cudaEventRecord(ax->start, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->in, ax->start, 0);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_tags, h_tags, (size_t)n, cudaMemcpyHostToDevice, s);
@@ -472,6 +479,7 @@ int paren_match_tree_bbox_host(const uint8_t* h_tags, const float* h_leaf_bbox, 
   if (r) return r;
   e = cudaMemcpyAsync(h_node_bbox, d_out, (size_t)n * 16, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ax->out_done, 0);
+  lk.unlock();
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "D2H results");
   return TB_OK;

@@ -108,3 +108,51 @@ def test_graph_capture_fused_call():
     ref = oracle.tree_bbox(tags.numpy(), boxes.numpy())
     assert np.array_equal(m.cpu().numpy(), m_ref) and np.array_equal(p.cpu().numpy(), p_ref)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+def test_concurrent_callers_on_separate_streams():
+    """Host threads driving the shared-side-stream entry points at once (ctypes
+    releases the GIL), each on its own stream and input: every result stays
+    bit-exact."""
+    import threading
+    import paper_2205_11659_b200 as tb
+    lib = tb.load()
+    old = lib.tb_debug_host_chunk_shift(12)
+    cases = []
+    for i in range(4):
+        t = scenegen.walk_tags(120_000 + 1000 * i, 40 + i, p_leaf=0.5)
+        b = scenegen.boxes(t.numel(), 40 + i, t)
+        m_ref, p_ref = oracle.paren_match(t.numpy())
+        cases.append((t, b, m_ref, p_ref, oracle.tree_bbox(t.numpy(), b.numpy())))
+    errors = []
+
+    def worker(i):
+        try:
+            t, b, m_ref, p_ref, ref = cases[i]
+            s = torch.cuda.Stream()
+            td, bd = t.cuda(), b.cuda()
+            hb = b.pin_memory()
+            hm = torch.empty(t.numel(), dtype=torch.int32).pin_memory()
+            hp = torch.empty_like(hm).pin_memory()
+            ho = torch.empty_like(hb).pin_memory()
+            for _ in range(5):
+                with torch.cuda.stream(s):
+                    m, p, out = tb.paren_match_tree_bbox(td, bd)
+                s.synchronize()
+                assert np.array_equal(m.cpu().numpy(), m_ref) and np.array_equal(p.cpu().numpy(), p_ref)
+                assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+                with torch.cuda.stream(s):
+                    tb.paren_match_tree_bbox_host(t.pin_memory(), hb, hm, hp, ho)
+                assert np.array_equal(ho.numpy().view(np.uint32), ref.view(np.uint32))
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    try:
+        th = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+    finally:
+        lib.tb_debug_host_chunk_shift(old)
+    assert not errors, errors
