@@ -33,6 +33,10 @@
  *     for CUDA-graph capture); size it with *_workspace_bytes(n).
  *   - Results are deterministic and bit-identical to the sequential
  *     definitions (Fig. 1), whatever the tiling.
+ *   - Threads: entry points may be called from several host threads at once
+ *     on different streams (the library's side streams and events are used
+ *     under a lock while enqueuing); calls on one stream are issued by one
+ *     host thread at a time.
  */
 #ifndef TREEBBOX_H
 #define TREEBBOX_H
