@@ -331,7 +331,7 @@ int paren_match_tree_bbox(const uint8_t* d_tags, const float* d_leaf_bbox, int64
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ax->side, ax->fork, 0);
   if (e == cudaSuccess) e = tb::bbm_launch_reduce(d_tags, d_leaf_bbox, n, d_node_bbox, bws, ax->side);
   if (e == cudaSuccess) e = cudaEventRecord(ax->join, ax->side);
-  if (e == cudaSuccess) e = tb::pm_rescan_launch(n, d_match, pmws, nullptr, true, s);
+  if (e == cudaSuccess) e = tb::pm_rescan_launch(n, d_match, pmws, nullptr, s);
   if (e == cudaSuccess) e = tb::pm_finish_launch(d_tags, n, d_match, d_parent, pmws, nullptr, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ax->join, 0);
   if (e == cudaSuccess) e = tb::bbm_launch_rest(d_tags, d_leaf_bbox, d_match, d_parent, n, d_node_bbox, bws, s);

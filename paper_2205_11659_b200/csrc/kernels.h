@@ -40,11 +40,10 @@ size_t pm_ctrl_bytes(int64_t n);
 cudaError_t pm_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
                       const ShardInit* init, cudaStream_t stream);
 cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
-                             cudaStream_t stream, bool mark_unmatched = true);
+                             cudaStream_t stream);
 cudaError_t pm_reduce_only_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
                                   cudaStream_t stream);
-cudaError_t pm_rescan_launch(int64_t n, int32_t* match, void* ws, const ShardInit* init, bool mark_unmatched,
-                             cudaStream_t stream);
+cudaError_t pm_rescan_launch(int64_t n, int32_t* match, void* ws, const ShardInit* init, cudaStream_t stream);
 cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
                              const ShardInit* init, cudaStream_t stream);
 cudaError_t pm_summary_launch(const uint8_t* tags, int64_t n, void* ws, int32_t* hdr, int32_t* opens,

@@ -350,6 +350,16 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
       d++;
     }
   }
+  // opens never closed (R4) get match = -1: this tile's slice entries that
+  // survive to the end of the stream (F1), its bottom min(b_T, smin_T - L_T);
+  // nothing else writes those slots
+  if (warp == NW - 1) {
+    const int L = (int)__ldg(p.ctrl.lw + T) - 1;
+    const int bT = __ldg(p.ctrl.agg + T).y;
+    const int sm = __ldg(p.ctrl.smin + T);
+    const int surv = min(bT, max(sm == INT_MAX ? bT : sm - L, 0));
+    for (int k = lane; k < surv; k += 32) p.match[__ldcg(p.slice + (int64_t)T * TILE + k) - p.offset] = -1;
+  }
 }
 
 // Chunk summary for sharding: the chunk's final stack (its unmatched opens,
@@ -357,7 +367,7 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
 // tile.  By the owner rule (F1) tile U's slice entries that survive to the end
 // are its bottom min(b_U, smin_U - L_U) ones, at heights L_U + k; the ranges of
 // different tiles are disjoint, so each tile copies its survivors into place
-// (one warp per tile, as pm_unmatched).
+// (one warp per tile; pm_finish marks never-closed opens by the same rule).
 __global__ void __launch_bounds__(256) pm_summary(Params p, int ntiles, int32_t* hdr, int32_t* opens) {
   const int lane = threadIdx.x & 31;
   const int U = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -372,22 +382,6 @@ __global__ void __launch_bounds__(256) pm_summary(Params p, int ntiles, int32_t*
   const int sm = __ldg(p.ctrl.smin + U);
   const int surv = min(bU, max(sm == INT_MAX ? bU : sm - L, 0));
   for (int k = lane; k < surv; k += 32) opens[L + k] = __ldcg(p.slice + (int64_t)U * TILE + k);
-}
-
-// Opens never closed (R4) get match = -1; every other open's match is written
-// by its close in pm_finish.  Entry k of tile U's slice sits at height L_U + k
-// and survives to the end iff it lies below the low-water mark of every later
-// tile (F1; smin from the tile scan): each tile marks its bottom
-// min(b_U, smin_U - L_U) entries (one warp per tile).
-__global__ void __launch_bounds__(256) pm_unmatched(Params p, int ntiles) {
-  const int lane = threadIdx.x & 31;
-  const int U = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (U >= ntiles) return;
-  const int L = (int)__ldg(p.ctrl.lw + U) - 1;
-  const int bU = __ldg(p.ctrl.agg + U).y;
-  const int sm = __ldg(p.ctrl.smin + U);
-  const int surv = min(bU, max(sm == INT_MAX ? bU : sm - L, 0));
-  for (int k = lane; k < surv; k += 32) p.match[__ldcg(p.slice + (int64_t)U * TILE + k) - p.offset] = -1;
 }
 
 }  // namespace pm
@@ -435,19 +429,14 @@ static cudaError_t pm_configure() {
   return cudaSuccess;
 }
 
-// tile scan (heights from the prefix `init`) and never-closed opens; the
-// per-tile aggregates and slices of pm_reduce do not depend on `init`, so the
-// shard protocol's phase 2 reuses phase 1's
-cudaError_t pm_rescan_launch(int64_t n, int32_t* match, void* ws, const ShardInit* init, bool mark_unmatched,
-                             cudaStream_t stream) {
+// tile scan (heights from the prefix `init`); the per-tile aggregates and
+// slices of pm_reduce do not depend on `init`, so the shard protocol's phase 2
+// reuses phase 1's
+cudaError_t pm_rescan_launch(int64_t n, int32_t* match, void* ws, const ShardInit* init, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int64_t ntiles = (n + pm::TILE - 1) / pm::TILE;
   pm::Params p = pm_params(nullptr, n, match, nullptr, ws, init);
-  cudaError_t err = tile_scan_launch(p.ctrl, ntiles, p.init.a, p.init.b, stream);
-  if (err != cudaSuccess || !mark_unmatched) return err;
-  TB_LAUNCH(stream, "pm_unmatched",
-            (pm::pm_unmatched<<<(unsigned)((ntiles + 7) / 8), 256, 0, stream>>>(p, (int)ntiles)));
-  return cudaGetLastError();
+  return tile_scan_launch(p.ctrl, ntiles, p.init.a, p.init.b, stream);
 }
 
 cudaError_t pm_reduce_only_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
@@ -462,10 +451,10 @@ cudaError_t pm_reduce_only_launch(const uint8_t* tags, int64_t n, int32_t* match
 }
 
 cudaError_t pm_reduce_launch(const uint8_t* tags, int64_t n, int32_t* match, void* ws, const ShardInit* init,
-                             cudaStream_t stream, bool mark_unmatched) {
+                             cudaStream_t stream) {
   cudaError_t err = pm_reduce_only_launch(tags, n, match, ws, init, stream);
   if (err != cudaSuccess) return err;
-  return pm_rescan_launch(n, match, ws, init, mark_unmatched, stream);
+  return pm_rescan_launch(n, match, ws, init, stream);
 }
 
 cudaError_t pm_finish_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,

@@ -153,7 +153,7 @@ struct PmChunk {
   // phase 1: chunk-local reduce + summary
   cudaError_t phase1() {
     ShardInit local{0, 0, nullptr, 0, off, nullptr};  // chunk-local frame, global indices
-    cudaError_t e = pm_reduce_launch(tags, n, match, ws, &local, s, /*mark_unmatched=*/false);
+    cudaError_t e = pm_reduce_launch(tags, n, match, ws, &local, s);
     if (e == cudaSuccess) e = pm_summary_launch(tags, n, ws, hdr, opens, s);
     return e;
   }
@@ -187,7 +187,7 @@ struct PmChunk {
       if (e != cudaSuccess) return e;
     }
     ShardInit init{(int)mine.a, H, stack, lo, off, pairs};
-    e = pm_rescan_launch(n, match, ws, &init, true, s);  // phase 1's per-tile aggregates and slices stand
+    e = pm_rescan_launch(n, match, ws, &init, s);  // phase 1's per-tile aggregates and slices stand
     if (e == cudaSuccess) e = pm_finish_launch(tags, n, match, parent, ws, &init, s);
     return e;
   }
