@@ -436,8 +436,13 @@ struct Smem {
 // element i of thread t lives at slot Kt + (i ^ (t & 7)): conflict-free both for
 // the coalesced copies (8 consecutive elements of one thread per 128-byte
 // wavefront) and for the per-thread accesses (8 threads, distinct slot & 7)
-__device__ __forceinline__ int slot(int t, int i) { return t * K + (i ^ (t & 7)); }
-__device__ __forceinline__ int slot_of(int e) { return slot(e / K, e % K); }
+// (bit form: K is a power of two >= 8 and indices are non-negative, so
+// slot(t, i) = (t*K | t & 7) ^ i and slot_of(e) = e ^ ((e / K) & 7) — no
+// signed-division fixups, one LOP3 per access once t's part is hoisted)
+constexpr int LOGK = K == 8 ? 3 : 4;
+__device__ __forceinline__ int slot(int t, int i) { return ((t << LOGK) | (t & 7)) ^ i; }
+__device__ __forceinline__ int slot_of(int e) { return e ^ (int)(((unsigned)e >> LOGK) & 7u); }
+__device__ __forceinline__ int thr_of(int e) { return (int)((unsigned)e >> LOGK); }
 
 // union of the clipped leaves of whole threads [a, b]: the suffix of a's warp,
 // the warps strictly between (table), the window part of b's warp ending at
@@ -545,7 +550,7 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
       } else {
         const int x = (int)(curX - gbase);
         acc = s.val[slot_of(x)];
-        ptr = x / K;
+        ptr = thr_of(x);
       }
     }
     int cb = 0;
@@ -586,7 +591,7 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
               g = X == xa ? ga : (X == xb ? gb : outer_ctx<SHARD>(p, X));
             } else {
               const int x = (int)(X - gbase);
-              g = isect(s.val[slot_of(x)], s.u.tl[x / K]);
+              g = isect(s.val[slot_of(x)], s.u.tl[thr_of(x)]);
             }
           }
           float4& me = s.val[slot(tid, i)];
@@ -618,9 +623,11 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
 #pragma unroll
   for (int i = 0; i < K; i++) {
     const uint32_t bit = 1u << i;
-    if (lm & bit) {
-      PT = unite(PT, s.val[slot(tid, i)]);
-    } else if (cm & bit) {
+    {  // leaves: a select, not a branch (every lane reads its slot)
+      const float4 u = unite(PT, s.val[slot(tid, i)]);
+      PT = (lm & bit) ? u : PT;
+    }
+    if (cm & bit) {
       const int m = mt[i];
       if (m >= gtstart) {
         const int o = (int)(m - gtstart);
@@ -696,7 +703,6 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
         const uint32_t bit = 1u << i;
         if (qt & bit) {
           p.su[tstart + i] = unite(R, after);
-          if (nvm & bit) p.never[atomicAdd(p.nnever, 1u)] = (int)(tstart + i);
         } else if (qi & bit) {
           const int c = (int)(mt[i] - gbase);
           float4& cv = s.val[slot_of(c)];
@@ -705,19 +711,24 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
             pk |= (uint64_t)(c | (i << 10)) << (16 * npk);
             npk++;
           } else {
-            const float4 U = unite(unite(R, range_union_threads(s, tid + 1, c / K - 1)), cv);
+            const float4 U = unite(unite(R, range_union_threads(s, tid + 1, thr_of(c) - 1)), cv);
             cv = U;
             if ((bm >> i) & 1u) s.val[slot(tid, i)] = U;
           }
         }
         if ((lm & bit) && ((qt | qi) & (bit - 1u))) R = unite(R, s.val[slot(tid, i)]);
       }
+      if (nvm) {  // blend opens never closed (R4), listed for bbm_final (any order)
+        unsigned k = atomicAdd(p.nnever, (unsigned)__popc(nvm));
+#pragma unroll 1
+        for (uint32_t q = nvm; q; q &= q - 1) p.never[k++] = (int)(tstart + __ffs(q) - 1);
+      }
 #pragma unroll 1
       for (int k = 0; k < npk; k++) {
         const int e = (int)(pk >> (16 * k)) & 0xffff;
         const int c = e & 1023, i = e >> 10;
         float4& cv = s.val[slot_of(c)];
-        const float4 U = unite(cv, range_union_threads(s, tid + 1, c / K - 1));
+        const float4 U = unite(cv, range_union_threads(s, tid + 1, thr_of(c) - 1));
         cv = U;
         if ((bm >> i) & 1u) s.val[slot(tid, i)] = U;
       }
