@@ -629,6 +629,7 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
     }
     if (cm & bit) {
       const int m = mt[i];
+      float4 st = m >= 0 ? PT : bEMPTY();  // outer node: completed in F or G; R3: EMPTY
       if (m >= gtstart) {
         const int o = (int)(m - gtstart);
         float4 U = bEMPTY();
@@ -638,14 +639,11 @@ __global__ void __launch_bounds__(NT, MINB) bbm_main(Params p) {
           lb &= lb - 1;
           U = unite(U, s.val[slot(tid, j)]);
         }
-        s.val[slot(tid, i)] = U;
+        st = U;
         if ((bm >> o) & 1u) s.val[slot(tid, o)] = U;
-      } else if (m >= 0) {
-        s.val[slot(tid, i)] = PT;  // completed by the open's thread (F) or in G
-        if (m < gbase) ecm |= bit;
-      } else {
-        s.val[slot(tid, i)] = bEMPTY();  // R3
       }
+      ecm |= ((unsigned)m < (unsigned)gbase) ? bit : 0u;
+      s.val[slot(tid, i)] = st;
     }
   }
   BBM_TRACE(T, 4);
