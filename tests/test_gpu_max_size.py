@@ -16,11 +16,18 @@ pytestmark = pytest.mark.gpu
 def test_one_billion_elements():
     import paper_2205_11659_b200 as tb
     n = 1 << 30
+    torch.cuda.empty_cache()  # blocks cached by earlier tests in this process
     free, _ = torch.cuda.mem_get_info()
     if free < 90 << 30:
         pytest.skip("needs ~90 GB of free device memory")
     tags = scenegen.walk_tags(n, 4, device="cuda")
-    boxes = scenegen.boxes(n, 4, tags, device="cuda")
+    # boxes by chunks of the same per-index hash (the whole-stream generator
+    # holds ~120 GB of fp64 / int64 temporaries at n = 2^30)
+    boxes = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+    step = 1 << 27
+    for s in range(0, n, step):
+        e = min(n, s + step)
+        boxes[s:e] = scenegen.boxes(e - s, 4, tags[s:e], offset=s, device="cuda")
     torch.cuda.empty_cache()  # the generators' temporaries; the library allocates its own workspace
     m, p = tb.paren_match(tags)
     out = tb.tree_bbox_matched(tags, boxes, m, p)
