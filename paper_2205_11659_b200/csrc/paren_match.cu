@@ -200,11 +200,20 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
   const int64_t tbase = base + (int64_t)tid * K;
   const bool full = base + TILE <= p.n;
 
-  const Walk16 w = walk16(load_tags16(p.tags, p.n, tbase, full));
+  const uint4 raw = load_tags16(p.tags, p.n, tbase, full);
+  // The incoming-stack range needs only H and the tile's a_T, both published by
+  // pass 1 (agg[T] is this tile's Bic), so warp 0 starts the owner search
+  // while the tag loads are in flight; its L2 round trips overlap the walk and
+  // the block scan instead of following them.
+  const int H = __ldg(p.ctrl.hstart + T);
+  const int aT = __ldg(p.ctrl.agg + T).x;
+  const int lo = max(H - 1 - aT, 0);  // lowest referenced height that exists
+  int cur = H - 1, from = T;
+  if (warp == 0) cur = find_runs(s, p.ctrl, cur, from, lo, p.init_lo);
+  const Walk16 w = walk16(raw);
   const int a_t = __popc(w.ucm), b_t = __popc(w.S);
   Bic ex, sx, tot;
   block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, false);
-  const int aT = tot.a;
   const int r_t = ex.b - ex.a;
   const int l_t = r_t - a_t;
   (void)b_t;
@@ -219,12 +228,8 @@ __global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
   }
   s.l[tid] = l_t;
   s.uo[tid] = w.S;
-  const int H = __ldg(p.ctrl.hstart + T);
-  const int lo = max(H - 1 - aT, 0);  // lowest referenced height that exists
-  int cur = H - 1, from = T;
   __syncthreads();
 
-  if (warp == 0) cur = find_runs(s, p.ctrl, cur, from, lo, p.init_lo);
   const int top_ref = thread_ref<NW, K>(wl, l_t, w.S, r_t - 1, s.win, s.wmin, s.l, s.uo);
   s.link[tid] = thread_ref<NW, K>(wl, l_t, w.S, l_t - 1, s.win, s.wmin, s.l, s.uo);
   for (int d = H + tid; d <= aT; d += NT) s.inc[d] = -1;  // below the root
