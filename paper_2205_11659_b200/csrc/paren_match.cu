@@ -190,8 +190,11 @@ __device__ __forceinline__ int find_runs(Smem& s, const Ctrl& c, int cur, int& f
   return cur;
 }
 
+#ifndef PM_FINISH_MINB
+#define PM_FINISH_MINB 4  // CTAs per SM (64 registers)
+#endif
 template <bool SHARD>
-__global__ void __launch_bounds__(NT, 4) pm_finish(Params p) {
+__global__ void __launch_bounds__(NT, PM_FINISH_MINB) pm_finish(Params p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
