@@ -103,6 +103,19 @@ def test_staircases():
     check(t2)
 
 
+def test_many_incoming_runs():
+    """One tile pops an incoming stack spread over more predecessor slices than
+    pm_finish gathers per batch (RUNCAP = 32 runs), so the run search repeats."""
+    for npred, per in ((40, 50), (70, 3), (33, 1)):
+        pred = torch.cat([torch.full((per,), 1, dtype=torch.uint8),
+                          torch.zeros(TILE - per, dtype=torch.uint8)])
+        closes = torch.full((npred * per + 5,), 3, dtype=torch.uint8)  # pops everything, then underflows
+        t = torch.cat([pred.repeat(npred), closes, torch.full((777,), 2, dtype=torch.uint8)])
+        check(t)
+        # the same closes one tile later, behind a tile of leaves
+        check(torch.cat([pred.repeat(npred), torch.zeros(TILE + 17, dtype=torch.uint8), closes]))
+
+
 def test_underflow_heavy_random():
     g = torch.Generator().manual_seed(5)
     for n in (1000, 50_000, 300_000):
