@@ -263,17 +263,15 @@ __global__ void __launch_bounds__(NT, PM_FINISH_MINB) pm_finish(Params p) {
   // (>= 0 in-tile element, < 0 incoming depth -ref-1) resolved where used
   const int gbase0 = (int)(p.offset + base);
   {
-    int ref = top_ref;
-    for (int d = 0; d <= a_t; d++) {
-      s.extv[d][tid] = SHARD ? ref : (ref >= 0 ? gbase0 + ref : s.inc[-ref - 1]);
-      if (ref >= 0) {
-        const int V = ref >> 4;
-        const uint32_t below = s.uo[V] & ((1u << (ref & 15)) - 1u);
-        ref = below ? (V << 4) + (31 - __clz(below)) : s.link[V];
-      } else {
-        ref -= 1;
-      }
+    // in-tile entries first (owner chain), then consecutive incoming depths
+    int ref = top_ref, d = 0;
+    for (; d <= a_t && ref >= 0; d++) {
+      s.extv[d][tid] = SHARD ? ref : gbase0 + ref;
+      const int V = ref >> 4;
+      const uint32_t below = s.uo[V] & ((1u << (ref & 15)) - 1u);
+      ref = below ? (V << 4) + (31 - __clz(below)) : s.link[V];
     }
+    for (; d <= a_t; d++, ref--) s.extv[d][tid] = SHARD ? ref : s.inc[-ref - 1];
   }
 
   // parent / match
