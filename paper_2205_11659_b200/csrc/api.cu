@@ -236,7 +236,15 @@ static int bbm_checks(const uint8_t* tags, const float* leaf, const int32_t* mat
   return TB_OK;
 }
 
-size_t tree_bbox_workspace_bytes(int64_t n) { return n > 0 ? BbWs(n).bytes : 0; }
+// The fused single-device path (fused.cu) runs paren_match + tree_bbox from one
+// tile pass; tb_debug_use_fused(0) selects the earlier two-call path
+// (paren_match, then the boxes from its match / parent) for comparisons.
+static int g_use_fused = 1;
+
+size_t tree_bbox_workspace_bytes(int64_t n) {
+  if (n <= 0) return 0;
+  return std::max(BbWs(n).bytes, tb::fused_workspace_bytes(n));
+}
 
 static int tree_bbox_ws_impl(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, float* d_node_bbox,
                              void* d_workspace, size_t workspace_bytes, void* stream, uint64_t* trace) {
@@ -246,6 +254,14 @@ static int tree_bbox_ws_impl(const uint8_t* d_tags, const float* d_leaf_bbox, in
   const BbWs L(n);
   if (!d_workspace || workspace_bytes < L.bytes)
     return fail(TB_ERR_ARG, "workspace too small: need %zu bytes", L.bytes);
+  if (g_use_fused && trace == nullptr) {
+    if (workspace_bytes < tb::fused_workspace_bytes(n))
+      return fail(TB_ERR_ARG, "workspace too small: need %zu bytes", tb::fused_workspace_bytes(n));
+    cudaError_t e = tb::fused_launch(d_tags, d_leaf_bbox, n, nullptr, nullptr, d_node_bbox, d_workspace,
+                                     (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "tree_bbox launch");
+    return TB_OK;
+  }
   char* w = (char*)d_workspace;
   int32_t* match = (int32_t*)(w + L.match_off);
   int32_t* parent = (int32_t*)(w + L.parent_off);
@@ -311,6 +327,15 @@ int paren_match_tree_bbox(const uint8_t* d_tags, const float* d_leaf_bbox, int64
   const size_t nb = (size_t)n * 16, n4 = (size_t)n * 4;
   if (overlap(d_match, n4, d_leaf_bbox, nb) || overlap(d_parent, n4, d_leaf_bbox, nb))
     return fail(TB_ERR_ALIAS, "match / parent overlap leaf_bbox");
+  if (g_use_fused) {
+    void* fws = nullptr;
+    r = get_ws(stream, 7, tb::fused_workspace_bytes(n), &fws);
+    if (r) return r;
+    cudaError_t e = tb::fused_launch(d_tags, d_leaf_bbox, n, d_match, d_parent, d_node_bbox, fws,
+                                     (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "paren_match_tree_bbox launch");
+    return TB_OK;
+  }
   void* pmws = nullptr;
   void* bws = nullptr;
   r = get_ws(stream, 0, tb::pm_workspace_bytes(n), &pmws);
@@ -567,6 +592,12 @@ int compact_scene(const uint8_t* d_tags, const float* d_boxes, int64_t n, const 
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }
+
+int tb_debug_use_fused(int on) {
+  const int old = g_use_fused;
+  if (on >= 0) g_use_fused = on ? 1 : 0;
+  return old;
+}
 
 /* Debug: capacity of bin_leaves' list of binned leaves (returns the previous
  * one); tests lower it to reach the streaming fill. */

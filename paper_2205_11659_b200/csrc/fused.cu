@@ -1,0 +1,945 @@
+// paren_match + tree_bbox in one tile pass (sm_100a).
+//
+// The matching (§2-§8 of the paper: Fig. 1's parent, and the
+// classical partner) and the two box passes (§6, §9: the clip
+// intersection of P:24/P:201/P:292 and the blend union of P:24/P:196/P:216-221,
+// stored at the close and scattered to a blend open) are computed by
+// the same kernel from the tags and boxes of one tile, so each element's tag
+// and box are read once and match, parent and node_bbox written once.
+//
+//   fz_reduce  one warp per 2048-element tile, tags only (+ the boxes of the
+//              tile's unmatched opens): the tile's Bic value (§3) and
+//              its stack slice (§7.1: unmatched opens, ascending)
+//              with each entry's tile-local cumulative clip lc.
+//   tile_scan  start heights H_T, low-water marks L_T, the 32-ary low-water
+//              hierarchy (owner rule F1), offsets of the incoming lists.
+//   fz_ctrl    (cooperative) per tile: TC(T) = context of the stack entry just
+//              below its slice, by pointer jumping over tiles (F3 at tile
+//              level; replaces the paper's scan of partition top boxes,
+//              P:292); slice contexts lc ∩ TC; the tile's incoming list = the
+//              a_T + 1 top entries of the stack at its start (owner rule F1
+//              over the published slices = the suffix relation of P:131-138).
+//   fz_main    one CTA per tile: register walk (Fig. 1 per thread), block Bic
+//              scan, thread-level owner lookups (F2), thread link contexts by
+//              pointer jumping over threads, one forward walk that clips,
+//              unions and emits parent/match, a backward walk for the unions
+//              of opens closed in a later thread or tile; coalesced copy-out.
+//   fz_hier    32-ary hierarchy of tile unions.
+//   fz_close   closes of nodes opened in an earlier tile: tile prefix ∪ the
+//              open's tile suffix ∪ the whole tiles between (F4/F7); blend
+//              opens and match[open] receive the result; blend opens never
+//              closed (R4) get the union of everything after them.
+#include <algorithm>
+#include <climits>
+#include <cooperative_groups.h>
+
+#include "boxes.cuh"
+#include "common.cuh"
+#include "kernels.h"
+#include "stackscan.cuh"
+#include "tile_common.cuh"
+
+namespace tb {
+namespace fz {
+
+constexpr int K = 16;          // elements per thread
+constexpr int LOGK = 4;
+constexpr int NT = 128;        // threads per tile
+constexpr int NW = NT / 32;
+constexpr int W = NT * K;      // tile = 2048 elements
+constexpr int LOGW = 11;
+constexpr int LV = 5;          // 32-ary levels of tile unions: 32^5 tiles > 2^31 / W
+constexpr int SKIP = INT_MIN;  // match slot written by another thread / kernel
+static_assert(W == (1 << LOGW) && K == (1 << LOGK), "tile shape");
+
+struct Params {
+  const uint8_t* tags;
+  const float4* boxes;
+  int64_t n;
+  int ntiles;
+  int32_t* match;      // may be null (tree_bbox alone)
+  int32_t* parent;     // may be null
+  float4* out;
+  Ctrl ctrl;
+  int64_t* aoff;       // [ntiles + 1] exclusive prefix of (a_T + 1)
+  int32_t* slice_idx;  // [ntiles * W] global index | blend << 31
+  float4* slice_box;   // [ntiles * W] lc (fz_reduce), then the true context (fz_ctrl)
+  float4* slice_su;    // [ntiles * W] union of the tile's clipped leaves after the entry (fz_main)
+  int2* inc;           // [aoff[ntiles]] incoming entry at depth D: (global index, slice ref), (-1, -1) = root
+  int32_t* xc;         // [aoff[ntiles]] the close that pops incoming depth D (non-root pops only)
+  float4* tu[LV];      // tile unions, 32-ary hierarchy
+  float4* pj_acc;      // [2 * ntiles] pointer jumping over tiles
+  int32_t* pj_ptr;     // [2 * ntiles]
+  int32_t* flag;       // [2]
+};
+
+// ----------------------------------------------------------------------------
+// workspace
+// ----------------------------------------------------------------------------
+struct Layout {
+  size_t ctrl, aoff, sidx, sbox, ssu, inc, xc, tu[LV], pja, pjp, flag, bytes;
+  int64_t ntiles;
+  explicit Layout(int64_t n) {
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    ntiles = (n + W - 1) / W;
+    const size_t cap = (size_t)ntiles * W;
+    const size_t ninc = (size_t)n + (size_t)ntiles;  // Σ (a_T + 1) <= closes + tiles
+    size_t o = 0;
+    ctrl = o; o = al(o + CtrlLayout(ntiles).bytes);
+    aoff = o; o = al(o + 8 * ((size_t)ntiles + 1));
+    sidx = o; o = al(o + 4 * cap);
+    sbox = o; o = al(o + 16 * cap);
+    ssu = o; o = al(o + 16 * cap);
+    inc = o; o = al(o + 8 * ninc);
+    xc = o; o = al(o + 4 * ninc);
+    int64_t m = ntiles;
+    for (int k = 0; k < LV; k++) {
+      tu[k] = o; o = al(o + 16 * (size_t)m);
+      m = (m + 31) / 32;
+    }
+    pja = o; o = al(o + 32 * (size_t)ntiles);
+    pjp = o; o = al(o + 8 * (size_t)ntiles);
+    flag = o; o = al(o + 16);
+    bytes = o;
+  }
+};
+
+static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, int32_t* match, int32_t* parent,
+                          float* out, void* ws) {
+  const Layout L(n);
+  char* b = (char*)ws;
+  Params p;
+  p.tags = tags;
+  p.boxes = (const float4*)boxes;
+  p.n = n;
+  p.ntiles = (int)L.ntiles;
+  p.match = match;
+  p.parent = parent;
+  p.out = (float4*)out;
+  p.ctrl = CtrlLayout(L.ntiles).bind(b + L.ctrl);
+  p.aoff = (int64_t*)(b + L.aoff);
+  p.slice_idx = (int32_t*)(b + L.sidx);
+  p.slice_box = (float4*)(b + L.sbox);
+  p.slice_su = (float4*)(b + L.ssu);
+  p.inc = (int2*)(b + L.inc);
+  p.xc = (int32_t*)(b + L.xc);
+  for (int k = 0; k < LV; k++) p.tu[k] = (float4*)(b + L.tu[k]);
+  p.pj_acc = (float4*)(b + L.pja);
+  p.pj_ptr = (int32_t*)(b + L.pjp);
+  p.flag = (int32_t*)(b + L.flag);
+  return p;
+}
+
+// tag bytes -> open / close / blend-open masks of 16 elements (bit i <-> byte i)
+__device__ __forceinline__ void classify16b(uint4 raw, uint32_t& om, uint32_t& cm, uint32_t& bm) {
+  uint32_t o = 0, c = 0, b = 0;
+  const uint32_t ws[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t x = ws[q];
+    const uint32_t bl = __vcmpeq4(x, 0x02020202u);
+    o |= byte_mask4(__vcmpeq4(x, 0x01010101u) | bl) << (4 * q);
+    c |= byte_mask4(__vcmpeq4(x, 0x03030303u)) << (4 * q);
+    b |= byte_mask4(bl) << (4 * q);
+  }
+  om = o;
+  cm = c;
+  bm = b;
+}
+
+// ----------------------------------------------------------------------------
+// fz_reduce: tile Bic values, slices and their local cumulative clips
+// ----------------------------------------------------------------------------
+constexpr int RL = W / 32;  // 64 elements per lane
+__global__ void __launch_bounds__(256) fz_reduce(Params p) {
+  __shared__ uint8_t bic4[256];  // Bic of 4 elements: index = open nibble | close nibble << 4; value a | b << 4
+  __shared__ uint8_t unm4[UNM4_ENTRIES];
+  const int lane = threadIdx.x & 31;
+  {
+    const int t = threadIdx.x;
+    Bic v{0, 0};
+#pragma unroll
+    for (int j = 0; j < 4; j++) v = bic_combine(v, Bic{(t >> (4 + j)) & 1, (t >> j) & 1});
+    bic4[t] = (uint8_t)(v.a | (v.b << 4));
+    unm4_fill(unm4, t, 256);
+  }
+  __syncthreads();
+  const int T = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (T >= p.ntiles) return;
+  const int64_t base = (int64_t)T * W, lbase = base + (int64_t)lane * RL;
+  uint32_t om[2], cm[2], bk[2];
+  {
+    uint4 raw[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int64_t g = lbase + 16 * q;
+      raw[q] = g + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags + g)) : load_tags16(p.tags, p.n, g, false);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      uint32_t o, c, b;
+      classify16b(raw[q], o, c, b);
+      if (q & 1) {
+        om[q >> 1] |= o << 16;
+        cm[q >> 1] |= c << 16;
+        bk[q >> 1] |= b << 16;
+      } else {
+        om[q >> 1] = o;
+        cm[q >> 1] = c;
+        bk[q >> 1] = b;
+      }
+    }
+  }
+  Bic lb{0, 0};
+#pragma unroll
+  for (int w = 0; w < 2; w++) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint32_t e = bic4[((om[w] >> (4 * q)) & 15u) | (((cm[w] >> (4 * q)) & 15u) << 4)];
+      lb = bic_combine(lb, Bic{(int)(e & 15u), (int)(e >> 4)});
+    }
+  }
+  Bic incl = lb, suf = lb;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Bic a{__shfl_up_sync(0xffffffffu, incl.a, off), __shfl_up_sync(0xffffffffu, incl.b, off)};
+    if (lane >= off) incl = bic_combine(a, incl);
+    const Bic b{__shfl_down_sync(0xffffffffu, suf.a, off), __shfl_down_sync(0xffffffffu, suf.b, off)};
+    if (lane + off < 32) suf = bic_combine(suf, b);
+  }
+  const Bic tot{__shfl_sync(0xffffffffu, incl.a, 31), __shfl_sync(0xffffffffu, incl.b, 31)};
+  Bic ex{__shfl_up_sync(0xffffffffu, incl.a, 1), __shfl_up_sync(0xffffffffu, incl.b, 1)};
+  Bic sx{__shfl_down_sync(0xffffffffu, suf.a, 1), __shfl_down_sync(0xffffffffu, suf.b, 1)};
+  if (lane == 0) ex = Bic{0, 0};
+  if (lane == 31) sx = Bic{0, 0};
+  if (lane == 0) p.ctrl.agg[T] = make_int2(tot.a, tot.b);
+  // the lane's unmatched opens that survive to the tile end: its bottom s_l,
+  // at tile-relative heights l + k, slice position l + k + a_T
+  const int l = ex.b - ex.a - lb.a;
+  const int s_l = max(lb.b - sx.a, 0);
+  uint32_t sv[2] = {0u, 0u};
+  if (s_l > 0) {
+    uint32_t um[2];
+    int P = 0;
+    um[1] = unm32(unm4, om[1], cm[1], P);
+    um[0] = unm32(unm4, om[0], cm[0], P);
+    int k = 0;
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      uint32_t m = um[w];
+      while (m && k < s_l) {
+        const uint32_t low = m & (~m + 1u);
+        sv[w] |= low;
+        m ^= low;
+        k++;
+      }
+    }
+  }
+  // lc = ∩ of the clip boxes of the slice entries at and below each entry
+  // (blend opens pass the clip through, R7): lane aggregate, exclusive ∩-scan
+  float4 agg = bINF();
+#pragma unroll
+  for (int w = 0; w < 2; w++)
+    for (uint32_t q = sv[w] & ~bk[w]; q; q &= q - 1) agg = isect(agg, __ldg(p.boxes + lbase + 32 * w + __ffs(q) - 1));
+  float4 x = agg;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float4 o = shfl_up_box(x, off);
+    if (lane >= off) x = isect(x, o);
+  }
+  float4 acc = shfl_up_box(x, 1);
+  if (lane == 0) acc = bINF();
+  int k = 0;
+#pragma unroll
+  for (int w = 0; w < 2; w++) {
+    for (uint32_t q = sv[w]; q; q &= q - 1) {
+      const int j = __ffs(q) - 1;
+      const int64_t e = lbase + 32 * w + j;
+      const uint32_t blend = (bk[w] >> j) & 1u;
+      if (!blend) acc = isect(acc, __ldg(p.boxes + e));
+      const int64_t pos = base + l + k + tot.a;
+      p.slice_idx[pos] = (int)((uint32_t)e | (blend << 31));
+      p.slice_box[pos] = acc;
+      k++;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// fz_ctrl (cooperative): TC by pointer jumping, slice contexts, incoming lists
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) fz_ctrl(Params p) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int nt = p.ntiles;
+  const int gwarp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+  // phase 1 (one warp per tile)
+  for (int T = gwarp; T < nt; T += nwarps) {
+    const int H = __ldg(p.ctrl.hstart + T);
+    const int aT = __ldg(p.ctrl.agg + T).x;
+    const int L = (int)__ldg(p.ctrl.lw + T) - 1;
+    const int64_t ioff = __ldg(p.aoff + T);
+    // TC(T): the entry at height L - 1 (the tile's link): slice entry of its owner
+    float4 acc = bINF();
+    int ptr = -1;
+    if (L >= 1) {
+      int LU = 0;
+      const int U = owner_search_done(p.ctrl, T, L - 1, LU);
+      if (U >= 0) {
+        acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - LU));
+        ptr = U;
+      }
+    }
+    if (lane == 0) {
+      p.pj_acc[T] = acc;
+      p.pj_ptr[T] = ptr;
+    }
+    // incoming list: depth D = 0..a_T <-> height H - 1 - D; below 0: the root
+    for (int D = max(H, 0) + lane; D <= aT; D += 32) p.inc[ioff + D] = make_int2(-1, -1);
+    int cur = H - 1, from = T;
+    const int lo = max(H - 1 - aT, 0);
+    while (cur >= lo) {
+      int LU = 0;
+      const int U = owner_search_done(p.ctrl, from, cur, LU);
+      if (U < 0) break;  // cannot happen on one device (every live entry was pushed by a tile)
+      const int hlo = max(LU, lo);
+      for (int h = cur - lane; h >= hlo; h -= 32) {
+        const int64_t ref = (int64_t)U * W + (h - LU);
+        p.inc[ioff + (H - 1 - h)] = make_int2(__ldcg(p.slice_idx + ref) & 0x7fffffff, (int)ref);
+      }
+      cur = LU - 1;
+      from = U;
+    }
+  }
+  // phase 2: TC(T) = acc ∩ TC(ptr), pointer jumping (thread per tile)
+  const int gt = (int)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  const int nthr = (int)(gridDim.x * (int64_t)blockDim.x);
+  float4* accb[2] = {p.pj_acc, p.pj_acc + nt};
+  int* ptrb[2] = {p.pj_ptr, p.pj_ptr + nt};
+  int cb = 0;
+  for (int round = 0; round < 40; round++) {
+    if (gt == 0) p.flag[round & 1] = 0;
+    grid.sync();
+    int any = 0;
+    for (int V = gt; V < nt; V += nthr) {
+      float4 a = __ldcg(accb[cb] + V);
+      int q = __ldcg(ptrb[cb] + V);
+      if (q >= 0) {
+        a = isect(a, __ldcg(accb[cb] + q));
+        q = __ldcg(ptrb[cb] + q);
+        any |= q >= 0;
+      }
+      accb[cb ^ 1][V] = a;
+      ptrb[cb ^ 1][V] = q;
+    }
+    any = __syncthreads_or(any);
+    if (any && threadIdx.x == 0) atomicOr(p.flag + (round & 1), 1);
+    cb ^= 1;
+    grid.sync();
+    if (__ldcg(p.flag + (round & 1)) == 0) break;
+  }
+  // phase 3: slice contexts lc ∩ TC (one warp per tile)
+  for (int T = gwarp; T < nt; T += nwarps) {
+    const int bT = __ldg(p.ctrl.agg + T).y;
+    if (bT == 0) continue;
+    const float4 tc = __ldcg(accb[cb] + T);
+    float4* sb = p.slice_box + (int64_t)T * W;
+    for (int k = lane; k < bT; k += 32) sb[k] = isect(__ldcg(sb + k), tc);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// fz_main
+// ----------------------------------------------------------------------------
+struct Walk {
+  uint32_t om, cm, bm, lm;  // opens, closes, blend opens, leaves (valid elements only)
+  uint32_t S;               // opens still on the thread stack at its end (thread-unmatched)
+  uint32_t plo, phi;        // nibble i: in-thread parent of element i
+  uint32_t mlo, mhi;        // nibble o: in-thread partner close of open o
+  uint32_t ext;             // elements whose parent lies before the thread
+  uint32_t ucm;             // closes with no in-thread open (they pop the stack at the thread start)
+};
+
+// Fig. 1 over the thread's 16 elements with a bitmask stack
+__device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
+  Walk w;
+  classify16b(raw, w.om, w.cm, w.bm);
+  w.om &= valid;
+  w.cm &= valid;
+  w.bm &= valid;
+  w.lm = valid & ~(w.om | w.cm);
+  uint32_t S = 0, plo = 0, phi = 0, mlo = 0, mhi = 0, ext = 0, ucm = 0;
+#pragma unroll
+  for (int i = 0; i < K; i++) {
+    const uint32_t bit = 1u << i;
+    const int top = 31 - __clz(S);  // -1 when the thread stack is empty
+    if (i < 8) plo |= (uint32_t)(top & 15) << (4 * i);
+    else phi |= (uint32_t)(top & 15) << (4 * (i - 8));
+    ext |= S ? 0u : bit;
+    const bool pop = (w.cm & bit) && S;
+    ucm |= ((w.cm & bit) && !S) ? bit : 0u;
+    const uint32_t pv = (uint32_t)i << (4 * (top & 7));
+    mlo |= (pop && top < 8) ? pv : 0u;
+    mhi |= (pop && top >= 8) ? pv : 0u;
+    S = (w.om & bit) ? (S | bit) : (pop ? (S ^ (1u << top)) : S);
+  }
+  w.S = S;
+  w.plo = plo;
+  w.phi = phi;
+  w.mlo = mlo;
+  w.mhi = mhi;
+  w.ext = ext;
+  w.ucm = ucm;
+  return w;
+}
+
+struct Smem {
+  float4 val[W];      // boxes -> lc / contexts / clips / unions (swizzled slots)
+  int32_t matchS[W];  // match values (global indices), copied out coalesced
+  union {
+    struct {
+      float4 acc[2][NT];
+      int ptr[2][NT];
+    } pj;             // thread link contexts by pointer jumping
+    struct {
+      float4 win[5][NT];  // union of thread unions over lanes [lane - 2^k + 1, lane] (within the warp)
+      float4 suf[NT];     // inclusive suffix within the warp
+    } un;
+  } u;
+  int32_t extv[K + 1][NT];  // global index of the entry at depth d of the thread's start stack (-1: root)
+  float4 tl[NT];            // context of each thread's link
+  int lwin[NW][5][32];      // low-water windows (thread owner lookups)
+  int lwmin[NW];
+  int l[NT];
+  uint32_t uo[NT];
+  int link[NT];
+  float4 wtu[NW];
+  float4 wmid[NW][NW];
+  Bic wtot[NW];
+};
+
+// element i of thread t lives at slot (t*K | t & 7) ^ i: conflict-free for the
+// per-thread accesses (8 lanes, distinct t & 7) and for the coalesced copies
+__device__ __forceinline__ int slot_of(int e) { return e ^ (int)(((unsigned)e >> LOGK) & 7u); }
+
+// union of the clipped leaves of whole threads [a, b] (F4)
+__device__ __forceinline__ float4 range_threads(const Smem& s, int a, int b) {
+  if (a > b) return bEMPTY();
+  const int wa = a >> 5, wb = b >> 5;
+  const int a2 = (wa == wb) ? a : (wb << 5);
+  const int len = b - a2 + 1;
+  const int k = min(31 - __clz(len), 4);
+  const float4 right = (len == 32) ? s.wtu[wb] : unite(s.u.un.win[k][b], s.u.un.win[k][a2 + (1 << k) - 1]);
+  if (wa == wb) return right;
+  return unite(unite(s.u.un.suf[a], right), s.wmid[wa][wb]);
+}
+
+// context of the incoming entry at depth D (H - 1 - D < 0: the root, INF)
+__device__ __forceinline__ float4 inc_ctx(const Params& p, int64_t ioff, int H, int D) {
+  if (H - 1 - D < 0) return bINF();
+  return __ldg(p.slice_box + __ldg(p.inc + ioff + D).y);
+}
+
+#ifndef FZ_MINB
+#define FZ_MINB 3
+#endif
+template <bool PM>
+__global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockIdx.x;
+  const int64_t base = (int64_t)T * W;
+  const int nvalid = (int)(p.n - base < W ? p.n - base : W);
+  const int gbase = (int)base;  // global indices fit in int32 (n <= 2^31 - 1)
+  const int tl0 = tid * K;      // tile-local index of the thread's first element
+  const int gtb = gbase + tl0;
+  const int sb = (tid << LOGK) | (tid & 7);  // slot(tid, i) = sb ^ i
+
+  // ---- A. loads, register walk -------------------------------------------------
+  const uint4 raw = load_tags16(p.tags, p.n, base + tl0, nvalid == W);
+  const int H = __ldg(p.ctrl.hstart + T);
+  const int aT = __ldg(p.ctrl.agg + T).x;
+  const int64_t ioff = __ldg(p.aoff + T);
+#pragma unroll
+  for (int j = 0; j < K; j++) {
+    const int e = j * NT + tid;
+    s.val[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bEMPTY();
+  }
+  const int nv_t = nvalid - tl0;
+  const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
+  const Walk w = walk(raw, valid);
+  const int a_t = __popc(w.ucm), b_t = __popc(w.S);
+
+  // ---- B. block Bic scan: relative height at the thread start, low-water mark
+  Bic ex, sx, tot;
+  block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, false);
+  const int r_t = ex.b - ex.a;
+  const int l_t = r_t - a_t;
+  for (uint32_t q = w.S; q; q &= q - 1) s.matchS[tl0 + __ffs(q) - 1] = -1;  // closed by another thread / tile
+  int wl[5];
+  lane_windows(l_t, wl);
+#pragma unroll
+  for (int k = 0; k < 5; k++) s.lwin[warp][k][lane] = wl[k];
+  {
+    const int o = __shfl_sync(0xffffffffu, wl[4], 15);
+    if (lane == 31) s.lwmin[warp] = min(wl[4], o);
+  }
+  s.l[tid] = l_t;
+  s.uo[tid] = w.S;
+  __syncthreads();
+
+  // ---- C. thread-level owner lookups (F2); lc of the thread-unmatched opens --
+  const int top_ref = thread_ref<NW, K>(wl, l_t, w.S, r_t - 1, s.lwin, s.lwmin, s.l, s.uo);
+  const int lk = thread_ref<NW, K>(wl, l_t, w.S, l_t - 1, s.lwin, s.lwmin, s.l, s.uo);
+  s.link[tid] = lk;
+  {
+    float4 acc = bINF();
+    for (uint32_t q = w.S; q; q &= q - 1) {
+      const int i = __ffs(q) - 1;
+      float4& v = s.val[sb ^ i];
+      if (!((w.bm >> i) & 1u)) acc = isect(acc, v);
+      v = acc;
+    }
+  }
+  __syncthreads();
+
+  // ---- D. context of each thread's link: TL(t) = lc(link) ∩ TL(thread of link)
+  {
+    float4 acc;
+    int ptr;
+    if (lk >= 0) {
+      acc = s.val[slot_of(lk)];
+      ptr = lk >> LOGK;
+    } else {
+      acc = inc_ctx(p, ioff, H, -lk - 1);
+      ptr = -1;
+    }
+    int cb = 0;
+    s.u.pj.acc[0][tid] = acc;
+    s.u.pj.ptr[0][tid] = ptr;
+    int any = __syncthreads_or(ptr >= 0);
+    while (any) {
+      if (ptr >= 0) {
+        acc = isect(acc, s.u.pj.acc[cb][ptr]);
+        ptr = s.u.pj.ptr[cb][ptr];
+      }
+      s.u.pj.acc[cb ^ 1][tid] = acc;
+      s.u.pj.ptr[cb ^ 1][tid] = ptr;
+      cb ^= 1;
+      any = __syncthreads_or(ptr >= 0);
+    }
+    s.tl[tid] = acc;
+  }
+  __syncthreads();
+
+  // ---- E. the stack at the thread start, depths 0..a_t: global indices
+  //      (parent / match), the partner of each popped in-tile open, and the
+  //      context at each depth where a leaf or open sits (ctx(d) kept in the
+  //      slot of the close c_d that ends depth d; the last one in a register)
+  float4 ctxLast = bINF();
+  uint32_t xcm = 0;  // closes popping an entry of an earlier tile
+  {
+    int ref = top_ref, d = 0, prevc = -1;
+    uint32_t q = w.ucm;
+    const uint32_t needm = w.ext & (w.lm | w.om);
+    for (; d <= a_t && ref >= 0; d++) {
+      const int ci = d < a_t ? __ffs(q) - 1 : K;
+      const uint32_t seg = ((1u << ci) - 1u) & ~((1u << (prevc + 1)) - 1u);  // elements at depth d
+      float4 cx = bINF();
+      if (seg & needm) cx = isect(s.val[slot_of(ref)], s.tl[ref >> LOGK]);
+      s.extv[d][tid] = gbase + ref;
+      if (d < a_t) {
+        s.matchS[ref] = gtb + ci;
+        s.val[sb ^ ci] = cx;
+        q &= q - 1;
+        prevc = ci;
+      } else {
+        ctxLast = cx;
+      }
+      const int V = ref >> LOGK;
+      const uint32_t below = s.uo[V] & ((1u << (ref & (K - 1))) - 1u);
+      ref = below ? (V << LOGK) + 31 - __clz(below) : s.link[V];
+    }
+    // the rest are consecutive entries of the incoming stack (a chain that
+    // leaves the tile never returns into it)
+    for (; d <= a_t; d++, ref--) {
+      const int ci = d < a_t ? __ffs(q) - 1 : K;
+      const uint32_t seg = ((1u << ci) - 1u) & ~((1u << (prevc + 1)) - 1u);  // elements at depth d
+      const int D = -ref - 1;
+      int gi = -1;
+      float4 cx = bINF();
+      if (H - 1 - D >= 0) {
+        const int2 e = __ldg(p.inc + ioff + D);
+        gi = e.x;
+        if (seg & needm) cx = __ldg(p.slice_box + e.y);
+      }
+      s.extv[d][tid] = gi;
+      if (d < a_t) {
+        if (gi >= 0) {
+          xcm |= 1u << ci;
+          p.xc[ioff + D] = gtb + ci;
+        }
+        s.val[sb ^ ci] = cx;
+        q &= q - 1;
+        prevc = ci;
+      } else {
+        ctxLast = cx;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- F. one forward walk: clips (ctx(e) = box ∩ ctx(parent), blend opens
+  //      pass it through, R6/R7), unions of in-thread nodes (an open saves
+  //      the enclosing accumulator in its close's slot), prefix unions at the
+  //      closes of outer nodes, parent / match
+  float4 PT = bEMPTY();
+  {
+    float4 acc = bEMPTY();
+    int d = 0;
+    int curGI = s.extv[0][tid];
+    int pv[4], mv[4];
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      const uint32_t bit = 1u << i;
+      const float4 v = s.val[sb ^ i];
+      const int pn = nib(w.plo, w.phi, i);
+      const bool isx = (w.ext & bit) != 0u;
+      float4 cpar;
+      if (isx) {
+        const uint32_t nc = w.ucm & ~(bit - 1u);
+        cpar = nc ? s.val[sb ^ (__ffs(nc) - 1)] : ctxLast;
+      } else {
+        cpar = s.val[sb ^ pn];
+      }
+      const float4 clipped = isect(v, cpar);
+      const int par = isx ? curGI : gtb + pn;
+      int m = -1;
+      if (w.lm & bit) {
+        s.val[sb ^ i] = clipped;
+        acc = unite(acc, clipped);
+        PT = unite(PT, clipped);
+      } else if (w.om & bit) {
+        s.val[sb ^ i] = (w.bm & bit) ? cpar : clipped;
+        if (w.S & bit) {
+          m = SKIP;
+        } else {
+          const int c = nib(w.mlo, w.mhi, i);
+          s.val[sb ^ c] = acc;
+          m = gtb + c;
+        }
+        acc = bEMPTY();
+      } else if (w.cm & bit) {
+        if (w.ucm & bit) {
+          s.val[sb ^ i] = curGI >= 0 ? PT : bEMPTY();  // R3: unmatched close -> EMPTY
+          m = curGI;
+          d++;
+          curGI = s.extv[d][tid];
+        } else {
+          s.val[sb ^ i] = acc;
+          if ((w.bm >> pn) & 1u) s.val[sb ^ pn] = acc;
+          acc = unite(v, acc);
+          m = gtb + pn;
+        }
+      }
+      pv[i & 3] = par;
+      mv[i & 3] = m;
+      if (PM && (i & 3) == 3) {
+        const int q4 = i >> 2;
+        if (nv_t >= 4 * q4 + 4) {
+          __stcs(reinterpret_cast<int4*>(p.parent + base + tl0) + q4, make_int4(pv[0], pv[1], pv[2], pv[3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            if (4 * q4 + j < nv_t) p.parent[base + tl0 + 4 * q4 + j] = pv[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          if (mv[j] != SKIP) s.matchS[tl0 + 4 * q4 + j] = mv[j];
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- G. thread unions: windows over lanes, suffixes, warp totals ----------
+  {
+    float4 wv = PT, sf = PT;
+    s.u.un.win[0][tid] = wv;
+#pragma unroll
+    for (int k = 1; k <= 5; k++) {
+      const int off = 1 << (k - 1);
+      const float4 a = shfl_up_box(wv, off);
+      if (lane >= off) wv = unite(wv, a);
+      if (k < 5) s.u.un.win[k][tid] = wv;
+      const float4 b = make_float4(__shfl_down_sync(0xffffffffu, sf.x, off), __shfl_down_sync(0xffffffffu, sf.y, off),
+                                   __shfl_down_sync(0xffffffffu, sf.z, off), __shfl_down_sync(0xffffffffu, sf.w, off));
+      if (lane + off < 32) sf = unite(sf, b);
+    }
+    s.u.un.suf[tid] = sf;
+    if (lane == 31) s.wtu[warp] = wv;
+  }
+  __syncthreads();
+  if (tid < NW * NW) {
+    const int x = tid / NW, y = tid % NW;
+    float4 m = bEMPTY();
+    for (int w2 = x + 1; w2 < y; w2++) m = unite(m, s.wtu[w2]);
+    s.wmid[x][y] = m;
+  }
+  __syncthreads();
+
+  // ---- H. opens left open at the thread end, top down with R = union of the
+  //      thread's leaves after them: closed by a later thread of the tile ->
+  //      finish that close (R ∪ the threads between ∪ the closer's prefix);
+  //      otherwise a slice entry: su = R ∪ the threads after.  Closes of
+  //      earlier tiles' nodes: the tile prefix before them (fz_close ends them)
+  if (w.S) {
+    const int first = __ffs(w.S) - 1;
+    float4 R = bEMPTY();
+    int k = b_t - 1;
+    bool have_after = false;
+    float4 after = bEMPTY();
+    for (int i = K - 1; i >= first; i--) {
+      const uint32_t bit = 1u << i;
+      if (w.S & bit) {
+        const int mc = s.matchS[tl0 + i];
+        if (mc >= 0) {
+          const int cl = mc - gbase;
+          float4& cv = s.val[slot_of(cl)];
+          const float4 U = unite(unite(R, range_threads(s, tid + 1, (cl >> LOGK) - 1)), cv);
+          cv = U;
+          if (w.bm & bit) s.val[sb ^ i] = U;
+        } else {
+          if (!have_after) {
+            after = range_threads(s, tid + 1, NT - 1);
+            have_after = true;
+          }
+          p.slice_su[base + l_t + k + aT] = unite(R, after);
+        }
+        k--;
+      } else if (w.lm & bit) {
+        R = unite(R, s.val[sb ^ i]);
+      }
+    }
+  }
+  if (xcm) {
+    const float4 pre = range_threads(s, 0, tid - 1);
+    for (uint32_t q = xcm; q; q &= q - 1) {
+      float4& cv = s.val[sb ^ (__ffs(q) - 1)];
+      cv = unite(cv, pre);
+    }
+  }
+  if (tid == 0) {
+    float4 tu = s.wtu[0];
+#pragma unroll
+    for (int w2 = 1; w2 < NW; w2++) tu = unite(tu, s.wtu[w2]);
+    p.tu[0][T] = tu;
+  }
+  __syncthreads();
+
+  // ---- I. coalesced copy-out -------------------------------------------------
+#pragma unroll
+  for (int j = 0; j < K; j++) {
+    const int e = j * NT + tid;
+    if (e < nvalid) __stcs(p.out + base + e, s.val[slot_of(e)]);
+  }
+  if (PM) {
+    for (int e4 = tid; e4 < W / 4; e4 += NT) {
+      const int e = 4 * e4;
+      if (e + 4 <= nvalid) {
+        __stcs(reinterpret_cast<int4*>(p.match + base) + e4,
+               make_int4(s.matchS[e], s.matchS[e + 1], s.matchS[e + 2], s.matchS[e + 3]));
+      } else {
+        for (int j = 0; j < 4; j++)
+          if (e + j < nvalid) p.match[base + e + j] = s.matchS[e + j];
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// fz_hier: level k of the tile-union hierarchy (one warp per group of 32)
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) fz_hier(Params p, int k, int m /* nodes at level k - 1 */) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if ((g << 5) >= m) return;
+  const int c = (g << 5) + lane;
+  float4 v = c < m ? __ldcg(p.tu[k - 1] + c) : bEMPTY();
+  v = warp_unite_all(v);
+  if (lane == 0) p.tu[k][g] = v;
+}
+
+// union over tiles [a, b] by one warp (a, b warp-uniform)
+__device__ float4 range_tiles(const Params& p, int a, int b) {
+  const int lane = threadIdx.x & 31;
+  float4 acc = bEMPTY();
+  int k = 0;
+  while (a <= b) {
+    const float4* val = p.tu[k];
+    if ((a >> 5) == (b >> 5) || k == LV - 1) {
+      for (int i = a + lane; i <= b; i += 32) acc = unite(acc, __ldcg(val + i));
+      break;
+    }
+    if (a & 31) {
+      const int e = a | 31;
+      const int i = a + lane;
+      if (i <= e) acc = unite(acc, __ldcg(val + i));
+      a = e + 1;
+    }
+    if ((b & 31) != 31) {
+      const int s0 = b & ~31;
+      const int i = s0 + lane;
+      if (i <= b) acc = unite(acc, __ldcg(val + i));
+      b = s0 - 1;
+    }
+    if (a > b) break;
+    a >>= 5;
+    b = ((b + 1) >> 5) - 1;
+    k++;
+  }
+  return warp_unite_all(acc);
+}
+
+// ----------------------------------------------------------------------------
+// fz_close: nodes opened in an earlier tile (one warp per tile)
+// ----------------------------------------------------------------------------
+template <bool PM>
+__global__ void __launch_bounds__(128) fz_close(Params p) {
+  const int lane = threadIdx.x & 31;
+  const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (T >= p.ntiles) return;
+  const int H = __ldg(p.ctrl.hstart + T);
+  const int aT = __ldg(p.ctrl.agg + T).x;
+  const int64_t ioff = __ldg(p.aoff + T);
+  const int npop = min(aT, max(H, 0));  // pops of real entries (depth D < H)
+  int cto = INT_MIN;                    // warp cache: the last tile range resolved
+  float4 cR = bEMPTY();
+  for (int j0 = 0; j0 < npop; j0 += 32) {
+    const int j = j0 + lane;
+    const bool valid = j < npop;
+    int c = 0, o = 0, To = 0;
+    float4 P = bEMPTY(), su = bEMPTY();
+    int kind = 0;
+    if (valid) {
+      const int2 e = __ldg(p.inc + ioff + j);
+      o = e.x;
+      To = e.y >> LOGW;
+      c = __ldg(p.xc + ioff + j);
+      P = __ldcg(p.out + c);
+      su = __ldg(p.slice_su + e.y);
+      kind = __ldg(p.slice_idx + e.y) < 0;
+    }
+    float4 R = bEMPTY();
+    bool pending = valid && To < T - 1;
+    if (pending && To == cto) {
+      R = cR;
+      pending = false;
+    }
+    uint32_t mask;
+    while ((mask = __ballot_sync(0xffffffffu, pending)) != 0u) {
+      const int tl = __shfl_sync(0xffffffffu, To, __ffs(mask) - 1);
+      const float4 Rl = range_tiles(p, tl + 1, T - 1);
+      if (pending && To == tl) {
+        R = Rl;
+        pending = false;
+      }
+      cto = tl;
+      cR = Rl;
+    }
+    if (valid) {
+      const float4 U = unite(unite(P, su), R);
+      p.out[c] = U;
+      if (kind) p.out[o] = U;
+      if (PM) p.match[o] = c;
+    }
+  }
+  // blend opens never closed (R4): the tile's slice entries that survive to
+  // the end of the stream (F1: its bottom min(b_T, smin_T - L_T))
+  const int bT = __ldg(p.ctrl.agg + T).y;
+  const int L = (int)__ldg(p.ctrl.lw + T) - 1;
+  const int sm = __ldg(p.ctrl.smin + T);
+  const int surv = min(bT, sm == INT_MAX ? bT : max(sm - L, 0));
+  if (surv > 0) {
+    bool anyb = false;
+    for (int k = lane; k < surv; k += 32) anyb |= __ldg(p.slice_idx + (int64_t)T * W + k) < 0;
+    if (__any_sync(0xffffffffu, anyb)) {
+      const float4 after = T + 1 < p.ntiles ? range_tiles(p, T + 1, p.ntiles - 1) : bEMPTY();
+      for (int k = lane; k < surv; k += 32) {
+        const int64_t ref = (int64_t)T * W + k;
+        const int si = __ldg(p.slice_idx + ref);
+        if (si < 0) p.out[si & 0x7fffffff] = unite(__ldg(p.slice_su + ref), after);
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+static int ctrl_blocks() {  // co-resident CTAs of the cooperative kernel
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fz_ctrl, 256, 0);
+  return sms * (occ > 0 ? occ : 1);
+}
+
+static cudaError_t setup() {
+  if (once_per_device(3)) {
+    cudaError_t e = cudaFuncSetAttribute(fz_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fz_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace fz
+
+size_t fused_workspace_bytes(int64_t n) { return n > 0 ? fz::Layout(n).bytes : 0; }
+int fused_tile_elems() { return fz::W; }
+
+cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, int32_t* match, int32_t* parent,
+                         float* node_bbox, void* ws, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t e = fz::setup();
+  if (e != cudaSuccess) return e;
+  const bool pm = match != nullptr;
+  fz::Params p = fz::make_params(tags, leaf_bbox, n, match, parent, node_bbox, ws);
+  const int nt = p.ntiles;
+  TB_LAUNCH(stream, "fz_reduce", (fz::fz_reduce<<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = tile_scan_launch(p.ctrl, nt, 0, 0, stream, p.aoff);
+  if (e != cudaSuccess) return e;
+  {
+    const int blocks = std::max(1, std::min((nt + 7) / 8, fz::ctrl_blocks()));
+    void* args[] = {(void*)&p};
+    void* tok;
+    prof_begin(stream, "fz_ctrl", &tok);
+    e = cudaLaunchCooperativeKernel((const void*)fz::fz_ctrl, dim3(blocks), dim3(256), args, 0, stream);
+    prof_end(stream, tok);
+    if (e != cudaSuccess) return e;
+  }
+  if (pm)
+    TB_LAUNCH(stream, "fz_main", (fz::fz_main<true><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p)));
+  else
+    TB_LAUNCH(stream, "fz_main", (fz::fz_main<false><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p)));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int m = nt;
+  for (int k = 1; k < fz::LV && m > 1; k++) {
+    const int groups = (m + 31) / 32;
+    TB_LAUNCH(stream, "fz_hier", (fz::fz_hier<<<(unsigned)((groups + 7) / 8), 256, 0, stream>>>(p, k, m)));
+    m = groups;
+  }
+  if (pm)
+    TB_LAUNCH(stream, "fz_close", (fz::fz_close<true><<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
+  else
+    TB_LAUNCH(stream, "fz_close", (fz::fz_close<false><<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
+  return cudaGetLastError();
+}
+
+}  // namespace tb

@@ -33,7 +33,9 @@ void prof_end(cudaStream_t s, void* token);
   } while (0)
 
 struct Ctrl;
-cudaError_t tile_scan_launch(const Ctrl& c, int64_t ntiles, int init_a, int init_h, cudaStream_t stream);
+// apre (optional, int64[ntiles + 1]): exclusive prefix sums of (a_T + 1), total last
+cudaError_t tile_scan_launch(const Ctrl& c, int64_t ntiles, int init_a, int init_h, cudaStream_t stream,
+                             int64_t* apre = nullptr);
 
 size_t pm_workspace_bytes(int64_t n);
 size_t pm_ctrl_bytes(int64_t n);
@@ -64,7 +66,14 @@ struct ShardOpen {
   int idx, pad0, pad1, pad2;
 };
 
-// tree_bbox from matching (tree_bbox_m.cu): the single-device path
+// paren_match + tree_bbox in one tile pass (fused.cu): the single-device path.
+// match / parent may be null (tree_bbox alone: only node_bbox is written).
+size_t fused_workspace_bytes(int64_t n);
+int fused_tile_elems();
+cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, int32_t* match, int32_t* parent,
+                         float* node_bbox, void* ws, cudaStream_t stream);
+
+// tree_bbox from matching (tree_bbox_m.cu)
 size_t bbm_workspace_bytes(int64_t n);
 int bbm_tile_elems();
 cudaError_t bbm_launch(const uint8_t* tags, const float* leaf_bbox, const int32_t* match, const int32_t* parent,

@@ -24,23 +24,34 @@ __device__ __forceinline__ Bic warp_incl_scan(Bic v, int lane) {
   return v;
 }
 
-__global__ void __launch_bounds__(NT) tile_scan(Ctrl c, int ntiles, Bic init) {
+__global__ void __launch_bounds__(NT) tile_scan(Ctrl c, int ntiles, Bic init, int64_t* apre) {
   __shared__ Bic wt[NW];
   __shared__ int wmin[NW];
+  __shared__ long long wsum[NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int span = ((ntiles + NW - 1) / NW + 31) & ~31;
   const int t0 = warp * span, t1 = min(t0 + span, ntiles);
   // pass A: total of this warp's range
   Bic carry{0, 0};
+  long long asum = 0;  // sum of (a_T + 1) over the warp's range (apre)
   for (int t = t0; t < t1; t += 32) {
     const int i = t + lane;
     const int2 g = i < t1 ? __ldcg(c.agg + i) : make_int2(0, 0);
     const Bic x = warp_incl_scan(Bic{g.x, g.y}, lane);
     const Bic last{__shfl_sync(0xffffffffu, x.a, 31), __shfl_sync(0xffffffffu, x.b, 31)};
     carry = bic_combine(carry, last);
+    if (apre) asum += __reduce_add_sync(0xffffffffu, i < t1 ? (unsigned)(g.x + 1) : 0u);
   }
-  if (lane == 0) wt[warp] = carry;
+  if (lane == 0) {
+    wt[warp] = carry;
+    wsum[warp] = asum;
+  }
   __syncthreads();
+  long long abase = 0;
+  if (apre) {
+    for (int w = 0; w < warp; w++) abase += wsum[w];
+    if (warp == NW - 1 && lane == 0) apre[ntiles] = abase + asum;
+  }
   Bic pre = init;
   for (int w = 0; w < warp; w++) pre = bic_combine(pre, wt[w]);
   if (warp == NW - 1 && lane == 0) {
@@ -57,6 +68,18 @@ __global__ void __launch_bounds__(NT) tile_scan(Ctrl c, int ntiles, Bic init) {
     Bic ex{__shfl_up_sync(0xffffffffu, x.a, 1), __shfl_up_sync(0xffffffffu, x.b, 1)};
     if (lane == 0) ex = Bic{0, 0};
     const Bic e = bic_combine(pre, ex);
+    if (apre) {
+      // exclusive prefix of (a_T + 1): offset of tile i's incoming list
+      int v = i < t1 ? g.x + 1 : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) v += y;
+      }
+      const int own = i < t1 ? g.x + 1 : 0;
+      if (i < t1) apre[i] = abase + (v - own);
+      abase += __shfl_sync(0xffffffffu, v, 31);
+    }
     if (i < t1) {
       c.hstart[i] = e.b;
       c.lw[i] = (uint32_t)max(e.b - g.x, 0) + 1u;
@@ -103,9 +126,11 @@ __global__ void __launch_bounds__(NT) tile_scan(Ctrl c, int ntiles, Bic init) {
 
 }  // namespace ts
 
-cudaError_t tile_scan_launch(const Ctrl& c, int64_t ntiles, int init_a, int init_h, cudaStream_t stream) {
+cudaError_t tile_scan_launch(const Ctrl& c, int64_t ntiles, int init_a, int init_h, cudaStream_t stream,
+                             int64_t* apre) {
   if (ntiles <= 0) return cudaSuccess;
-  TB_LAUNCH(stream, "tile_scan", (ts::tile_scan<<<1, ts::NT, 0, stream>>>(c, (int)ntiles, Bic{init_a, init_h})));
+  TB_LAUNCH(stream, "tile_scan",
+            (ts::tile_scan<<<1, ts::NT, 0, stream>>>(c, (int)ntiles, Bic{init_a, init_h}, apre)));
   return cudaGetLastError();
 }
 
