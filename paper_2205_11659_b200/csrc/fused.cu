@@ -49,7 +49,6 @@ constexpr int NW = NT / 32;
 constexpr int W = NT * K;      // tile = 2048 elements
 constexpr int LOGW = 11;
 constexpr int LV = 5;          // 32-ary levels of tile unions: 32^5 tiles > 2^31 / W
-constexpr int SKIP = INT_MIN;  // match slot written by another thread / kernel
 static_assert(W == (1 << LOGW) && K == (1 << LOGK), "tile shape");
 
 struct Params {
@@ -395,51 +394,45 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   return w;
 }
 
+constexpr int LT = 7;    // levels of the sparse table over threads: windows of 1 .. 64 threads
+constexpr int RCAP = 8;  // segment unions kept per thread (more unmatched opens: recomputed in H)
+static_assert((1 << LT) >= NT, "sparse table covers the tile");
+
 struct Smem {
-  float4 val[W];      // boxes -> lc / contexts / clips / unions (swizzled slots)
-  int32_t matchS[W];  // match values (global indices), copied out coalesced
+  float4 val[W + NT];               // boxes -> lc / contexts / clips / unions (swizzled slots); val[W + t] = TL(t)
+  int32_t matchS[W + W / K];        // match values (global indices), padded: element e at e + e / K
   union {
     struct {
-      float4 acc[2][NT];
-      int ptr[2][NT];
-    } pj;             // thread link contexts by pointer jumping
+      int lwin[NW][5][32];          // low-water windows (thread owner lookups)
+      int lwmin[NW];
+    } ref;
     struct {
-      float4 win[5][NT];  // union of thread unions over lanes [lane - 2^k + 1, lane] (within the warp)
-      float4 suf[NT];     // inclusive suffix within the warp
-    } un;
+      float4 acc[2][NT];            // thread link contexts by pointer jumping
+      int ptr[2][NT];
+    } pj;
+    float4 st[LT][NT];              // st[k][t] = union of the clipped leaves of threads [t, t + 2^k)
   } u;
-  int32_t extv[K + 1][NT];  // global index of the entry at depth d of the thread's start stack (-1: root)
-  float4 tl[NT];            // context of each thread's link
-  int lwin[NW][5][32];      // low-water windows (thread owner lookups)
-  int lwmin[NW];
+  struct {
+    float4 rbuf[RCAP][NT];  // F-H: the accumulator at each thread-unmatched open (k < RCAP)
+  } u2;
   int l[NT];
   uint32_t uo[NT];
   int link[NT];
-  float4 wtu[NW];
-  float4 wmid[NW][NW];
   Bic wtot[NW];
 };
 
 // element i of thread t lives at slot (t*K | t & 7) ^ i: conflict-free for the
 // per-thread accesses (8 lanes, distinct t & 7) and for the coalesced copies
 __device__ __forceinline__ int slot_of(int e) { return e ^ (int)(((unsigned)e >> LOGK) & 7u); }
+__device__ __forceinline__ int mpad(int e) { return e + (int)((unsigned)e >> LOGK); }
 
-// union of the clipped leaves of whole threads [a, b] (F4)
+// union of the clipped leaves of whole threads [a, b] (F4): two overlapping
+// windows of the sparse table (min/max are idempotent)
 __device__ __forceinline__ float4 range_threads(const Smem& s, int a, int b) {
-  if (a > b) return bEMPTY();
-  const int wa = a >> 5, wb = b >> 5;
-  const int a2 = (wa == wb) ? a : (wb << 5);
-  const int len = b - a2 + 1;
-  const int k = min(31 - __clz(len), 4);
-  const float4 right = (len == 32) ? s.wtu[wb] : unite(s.u.un.win[k][b], s.u.un.win[k][a2 + (1 << k) - 1]);
-  if (wa == wb) return right;
-  return unite(unite(s.u.un.suf[a], right), s.wmid[wa][wb]);
-}
-
-// context of the incoming entry at depth D (H - 1 - D < 0: the root, INF)
-__device__ __forceinline__ float4 inc_ctx(const Params& p, int64_t ioff, int H, int D) {
-  if (H - 1 - D < 0) return bINF();
-  return __ldg(p.slice_box + __ldg(p.inc + ioff + D).y);
+  const int len = b - a + 1;
+  if (len <= 0) return bEMPTY();
+  const int k = min(31 - __clz(len), LT - 1);
+  return unite(s.u.st[k][a], s.u.st[k][b - (1 << k) + 1]);
 }
 
 #ifndef FZ_MINB
@@ -457,6 +450,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   const int tl0 = tid * K;      // tile-local index of the thread's first element
   const int gtb = gbase + tl0;
   const int sb = (tid << LOGK) | (tid & 7);  // slot(tid, i) = sb ^ i
+  const int mb = mpad(tl0);                  // matchS index of element i = mb + i
 
   // ---- A. loads, register walk -------------------------------------------------
   const uint4 raw = load_tags16(p.tags, p.n, base + tl0, nvalid == W);
@@ -478,22 +472,22 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, false);
   const int r_t = ex.b - ex.a;
   const int l_t = r_t - a_t;
-  for (uint32_t q = w.S; q; q &= q - 1) s.matchS[tl0 + __ffs(q) - 1] = -1;  // closed by another thread / tile
+  for (uint32_t q = w.S; q; q &= q - 1) s.matchS[mb + __ffs(q) - 1] = -1;  // closed by another thread / tile
   int wl[5];
   lane_windows(l_t, wl);
 #pragma unroll
-  for (int k = 0; k < 5; k++) s.lwin[warp][k][lane] = wl[k];
+  for (int k = 0; k < 5; k++) s.u.ref.lwin[warp][k][lane] = wl[k];
   {
     const int o = __shfl_sync(0xffffffffu, wl[4], 15);
-    if (lane == 31) s.lwmin[warp] = min(wl[4], o);
+    if (lane == 31) s.u.ref.lwmin[warp] = min(wl[4], o);
   }
   s.l[tid] = l_t;
   s.uo[tid] = w.S;
   __syncthreads();
 
   // ---- C. thread-level owner lookups (F2); lc of the thread-unmatched opens --
-  const int top_ref = thread_ref<NW, K>(wl, l_t, w.S, r_t - 1, s.lwin, s.lwmin, s.l, s.uo);
-  const int lk = thread_ref<NW, K>(wl, l_t, w.S, l_t - 1, s.lwin, s.lwmin, s.l, s.uo);
+  const int top_ref = thread_ref<NW, K>(wl, l_t, w.S, r_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.l, s.uo);
+  const int lk = thread_ref<NW, K>(wl, l_t, w.S, l_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.l, s.uo);
   s.link[tid] = lk;
   {
     float4 acc = bINF();
@@ -507,15 +501,23 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   __syncthreads();
 
   // ---- D. context of each thread's link: TL(t) = lc(link) ∩ TL(thread of link)
+  //      (pointer jumping over threads); the link's global index
+  int giLast;
   {
-    float4 acc;
-    int ptr;
+    float4 acc = bINF();
+    int ptr = -1;
     if (lk >= 0) {
       acc = s.val[slot_of(lk)];
       ptr = lk >> LOGK;
+      giLast = gbase + lk;
     } else {
-      acc = inc_ctx(p, ioff, H, -lk - 1);
-      ptr = -1;
+      const int D = -lk - 1;
+      giLast = -1;
+      if (H - 1 - D >= 0) {
+        const int2 e = __ldg(p.inc + ioff + D);
+        giLast = e.x;
+        acc = __ldg(p.slice_box + e.y);
+      }
     }
     int cb = 0;
     s.u.pj.acc[0][tid] = acc;
@@ -531,162 +533,131 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       cb ^= 1;
       any = __syncthreads_or(ptr >= 0);
     }
-    s.tl[tid] = acc;
+    s.val[W + tid] = acc;
   }
   __syncthreads();
 
-  // ---- E. the stack at the thread start, depths 0..a_t: global indices
-  //      (parent / match), the partner of each popped in-tile open, and the
-  //      context at each depth where a leaf or open sits (ctx(d) kept in the
-  //      slot of the close c_d that ends depth d; the last one in a register)
-  float4 ctxLast = bINF();
+  // ---- E. entries popped by this thread's unmatched closes c_0 .. c_{a_t - 1}
+  //      (c_d pops the entry at depth d of the thread's start stack): c_d's
+  //      match (= its parent and that of the elements before it at depth d) in
+  //      matchS[c_d]; the partner of a popped in-tile open; the context at
+  //      depth d where a leaf or open sits there, in c_d's slot (depth a_t:
+  //      the link, TL(t))
   uint32_t xcm = 0;  // closes popping an entry of an earlier tile
   {
     int ref = top_ref, d = 0, prevc = -1;
     uint32_t q = w.ucm;
     const uint32_t needm = w.ext & (w.lm | w.om);
-    for (; d <= a_t && ref >= 0; d++) {
-      const int ci = d < a_t ? __ffs(q) - 1 : K;
+    for (; d < a_t && ref >= 0; d++) {
+      const int ci = __ffs(q) - 1;
+      q &= q - 1;
       const uint32_t seg = ((1u << ci) - 1u) & ~((1u << (prevc + 1)) - 1u);  // elements at depth d
-      float4 cx = bINF();
-      if (seg & needm) cx = isect(s.val[slot_of(ref)], s.tl[ref >> LOGK]);
-      s.extv[d][tid] = gbase + ref;
-      if (d < a_t) {
-        s.matchS[ref] = gtb + ci;
-        s.val[sb ^ ci] = cx;
-        q &= q - 1;
-        prevc = ci;
-      } else {
-        ctxLast = cx;
-      }
+      prevc = ci;
+      s.matchS[mb + ci] = gbase + ref;
+      s.matchS[mpad(ref)] = gtb + ci;
+      if (seg & needm) s.val[sb ^ ci] = isect(s.val[slot_of(ref)], s.val[W + (ref >> LOGK)]);
       const int V = ref >> LOGK;
       const uint32_t below = s.uo[V] & ((1u << (ref & (K - 1))) - 1u);
       ref = below ? (V << LOGK) + 31 - __clz(below) : s.link[V];
     }
     // the rest are consecutive entries of the incoming stack (a chain that
     // leaves the tile never returns into it)
-    for (; d <= a_t; d++, ref--) {
-      const int ci = d < a_t ? __ffs(q) - 1 : K;
-      const uint32_t seg = ((1u << ci) - 1u) & ~((1u << (prevc + 1)) - 1u);  // elements at depth d
+    for (; d < a_t; d++, ref--) {
+      const int ci = __ffs(q) - 1;
+      q &= q - 1;
+      const uint32_t seg = ((1u << ci) - 1u) & ~((1u << (prevc + 1)) - 1u);
+      prevc = ci;
       const int D = -ref - 1;
       int gi = -1;
       float4 cx = bINF();
       if (H - 1 - D >= 0) {
         const int2 e = __ldg(p.inc + ioff + D);
         gi = e.x;
+        xcm |= 1u << ci;
+        p.xc[ioff + D] = gtb + ci;
         if (seg & needm) cx = __ldg(p.slice_box + e.y);
       }
-      s.extv[d][tid] = gi;
-      if (d < a_t) {
-        if (gi >= 0) {
-          xcm |= 1u << ci;
-          p.xc[ioff + D] = gtb + ci;
-        }
-        s.val[sb ^ ci] = cx;
-        q &= q - 1;
-        prevc = ci;
-      } else {
-        ctxLast = cx;
-      }
+      s.matchS[mb + ci] = gi;
+      if (seg & needm) s.val[sb ^ ci] = cx;
     }
   }
   __syncthreads();
 
   // ---- F. one forward walk: clips (ctx(e) = box ∩ ctx(parent), blend opens
-  //      pass it through, R6/R7), unions of in-thread nodes (an open saves
-  //      the enclosing accumulator in its close's slot), prefix unions at the
-  //      closes of outer nodes, parent / match
-  float4 PT = bEMPTY();
+  //      pass it through, R6/R7), unions of in-thread nodes (an open saves the
+  //      enclosing accumulator -- in its close's slot when the close is in the
+  //      thread, else in rbuf -- and restarts it), parent / match.  By the Bic
+  //      normal form all of a thread's unmatched closes precede its unmatched
+  //      opens and the thread stack is empty at them, so there the
+  //      accumulator holds the thread's prefix union.
+  float4 acc = bEMPTY();
   {
-    float4 acc = bEMPTY();
-    int d = 0;
-    int curGI = s.extv[0][tid];
-    int pv[4], mv[4];
+    int pv[4];
 #pragma unroll
     for (int i = 0; i < K; i++) {
       const uint32_t bit = 1u << i;
       const float4 v = s.val[sb ^ i];
       const int pn = nib(w.plo, w.phi, i);
+      const int pt = nib(w.mlo, w.mhi, i);
       const bool isx = (w.ext & bit) != 0u;
-      float4 cpar;
-      if (isx) {
-        const uint32_t nc = w.ucm & ~(bit - 1u);
-        cpar = nc ? s.val[sb ^ (__ffs(nc) - 1)] : ctxLast;
-      } else {
-        cpar = s.val[sb ^ pn];
-      }
+      const uint32_t nc = w.ucm & ~(bit - 1u);  // unmatched closes at or after i
+      const int j = __ffs(nc) - 1;             // the next one: c_d of element i's depth d
+      const int cidx = isx ? (nc ? (sb ^ j) : W + tid) : (sb ^ pn);
+      const float4 cpar = s.val[cidx];
+      const int mj = s.matchS[mb + max(j, 0)];
+      const int par = isx ? (nc ? mj : giLast) : gtb + pn;
       const float4 clipped = isect(v, cpar);
-      const int par = isx ? curGI : gtb + pn;
-      int m = -1;
-      if (w.lm & bit) {
-        s.val[sb ^ i] = clipped;
-        acc = unite(acc, clipped);
-        PT = unite(PT, clipped);
-      } else if (w.om & bit) {
-        s.val[sb ^ i] = (w.bm & bit) ? cpar : clipped;
-        if (w.S & bit) {
-          m = SKIP;
-        } else {
-          const int c = nib(w.mlo, w.mhi, i);
-          s.val[sb ^ c] = acc;
-          m = gtb + c;
-        }
-        acc = bEMPTY();
-      } else if (w.cm & bit) {
-        if (w.ucm & bit) {
-          s.val[sb ^ i] = curGI >= 0 ? PT : bEMPTY();  // R3: unmatched close -> EMPTY
-          m = curGI;
-          d++;
-          curGI = s.extv[d][tid];
-        } else {
-          s.val[sb ^ i] = acc;
-          if ((w.bm >> pn) & 1u) s.val[sb ^ pn] = acc;
-          acc = unite(v, acc);
-          m = gtb + pn;
-        }
+      const bool isL = (w.lm & bit) != 0u, isB = (w.bm & bit) != 0u;
+      const bool isO = (w.om & bit) != 0u, isC = (w.cm & bit) != 0u, isU = (w.ucm & bit) != 0u;
+      const bool isUO = (w.S & bit) != 0u;
+      const bool isMC = isC && !isU;
+      // own slot: leaf / clip open -> clipped; blend open -> parent context;
+      // close -> union (in-thread node) / prefix (outer node) / EMPTY (R3)
+      float4 o = isB ? cpar : clipped;
+      o = isC ? ((isU && par < 0) ? bEMPTY() : acc) : o;
+      s.val[sb ^ i] = o;
+      if (isO) {
+        const int k = __popc(w.S & (bit - 1u));
+        if (!isUO) s.val[sb ^ pt] = acc;
+        else if (k < RCAP) s.u2.rbuf[k][tid] = acc;
       }
+      if (isMC && ((w.bm >> pn) & 1u)) s.val[sb ^ pn] = acc;
+      const float4 add = isL ? clipped : (isMC ? v : bEMPTY());
+      acc = unite(acc, add);
+      acc = isO ? bEMPTY() : acc;
+      if (PM && !(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + (isO ? pt : pn);
       pv[i & 3] = par;
-      mv[i & 3] = m;
       if (PM && (i & 3) == 3) {
         const int q4 = i >> 2;
         if (nv_t >= 4 * q4 + 4) {
           __stcs(reinterpret_cast<int4*>(p.parent + base + tl0) + q4, make_int4(pv[0], pv[1], pv[2], pv[3]));
         } else {
 #pragma unroll
-          for (int j = 0; j < 4; j++)
-            if (4 * q4 + j < nv_t) p.parent[base + tl0 + 4 * q4 + j] = pv[j];
+          for (int jj = 0; jj < 4; jj++)
+            if (4 * q4 + jj < nv_t) p.parent[base + tl0 + 4 * q4 + jj] = pv[jj];
         }
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-          if (mv[j] != SKIP) s.matchS[tl0 + 4 * q4 + j] = mv[j];
       }
     }
   }
-  __syncthreads();
-
-  // ---- G. thread unions: windows over lanes, suffixes, warp totals ----------
+  // the thread's union: the prefix at its first unmatched open ∪ the segments
+  const bool ovf = b_t > RCAP;
   {
-    float4 wv = PT, sf = PT;
-    s.u.un.win[0][tid] = wv;
+    float4 tu = acc;
+    if (!ovf) {
+      for (int k = 0; k < b_t; k++) tu = unite(tu, s.u2.rbuf[k][tid]);
+    } else {
 #pragma unroll
-    for (int k = 1; k <= 5; k++) {
-      const int off = 1 << (k - 1);
-      const float4 a = shfl_up_box(wv, off);
-      if (lane >= off) wv = unite(wv, a);
-      if (k < 5) s.u.un.win[k][tid] = wv;
-      const float4 b = make_float4(__shfl_down_sync(0xffffffffu, sf.x, off), __shfl_down_sync(0xffffffffu, sf.y, off),
-                                   __shfl_down_sync(0xffffffffu, sf.z, off), __shfl_down_sync(0xffffffffu, sf.w, off));
-      if (lane + off < 32) sf = unite(sf, b);
+      for (int i = 0; i < K; i++)
+        if ((w.lm >> i) & 1u) tu = unite(tu, s.val[sb ^ i]);
     }
-    s.u.un.suf[tid] = sf;
-    if (lane == 31) s.wtu[warp] = wv;
+    s.u.st[0][tid] = tu;
   }
-  __syncthreads();
-  if (tid < NW * NW) {
-    const int x = tid / NW, y = tid % NW;
-    float4 m = bEMPTY();
-    for (int w2 = x + 1; w2 < y; w2++) m = unite(m, s.wtu[w2]);
-    s.wmid[x][y] = m;
+
+  // ---- G. sparse table of thread unions ------------------------------------
+#pragma unroll
+  for (int k = 1; k < LT; k++) {
+    __syncthreads();
+    s.u.st[k][tid] = unite(s.u.st[k - 1][tid], s.u.st[k - 1][min(tid + (1 << (k - 1)), NT - 1)]);
   }
   __syncthreads();
 
@@ -696,31 +667,39 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   //      otherwise a slice entry: su = R ∪ the threads after.  Closes of
   //      earlier tiles' nodes: the tile prefix before them (fz_close ends them)
   if (w.S) {
-    const int first = __ffs(w.S) - 1;
-    float4 R = bEMPTY();
-    int k = b_t - 1;
-    bool have_after = false;
-    float4 after = bEMPTY();
-    for (int i = K - 1; i >= first; i--) {
-      const uint32_t bit = 1u << i;
-      if (w.S & bit) {
-        const int mc = s.matchS[tl0 + i];
-        if (mc >= 0) {
-          const int cl = mc - gbase;
-          float4& cv = s.val[slot_of(cl)];
-          const float4 U = unite(unite(R, range_threads(s, tid + 1, (cl >> LOGK) - 1)), cv);
-          cv = U;
-          if (w.bm & bit) s.val[sb ^ i] = U;
-        } else {
-          if (!have_after) {
-            after = range_threads(s, tid + 1, NT - 1);
-            have_after = true;
-          }
-          p.slice_su[base + l_t + k + aT] = unite(R, after);
+    const float4 after = range_threads(s, tid + 1, NT - 1);
+    auto handle = [&](int i, int k, const float4& R) {
+      const int mc = s.matchS[mb + i];
+      if (mc >= 0) {
+        const int cl = mc - gbase;
+        float4& cv = s.val[slot_of(cl)];
+        const float4 U = unite(unite(R, range_threads(s, tid + 1, (cl >> LOGK) - 1)), cv);
+        cv = U;
+        if ((w.bm >> i) & 1u) s.val[sb ^ i] = U;
+      } else {
+        p.slice_su[base + l_t + k + aT] = unite(R, after);
+      }
+    };
+    if (!ovf) {
+      float4 R = acc;  // segment after the top open
+      uint32_t q = w.S;
+      for (int k = b_t - 1; k >= 0; k--) {
+        const int i = 31 - __clz(q);
+        q ^= 1u << i;
+        handle(i, k, R);
+        R = unite(R, s.u2.rbuf[k][tid]);
+      }
+    } else {
+      float4 R = bEMPTY();
+      int k = b_t - 1;
+      for (int i = K - 1; i >= 0; i--) {
+        const uint32_t bit = 1u << i;
+        if (w.S & bit) {
+          handle(i, k, R);
+          k--;
+        } else if (w.lm & bit) {
+          R = unite(R, s.val[sb ^ i]);
         }
-        k--;
-      } else if (w.lm & bit) {
-        R = unite(R, s.val[sb ^ i]);
       }
     }
   }
@@ -731,12 +710,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       cv = unite(cv, pre);
     }
   }
-  if (tid == 0) {
-    float4 tu = s.wtu[0];
-#pragma unroll
-    for (int w2 = 1; w2 < NW; w2++) tu = unite(tu, s.wtu[w2]);
-    p.tu[0][T] = tu;
-  }
+  if (tid == 0) p.tu[0][T] = range_threads(s, 0, NT - 1);
   __syncthreads();
 
   // ---- I. coalesced copy-out -------------------------------------------------
@@ -746,14 +720,17 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
     if (e < nvalid) __stcs(p.out + base + e, s.val[slot_of(e)]);
   }
   if (PM) {
-    for (int e4 = tid; e4 < W / 4; e4 += NT) {
-      const int e = 4 * e4;
+#pragma unroll
+    for (int j = 0; j < W / 4 / NT; j++) {
+      const int e = 4 * (j * NT + tid);
+      const int pe = mpad(e);
+      const int4 v4 = make_int4(s.matchS[pe], s.matchS[pe + 1], s.matchS[pe + 2], s.matchS[pe + 3]);
       if (e + 4 <= nvalid) {
-        __stcs(reinterpret_cast<int4*>(p.match + base) + e4,
-               make_int4(s.matchS[e], s.matchS[e + 1], s.matchS[e + 2], s.matchS[e + 3]));
+        __stcs(reinterpret_cast<int4*>(p.match + base + e), v4);
       } else {
-        for (int j = 0; j < 4; j++)
-          if (e + j < nvalid) p.match[base + e + j] = s.matchS[e + j];
+        if (e < nvalid) p.match[base + e] = v4.x;
+        if (e + 1 < nvalid) p.match[base + e + 1] = v4.y;
+        if (e + 2 < nvalid) p.match[base + e + 2] = v4.z;
       }
     }
   }

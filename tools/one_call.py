@@ -14,6 +14,10 @@ n = tags.numel()
 if a.op == "pm":
     m = torch.empty(n, dtype=torch.int32, device="cuda"); p = torch.empty_like(m)
     for _ in range(a.reps): tb.paren_match(tags, m, p)
+elif a.op == "pair":
+    boxes = scenegen.boxes(n, 7, tags, device="cuda"); out = torch.empty_like(boxes)
+    m = torch.empty(n, dtype=torch.int32, device="cuda"); p = torch.empty_like(m)
+    for _ in range(a.reps): tb.paren_match_tree_bbox(tags, boxes, m, p, out)
 else:
     boxes = scenegen.boxes(n, 7, tags, device="cuda"); out = torch.empty_like(boxes)
     for _ in range(a.reps): tb.tree_bbox(tags, boxes, out)
