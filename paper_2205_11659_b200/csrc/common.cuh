@@ -91,7 +91,7 @@ __device__ __forceinline__ int select_bit(uint32_t m, int j) {
 // or more already matches every open of the nibble).  Index = o | c << 4 | pin << 8.
 // ---------------------------------------------------------------------------
 constexpr int UNM4_ENTRIES = 256 * 5;
-__device__ __forceinline__ uint8_t unm4_entry(int idx) {
+__host__ __device__ __forceinline__ uint8_t unm4_entry(int idx) {
   const int o = idx & 15, c = (idx >> 4) & 15, pin = idx >> 8;
   int P = pin, mask = 0;
   for (int j = 3; j >= 0; j--) {

@@ -60,37 +60,47 @@ struct Params {
   int32_t* parent;     // may be null
   float4* out;
   Ctrl ctrl;
-  int64_t* aoff;       // [ntiles + 1] exclusive prefix of (a_T + 1)
+  int64_t* aoff;       // [ntiles + 1] exclusive prefix of a_T (pop records); incoming list of T at aoff[T] + T
   int32_t* slice_idx;  // [ntiles * W] global index | blend << 31
-  float4* slice_box;   // [ntiles * W] lc (fz_reduce), then the true context (fz_ctrl)
+  float4* slice_box;   // [ntiles * W] lc: ∩ of the clip boxes of the slice entries at and below (fz_reduce)
   float4* slice_su;    // [ntiles * W] union of the tile's clipped leaves after the entry (fz_main)
-  int2* inc;           // [aoff[ntiles]] incoming entry at depth D: (global index, slice ref), (-1, -1) = root
-  int32_t* xc;         // [aoff[ntiles]] the close that pops incoming depth D (non-root pops only)
+  int4* pop;           // [aoff[ntiles]] close popping incoming depth D: (close, open, slice ref, blend); root: close -1
+  float4* popu;        // [aoff[ntiles]] the tile's union before that close
   float4* tu[LV];      // tile unions, 32-ary hierarchy
   float4* pj_acc;      // [2 * ntiles] pointer jumping over tiles
   int32_t* pj_ptr;     // [2 * ntiles]
-  int32_t* flag;       // [2]
+  int32_t* pj_own;     // [ntiles] link owner: the tile that pushed the entry just below the tile's slice (-1: root)
+  int2* runs;          // [ntiles * RMAX] the tile's incoming stack by owner: (owner U, L_U), heights [L_U, previous L)
+  int32_t* nruns;      // [ntiles] number of runs covering the a_T + 1 top entries (may exceed RMAX)
+  float4* tc;          // [ntiles] TC(T) = context of that entry
+  int32_t* flag;       // [3]
+  int4* blk;           // [gridDim of fz_ctrl] block aggregates (a, b, sum lo, sum hi)
+  int32_t* blkmin;     // [gridDim of fz_ctrl] min low-water mark of the block's tiles
+  int chunk;           // fz_ctrl: tiles per block (multiple of 32)
+  uint64_t* trace;     // optional (debug): fz_ctrl phase timestamps, block 0
 };
+constexpr int MAXCTRL = 4096;  // fz_ctrl blocks (co-resident CTAs) provided for
+constexpr int RMAX = 8;        // runs of the incoming stack kept per tile (more: followed in fz_main)
 
 // ----------------------------------------------------------------------------
 // workspace
 // ----------------------------------------------------------------------------
 struct Layout {
-  size_t ctrl, aoff, sidx, sbox, ssu, inc, xc, tu[LV], pja, pjp, flag, bytes;
+  size_t ctrl, aoff, sidx, sbox, ssu, pop, popu, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, bytes;
   int64_t ntiles;
   explicit Layout(int64_t n) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     ntiles = (n + W - 1) / W;
     const size_t cap = (size_t)ntiles * W;
-    const size_t ninc = (size_t)n + (size_t)ntiles;  // Σ (a_T + 1) <= closes + tiles
+    const size_t npop = (size_t)n;                    // Σ a_T <= closes
     size_t o = 0;
     ctrl = o; o = al(o + CtrlLayout(ntiles).bytes);
     aoff = o; o = al(o + 8 * ((size_t)ntiles + 1));
     sidx = o; o = al(o + 4 * cap);
     sbox = o; o = al(o + 16 * cap);
     ssu = o; o = al(o + 16 * cap);
-    inc = o; o = al(o + 8 * ninc);
-    xc = o; o = al(o + 4 * ninc);
+    pop = o; o = al(o + 16 * npop);
+    popu = o; o = al(o + 16 * npop);
     int64_t m = ntiles;
     for (int k = 0; k < LV; k++) {
       tu[k] = o; o = al(o + 16 * (size_t)m);
@@ -98,7 +108,13 @@ struct Layout {
     }
     pja = o; o = al(o + 32 * (size_t)ntiles);
     pjp = o; o = al(o + 8 * (size_t)ntiles);
+    pjo = o; o = al(o + 4 * (size_t)ntiles);
+    tcs = o; o = al(o + 16 * (size_t)ntiles);
+    rns = o; o = al(o + 8 * RMAX * (size_t)ntiles);
+    nrs = o; o = al(o + 4 * (size_t)ntiles);
     flag = o; o = al(o + 16);
+    blk = o; o = al(o + 16 * MAXCTRL);
+    blkmin = o; o = al(o + 4 * MAXCTRL);
     bytes = o;
   }
 };
@@ -120,12 +136,20 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.slice_idx = (int32_t*)(b + L.sidx);
   p.slice_box = (float4*)(b + L.sbox);
   p.slice_su = (float4*)(b + L.ssu);
-  p.inc = (int2*)(b + L.inc);
-  p.xc = (int32_t*)(b + L.xc);
+  p.pop = (int4*)(b + L.pop);
+  p.popu = (float4*)(b + L.popu);
   for (int k = 0; k < LV; k++) p.tu[k] = (float4*)(b + L.tu[k]);
   p.pj_acc = (float4*)(b + L.pja);
   p.pj_ptr = (int32_t*)(b + L.pjp);
+  p.pj_own = (int32_t*)(b + L.pjo);
+  p.tc = (float4*)(b + L.tcs);
+  p.runs = (int2*)(b + L.rns);
+  p.nruns = (int32_t*)(b + L.nrs);
   p.flag = (int32_t*)(b + L.flag);
+  p.blk = (int4*)(b + L.blk);
+  p.blkmin = (int32_t*)(b + L.blkmin);
+  p.chunk = 32;
+  p.trace = nullptr;
   return p;
 }
 
@@ -149,10 +173,12 @@ __device__ __forceinline__ void classify16b(uint4 raw, uint32_t& om, uint32_t& c
 // ----------------------------------------------------------------------------
 // fz_reduce: tile Bic values, slices and their local cumulative clips
 // ----------------------------------------------------------------------------
+__device__ uint8_t g_unm4[UNM4_ENTRIES];  // common.cuh unm4_entry, filled once per device
+
 constexpr int RL = W / 32;  // 64 elements per lane
 __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   __shared__ uint8_t bic4[256];  // Bic of 4 elements: index = open nibble | close nibble << 4; value a | b << 4
-  __shared__ uint8_t unm4[UNM4_ENTRIES];
+  __shared__ __align__(16) uint8_t unm4[UNM4_ENTRIES];
   const int lane = threadIdx.x & 31;
   {
     const int t = threadIdx.x;
@@ -160,7 +186,8 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
 #pragma unroll
     for (int j = 0; j < 4; j++) v = bic_combine(v, Bic{(t >> (4 + j)) & 1, (t >> j) & 1});
     bic4[t] = (uint8_t)(v.a | (v.b << 4));
-    unm4_fill(unm4, t, 256);
+    if (t < UNM4_ENTRIES / 16)
+      reinterpret_cast<uint4*>(unm4)[t] = reinterpret_cast<const uint4*>(g_unm4)[t];
   }
   __syncthreads();
   const int T = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -265,62 +292,334 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
 }
 
 // ----------------------------------------------------------------------------
-// fz_ctrl (cooperative): TC by pointer jumping, slice contexts, incoming lists
+// fz_ctrl (cooperative): tile scan, low-water hierarchy, TC by pointer jumping,
+// slice contexts
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) fz_ctrl(Params p) {
+// Bic value of a run of tiles (§3) and the sum of their a
+struct Agg {
+  int a, b;
+  long long s;
+};
+__device__ __forceinline__ Agg agg_combine(Agg x, Agg y) {
+  const Bic c = bic_combine(Bic{x.a, x.b}, Bic{y.a, y.b});
+  return Agg{c.a, c.b, x.s + y.s};
+}
+__device__ __forceinline__ Agg shfl_up_agg(Agg v, int d) {
+  return Agg{__shfl_up_sync(0xffffffffu, v.a, d), __shfl_up_sync(0xffffffffu, v.b, d),
+             (long long)__shfl_up_sync(0xffffffffu, (unsigned long long)v.s, d)};
+}
+constexpr int NTC = 1024;  // fz_ctrl threads per block (one block per SM: cheap grid barriers)
+constexpr int NWC = NTC / 32;
+// exclusive scan of v over the block's threads in thread order
+__device__ __forceinline__ void block_excl(Agg v, Agg& ex, Agg& tot, Agg* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Agg incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Agg o = shfl_up_agg(incl, off);
+    if (lane >= off) incl = agg_combine(o, incl);
+  }
+  if (lane == 31) sh[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {  // scan of the warp totals
+    Agg x = sh[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const Agg o = shfl_up_agg(x, off);
+      if (lane >= off) x = agg_combine(o, x);
+    }
+    sh[lane] = x;  // inclusive
+  }
+  __syncthreads();
+  const Agg wpre = warp ? sh[warp - 1] : Agg{0, 0, 0};
+  Agg e = shfl_up_agg(incl, 1);
+  if (lane == 0) e = Agg{0, 0, 0};
+  ex = agg_combine(wpre, e);
+  tot = sh[NWC - 1];
+  __syncthreads();
+}
+__device__ __forceinline__ int block_min(int v, int* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = __reduce_min_sync(0xffffffffu, v);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  const int m = __reduce_min_sync(0xffffffffu, sh[lane]);
+  __syncthreads();
+  return m;
+}
+
+// owner rule F1 over the low-water hierarchy written by this kernel (L2 loads)
+__device__ __forceinline__ int owner_search_cg(const Ctrl& c, int from, int X, int& Lout) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t ux = (uint32_t)X;
+  {
+    const int t = from - 1 - lane;
+    const uint32_t v = t >= 0 ? __ldcg(c.lw + t) - 1u : 0xffffffffu;
+    const unsigned m = __ballot_sync(0xffffffffu, t >= 0 && v <= ux);
+    if (m) {
+      const int k = __ffs(m) - 1;
+      Lout = (int)__shfl_sync(0xffffffffu, v, k);
+      return from - 1 - k;
+    }
+    if (from <= 32) return -1;
+    from -= 32;
+  }
+  int idx = from;
+#pragma unroll 1
+  for (int k = 0; k < HLEVELS; k++) {
+    const int g = idx >> 5, r = idx & 31;
+    const uint32_t v = lane < r ? __ldcg(c.lv[k] + ((size_t)g << 5) + lane) - 1u : 0xffffffffu;
+    const unsigned m = __ballot_sync(0xffffffffu, lane < r && v <= ux);
+    if (m) {
+      int E = (g << 5) + (31 - __clz(m));
+      uint32_t L = __shfl_sync(0xffffffffu, v, 31 - __clz(m));
+#pragma unroll 1
+      for (int j = k - 1; j >= 0; j--) {
+        const uint32_t v2 = __ldcg(c.lv[j] + ((size_t)E << 5) + lane) - 1u;
+        const unsigned m2 = __ballot_sync(0xffffffffu, v2 <= ux);
+        const int top = 31 - __clz(m2);
+        L = __shfl_sync(0xffffffffu, v2, top);
+        E = (E << 5) + top;
+      }
+      Lout = (int)L;
+      return E;
+    }
+    idx = g;
+    if (idx == 0) break;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define FZ_TRACE(k)                                                              \
+  do {                                                                           \
+    if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[(k)] = gtimer(); \
+  } while (0)
+
+constexpr int CMAX = 1024;  // tiles per fz_ctrl block kept in shared memory (larger chunks: no in-block ANSV)
+constexpr int CLOG = 10;
+
+__global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  const int lane = threadIdx.x & 31;
-  const int nt = p.ntiles;
-  const int gwarp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  const int nwarps = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
-  // phase 1 (one warp per tile)
-  for (int T = gwarp; T < nt; T += nwarps) {
-    const int H = __ldg(p.ctrl.hstart + T);
-    const int aT = __ldg(p.ctrl.agg + T).x;
-    const int L = (int)__ldg(p.ctrl.lw + T) - 1;
-    const int64_t ioff = __ldg(p.aoff + T);
-    // TC(T): the entry at height L - 1 (the tile's link): slice entry of its owner
-    float4 acc = bINF();
-    int ptr = -1;
-    if (L >= 1) {
-      int LU = 0;
-      const int U = owner_search_done(p.ctrl, T, L - 1, LU);
-      if (U >= 0) {
-        acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - LU));
-        ptr = U;
-      }
+  __shared__ Agg sh[NWC];
+  __shared__ int shm[NWC];
+  __shared__ int mw[CLOG][CMAX];  // ANSV windows over the chunk (levels >= 1)
+  __shared__ int nun;
+  __shared__ int unres[CMAX];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nt = p.ntiles, G = gridDim.x, bx = blockIdx.x;
+  const int C = p.chunk;  // tiles per block, a multiple of 32 (level-1 groups stay inside a block)
+  const int t0 = min(bx * C, nt), t1 = min(t0 + C, nt);
+  const int per = (C + NTC - 1) / NTC;
+  const int ta = min(t0 + tid * per, t1), tb = min(ta + per, t1);  // this thread's tiles
+  FZ_TRACE(0);
+
+  // P0: Bic value and a-sum of the block's tiles
+  Agg v{0, 0, 0};
+  for (int T = ta; T < tb; T++) {
+    const int2 g = __ldcg(p.ctrl.agg + T);
+    v = agg_combine(v, Agg{g.x, g.y, g.x});
+  }
+  Agg ex, tot;
+  block_excl(v, ex, tot, sh);
+  if (tid == 0) {
+    p.blk[bx] = make_int4(tot.a, tot.b, (int)(unsigned)(tot.s & 0xffffffffll), (int)(tot.s >> 32));
+    if (bx == 0) p.flag[0] = p.flag[1] = p.flag[2] = 0;
+  }
+  grid.sync();
+  FZ_TRACE(1);
+
+  // P1: prefix over earlier blocks; start heights H, low-water marks L = max(H - a, 0),
+  // pop offsets; level 1 of the low-water hierarchy (32-tile groups inside the block)
+  Agg pre;
+  {
+    const int perb = (bx + NTC - 1) / NTC;
+    const int ba = min(tid * perb, bx), bb = min(ba + perb, bx);
+    Agg u{0, 0, 0};
+    for (int j = ba; j < bb; j++) {
+      const int4 x = __ldcg(p.blk + j);
+      u = agg_combine(u, Agg{x.x, x.y, (long long)(((unsigned long long)(unsigned)x.w << 32) | (unsigned)x.z)});
     }
-    if (lane == 0) {
-      p.pj_acc[T] = acc;
-      p.pj_ptr[T] = ptr;
+    Agg ux, ut;
+    block_excl(u, ux, ut, sh);
+    pre = ut;
+  }
+  int lmin = INT_MAX;
+  {
+    Agg cur = agg_combine(pre, ex);
+    for (int T = ta; T < tb; T++) {
+      const int2 g = __ldcg(p.ctrl.agg + T);
+      const int H = cur.b;
+      const int L = max(H - g.x, 0);
+      p.ctrl.hstart[T] = H;
+      p.ctrl.lw[T] = (uint32_t)L + 1u;
+      p.aoff[T] = cur.s;
+      lmin = min(lmin, L);
+      cur = agg_combine(cur, Agg{g.x, g.y, g.x});
     }
-    // incoming list: depth D = 0..a_T <-> height H - 1 - D; below 0: the root
-    for (int D = max(H, 0) + lane; D <= aT; D += 32) p.inc[ioff + D] = make_int2(-1, -1);
-    int cur = H - 1, from = T;
-    const int lo = max(H - 1 - aT, 0);
-    while (cur >= lo) {
-      int LU = 0;
-      const int U = owner_search_done(p.ctrl, from, cur, LU);
-      if (U < 0) break;  // cannot happen on one device (every live entry was pushed by a tile)
-      const int hlo = max(LU, lo);
-      for (int h = cur - lane; h >= hlo; h -= 32) {
-        const int64_t ref = (int64_t)U * W + (h - LU);
-        p.inc[ioff + (H - 1 - h)] = make_int2(__ldcg(p.slice_idx + ref) & 0x7fffffff, (int)ref);
-      }
-      cur = LU - 1;
-      from = U;
+    if (tb == nt && ta < tb) {
+      *p.ctrl.total = make_int2(cur.a, cur.b);
+      p.aoff[nt] = cur.s;
     }
   }
-  // phase 2: TC(T) = acc ∩ TC(ptr), pointer jumping (thread per tile)
-  const int gt = (int)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
-  const int nthr = (int)(gridDim.x * (int64_t)blockDim.x);
+  lmin = block_min(lmin, shm);
+  if (tid == 0) p.blkmin[bx] = lmin;
+  for (int g = (t0 >> 5) + warp; g < ((t1 + 31) >> 5); g += NWC) {
+    const int i = g * 32 + lane;
+    uint32_t x = i < nt ? __ldcg(p.ctrl.lw + i) : 0xffffffffu;
+    x = __reduce_min_sync(0xffffffffu, x);
+    if (lane == 0) p.ctrl.lv[1][g] = x;
+  }
+  grid.sync();
+  FZ_TRACE(2);
+
+  // P2: smin (min L over the later tiles: which slice entries survive to the
+  // end, F1); the upper levels of the hierarchy (block 0)
+  {
+    int after = INT_MAX;
+    for (int j = bx + 1 + tid; j < G; j += NTC) after = min(after, __ldcg(p.blkmin + j));
+    after = block_min(after, shm);
+    int mine = INT_MAX;
+    for (int T = ta; T < tb; T++) mine = min(mine, (int)__ldcg(p.ctrl.lw + T) - 1);
+    // exclusive suffix min over the threads after this one
+    int x = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_down_sync(0xffffffffu, x, off);
+      if (lane + off < 32) x = min(x, y);
+    }
+    if (lane == 0) shm[warp] = x;
+    __syncthreads();
+    int later = after;
+    for (int w = warp + 1; w < NWC; w++) later = min(later, shm[w]);
+    int sx = __shfl_down_sync(0xffffffffu, x, 1);
+    if (lane == 31) sx = INT_MAX;
+    int run = min(later, sx);
+    for (int T = tb - 1; T >= ta; T--) {
+      p.ctrl.smin[T] = run;
+      run = min(run, (int)__ldcg(p.ctrl.lw + T) - 1);
+    }
+    __syncthreads();
+  }
+  if (bx == 0) {
+    int m = (nt + 31) / 32;  // nodes at level 1
+    for (int k = 2; k < HLEVELS; k++) {
+      __syncthreads();
+      const int groups = (m + 31) / 32;
+      for (int g = warp; g < groups; g += NWC) {
+        const int i = g * 32 + lane;
+        uint32_t x = i < m ? __ldcg(p.ctrl.lv[k - 1] + i) : 0xffffffffu;
+        x = __reduce_min_sync(0xffffffffu, x);
+        if (lane == 0) p.ctrl.lv[k][g] = x;
+      }
+      m = groups;
+    }
+  }
+  grid.sync();
+  FZ_TRACE(3);
+
+  // P3: the link owner of each tile = the tile that pushed the entry at height
+  // L_T - 1 (F1: the last tile U < T with L_U < L_T, a previous-smaller value)
+  // and TC's initial pointer.  Inside the block's chunk by binary lifting over
+  // window minima in shared memory; tiles with no smaller value earlier in the
+  // chunk ask the global hierarchy (one warp each).
+  const bool local = C <= CMAX;
+  if (tid == 0) nun = 0;
+  if (local) {
+    // mw[k][i] = min L over chunk tiles [i - 2^k + 1, i] (k >= 1; level 0 read from lw)
+    const int cn = t1 - t0;
+    __syncthreads();
+    for (int k = 1; k < CLOG && (1 << k) <= cn; k++) {
+      for (int i = tid; i < cn; i += NTC) {
+        const int h = 1 << (k - 1);
+        const int a = k == 1 ? (int)__ldcg(p.ctrl.lw + t0 + i) - 1 : mw[k - 1][i];
+        const int b = i - h >= 0 ? (k == 1 ? (int)__ldcg(p.ctrl.lw + t0 + i - h) - 1 : mw[k - 1][i - h]) : INT_MAX;
+        mw[k][i] = min(a, b);
+      }
+      __syncthreads();
+    }
+    for (int T = t0 + tid; T < t1; T += NTC) {
+      const int L = (int)__ldcg(p.ctrl.lw + T) - 1;
+      int U = -1;
+      if (L >= 1) {
+        int pos = T - 1 - t0;  // chunk-local
+        for (int k = CLOG - 1; k >= 1; k--) {
+          if ((1 << k) <= cn && pos - (1 << k) + 1 >= 0 && mw[k][pos] >= L) pos -= 1 << k;
+        }
+        if (pos >= 0 && (int)__ldcg(p.ctrl.lw + t0 + pos) - 1 >= L) pos--;
+        if (pos >= 0) {
+          U = t0 + pos;
+        } else {
+          unres[atomicAdd(&nun, 1)] = T;
+          continue;
+        }
+      }
+      float4 acc = bINF();
+      if (U >= 0) acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - ((int)__ldcg(p.ctrl.lw + U) - 1)));
+      p.pj_acc[T] = acc;
+      p.pj_ptr[T] = U;
+      p.pj_own[T] = U;
+    }
+    __syncthreads();
+  }
+  {
+    // unresolved tiles (or every tile when the chunk is too long for shared memory)
+    const int cnt = local ? nun : (t1 - t0);
+    for (int j = warp; j < cnt; j += NWC) {
+      const int T = local ? unres[j] : t0 + j;
+      const int L = (int)__ldcg(p.ctrl.lw + T) - 1;
+      float4 acc = bINF();
+      int U = -1;
+      if (L >= 1) {
+        int LU = 0;
+        U = owner_search_cg(p.ctrl, T, L - 1, LU);
+        if (U >= 0) acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - LU));
+      }
+      if (lane == 0) {
+        p.pj_acc[T] = acc;
+        p.pj_ptr[T] = U;
+        p.pj_own[T] = U;
+      }
+    }
+  }
+  grid.sync();
+  FZ_TRACE(4);
+
+  // P4: TC(T) = acc ∩ TC(ptr) by pointer jumping (thread per tile), one grid
+  // barrier per round; flag r % 3 collects round r's "not done", flag
+  // (r + 1) % 3 is cleared in round r
+  const int gt = (int)(bx * (int64_t)blockDim.x + tid);
+  const int nthr = (int)(G * (int64_t)blockDim.x);
+  // the incoming stack of each tile (its a_T + 1 top entries) as runs of one
+  // owner each: T - 1 owns heights [L_{T-1}, H_T); below a run of U the owner
+  // is U's link owner (F1) -- a walk along the link-owner pointers
+  for (int T = gt; T < nt; T += nthr) {
+    const int H = __ldcg(p.ctrl.hstart + T);
+    const int aT = __ldcg(p.ctrl.agg + T).x;
+    const int lo = max(H - 1 - aT, 0);
+    int hi = H - 1, U = T - 1, k = 0;
+    while (hi >= lo && U >= 0) {
+      const int LU = (int)__ldcg(p.ctrl.lw + U) - 1;
+      const int nxt = __ldcg(p.pj_own + U);
+      if (LU <= hi) {
+        if (k < RMAX) p.runs[(int64_t)T * RMAX + k] = make_int2(U, LU);
+        k++;
+        hi = LU - 1;
+      }
+      U = nxt;
+    }
+    p.nruns[T] = k;
+  }
   float4* accb[2] = {p.pj_acc, p.pj_acc + nt};
   int* ptrb[2] = {p.pj_ptr, p.pj_ptr + nt};
   int cb = 0;
-  for (int round = 0; round < 40; round++) {
-    if (gt == 0) p.flag[round & 1] = 0;
-    grid.sync();
+  for (int round = 0; round < 64; round++) {
+    if (gt == 0) p.flag[(round + 1) % 3] = 0;
     int any = 0;
     for (int V = gt; V < nt; V += nthr) {
       float4 a = __ldcg(accb[cb] + V);
@@ -334,19 +633,18 @@ __global__ void __launch_bounds__(256) fz_ctrl(Params p) {
       ptrb[cb ^ 1][V] = q;
     }
     any = __syncthreads_or(any);
-    if (any && threadIdx.x == 0) atomicOr(p.flag + (round & 1), 1);
+    if (any && tid == 0) atomicOr(p.flag + round % 3, 1);
     cb ^= 1;
     grid.sync();
-    if (__ldcg(p.flag + (round & 1)) == 0) break;
+    if (__ldcg(p.flag + round % 3) == 0) {
+      if (p.trace && bx == 0 && tid == 0) p.trace[6] = (uint64_t)round + 1;
+      break;
+    }
   }
-  // phase 3: slice contexts lc ∩ TC (one warp per tile)
-  for (int T = gwarp; T < nt; T += nwarps) {
-    const int bT = __ldg(p.ctrl.agg + T).y;
-    if (bT == 0) continue;
-    const float4 tc = __ldcg(accb[cb] + T);
-    float4* sb = p.slice_box + (int64_t)T * W;
-    for (int k = lane; k < bT; k += 32) sb[k] = isect(__ldcg(sb + k), tc);
-  }
+  FZ_TRACE(5);
+  // P5: TC for the main pass (slice context = lc ∩ TC of the slice's tile)
+  for (int V = gt; V < nt; V += nthr) p.tc[V] = __ldcg(accb[cb] + V);
+  FZ_TRACE(7);
 }
 
 // ----------------------------------------------------------------------------
@@ -418,6 +716,7 @@ struct Smem {
   int l[NT];
   uint32_t uo[NT];
   int link[NT];
+  int2 runs[RMAX];
   Bic wtot[NW];
 };
 
@@ -433,6 +732,23 @@ __device__ __forceinline__ float4 range_threads(const Smem& s, int a, int b) {
   if (len <= 0) return bEMPTY();
   const int k = min(31 - __clz(len), LT - 1);
   return unite(s.u.st[k][a], s.u.st[k][b - (1 << k) + 1]);
+}
+
+// slice reference (owner tile * W + slice position) of the entry at height h
+// (>= 0) of the tile's incoming stack: the first run whose low-water mark is
+// <= h; past the stored runs, the walk along the link owners continues
+__device__ __forceinline__ int inc_ref(const Params& p, const Smem& s, int nruns, int h) {
+  const int nr = min(nruns, RMAX);
+  for (int k = 0; k < nr; k++) {
+    const int2 r = s.runs[k];
+    if (r.y <= h) return r.x * W + (h - r.y);
+  }
+  int U = __ldg(p.pj_own + s.runs[RMAX - 1].x);
+  while (true) {  // only when the incoming stack has more than RMAX runs
+    const int LU = (int)__ldg(p.ctrl.lw + U) - 1;
+    if (LU <= h) return U * W + (h - LU);
+    U = __ldg(p.pj_own + U);
+  }
 }
 
 #ifndef FZ_MINB
@@ -456,12 +772,15 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   const uint4 raw = load_tags16(p.tags, p.n, base + tl0, nvalid == W);
   const int H = __ldg(p.ctrl.hstart + T);
   const int aT = __ldg(p.ctrl.agg + T).x;
-  const int64_t ioff = __ldg(p.aoff + T);
+  const int64_t poff = __ldg(p.aoff + T);  // pop records of this tile: [poff, poff + a_T)
 #pragma unroll
   for (int j = 0; j < K; j++) {
     const int e = j * NT + tid;
     s.val[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bEMPTY();
   }
+  // the tile's incoming stack as runs of one owner tile each (fz_ctrl)
+  if (tid < RMAX) s.runs[tid] = __ldg(p.runs + (int64_t)T * RMAX + tid);
+  const int nruns = __ldg(p.nruns + T);
   const int nv_t = nvalid - tl0;
   const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
   const Walk w = walk(raw, valid);
@@ -514,9 +833,9 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       const int D = -lk - 1;
       giLast = -1;
       if (H - 1 - D >= 0) {
-        const int2 e = __ldg(p.inc + ioff + D);
-        giLast = e.x;
-        acc = __ldg(p.slice_box + e.y);
+        const int ref = inc_ref(p, s, nruns, H - 1 - D);
+        giLast = __ldg(p.slice_idx + ref) & 0x7fffffff;
+        acc = isect(__ldg(p.slice_box + ref), __ldg(p.tc + (ref >> LOGW)));
       }
     }
     int cb = 0;
@@ -543,7 +862,8 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   //      matchS[c_d]; the partner of a popped in-tile open; the context at
   //      depth d where a leaf or open sits there, in c_d's slot (depth a_t:
   //      the link, TL(t))
-  uint32_t xcm = 0;  // closes popping an entry of an earlier tile
+  uint32_t xcm = 0;  // closes popping an entry of an earlier tile (incoming depths dx0, dx0 + 1, ...)
+  int dx0 = 0;
   {
     int ref = top_ref, d = 0, prevc = -1;
     uint32_t q = w.ucm;
@@ -571,11 +891,15 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       int gi = -1;
       float4 cx = bINF();
       if (H - 1 - D >= 0) {
-        const int2 e = __ldg(p.inc + ioff + D);
-        gi = e.x;
+        const int ref = inc_ref(p, s, nruns, H - 1 - D);
+        const int si = __ldg(p.slice_idx + ref);
+        gi = si & 0x7fffffff;
+        if (!xcm) dx0 = D;
         xcm |= 1u << ci;
-        p.xc[ioff + D] = gtb + ci;
-        if (seg & needm) cx = __ldg(p.slice_box + e.y);
+        p.pop[poff + D] = make_int4(gtb + ci, gi, ref, si < 0);
+        if (seg & needm) cx = isect(__ldg(p.slice_box + ref), __ldg(p.tc + (ref >> LOGW)));
+      } else {
+        p.pop[poff + D] = make_int4(-1, -1, -1, 0);  // pops the root (R3)
       }
       s.matchS[mb + ci] = gi;
       if (seg & needm) s.val[sb ^ ci] = cx;
@@ -705,10 +1029,8 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   }
   if (xcm) {
     const float4 pre = range_threads(s, 0, tid - 1);
-    for (uint32_t q = xcm; q; q &= q - 1) {
-      float4& cv = s.val[sb ^ (__ffs(q) - 1)];
-      cv = unite(cv, pre);
-    }
+    int D = dx0;
+    for (uint32_t q = xcm; q; q &= q - 1, D++) p.popu[poff + D] = unite(s.val[sb ^ (__ffs(q) - 1)], pre);
   }
   if (tid == 0) p.tu[0][T] = range_threads(s, 0, NT - 1);
   __syncthreads();
@@ -749,65 +1071,66 @@ __global__ void __launch_bounds__(256) fz_hier(Params p, int k, int m /* nodes a
   if (lane == 0) p.tu[k][g] = v;
 }
 
-// union over tiles [a, b] by one warp (a, b warp-uniform)
-__device__ float4 range_tiles(const Params& p, int a, int b) {
+// union over tiles [a, b] by one warp (a, b warp-uniform): per level of the
+// 32-ary hierarchy the partial groups at both ends, every load issued at once
+__device__ __forceinline__ float4 range_tiles(const Params& p, int a, int b) {
   const int lane = threadIdx.x & 31;
   float4 acc = bEMPTY();
-  int k = 0;
-  while (a <= b) {
-    const float4* val = p.tu[k];
-    if ((a >> 5) == (b >> 5) || k == LV - 1) {
-      for (int i = a + lane; i <= b; i += 32) acc = unite(acc, __ldcg(val + i));
-      break;
+#pragma unroll
+  for (int k = 0; k < LV; k++) {
+    int i1 = -1, i2 = -1;
+    if (a <= b) {
+      if ((a >> 5) == (b >> 5) || k == LV - 1) {
+        if (a + lane <= b) i1 = a + lane;
+        a = 1;
+        b = 0;
+      } else {
+        if (a & 31) {
+          const int e = a | 31;
+          if (a + lane <= e) i1 = a + lane;
+          a = e + 1;
+        }
+        if ((b & 31) != 31) {
+          const int s0 = b & ~31;
+          if (s0 + lane <= b) i2 = s0 + lane;
+          b = s0 - 1;
+        }
+        if (a <= b) {
+          a >>= 5;
+          b = ((b + 1) >> 5) - 1;
+        }
+      }
     }
-    if (a & 31) {
-      const int e = a | 31;
-      const int i = a + lane;
-      if (i <= e) acc = unite(acc, __ldcg(val + i));
-      a = e + 1;
-    }
-    if ((b & 31) != 31) {
-      const int s0 = b & ~31;
-      const int i = s0 + lane;
-      if (i <= b) acc = unite(acc, __ldcg(val + i));
-      b = s0 - 1;
-    }
-    if (a > b) break;
-    a >>= 5;
-    b = ((b + 1) >> 5) - 1;
-    k++;
+    const float4 v1 = i1 >= 0 ? __ldcg(p.tu[k] + i1) : bEMPTY();
+    const float4 v2 = i2 >= 0 ? __ldcg(p.tu[k] + i2) : bEMPTY();
+    acc = unite(acc, unite(v1, v2));
   }
   return warp_unite_all(acc);
 }
 
 // ----------------------------------------------------------------------------
-// fz_close: nodes opened in an earlier tile (one warp per tile)
+// fz_close: nodes opened in an earlier tile (one warp per tile, 32 pops at a time)
 // ----------------------------------------------------------------------------
 template <bool PM>
 __global__ void __launch_bounds__(128) fz_close(Params p) {
   const int lane = threadIdx.x & 31;
   const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (T >= p.ntiles) return;
-  const int H = __ldg(p.ctrl.hstart + T);
-  const int aT = __ldg(p.ctrl.agg + T).x;
-  const int64_t ioff = __ldg(p.aoff + T);
-  const int npop = min(aT, max(H, 0));  // pops of real entries (depth D < H)
-  int cto = INT_MIN;                    // warp cache: the last tile range resolved
+  const int64_t poff = __ldg(p.aoff + T);
+  const int npop = (int)(__ldg(p.aoff + T + 1) - poff);
+  int cto = INT_MIN;  // warp cache: the last tile range resolved
   float4 cR = bEMPTY();
   for (int j0 = 0; j0 < npop; j0 += 32) {
     const int j = j0 + lane;
-    const bool valid = j < npop;
-    int c = 0, o = 0, To = 0;
+    int4 r = make_int4(-1, -1, -1, 0);
+    if (j < npop) r = __ldcg(p.pop + poff + j);
+    const bool valid = r.x >= 0;  // root pops (R3) have no node
+    int To = T;
     float4 P = bEMPTY(), su = bEMPTY();
-    int kind = 0;
     if (valid) {
-      const int2 e = __ldg(p.inc + ioff + j);
-      o = e.x;
-      To = e.y >> LOGW;
-      c = __ldg(p.xc + ioff + j);
-      P = __ldcg(p.out + c);
-      su = __ldg(p.slice_su + e.y);
-      kind = __ldg(p.slice_idx + e.y) < 0;
+      To = r.z >> LOGW;
+      P = __ldcg(p.popu + poff + j);
+      su = __ldg(p.slice_su + r.z);
     }
     float4 R = bEMPTY();
     bool pending = valid && To < T - 1;
@@ -828,9 +1151,9 @@ __global__ void __launch_bounds__(128) fz_close(Params p) {
     }
     if (valid) {
       const float4 U = unite(unite(P, su), R);
-      p.out[c] = U;
-      if (kind) p.out[o] = U;
-      if (PM) p.match[o] = c;
+      p.out[r.x] = U;
+      if (r.w) p.out[r.y] = U;
+      if (PM) p.match[r.y] = r.x;
     }
   }
   // blend opens never closed (R4): the tile's slice entries that survive to
@@ -843,7 +1166,7 @@ __global__ void __launch_bounds__(128) fz_close(Params p) {
     bool anyb = false;
     for (int k = lane; k < surv; k += 32) anyb |= __ldg(p.slice_idx + (int64_t)T * W + k) < 0;
     if (__any_sync(0xffffffffu, anyb)) {
-      const float4 after = T + 1 < p.ntiles ? range_tiles(p, T + 1, p.ntiles - 1) : bEMPTY();
+      const float4 after = range_tiles(p, T + 1, p.ntiles - 1);
       for (int k = lane; k < surv; k += 32) {
         const int64_t ref = (int64_t)T * W + k;
         const int si = __ldg(p.slice_idx + ref);
@@ -860,8 +1183,8 @@ static int ctrl_blocks() {  // co-resident CTAs of the cooperative kernel
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fz_ctrl, 256, 0);
-  return sms * (occ > 0 ? occ : 1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fz_ctrl, NTC, 0);
+  return std::min(MAXCTRL, sms * std::min(occ > 0 ? occ : 1, 1));
 }
 
 static cudaError_t setup() {
@@ -869,12 +1192,18 @@ static cudaError_t setup() {
     cudaError_t e = cudaFuncSetAttribute(fz_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fz_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    uint8_t tab[UNM4_ENTRIES];
+    for (int i = 0; i < UNM4_ENTRIES; i++) tab[i] = unm4_entry(i);
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_unm4, tab, sizeof tab);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
 }  // namespace fz
+
+static uint64_t* g_fz_trace = nullptr;  // debug hook (tb_debug_fz_trace)
+void fused_set_trace(uint64_t* dev) { g_fz_trace = dev; }
 
 size_t fused_workspace_bytes(int64_t n) { return n > 0 ? fz::Layout(n).bytes : 0; }
 int fused_tile_elems() { return fz::W; }
@@ -886,17 +1215,20 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
   if (e != cudaSuccess) return e;
   const bool pm = match != nullptr;
   fz::Params p = fz::make_params(tags, leaf_bbox, n, match, parent, node_bbox, ws);
+  p.trace = g_fz_trace;
   const int nt = p.ntiles;
   TB_LAUNCH(stream, "fz_reduce", (fz::fz_reduce<<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
   e = cudaGetLastError();
-  if (e == cudaSuccess) e = tile_scan_launch(p.ctrl, nt, 0, 0, stream, p.aoff);
   if (e != cudaSuccess) return e;
   {
-    const int blocks = std::max(1, std::min((nt + 7) / 8, fz::ctrl_blocks()));
+    // enough blocks for the per-tile warps of P3 / P5, at most the co-resident
+    // count; chunks of whole 32-tile groups
+    const int G = std::max(1, std::min((nt + 31) / 32, fz::ctrl_blocks()));
+    p.chunk = (((nt + G - 1) / G) + 31) & ~31;
     void* args[] = {(void*)&p};
     void* tok;
     prof_begin(stream, "fz_ctrl", &tok);
-    e = cudaLaunchCooperativeKernel((const void*)fz::fz_ctrl, dim3(blocks), dim3(256), args, 0, stream);
+    e = cudaLaunchCooperativeKernel((const void*)fz::fz_ctrl, dim3(G), dim3(fz::NTC), args, 0, stream);
     prof_end(stream, tok);
     if (e != cudaSuccess) return e;
   }

@@ -69,6 +69,7 @@ struct ShardOpen {
 // paren_match + tree_bbox in one tile pass (fused.cu): the single-device path.
 // match / parent may be null (tree_bbox alone: only node_bbox is written).
 size_t fused_workspace_bytes(int64_t n);
+void fused_set_trace(uint64_t* dev);  // debug: fz_ctrl phase timestamps (8 x u64 device buffer) or null
 int fused_tile_elems();
 cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, int32_t* match, int32_t* parent,
                          float* node_bbox, void* ws, cudaStream_t stream);
