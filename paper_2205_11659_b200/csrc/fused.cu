@@ -654,9 +654,10 @@ struct Walk {
   uint32_t om, cm, bm, lm;  // opens, closes, blend opens, leaves (valid elements only)
   uint32_t S;               // opens still on the thread stack at its end (thread-unmatched)
   uint32_t plo, phi;        // nibble i: in-thread parent of element i
-  uint32_t mlo, mhi;        // nibble o: in-thread partner close of open o
+  uint32_t mlo, mhi;        // nibble i: in-thread partner of element i (matched opens and closes)
   uint32_t ext;             // elements whose parent lies before the thread
   uint32_t ucm;             // closes with no in-thread open (they pop the stack at the thread start)
+  uint32_t mcb;             // closes whose (in-thread) open is a blend
 };
 
 // Fig. 1 over the thread's 16 elements with a bitmask stack
@@ -667,7 +668,7 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   w.cm &= valid;
   w.bm &= valid;
   w.lm = valid & ~(w.om | w.cm);
-  uint32_t S = 0, plo = 0, phi = 0, mlo = 0, mhi = 0, ext = 0, ucm = 0;
+  uint32_t S = 0, plo = 0, phi = 0, mlo = 0, mhi = 0, ext = 0, ucm = 0, mcb = 0;
 #pragma unroll
   for (int i = 0; i < K; i++) {
     const uint32_t bit = 1u << i;
@@ -677,9 +678,12 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
     ext |= S ? 0u : bit;
     const bool pop = (w.cm & bit) && S;
     ucm |= ((w.cm & bit) && !S) ? bit : 0u;
+    mcb |= (pop && ((w.bm >> top) & 1u)) ? bit : 0u;
     const uint32_t pv = (uint32_t)i << (4 * (top & 7));
     mlo |= (pop && top < 8) ? pv : 0u;
     mhi |= (pop && top >= 8) ? pv : 0u;
+    if (i < 8) mlo |= pop ? (uint32_t)top << (4 * i) : 0u;  // the close's own partner
+    else mhi |= pop ? (uint32_t)top << (4 * (i - 8)) : 0u;
     S = (w.om & bit) ? (S | bit) : (pop ? (S ^ (1u << top)) : S);
   }
   w.S = S;
@@ -689,15 +693,17 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   w.mhi = mhi;
   w.ext = ext;
   w.ucm = ucm;
+  w.mcb = mcb;
   return w;
 }
 
-constexpr int LT = 7;    // levels of the sparse table over threads: windows of 1 .. 64 threads
-constexpr int RCAP = 8;  // segment unions kept per thread (more unmatched opens: recomputed in H)
-static_assert((1 << LT) >= NT, "sparse table covers the tile");
+constexpr int RCAP = 7;  // segment unions kept per thread (more unmatched opens: recomputed in H1)
 
+// Shared memory of fz_main (<= 56 KB: four CTAs per SM).  The scratch region u
+// is reused phase by phase: B-C owner windows; D link contexts; (l, uo, link
+// kept through E); F-H1 segment unions; G-H2 the range table over threads.
 struct Smem {
-  float4 val[W + NT];               // boxes -> lc / contexts / clips / unions (swizzled slots); val[W + t] = TL(t)
+  float4 val[W];                    // boxes -> lc / contexts / clips / unions (swizzled slots)
   int32_t matchS[W + W / K];        // match values (global indices), padded: element e at e + e / K
   union {
     struct {
@@ -707,31 +713,43 @@ struct Smem {
     struct {
       float4 acc[2][NT];            // thread link contexts by pointer jumping
       int ptr[2][NT];
+      int l[NT];                    // kept B-E
+      uint32_t uo[NT];
+      int link[NT];
     } pj;
-    float4 st[LT][NT];              // st[k][t] = union of the clipped leaves of threads [t, t + 2^k)
+    float4 rbuf[RCAP][NT];          // F-H1: the accumulator at each thread-unmatched open (k < RCAP)
+    struct {
+      float4 win[5][NT];            // win[k][t] = union of threads [t - 2^k + 1, t] within t's warp (k = 0: t)
+      float4 pre[NT];               // inclusive prefix within the warp
+      float4 suf[NT];               // inclusive suffix within the warp
+    } rt;
   } u;
-  struct {
-    float4 rbuf[RCAP][NT];  // F-H: the accumulator at each thread-unmatched open (k < RCAP)
-  } u2;
-  int l[NT];
-  uint32_t uo[NT];
-  int link[NT];
   int2 runs[RMAX];
+  uint32_t bmS[NT];                 // blend opens of each thread
+  float4 wtu[NW];                   // warp unions
+  float4 wmid[NW][NW];              // union of the warps strictly between
   Bic wtot[NW];
 };
+static_assert(sizeof(Smem) <= 56 * 1024, "four CTAs per SM");
 
 // element i of thread t lives at slot (t*K | t & 7) ^ i: conflict-free for the
 // per-thread accesses (8 lanes, distinct t & 7) and for the coalesced copies
 __device__ __forceinline__ int slot_of(int e) { return e ^ (int)(((unsigned)e >> LOGK) & 7u); }
 __device__ __forceinline__ int mpad(int e) { return e + (int)((unsigned)e >> LOGK); }
 
-// union of the clipped leaves of whole threads [a, b] (F4): two overlapping
-// windows of the sparse table (min/max are idempotent)
+// union of the clipped leaves of whole threads [a, b] (F4): inside one warp two
+// overlapping backward windows (min/max are idempotent); across warps the
+// suffix of a's warp, the warps between, the prefix of b's warp
 __device__ __forceinline__ float4 range_threads(const Smem& s, int a, int b) {
-  const int len = b - a + 1;
-  if (len <= 0) return bEMPTY();
-  const int k = min(31 - __clz(len), LT - 1);
-  return unite(s.u.st[k][a], s.u.st[k][b - (1 << k) + 1]);
+  if (a > b) return bEMPTY();
+  const int wa = a >> 5, wb = b >> 5;
+  if (wa == wb) {
+    const int len = b - a + 1;
+    if (len == 32) return s.wtu[wa];
+    const int k = 31 - __clz(len);
+    return unite(s.u.rt.win[k][b], s.u.rt.win[k][a + (1 << k) - 1]);
+  }
+  return unite(unite(s.u.rt.suf[a], s.u.rt.pre[b]), s.wmid[wa][wb]);
 }
 
 // slice reference (owner tile * W + slice position) of the entry at height h
@@ -752,7 +770,7 @@ __device__ __forceinline__ int inc_ref(const Params& p, const Smem& s, int nruns
 }
 
 #ifndef FZ_MINB
-#define FZ_MINB 3
+#define FZ_MINB 4
 #endif
 template <bool PM>
 __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
@@ -800,14 +818,15 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
     const int o = __shfl_sync(0xffffffffu, wl[4], 15);
     if (lane == 31) s.u.ref.lwmin[warp] = min(wl[4], o);
   }
-  s.l[tid] = l_t;
-  s.uo[tid] = w.S;
+  s.u.pj.l[tid] = l_t;
+  s.u.pj.uo[tid] = w.S;
+  s.bmS[tid] = w.bm;
   __syncthreads();
 
   // ---- C. thread-level owner lookups (F2); lc of the thread-unmatched opens --
-  const int top_ref = thread_ref<NW, K>(wl, l_t, w.S, r_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.l, s.uo);
-  const int lk = thread_ref<NW, K>(wl, l_t, w.S, l_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.l, s.uo);
-  s.link[tid] = lk;
+  const int top_ref = thread_ref<NW, K>(wl, l_t, w.S, r_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.u.pj.l, s.u.pj.uo);
+  const int lk = thread_ref<NW, K>(wl, l_t, w.S, l_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.u.pj.l, s.u.pj.uo);
+  s.u.pj.link[tid] = lk;
   {
     float4 acc = bINF();
     for (uint32_t q = w.S; q; q &= q - 1) {
@@ -821,7 +840,8 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
 
   // ---- D. context of each thread's link: TL(t) = lc(link) ∩ TL(thread of link)
   //      (pointer jumping over threads); the link's global index
-  int giLast;
+  int giLast, cbf;
+  float4 TL;
   {
     float4 acc = bINF();
     int ptr = -1;
@@ -852,9 +872,9 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       cb ^= 1;
       any = __syncthreads_or(ptr >= 0);
     }
-    s.val[W + tid] = acc;
+    TL = acc;
+    cbf = cb;  // pj.acc[cbf] holds every thread's TL
   }
-  __syncthreads();
 
   // ---- E. entries popped by this thread's unmatched closes c_0 .. c_{a_t - 1}
   //      (c_d pops the entry at depth d of the thread's start stack): c_d's
@@ -863,6 +883,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   //      depth d where a leaf or open sits there, in c_d's slot (depth a_t:
   //      the link, TL(t))
   uint32_t xcm = 0;  // closes popping an entry of an earlier tile (incoming depths dx0, dx0 + 1, ...)
+  uint32_t icm = 0;  // closes popping an open of an earlier thread of this tile
   int dx0 = 0;
   {
     int ref = top_ref, d = 0, prevc = -1;
@@ -873,12 +894,13 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       q &= q - 1;
       const uint32_t seg = ((1u << ci) - 1u) & ~((1u << (prevc + 1)) - 1u);  // elements at depth d
       prevc = ci;
+      icm |= 1u << ci;
       s.matchS[mb + ci] = gbase + ref;
       s.matchS[mpad(ref)] = gtb + ci;
-      if (seg & needm) s.val[sb ^ ci] = isect(s.val[slot_of(ref)], s.val[W + (ref >> LOGK)]);
+      if (seg & needm) s.val[sb ^ ci] = isect(s.val[slot_of(ref)], s.u.pj.acc[cbf][ref >> LOGK]);
       const int V = ref >> LOGK;
-      const uint32_t below = s.uo[V] & ((1u << (ref & (K - 1))) - 1u);
-      ref = below ? (V << LOGK) + 31 - __clz(below) : s.link[V];
+      const uint32_t below = s.u.pj.uo[V] & ((1u << (ref & (K - 1))) - 1u);
+      ref = below ? (V << LOGK) + 31 - __clz(below) : s.u.pj.link[V];
     }
     // the rest are consecutive entries of the incoming stack (a chain that
     // leaves the tile never returns into it)
@@ -891,13 +913,13 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       int gi = -1;
       float4 cx = bINF();
       if (H - 1 - D >= 0) {
-        const int ref = inc_ref(p, s, nruns, H - 1 - D);
-        const int si = __ldg(p.slice_idx + ref);
+        const int rf = inc_ref(p, s, nruns, H - 1 - D);
+        const int si = __ldg(p.slice_idx + rf);
         gi = si & 0x7fffffff;
         if (!xcm) dx0 = D;
         xcm |= 1u << ci;
-        p.pop[poff + D] = make_int4(gtb + ci, gi, ref, si < 0);
-        if (seg & needm) cx = isect(__ldg(p.slice_box + ref), __ldg(p.tc + (ref >> LOGW)));
+        p.pop[poff + D] = make_int4(gtb + ci, gi, rf, si < 0);
+        if (seg & needm) cx = isect(__ldg(p.slice_box + rf), __ldg(p.tc + (rf >> LOGW)));
       } else {
         p.pop[poff + D] = make_int4(-1, -1, -1, 0);  // pops the root (R3)
       }
@@ -913,28 +935,36 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   //      thread, else in rbuf -- and restarts it), parent / match.  By the Bic
   //      normal form all of a thread's unmatched closes precede its unmatched
   //      opens and the thread stack is empty at them, so there the
-  //      accumulator holds the thread's prefix union.
+  //      accumulator holds the thread's prefix union.  Element 15's slot holds
+  //      TL (the context after the last unmatched close) until 15 is reached:
+  //      if 15 is an unmatched close nothing needs TL, if it is a matched
+  //      close its open overwrites the slot after every reader of TL.
   float4 acc = bEMPTY();
   {
+    const bool u15 = (w.ucm >> (K - 1)) & 1u;
+    const float4 v15 = s.val[sb ^ (K - 1)];
+    if (!u15) s.val[sb ^ (K - 1)] = TL;
     int pv[4];
 #pragma unroll
     for (int i = 0; i < K; i++) {
       const uint32_t bit = 1u << i;
-      const float4 v = s.val[sb ^ i];
-      const int pn = nib(w.plo, w.phi, i);
-      const int pt = nib(w.mlo, w.mhi, i);
-      const bool isx = (w.ext & bit) != 0u;
-      const uint32_t nc = w.ucm & ~(bit - 1u);  // unmatched closes at or after i
-      const int j = __ffs(nc) - 1;             // the next one: c_d of element i's depth d
-      const int cidx = isx ? (nc ? (sb ^ j) : W + tid) : (sb ^ pn);
-      const float4 cpar = s.val[cidx];
-      const int mj = s.matchS[mb + max(j, 0)];
-      const int par = isx ? (nc ? mj : giLast) : gtb + pn;
-      const float4 clipped = isect(v, cpar);
       const bool isL = (w.lm & bit) != 0u, isB = (w.bm & bit) != 0u;
       const bool isO = (w.om & bit) != 0u, isC = (w.cm & bit) != 0u, isU = (w.ucm & bit) != 0u;
       const bool isUO = (w.S & bit) != 0u;
       const bool isMC = isC && !isU;
+      float4 v = s.val[sb ^ i];
+      if (i == K - 1 && !isMC) v = v15;
+      const int pn = nib(w.plo, w.phi, i);
+      const int pt = nib(w.mlo, w.mhi, i);
+      const bool isx = (w.ext & bit) != 0u;
+      const uint32_t nc = w.ucm & ~(bit - 1u);  // unmatched closes at or after i
+      const int j = nc ? __ffs(nc) - 1 : K - 1;  // the next one: c_d of element i's depth d (none: TL)
+      // a close takes nothing from its parent: clipped = v (INF slot not needed, v ∩ v = v)
+      const int cidx = isC ? (sb ^ i) : (isx ? (sb ^ j) : (sb ^ pn));
+      const float4 cpar = s.val[cidx];
+      const int mj = s.matchS[mb + j];
+      const int par = isx ? (nc ? mj : giLast) : gtb + pn;
+      const float4 clipped = isect(v, cpar);
       // own slot: leaf / clip open -> clipped; blend open -> parent context;
       // close -> union (in-thread node) / prefix (outer node) / EMPTY (R3)
       float4 o = isB ? cpar : clipped;
@@ -942,14 +972,14 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       s.val[sb ^ i] = o;
       if (isO) {
         const int k = __popc(w.S & (bit - 1u));
-        if (!isUO) s.val[sb ^ pt] = acc;
-        else if (k < RCAP) s.u2.rbuf[k][tid] = acc;
+        float4* dst = isUO ? &s.u.rbuf[min(k, RCAP - 1)][tid] : &s.val[sb ^ pt];
+        if (!isUO || k < RCAP) *dst = acc;
       }
-      if (isMC && ((w.bm >> pn) & 1u)) s.val[sb ^ pn] = acc;
-      const float4 add = isL ? clipped : (isMC ? v : bEMPTY());
+      if ((w.mcb & bit) != 0u) s.val[sb ^ pn] = acc;
+      const float4 add = (isL || isMC) ? clipped : bEMPTY();
       acc = unite(acc, add);
       acc = isO ? bEMPTY() : acc;
-      if (PM && !(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + (isO ? pt : pn);
+      if (PM && !(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + pt;
       pv[i & 3] = par;
       if (PM && (i & 3) == 3) {
         const int q4 = i >> 2;
@@ -965,41 +995,59 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   }
   // the thread's union: the prefix at its first unmatched open ∪ the segments
   const bool ovf = b_t > RCAP;
-  {
-    float4 tu = acc;
-    if (!ovf) {
-      for (int k = 0; k < b_t; k++) tu = unite(tu, s.u2.rbuf[k][tid]);
-    } else {
+  float4 tu = acc;
+  if (!ovf) {
+    for (int k = 0; k < b_t; k++) tu = unite(tu, s.u.rbuf[k][tid]);
+  } else {
 #pragma unroll
-      for (int i = 0; i < K; i++)
-        if ((w.lm >> i) & 1u) tu = unite(tu, s.val[sb ^ i]);
-    }
-    s.u.st[0][tid] = tu;
+    for (int i = 0; i < K; i++)
+      if ((w.lm >> i) & 1u) tu = unite(tu, s.val[sb ^ i]);
   }
-
-  // ---- G. sparse table of thread unions ------------------------------------
+  // warp-level prefix / suffix of the thread unions, warp totals
+  float4 pw = tu, sw = tu;
 #pragma unroll
-  for (int k = 1; k < LT; k++) {
-    __syncthreads();
-    s.u.st[k][tid] = unite(s.u.st[k - 1][tid], s.u.st[k - 1][min(tid + (1 << (k - 1)), NT - 1)]);
+  for (int off = 1; off < 32; off <<= 1) {
+    const float4 a = shfl_up_box(pw, off);
+    if (lane >= off) pw = unite(pw, a);
+    const float4 b = make_float4(__shfl_down_sync(0xffffffffu, sw.x, off), __shfl_down_sync(0xffffffffu, sw.y, off),
+                                 __shfl_down_sync(0xffffffffu, sw.z, off), __shfl_down_sync(0xffffffffu, sw.w, off));
+    if (lane + off < 32) sw = unite(sw, b);
   }
+  if (lane == 31) s.wtu[warp] = pw;
   __syncthreads();
+  if (tid < NW * NW) {
+    const int x = tid / NW, y = tid % NW;
+    float4 m = bEMPTY();
+    for (int w2 = x + 1; w2 < y; w2++) m = unite(m, s.wtu[w2]);
+    s.wmid[x][y] = m;
+  }
+  // union of the threads before / after this one (tile prefix / suffix)
+  float4 pre = bEMPTY(), after = bEMPTY();
+  {
+    const float4 pe = shfl_up_box(pw, 1);
+    if (lane > 0) pre = pe;
+    const float4 se = make_float4(__shfl_down_sync(0xffffffffu, sw.x, 1), __shfl_down_sync(0xffffffffu, sw.y, 1),
+                                  __shfl_down_sync(0xffffffffu, sw.z, 1), __shfl_down_sync(0xffffffffu, sw.w, 1));
+    if (lane < 31) after = se;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; w2++) {
+      if (w2 < warp) pre = unite(pre, s.wtu[w2]);
+      if (w2 > warp) after = unite(after, s.wtu[w2]);
+    }
+  }
 
-  // ---- H. opens left open at the thread end, top down with R = union of the
-  //      thread's leaves after them: closed by a later thread of the tile ->
-  //      finish that close (R ∪ the threads between ∪ the closer's prefix);
-  //      otherwise a slice entry: su = R ∪ the threads after.  Closes of
-  //      earlier tiles' nodes: the tile prefix before them (fz_close ends them)
+  // ---- H1. opens left open at the thread end, top down with R = union of the
+  //      thread's leaves after them (the segment unions): closed by a later
+  //      thread of the tile -> that close's slot takes R (the closer adds the
+  //      threads between in H2); otherwise a slice entry: su = R ∪ the threads
+  //      after.  Closes of earlier tiles' nodes: the tile prefix before them
+  //      into their pop records (fz_close ends them)
   if (w.S) {
-    const float4 after = range_threads(s, tid + 1, NT - 1);
     auto handle = [&](int i, int k, const float4& R) {
       const int mc = s.matchS[mb + i];
       if (mc >= 0) {
-        const int cl = mc - gbase;
-        float4& cv = s.val[slot_of(cl)];
-        const float4 U = unite(unite(R, range_threads(s, tid + 1, (cl >> LOGK) - 1)), cv);
-        cv = U;
-        if ((w.bm >> i) & 1u) s.val[sb ^ i] = U;
+        float4& cv = s.val[slot_of(mc - gbase)];
+        cv = unite(cv, R);
       } else {
         p.slice_su[base + l_t + k + aT] = unite(R, after);
       }
@@ -1011,7 +1059,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
         const int i = 31 - __clz(q);
         q ^= 1u << i;
         handle(i, k, R);
-        R = unite(R, s.u2.rbuf[k][tid]);
+        R = unite(R, s.u.rbuf[k][tid]);
       }
     } else {
       float4 R = bEMPTY();
@@ -1028,11 +1076,44 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
     }
   }
   if (xcm) {
-    const float4 pre = range_threads(s, 0, tid - 1);
     int D = dx0;
     for (uint32_t q = xcm; q; q &= q - 1, D++) p.popu[poff + D] = unite(s.val[sb ^ (__ffs(q) - 1)], pre);
   }
-  if (tid == 0) p.tu[0][T] = range_threads(s, 0, NT - 1);
+  if (tid == 0) {
+    float4 t = s.wtu[0];
+#pragma unroll
+    for (int w2 = 1; w2 < NW; w2++) t = unite(t, s.wtu[w2]);
+    p.tu[0][T] = t;
+  }
+  __syncthreads();
+
+  // ---- G. range table over threads (the segment buffer is dead) --------------
+  {
+    float4 wv = tu;
+    s.u.rt.win[0][tid] = wv;
+#pragma unroll
+    for (int k = 1; k < 5; k++) {
+      const int off = 1 << (k - 1);
+      const float4 a = shfl_up_box(wv, off);
+      if (lane >= off) wv = unite(wv, a);
+      s.u.rt.win[k][tid] = wv;
+    }
+    s.u.rt.pre[tid] = pw;
+    s.u.rt.suf[tid] = sw;
+  }
+  __syncthreads();
+
+  // ---- H2. closes of nodes opened in an earlier thread of the tile: add the
+  //      threads between; a blend open receives the union
+  for (uint32_t q = icm; q; q &= q - 1) {
+    const int ci = __ffs(q) - 1;
+    const int o = s.matchS[mb + ci] - gbase;
+    const int to = o >> LOGK;
+    float4& cv = s.val[sb ^ ci];
+    const float4 U = unite(cv, range_threads(s, to + 1, tid - 1));
+    cv = U;
+    if ((s.bmS[to] >> (o & (K - 1))) & 1u) s.val[slot_of(o)] = U;
+  }
   __syncthreads();
 
   // ---- I. coalesced copy-out -------------------------------------------------
@@ -1192,6 +1273,10 @@ static cudaError_t setup() {
     cudaError_t e = cudaFuncSetAttribute(fz_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fz_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fz_main<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fz_main<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     uint8_t tab[UNM4_ENTRIES];
     for (int i = 0; i < UNM4_ENTRIES; i++) tab[i] = unm4_entry(i);
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_unm4, tab, sizeof tab);
