@@ -660,7 +660,8 @@ struct Walk {
   uint32_t mcb;             // closes whose (in-thread) open is a blend
 };
 
-// Fig. 1 over the thread's 16 elements with a bitmask stack
+// Fig. 1 over the thread's 16 elements with a bitmask stack (four
+// groups of four elements: a rolled outer loop keeps the code small)
 __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   Walk w;
   classify16b(raw, w.om, w.cm, w.bm);
@@ -669,22 +670,31 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   w.bm &= valid;
   w.lm = valid & ~(w.om | w.cm);
   uint32_t S = 0, plo = 0, phi = 0, mlo = 0, mhi = 0, ext = 0, ucm = 0, mcb = 0;
+#pragma unroll 1
+  for (int q = 0; q < K / 4; q++) {
+    const bool lo = q < 2;  // warp-uniform
 #pragma unroll
-  for (int i = 0; i < K; i++) {
-    const uint32_t bit = 1u << i;
-    const int top = 31 - __clz(S);  // -1 when the thread stack is empty
-    if (i < 8) plo |= (uint32_t)(top & 15) << (4 * i);
-    else phi |= (uint32_t)(top & 15) << (4 * (i - 8));
-    ext |= S ? 0u : bit;
-    const bool pop = (w.cm & bit) && S;
-    ucm |= ((w.cm & bit) && !S) ? bit : 0u;
-    mcb |= (pop && ((w.bm >> top) & 1u)) ? bit : 0u;
-    const uint32_t pv = (uint32_t)i << (4 * (top & 7));
-    mlo |= (pop && top < 8) ? pv : 0u;
-    mhi |= (pop && top >= 8) ? pv : 0u;
-    if (i < 8) mlo |= pop ? (uint32_t)top << (4 * i) : 0u;  // the close's own partner
-    else mhi |= pop ? (uint32_t)top << (4 * (i - 8)) : 0u;
-    S = (w.om & bit) ? (S | bit) : (pop ? (S ^ (1u << top)) : S);
+    for (int j = 0; j < 4; j++) {
+      const int i = 4 * q + j;
+      const int sh = 4 * (i & 7);
+      const uint32_t bit = 1u << i;
+      const int top = 31 - __clz(S);  // -1 when the thread stack is empty
+      const uint32_t pn = (uint32_t)(top & 15) << sh;
+      if (lo) plo |= pn;
+      else phi |= pn;
+      ext |= S ? 0u : bit;
+      const bool pop = (w.cm & bit) && S;
+      ucm |= ((w.cm & bit) && !S) ? bit : 0u;
+      mcb |= (pop && ((w.bm >> top) & 1u)) ? bit : 0u;
+      // partner nibbles: the open's (at the pop) and the close's own
+      const uint32_t pv = pop ? (uint32_t)i << (4 * (top & 7)) : 0u;
+      mlo |= top < 8 ? pv : 0u;
+      mhi |= top >= 8 ? pv : 0u;
+      const uint32_t cv = pop ? pn : 0u;
+      if (lo) mlo |= cv;
+      else mhi |= cv;
+      S = (w.om & bit) ? (S | bit) : (pop ? (S ^ (1u << top)) : S);
+    }
   }
   w.S = S;
   w.plo = plo;
@@ -944,51 +954,56 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
     const bool u15 = (w.ucm >> (K - 1)) & 1u;
     const float4 v15 = s.val[sb ^ (K - 1)];
     if (!u15) s.val[sb ^ (K - 1)] = TL;
-    int pv[4];
+#pragma unroll 1
+    for (int q = 0; q < K / 4; q++) {
+      const uint32_t pw4 = q < 2 ? w.plo : w.phi, mw4 = q < 2 ? w.mlo : w.mhi;
+      int pv[4];
 #pragma unroll
-    for (int i = 0; i < K; i++) {
-      const uint32_t bit = 1u << i;
-      const bool isL = (w.lm & bit) != 0u, isB = (w.bm & bit) != 0u;
-      const bool isO = (w.om & bit) != 0u, isC = (w.cm & bit) != 0u, isU = (w.ucm & bit) != 0u;
-      const bool isUO = (w.S & bit) != 0u;
-      const bool isMC = isC && !isU;
-      float4 v = s.val[sb ^ i];
-      if (i == K - 1 && !isMC) v = v15;
-      const int pn = nib(w.plo, w.phi, i);
-      const int pt = nib(w.mlo, w.mhi, i);
-      const bool isx = (w.ext & bit) != 0u;
-      const uint32_t nc = w.ucm & ~(bit - 1u);  // unmatched closes at or after i
-      const int j = nc ? __ffs(nc) - 1 : K - 1;  // the next one: c_d of element i's depth d (none: TL)
-      // a close takes nothing from its parent: clipped = v (INF slot not needed, v ∩ v = v)
-      const int cidx = isC ? (sb ^ i) : (isx ? (sb ^ j) : (sb ^ pn));
-      const float4 cpar = s.val[cidx];
-      const int mj = s.matchS[mb + j];
-      const int par = isx ? (nc ? mj : giLast) : gtb + pn;
-      const float4 clipped = isect(v, cpar);
-      // own slot: leaf / clip open -> clipped; blend open -> parent context;
-      // close -> union (in-thread node) / prefix (outer node) / EMPTY (R3)
-      float4 o = isB ? cpar : clipped;
-      o = isC ? ((isU && par < 0) ? bEMPTY() : acc) : o;
-      s.val[sb ^ i] = o;
-      if (isO) {
-        const int k = __popc(w.S & (bit - 1u));
-        float4* dst = isUO ? &s.u.rbuf[min(k, RCAP - 1)][tid] : &s.val[sb ^ pt];
-        if (!isUO || k < RCAP) *dst = acc;
+      for (int jq = 0; jq < 4; jq++) {
+        const int i = 4 * q + jq;
+        const uint32_t bit = 1u << i;
+        const bool isL = (w.lm & bit) != 0u, isB = (w.bm & bit) != 0u;
+        const bool isO = (w.om & bit) != 0u, isC = (w.cm & bit) != 0u, isU = (w.ucm & bit) != 0u;
+        const bool isUO = (w.S & bit) != 0u;
+        const bool isMC = isC && !isU;
+        float4 v = s.val[sb ^ i];
+        if (jq == 3 && q == K / 4 - 1 && !isMC) v = v15;
+        const int sh = 4 * ((q & 1) * 4 + jq);
+        const int pn = (int)((pw4 >> sh) & 15u);
+        const int pt = (int)((mw4 >> sh) & 15u);
+        const bool isx = (w.ext & bit) != 0u;
+        const uint32_t nc = w.ucm & ~(bit - 1u);  // unmatched closes at or after i
+        const int j = nc ? __ffs(nc) - 1 : K - 1;  // the next one: c_d of element i's depth d (none: TL)
+        // a close takes nothing from its parent (clipped = v ∩ v = v)
+        const int cidx = isC ? (sb ^ i) : (isx ? (sb ^ j) : (sb ^ pn));
+        const float4 cpar = s.val[cidx];
+        const int mj = s.matchS[mb + j];
+        const int par = isx ? (nc ? mj : giLast) : gtb + pn;
+        const float4 clipped = isect(v, cpar);
+        // own slot: leaf / clip open -> clipped; blend open -> parent context;
+        // close -> union (in-thread node) / prefix (outer node) / EMPTY (R3)
+        float4 o = isB ? cpar : clipped;
+        o = isC ? ((isU && par < 0) ? bEMPTY() : acc) : o;
+        s.val[sb ^ i] = o;
+        if (isO) {
+          const int k = __popc(w.S & (bit - 1u));
+          float4* dst = isUO ? &s.u.rbuf[min(k, RCAP - 1)][tid] : &s.val[sb ^ pt];
+          if (!isUO || k < RCAP) *dst = acc;
+        }
+        if ((w.mcb & bit) != 0u) s.val[sb ^ pn] = acc;
+        const float4 add = (isL || isMC) ? clipped : bEMPTY();
+        acc = unite(acc, add);
+        acc = isO ? bEMPTY() : acc;
+        if (PM && !(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + pt;
+        pv[jq] = par;
       }
-      if ((w.mcb & bit) != 0u) s.val[sb ^ pn] = acc;
-      const float4 add = (isL || isMC) ? clipped : bEMPTY();
-      acc = unite(acc, add);
-      acc = isO ? bEMPTY() : acc;
-      if (PM && !(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + pt;
-      pv[i & 3] = par;
-      if (PM && (i & 3) == 3) {
-        const int q4 = i >> 2;
-        if (nv_t >= 4 * q4 + 4) {
-          __stcs(reinterpret_cast<int4*>(p.parent + base + tl0) + q4, make_int4(pv[0], pv[1], pv[2], pv[3]));
+      if (PM) {
+        if (nv_t >= 4 * q + 4) {
+          __stcs(reinterpret_cast<int4*>(p.parent + base + tl0) + q, make_int4(pv[0], pv[1], pv[2], pv[3]));
         } else {
 #pragma unroll
           for (int jj = 0; jj < 4; jj++)
-            if (4 * q4 + jj < nv_t) p.parent[base + tl0 + 4 * q4 + jj] = pv[jj];
+            if (4 * q + jj < nv_t) p.parent[base + tl0 + 4 * q + jj] = pv[jj];
         }
       }
     }
