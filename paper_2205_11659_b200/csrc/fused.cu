@@ -31,7 +31,12 @@
 //              closed (R4) get the union of everything after them.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "boxes.cuh"
 #include "common.cuh"
@@ -78,6 +83,14 @@ struct Params {
   int32_t* blkmin;     // [gridDim of fz_ctrl] min low-water mark of the block's tiles
   int chunk;           // fz_ctrl: tiles per block (multiple of 32)
   uint64_t* trace;     // optional (debug): fz_ctrl phase timestamps, block 0
+  int use_tma;         // fz_main: full tiles move their boxes with TMA (tensor maps below)
+};
+// TMA descriptors of fz_main: per array (leaf boxes in, node boxes out) one 2D
+// map per half of the thread rows: {32 floats, n/16 rows}, row stride 256 B,
+// box {32, NT}, 128-byte swizzle (the slot layout of Smem::val)
+struct Maps {
+  CUtensorMap in[2];
+  CUtensorMap out[2];
 };
 constexpr int MAXCTRL = 4096;  // fz_ctrl blocks (co-resident CTAs) provided for
 constexpr int RMAX = 8;        // runs of the incoming stack kept per tile (more: followed in fz_main)
@@ -150,6 +163,7 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.blkmin = (int32_t*)(b + L.blkmin);
   p.chunk = 32;
   p.trace = nullptr;
+  p.use_tma = 0;
   return p;
 }
 
@@ -707,7 +721,8 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   return w;
 }
 
-constexpr int RCAP = 7;  // segment unions kept per thread (more unmatched opens: recomputed in H1)
+constexpr int RCAP = 7;      // segment unions kept per thread (more unmatched opens: recomputed in H1)
+constexpr int INCCAP = 192;  // incoming entries cached in shared memory (deeper ones: read from global)
 
 // Shared memory of fz_main (<= 56 KB: four CTAs per SM).  The scratch region u
 // is reused phase by phase: B-C owner windows; D link contexts; (l, uo, link
@@ -726,6 +741,10 @@ struct Smem {
       int l[NT];                    // kept B-E
       uint32_t uo[NT];
       int link[NT];
+      int inc_idx[INCCAP];          // A-E: incoming entries at depth D < INCCAP (cp.async): slice_idx value (-1: root)
+      int inc_ref[INCCAP];          //      slice reference
+      float4 inc_box[INCCAP];       //      lc
+      float4 inc_tc[INCCAP];        //      TC of the owner tile
     } pj;
     float4 rbuf[RCAP][NT];          // F-H1: the accumulator at each thread-unmatched open (k < RCAP)
     struct {
@@ -735,6 +754,7 @@ struct Smem {
     } rt;
   } u;
   int2 runs[RMAX];
+  uint64_t mbar;                    // TMA completion of the box tile
   uint32_t bmS[NT];                 // blend opens of each thread
   float4 wtu[NW];                   // warp unions
   float4 wmid[NW][NW];              // union of the warps strictly between
@@ -742,9 +762,16 @@ struct Smem {
 };
 static_assert(sizeof(Smem) <= 56 * 1024, "four CTAs per SM");
 
-// element i of thread t lives at slot (t*K | t & 7) ^ i: conflict-free for the
-// per-thread accesses (8 lanes, distinct t & 7) and for the coalesced copies
-__device__ __forceinline__ int slot_of(int e) { return e ^ (int)(((unsigned)e >> LOGK) & 7u); }
+// Box slots: the tile as two halves (elements 0-7 and 8-15 of every thread),
+// each NT rows of 128 bytes with the TMA 128-byte swizzle: element i of thread
+// t lives at slot (i / 8) * 8 NT + 8 t + ((i mod 8) ^ (t mod 8)).  One TMA box
+// per half moves a whole tile; the per-thread accesses are conflict-free (8
+// lanes, distinct t mod 8).
+__device__ __forceinline__ int slot_of(int e) {
+  const int t = e >> LOGK, i = e & (K - 1);
+  return ((i & 8) << 7) | (t << 3) | ((i & 7) ^ (t & 7));
+}
+static_assert(NT * 8 == 1024 && K == 16, "slot layout");
 __device__ __forceinline__ int mpad(int e) { return e + (int)((unsigned)e >> LOGK); }
 
 // union of the clipped leaves of whole threads [a, b] (F4): inside one warp two
@@ -760,6 +787,47 @@ __device__ __forceinline__ float4 range_threads(const Smem& s, int a, int b) {
     return unite(s.u.rt.win[k][b], s.u.rt.win[k][a + (1 << k) - 1]);
   }
   return unite(unite(s.u.rt.suf[a], s.u.rt.pre[b]), s.wmid[wa][wb]);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred pr; mbarrier.try_wait.parity.shared::cta.b64 pr, [%1], %2; selp.u32 %0, 1, 0, pr; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(src)
+               : "memory");
 }
 
 // slice reference (owner tile * W + slice position) of the entry at height h
@@ -783,7 +851,7 @@ __device__ __forceinline__ int inc_ref(const Params& p, const Smem& s, int nruns
 #define FZ_MINB 4
 #endif
 template <bool PM>
-__global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
+__global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_constant__ Maps maps) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -793,7 +861,8 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   const int gbase = (int)base;  // global indices fit in int32 (n <= 2^31 - 1)
   const int tl0 = tid * K;      // tile-local index of the thread's first element
   const int gtb = gbase + tl0;
-  const int sb = (tid << LOGK) | (tid & 7);  // slot(tid, i) = sb ^ i
+  const int sb = (tid << 3) | (tid & 7);  // slot(tid, i) = ((i & 8) << 7) | (sb ^ (i & 7))
+  auto sl = [sb](int i) { return ((i & 8) << 7) | (sb ^ (i & 7)); };
   const int mb = mpad(tl0);                  // matchS index of element i = mb + i
 
   // ---- A. loads, register walk -------------------------------------------------
@@ -801,13 +870,30 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   const int H = __ldg(p.ctrl.hstart + T);
   const int aT = __ldg(p.ctrl.agg + T).x;
   const int64_t poff = __ldg(p.aoff + T);  // pop records of this tile: [poff, poff + a_T)
-#pragma unroll
-  for (int j = 0; j < K; j++) {
-    const int e = j * NT + tid;
-    s.val[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bEMPTY();
+  // the boxes of a full tile arrive by TMA (two 16 KB boxes, one per half of
+  // the thread rows); the last, partial tile is copied by the threads
+  const uint32_t val_sa = smem_u32(&s.val[0]), mbar = smem_u32(&s.mbar);
+  const bool tma = p.use_tma && nvalid == W && (val_sa & 1023u) == 0u;
+  if (tma) {
+    if (tid == 0) {
+      mbar_init(mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(mbar, 2 * NT * 128);
+      tma_load_2d(val_sa, &maps.in[0], 0, T * NT, mbar);
+      tma_load_2d(val_sa + NT * 128, &maps.in[1], 0, T * NT, mbar);
+    }
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < K; j++) {
+      const int e = j * NT + tid;
+      s.val[slot_of(e)] = e < nvalid ? __ldg(p.boxes + base + e) : bEMPTY();
+    }
   }
   // the tile's incoming stack as runs of one owner tile each (fz_ctrl)
-  if (tid < RMAX) s.runs[tid] = __ldg(p.runs + (int64_t)T * RMAX + tid);
+  if (tid < RMAX) {
+    cp_async8(smem_u32(&s.runs[tid]), p.runs + (int64_t)T * RMAX + tid);
+    cp_async_commit();
+  }
   const int nruns = __ldg(p.nruns + T);
   const int nv_t = nvalid - tl0;
   const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
@@ -815,6 +901,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   const int a_t = __popc(w.ucm), b_t = __popc(w.S);
 
   // ---- B. block Bic scan: relative height at the thread start, low-water mark
+  if (tid < RMAX) cp_async_wait_all();
   Bic ex, sx, tot;
   block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, false);
   const int r_t = ex.b - ex.a;
@@ -834,18 +921,44 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   __syncthreads();
 
   // ---- C. thread-level owner lookups (F2); lc of the thread-unmatched opens --
-  const int top_ref = thread_ref<NW, K>(wl, l_t, w.S, r_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.u.pj.l, s.u.pj.uo);
-  const int lk = thread_ref<NW, K>(wl, l_t, w.S, l_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.u.pj.l, s.u.pj.uo);
+  // the incoming entries at depths D < INCCAP, fetched asynchronously (used in D-E)
+  const int ninc = min(aT + 1, INCCAP);
+  for (int D = tid; D < ninc; D += NT) {
+    const int h = H - 1 - D;
+    if (h < 0) {
+      s.u.pj.inc_idx[D] = -1;
+      s.u.pj.inc_ref[D] = -1;
+      s.u.pj.inc_box[D] = bINF();
+      s.u.pj.inc_tc[D] = bINF();
+    } else {
+      const int ref = inc_ref(p, s, nruns, h);
+      s.u.pj.inc_ref[D] = ref;
+      cp_async4(smem_u32(&s.u.pj.inc_idx[D]), p.slice_idx + ref);
+      cp_async16(smem_u32(&s.u.pj.inc_box[D]), p.slice_box + ref);
+      cp_async16(smem_u32(&s.u.pj.inc_tc[D]), p.tc + (ref >> LOGW));
+    }
+  }
+  cp_async_commit();
+  int top_ref = 0, lk = 0;
+#pragma unroll 1
+  for (int qq = 0; qq < 2; qq++) {  // one inlined copy of the lookup
+    const int r = thread_ref<NW, K>(wl, l_t, w.S, qq ? l_t - 1 : r_t - 1, s.u.ref.lwin, s.u.ref.lwmin, s.u.pj.l,
+                                    s.u.pj.uo);
+    if (qq) lk = r;
+    else top_ref = r;
+  }
   s.u.pj.link[tid] = lk;
+  if (tma) mbar_wait(mbar, 0);
   {
     float4 acc = bINF();
     for (uint32_t q = w.S; q; q &= q - 1) {
       const int i = __ffs(q) - 1;
-      float4& v = s.val[sb ^ i];
+      float4& v = s.val[sl(i)];
       if (!((w.bm >> i) & 1u)) acc = isect(acc, v);
       v = acc;
     }
   }
+  cp_async_wait_all();
   __syncthreads();
 
   // ---- D. context of each thread's link: TL(t) = lc(link) ∩ TL(thread of link)
@@ -863,9 +976,14 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       const int D = -lk - 1;
       giLast = -1;
       if (H - 1 - D >= 0) {
-        const int ref = inc_ref(p, s, nruns, H - 1 - D);
-        giLast = __ldg(p.slice_idx + ref) & 0x7fffffff;
-        acc = isect(__ldg(p.slice_box + ref), __ldg(p.tc + (ref >> LOGW)));
+        if (D < INCCAP) {
+          giLast = s.u.pj.inc_idx[D] & 0x7fffffff;
+          acc = isect(s.u.pj.inc_box[D], s.u.pj.inc_tc[D]);
+        } else {
+          const int ref = inc_ref(p, s, nruns, H - 1 - D);
+          giLast = __ldg(p.slice_idx + ref) & 0x7fffffff;
+          acc = isect(__ldg(p.slice_box + ref), __ldg(p.tc + (ref >> LOGW)));
+        }
       }
     }
     int cb = 0;
@@ -907,7 +1025,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       icm |= 1u << ci;
       s.matchS[mb + ci] = gbase + ref;
       s.matchS[mpad(ref)] = gtb + ci;
-      if (seg & needm) s.val[sb ^ ci] = isect(s.val[slot_of(ref)], s.u.pj.acc[cbf][ref >> LOGK]);
+      if (seg & needm) s.val[sl(ci)] = isect(s.val[slot_of(ref)], s.u.pj.acc[cbf][ref >> LOGK]);
       const int V = ref >> LOGK;
       const uint32_t below = s.u.pj.uo[V] & ((1u << (ref & (K - 1))) - 1u);
       ref = below ? (V << LOGK) + 31 - __clz(below) : s.u.pj.link[V];
@@ -923,18 +1041,25 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       int gi = -1;
       float4 cx = bINF();
       if (H - 1 - D >= 0) {
-        const int rf = inc_ref(p, s, nruns, H - 1 - D);
-        const int si = __ldg(p.slice_idx + rf);
+        int rf, si;
+        if (D < INCCAP) {
+          rf = s.u.pj.inc_ref[D];
+          si = s.u.pj.inc_idx[D];
+          if (seg & needm) cx = isect(s.u.pj.inc_box[D], s.u.pj.inc_tc[D]);
+        } else {
+          rf = inc_ref(p, s, nruns, H - 1 - D);
+          si = __ldg(p.slice_idx + rf);
+          if (seg & needm) cx = isect(__ldg(p.slice_box + rf), __ldg(p.tc + (rf >> LOGW)));
+        }
         gi = si & 0x7fffffff;
         if (!xcm) dx0 = D;
         xcm |= 1u << ci;
         p.pop[poff + D] = make_int4(gtb + ci, gi, rf, si < 0);
-        if (seg & needm) cx = isect(__ldg(p.slice_box + rf), __ldg(p.tc + (rf >> LOGW)));
       } else {
         p.pop[poff + D] = make_int4(-1, -1, -1, 0);  // pops the root (R3)
       }
       s.matchS[mb + ci] = gi;
-      if (seg & needm) s.val[sb ^ ci] = cx;
+      if (seg & needm) s.val[sl(ci)] = cx;
     }
   }
   __syncthreads();
@@ -952,8 +1077,8 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   float4 acc = bEMPTY();
   {
     const bool u15 = (w.ucm >> (K - 1)) & 1u;
-    const float4 v15 = s.val[sb ^ (K - 1)];
-    if (!u15) s.val[sb ^ (K - 1)] = TL;
+    const float4 v15 = s.val[sl(K - 1)];
+    if (!u15) s.val[sl(K - 1)] = TL;
 #pragma unroll 1
     for (int q = 0; q < K / 4; q++) {
       const uint32_t pw4 = q < 2 ? w.plo : w.phi, mw4 = q < 2 ? w.mlo : w.mhi;
@@ -966,7 +1091,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
         const bool isO = (w.om & bit) != 0u, isC = (w.cm & bit) != 0u, isU = (w.ucm & bit) != 0u;
         const bool isUO = (w.S & bit) != 0u;
         const bool isMC = isC && !isU;
-        float4 v = s.val[sb ^ i];
+        float4 v = s.val[sl(i)];
         if (jq == 3 && q == K / 4 - 1 && !isMC) v = v15;
         const int sh = 4 * ((q & 1) * 4 + jq);
         const int pn = (int)((pw4 >> sh) & 15u);
@@ -975,7 +1100,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
         const uint32_t nc = w.ucm & ~(bit - 1u);  // unmatched closes at or after i
         const int j = nc ? __ffs(nc) - 1 : K - 1;  // the next one: c_d of element i's depth d (none: TL)
         // a close takes nothing from its parent (clipped = v ∩ v = v)
-        const int cidx = isC ? (sb ^ i) : (isx ? (sb ^ j) : (sb ^ pn));
+        const int cidx = isC ? sl(i) : (isx ? sl(j) : sl(pn));
         const float4 cpar = s.val[cidx];
         const int mj = s.matchS[mb + j];
         const int par = isx ? (nc ? mj : giLast) : gtb + pn;
@@ -984,13 +1109,13 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
         // close -> union (in-thread node) / prefix (outer node) / EMPTY (R3)
         float4 o = isB ? cpar : clipped;
         o = isC ? ((isU && par < 0) ? bEMPTY() : acc) : o;
-        s.val[sb ^ i] = o;
+        s.val[sl(i)] = o;
         if (isO) {
           const int k = __popc(w.S & (bit - 1u));
-          float4* dst = isUO ? &s.u.rbuf[min(k, RCAP - 1)][tid] : &s.val[sb ^ pt];
+          float4* dst = isUO ? &s.u.rbuf[min(k, RCAP - 1)][tid] : &s.val[sl(pt)];
           if (!isUO || k < RCAP) *dst = acc;
         }
-        if ((w.mcb & bit) != 0u) s.val[sb ^ pn] = acc;
+        if ((w.mcb & bit) != 0u) s.val[sl(pn)] = acc;
         const float4 add = (isL || isMC) ? clipped : bEMPTY();
         acc = unite(acc, add);
         acc = isO ? bEMPTY() : acc;
@@ -1012,11 +1137,12 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   const bool ovf = b_t > RCAP;
   float4 tu = acc;
   if (!ovf) {
+#pragma unroll 1
     for (int k = 0; k < b_t; k++) tu = unite(tu, s.u.rbuf[k][tid]);
   } else {
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < K; i++)
-      if ((w.lm >> i) & 1u) tu = unite(tu, s.val[sb ^ i]);
+      if ((w.lm >> i) & 1u) tu = unite(tu, s.val[sl(i)]);
   }
   // warp-level prefix / suffix of the thread unions, warp totals
   float4 pw = tu, sw = tu;
@@ -1033,6 +1159,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
   if (tid < NW * NW) {
     const int x = tid / NW, y = tid % NW;
     float4 m = bEMPTY();
+#pragma unroll 1
     for (int w2 = x + 1; w2 < y; w2++) m = unite(m, s.wtu[w2]);
     s.wmid[x][y] = m;
   }
@@ -1085,14 +1212,14 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
           handle(i, k, R);
           k--;
         } else if (w.lm & bit) {
-          R = unite(R, s.val[sb ^ i]);
+          R = unite(R, s.val[sl(i)]);
         }
       }
     }
   }
   if (xcm) {
     int D = dx0;
-    for (uint32_t q = xcm; q; q &= q - 1, D++) p.popu[poff + D] = unite(s.val[sb ^ (__ffs(q) - 1)], pre);
+    for (uint32_t q = xcm; q; q &= q - 1, D++) p.popu[poff + D] = unite(s.val[sl(__ffs(q) - 1)], pre);
   }
   if (tid == 0) {
     float4 t = s.wtu[0];
@@ -1124,18 +1251,27 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
     const int ci = __ffs(q) - 1;
     const int o = s.matchS[mb + ci] - gbase;
     const int to = o >> LOGK;
-    float4& cv = s.val[sb ^ ci];
+    float4& cv = s.val[sl(ci)];
     const float4 U = unite(cv, range_threads(s, to + 1, tid - 1));
     cv = U;
     if ((s.bmS[to] >> (o & (K - 1))) & 1u) s.val[slot_of(o)] = U;
   }
+  if (tma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> the TMA store
   __syncthreads();
 
-  // ---- I. coalesced copy-out -------------------------------------------------
-#pragma unroll
-  for (int j = 0; j < K; j++) {
-    const int e = j * NT + tid;
-    if (e < nvalid) __stcs(p.out + base + e, s.val[slot_of(e)]);
+  // ---- I. copy-out: node boxes by TMA (full tiles), match coalesced ---------
+  if (tma) {
+    if (tid == 0) {
+      tma_store_2d(&maps.out[0], 0, T * NT, val_sa);
+      tma_store_2d(&maps.out[1], 0, T * NT, val_sa + NT * 128);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < K; j++) {
+      const int e = j * NT + tid;
+      if (e < nvalid) __stcs(p.out + base + e, s.val[slot_of(e)]);
+    }
   }
   if (PM) {
 #pragma unroll
@@ -1152,6 +1288,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p) {
       }
     }
   }
+  if (tma && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ----------------------------------------------------------------------------
@@ -1275,6 +1412,41 @@ __global__ void __launch_bounds__(128) fz_close(Params p) {
 // ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }
+  return fn;
+}
+
+// the four maps of fz_main over boxes / node_bbox (full thread rows only: the
+// partial last tile never uses them); false: TMA unavailable
+static bool make_maps(const float* boxes, float* out, int64_t n, Maps& m) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encode_fn();
+  const uint64_t rows = (uint64_t)(n / K);
+  if (!enc || rows < (uint64_t)NT) return false;
+  const cuuint64_t dims[2] = {32, rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 16};
+  const cuuint32_t box[2] = {32, NT};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int h = 0; h < 2; h++) {
+    CUresult r = enc(&m.in[h], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)(boxes + 32 * h), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    r = enc(&m.out[h], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)(out + 32 * h), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+  }
+  return true;
+}
+
 static int ctrl_blocks() {  // co-resident CTAs of the cooperative kernel
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
@@ -1304,9 +1476,24 @@ static cudaError_t setup() {
 
 static uint64_t* g_fz_trace = nullptr;  // debug hook (tb_debug_fz_trace)
 void fused_set_trace(uint64_t* dev) { g_fz_trace = dev; }
+static int g_fz_tma = 1;  // debug hook (tb_debug_fz_tma): 0 = the threads copy every tile
+int fused_set_tma(int on) {
+  const int old = g_fz_tma;
+  if (on >= 0) g_fz_tma = on;
+  return old;
+}
 
 size_t fused_workspace_bytes(int64_t n) { return n > 0 ? fz::Layout(n).bytes : 0; }
 int fused_tile_elems() { return fz::W; }
+
+// debug: TB_FZ_SYNC=1 synchronises after every launch and names the failing one
+static cudaError_t dbg_sync(cudaStream_t s, const char* what) {
+  static const bool on = getenv("TB_FZ_SYNC") != nullptr;
+  if (!on) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) fprintf(stderr, "fused: %s failed: %s\n", what, cudaGetErrorString(e));
+  return e;
+}
 
 cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, int32_t* match, int32_t* parent,
                          float* node_bbox, void* ws, cudaStream_t stream) {
@@ -1319,6 +1506,7 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
   const int nt = p.ntiles;
   TB_LAUNCH(stream, "fz_reduce", (fz::fz_reduce<<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
   e = cudaGetLastError();
+  if (e == cudaSuccess) e = dbg_sync(stream, "fz_reduce");
   if (e != cudaSuccess) return e;
   {
     // enough blocks for the per-tile warps of P3 / P5, at most the co-resident
@@ -1330,25 +1518,34 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
     prof_begin(stream, "fz_ctrl", &tok);
     e = cudaLaunchCooperativeKernel((const void*)fz::fz_ctrl, dim3(G), dim3(fz::NTC), args, 0, stream);
     prof_end(stream, tok);
+    if (e == cudaSuccess) e = dbg_sync(stream, "fz_ctrl");
     if (e != cudaSuccess) return e;
   }
+  fz::Maps maps;
+  memset(&maps, 0, sizeof maps);
+  p.use_tma = g_fz_tma && fz::make_maps(leaf_bbox, node_bbox, n, maps) ? 1 : 0;
   if (pm)
-    TB_LAUNCH(stream, "fz_main", (fz::fz_main<true><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p)));
+    TB_LAUNCH(stream, "fz_main", (fz::fz_main<true><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p, maps)));
   else
-    TB_LAUNCH(stream, "fz_main", (fz::fz_main<false><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p)));
+    TB_LAUNCH(stream, "fz_main", (fz::fz_main<false><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p, maps)));
   e = cudaGetLastError();
+  if (e == cudaSuccess) e = dbg_sync(stream, "fz_main");
   if (e != cudaSuccess) return e;
   int m = nt;
   for (int k = 1; k < fz::LV && m > 1; k++) {
     const int groups = (m + 31) / 32;
     TB_LAUNCH(stream, "fz_hier", (fz::fz_hier<<<(unsigned)((groups + 7) / 8), 256, 0, stream>>>(p, k, m)));
+    e = dbg_sync(stream, "fz_hier");
+    if (e != cudaSuccess) return e;
     m = groups;
   }
   if (pm)
     TB_LAUNCH(stream, "fz_close", (fz::fz_close<true><<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
   else
     TB_LAUNCH(stream, "fz_close", (fz::fz_close<false><<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = dbg_sync(stream, "fz_close");
+  return e;
 }
 
 }  // namespace tb

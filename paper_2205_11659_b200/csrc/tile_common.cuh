@@ -24,6 +24,7 @@ struct Walk16 {
 __device__ __forceinline__ uint4 load_tags16(const uint8_t* tags, int64_t n, int64_t tbase, bool full) {
   if (full) return ld_stream_v4(tags + tbase);
   uint32_t wv[4] = {0, 0, 0, 0};
+#pragma unroll 1
   for (int i = 0; i < 16; i++) {
     const int64_t g = tbase + i;
     const uint32_t v = g < n ? tags[g] : 0u;  // padding = leaf = Bic identity

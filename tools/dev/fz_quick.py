@@ -45,6 +45,8 @@ def cases():
 def check():
     fails = 0
     for name, t in cases():
+        if os.environ.get("FZ_VERBOSE"):
+            print("case", name, flush=True)
         t = t.contiguous()
         n = t.numel()
         b = scenegen.boxes(n, 7, t)
@@ -123,6 +125,10 @@ if __name__ == "__main__":
     rc = 0
     if what in ("check", "both"):
         rc = check()
+    if what in ("notma",):
+        tb.load().tb_debug_fz_tma(0)
+        rc = check()
+        tb.load().tb_debug_fz_tma(1)
     if what in ("time", "both"):
         timing(int(sys.argv[2]) if len(sys.argv) > 2 else 27)
     sys.exit(1 if rc else 0)
