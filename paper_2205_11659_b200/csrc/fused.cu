@@ -31,6 +31,7 @@
 //              closed (R4) get the union of everything after them.
 #include <algorithm>
 #include <climits>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -761,6 +762,9 @@ struct Smem {
   Bic wtot[NW];
 };
 static_assert(sizeof(Smem) <= 56 * 1024, "four CTAs per SM");
+// rbuf addressed as val[RB0 + k * NT + t] (both arrays of float4 in one shared block)
+constexpr int RB0 = (int)((offsetof(Smem, u) - offsetof(Smem, val)) / sizeof(float4));
+static_assert((offsetof(Smem, u) - offsetof(Smem, val)) % sizeof(float4) == 0, "rbuf alignment");
 
 // Box slots: the tile as two halves (elements 0-7 and 8-15 of every thread),
 // each NT rows of 128 bytes with the TMA 128-byte swizzle: element i of thread
@@ -862,7 +866,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   const int tl0 = tid * K;      // tile-local index of the thread's first element
   const int gtb = gbase + tl0;
   const int sb = (tid << 3) | (tid & 7);  // slot(tid, i) = ((i & 8) << 7) | (sb ^ (i & 7))
-  auto sl = [sb](int i) { return ((i & 8) << 7) | (sb ^ (i & 7)); };
+  auto sl = [sb](int i) { return (sb ^ (i & 7)) | ((i << 7) & 1024); };
   const int mb = mpad(tl0);                  // matchS index of element i = mb + i
 
   // ---- A. loads, register walk -------------------------------------------------
@@ -1100,7 +1104,8 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         const uint32_t nc = w.ucm & ~(bit - 1u);  // unmatched closes at or after i
         const int j = nc ? __ffs(nc) - 1 : K - 1;  // the next one: c_d of element i's depth d (none: TL)
         // a close takes nothing from its parent (clipped = v ∩ v = v)
-        const int cidx = isC ? sl(i) : (isx ? sl(j) : sl(pn));
+        const int spn = sl(pn);
+        const int cidx = isC ? sl(i) : sl(isx ? j : pn);
         const float4 cpar = s.val[cidx];
         const int mj = s.matchS[mb + j];
         const int par = isx ? (nc ? mj : giLast) : gtb + pn;
@@ -1111,11 +1116,12 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         o = isC ? ((isU && par < 0) ? bEMPTY() : acc) : o;
         s.val[sl(i)] = o;
         if (isO) {
+          // the enclosing accumulator: into the close's slot, or rbuf for an open left open
           const int k = __popc(w.S & (bit - 1u));
-          float4* dst = isUO ? &s.u.rbuf[min(k, RCAP - 1)][tid] : &s.val[sl(pt)];
-          if (!isUO || k < RCAP) *dst = acc;
+          const int di = isUO ? RB0 + min(k, RCAP - 1) * NT + tid : sl(pt);
+          if (!isUO || k < RCAP) s.val[di] = acc;
         }
-        if ((w.mcb & bit) != 0u) s.val[sl(pn)] = acc;
+        if ((w.mcb & bit) != 0u) s.val[spn] = acc;
         const float4 add = (isL || isMC) ? clipped : bEMPTY();
         acc = unite(acc, add);
         acc = isO ? bEMPTY() : acc;
