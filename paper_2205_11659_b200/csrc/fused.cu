@@ -190,6 +190,19 @@ __device__ __forceinline__ void classify16b(uint4 raw, uint32_t& om, uint32_t& c
 // ----------------------------------------------------------------------------
 __device__ uint8_t g_unm4[UNM4_ENTRIES];  // common.cuh unm4_entry, filled once per device
 
+// position of the j-th (0-based) set bit of m (m has more than j set bits)
+__device__ __forceinline__ int select_bit32(uint32_t m, int j) {
+  int pos = 0, c = __popc(m & 0xffffu);
+  if (j >= c) { j -= c; pos = 16; m >>= 16; }
+  c = __popc(m & 0xffu);
+  if (j >= c) { j -= c; pos += 8; m >>= 8; }
+  c = __popc(m & 0xfu);
+  if (j >= c) { j -= c; pos += 4; m >>= 4; }
+  c = __popc(m & 0x3u);
+  if (j >= c) { j -= c; pos += 2; m >>= 2; }
+  return pos + (j >= (int)(m & 1u) ? 1 : 0);
+}
+
 constexpr int RL = W / 32;  // 64 elements per lane
 __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   __shared__ uint8_t bic4[256];  // Bic of 4 elements: index = open nibble | close nibble << 4; value a | b << 4
@@ -255,53 +268,67 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   if (lane == 31) sx = Bic{0, 0};
   if (lane == 0) p.ctrl.agg[T] = make_int2(tot.a, tot.b);
   // the lane's unmatched opens that survive to the tile end: its bottom s_l,
-  // at tile-relative heights l + k, slice position l + k + a_T
+  // at tile-relative heights l + k, slice positions [l + a_T, l + a_T + s_l)
   const int l = ex.b - ex.a - lb.a;
   const int s_l = max(lb.b - sx.a, 0);
-  uint32_t sv[2] = {0u, 0u};
+  uint32_t sv0 = 0u, sv1 = 0u;
   if (s_l > 0) {
-    uint32_t um[2];
     int P = 0;
-    um[1] = unm32(unm4, om[1], cm[1], P);
-    um[0] = unm32(unm4, om[0], cm[0], P);
-    int k = 0;
-#pragma unroll
-    for (int w = 0; w < 2; w++) {
-      uint32_t m = um[w];
-      while (m && k < s_l) {
-        const uint32_t low = m & (~m + 1u);
-        sv[w] |= low;
-        m ^= low;
-        k++;
-      }
+    const uint32_t um1 = unm32(unm4, om[1], cm[1], P);
+    const uint32_t um0 = unm32(unm4, om[0], cm[0], P);
+    const int c0 = __popc(um0);
+    if (s_l <= c0) {
+      sv0 = um0 & ((2u << select_bit32(um0, s_l - 1)) - 1u);
+    } else {
+      sv0 = um0;
+      sv1 = um1 & ((2u << select_bit32(um1, s_l - c0 - 1)) - 1u);
     }
   }
   // lc = ∩ of the clip boxes of the slice entries at and below each entry
-  // (blend opens pass the clip through, R7): lane aggregate, exclusive ∩-scan
-  float4 agg = bINF();
-#pragma unroll
-  for (int w = 0; w < 2; w++)
-    for (uint32_t q = sv[w] & ~bk[w]; q; q &= q - 1) agg = isect(agg, __ldg(p.boxes + lbase + 32 * w + __ffs(q) - 1));
-  float4 x = agg;
+  // (blend opens pass the clip through, R7), 32 slice positions at a time:
+  // position -> owning lane (the lanes' ranges are contiguous, in lane order)
+  // -> element, one gather per lane, an inclusive ∩-scan over the lanes
+  const int start = l + tot.a;
+  int endm = s_l > 0 ? start + s_l : 0;  // running max of the range ends
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    const float4 o = shfl_up_box(x, off);
-    if (lane >= off) x = isect(x, o);
+    const int y = __shfl_up_sync(0xffffffffu, endm, off);
+    if (lane >= off) endm = max(endm, y);
   }
-  float4 acc = shfl_up_box(x, 1);
-  if (lane == 0) acc = bINF();
-  int k = 0;
+  float4 carry = bINF();
+  for (int p0 = 0; p0 < tot.b; p0 += 32) {
+    const int pos = p0 + lane;
+    int L = 0;  // first lane with endm > pos
 #pragma unroll
-  for (int w = 0; w < 2; w++) {
-    for (uint32_t q = sv[w]; q; q &= q - 1) {
-      const int j = __ffs(q) - 1;
-      const int64_t e = lbase + 32 * w + j;
-      const uint32_t blend = (bk[w] >> j) & 1u;
-      if (!blend) acc = isect(acc, __ldg(p.boxes + e));
-      const int64_t pos = base + l + k + tot.a;
-      p.slice_idx[pos] = (int)((uint32_t)e | (blend << 31));
-      p.slice_box[pos] = acc;
-      k++;
+    for (int k = 4; k >= 0; k--) {
+      const int e = __shfl_sync(0xffffffffu, endm, L + (1 << k) - 1);
+      if (e <= pos) L += 1 << k;
+    }
+    L = min(L, 31);
+    const int ostart = __shfl_sync(0xffffffffu, start, L);
+    const uint32_t o0 = __shfl_sync(0xffffffffu, sv0, L), o1 = __shfl_sync(0xffffffffu, sv1, L);
+    const uint32_t b0 = __shfl_sync(0xffffffffu, bk[0], L), b1 = __shfl_sync(0xffffffffu, bk[1], L);
+    const bool act = pos < tot.b;
+    float4 v = bINF();
+    uint32_t e = 0u, blend = 0u;
+    if (act) {
+      const int k = pos - ostart, c0 = __popc(o0);
+      const int j = k < c0 ? select_bit32(o0, k) : 32 + select_bit32(o1, k - c0);
+      blend = ((j < 32 ? b0 : b1) >> (j & 31)) & 1u;
+      e = (uint32_t)(base + L * RL + j);
+      if (!blend) v = __ldg(p.boxes + e);
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float4 o = shfl_up_box(v, off);
+      if (lane >= off) v = isect(v, o);
+    }
+    v = isect(v, carry);
+    carry = make_float4(__shfl_sync(0xffffffffu, v.x, 31), __shfl_sync(0xffffffffu, v.y, 31),
+                        __shfl_sync(0xffffffffu, v.z, 31), __shfl_sync(0xffffffffu, v.w, 31));
+    if (act) {
+      p.slice_idx[base + pos] = (int)(e | (blend << 31));
+      p.slice_box[base + pos] = v;
     }
   }
 }

@@ -51,6 +51,8 @@ def main():
             out = torch.empty_like(boxes)
             med, mn = time_fn(lambda: tb.tree_bbox(tags, boxes, out), flush=flush)
             row.update({"tb_ms": med, "tb_Gelem_s": n / med / 1e6, "tb_GBs": 33 * n / med / 1e6})
+            med, mn = time_fn(lambda: tb.paren_match_tree_bbox(tags, boxes, m, p, out), flush=flush)
+            row.update({"pair_ms": med, "pair_Gelem_s": n / med / 1e6, "pair_GBs": 41 * n / med / 1e6})
         if args.transform and name.upper() != "J1":
             tb.paren_match(tags, m, p)
             loc = torch.zeros((n, 6), dtype=torch.float32, device="cuda")
