@@ -8,17 +8,19 @@ Workload (BASELINE.json metric "G elements/s for paren_match+tree_bbox"): the
 paper's random push/pop stream (configs[4], "random-depth stream"),
 synthetic, 2^27 elements per GPU (weak scaling; N = 8 is the 1B-element
 stream), 50 % leaves, 75 % of opens are clips, unbalanced tail kept.  One
-step = paren_match_tree_bbox over the resident stream: match / parent (as
-paren_match) and node_bbox (as tree_bbox_matched on them) in one device call,
-the box reduce pass overlapped with paren_match; N > 1: the sharded
-paren_match then tree_bbox_matched.  Inputs (2.2 GB
-per GPU) exceed the 126 MB L2, so no flush between steps.
+step = paren_match_tree_bbox over the resident stream: match, parent and
+node_bbox from one fused tile pass (csrc/fused.cu); N > 1: the sharded
+paren_match then tree_bbox_matched.  Inputs (2.2 GB per GPU) exceed the 126 MB
+L2, so no flush between steps.  --config C2|C3|C3L|C4 times another config of
+SURVEY §8(d) on one GPU (with an L2 flush between steps when it fits in L2).
 
 Printed (rank 0, one JSON line): value = elements x steps / max-over-ranks
 device time; roofline of the dominant kernel (algorithmic bytes / its
-event-timed duration vs the measured HBM copy peak); cpu_baseline = the
-oracle (single thread) on the host; e2e = the same metric through the
-host-buffer C-ABI calls (H2D + D2H inside the timed region).
+event-timed duration vs the measured HBM copy peak); calls = paren_match,
+tree_bbox and the pair timed separately (SURVEY §8(d) bytes: 9, 33, 42 per
+element, fractions of 8 TB/s and of the measured peak); cpu_baseline = the
+oracle (one pinned host thread, median of 3); e2e = the same metric through the
+host-buffer C-ABI call (H2D + D2H inside the timed region).
 """
 from __future__ import annotations
 
@@ -39,9 +41,15 @@ import torch  # noqa: E402
 
 METRIC = "G elements/s for paren_match+tree_bbox"
 UNIT = "Gelem/s"
-BYTES_PM = 9     # 1 B tag in, 4 B match + 4 B parent out
-BYTES_TB = 41    # tree_bbox_matched: 1 B tag + 16 B box + 4 B match + 4 B parent in, 16 B box out
-BYTES_PAIR = 41  # the step's own inputs and outputs: 1 B tag + 16 B box in; 4 + 4 + 16 B out
+BYTES_PM = 9     # paren_match: 1 B tag in, 4 B match + 4 B parent out
+BYTES_TB = 33    # tree_bbox: 1 B tag + 16 B box in, 16 B box out
+BYTES_PAIR = 42  # paren_match + tree_bbox as two calls
+NOMINAL_GBS = 8000.0  # the north star's roofline denominator (8 TB/s)
+# algorithmic bytes per element of each kernel (its share of the path's own
+# inputs / outputs; workspace traffic is not algorithmic and shows up in traffic)
+KERNEL_BYTES = {"fz_main": 41,     # tags + boxes in; match, parent, node_bbox out (the fused pass)
+                "fz_reduce": 1,    # tags
+                "pm_finish": 9, "pm_reduce": 1, "bbm_main": 33, "bbm_reduce": 1}
 
 
 def parse():
@@ -54,7 +62,31 @@ def parse():
     ap.add_argument("--seed", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default="C5", help="C5 (default, the metric's workload) or C2/C3/C3L/C4 (one GPU)")
+    ap.add_argument("--no-calls", action="store_true", help="skip the separate paren_match / tree_bbox timings")
     return ap.parse_args()
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def pin_one_core():
+    """Pin this process to one core for the oracle timing (restored after)."""
+    try:
+        old = os.sched_getaffinity(0)
+        core = min(old)
+        os.sched_setaffinity(0, {core})
+        return old, core
+    except Exception:
+        return None, None
 
 
 # ----------------------------------------------------------------------------
@@ -137,26 +169,83 @@ def profile_traffic():
 # ----------------------------------------------------------------------------
 # reference arm: the oracle on host cores
 # ----------------------------------------------------------------------------
-def bench_config(args, world):
+def bench_config(args, world, n=None, desc=None):
     """The workload description shared by both arms (the reference arm times a
     bounded sample of it, described in its cpu_baseline)."""
+    if args.config.upper() != "C5":
+        return {"workload": desc or args.config, "n_per_gpu": n, "config": args.config.upper(),
+                "l2": "L2 flushed (512 MB write) before every timed step" if n * 17 < (256 << 20)
+                else "inputs larger than L2; no flush",
+                "parallelism": "single GPU"}
     return {"workload": f"C5 random-depth walk stream, 2^{args.log2n} elements per GPU "
                         f"(global stream {world} x 2^{args.log2n}); 50% leaves, 75% clips",
-            "n_per_gpu": 1 << args.log2n, "seed": args.seed,
+            "n_per_gpu": 1 << args.log2n, "seed": args.seed, "config": "C5",
             "l2": "inputs (2.2 GB/GPU) larger than L2; no flush",
             "parallelism": f"contiguous shards x{world}" if world > 1 else "single GPU"}
+
+
+def make_inputs(args, rank, world, dev):
+    """Tags / boxes of the timed config, generated on the device (seeded)."""
+    import scenegen
+    if args.config.upper() != "C5":
+        tags, info = scenegen.config(args.config, device=dev)
+        tags = tags.to(dev)
+        n = tags.numel()
+        boxes = scenegen.boxes(n, args.seed, tags, device=dev)
+        return tags, boxes, n, info.get("workload")
+    n = 1 << args.log2n
+    offset = rank * n
+    s_before = sum(scenegen.walk_step_sum(n, args.seed, offset=r * n, device=dev) for r in range(rank))
+    tags = scenegen.walk_tags(n, args.seed, device=dev, offset=offset, s_before=s_before)
+    boxes = scenegen.boxes(n, args.seed, tags, offset=offset, device=dev)
+    return tags, boxes, n, None
+
+
+def oracle_seconds(tags_np, boxes_np, reps):
+    """The oracle (both walks) on one pinned host thread: median of reps runs."""
+    import numpy as np
+    import oracle
+    n = len(tags_np)
+    m_ = np.empty(n, np.int32)
+    p_ = np.empty(n, np.int32)
+    o_ = np.empty((n, 4), np.float32)
+    old, core = pin_one_core()
+    ts = []
+    try:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            oracle.paren_match(tags_np, m_, p_)
+            oracle.tree_bbox(tags_np, boxes_np, o_)
+            ts.append(time.perf_counter() - t0)
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+    return statistics.median(ts), core
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    import scenegen
+    dev = "cpu"
+    if args.config.upper() != "C5":
+        tags_t, info = scenegen.config(args.config)
+        desc = info.get("workload")
+    else:
+        tags_t, desc = None, None
+    if tags_t is None:
+        log2s = min(args.log2n, 24)
+        tags_t = scenegen.walk_tags(1 << log2s, args.seed)
+        sample = (f"first 2^{log2s} elements of the bench stream per step (the oracle, oracle/oracle.c -O2, "
+                  f"is sequential; its time is linear in the elements)")
+    else:
+        tags_t = tags_t[: 1 << 24].contiguous()
+        sample = f"first {tags_t.numel()} elements of {args.config.upper()} per step"
+    ns = tags_t.numel()
+    tags = tags_t.numpy()
+    boxes = scenegen.boxes(ns, args.seed, tags_t).numpy()
     import numpy as np
     import oracle
-    import scenegen
-    log2s = min(args.log2n, 24)
-    ns = 1 << log2s
-    tags = scenegen.walk_tags(ns, args.seed).numpy()
-    boxes = scenegen.boxes(ns, args.seed, torch.from_numpy(tags)).numpy()
     match = np.empty(ns, np.int32)
     parent = np.empty(ns, np.int32)
     out = np.empty((ns, 4), np.float32)
@@ -165,22 +254,26 @@ def run_reference(args, rank, world):
         oracle.paren_match(tags, match, parent)
         oracle.tree_bbox(tags, boxes, out)
 
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = time.perf_counter() - t0
+    old, core = pin_one_core()
+    try:
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        dt = time.perf_counter() - t0
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
     value = ns * args.steps / dt / 1e9
-    sample = (f"first 2^{log2s} elements of the bench stream per step (the oracle, oracle/oracle.c -O2, "
-              f"is sequential; its time is linear in the elements)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32",
         "data": "synthetic",
-        "config": bench_config(args, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "config": bench_config(args, world, None if args.config.upper() == "C5" else ns, desc),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model(), "pinned_core": core, "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -194,12 +287,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.config.upper() != "C5":
+        raise SystemExit("--config other than C5 runs on one GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
 
     import paper_2205_11659_b200 as tb
-    import scenegen
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -210,17 +304,15 @@ def main():
     lib.tb_launch_count.restype = ctypes.c_longlong
     lib.tb_profile_read.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
 
-    n = 1 << args.log2n
-    offset = rank * n
-    s_before = sum(scenegen.walk_step_sum(n, args.seed, offset=r * n, device=dev) for r in range(rank))
-    tags = scenegen.walk_tags(n, args.seed, device=dev, offset=offset, s_before=s_before)
-    boxes = scenegen.boxes(n, args.seed, tags, offset=offset, device=dev)
+    tags, boxes, n, desc = make_inputs(args, rank, world, dev)
     match = torch.empty(n, dtype=torch.int32, device=dev)
     parent = torch.empty(n, dtype=torch.int32, device=dev)
     out = torch.empty((n, 4), dtype=torch.float32, device=dev)
     shard = None
     if world > 1:
-        shard = tb.ShardContext(world, rank, offset, n)
+        shard = tb.ShardContext(world, rank, (1 << args.log2n) * rank, n)
+    # inputs that fit in L2 get a 512 MB write between timed steps (outside the timing)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if n * 17 < (256 << 20) else None
 
     def step():
         if shard is None:
@@ -234,6 +326,30 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
+    def timed(fn, steps):
+        """Device time of `steps` calls of fn (ms), CUDA events on this stream;
+        with the L2 flush between calls when the inputs fit in L2."""
+        if flush is None:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(steps):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b)
+        tot = 0.0
+        for _ in range(steps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            tot += a.elapsed_time(b)
+        return tot
+
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -242,15 +358,8 @@ def main():
     clocks = ClockSampler(dev.index if dev.index is not None else 0)
     clocks.start()
     launches0 = lib.tb_launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        step()
-    ev1.record()
-    torch.cuda.synchronize()
+    ms = timed(step, args.steps)
     launches = lib.tb_launch_count() - launches0
-    ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     barrier()
     if world > 1:
@@ -260,30 +369,51 @@ def main():
         ms = float(t.item())
     ms_per_step = ms / args.steps
     value = world * n * args.steps / (ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
 
     # --- roofline: per-kernel event timing over a second run of the same steps
     lib.tb_profile_enable(1)
     lib.tb_profile_read(None, 0)
     for _ in range(args.steps):
+        if flush is not None:
+            flush.zero_()
         step()
     torch.cuda.synchronize()
     buf = ctypes.create_string_buffer(1 << 16)
     lib.tb_profile_read(buf, len(buf))
     lib.tb_profile_enable(0)
     per_kernel = json.loads(buf.value.decode() or "{}")
-    alg_bytes = {"pm_finish": BYTES_PM * n, "pm_reduce": 1 * n, "bbm_main": BYTES_TB * n, "bbm_reduce": 5 * n,
-                 "bb_finish": 33 * n, "bb_reduce": 1 * n}
-    dom = max(per_kernel.items(), key=lambda kv: kv[1][1])[0] if per_kernel else "bbm_main"
+    dom = max(per_kernel.items(), key=lambda kv: kv[1][1])[0] if per_kernel else "fz_main"
     cnt, tot_ms = per_kernel.get(dom, [1, float("nan")])
     avg_ms = tot_ms / max(cnt, 1)
-    peak, peak_src = measured_peak()
-    achieved = alg_bytes.get(dom, BYTES_TB * n) / (avg_ms / 1e3) / 1e9
+    kb = KERNEL_BYTES.get(dom, BYTES_PAIR)
+    achieved = kb * n / (avg_ms / 1e3) / 1e9
     traffic = profile_traffic().get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "kernel_ms": avg_ms,
+                "kernel_bytes_per_elem": kb, "kernel_ms": avg_ms,
+                "frac_of_8TBs": achieved / NOMINAL_GBS,
                 "step_share": tot_ms / max(sum(v[1] for v in per_kernel.values()), 1e-9),
                 "per_kernel_ms": {k: v[1] / max(v[0], 1) for k, v in per_kernel.items()}}
+
+    # --- the two calls of the north star timed separately, and the pair
+    calls = None
+    if not args.no_calls and shard is None:
+        k = max(3, min(args.steps, 10))
+        for _ in range(2):  # warm-up (workspace allocation of each call)
+            tb.paren_match(tags, match, parent)
+            tb.tree_bbox(tags, boxes, out)
+        torch.cuda.synchronize()
+        pm_ms = timed(lambda: tb.paren_match(tags, match, parent), k) / k
+        tb_ms = timed(lambda: tb.tree_bbox(tags, boxes, out), k) / k
+
+        def rec(nb, t):
+            gbs = nb * n / (t / 1e3) / 1e9
+            return {"ms": t, "Gelem_s": n / (t / 1e3) / 1e9, "bytes_per_elem": nb, "GBs": gbs,
+                    "frac_of_8TBs": gbs / NOMINAL_GBS, "frac_of_measured": gbs / peak}
+        calls = {"paren_match": rec(BYTES_PM, pm_ms), "tree_bbox": rec(BYTES_TB, tb_ms),
+                 "pair_two_calls": rec(BYTES_PAIR, pm_ms + tb_ms),
+                 "pair_fused_step": rec(BYTES_PAIR, ms_per_step)}
 
     # --- e2e through the host-buffer C ABI
     e2e = None
@@ -293,7 +423,7 @@ def main():
         h_match = torch.empty(n, dtype=torch.int32).pin_memory()
         h_parent = torch.empty(n, dtype=torch.int32).pin_memory()
         h_out = torch.empty((n, 4), dtype=torch.float32).pin_memory()
-        e_steps = max(1, min(args.steps, 3))
+        e_steps = max(1, min(args.steps, 5))
 
         def estep():
             if shard is None:
@@ -328,37 +458,29 @@ def main():
                "api": ("paren_match_tree_bbox_host (pinned host buffers)" if shard is None else
                        "pinned H2D + ShardContext.paren_match/tree_bbox + D2H")}
 
-    # --- oracle on the host (rank 0, N = 1 only)
+    # --- oracle on the host (rank 0, N = 1 only): one pinned thread, median of 3
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import numpy as np
-        import oracle
-        ht = tags.cpu().numpy()
-        hb = boxes.cpu().numpy()
-        m_ = np.empty(n, np.int32)
-        p_ = np.empty(n, np.int32)
-        o_ = np.empty((n, 4), np.float32)
-        t0 = time.perf_counter()
-        oracle.paren_match(ht, m_, p_)
-        oracle.tree_bbox(ht, hb, o_)
-        dt = time.perf_counter() - t0
-        cpu = {"value": n / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"the full bench workload (2^{args.log2n} elements), one pass of both oracle walks",
-               "seconds": dt, "host_cpus": os.cpu_count()}
+        sec, core = oracle_seconds(tags.cpu().numpy(), boxes.cpu().numpy(), 3)
+        cpu = {"value": n / sec / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"the full bench workload ({n} elements), both oracle walks, median of 3 runs",
+               "seconds": sec, "cpu_model": cpu_model(), "pinned_core": core, "host_cpus": os.cpu_count()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32", "data": "synthetic",
-            "config": bench_config(args, world),
+            "config": bench_config(args, world, n, desc),
             "roofline": roofline,
+            "calls": calls,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
             "pair_bytes_per_elem": BYTES_PAIR,
             "pair_hbm_frac": BYTES_PAIR * n * world / (ms_per_step / 1e3) / 1e9 / (peak * world),
+            "pair_frac_of_8TBs": BYTES_PAIR * n * world / (ms_per_step / 1e3) / 1e9 / (NOMINAL_GBS * world),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
