@@ -70,8 +70,7 @@ struct Params {
   int32_t* slice_idx;  // [ntiles * W] global index | blend << 31
   float4* slice_box;   // [ntiles * W] lc: ∩ of the clip boxes of the slice entries at and below (fz_reduce)
   float4* slice_su;    // [ntiles * W] union of the tile's clipped leaves after the entry (fz_main)
-  int4* pop;           // [aoff[ntiles]] close popping incoming depth D: (close, open, slice ref, blend); root: close -1
-  float4* popu;        // [aoff[ntiles]] the tile's union before that close
+  int2* pop;           // [aoff[ntiles]] close popping incoming depth D: (close, slice ref of its open); root: (-1, -1)
   float4* tu[LV];      // tile unions, 32-ary hierarchy
   float4* pj_acc;      // [2 * ntiles] pointer jumping over tiles
   int32_t* pj_ptr;     // [2 * ntiles]
@@ -100,7 +99,7 @@ constexpr int RMAX = 8;        // runs of the incoming stack kept per tile (more
 // workspace
 // ----------------------------------------------------------------------------
 struct Layout {
-  size_t ctrl, aoff, sidx, sbox, ssu, pop, popu, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, bytes;
+  size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, bytes;
   int64_t ntiles;
   explicit Layout(int64_t n) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -113,8 +112,7 @@ struct Layout {
     sidx = o; o = al(o + 4 * cap);
     sbox = o; o = al(o + 16 * cap);
     ssu = o; o = al(o + 16 * cap);
-    pop = o; o = al(o + 16 * npop);
-    popu = o; o = al(o + 16 * npop);
+    pop = o; o = al(o + 8 * npop);
     int64_t m = ntiles;
     for (int k = 0; k < LV; k++) {
       tu[k] = o; o = al(o + 16 * (size_t)m);
@@ -150,8 +148,7 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.slice_idx = (int32_t*)(b + L.sidx);
   p.slice_box = (float4*)(b + L.sbox);
   p.slice_su = (float4*)(b + L.ssu);
-  p.pop = (int4*)(b + L.pop);
-  p.popu = (float4*)(b + L.popu);
+  p.pop = (int2*)(b + L.pop);
   for (int k = 0; k < LV; k++) p.tu[k] = (float4*)(b + L.tu[k]);
   p.pj_acc = (float4*)(b + L.pja);
   p.pj_ptr = (int32_t*)(b + L.pjp);
@@ -1041,9 +1038,8 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   //      matchS[c_d]; the partner of a popped in-tile open; the context at
   //      depth d where a leaf or open sits there, in c_d's slot (depth a_t:
   //      the link, TL(t))
-  uint32_t xcm = 0;  // closes popping an entry of an earlier tile (incoming depths dx0, dx0 + 1, ...)
+  uint32_t xcm = 0;  // closes popping an entry of an earlier tile
   uint32_t icm = 0;  // closes popping an open of an earlier thread of this tile
-  int dx0 = 0;
   {
     int ref = top_ref, d = 0, prevc = -1;
     uint32_t q = w.ucm;
@@ -1083,11 +1079,10 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
           if (seg & needm) cx = isect(__ldg(p.slice_box + rf), __ldg(p.tc + (rf >> LOGW)));
         }
         gi = si & 0x7fffffff;
-        if (!xcm) dx0 = D;
         xcm |= 1u << ci;
-        p.pop[poff + D] = make_int4(gtb + ci, gi, rf, si < 0);
+        p.pop[poff + D] = make_int2(gtb + ci, rf);
       } else {
-        p.pop[poff + D] = make_int4(-1, -1, -1, 0);  // pops the root (R3)
+        p.pop[poff + D] = make_int2(-1, -1);  // pops the root (R3)
       }
       s.matchS[mb + ci] = gi;
       if (seg & needm) s.val[sl(ci)] = cx;
@@ -1250,9 +1245,9 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
       }
     }
   }
-  if (xcm) {
-    int D = dx0;
-    for (uint32_t q = xcm; q; q &= q - 1, D++) p.popu[poff + D] = unite(s.val[sl(__ffs(q) - 1)], pre);
+  for (uint32_t q = xcm; q; q &= q - 1) {  // the tile prefix before the close (fz_close reads it back)
+    float4& cv = s.val[sl(__ffs(q) - 1)];
+    cv = unite(cv, pre);
   }
   if (tid == 0) {
     float4 t = s.wtu[0];
@@ -1384,19 +1379,23 @@ __global__ void __launch_bounds__(128) fz_close(Params p) {
   if (T >= p.ntiles) return;
   const int64_t poff = __ldg(p.aoff + T);
   const int npop = (int)(__ldg(p.aoff + T + 1) - poff);
+  const int bT = __ldg(p.ctrl.agg + T).y;
+  const int L = (int)__ldg(p.ctrl.lw + T) - 1;
+  const int sm = __ldg(p.ctrl.smin + T);
   int cto = INT_MIN;  // warp cache: the last tile range resolved
   float4 cR = bEMPTY();
   for (int j0 = 0; j0 < npop; j0 += 32) {
     const int j = j0 + lane;
-    int4 r = make_int4(-1, -1, -1, 0);
+    int2 r = make_int2(-1, -1);
     if (j < npop) r = __ldcg(p.pop + poff + j);
     const bool valid = r.x >= 0;  // root pops (R3) have no node
-    int To = T;
+    int To = T, si = 0;
     float4 P = bEMPTY(), su = bEMPTY();
     if (valid) {
-      To = r.z >> LOGW;
-      P = __ldcg(p.popu + poff + j);
-      su = __ldg(p.slice_su + r.z);
+      To = r.y >> LOGW;
+      P = __ldcg(p.out + r.x);  // the tile prefix before the close (fz_main)
+      su = __ldg(p.slice_su + r.y);
+      si = __ldg(p.slice_idx + r.y);
     }
     float4 R = bEMPTY();
     bool pending = valid && To < T - 1;
@@ -1417,16 +1416,14 @@ __global__ void __launch_bounds__(128) fz_close(Params p) {
     }
     if (valid) {
       const float4 U = unite(unite(P, su), R);
+      const int o = si & 0x7fffffff;
       p.out[r.x] = U;
-      if (r.w) p.out[r.y] = U;
-      if (PM) p.match[r.y] = r.x;
+      if (si < 0) p.out[o] = U;  // a blend open
+      if (PM) p.match[o] = r.x;
     }
   }
   // blend opens never closed (R4): the tile's slice entries that survive to
   // the end of the stream (F1: its bottom min(b_T, smin_T - L_T))
-  const int bT = __ldg(p.ctrl.agg + T).y;
-  const int L = (int)__ldg(p.ctrl.lw + T) - 1;
-  const int sm = __ldg(p.ctrl.smin + T);
   const int surv = min(bT, sm == INT_MAX ? bT : max(sm - L, 0));
   if (surv > 0) {
     bool anyb = false;
