@@ -67,6 +67,13 @@ const char *tb_last_error(void);
 /* Library version string. */
 const char *tb_version(void);
 
+/* Free the library's cached device workspaces of the current device (the
+ * per-(device, stream) caches of the calls below and the shard protocols'
+ * arenas).  Synchronizes the device first; no call may be in flight on any
+ * stream of it.  The next call re-allocates what it needs.  Returns 0 or
+ * TB_ERR_CUDA. */
+int tb_release_workspaces(void);
+
 /* ------------------------------------------------------------------------
  * paren_match — parentheses matching (§2; §3; §4)
  *

@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "bin_leaves", "compact_scene", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["release_workspaces", "paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "bin_leaves", "compact_scene", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard"]
 
@@ -44,6 +44,7 @@ def load():
             sigs = {
                 "tb_last_error": ([], ctypes.c_char_p),
                 "tb_version": ([], ctypes.c_char_p),
+                "tb_release_workspaces": ([], ctypes.c_int),
                 "paren_match": ([P, I64, P, P, P], ctypes.c_int),
                 "paren_match_ws": ([P, I64, P, P, P, SZ, P], ctypes.c_int),
                 "paren_match_workspace_bytes": ([I64], SZ),
@@ -278,6 +279,14 @@ def compact_scene(tags: torch.Tensor, boxes: torch.Tensor | None, keep_map: byte
                                  ctypes.byref(cnt), _stream(tags.device)))
     k = cnt.value
     return t_out[:k], (b_out[:k] if b_out is not None else None), idx[:k]
+
+
+def release_workspaces(device=None):
+    """Free the library's cached device workspaces of `device` (default: the
+    current device); the next call re-allocates what it needs."""
+    lib = load()
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        _check(lib.tb_release_workspaces())
 
 
 def workspace_bytes(n: int) -> dict:

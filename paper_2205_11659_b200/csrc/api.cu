@@ -12,6 +12,7 @@
 #ifdef TB_WITH_NCCL
 #include <nccl.h>
 namespace tb {
+int shard_release_arenas(int dev);
 cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* match, int32_t* parent,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err);
 cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t* match, const int32_t* parent,
@@ -157,6 +158,29 @@ int bb_checks(const uint8_t* tags, const float* leaf, int64_t n, float* out) {
 extern "C" {
 
 const char* tb_last_error(void) { return g_err; }
+
+int tb_release_workspaces(void) {
+  g_err[0] = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "tb_release_workspaces");
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_ws.begin(); it != g_ws.end();) {
+      if (it->first.first / 16 == dev) {
+        cudaFree(it->second.p);
+        it = g_ws.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+#ifdef TB_WITH_NCCL
+  tb::shard_release_arenas(dev);
+#endif
+  return TB_OK;
+}
 const char* tb_version(void) { return "treebbox-b200 0.1 (sm_100a)"; }
 
 size_t paren_match_workspace_bytes(int64_t n) { return n > 0 ? tb::pm_workspace_bytes(n) : 0; }

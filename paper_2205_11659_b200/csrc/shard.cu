@@ -70,6 +70,25 @@ struct Arena {
 };
 std::mutex g_arena_mu;
 std::map<std::pair<int, cudaStream_t>, Arena> g_arenas;
+}  // namespace
+
+// tb_release_workspaces: free every shard arena of the current device (the
+// caller guarantees no call is in flight on any stream of it)
+int shard_release_arenas(int dev) {
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  int freed = 0;
+  for (auto it = g_arenas.begin(); it != g_arenas.end();) {
+    if (it->first.first / 8 == dev) {
+      for (auto& b : it->second.blocks) cudaFree(b.first);
+      it = g_arenas.erase(it);
+      freed++;
+    } else {
+      ++it;
+    }
+  }
+  return freed;
+}
+namespace {
 
 class Scratch {
  public:
