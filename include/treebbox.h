@@ -85,10 +85,11 @@ int tb_release_workspaces(void);
  * d_match  : device int32[n] out.  Classical partner: matched opens and
  *            closes point at each other; leaves, opens never closed (R4) and
  *            closes with nothing to close (R3) get -1.
- * Computation: a reduce pass over the tags (decoupled-look-back scan of the
- * bicyclic monoid, publishing each tile's stack slice,
- * P:229-233) and a finish pass (in-tile resolution, cross-tile lookup by the
- * suffix relation).  HBM traffic ~10 bytes/element (+ slices).
+ * Computation: a reduce pass over the tags (each 4096-element tile's value
+ * in the bicyclic monoid, and its stack slice), a scan of
+ * the tile values (one CTA: start heights, low-water marks and their 32-ary
+ * min hierarchy) and a finish pass (in-tile resolution, cross-tile lookup by
+ * the suffix relation).  HBM traffic ~10 bytes/element (+ slices).
  * ------------------------------------------------------------------------ */
 int paren_match(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *d_parent,
                 void *stream);
@@ -130,8 +131,9 @@ int paren_match_bytes(const uint8_t *d_bytes, int64_t n, const uint8_t *h_class_
  * order -0 below +0 and ignore NaN operands (R12; the measured semantics of
  * PTX min/max.f32), so results are unique bit patterns.  Boxes are never
  * canonicalised (R9).
- * Matching is computed internally (paren_match into the workspace), then
- * the boxes follow from it as in tree_bbox_matched below.
+ * The matching structure is re-derived inside the same tile pass that
+ * computes the boxes (the fused pass of paren_match_tree_bbox, without its
+ * match / parent stores): ~34 bytes/element of HBM traffic (+ slices).
  * ------------------------------------------------------------------------ */
 int tree_bbox(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, float *d_node_bbox,
               void *stream);
@@ -146,8 +148,7 @@ int tree_bbox_ws(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, flo
  * d_match, d_parent: device int32[n], exactly paren_match's outputs for
  * d_tags (16-byte aligned; not checked for consistency — other values give
  * undefined node_bbox but never out-of-bounds accesses only if they are
- * paren_match's).  tree_bbox(...) is paren_match into its workspace followed
- * by this call.  With the parent of every element known, an element's clip is
+ * paren_match's).  With the parent of every element known, an element's clip is
  * box ∩ clip(parent) and a node's union is the union of the clipped
  * leaves strictly between its open and its close; both are
  * evaluated per tile with the cross-tile parts taken from the tiles' slices

@@ -17,25 +17,6 @@ __device__ __forceinline__ Bic bic_combine(Bic x, Bic y) {
   return Bic{x.a + y.a - m, x.b + y.b - m};
 }
 
-// ---------------------------------------------------------------------------
-// Memory-model helper (PTX, gpu scope): acquire loads of published slots.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Spin until a published u32 slot is nonzero (values are stored +1).
-__device__ __forceinline__ uint32_t wait_u32(const uint32_t* p) {
-  uint32_t v = ld_acquire_u32(p);
-  while (v == 0) {
-    // pure spin (nanosleep granularity is too coarse here)
-    v = ld_acquire_u32(p);
-  }
-  return v;
-}
-
 // Streaming 16-byte load that does not allocate in L1.
 __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
   uint4 r;

@@ -4,12 +4,13 @@
 //
 // pm_reduce (pass 1, reads 1 B/element):
 //   register walk per thread -> Bic (a_t, b_t) (§3); forward and
-//   reverse block scans; the tile's stack slice Stk(enum(s)[p..p+w]) (§7.1
+//   reverse warp scans; the tile's stack slice Stk(enum(s)[p..p+w]) (§7.1
 //   its unmatched opens, ascending) is written to the workspace and
-//   each of those opens gets a -1 placeholder in match[]; decoupled look-back
-//   (single pass over the tiles, the paper's future-work item P:381) gives the
-//   stack height H at the tile start; the low-water mark L = max(H - a_T, 0)
-//   is published into a 32-ary min hierarchy.
+//   the tile's Bic value published.  tile_scan (one CTA, tilescan.cu) turns the
+//   tile values into the stack height H at each tile start and the low-water
+//   marks L = max(H - a_T, 0) with their 32-ary min hierarchy.  (A single-pass
+//   decoupled look-back, the paper's future-work item P:381, was built in
+//   round 1 and measured slower than reduce + scan at these sizes.)
 // pm_finish (pass 2, reads 1 B/element, writes 8 B/element):
 //   the same register walk; thread-level owner lookups resolve references to
 //   earlier threads of the tile; the needed top of the incoming stack (a_T+1

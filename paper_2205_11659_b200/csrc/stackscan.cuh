@@ -57,90 +57,6 @@ struct CtrlLayout {
 };
 
 // ---------------------------------------------------------------------------
-// Owner search (one warp): the last tile U < from with L_U <= X (X >= 0).
-// Returns U (and its L in Lout), or -1 if no tile qualifies (then the entry
-// belongs to the stack that was live before tile 0, i.e. the shard's
-// incoming stack).  Every visited entry is complete-before-`from`, so the
-// spins only wait on tiles that are already running or done.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int owner_search(const Ctrl& c, int from, int X, int& Lout) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t ux = (uint32_t)X;
-  int idx = from;
-#pragma unroll 1
-  for (int k = 0; k < HLEVELS; k++) {
-    const int g = idx >> 5, r = idx & 31;
-    uint32_t v = 0xffffffffu;
-    if (lane < r) v = wait_u32(c.lv[k] + ((size_t)g << 5) + lane) - 1u;
-    const unsigned m = __ballot_sync(0xffffffffu, lane < r && v <= ux);
-    if (m) {
-      int E = (g << 5) + (31 - __clz(m));
-      uint32_t L = __shfl_sync(0xffffffffu, v, 31 - __clz(m));
-#pragma unroll 1
-      for (int j = k - 1; j >= 0; j--) {
-        const uint32_t v2 = wait_u32(c.lv[j] + ((size_t)E << 5) + lane) - 1u;
-        const unsigned m2 = __ballot_sync(0xffffffffu, v2 <= ux);
-        const int top = 31 - __clz(m2);
-        L = __shfl_sync(0xffffffffu, v2, top);
-        E = (E << 5) + top;
-      }
-      Lout = (int)L;
-      return E;
-    }
-    idx = g;
-    if (idx == 0) break;
-  }
-  return -1;
-}
-
-// Low-water marks of the 32 tiles before `base` (lane j <-> tile base-1-j),
-// read once and kept in a register; 0 = not yet published.  Searches from
-// any `from` in (base-32, base] are answered from it while it covers them,
-// waiting only for the tiles that are actually needed (closest first).
-struct LwWindow {
-  int base;
-  uint32_t v;  // lw + 1 as published, 0 = unknown
-};
-
-__device__ __forceinline__ LwWindow lw_window_load(const Ctrl& c, int base) {
-  const int lane = threadIdx.x & 31;
-  const int t = base - 1 - lane;
-  LwWindow w;
-  w.base = base;
-  w.v = t >= 0 ? ld_acquire_u32(c.lw + t) : 0xffffffffu;  // 0xffffffff: no tile
-  return w;
-}
-
-// Search via the window first; falls back to the hierarchy if the answer is
-// older than the window.
-__device__ __forceinline__ int owner_search_win(const Ctrl& c, LwWindow& w, int from, int X, int& Lout) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t ux = (uint32_t)X;
-  const int t = w.base - 1 - lane;
-  const bool cand = t < from && t >= 0;
-  while (true) {
-    // closest candidate lane whose value is known and qualifies, with all
-    // closer candidates known (and not qualifying)
-    const bool known = w.v != 0u;
-    const bool q = cand && known && (w.v - 1u) <= ux;
-    const unsigned mq = __ballot_sync(0xffffffffu, q);
-    const unsigned mu = __ballot_sync(0xffffffffu, cand && !known);
-    const unsigned first_q = mq & (~mq + 1u);          // lowest qualifying lane
-    const unsigned before = first_q ? (first_q - 1u) : 0xffffffffu;
-    if (mq && (mu & before) == 0u) {
-      const int k = __ffs(mq) - 1;
-      Lout = (int)(__shfl_sync(0xffffffffu, w.v, k) - 1u);
-      return w.base - 1 - k;
-    }
-    if (!mq && !mu) break;  // nothing in the window qualifies
-    // wait for the unknown candidates that matter (closer than any hit)
-    if (cand && !known && (mq == 0u || ((1u << lane) & before))) w.v = wait_u32(c.lw + t);
-  }
-  if (w.base - 32 <= 0) return -1;
-  return owner_search(c, min(from, w.base - 32), X, Lout);
-}
-
-// ---------------------------------------------------------------------------
 // Owner search over a COMPLETE hierarchy (finish pass: the reduce pass has
 // ended, every value is published, plain loads suffice).  Same contract as
 // owner_search.  The first 32 predecessors of `from` are tested in one

@@ -12,7 +12,7 @@ import sys
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
         "nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3}
-OURS = ("pm_", "tile_scan", "bbm_", "tt_", "bin_", "count_k", "scatter_k", "excl_scan", "scan_", "classify_bytes")
+OURS = ("fz_", "pm_", "tile_scan", "bbm_", "tt_", "bin_", "count_k", "scatter_k", "excl_scan", "scan_", "classify_bytes")
 
 
 def main():
@@ -22,7 +22,7 @@ def main():
     per = collections.OrderedDict()
     for r in rows[1:]:
         name = r[ix["Kernel Name"]]
-        short = name.split("(")[0].split("<")[0].split("::")[-1].strip()
+        short = name.split("(")[0].split("<")[0].split("::")[-1].split()[-1]
         if not short.startswith(OURS):
             continue
         v = float(r[ix["Metric Value"]].replace(",", "")) * UNIT.get(r[ix["Metric Unit"]], 1)
