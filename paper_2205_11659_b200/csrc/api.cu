@@ -618,6 +618,7 @@ int compact_scene(const uint8_t* d_tags, const float* d_boxes, int64_t n, const 
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }
 
 int tb_debug_fz_tma(int on) { return tb::fused_set_tma(on); }
+int tb_debug_fz_abl(int mask) { return tb::fused_set_abl(mask); }
 
 int tb_debug_fz_trace(void* dev_buf) {
   tb::fused_set_trace((uint64_t*)dev_buf);

@@ -84,6 +84,7 @@ struct Params {
   int chunk;           // fz_ctrl: tiles per block (multiple of 32)
   uint64_t* trace;     // optional (debug): fz_ctrl phase timestamps, block 0
   int use_tma;         // fz_main: full tiles move their boxes with TMA (tensor maps below)
+  int abl;             // debug (timing experiments only, results wrong): skip phases of fz_main
 };
 // TMA descriptors of fz_main: per array (leaf boxes in, node boxes out) one 2D
 // map per half of the thread rows: {32 floats, n/16 rows}, row stride 256 B,
@@ -162,6 +163,7 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.chunk = 32;
   p.trace = nullptr;
   p.use_tma = 0;
+  p.abl = 0;
   return p;
 }
 
@@ -711,29 +713,37 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   uint32_t S = 0, plo = 0, phi = 0, mlo = 0, mhi = 0, ext = 0, ucm = 0, mcb = 0;
 #pragma unroll 1
   for (int q = 0; q < K / 4; q++) {
-    const bool lo = q < 2;  // warp-uniform
+    const int i0 = 4 * q;
+    const uint32_t oq = w.om >> i0, cq = w.cm >> i0;  // bit tests below use immediates
+    uint32_t gp = 0, gm = 0, gx = 0, gu = 0, gb = 0;   // the group's nibbles / bits
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      const int i = 4 * q + j;
-      const int sh = 4 * (i & 7);
-      const uint32_t bit = 1u << i;
+      const int i = i0 + j;
       const int top = 31 - __clz(S);  // -1 when the thread stack is empty
-      const uint32_t pn = (uint32_t)(top & 15) << sh;
-      if (lo) plo |= pn;
-      else phi |= pn;
-      ext |= S ? 0u : bit;
-      const bool pop = (w.cm & bit) && S;
-      ucm |= ((w.cm & bit) && !S) ? bit : 0u;
-      mcb |= (pop && ((w.bm >> top) & 1u)) ? bit : 0u;
+      gp |= (uint32_t)(top & 15) << (4 * j);
+      gx |= S ? 0u : (1u << j);
+      const bool isc = (cq >> j) & 1u;
+      const bool pop = isc && S;
+      gu |= (isc && !S) ? (1u << j) : 0u;
+      gb |= (pop && ((w.bm >> top) & 1u)) ? (1u << j) : 0u;
       // partner nibbles: the open's (at the pop) and the close's own
       const uint32_t pv = pop ? (uint32_t)i << (4 * (top & 7)) : 0u;
       mlo |= top < 8 ? pv : 0u;
       mhi |= top >= 8 ? pv : 0u;
-      const uint32_t cv = pop ? pn : 0u;
-      if (lo) mlo |= cv;
-      else mhi |= cv;
-      S = (w.om & bit) ? (S | bit) : (pop ? (S ^ (1u << top)) : S);
+      gm |= pop ? (uint32_t)(top & 15) << (4 * j) : 0u;
+      S = ((oq >> j) & 1u) ? (S | (1u << i)) : (pop ? (S ^ (1u << top)) : S);
     }
+    const int sh = 16 * (q & 1);
+    if (q < 2) {
+      plo |= gp << sh;
+      mlo |= gm << sh;
+    } else {
+      phi |= gp << sh;
+      mhi |= gm << sh;
+    }
+    ext |= gx << i0;
+    ucm |= gu << i0;
+    mcb |= gb << i0;
   }
   w.S = S;
   w.plo = plo;
@@ -1040,25 +1050,45 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   //      the link, TL(t))
   uint32_t xcm = 0;  // closes popping an entry of an earlier tile
   uint32_t icm = 0;  // closes popping an open of an earlier thread of this tile
-  {
+#pragma unroll 1
+  for (int rep = 0; rep < ((p.abl & 64) ? 2 : 1); rep++) {
+    xcm = icm = 0;
     int ref = top_ref, d = 0, prevc = -1;
     uint32_t q = w.ucm;
     const uint32_t needm = w.ext & (w.lm | w.om);
-    for (; d < a_t && ref >= 0; d++) {
-      const int ci = __ffs(q) - 1;
-      q &= q - 1;
-      const uint32_t seg = ((1u << ci) - 1u) & ~((1u << (prevc + 1)) - 1u);  // elements at depth d
-      prevc = ci;
-      icm |= 1u << ci;
-      s.matchS[mb + ci] = gbase + ref;
-      s.matchS[mpad(ref)] = gtb + ci;
-      if (seg & needm) s.val[sl(ci)] = isect(s.val[slot_of(ref)], s.u.pj.acc[cbf][ref >> LOGK]);
-      const int V = ref >> LOGK;
-      const uint32_t below = s.u.pj.uo[V] & ((1u << (ref & (K - 1))) - 1u);
-      ref = below ? (V << LOGK) + 31 - __clz(below) : s.u.pj.link[V];
+    if (p.abl & 1) d = a_t;
+    if (p.abl & 32) ref = -1;
+    if (d < a_t && ref >= 0) {
+      // the owner thread's unmatched-open mask stays in a register; shared
+      // memory is read again only when the chain moves to another thread
+      int V = ref >> LOGK, bp = ref & (K - 1);
+      uint32_t uV = s.u.pj.uo[V];
+      while (true) {
+        const int e = (V << LOGK) | bp;  // the entry at depth d: a tile-local open
+        const int ci = __ffs(q) - 1;
+        q &= q - 1;
+        const uint32_t seg = ((1u << ci) - 1u) & ~((1u << (prevc + 1)) - 1u);  // elements at depth d
+        prevc = ci;
+        icm |= 1u << ci;
+        s.matchS[mb + ci] = gbase + e;
+        s.matchS[mpad(e)] = gtb + ci;
+        if ((seg & needm) && !(p.abl & 8)) s.val[sl(ci)] = isect(s.val[slot_of(e)], s.u.pj.acc[cbf][V]);
+        if (++d >= a_t) break;
+        const uint32_t below = uV & ((1u << bp) - 1u);
+        if (below) {
+          bp = 31 - __clz(below);
+        } else {
+          ref = s.u.pj.link[V];
+          if (ref < 0) break;  // the rest is in the incoming stack
+          V = ref >> LOGK;
+          bp = ref & (K - 1);
+          uV = s.u.pj.uo[V];
+        }
+      }
     }
     // the rest are consecutive entries of the incoming stack (a chain that
     // leaves the tile never returns into it)
+    if (p.abl & 16) d = a_t;
     for (; d < a_t; d++, ref--) {
       const int ci = __ffs(q) - 1;
       q &= q - 1;
@@ -1106,28 +1136,33 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
     const float4 v15 = s.val[sl(K - 1)];
     if (!u15) s.val[sl(K - 1)] = TL;
 #pragma unroll 1
-    for (int q = 0; q < K / 4; q++) {
-      const uint32_t pw4 = q < 2 ? w.plo : w.phi, mw4 = q < 2 ? w.mlo : w.mhi;
+    for (int q = 0; q < ((p.abl & 2) ? 0 : K / 4); q++) {
+      // the masks shifted once per group: bit tests below use immediates
+      const int i0 = 4 * q;
+      const uint32_t Lq = w.lm >> i0, Bq = w.bm >> i0, Oq = w.om >> i0, Cq = w.cm >> i0, Uq = w.ucm >> i0;
+      const uint32_t Sq = w.S >> i0, Xq = w.ext >> i0, MBq = w.mcb >> i0;
+      const uint32_t pwq = (q < 2 ? w.plo : w.phi) >> (16 * (q & 1)), mwq = (q < 2 ? w.mlo : w.mhi) >> (16 * (q & 1));
+      const int kq = __popc(w.S & ((1u << i0) - 1u));      // thread-unmatched opens before the group
+      const int sbq = ((q >> 1) << 10) | (sb ^ ((q & 1) << 2));  // slot of element i0 + jq = sbq ^ jq
       int pv[4];
 #pragma unroll
       for (int jq = 0; jq < 4; jq++) {
-        const int i = 4 * q + jq;
-        const uint32_t bit = 1u << i;
-        const bool isL = (w.lm & bit) != 0u, isB = (w.bm & bit) != 0u;
-        const bool isO = (w.om & bit) != 0u, isC = (w.cm & bit) != 0u, isU = (w.ucm & bit) != 0u;
-        const bool isUO = (w.S & bit) != 0u;
+        const int i = i0 + jq;
+        const bool isL = (Lq >> jq) & 1u, isB = (Bq >> jq) & 1u;
+        const bool isO = (Oq >> jq) & 1u, isC = (Cq >> jq) & 1u, isU = (Uq >> jq) & 1u;
+        const bool isUO = (Sq >> jq) & 1u;
         const bool isMC = isC && !isU;
-        float4 v = s.val[sl(i)];
+        const int si = sbq ^ jq;
+        float4 v = s.val[si];
         if (jq == 3 && q == K / 4 - 1 && !isMC) v = v15;
-        const int sh = 4 * ((q & 1) * 4 + jq);
-        const int pn = (int)((pw4 >> sh) & 15u);
-        const int pt = (int)((mw4 >> sh) & 15u);
-        const bool isx = (w.ext & bit) != 0u;
-        const uint32_t nc = w.ucm & ~(bit - 1u);  // unmatched closes at or after i
-        const int j = nc ? __ffs(nc) - 1 : K - 1;  // the next one: c_d of element i's depth d (none: TL)
+        const int pn = (int)((pwq >> (4 * jq)) & 15u);
+        const int pt = (int)((mwq >> (4 * jq)) & 15u);
+        const bool isx = (Xq >> jq) & 1u;
+        const uint32_t nc = Uq >> jq;                        // unmatched closes at or after i
+        const int j = nc ? i + __ffs(nc) - 1 : K - 1;        // the next one: c_d of element i's depth d (none: TL)
         // a close takes nothing from its parent (clipped = v ∩ v = v)
         const int spn = sl(pn);
-        const int cidx = isC ? sl(i) : sl(isx ? j : pn);
+        const int cidx = isC ? si : sl(isx ? j : pn);
         const float4 cpar = s.val[cidx];
         const int mj = s.matchS[mb + j];
         const int par = isx ? (nc ? mj : giLast) : gtb + pn;
@@ -1136,14 +1171,14 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         // close -> union (in-thread node) / prefix (outer node) / EMPTY (R3)
         float4 o = isB ? cpar : clipped;
         o = isC ? ((isU && par < 0) ? bEMPTY() : acc) : o;
-        s.val[sl(i)] = o;
+        s.val[si] = o;
         if (isO) {
           // the enclosing accumulator: into the close's slot, or rbuf for an open left open
-          const int k = __popc(w.S & (bit - 1u));
+          const int k = kq + __popc(Sq & ((1u << jq) - 1u));
           const int di = isUO ? RB0 + min(k, RCAP - 1) * NT + tid : sl(pt);
           if (!isUO || k < RCAP) s.val[di] = acc;
         }
-        if ((w.mcb & bit) != 0u) s.val[spn] = acc;
+        if ((MBq >> jq) & 1u) s.val[spn] = acc;
         const float4 add = (isL || isMC) ? clipped : bEMPTY();
         acc = unite(acc, add);
         acc = isO ? bEMPTY() : acc;
@@ -1212,7 +1247,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   //      threads between in H2); otherwise a slice entry: su = R ∪ the threads
   //      after.  Closes of earlier tiles' nodes: the tile prefix before them
   //      into their pop records (fz_close ends them)
-  if (w.S) {
+  if (w.S && !(p.abl & 4)) {
     auto handle = [&](int i, int k, const float4& R) {
       const int mc = s.matchS[mb + i];
       if (mc >= 0) {
@@ -1275,7 +1310,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
 
   // ---- H2. closes of nodes opened in an earlier thread of the tile: add the
   //      threads between; a blend open receives the union
-  for (uint32_t q = icm; q; q &= q - 1) {
+  for (uint32_t q = (p.abl & 4) ? 0u : icm; q; q &= q - 1) {
     const int ci = __ffs(q) - 1;
     const int o = s.matchS[mb + ci] - gbase;
     const int to = o >> LOGK;
@@ -1507,6 +1542,12 @@ static cudaError_t setup() {
 static uint64_t* g_fz_trace = nullptr;  // debug hook (tb_debug_fz_trace)
 void fused_set_trace(uint64_t* dev) { g_fz_trace = dev; }
 static int g_fz_tma = 1;  // debug hook (tb_debug_fz_tma): 0 = the threads copy every tile
+static int g_fz_abl = 0;  // debug hook (tb_debug_fz_abl): phase-skipping timing experiments (wrong results)
+int fused_set_abl(int m) {
+  const int old = g_fz_abl;
+  if (m >= 0) g_fz_abl = m;
+  return old;
+}
 int fused_set_tma(int on) {
   const int old = g_fz_tma;
   if (on >= 0) g_fz_tma = on;
@@ -1554,6 +1595,7 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
   fz::Maps maps;
   memset(&maps, 0, sizeof maps);
   p.use_tma = g_fz_tma && fz::make_maps(leaf_bbox, node_bbox, n, maps) ? 1 : 0;
+  p.abl = g_fz_abl;
   if (pm)
     TB_LAUNCH(stream, "fz_main", (fz::fz_main<true><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p, maps)));
   else

@@ -70,7 +70,8 @@ struct ShardOpen {
 // match / parent may be null (tree_bbox alone: only node_bbox is written).
 size_t fused_workspace_bytes(int64_t n);
 void fused_set_trace(uint64_t* dev);  // debug: fz_ctrl phase timestamps (8 x u64 device buffer) or null
-int fused_set_tma(int on);            // debug: TMA box transfers in fz_main (1, default) or thread copies (0)
+int fused_set_tma(int on);
+int fused_set_abl(int mask);          // debug: skip fz_main phases (1 start stacks, 2 forward walk, 4 cross-thread unions)            // debug: TMA box transfers in fz_main (1, default) or thread copies (0)
 int fused_tile_elems();
 cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, int32_t* match, int32_t* parent,
                          float* node_bbox, void* ws, cudaStream_t stream);
