@@ -26,25 +26,49 @@ __device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
   return r;
 }
 
-// Per-byte classification of 4 tag bytes into a 4-bit mask (bit i <-> byte i).
-__device__ __forceinline__ uint32_t byte_mask4(uint32_t cmp /* 0xff per hit */) {
-  uint32_t m = cmp & 0x01010101u;
-  return (m * 0x01020408u) >> 24;
+// Tag bytes -> element bit masks (bit i <-> byte i of 16).  Tags 0..3 carry
+// two bits: lo = bit 0, hi = bit 1 (OPEN_CLIP 1 = lo, OPEN_BLEND 2 = hi,
+// CLOSE 3 = both); any byte >= 4 is a leaf (R2).  Bit 0 of the four bytes of
+// a and of b go to bits 24..27 and 28..31 of the product (one multiply per 8
+// elements; the shifted copies never overlap, so no carries).
+__host__ __device__ __forceinline__ uint32_t gather8(uint32_t a, uint32_t b) {
+  return ((a & 0x01010101u) | ((b << 4) & 0x10101010u)) * 0x01020408u;
 }
-// 16 tag bytes -> (open mask, close mask), bit i <-> element i.
-__device__ __forceinline__ void classify16(uint4 w, uint32_t& om, uint32_t& cm) {
-  uint32_t o = 0, c = 0;
-  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    uint32_t x = ws[q];
-    uint32_t op = __vcmpeq4(x, 0x01010101u) | __vcmpeq4(x, 0x02020202u);
-    uint32_t cl = __vcmpeq4(x, 0x03030303u);
-    o |= byte_mask4(op) << (4 * q);
-    c |= byte_mask4(cl) << (4 * q);
+__host__ __device__ __forceinline__ uint32_t top_bytes(uint32_t r0, uint32_t r1) {  // byte 3 of r0, r1 -> bits 0..15
+#ifdef __CUDA_ARCH__
+  return __byte_perm(r0, r1, 0x0073u) & 0xffffu;
+#else
+  return (r0 >> 24) | ((r1 >> 16) & 0xff00u);
+#endif
+}
+// (lo, hi) masks of 16 bytes with every byte >= 4 cleared from both
+__host__ __device__ __forceinline__ void tag_bits16(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t& lo,
+                                                    uint32_t& hi) {
+  lo = top_bytes(gather8(x0, x1), gather8(x2, x3));
+  hi = top_bytes(gather8(x0 >> 1, x1 >> 1), gather8(x2 >> 1, x3 >> 1));
+  if ((x0 | x1 | x2 | x3) & 0xfcfcfcfcu) {
+    // per byte: ((x >> 2) & 0x3f) + 0x3f has bit 6 set iff x >= 4 (no carry between bytes)
+    const uint32_t j0 = (((x0 >> 2) & 0x3f3f3f3fu) + 0x3f3f3f3fu) >> 6, j1 = (((x1 >> 2) & 0x3f3f3f3fu) + 0x3f3f3f3fu) >> 6;
+    const uint32_t j2 = (((x2 >> 2) & 0x3f3f3f3fu) + 0x3f3f3f3fu) >> 6, j3 = (((x3 >> 2) & 0x3f3f3f3fu) + 0x3f3f3f3fu) >> 6;
+    const uint32_t junk = top_bytes(gather8(j0, j1), gather8(j2, j3));
+    lo &= ~junk;
+    hi &= ~junk;
   }
-  om = o;
-  cm = c;
+}
+// 16 tag bytes -> (open mask, close mask)
+__host__ __device__ __forceinline__ void classify16(uint4 w, uint32_t& om, uint32_t& cm) {
+  uint32_t lo, hi;
+  tag_bits16(w.x, w.y, w.z, w.w, lo, hi);
+  om = lo ^ hi;
+  cm = lo & hi;
+}
+// 16 tag bytes -> (open mask, close mask, blend-open mask)
+__host__ __device__ __forceinline__ void classify16b(uint4 w, uint32_t& om, uint32_t& cm, uint32_t& bm) {
+  uint32_t lo, hi;
+  tag_bits16(w.x, w.y, w.z, w.w, lo, hi);
+  om = lo ^ hi;
+  cm = lo & hi;
+  bm = hi & ~lo;
 }
 
 // Index of the j-th (0-based) lowest set bit of a 16-bit mask m (m has > j

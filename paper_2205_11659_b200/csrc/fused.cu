@@ -167,22 +167,6 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   return p;
 }
 
-// tag bytes -> open / close / blend-open masks of 16 elements (bit i <-> byte i)
-__device__ __forceinline__ void classify16b(uint4 raw, uint32_t& om, uint32_t& cm, uint32_t& bm) {
-  uint32_t o = 0, c = 0, b = 0;
-  const uint32_t ws[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const uint32_t x = ws[q];
-    const uint32_t bl = __vcmpeq4(x, 0x02020202u);
-    o |= byte_mask4(__vcmpeq4(x, 0x01010101u) | bl) << (4 * q);
-    c |= byte_mask4(__vcmpeq4(x, 0x03030303u)) << (4 * q);
-    b |= byte_mask4(bl) << (4 * q);
-  }
-  om = o;
-  cm = c;
-  bm = b;
-}
 
 // ----------------------------------------------------------------------------
 // fz_reduce: tile Bic values, slices and their local cumulative clips

@@ -153,18 +153,9 @@ __device__ __forceinline__ uint64_t gtime() {
 // tag byte classes of K elements (K / 4 words): om = opens (clip or blend),
 // bm = blend opens, cm = closes; everything else is a leaf (R2)
 __device__ __forceinline__ void classifyK(const uint32_t (&ws)[K / 4], uint32_t& om, uint32_t& cm, uint32_t& bm) {
-  uint32_t o = 0, c = 0, b = 0;
-#pragma unroll
-  for (int q = 0; q < K / 4; q++) {
-    const uint32_t x = ws[q];
-    const uint32_t bl = __vcmpeq4(x, 0x02020202u);
-    o |= byte_mask4(__vcmpeq4(x, 0x01010101u) | bl) << (4 * q);
-    c |= byte_mask4(__vcmpeq4(x, 0x03030303u)) << (4 * q);
-    b |= byte_mask4(bl) << (4 * q);
-  }
-  om = o;
-  cm = c;
-  bm = b;
+  static_assert(K == 8 || K == 16, "classifyK");
+  const uint4 w = K == 16 ? make_uint4(ws[0], ws[1], ws[2 % (K / 4)], ws[3 % (K / 4)]) : make_uint4(ws[0], ws[1], 0u, 0u);
+  classify16b(w, om, cm, bm);
 }
 
 __device__ __forceinline__ void load_tagsK(const uint8_t* tags, int64_t n, int64_t tbase, uint32_t (&wv)[K / 4]) {
@@ -263,15 +254,12 @@ __global__ void __launch_bounds__(128) bbm_reduce(Params p) {
   if (lbase + RK <= p.n) {
     const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase));
     const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase) + 1);
-    const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-#pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const uint32_t x = tw[q];
-      const uint32_t bl = __vcmpeq4(x, 0x02020202u);
-      om |= byte_mask4(__vcmpeq4(x, 0x01010101u) | bl) << (4 * q);
-      cm |= byte_mask4(__vcmpeq4(x, 0x03030303u)) << (4 * q);
-      bmask |= byte_mask4(bl) << (4 * q);
-    }
+    uint32_t o1, c1, b1;
+    classify16b(t0, om, cm, bmask);
+    classify16b(t1, o1, c1, b1);
+    om |= o1 << 16;
+    cm |= c1 << 16;
+    bmask |= b1 << 16;
   } else {
     for (int i = 0; i < RK; i++) {
       const int64_t g = lbase + i;

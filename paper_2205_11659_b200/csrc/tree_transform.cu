@@ -88,10 +88,10 @@ __global__ void __launch_bounds__(128) tt_reduce(Params p) {
   if (lbase + RK <= p.n) {
     const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase));
     const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(p.tags + lbase) + 1);
-    const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-#pragma unroll
-    for (int q = 0; q < 8; q++)
-      om |= byte_mask4(__vcmpeq4(tw[q], 0x01010101u) | __vcmpeq4(tw[q], 0x02020202u)) << (4 * q);
+    uint32_t o1, c0, c1;
+    classify16(t0, om, c0);
+    classify16(t1, o1, c1);
+    om |= o1 << 16;
   } else {
     for (int i = 0; i < RK && lbase + i < p.n; i++)
       if (is_open(p.tags[lbase + i])) om |= 1u << i;
