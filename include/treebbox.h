@@ -54,6 +54,7 @@ extern "C" {
 #define TB_ERR_ALIAS -3  /* an output overlaps an input or another output */
 #define TB_ERR_CUDA -4   /* CUDA launch / allocation / copy error */
 #define TB_ERR_NCCL -5   /* NCCL error (sharded entry points) */
+#define TB_ERR_CAPACITY -6 /* sharded call: a chunk's Bic value exceeds the fixed capacity (a + 1 or b > cap) */
 
 /* Tag byte values (R2). */
 #define TB_LEAF 0
@@ -272,15 +273,36 @@ int tb_comm_destroy(void *comm);
 int paren_match_shard(const uint8_t *d_tags, int64_t n_local, int64_t offset, int32_t *d_match,
                       int32_t *d_parent, void *comm, void *stream);
 /* tree_bbox over contiguous chunks: d_leaf_bbox / d_node_bbox hold the chunk's
- * n_local boxes.  Runs paren_match_shard (global matching) first, then the
- * boxes from the matching: exchange 1 carries each chunk's final stack (opens
- * closed after it or never) with chunk-local cumulative clips, from which every
- * rank derives the true contexts of earlier chunks' opens; exchange 2 carries
- * chunk unions, the union after each final-stack open and the closes of
- * earlier chunks' nodes with their prefix unions, from which every rank
- * finishes the nodes that span chunks (F4). */
+ * n_local boxes.  paren_match_tree_bbox_shard below without match / parent,
+ * capacity tb_shard_default_cap(n_local), then tb_shard_status (synchronises
+ * `stream`; TB_ERR_CAPACITY when a chunk is deeper than that capacity). */
 int tree_bbox_shard(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n_local, int64_t offset,
                     float *d_node_bbox, void *comm, void *stream);
+/* The bench step sharded: paren_match + tree_bbox of the fused one-device pass
+ * (fused.cu) over contiguous chunks with TWO fixed-size NCCL all-gathers and no
+ * host synchronisation (csrc/fused_shard.cuh):
+ *   exchange 1: each chunk's Bic value (a, b) and its final stack
+ *     (the b opens it leaves open, bottom to top: global index | blend << 31,
+ *     context inside the chunk), cap entries per rank;
+ *   exchange 2: each chunk's union, the union after each final-stack open to
+ *     the chunk end, and the closes of earlier chunks' opens with this
+ *     chunk's part of their union (cap entries per rank).
+ * Every rank composes the top of its incoming stack from the headers (the
+ * owner rule over chunks, F1) before its main pass and finishes the nodes
+ * that span chunks after exchange 2.  `cap` must be equal on every rank and
+ * bound every chunk's a + 1 and b (tb_shard_default_cap(n_local) = 4 sqrt(n)
+ * + 4096 suits random streams; a deep stream needs up to n_local + 2).  The
+ * call returns once the work is enqueued; an overflow of cap is detected on
+ * the device (every rank sees the headers) and reported by tb_shard_status,
+ * which waits for the stream: TB_ERR_CAPACITY, outputs undefined.
+ * d_match / d_parent may both be null (tree_bbox alone). */
+int64_t tb_shard_default_cap(int64_t n_local);
+int paren_match_tree_bbox_shard(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n_local, int64_t offset,
+                                int64_t cap, int32_t *d_match, int32_t *d_parent, float *d_node_bbox, void *comm,
+                                void *stream);
+/* TB_ERR_CAPACITY if the last paren_match_tree_bbox_shard call on `stream`
+ * overflowed its capacity, else 0.  Synchronises `stream`. */
+int tb_shard_status(void *stream);
 /* The same from a matching already computed by paren_match_shard (d_match /
  * d_parent: the chunk's n_local entries, GLOBAL indices). */
 int tree_bbox_matched_shard(const uint8_t *d_tags, const float *d_leaf_bbox, const int32_t *d_match,

@@ -21,7 +21,7 @@ from . import build as _build
 
 __all__ = ["release_workspaces", "paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "bin_leaves", "compact_scene", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
-           "tree_bbox_vshard"]
+           "tree_bbox_vshard", "pair_vshard", "shard_default_cap"]
 
 LIB_PATH = _build.LIB
 _lock = threading.Lock()
@@ -77,6 +77,10 @@ def load():
                 "tb_debug_fz_abl": ([ctypes.c_int], ctypes.c_int),
                 "tb_debug_bins_cap": ([I64], I64),
                 "tree_bbox_shard": ([P, P, I64, I64, P, P, P], ctypes.c_int),
+                "paren_match_tree_bbox_shard": ([P, P, I64, I64, I64, P, P, P, P, P], ctypes.c_int),
+                "tb_shard_status": ([P], ctypes.c_int),
+                "tb_shard_default_cap": ([I64], I64),
+                "tb_debug_pair_vshard": ([P, P, I64, ctypes.c_int, I64, P, P, P, P], ctypes.c_int),
                 "tree_bbox_matched_shard": ([P, P, P, P, I64, I64, P, P, P], ctypes.c_int),
                 "tb_launch_count": ([], ctypes.c_longlong),
                 "tb_profile_enable": ([ctypes.c_int], ctypes.c_int),
@@ -368,6 +372,35 @@ def tree_bbox_vshard(tags: torch.Tensor, leaf_bbox: torch.Tensor, nshards: int):
     return out
 
 
+def shard_default_cap(n_local: int) -> int:
+    """Default capacity of a sharded call (every chunk's Bic a + 1 and b must
+    fit): 4 sqrt(n_local) + 4096, at most n_local + 2."""
+    return int(load().tb_shard_default_cap(int(n_local)))
+
+
+def pair_vshard(tags: torch.Tensor, leaf_bbox: torch.Tensor, nshards: int, cap: int = None, pm: bool = True):
+    """Test hook: paren_match_tree_bbox by the sharded fused protocol with
+    `nshards` virtual shards of one device buffer on one GPU (the chunks run
+    the three phases in lockstep; their slots are the gathered buffers).
+    Returns (match, parent, node_bbox); match / parent are None when pm=False."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    _need_cuda(leaf_bbox, "leaf_bbox", torch.float32)
+    n = tags.numel()
+    if leaf_bbox.shape != (n, 4):
+        raise ValueError("leaf_bbox must be (n, 4)")
+    if cap is None:
+        cap = shard_default_cap((n + nshards - 1) // nshards + 16)  # chunk borders: multiples of 16
+    out = torch.empty_like(leaf_bbox)
+    match = torch.empty(n, dtype=torch.int32, device=tags.device) if pm else None
+    parent = torch.empty(n, dtype=torch.int32, device=tags.device) if pm else None
+    with torch.cuda.device(tags.device):
+        _check(lib.tb_debug_pair_vshard(tags.data_ptr(), leaf_bbox.data_ptr(), n, nshards, int(cap),
+                                        match.data_ptr() if pm else None, parent.data_ptr() if pm else None,
+                                        out.data_ptr(), _stream(tags.device)))
+    return match, parent, out
+
+
 class ShardContext:
     """One rank of a sharded run (one process per GPU, contiguous chunks in
     rank order).  Bootstraps the library's own NCCL communicator through the
@@ -387,6 +420,10 @@ class ShardContext:
         t = torch.tensor(list(bytes(buf)), dtype=torch.uint8,
                          device=self.device if backend == "nccl" else "cpu")
         dist.broadcast(t, 0)
+        # one capacity on every rank: from the largest chunk (once, at setup)
+        nm = torch.tensor([int(n_local)], dtype=torch.int64, device=t.device)
+        dist.all_reduce(nm, op=dist.ReduceOp.MAX)
+        self.default_cap = shard_default_cap(int(nm.item()))
         ident = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
         comm = ctypes.c_void_p()
         with torch.cuda.device(self.device):
@@ -408,6 +445,38 @@ class ShardContext:
             _check(lib.tree_bbox_shard(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), self.offset,
                                        node_bbox.data_ptr(), self.comm, _stream(tags.device)))
         return node_bbox
+
+    def paren_match_tree_bbox(self, tags: torch.Tensor, leaf_bbox: torch.Tensor, match: torch.Tensor,
+                              parent: torch.Tensor, node_bbox: torch.Tensor, cap: int = None, check: bool = True):
+        """The bench step on this rank's chunk: two fixed-size all-gathers, no
+        host synchronisation.  `cap` must be equal on every rank (default:
+        shard_default_cap of the largest chunk, ceil(n_total / world)).  With
+        check=False the call only enqueues; call status() before trusting the
+        outputs (an overflow of cap raises there)."""
+        lib = load()
+        _need_cuda(tags, "tags", torch.uint8)
+        _need_cuda(leaf_bbox, "leaf_bbox", torch.float32)
+        for t, nm in ((match, "match"), (parent, "parent")):
+            _need_cuda(t, nm, torch.int32)
+            if t.numel() != tags.numel():
+                raise ValueError(f"{nm} must have n_local elements")
+        _need_cuda(node_bbox, "node_bbox", torch.float32)
+        if leaf_bbox.shape != (tags.numel(), 4) or node_bbox.shape != (tags.numel(), 4):
+            raise ValueError("leaf_bbox / node_bbox must be (n_local, 4)")
+        if cap is None:
+            cap = self.default_cap
+        with torch.cuda.device(tags.device):
+            _check(lib.paren_match_tree_bbox_shard(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), self.offset,
+                                                   int(cap), match.data_ptr(), parent.data_ptr(), node_bbox.data_ptr(),
+                                                   self.comm, _stream(tags.device)))
+            if check:
+                _check(lib.tb_shard_status(_stream(tags.device)))
+        return match, parent, node_bbox
+
+    def status(self):
+        """Wait for this rank's last sharded call; raises on a capacity overflow."""
+        with torch.cuda.device(self.device):
+            _check(load().tb_shard_status(_stream(self.device)))
 
     def tree_bbox_matched(self, tags: torch.Tensor, leaf_bbox: torch.Tensor, match: torch.Tensor,
                           parent: torch.Tensor, node_bbox: torch.Tensor):

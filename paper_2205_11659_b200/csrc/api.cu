@@ -1,5 +1,6 @@
 // C ABI (include/treebbox.h): argument validation, workspace cache, launches.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -13,12 +14,17 @@
 #include <nccl.h>
 namespace tb {
 int shard_release_arenas(int dev);
+cudaError_t fz_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, int cap, int32_t* match,
+                      int32_t* parent, float* out, cudaStream_t s, int* overflow);
+cudaError_t fz_shard_status(cudaStream_t s, int* overflow);
 cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* match, int32_t* parent,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err);
 cudaError_t bbm_nccl_shard(const uint8_t* tags, const float* leaf, const int32_t* match, const int32_t* parent,
                            int64_t n, int64_t off, float* out, ncclComm_t comm, cudaStream_t s, int* nccl_err);
 cudaError_t bb_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, float* out,
                           ncclComm_t comm, cudaStream_t s, int* nccl_err);
+cudaError_t fz_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, int cap, int32_t* match,
+                          int32_t* parent, float* out, ncclComm_t comm, cudaStream_t s, int* nccl_err);
 }
 #endif
 
@@ -725,15 +731,77 @@ int tree_bbox_shard(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n_l
   if (offset < 0 || offset + n_local > kMaxN) return fail(TB_ERR_ARG, "offset + n_local out of range");
   if (!comm) return fail(TB_ERR_ARG, "null communicator");
 #ifdef TB_WITH_NCCL
+  // the fused protocol without match / parent, default capacity, checked
   int nerr = 0;
-  cudaError_t e = tb::bb_nccl_shard(d_tags, d_leaf_bbox, n_local, offset, d_node_bbox, (ncclComm_t)comm,
-                                    (cudaStream_t)stream, &nerr);
-  if (nerr) return fail(TB_ERR_NCCL, "NCCL error %d", nerr);
+  cudaError_t e = tb::fz_nccl_shard(d_tags, d_leaf_bbox, n_local, offset, (int)tb_shard_default_cap(n_local),
+                                    nullptr, nullptr, d_node_bbox, (ncclComm_t)comm, (cudaStream_t)stream, &nerr);
+  if (nerr) return fail(TB_ERR_NCCL, "NCCL error");
   if (e != cudaSuccess) return cuda_fail(e, "tree_bbox_shard");
+  return tb_shard_status(stream);
+#else
+  return fail(TB_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+int64_t tb_shard_default_cap(int64_t n_local) {
+  if (n_local < 0) n_local = 0;
+  int64_t r = (int64_t)std::sqrt((double)n_local);
+  while (r * r < n_local) r++;
+  return std::min<int64_t>(4 * r + 4096, n_local + 2);
+}
+
+int paren_match_tree_bbox_shard(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n_local, int64_t offset,
+                                int64_t cap, int32_t* d_match, int32_t* d_parent, float* d_node_bbox, void* comm,
+                                void* stream) {
+  g_err[0] = 0;
+  int r = pm_checks(d_tags, n_local, d_match, d_parent);
+  if (r) return r;
+  r = bbm_checks(d_tags, d_leaf_bbox, d_match, d_parent, n_local, d_node_bbox);
+  if (r) return r;
+  const size_t nb = (size_t)n_local * 16, n4 = (size_t)n_local * 4;
+  if (overlap(d_match, n4, d_leaf_bbox, nb) || overlap(d_parent, n4, d_leaf_bbox, nb))
+    return fail(TB_ERR_ALIAS, "match / parent overlap leaf_bbox");
+  if (offset < 0 || offset + n_local > kMaxN) return fail(TB_ERR_ARG, "offset + n_local out of range");
+  if (cap < 1 || cap > kMaxN) return fail(TB_ERR_ARG, "cap out of range");
+  if (!comm) return fail(TB_ERR_ARG, "null communicator");
+#ifdef TB_WITH_NCCL
+  int nerr = 0;
+  cudaError_t e = tb::fz_nccl_shard(d_tags, d_leaf_bbox, n_local, offset, (int)cap, d_match, d_parent, d_node_bbox,
+                                    (ncclComm_t)comm, (cudaStream_t)stream, &nerr);
+  if (nerr) return fail(TB_ERR_NCCL, "NCCL error (ncclAllGather / ncclCommGetAsyncError)");
+  if (e != cudaSuccess) return cuda_fail(e, "paren_match_tree_bbox_shard");
   return TB_OK;
 #else
   return fail(TB_ERR_NCCL, "built without NCCL");
 #endif
+}
+
+int tb_shard_status(void* stream) {
+  g_err[0] = 0;
+  int ovf = 0;
+  cudaError_t e = tb::fz_shard_status((cudaStream_t)stream, &ovf);
+  if (e != cudaSuccess) return cuda_fail(e, "tb_shard_status");
+  if (ovf) return fail(TB_ERR_CAPACITY, "a chunk's Bic value exceeds the sharded call's capacity (a + 1 or b > cap)");
+  return TB_OK;
+}
+
+int tb_debug_pair_vshard(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, int nshards, int64_t cap,
+                         int32_t* d_match, int32_t* d_parent, float* d_node_bbox, void* stream) {
+  g_err[0] = 0;
+  int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
+  if (r || n == 0) return r;
+  if (d_match || d_parent) {
+    r = pm_checks(d_tags, n, d_match, d_parent);
+    if (r) return r;
+  }
+  if (nshards < 1 || nshards > 256) return fail(TB_ERR_ARG, "bad shard count");
+  if (cap < 1 || cap > kMaxN) return fail(TB_ERR_ARG, "cap out of range");
+  int ovf = 0;
+  cudaError_t e = tb::fz_vshard(d_tags, d_leaf_bbox, n, nshards, (int)cap, d_match, d_parent, d_node_bbox,
+                                (cudaStream_t)stream, &ovf);
+  if (e != cudaSuccess) return cuda_fail(e, "pair vshard");
+  if (ovf) return fail(TB_ERR_CAPACITY, "a chunk's Bic value exceeds cap");
+  return TB_OK;
 }
 
 int tree_bbox_matched_shard(const uint8_t* d_tags, const float* d_leaf_bbox, const int32_t* d_match,

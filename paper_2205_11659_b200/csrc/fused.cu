@@ -85,7 +85,18 @@ struct Params {
   uint64_t* trace;     // optional (debug): fz_ctrl phase timestamps, block 0
   int use_tma;         // fz_main: full tiles move their boxes with TMA (tensor maps below)
   int abl;             // debug (timing experiments only, results wrong): skip phases of fz_main
+  // shard mode (fused_shard.cuh; all zero / null on one device): the chunk's
+  // first element has global index goff; heights are offset by h0 and the
+  // h0 entries below are the imported stack, a virtual slice at vbase
+  int goff;
+  int h0;
+  int vbase;           // ntiles * W: slice reference of imported height 0
+  int32_t* shd;        // [SHD] shd[1]: overflow of the shard capacity (compose step)
+  int32_t* tcend;      // [ntiles] end of TC's pointer chain: -1 root, -2 - h imported height h
+  int32_t* exc;        // [h0] shard: the close popping imported height h (-1: none)
+  float4* exu;         // [h0] shard: its union over this chunk (the prefix before the close)
 };
+constexpr int SHD = 64;
 // TMA descriptors of fz_main: per array (leaf boxes in, node boxes out) one 2D
 // map per half of the thread rows: {32 floats, n/16 rows}, row stride 256 B,
 // box {32, NT}, 128-byte swizzle (the slot layout of Smem::val)
@@ -100,14 +111,16 @@ constexpr int RMAX = 8;        // runs of the incoming stack kept per tile (more
 // workspace
 // ----------------------------------------------------------------------------
 struct Layout {
-  size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, bytes;
+  size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, shd, tce, bytes;
   int64_t ntiles;
-  explicit Layout(int64_t n) {
+  explicit Layout(int64_t n, int h0 = 0) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     ntiles = (n + W - 1) / W;
-    const size_t cap = (size_t)ntiles * W;
+    const size_t cap = (size_t)ntiles * W + (size_t)h0;  // + the imported stack (shard mode)
+    const size_t ntc = (size_t)ntiles + ((size_t)h0 + W - 1) / W;
     const size_t npop = (size_t)n;                    // Σ a_T <= closes
     size_t o = 0;
+    shd = o; o = al(o + 4 * SHD);  // first: at the same offset for every n (fused_shard_status)
     ctrl = o; o = al(o + CtrlLayout(ntiles).bytes);
     aoff = o; o = al(o + 8 * ((size_t)ntiles + 1));
     sidx = o; o = al(o + 4 * cap);
@@ -122,19 +135,20 @@ struct Layout {
     pja = o; o = al(o + 32 * (size_t)ntiles);
     pjp = o; o = al(o + 8 * (size_t)ntiles);
     pjo = o; o = al(o + 4 * (size_t)ntiles);
-    tcs = o; o = al(o + 16 * (size_t)ntiles);
+    tcs = o; o = al(o + 16 * ntc);
     rns = o; o = al(o + 8 * RMAX * (size_t)ntiles);
     nrs = o; o = al(o + 4 * (size_t)ntiles);
     flag = o; o = al(o + 16);
     blk = o; o = al(o + 16 * MAXCTRL);
     blkmin = o; o = al(o + 4 * MAXCTRL);
+    tce = o; o = al(o + 4 * (size_t)ntiles);
     bytes = o;
   }
 };
 
 static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, int32_t* match, int32_t* parent,
-                          float* out, void* ws) {
-  const Layout L(n);
+                          float* out, void* ws, int h0 = 0, int goff = 0) {
+  const Layout L(n, h0);
   char* b = (char*)ws;
   Params p;
   p.tags = tags;
@@ -164,6 +178,13 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.trace = nullptr;
   p.use_tma = 0;
   p.abl = 0;
+  p.goff = goff;
+  p.h0 = h0;
+  p.vbase = (int)(L.ntiles * W);
+  p.shd = (int32_t*)(b + L.shd);
+  p.tcend = (int32_t*)(b + L.tce);
+  p.exc = nullptr;
+  p.exu = nullptr;
   return p;
 }
 
@@ -300,6 +321,7 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
       blend = ((j < 32 ? b0 : b1) >> (j & 31)) & 1u;
       e = (uint32_t)(base + L * RL + j);
       if (!blend) v = __ldg(p.boxes + e);
+      e += (uint32_t)p.goff;
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -454,7 +476,9 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   block_excl(v, ex, tot, sh);
   if (tid == 0) {
     p.blk[bx] = make_int4(tot.a, tot.b, (int)(unsigned)(tot.s & 0xffffffffll), (int)(tot.s >> 32));
-    if (bx == 0) p.flag[0] = p.flag[1] = p.flag[2] = 0;
+    if (bx == 0) {
+      p.flag[0] = p.flag[1] = p.flag[2] = 0;
+    }
   }
   grid.sync();
   FZ_TRACE(1);
@@ -479,7 +503,9 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
     Agg cur = agg_combine(pre, ex);
     for (int T = ta; T < tb; T++) {
       const int2 g = __ldcg(p.ctrl.agg + T);
-      const int H = cur.b;
+      // one device: the height is the prefix's b (its a closes popped the root);
+      // shard mode: h0 imported entries below, the prefix's a of them popped
+      const int H = p.h0 ? p.h0 - cur.a + cur.b : cur.b;
       const int L = max(H - g.x, 0);
       p.ctrl.hstart[T] = H;
       p.ctrl.lw[T] = (uint32_t)L + 1u;
@@ -587,7 +613,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
       float4 acc = bINF();
       if (U >= 0) acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - ((int)__ldcg(p.ctrl.lw + U) - 1)));
       p.pj_acc[T] = acc;
-      p.pj_ptr[T] = U;
+      p.pj_ptr[T] = U >= 0 || L < 1 ? U : -2 - (L - 1);  // no local owner: imported height L - 1
       p.pj_own[T] = U;
     }
     __syncthreads();
@@ -607,7 +633,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
       }
       if (lane == 0) {
         p.pj_acc[T] = acc;
-        p.pj_ptr[T] = U;
+        p.pj_ptr[T] = U >= 0 || L < 1 ? U : -2 - (L - 1);
         p.pj_own[T] = U;
       }
     }
@@ -668,7 +694,10 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   }
   FZ_TRACE(5);
   // P5: TC for the main pass (slice context = lc ∩ TC of the slice's tile)
-  for (int V = gt; V < nt; V += nthr) p.tc[V] = __ldcg(accb[cb] + V);
+  for (int V = gt; V < nt; V += nthr) {
+    p.tc[V] = __ldcg(accb[cb] + V);
+    p.tcend[V] = __ldcg(ptrb[cb] + V);  // -1, or -2 - h: TC still lacks imported height h's context
+  }
   FZ_TRACE(7);
 }
 
@@ -861,12 +890,15 @@ __device__ __forceinline__ int inc_ref(const Params& p, const Smem& s, int nruns
     const int2 r = s.runs[k];
     if (r.y <= h) return r.x * W + (h - r.y);
   }
-  int U = __ldg(p.pj_own + s.runs[RMAX - 1].x);
-  while (true) {  // only when the incoming stack has more than RMAX runs
-    const int LU = (int)__ldg(p.ctrl.lw + U) - 1;
-    if (LU <= h) return U * W + (h - LU);
-    U = __ldg(p.pj_own + U);
+  if (nruns > RMAX) {  // the incoming stack has more than RMAX runs
+    int U = __ldg(p.pj_own + s.runs[RMAX - 1].x);
+    while (U >= 0) {
+      const int LU = (int)__ldg(p.ctrl.lw + U) - 1;
+      if (LU <= h) return U * W + (h - LU);
+      U = __ldg(p.pj_own + U);
+    }
   }
+  return p.vbase + h;  // below every run of this chunk: the imported stack (shard mode)
 }
 
 #ifndef FZ_MINB
@@ -880,7 +912,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   const int T = blockIdx.x;
   const int64_t base = (int64_t)T * W;
   const int nvalid = (int)(p.n - base < W ? p.n - base : W);
-  const int gbase = (int)base;  // global indices fit in int32 (n <= 2^31 - 1)
+  const int gbase = p.goff + (int)base;  // global indices fit in int32 (n <= 2^31 - 1)
   const int tl0 = tid * K;      // tile-local index of the thread's first element
   const int gtb = gbase + tl0;
   const int sb = (tid << 3) | (tid & 7);  // slot(tid, i) = ((i & 8) << 7) | (sb ^ (i & 7))
@@ -998,14 +1030,16 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
       const int D = -lk - 1;
       giLast = -1;
       if (H - 1 - D >= 0) {
+        int si;
         if (D < INCCAP) {
-          giLast = s.u.pj.inc_idx[D] & 0x7fffffff;
+          si = s.u.pj.inc_idx[D];
           acc = isect(s.u.pj.inc_box[D], s.u.pj.inc_tc[D]);
         } else {
           const int ref = inc_ref(p, s, nruns, H - 1 - D);
-          giLast = __ldg(p.slice_idx + ref) & 0x7fffffff;
+          si = __ldg(p.slice_idx + ref);
           acc = isect(__ldg(p.slice_box + ref), __ldg(p.tc + (ref >> LOGW)));
         }
+        giLast = si == -1 ? -1 : si & 0x7fffffff;  // -1: an imported slot below the global root (INF)
       }
     }
     int cb = 0;
@@ -1092,9 +1126,13 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
           si = __ldg(p.slice_idx + rf);
           if (seg & needm) cx = isect(__ldg(p.slice_box + rf), __ldg(p.tc + (rf >> LOGW)));
         }
-        gi = si & 0x7fffffff;
-        xcm |= 1u << ci;
-        p.pop[poff + D] = make_int2(gtb + ci, rf);
+        if (si != -1) {
+          gi = si & 0x7fffffff;
+          xcm |= 1u << ci;
+          p.pop[poff + D] = make_int2(gtb + ci, rf);
+        } else {
+          p.pop[poff + D] = make_int2(-1, -1);  // an imported slot below the global root (R3)
+        }
       } else {
         p.pop[poff + D] = make_int2(-1, -1);  // pops the root (R3)
       }
@@ -1410,11 +1448,14 @@ __global__ void __launch_bounds__(128) fz_close(Params p) {
     const bool valid = r.x >= 0;  // root pops (R3) have no node
     int To = T, si = 0;
     float4 P = bEMPTY(), su = bEMPTY();
+    const bool imp = r.y >= p.vbase;  // pops an imported entry (shard mode): opened on another chunk
     if (valid) {
-      To = r.y >> LOGW;
-      P = __ldcg(p.out + r.x);  // the tile prefix before the close (fz_main)
-      su = __ldg(p.slice_su + r.y);
-      si = __ldg(p.slice_idx + r.y);
+      To = imp ? -1 : r.y >> LOGW;
+      P = __ldcg(p.out + (r.x - p.goff));  // the tile prefix before the close (fz_main)
+      if (!imp) {
+        su = __ldg(p.slice_su + r.y);
+        si = __ldg(p.slice_idx + r.y);
+      }
     }
     float4 R = bEMPTY();
     bool pending = valid && To < T - 1;
@@ -1435,12 +1476,19 @@ __global__ void __launch_bounds__(128) fz_close(Params p) {
     }
     if (valid) {
       const float4 U = unite(unite(P, su), R);
-      const int o = si & 0x7fffffff;
-      p.out[r.x] = U;
-      if (si < 0) p.out[o] = U;  // a blend open
-      if (PM) p.match[o] = r.x;
+      p.out[r.x - p.goff] = U;
+      if (imp) {  // this chunk's part of the node; the rest after the exchange (fused_shard.cuh)
+        const int h = r.y - p.vbase;
+        p.exc[h] = r.x;
+        p.exu[h] = U;
+      } else {
+        const int o = (si & 0x7fffffff) - p.goff;
+        if (si < 0) p.out[o] = U;  // a blend open
+        if (PM) p.match[o] = r.x;
+      }
     }
   }
+  if (p.h0) return;  // shard mode: the chunk's final stack is finished after the exchange
   // blend opens never closed (R4): the tile's slice entries that survive to
   // the end of the stream (F1: its bottom min(b_T, smin_T - L_T))
   const int surv = min(bT, sm == INT_MAX ? bT : max(sm - L, 0));
@@ -1452,7 +1500,7 @@ __global__ void __launch_bounds__(128) fz_close(Params p) {
       for (int k = lane; k < surv; k += 32) {
         const int64_t ref = (int64_t)T * W + k;
         const int si = __ldg(p.slice_idx + ref);
-        if (si < 0) p.out[si & 0x7fffffff] = unite(__ldg(p.slice_su + ref), after);
+        if (si < 0) p.out[(si & 0x7fffffff) - p.goff] = unite(__ldg(p.slice_su + ref), after);
       }
     }
   }
@@ -1550,41 +1598,39 @@ static cudaError_t dbg_sync(cudaStream_t s, const char* what) {
   return e;
 }
 
-cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, int32_t* match, int32_t* parent,
-                         float* node_bbox, void* ws, cudaStream_t stream) {
-  if (n <= 0) return cudaSuccess;
-  cudaError_t e = fz::setup();
-  if (e != cudaSuccess) return e;
-  const bool pm = match != nullptr;
-  fz::Params p = fz::make_params(tags, leaf_bbox, n, match, parent, node_bbox, ws);
-  p.trace = g_fz_trace;
+// the passes before the main pass: tile Bic values and slices, then the
+// cooperative control kernel (tile scan, link owners, TC)
+static cudaError_t launch_front(fz::Params& p, cudaStream_t stream) {
   const int nt = p.ntiles;
   TB_LAUNCH(stream, "fz_reduce", (fz::fz_reduce<<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
-  e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = dbg_sync(stream, "fz_reduce");
   if (e != cudaSuccess) return e;
-  {
-    // enough blocks for the per-tile warps of P3 / P5, at most the co-resident
-    // count; chunks of whole 32-tile groups
-    const int G = std::max(1, std::min((nt + 31) / 32, fz::ctrl_blocks()));
-    p.chunk = (((nt + G - 1) / G) + 31) & ~31;
-    void* args[] = {(void*)&p};
-    void* tok;
-    prof_begin(stream, "fz_ctrl", &tok);
-    e = cudaLaunchCooperativeKernel((const void*)fz::fz_ctrl, dim3(G), dim3(fz::NTC), args, 0, stream);
-    prof_end(stream, tok);
-    if (e == cudaSuccess) e = dbg_sync(stream, "fz_ctrl");
-    if (e != cudaSuccess) return e;
-  }
+  // enough blocks for the per-tile warps of P3 / P5, at most the co-resident
+  // count; chunks of whole 32-tile groups
+  const int G = std::max(1, std::min((nt + 31) / 32, fz::ctrl_blocks()));
+  p.chunk = (((nt + G - 1) / G) + 31) & ~31;
+  void* args[] = {(void*)&p};
+  void* tok;
+  prof_begin(stream, "fz_ctrl", &tok);
+  e = cudaLaunchCooperativeKernel((const void*)fz::fz_ctrl, dim3(G), dim3(fz::NTC), args, 0, stream);
+  prof_end(stream, tok);
+  if (e == cudaSuccess) e = dbg_sync(stream, "fz_ctrl");
+  return e;
+}
+
+// the main pass, the tile-union hierarchy and the close pass
+static cudaError_t launch_back(fz::Params& p, const float* leaf_bbox, float* node_bbox, bool pm, cudaStream_t stream) {
+  const int nt = p.ntiles;
   fz::Maps maps;
   memset(&maps, 0, sizeof maps);
-  p.use_tma = g_fz_tma && fz::make_maps(leaf_bbox, node_bbox, n, maps) ? 1 : 0;
+  p.use_tma = g_fz_tma && fz::make_maps(leaf_bbox, node_bbox, p.n, maps) ? 1 : 0;
   p.abl = g_fz_abl;
   if (pm)
     TB_LAUNCH(stream, "fz_main", (fz::fz_main<true><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p, maps)));
   else
     TB_LAUNCH(stream, "fz_main", (fz::fz_main<false><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p, maps)));
-  e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = dbg_sync(stream, "fz_main");
   if (e != cudaSuccess) return e;
   int m = nt;
@@ -1603,5 +1649,19 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
   if (e == cudaSuccess) e = dbg_sync(stream, "fz_close");
   return e;
 }
+
+cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, int32_t* match, int32_t* parent,
+                         float* node_bbox, void* ws, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t e = fz::setup();
+  if (e != cudaSuccess) return e;
+  fz::Params p = fz::make_params(tags, leaf_bbox, n, match, parent, node_bbox, ws);
+  p.trace = g_fz_trace;
+  e = launch_front(p, stream);
+  if (e != cudaSuccess) return e;
+  return launch_back(p, leaf_bbox, node_bbox, match != nullptr, stream);
+}
+
+#include "fused_shard.cuh"
 
 }  // namespace tb

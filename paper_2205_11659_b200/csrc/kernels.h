@@ -71,7 +71,21 @@ struct ShardOpen {
 size_t fused_workspace_bytes(int64_t n);
 void fused_set_trace(uint64_t* dev);  // debug: fz_ctrl phase timestamps (8 x u64 device buffer) or null
 int fused_set_tma(int on);
-int fused_set_abl(int mask);          // debug: skip fz_main phases (1 start stacks, 2 forward walk, 4 cross-thread unions)            // debug: TMA box transfers in fz_main (1, default) or thread copies (0)
+int fused_set_abl(int mask);  // debug: skip fz_main phases (1 start stacks, 2 forward walk, 4 cross-thread unions)
+// the fused pass over one chunk of a sharded stream (fused_shard.cuh): three
+// phases around two fixed-size exchanges of slot1 / slot2 (cap: the largest
+// Bic a + 1 and b of a chunk; equal on every rank)
+size_t fused_shard_workspace_bytes(int64_t n, int cap);
+size_t fused_shard_slot1_bytes(int cap);
+size_t fused_shard_slot2_bytes(int cap);
+cudaError_t fused_shard_phase1(const uint8_t* tags, const float* leaf_bbox, int64_t n, int64_t goff, int cap,
+                               void* ws, void* slot1, cudaStream_t stream);
+cudaError_t fused_shard_phase2(const uint8_t* tags, const float* leaf_bbox, int64_t n, int64_t goff, int cap, int G,
+                               int g, int32_t* match, int32_t* parent, float* node_bbox, void* ws, const void* recv1,
+                               void* slot2, cudaStream_t stream);
+cudaError_t fused_shard_phase3(int64_t n, int64_t goff, int cap, int G, int g, int32_t* match, float* node_bbox,
+                               void* ws, const void* recv1, const void* recv2, cudaStream_t stream);
+int fused_shard_status(int64_t n, int cap, void* ws, cudaStream_t stream, cudaError_t* err);
 int fused_tile_elems();
 cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n, int32_t* match, int32_t* parent,
                          float* node_bbox, void* ws, cudaStream_t stream);

@@ -74,7 +74,9 @@ std::map<std::pair<int, cudaStream_t>, Arena> g_arenas;
 
 // tb_release_workspaces: free every shard arena of the current device (the
 // caller guarantees no call is in flight on any stream of it)
+void fz_forget_last(int dev);
 int shard_release_arenas(int dev) {
+  fz_forget_last(dev);
   std::lock_guard<std::mutex> lk(g_arena_mu);
   int freed = 0;
   for (auto it = g_arenas.begin(); it != g_arenas.end();) {
@@ -662,5 +664,135 @@ cudaError_t pm_nccl_shard(const uint8_t* tags, int64_t n, int64_t off, int32_t* 
   return e;
 }
 #endif
+
+// ---- the fused pass over shards (fused_shard.cuh) -------------------------------
+// Buffers of one rank: workspace, its two slots and the two gathered copies,
+// from the per-(device, stream) arena (no allocation in a steady state).
+namespace {
+struct FzBufs {
+  char* ws = nullptr;
+  char* slot1 = nullptr;
+  char* recv1 = nullptr;
+  char* slot2 = nullptr;
+  char* recv2 = nullptr;
+};
+cudaError_t fz_bufs(Scratch& sc, int64_t n, int cap, int G, int nws, FzBufs& b) {
+  const size_t wsb = fused_shard_workspace_bytes(std::max<int64_t>(n, 1), cap);
+  const size_t s1 = fused_shard_slot1_bytes(cap), s2 = fused_shard_slot2_bytes(cap);
+  cudaError_t e = sc.get(wsb * (size_t)nws, &b.ws);
+  if (e == cudaSuccess) e = sc.get(s1, &b.slot1);
+  if (e == cudaSuccess) e = sc.get(s1 * (size_t)G, &b.recv1);
+  if (e == cudaSuccess) e = sc.get(s2, &b.slot2);
+  if (e == cudaSuccess) e = sc.get(s2 * (size_t)G, &b.recv2);
+  return e;
+}
+std::mutex g_fzlast_mu;
+struct FzLast {
+  int64_t n;
+  int cap;
+  char* ws;
+};
+std::map<std::pair<int, cudaStream_t>, FzLast> g_fzlast;  // the last call's workspace (status)
+}  // namespace
+
+// Virtual shards (tests): G contiguous chunks of one buffer, the phases in
+// lockstep on one stream; chunk k's slots ARE the k-th parts of the gathered
+// buffers, so the exchanges are no-ops.
+cudaError_t fz_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, int cap, int32_t* match,
+                      int32_t* parent, float* out, cudaStream_t s, int* overflow) {
+  Scratch sc(s, 3);
+  cudaError_t e = sc.begin();
+  if (e != cudaSuccess) return e;
+  // chunk borders at multiples of 16 elements (the kernels' 16-byte alignment of
+  // every array); chunks may be empty
+  auto off = [&](int k) { return k >= G ? n : (n * k / G) & ~int64_t(15); };
+  int64_t nmax = 0;
+  for (int k = 0; k < G; k++) nmax = std::max(nmax, off(k + 1) - off(k));
+  FzBufs b;
+  e = fz_bufs(sc, nmax, cap, G, G, b);
+  if (e != cudaSuccess) return e;
+  const size_t wsb = fused_shard_workspace_bytes(std::max<int64_t>(nmax, 1), cap);
+  const size_t s1 = fused_shard_slot1_bytes(cap), s2 = fused_shard_slot2_bytes(cap);
+  for (int k = 0; k < G && e == cudaSuccess; k++)
+    e = fused_shard_phase1(tags + off(k), leaf + 4 * off(k), off(k + 1) - off(k), off(k), cap, b.ws + wsb * k,
+                           b.recv1 + s1 * k, s);
+  for (int k = 0; k < G && e == cudaSuccess; k++)
+    e = fused_shard_phase2(tags + off(k), leaf + 4 * off(k), off(k + 1) - off(k), off(k), cap, G, k,
+                           match ? match + off(k) : nullptr, parent ? parent + off(k) : nullptr, out + 4 * off(k),
+                           b.ws + wsb * k, b.recv1, b.recv2 + s2 * k, s);
+  for (int k = 0; k < G && e == cudaSuccess; k++)
+    e = fused_shard_phase3(off(k + 1) - off(k), off(k), cap, G, k, match ? match + off(k) : nullptr,
+                           out + 4 * off(k), b.ws + wsb * k, b.recv1, b.recv2, s);
+  if (e == cudaSuccess && overflow) {
+    cudaError_t e2 = cudaSuccess;
+    *overflow = 0;
+    for (int k = 0; k < G && e2 == cudaSuccess; k++)
+      *overflow |= fused_shard_status(std::max<int64_t>(nmax, 1), cap, b.ws + wsb * k, s, &e2);
+    e = e2;
+  }
+  return e;
+}
+
+#ifdef TB_WITH_NCCL
+// One rank over NCCL: two all-gathers of fixed size, nothing waits on the host.
+// NCCL failures (including asynchronous ones: ncclCommGetAsyncError after each
+// collective is enqueued) are reported through *nccl_err.
+cudaError_t fz_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int64_t off, int cap, int32_t* match,
+                          int32_t* parent, float* out, ncclComm_t comm, cudaStream_t s, int* nccl_err) {
+  *nccl_err = 0;
+  int G = 0, g = 0;
+  if (ncclCommCount(comm, &G) != ncclSuccess || ncclCommUserRank(comm, &g) != ncclSuccess) {
+    *nccl_err = 1;
+    return cudaSuccess;
+  }
+  Scratch sc(s, 3);
+  cudaError_t e = sc.begin();
+  if (e != cudaSuccess) return e;
+  FzBufs b;
+  e = fz_bufs(sc, n, cap, G, 1, b);
+  if (e != cudaSuccess) return e;
+  auto nccl_ok = [&](ncclResult_t r) {
+    ncclResult_t ar = ncclSuccess;
+    if (r == ncclSuccess) r = ncclCommGetAsyncError(comm, &ar);
+    if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) *nccl_err = 1;
+    return !*nccl_err;
+  };
+  const size_t s1 = fused_shard_slot1_bytes(cap), s2 = fused_shard_slot2_bytes(cap);
+  e = fused_shard_phase1(tags, leaf, n, off, cap, b.ws, b.slot1, s);
+  if (e != cudaSuccess || !nccl_ok(ncclAllGather(b.slot1, b.recv1, s1, ncclUint8, comm, s))) return e;
+  e = fused_shard_phase2(tags, leaf, n, off, cap, G, g, match, parent, out, b.ws, b.recv1, b.slot2, s);
+  if (e != cudaSuccess || !nccl_ok(ncclAllGather(b.slot2, b.recv2, s2, ncclUint8, comm, s))) return e;
+  e = fused_shard_phase3(n, off, cap, G, g, match, out, b.ws, b.recv1, b.recv2, s);
+  if (e == cudaSuccess) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_fzlast_mu);
+    g_fzlast[{dev, s}] = FzLast{n, cap, b.ws};
+  }
+  return e;
+}
+#endif
+
+void fz_forget_last(int dev) {
+  std::lock_guard<std::mutex> lk(g_fzlast_mu);
+  for (auto it = g_fzlast.begin(); it != g_fzlast.end();) it = it->first.first == dev ? g_fzlast.erase(it) : std::next(it);
+}
+
+// overflow flag of the last sharded call on this (device, stream): waits for it
+cudaError_t fz_shard_status(cudaStream_t s, int* overflow) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  FzLast last{-1, 0, nullptr};
+  {
+    std::lock_guard<std::mutex> lk(g_fzlast_mu);
+    auto it = g_fzlast.find({dev, s});
+    if (it != g_fzlast.end()) last = it->second;
+  }
+  *overflow = 0;
+  if (!last.ws) return cudaSuccess;
+  *overflow = fused_shard_status(std::max<int64_t>(last.n, 1), last.cap, last.ws, s, &e);
+  return e;
+}
 
 }  // namespace tb
