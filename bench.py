@@ -296,6 +296,10 @@ def main():
     import paper_2205_11659_b200 as tb
     if world > 1:
         import torch.distributed as dist
+        # the communicators' setup (ranks, transports, NVLS) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
@@ -317,9 +321,8 @@ def main():
     def step():
         if shard is None:
             tb.paren_match_tree_bbox(tags, boxes, match, parent, out)
-        else:
-            shard.paren_match(tags, match, parent)
-            shard.tree_bbox_matched(tags, boxes, match, parent, out)
+        else:  # two fixed-size all-gathers, no host synchronisation (status checked after timing)
+            shard.paren_match_tree_bbox(tags, boxes, match, parent, out, check=False)
 
     def barrier():
         if world > 1:
@@ -361,6 +364,8 @@ def main():
     ms = timed(step, args.steps)
     launches = lib.tb_launch_count() - launches0
     clk = clocks.stop()
+    if shard is not None:
+        shard.status()  # capacity overflow of any timed step would raise here
     barrier()
     if world > 1:
         import torch.distributed as dist
@@ -456,7 +461,7 @@ def main():
                "h2d_bytes_per_step": 17 * n, "d2h_bytes_per_step": 24 * n,
                "steps": e_steps,
                "api": ("paren_match_tree_bbox_host (pinned host buffers)" if shard is None else
-                       "pinned H2D + ShardContext.paren_match/tree_bbox + D2H")}
+                       "pinned H2D + ShardContext.paren_match_tree_bbox + D2H")}
 
     # --- oracle on the host (rank 0, N = 1 only): one pinned thread, median of 3
     cpu = None

@@ -1,6 +1,6 @@
-"""Dev: one step of the sharded path (NCCL world of one rank) against the
-unsharded step on the same 2^27 stream (CUDA events), to see the protocol's
-own overhead: extra passes, host syncs, exchange copies."""
+"""Dev: the sharded bench step (paren_match_tree_bbox_shard, NCCL world of one
+rank) against the unsharded fused step on the same stream (CUDA events): the
+protocol's own overhead (export / compose / fix-up kernels, two all-gathers)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, torch.distributed as dist
@@ -17,15 +17,17 @@ def t(fn, k=10):
     torch.cuda.synchronize(); a.record()
     for _ in range(k): fn()
     b.record(); torch.cuda.synchronize(); return a.elapsed_time(b) / k
-plain = t(lambda: (tb.paren_match(tags, m, p), tb.tree_bbox_matched(tags, boxes, m, p, out)))
-ref = out.clone()
-shard = t(lambda: (ctx.paren_match(tags, m, p), ctx.tree_bbox_matched(tags, boxes, m, p, out)))
-print(f"n=2^{n.bit_length()-1} plain {plain:.3f} ms  shard(world 1) {shard:.3f} ms  same={torch.equal(out.view(torch.int32), ref.view(torch.int32))}")
+plain = t(lambda: tb.paren_match_tree_bbox(tags, boxes, m, p, out))
+ref = (m.clone(), p.clone(), out.clone())
+shard = t(lambda: ctx.paren_match_tree_bbox(tags, boxes, m, p, out, check=False))
+ctx.status()
+same = torch.equal(m, ref[0]) and torch.equal(p, ref[1]) and torch.equal(out.view(torch.int32), ref[2].view(torch.int32))
+print(f"n=2^{n.bit_length()-1} plain {plain:.3f} ms  shard(world 1) {shard:.3f} ms  (+{(shard / plain - 1) * 100:.1f} %)  same={same}")
 import ctypes, json
 lib = tb.load()
 lib.tb_profile_read.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
-for name, fn in (("plain", lambda: (tb.paren_match(tags, m, p), tb.tree_bbox_matched(tags, boxes, m, p, out))),
-                 ("shard", lambda: (ctx.paren_match(tags, m, p), ctx.tree_bbox_matched(tags, boxes, m, p, out)))):
+for name, fn in (("plain", lambda: tb.paren_match_tree_bbox(tags, boxes, m, p, out)),
+                 ("shard", lambda: ctx.paren_match_tree_bbox(tags, boxes, m, p, out, check=False))):
     lib.tb_profile_enable(1); lib.tb_profile_read(None, 0)
     for _ in range(5): fn()
     torch.cuda.synchronize()
