@@ -261,8 +261,10 @@ int paren_match_tree_bbox_host(const uint8_t *h_tags, const float *h_leaf_bbox, 
  * NCCL all-gathers on `comm`, and each rank finishes locally; a close whose
  * open lies in an earlier chunk is reported to that chunk in a second small
  * all-gather.  `comm` is an ncclComm_t (from tb_comm_init).  Collective: all
- * ranks must call with their chunks.  The call synchronises `stream` (the
- * exchange sizes are read on the host).
+ * ranks must call with their chunks.  paren_match_shard and
+ * tree_bbox_matched_shard synchronise `stream` (their exchange sizes are read
+ * on the host; tree_bbox_matched_shard takes at most 64 ranks);
+ * paren_match_tree_bbox_shard (the bench step) does not.
  * ------------------------------------------------------------------------ */
 #define TB_UNIQUE_ID_BYTES 128
 /* Rank 0 creates an id; broadcast its 128 bytes to the other ranks. */
@@ -274,8 +276,9 @@ int paren_match_shard(const uint8_t *d_tags, int64_t n_local, int64_t offset, in
                       int32_t *d_parent, void *comm, void *stream);
 /* tree_bbox over contiguous chunks: d_leaf_bbox / d_node_bbox hold the chunk's
  * n_local boxes.  paren_match_tree_bbox_shard below without match / parent,
- * capacity tb_shard_default_cap(n_local), then tb_shard_status (synchronises
- * `stream`; TB_ERR_CAPACITY when a chunk is deeper than that capacity). */
+ * capacity tb_shard_default_cap of the largest chunk (an all-reduce over the
+ * ranks), then tb_shard_status (synchronises `stream`; TB_ERR_CAPACITY when a
+ * chunk is deeper than that capacity). */
 int tree_bbox_shard(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n_local, int64_t offset,
                     float *d_node_bbox, void *comm, void *stream);
 /* The bench step sharded: paren_match + tree_bbox of the fused one-device pass

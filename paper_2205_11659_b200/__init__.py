@@ -106,6 +106,23 @@ def _stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def _need_host(t: torch.Tensor, name: str, dtype, numel: int | None = None):
+    """A CPU tensor of this dtype, contiguous, with `numel` elements."""
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a CPU (preferably pinned) tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {t.numel()}")
+
+
+def _need_size(t: torch.Tensor, name: str, numel: int):
+    if t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {t.numel()}")
+
+
 def _need_cuda(t: torch.Tensor, name: str, dtype):
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor")
@@ -305,6 +322,10 @@ def paren_match_host(tags: torch.Tensor, match: torch.Tensor, parent: torch.Tens
                      device=None):
     """End-to-end host-buffer call (copies in, computes, copies out, syncs)."""
     lib = load()
+    n = tags.numel()
+    _need_host(tags, "tags", torch.uint8)
+    _need_host(match, "match", torch.int32, n)
+    _need_host(parent, "parent", torch.int32, n)
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     with torch.cuda.device(dev):
         _check(lib.paren_match_host(tags.data_ptr(), tags.numel(), match.data_ptr(),
@@ -315,6 +336,10 @@ def paren_match_host(tags: torch.Tensor, match: torch.Tensor, parent: torch.Tens
 def tree_bbox_host(tags: torch.Tensor, leaf_bbox: torch.Tensor, node_bbox: torch.Tensor,
                    device=None):
     lib = load()
+    n = tags.numel()
+    _need_host(tags, "tags", torch.uint8)
+    _need_host(leaf_bbox, "leaf_bbox", torch.float32, 4 * n)
+    _need_host(node_bbox, "node_bbox", torch.float32, 4 * n)
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     with torch.cuda.device(dev):
         _check(lib.tree_bbox_host(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(),
@@ -327,6 +352,12 @@ def paren_match_tree_bbox_host(tags: torch.Tensor, leaf_bbox: torch.Tensor, matc
     """The whole hot path from (pinned) host tensors: copies in, paren_match,
     tree_bbox_matched, copies out, synchronises."""
     lib = load()
+    n = tags.numel()
+    _need_host(tags, "tags", torch.uint8)
+    _need_host(leaf_bbox, "leaf_bbox", torch.float32, 4 * n)
+    _need_host(match, "match", torch.int32, n)
+    _need_host(parent, "parent", torch.int32, n)
+    _need_host(node_bbox, "node_bbox", torch.float32, 4 * n)
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     with torch.cuda.device(dev):
         _check(lib.paren_match_tree_bbox_host(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), match.data_ptr(),
@@ -433,6 +464,9 @@ class ShardContext:
     def paren_match(self, tags: torch.Tensor, match: torch.Tensor, parent: torch.Tensor):
         lib = load()
         _need_cuda(tags, "tags", torch.uint8)
+        for t, nm in ((match, "match"), (parent, "parent")):
+            _need_cuda(t, nm, torch.int32)
+            _need_size(t, nm, tags.numel())
         with torch.cuda.device(tags.device):
             _check(lib.paren_match_shard(tags.data_ptr(), tags.numel(), self.offset, match.data_ptr(),
                                          parent.data_ptr(), self.comm, _stream(tags.device)))
@@ -441,6 +475,9 @@ class ShardContext:
     def tree_bbox(self, tags: torch.Tensor, leaf_bbox: torch.Tensor, node_bbox: torch.Tensor):
         lib = load()
         _need_cuda(tags, "tags", torch.uint8)
+        for t, nm in ((leaf_bbox, "leaf_bbox"), (node_bbox, "node_bbox")):
+            _need_cuda(t, nm, torch.float32)
+            _need_size(t, nm, 4 * tags.numel())
         with torch.cuda.device(tags.device):
             _check(lib.tree_bbox_shard(tags.data_ptr(), leaf_bbox.data_ptr(), tags.numel(), self.offset,
                                        node_bbox.data_ptr(), self.comm, _stream(tags.device)))
@@ -483,6 +520,12 @@ class ShardContext:
         """Boxes from this rank's slice of the global matching (paren_match above)."""
         lib = load()
         _need_cuda(tags, "tags", torch.uint8)
+        for t, nm in ((leaf_bbox, "leaf_bbox"), (node_bbox, "node_bbox")):
+            _need_cuda(t, nm, torch.float32)
+            _need_size(t, nm, 4 * tags.numel())
+        for t, nm in ((match, "match"), (parent, "parent")):
+            _need_cuda(t, nm, torch.int32)
+            _need_size(t, nm, tags.numel())
         with torch.cuda.device(tags.device):
             _check(lib.tree_bbox_matched_shard(tags.data_ptr(), leaf_bbox.data_ptr(), match.data_ptr(),
                                                parent.data_ptr(), tags.numel(), self.offset, node_bbox.data_ptr(),

@@ -731,10 +731,25 @@ int tree_bbox_shard(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n_l
   if (offset < 0 || offset + n_local > kMaxN) return fail(TB_ERR_ARG, "offset + n_local out of range");
   if (!comm) return fail(TB_ERR_ARG, "null communicator");
 #ifdef TB_WITH_NCCL
-  // the fused protocol without match / parent, default capacity, checked
+  // the fused protocol without match / parent, checked; its capacity must be
+  // equal on every rank: the default for the largest chunk (an all-reduce)
+  int nranks = 0;
+  if (ncclCommCount((ncclComm_t)comm, &nranks) != ncclSuccess) return fail(TB_ERR_NCCL, "ncclCommCount");
+  if (nranks > 256) return fail(TB_ERR_ARG, "tree_bbox_shard supports at most 256 ranks");
+  void* nmx = nullptr;
+  r = get_ws(stream, 11, 256, &nmx);
+  if (r) return r;
+  int64_t nl = n_local;
+  cudaError_t e = cudaMemcpyAsync(nmx, &nl, sizeof nl, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  if (e == cudaSuccess &&
+      ncclAllReduce(nmx, nmx, 1, ncclInt64, ncclMax, (ncclComm_t)comm, (cudaStream_t)stream) != ncclSuccess)
+    return fail(TB_ERR_NCCL, "ncclAllReduce");
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&nl, nmx, sizeof nl, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_bbox_shard");
   int nerr = 0;
-  cudaError_t e = tb::fz_nccl_shard(d_tags, d_leaf_bbox, n_local, offset, (int)tb_shard_default_cap(n_local),
-                                    nullptr, nullptr, d_node_bbox, (ncclComm_t)comm, (cudaStream_t)stream, &nerr);
+  e = tb::fz_nccl_shard(d_tags, d_leaf_bbox, n_local, offset, (int)tb_shard_default_cap(nl), nullptr, nullptr,
+                        d_node_bbox, (ncclComm_t)comm, (cudaStream_t)stream, &nerr);
   if (nerr) return fail(TB_ERR_NCCL, "NCCL error");
   if (e != cudaSuccess) return cuda_fail(e, "tree_bbox_shard");
   return tb_shard_status(stream);
@@ -765,6 +780,9 @@ int paren_match_tree_bbox_shard(const uint8_t* d_tags, const float* d_leaf_bbox,
   if (cap < 1 || cap > kMaxN) return fail(TB_ERR_ARG, "cap out of range");
   if (!comm) return fail(TB_ERR_ARG, "null communicator");
 #ifdef TB_WITH_NCCL
+  int nranks = 0;
+  if (ncclCommCount((ncclComm_t)comm, &nranks) != ncclSuccess) return fail(TB_ERR_NCCL, "ncclCommCount");
+  if (nranks > 256) return fail(TB_ERR_ARG, "paren_match_tree_bbox_shard supports at most 256 ranks");
   int nerr = 0;
   cudaError_t e = tb::fz_nccl_shard(d_tags, d_leaf_bbox, n_local, offset, (int)cap, d_match, d_parent, d_node_bbox,
                                     (ncclComm_t)comm, (cudaStream_t)stream, &nerr);
@@ -813,6 +831,9 @@ int tree_bbox_matched_shard(const uint8_t* d_tags, const float* d_leaf_bbox, con
   if (offset < 0 || offset + n_local > kMaxN) return fail(TB_ERR_ARG, "offset + n_local out of range");
   if (!comm) return fail(TB_ERR_ARG, "null communicator");
 #ifdef TB_WITH_NCCL
+  int nranks = 0;
+  if (ncclCommCount((ncclComm_t)comm, &nranks) != ncclSuccess) return fail(TB_ERR_NCCL, "ncclCommCount");
+  if (nranks > 64) return fail(TB_ERR_ARG, "tree_bbox_matched_shard supports at most 64 ranks");
   int nerr = 0;
   cudaError_t e = tb::bbm_nccl_shard(d_tags, d_leaf_bbox, d_match, d_parent, n_local, offset, d_node_bbox,
                                      (ncclComm_t)comm, (cudaStream_t)stream, &nerr);
@@ -829,7 +850,7 @@ int tb_debug_tree_bbox_vshard(const uint8_t* d_tags, const float* d_leaf_bbox, i
   g_err[0] = 0;
   int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
   if (r || n == 0) return r;
-  if (nshards < 1 || nshards > n) return fail(TB_ERR_ARG, "bad shard count");
+  if (nshards < 1 || nshards > n || nshards > 64) return fail(TB_ERR_ARG, "bad shard count (1 .. min(n, 64))");
   cudaError_t e = tb::bb_vshard(d_tags, d_leaf_bbox, n, nshards, d_node_bbox, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "tree_bbox vshard");
   return TB_OK;

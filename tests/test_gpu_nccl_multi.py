@@ -61,6 +61,7 @@ def rank_main():
     run("blend-only walk", scenegen.walk_tags(1 << 19, 8, p_clip=0.0))
     run("root pops", torch.where(torch.arange(1 << 18) % 7 == 0, 3, scenegen.walk_tags(1 << 18, 9)).to(torch.uint8))
     run("deep chain", scenegen.deep_chain_tags(1 << 18, 4), cap=(1 << 18) + 2)
+    run("empty ranks", scenegen.walk_tags(16 * world - 13, 6))  # chunk borders at multiples of 16: some empty
     flag = torch.tensor([len(fails)], device=dev)
     dist.all_reduce(flag)
     dist.destroy_process_group()
