@@ -55,6 +55,8 @@ def _load():
             lib.oracle_count_unmatched.restype = ctypes.c_int
             lib.oracle_tree_transform.argtypes = [P, P, ctypes.c_int64, P]
             lib.oracle_tree_transform.restype = ctypes.c_int
+            lib.oracle_tree_fold.argtypes = [P, P, ctypes.c_int64, P]
+            lib.oracle_tree_fold.restype = ctypes.c_int
             lib.oracle_bin_leaves.argtypes = [P, P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_float,
                                               P, P, P, ctypes.c_int64]
             lib.oracle_bin_leaves.restype = ctypes.c_int64
@@ -102,6 +104,21 @@ def tree_transform(tags: np.ndarray, local: np.ndarray):
     res = np.empty((n, 6), np.float64)
     if _load().oracle_tree_transform(_ptr(tags), _ptr(loc), n, _ptr(res)) != 0:
         raise MemoryError("oracle_tree_transform: allocation failed")
+    return res
+
+
+def tree_fold(tags: np.ndarray, x: np.ndarray):
+    """2x2 matrices mod 2^32 multiplied UP the tree in stream order (R17):
+    uint32 [n, 4] in (a, b, c, d); returns uint32 [n, 4] (node value at its
+    open and close, leaves their own payload, unmatched closes the identity)."""
+    tags = np.ascontiguousarray(tags, dtype=np.uint8)
+    xx = np.ascontiguousarray(x, dtype=np.uint32).reshape(-1, 4)
+    n = tags.shape[0]
+    if xx.shape[0] != n:
+        raise ValueError("x must have n rows")
+    res = np.empty((n, 4), np.uint32)
+    if _load().oracle_tree_fold(_ptr(tags), _ptr(xx), n, _ptr(res)) != 0:
+        raise MemoryError("oracle_tree_fold: allocation failed")
     return res
 
 

@@ -253,6 +253,75 @@ int oracle_tree_transform(const uint8_t *tags, const float *local, int64_t n, do
 }
 
 /* ------------------------------------------------------------------------ */
+/* oracle_tree_fold — a generic monoid payload UP the tree                   */
+/* (the "up" half: blends are upward flow;  */
+/* the union structure run in reverse; "it can compute any monoid",  */
+/* P:32; reading R17).                                               */
+/*                                                                           */
+/* The blend stack of P:26 with its union replaced by the ordered product   */
+/* of a monoid: 2x2 matrices over the integers mod 2^32 (uint32 wrap-around  */
+/* arithmetic: exactly associative, neither commutative nor idempotent).    */
+/*   leaf          out = its own payload; the enclosing entry's product     */
+/*                 takes it on the right (stream order)                     */
+/*   open          pushes an entry with the identity                        */
+/*   close         out = the product of the node it closes, also written    */
+/*                 to its open (as blends); the enclosing entry's    */
+/*                 product takes it on the right                            */
+/*   unmatched close  out = identity, stack unchanged (R3)                  */
+/*   end           opens still on the stack are closed implicitly (R4)      */
+/* So a node's value is the product, in stream order, of the payloads of    */
+/* the leaves strictly between its open and close.                          */
+/* Matrix layout (a, b, c, d) = [[a, b], [c, d]]; payload of opens/closes   */
+/* is ignored.  x, out: n*4 uint32.  Returns 0, or -1 on allocation failure. */
+/* ------------------------------------------------------------------------ */
+typedef struct { uint32_t a, b, c, d; } m2_t;
+
+static m2_t m2_mul(m2_t X, m2_t Y)
+{
+    m2_t r;
+    r.a = X.a * Y.a + X.b * Y.c;
+    r.b = X.a * Y.b + X.b * Y.d;
+    r.c = X.c * Y.a + X.d * Y.c;
+    r.d = X.c * Y.b + X.d * Y.d;
+    return r;
+}
+
+int oracle_tree_fold(const uint8_t *tags, const uint32_t *x, int64_t n, uint32_t *out)
+{
+    const m2_t I = { 1, 0, 0, 1 };
+    m2_t *acc = (m2_t *)malloc((size_t)(n + 1) * sizeof(m2_t));
+    int64_t *open = (int64_t *)malloc((size_t)(n + 1) * sizeof(int64_t));
+    if (!acc || !open) { free(acc); free(open); return -1; }
+    m2_t *o = (m2_t *)out;
+    const m2_t *in = (const m2_t *)x;
+    int64_t sp = 0;
+    acc[sp] = I; open[sp] = -1; sp++;                 /* the root */
+    for (int64_t i = 0; i < n; i++) {
+        const uint8_t t = tags[i];
+        if (t == TAG_OPEN_CLIP || t == TAG_OPEN_BLEND) {
+            o[i] = I;                                 /* overwritten at its close */
+            acc[sp] = I; open[sp] = i; sp++;
+        } else if (t == TAG_CLOSE) {
+            if (sp == 1) { o[i] = I; continue; }      /* R3 */
+            sp--;
+            o[i] = acc[sp];
+            o[open[sp]] = acc[sp];
+            acc[sp - 1] = m2_mul(acc[sp - 1], acc[sp]);
+        } else {
+            o[i] = in[i];
+            acc[sp - 1] = m2_mul(acc[sp - 1], in[i]);
+        }
+    }
+    while (sp > 1) {                                  /* R4: implicit closes */
+        sp--;
+        o[open[sp]] = acc[sp];
+        acc[sp - 1] = m2_mul(acc[sp - 1], acc[sp]);
+    }
+    free(acc); free(open);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* oracle_bin_leaves — culling and binning of the clipped leaf boxes        */
 /* (the motivating use: "input to visibility       */
 /* culling and binning"; reading R16).                          */
