@@ -193,6 +193,25 @@ int tree_transform(const uint8_t *d_tags, const float *d_local, const int32_t *d
                    int64_t n, float *d_world, void *stream);
 
 /* ------------------------------------------------------------------------
+ * tree_fold — a generic monoid payload UP the tree (SURVEY §8(f) NEXT row 2,
+ * the "up" half: blends are upward flow; unions run in reverse, P:298;
+ * "any monoid"; reading R17).
+ *
+ * d_x     : device uint32[n][4], a 2x2 matrix (a, b, c, d) = [[a, b], [c, d]]
+ *           per element; products are taken mod 2^32 (exactly associative,
+ *           neither commutative nor idempotent).  Read for leaves only.
+ * d_match : paren_match's match for d_tags.
+ * d_out   : device uint32[n][4] out: a node's value — the product, in stream
+ *           order, of the payloads of the leaves strictly between its open and
+ *           its close — at its open and its close; an open never closed: the
+ *           leaves after it to the stream end (R4); a leaf: its own payload; an
+ *           unmatched close: the identity (R3).  Bit-exact at any size.
+ * All device pointers 16-byte aligned; out must not overlap an input.
+ * ------------------------------------------------------------------------ */
+int tree_fold(const uint8_t *d_tags, const uint32_t *d_x, const int32_t *d_match, int64_t n, uint32_t *d_out,
+              void *stream);
+
+/* ------------------------------------------------------------------------
  * bin_leaves — culling and binning of the clipped leaf boxes (SURVEY §8(f)
  * NEXT row 4; "input to visibility culling and binning"; R16)
  *

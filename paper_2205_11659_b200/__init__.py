@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["release_workspaces", "paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "bin_leaves", "compact_scene", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["release_workspaces", "paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "tree_fold", "bin_leaves", "compact_scene", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard", "pair_vshard", "shard_default_cap"]
 
@@ -57,6 +57,7 @@ def load():
                 "paren_match_tree_bbox_host": ([P, P, I64, P, P, P, P], ctypes.c_int),
                 "paren_match_bytes": ([P, I64, P, P, P, P], ctypes.c_int),
                 "tree_transform": ([P, P, P, P, I64, P, P], ctypes.c_int),
+                "tree_fold": ([P, P, P, I64, P, P], ctypes.c_int),
                 "compact_scene": ([P, P, I64, P, P, P, P, P, P], ctypes.c_int),
                 "bin_leaves": ([P, P, I64, ctypes.c_int, ctypes.c_int, ctypes.c_float, P, P, P, I64, P, P],
                                ctypes.c_int),
@@ -254,6 +255,31 @@ def tree_transform(tags: torch.Tensor, local: torch.Tensor, match: torch.Tensor,
         _check(lib.tree_transform(tags.data_ptr(), local.data_ptr(), match.data_ptr(), parent.data_ptr(), n,
                                   world.data_ptr(), _stream(tags.device)))
     return world
+
+
+def tree_fold(tags: torch.Tensor, x: torch.Tensor, match: torch.Tensor, out: torch.Tensor | None = None):
+    """2x2 matrices mod 2^32 multiplied UP the tree in stream order (R17).
+    x: CUDA [n, 4] int32 or uint32 (a, b, c, d); match: paren_match's match.
+    Returns [n, 4] of x's dtype: node values at opens and closes, leaves echo
+    their payload, unmatched closes the identity."""
+    lib = load()
+    _need_cuda(tags, "tags", torch.uint8)
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype not in (torch.int32, torch.uint32):
+        raise TypeError("x must be a CUDA int32 / uint32 tensor")
+    if not x.is_contiguous():
+        raise ValueError("x must be contiguous")
+    _need_cuda(match, "match", torch.int32)
+    n = tags.numel()
+    if x.numel() != 4 * n or match.numel() != n:
+        raise ValueError("x must be [n, 4], match [n]")
+    if out is None:
+        out = torch.empty((n, 4), dtype=x.dtype, device=tags.device)
+    if not out.is_cuda or out.dtype != x.dtype or out.numel() != 4 * n or not out.is_contiguous():
+        raise ValueError("out must be a contiguous CUDA [n, 4] tensor of x's dtype")
+    with torch.cuda.device(tags.device):
+        _check(lib.tree_fold(tags.data_ptr(), x.data_ptr(), match.data_ptr(), n, out.data_ptr(),
+                             _stream(tags.device)))
+    return out
 
 
 def bin_leaves(tags: torch.Tensor, node_bbox: torch.Tensor, grid_w: int, grid_h: int, bin_size: float):

@@ -580,6 +580,25 @@ int tree_transform(const uint8_t* d_tags, const float* d_local, const int32_t* d
   return TB_OK;
 }
 
+int tree_fold(const uint8_t* d_tags, const uint32_t* d_x, const int32_t* d_match, int64_t n, uint32_t* d_out,
+              void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r || n == 0) return r;
+  if (!d_tags || !d_x || !d_match || !d_out) return fail(TB_ERR_ARG, "null pointer with n > 0");
+  if (!aligned16(d_tags) || !aligned16(d_x) || !aligned16(d_match) || !aligned16(d_out))
+    return fail(TB_ERR_ALIGN, "tags, x, match and out must be 16-byte aligned");
+  const size_t nb = (size_t)n * 16, n4 = (size_t)n * 4;
+  if (overlap(d_out, nb, d_x, nb) || overlap(d_out, nb, d_tags, (size_t)n) || overlap(d_out, nb, d_match, n4))
+    return fail(TB_ERR_ALIAS, "out overlaps an input");
+  void* ws = nullptr;
+  r = get_ws(stream, 12, tb::tf_workspace_bytes(n), &ws);
+  if (r) return r;
+  cudaError_t e = tb::tf_launch(d_tags, d_x, d_match, n, d_out, ws, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "tree_fold launch");
+  return TB_OK;
+}
+
 int bin_leaves(const uint8_t* d_tags, const float* d_node_bbox, int64_t n, int grid_w, int grid_h, float bin_size,
                int32_t* d_counts, int32_t* d_offsets, int32_t* d_items, int64_t capacity, int64_t* h_total,
                void* stream) {

@@ -151,6 +151,11 @@ size_t tt_workspace_bytes(int64_t n);
 cudaError_t tt_launch(const uint8_t* tags, const float* local, const int32_t* match, const int32_t* parent,
                       int64_t n, float* world, void* ws, cudaStream_t stream);
 
+// 2x2 matrices mod 2^32 multiplied up the tree (tree_fold.cu)
+size_t tf_workspace_bytes(int64_t n);
+cudaError_t tf_launch(const uint8_t* tags, const uint32_t* x, const int32_t* match, int64_t n, uint32_t* out,
+                      void* ws, cudaStream_t stream);
+
 // culling + binning of clipped leaf boxes (bins.cu); synchronises to read the total
 size_t bins_workspace_bytes(int nb);
 int64_t bins_debug_cap(int64_t cap);
