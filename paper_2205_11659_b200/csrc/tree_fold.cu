@@ -74,11 +74,16 @@ struct Params {
 };
 
 struct Smem {
+  M xs[W];           // the tile's payloads (swizzled slots: conflict-free per-thread rows)
   M pre[NT];         // product of threads [0, t)
   M suf[NT];         // product of threads (t, NT)
   M dl[DL][NT];      // disjoint sparse table: level h, thread t: t's half-block product toward the middle
   int cnt;
 };
+
+// element i of thread t: slot ((i & 8) << 7) | 8 t + ((i & 7) ^ (t & 7)) -- 8
+// consecutive lanes read 8 distinct 16-byte bank groups
+__device__ __forceinline__ int slot(int t, int i) { return ((i & 8) << 7) | (t << 3) | ((i & 7) ^ (t & 7)); }
 
 // product of threads [l, r] (l <= r): two lookups in the disjoint sparse table
 __device__ __forceinline__ M thread_range(const Smem& s, int l, int r) {
@@ -89,13 +94,20 @@ __device__ __forceinline__ M thread_range(const Smem& s, int l, int r) {
 }
 
 __global__ void __launch_bounds__(NT) tf_tile(Params p) {
-  __shared__ Smem s;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31;
   const int T = blockIdx.x;
   const int64_t base = (int64_t)T * W;
   const int nvalid = (int)(p.n - base < W ? p.n - base : W);
   const int tl0 = tid * K;
   if (tid == 0) s.cnt = 0;
+  // payloads in (coalesced), tags and match of the thread's 16 elements
+#pragma unroll 4
+  for (int j = 0; j < K; j++) {
+    const int e = j * NT + tid;
+    s.xs[slot(e >> 4, e & 15)] = e < nvalid ? __ldg(p.x + base + e) : mid();
+  }
   uint32_t om = 0, cm = 0, lm = 0;
   {
     uint4 raw = make_uint4(0, 0, 0, 0);
@@ -113,54 +125,6 @@ __global__ void __launch_bounds__(NT) tf_tile(Params p) {
     cm &= valid;
     lm = valid & ~(om | cm);
   }
-  // the thread's payloads (identity off the leaves) and its ordered product
-  M xs[K];
-  M tprod = mid();
-#pragma unroll
-  for (int i = 0; i < K; i++) {
-    xs[i] = ((lm >> i) & 1u) ? __ldg(p.x + base + tl0 + i) : mid();
-    tprod = mul(tprod, xs[i]);
-  }
-  // disjoint sparse table over the threads: level 0 = the thread products;
-  // level h (blocks of 2^h, halves of 2^(h-1)): a left-half thread holds the
-  // product from it to the half's end, a right-half thread from the half's
-  // start to it (segmented ordered scans: shuffles inside a warp, one carry
-  // across the two warps of a 64-thread half)
-  s.dl[0][tid] = tprod;
-#pragma unroll
-  for (int h = 1; h < DL; h++) {
-    const int half = 1 << (h - 1);
-    const bool right = (tid >> (h - 1)) & 1;
-    const int seg = min(half, 32);
-    const int ls = lane & (seg - 1);  // position inside the warp-level segment
-    // inclusive prefix and suffix within the segment, in every lane (the
-    // shuffles need the whole warp); right-half lanes keep the prefix
-    M pv = tprod, sv = tprod;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const M a = shfl_up_m(pv, off), b = shfl_down_m(sv, off);
-      if (off < seg && ls >= off) pv = mul(a, pv);
-      if (off < seg && ls + off < seg) sv = mul(sv, b);
-    }
-    M v = right ? pv : sv;
-    // halves of 64 add the other warp of the half
-    s.dl[h][tid] = v;
-    if (half == 64) {
-      __syncthreads();
-      if (right && (tid & 32)) v = mul(s.dl[h][tid - lane - 1], v);        // · prefix of the half's first warp
-      if (!right && !(tid & 32)) v = mul(v, s.dl[h][(tid | 31) + 1]);     // · suffix of the half's second warp
-      __syncthreads();
-      s.dl[h][tid] = v;
-    }
-  }
-  // prefix / suffix over the threads (exclusive)
-  __syncthreads();
-  s.pre[tid] = thread_range(s, 0, tid - 1);
-  s.suf[tid] = thread_range(s, tid + 1, NT - 1);
-  if (tid == 0) p.tp[0][T] = thread_range(s, 0, NT - 1);
-  __syncthreads();
-
-  // elements: leaves echo, unmatched closes get the identity, nodes
   int32_t mt[K];
 #pragma unroll
   for (int q = 0; q < K / 4; q++) {
@@ -178,66 +142,129 @@ __global__ void __launch_bounds__(NT) tf_tile(Params p) {
     mt[4 * q + 3] = v.w;
   }
   const int64_t gb = base + tl0;  // global index of element 0 of the thread
-  // pass 1: leaves; unmatched closes; nodes inside the thread; the open side of
-  // nodes leaving the thread (suffix after the open: its thread part, then the
-  // threads after it up to the close's thread or the tile end)
+  __syncthreads();
+
+  // Outputs go to the slots of xs (a leaf's output is its payload, opens and
+  // closes carry no payload) and leave in one coalesced copy at the end.
+  // Forward walk of the thread: its product; nodes inside the thread (a stack
+  // of their running products); the prefix before each close of an open
+  // outside the thread (parked in the close's slot until pass 2)
+  M P = mid();
+  {
+    M stk[K / 2 + 1];
+    int d = 0;
 #pragma unroll
-  for (int i = 0; i < K; i++) {
-    const int64_t g = gb + i;
-    if ((lm >> i) & 1u) {
-      p.out[g] = xs[i];
-    } else if ((cm >> i) & 1u) {
-      if (mt[i] < 0) p.out[g] = mid();
-    } else if ((om >> i) & 1u) {
-      const int64_t c = mt[i];
-      M v = mid();
-      if (c >= 0 && c < gb + K) {  // closed in this thread: the leaves strictly between
-#pragma unroll
-        for (int j = i + 1; j < K; j++)
-          if (gb + j < c) v = mul(v, xs[j]);
-        p.out[g] = v;
-        p.out[c] = v;
-      } else {
-#pragma unroll
-        for (int j = i + 1; j < K; j++) v = mul(v, xs[j]);  // the rest of the thread
-        const int64_t tile_end = base + W;
-        if (c >= 0 && c < tile_end) {  // closed by a later thread of the tile
-          v = mul(v, thread_range(s, tid + 1, (int)((c - base) >> 4) - 1));
-        } else {  // closed in a later tile or never: the tile suffix
-          v = mul(v, s.suf[tid]);
+    for (int i = 0; i < K; i++) {
+      const int64_t g = gb + i;
+      if ((lm >> i) & 1u) {
+        const M v = s.xs[slot(tid, i)];
+        P = mul(P, v);
+        if (d > 0) stk[d - 1] = mul(stk[d - 1], v);
+      } else if ((om >> i) & 1u) {
+        if (mt[i] >= 0 && mt[i] < gb + K) stk[d++] = mid();  // closed in this thread
+      } else if ((cm >> i) & 1u) {
+        const int64_t o = mt[i];
+        if (o < 0) {
+          s.xs[slot(tid, i)] = mid();  // R3
+        } else if (o >= gb) {
+          const M u = stk[--d];
+          s.xs[slot(tid, i)] = u;
+          s.xs[slot(tid, (int)(o - gb))] = u;
+          if (d > 0) stk[d - 1] = mul(stk[d - 1], u);
+        } else {
+          s.xs[slot(tid, i)] = P;  // the thread prefix before the close (pass 2 completes it)
         }
-        p.out[g] = v;
       }
     }
   }
-  __syncthreads();  // the open sides (global writes) are visible to the block
-  // pass 2: closes of opens in an earlier thread of the tile (their open side
-  // is parked in out[o]); closes of earlier tiles' opens park the tile prefix
-  // and are listed; opens never closed or closed beyond the tile are listed
+  // disjoint sparse table over the threads: level 0 = the thread products;
+  // level h (blocks of 2^h, halves of 2^(h-1)): a left-half thread holds the
+  // product from it to the half's end, a right-half thread from the half's
+  // start to it (segmented ordered scans: shuffles inside a warp, one carry
+  // across the two warps of a 64-thread half)
+  s.dl[0][tid] = P;
+#pragma unroll
+  for (int h = 1; h < DL; h++) {
+    const int half = 1 << (h - 1);
+    const bool right = (tid >> (h - 1)) & 1;
+    const int seg = min(half, 32);
+    const int ls = lane & (seg - 1);  // position inside the warp-level segment
+    // inclusive prefix and suffix within the segment, in every lane (the
+    // shuffles need the whole warp); right-half lanes keep the prefix
+    M pv = P, sv = P;
+#pragma unroll
+    for (int off = 1; off < seg; off <<= 1) {  // seg is a constant of the unrolled level
+      const M a = shfl_up_m(pv, off), b = shfl_down_m(sv, off);
+      if (ls >= off) pv = mul(a, pv);
+      if (ls + off < seg) sv = mul(sv, b);
+    }
+    M v = right ? pv : sv;
+    // halves of 64 add the other warp of the half
+    s.dl[h][tid] = v;
+    if (half == 64) {
+      __syncthreads();
+      if (right && (tid & 32)) v = mul(s.dl[h][tid - lane - 1], v);        // · prefix of the half's first warp
+      if (!right && !(tid & 32)) v = mul(v, s.dl[h][(tid | 31) + 1]);     // · suffix of the half's second warp
+      __syncthreads();
+      s.dl[h][tid] = v;
+    }
+  }
+  __syncthreads();
+  s.pre[tid] = thread_range(s, 0, tid - 1);
+  s.suf[tid] = thread_range(s, tid + 1, NT - 1);
+  if (tid == 0) p.tp[0][T] = thread_range(s, 0, NT - 1);
+  __syncthreads();
+
+  // pass 1 (backward walk): the open side of nodes leaving the thread -- the
+  // rest of the thread after the open, then the threads up to the close's
+  // thread (or the tile end: closed in a later tile or never)
+  {
+    M S = mid();
+#pragma unroll
+    for (int i = K - 1; i >= 0; i--) {
+      if ((om >> i) & 1u) {
+        const int64_t c = mt[i];
+        if (c < 0 || c >= gb + K) {
+          const M r = c >= 0 && c < base + W ? thread_range(s, tid + 1, (int)((c - base) >> 4) - 1) : s.suf[tid];
+          s.xs[slot(tid, i)] = mul(S, r);
+        }
+      }
+      if ((lm >> i) & 1u) S = mul(s.xs[slot(tid, i)], S);
+    }
+  }
+  __syncthreads();  // the open sides are in their slots
+  // pass 2: closes of opens in an earlier thread of the tile (open side parked
+  // in out[o], this thread's prefix in out[c]); closes of earlier tiles' opens
+  // get the tile prefix and are listed, as are opens never closed
 #pragma unroll
   for (int i = 0; i < K; i++) {
     const int64_t g = gb + i;
-    const bool isc = (cm >> i) & 1u, iso = (om >> i) & 1u;
-    if (!isc && !iso) continue;
-    const int64_t o = mt[i];
-    if (isc && o >= 0 && o < gb) {
-      M v = mid();  // the leaves of this thread before the close
-#pragma unroll
-      for (int j = 0; j < i; j++) v = mul(v, xs[j]);
-      if (o >= base) {
-        const M u = mul(__ldcg(p.out + o), v);
-        p.out[g] = u;
-        p.out[o] = u;
-      } else {
-        p.out[g] = mul(s.pre[tid], v);
-        p.list[base + atomicAdd(&s.cnt, 1)] = (int32_t)g;
+    if ((cm >> i) & 1u) {
+      const int64_t o = mt[i];
+      if (o >= 0 && o < gb) {
+        const M v = s.xs[slot(tid, i)];
+        if (o >= base) {
+          const int lo = (int)(o - base);
+          M& so = s.xs[slot(lo >> 4, lo & 15)];
+          const M u = mul(so, v);
+          s.xs[slot(tid, i)] = u;
+          so = u;
+        } else {
+          s.xs[slot(tid, i)] = mul(s.pre[tid], v);
+          p.list[base + atomicAdd(&s.cnt, 1)] = (int32_t)g;
+        }
       }
-    } else if (iso && (o < 0 || o >= base + W)) {
-      if (o < 0) p.list[base + atomicAdd(&s.cnt, 1)] = (int32_t)g;
+    } else if (((om >> i) & 1u) && mt[i] < 0) {
+      p.list[base + atomicAdd(&s.cnt, 1)] = (int32_t)g;
     }
   }
   __syncthreads();
   if (tid == 0) p.nlist[T] = s.cnt;
+#pragma unroll 4
+  for (int j = 0; j < K; j++) {  // coalesced copy-out
+    const int e = j * NT + tid;
+    if (e < nvalid) p.out[base + e] = s.xs[slot(e >> 4, e & 15)];
+  }
 }
 
 __global__ void __launch_bounds__(256) tf_hier(Params p, int k, int m /* nodes at level k - 1 */) {
@@ -249,29 +276,26 @@ __global__ void __launch_bounds__(256) tf_hier(Params p, int k, int m /* nodes a
   if (lane == 0) p.tp[k][g] = v;
 }
 
-// ordered product of tiles a .. b (warp-cooperative; a > b: identity):
-// disjoint pieces, a's partial group and b's partial group at each level
+// ordered product of tiles a .. b by one thread (a > b: identity): disjoint
+// pieces, a's partial group and b's partial group at each level
 __device__ M range_tiles(const Params& p, int a, int b) {
-  const int lane = threadIdx.x & 31;
   M left = mid(), right = mid();
   for (int k = 0; k < LV && a <= b; k++) {
     if ((a >> 5) == (b >> 5)) {
-      const int i = (a & ~31) + lane;
-      const M v = warp_prod(i >= a && i <= b ? __ldcg(p.tp[k] + i) : mid());
-      left = mul(left, v);
+      for (int i = a; i <= b; i++) left = mul(left, __ldcg(p.tp[k] + i));
       a = b + 1;
       break;
     }
     if (a & 31) {
-      const int i = (a & ~31) + lane;
-      left = mul(left, warp_prod(i >= a ? __ldcg(p.tp[k] + i) : mid()));
+      for (int i = a; i <= (a | 31); i++) left = mul(left, __ldcg(p.tp[k] + i));
       a = (a >> 5) + 1;
     } else {
       a >>= 5;
     }
     if ((b & 31) != 31) {
-      const int i = (b & ~31) + lane;
-      right = mul(warp_prod(i <= b ? __ldcg(p.tp[k] + i) : mid()), right);
+      M r = mid();
+      for (int i = b & ~31; i <= b; i++) r = mul(r, __ldcg(p.tp[k] + i));
+      right = mul(r, right);
       b = (b >> 5) - 1;
     } else {
       b >>= 5;
@@ -280,33 +304,22 @@ __device__ M range_tiles(const Params& p, int a, int b) {
   return mul(left, right);
 }
 
+// one warp per tile, one listed element per lane
 __global__ void __launch_bounds__(128) tf_cross(Params p) {
   const int lane = threadIdx.x & 31;
   const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (T >= p.ntiles) return;
   const int cnt = __ldg(p.nlist + T);
   const int64_t base = (int64_t)T * W;
-  for (int j = 0; j < cnt; j++) {  // one item at a time: the warp splits its tile range
+  for (int j = lane; j < cnt; j += 32) {
     const int64_t e = __ldg(p.list + base + j);
     const int32_t o = __ldg(p.match + e);
-    const bool close = p.tags[e] == 3;
-    int a, b;
-    if (close) {
-      a = (int)(o >> LOGW) + 1;
-      b = T - 1;
+    if (p.tags[e] == 3) {  // a close of an earlier tile's open: S(o) · tiles between · P(e)
+      const M u = mul(mul(__ldcg(p.out + o), range_tiles(p, (int)(o >> LOGW) + 1, T - 1)), __ldcg(p.out + e));
+      p.out[e] = u;
+      p.out[o] = u;
     } else {  // an open never closed (R4): every later tile
-      a = T + 1;
-      b = p.ntiles - 1;
-    }
-    const M mid_tiles = range_tiles(p, a, b);
-    if (lane == 0) {
-      if (close) {
-        const M u = mul(mul(__ldcg(p.out + o), mid_tiles), __ldcg(p.out + e));
-        p.out[e] = u;
-        p.out[o] = u;
-      } else {
-        p.out[e] = mul(__ldcg(p.out + e), mid_tiles);
-      }
+      p.out[e] = mul(__ldcg(p.out + e), range_tiles(p, T + 1, p.ntiles - 1));
     }
   }
 }
@@ -348,7 +361,11 @@ cudaError_t tf_launch(const uint8_t* tags, const uint32_t* x, const int32_t* mat
   p.list = reinterpret_cast<int32_t*>((char*)ws + L.list);
   p.nlist = reinterpret_cast<int32_t*>((char*)ws + L.nlist);
   const int nt = p.ntiles;
-  TB_LAUNCH(stream, "tf_tile", (tf::tf_tile<<<(unsigned)nt, tf::NT, 0, stream>>>(p)));
+  if (once_per_device(4)) {
+    cudaError_t e0 = cudaFuncSetAttribute(tf::tf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(tf::Smem));
+    if (e0 != cudaSuccess) return e0;
+  }
+  TB_LAUNCH(stream, "tf_tile", (tf::tf_tile<<<(unsigned)nt, tf::NT, sizeof(tf::Smem), stream>>>(p)));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int m = nt;
