@@ -243,6 +243,24 @@ int bin_leaves(const uint8_t *d_tags, const float *d_node_bbox, int64_t n, int g
  *               full stream.
  * *h_n_out    : HOST out, the number kept.  The call synchronises `stream`.
  * ------------------------------------------------------------------------ */
+/* ------------------------------------------------------------------------
+ * paren_match_tree_bbox_scene — stream compaction fused into the hot path's
+ * tile loader: the FULL scene stream in,
+ * the bench step's outputs for its kept elements out, with no compaction
+ * pass over HBM.  Elements whose byte has h_keep_map[byte] == 0 are dropped:
+ * null for the matching and the boxes (no Bic, no box, no output).  Kept
+ * element k (k-th in stream order) gets:
+ *   d_tags_out[k], d_index_out[k] (its index in the full stream),
+ *   d_match[k], d_parent[k] (compacted indices, as paren_match on the
+ *   compacted stream), d_node_bbox[k] (as tree_bbox on the compacted stream);
+ * *d_n_out (device int64) = the kept count.  Capacity n for every output.
+ * d_match and d_parent may both be null (boxes only).  Stream-ordered; no
+ * host synchronisation.  Same results as compact_scene followed by
+ * paren_match_tree_bbox on its output, bit for bit.
+ * ------------------------------------------------------------------------ */
+int paren_match_tree_bbox_scene(const uint8_t *d_scene, const float *d_boxes, int64_t n, const uint8_t *h_keep_map,
+                                uint8_t *d_tags_out, int32_t *d_index_out, int32_t *d_match, int32_t *d_parent,
+                                float *d_node_bbox, int64_t *d_n_out, void *stream);
 int compact_scene(const uint8_t *d_tags, const float *d_boxes, int64_t n, const uint8_t *h_keep_map,
                   uint8_t *d_tags_out, float *d_boxes_out, int32_t *d_index_out, int64_t *h_n_out, void *stream);
 

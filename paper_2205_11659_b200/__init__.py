@@ -19,7 +19,7 @@ import torch
 
 from . import build as _build
 
-__all__ = ["release_workspaces", "paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "tree_fold", "bin_leaves", "compact_scene", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
+__all__ = ["release_workspaces", "paren_match", "paren_match_bytes", "tree_bbox", "tree_transform", "tree_fold", "bin_leaves", "compact_scene", "paren_match_tree_bbox_scene", "tree_bbox_matched", "paren_match_tree_bbox_host", "paren_match_host", "tree_bbox_host", "count_unmatched",
            "load", "TreeBBoxError", "LIB_PATH", "workspace_bytes", "ShardContext", "paren_match_vshard",
            "tree_bbox_vshard", "pair_vshard", "shard_default_cap"]
 
@@ -58,6 +58,7 @@ def load():
                 "paren_match_bytes": ([P, I64, P, P, P, P], ctypes.c_int),
                 "tree_transform": ([P, P, P, P, I64, P, P], ctypes.c_int),
                 "tree_fold": ([P, P, P, I64, P, P], ctypes.c_int),
+                "paren_match_tree_bbox_scene": ([P, P, I64, P, P, P, P, P, P, P, P], ctypes.c_int),
                 "compact_scene": ([P, P, I64, P, P, P, P, P, P], ctypes.c_int),
                 "bin_leaves": ([P, P, I64, ctypes.c_int, ctypes.c_int, ctypes.c_float, P, P, P, I64, P, P],
                                ctypes.c_int),
@@ -327,6 +328,44 @@ def compact_scene(tags: torch.Tensor, boxes: torch.Tensor | None, keep_map: byte
                                  ctypes.byref(cnt), _stream(tags.device)))
     k = cnt.value
     return t_out[:k], (b_out[:k] if b_out is not None else None), idx[:k]
+
+
+def paren_match_tree_bbox_scene(scene: torch.Tensor, boxes: torch.Tensor, keep_map: bytes | None = None,
+                                pm: bool = True, sync: bool = True):
+    """The bench step on a FULL scene stream with the compaction fused into the
+    tile loader: elements whose byte has keep_map[byte] == 0 (default: keep
+    bytes 0-3, the hierarchy tags) are dropped.  Returns (tags, index, match,
+    parent, node_bbox, n_kept) for the kept elements in stream order; match /
+    parent are compacted indices (None when pm=False).  sync=False returns the
+    capacity-n tensors and n_kept as a device int64 tensor (no host sync)."""
+    lib = load()
+    _need_cuda(scene, "scene", torch.uint8)
+    _need_cuda(boxes, "boxes", torch.float32)
+    n = scene.numel()
+    if boxes.numel() != 4 * n:
+        raise ValueError("boxes must be [n, 4]")
+    if keep_map is None:
+        keep_map = bytes([1, 1, 1, 1] + [0] * 252)
+    if len(keep_map) != 256:
+        raise ValueError("keep_map must have 256 entries")
+    dev = scene.device
+    m = max(n, 1)
+    t_out = torch.empty(m, dtype=torch.uint8, device=dev)
+    idx = torch.empty(m, dtype=torch.int32, device=dev)
+    out = torch.empty((m, 4), dtype=torch.float32, device=dev)
+    match = torch.empty(m, dtype=torch.int32, device=dev) if pm else None
+    parent = torch.empty(m, dtype=torch.int32, device=dev) if pm else None
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    km = (ctypes.c_uint8 * 256)(*bytes(keep_map))
+    with torch.cuda.device(dev):
+        _check(lib.paren_match_tree_bbox_scene(scene.data_ptr(), boxes.data_ptr(), n, km, t_out.data_ptr(),
+                                               idx.data_ptr(), match.data_ptr() if pm else None,
+                                               parent.data_ptr() if pm else None, out.data_ptr(), cnt.data_ptr(),
+                                               _stream(dev)))
+    if not sync:
+        return t_out, idx, match, parent, out, cnt
+    k = int(cnt.item())
+    return (t_out[:k], idx[:k], match[:k] if pm else None, parent[:k] if pm else None, out[:k], k)
 
 
 def release_workspaces(device=None):

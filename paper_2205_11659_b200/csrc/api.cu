@@ -638,6 +638,33 @@ int compact_scene(const uint8_t* d_tags, const float* d_boxes, int64_t n, const 
   return TB_OK;
 }
 
+int paren_match_tree_bbox_scene(const uint8_t* d_scene, const float* d_boxes, int64_t n, const uint8_t* h_keep_map,
+                                uint8_t* d_tags_out, int32_t* d_index_out, int32_t* d_match, int32_t* d_parent,
+                                float* d_node_bbox, int64_t* d_n_out, void* stream) {
+  g_err[0] = 0;
+  int r = check_n(n);
+  if (r) return r;
+  if (!h_keep_map || !d_n_out) return fail(TB_ERR_ARG, "null pointer");
+  if (n > 0 && (!d_scene || !d_boxes || !d_tags_out || !d_index_out || !d_node_bbox || !d_match != !d_parent))
+    return fail(TB_ERR_ARG, "null pointer with n > 0");
+  if (n > 0 && (!aligned16(d_scene) || !aligned16(d_boxes) || !aligned16(d_node_bbox) ||
+                (d_match && (!aligned16(d_match) || !aligned16(d_parent)))))
+    return fail(TB_ERR_ALIGN, "scene, boxes, node_bbox, match and parent must be 16-byte aligned");
+  const size_t nb = (size_t)n * 16, n4 = (size_t)n * 4;
+  if (overlap(d_node_bbox, nb, d_boxes, nb) || overlap(d_node_bbox, nb, d_scene, (size_t)n) ||
+      overlap(d_tags_out, (size_t)n, d_scene, (size_t)n) || overlap(d_index_out, n4, d_boxes, nb) ||
+      (d_match && (overlap(d_match, n4, d_boxes, nb) || overlap(d_parent, n4, d_boxes, nb) ||
+                   overlap(d_match, n4, d_parent, n4))))
+    return fail(TB_ERR_ALIAS, "an output overlaps an input or another output");
+  void* ws = nullptr;
+  r = get_ws(stream, 13, n > 0 ? tb::fused_workspace_bytes(n) : 256, &ws);
+  if (r) return r;
+  cudaError_t e = tb::fused_scene_launch(d_scene, d_boxes, n, h_keep_map, d_tags_out, d_index_out, d_match, d_parent,
+                                         d_node_bbox, d_n_out, ws, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "paren_match_tree_bbox_scene launch");
+  return TB_OK;
+}
+
 /* Debug (not in the public header): tree_bbox with per-tile phase timestamps
  * (globaltimer ns) of the finish pass in d_trace[tile * 16 + slot]. */
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }

@@ -95,6 +95,16 @@ struct Params {
   int32_t* tcend;      // [ntiles] end of TC's pointer chain: -1 root, -2 - h imported height h
   int32_t* exc;        // [h0] shard: the close popping imported height h (-1: none)
   float4* exu;         // [h0] shard: its union over this chunk (the prefix before the close)
+  // scene mode (fused stream compaction): elements whose
+  // byte is not in the keep table are dropped -- null for the walk (no Bic,
+  // no box), no output; every output lands at the element's index in the
+  // compacted stream, and match / parent values are compacted indices
+  int scene;
+  const uint32_t* keepw;  // [8] 256-bit keep table
+  int32_t* kcnt;       // [ntiles] kept elements per tile (fz_reduce)
+  int64_t* koff;       // [ntiles + 1] their exclusive prefix (fz_ctrl); koff[ntiles] = the total
+  uint8_t* tags_out;   // [n] compacted tags
+  int32_t* index_out;  // [n] index in the full stream of each compacted element
 };
 constexpr int SHD = 64;
 // TMA descriptors of fz_main: per array (leaf boxes in, node boxes out) one 2D
@@ -111,7 +121,8 @@ constexpr int RMAX = 8;        // runs of the incoming stack kept per tile (more
 // workspace
 // ----------------------------------------------------------------------------
 struct Layout {
-  size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, shd, tce, bytes;
+  size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, shd, tce, kct, kof,
+      kpw, bytes;
   int64_t ntiles;
   explicit Layout(int64_t n, int h0 = 0) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -142,6 +153,9 @@ struct Layout {
     blk = o; o = al(o + 16 * MAXCTRL);
     blkmin = o; o = al(o + 4 * MAXCTRL);
     tce = o; o = al(o + 4 * (size_t)ntiles);
+    kct = o; o = al(o + 4 * (size_t)ntiles);
+    kof = o; o = al(o + 8 * ((size_t)ntiles + 1));
+    kpw = o; o = al(o + 32);
     bytes = o;
   }
 };
@@ -185,6 +199,12 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.tcend = (int32_t*)(b + L.tce);
   p.exc = nullptr;
   p.exu = nullptr;
+  p.scene = 0;
+  p.keepw = (const uint32_t*)(b + L.kpw);
+  p.kcnt = (int32_t*)(b + L.kct);
+  p.koff = (int64_t*)(b + L.kof);
+  p.tags_out = nullptr;
+  p.index_out = nullptr;
   return p;
 }
 
@@ -207,6 +227,18 @@ __device__ __forceinline__ int select_bit32(uint32_t m, int j) {
   return pos + (j >= (int)(m & 1u) ? 1 : 0);
 }
 
+// scene mode: bit i = byte i of the 16 is kept (256-bit table, L1-cached)
+__device__ __forceinline__ uint32_t keep16(const uint32_t* keepw, uint4 raw) {
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 16; i++) {
+    const uint32_t b = (w[i >> 2] >> (8 * (i & 3))) & 255u;
+    m |= ((__ldg(keepw + (b >> 5)) >> (b & 31)) & 1u) << i;
+  }
+  return m;
+}
+
 constexpr int RL = W / 32;  // 64 elements per lane
 __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   __shared__ uint8_t bic4[256];  // Bic of 4 elements: index = open nibble | close nibble << 4; value a | b << 4
@@ -225,7 +257,7 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   const int T = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (T >= p.ntiles) return;
   const int64_t base = (int64_t)T * W, lbase = base + (int64_t)lane * RL;
-  uint32_t om[2], cm[2], bk[2];
+  uint32_t om[2], cm[2], bk[2], km[2] = {0u, 0u};
   {
     uint4 raw[4];
 #pragma unroll
@@ -237,6 +269,16 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
     for (int q = 0; q < 4; q++) {
       uint32_t o, c, b;
       classify16b(raw[q], o, c, b);
+      if (p.scene) {  // dropped elements: neither opens nor closes (and no leaves)
+        const int64_t g = lbase + 16 * q;
+        const int64_t rem = p.n - g;
+        const int nv = rem <= 0 ? 0 : (rem >= 16 ? 16 : (int)rem);
+        const uint32_t k = keep16(p.keepw, raw[q]) & (nv >= 16 ? 0xffffu : ((1u << nv) - 1u));
+        o &= k;
+        c &= k;
+        b &= k;
+        km[q >> 1] |= k << (16 * (q & 1));
+      }
       if (q & 1) {
         om[q >> 1] |= o << 16;
         cm[q >> 1] |= c << 16;
@@ -271,6 +313,20 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   if (lane == 0) ex = Bic{0, 0};
   if (lane == 31) sx = Bic{0, 0};
   if (lane == 0) p.ctrl.agg[T] = make_int2(tot.a, tot.b);
+  // scene mode: the lane's kept elements before it (a slice entry's index in
+  // the compacted stream is the tile's offset, added by fz_ctrl, + this)
+  int kex = 0;
+  if (p.scene) {
+    const int kc = __popc(km[0]) + __popc(km[1]);
+    int ki = kc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, ki, off);
+      if (lane >= off) ki += y;
+    }
+    kex = ki - kc;
+    if (lane == 31) p.kcnt[T] = ki;
+  }
   // the lane's unmatched opens that survive to the tile end: its bottom s_l,
   // at tile-relative heights l + k, slice positions [l + a_T, l + a_T + s_l)
   const int l = ex.b - ex.a - lb.a;
@@ -312,6 +368,8 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
     const int ostart = __shfl_sync(0xffffffffu, start, L);
     const uint32_t o0 = __shfl_sync(0xffffffffu, sv0, L), o1 = __shfl_sync(0xffffffffu, sv1, L);
     const uint32_t b0 = __shfl_sync(0xffffffffu, bk[0], L), b1 = __shfl_sync(0xffffffffu, bk[1], L);
+    const uint32_t k0 = __shfl_sync(0xffffffffu, km[0], L), k1 = __shfl_sync(0xffffffffu, km[1], L);
+    const int kx = __shfl_sync(0xffffffffu, kex, L);
     const bool act = pos < tot.b;
     float4 v = bINF();
     uint32_t e = 0u, blend = 0u;
@@ -322,6 +380,8 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
       e = (uint32_t)(base + L * RL + j);
       if (!blend) v = __ldg(p.boxes + e);
       e += (uint32_t)p.goff;
+      if (p.scene)  // tile-local compacted index
+        e = (uint32_t)(kx + (j < 32 ? __popc(k0 & ((1u << j) - 1u)) : __popc(k0) + __popc(k1 & ((1u << (j - 32)) - 1u))));
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -467,11 +527,13 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   FZ_TRACE(0);
 
   // P0: Bic value and a-sum of the block's tiles
-  Agg v{0, 0, 0};
-  for (int T = ta; T < tb; T++) {
+  // s = Σa (pop offsets) + 2^32 Σkept (scene mode): both sums < 2^31
+  auto tile_agg = [&](int T) {
     const int2 g = __ldcg(p.ctrl.agg + T);
-    v = agg_combine(v, Agg{g.x, g.y, g.x});
-  }
+    return Agg{g.x, g.y, g.x + (p.scene ? (long long)__ldcg(p.kcnt + T) << 32 : 0ll)};
+  };
+  Agg v{0, 0, 0};
+  for (int T = ta; T < tb; T++) v = agg_combine(v, tile_agg(T));
   Agg ex, tot;
   block_excl(v, ex, tot, sh);
   if (tid == 0) {
@@ -503,19 +565,21 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
     Agg cur = agg_combine(pre, ex);
     for (int T = ta; T < tb; T++) {
       const int2 g = __ldcg(p.ctrl.agg + T);
+      if (p.scene) p.koff[T] = cur.s >> 32;
       // one device: the height is the prefix's b (its a closes popped the root);
       // shard mode: h0 imported entries below, the prefix's a of them popped
       const int H = p.h0 ? p.h0 - cur.a + cur.b : cur.b;
       const int L = max(H - g.x, 0);
       p.ctrl.hstart[T] = H;
       p.ctrl.lw[T] = (uint32_t)L + 1u;
-      p.aoff[T] = cur.s;
+      p.aoff[T] = cur.s & 0xffffffffll;
       lmin = min(lmin, L);
-      cur = agg_combine(cur, Agg{g.x, g.y, g.x});
+      cur = agg_combine(cur, tile_agg(T));
     }
     if (tb == nt && ta < tb) {
       *p.ctrl.total = make_int2(cur.a, cur.b);
-      p.aoff[nt] = cur.s;
+      p.aoff[nt] = cur.s & 0xffffffffll;
+      if (p.scene) p.koff[nt] = cur.s >> 32;
     }
   }
   lmin = block_min(lmin, shm);
@@ -697,6 +761,11 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   for (int V = gt; V < nt; V += nthr) {
     p.tc[V] = __ldcg(accb[cb] + V);
     p.tcend[V] = __ldcg(ptrb[cb] + V);  // -1, or -2 - h: TC still lacks imported height h's context
+    if (p.scene) {  // slice entries: tile-local compacted index -> compacted index
+      const int bT = __ldcg(p.ctrl.agg + V).y;
+      const int ko = (int)__ldcg(p.koff + V);
+      for (int k = 0; k < bT; k++) p.slice_idx[(int64_t)V * W + k] += ko;
+    }
   }
   FZ_TRACE(7);
 }
@@ -807,6 +876,8 @@ struct Smem {
   float4 wtu[NW];                   // warp unions
   float4 wmid[NW][NW];              // union of the warps strictly between
   Bic wtot[NW];
+  uint32_t kS[NT];                  // scene mode: kept elements of threads before t << 16 | t's kept mask
+  int kw[NW];
 };
 static_assert(sizeof(Smem) <= 56 * 1024, "four CTAs per SM");
 // rbuf addressed as val[RB0 + k * NT + t] (both arrays of float4 in one shared block)
@@ -904,7 +975,7 @@ __device__ __forceinline__ int inc_ref(const Params& p, const Smem& s, int nruns
 #ifndef FZ_MINB
 #define FZ_MINB 4
 #endif
-template <bool PM>
+template <bool PM, bool SC>
 __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_constant__ Maps maps) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
@@ -950,7 +1021,8 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   }
   const int nruns = __ldg(p.nruns + T);
   const int nv_t = nvalid - tl0;
-  const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
+  const uint32_t valid = (nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u))) &
+                         (SC ? keep16(p.keepw, raw) : 0xffffu);  // scene: dropped elements are null
   const Walk w = walk(raw, valid);
   const int a_t = __popc(w.ucm), b_t = __popc(w.S);
 
@@ -958,6 +1030,29 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   if (tid < RMAX) cp_async_wait_all();
   Bic ex, sx, tot;
   block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, false);
+  int koffT = 0, kpt = 0;  // scene mode: compacted index of the tile's / the thread's first kept element
+  if (SC) {
+    koffT = (int)__ldg(p.koff + T);
+    const int kc = __popc(valid);
+    int ki = kc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, ki, off);
+      if (lane >= off) ki += y;
+    }
+    if (lane == 31) s.kw[warp] = ki;
+    __syncthreads();
+    kpt = ki - kc;
+    for (int w2 = 0; w2 < warp; w2++) kpt += s.kw[w2];
+    s.kS[tid] = ((uint32_t)kpt << 16) | valid;
+  }
+  // scene mode: tile-local element -> its compacted index; a value (global
+  // index in the tile, or an earlier tile's compacted index, or -1) -> compacted
+  auto kpos = [&](int e) {
+    const uint32_t kw = s.kS[e >> 4];
+    return koffT + (int)(kw >> 16) + __popc(kw & ((1u << (e & 15)) - 1u) & 0xffffu);
+  };
+  auto conv = [&](int v) { return v < 0 ? -1 : (v >= gbase ? kpos(v - gbase) : v); };
   const int r_t = ex.b - ex.a;
   const int l_t = r_t - a_t;
   for (uint32_t q = w.S; q; q &= q - 1) s.matchS[mb + __ffs(q) - 1] = -1;  // closed by another thread / tile
@@ -1129,7 +1224,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         if (si != -1) {
           gi = si & 0x7fffffff;
           xcm |= 1u << ci;
-          p.pop[poff + D] = make_int2(gtb + ci, rf);
+          p.pop[poff + D] = make_int2(SC ? koffT + kpt + __popc(valid & ((1u << ci) - 1u)) : gtb + ci, rf);
         } else {
           p.pop[poff + D] = make_int2(-1, -1);  // an imported slot below the global root (R3)
         }
@@ -1207,7 +1302,13 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         if (PM && !(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + pt;
         pv[jq] = par;
       }
-      if (PM) {
+      if (PM && SC) {
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          const int i = 4 * q + jj;
+          if ((valid >> i) & 1u) p.parent[koffT + kpt + __popc(valid & ((1u << i) - 1u))] = conv(pv[jj]);
+        }
+      } else if (PM) {
         if (nv_t >= 4 * q + 4) {
           __stcs(reinterpret_cast<int4*>(p.parent + base + tl0) + q, make_int4(pv[0], pv[1], pv[2], pv[3]));
         } else {
@@ -1345,7 +1446,18 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   __syncthreads();
 
   // ---- I. copy-out: node boxes by TMA (full tiles), match coalesced ---------
-  if (tma) {
+  if (SC) {  // kept elements to their compacted indices
+#pragma unroll 1
+    for (int j = 0; j < K; j++) {
+      const int e = j * NT + tid;
+      if (e >= nvalid || !((s.kS[e >> 4] >> (e & 15)) & 1u)) continue;
+      const int pos = kpos(e);
+      __stcs(p.out + pos, s.val[slot_of(e)]);
+      if (PM) p.match[pos] = conv(s.matchS[mpad(e)]);
+      p.tags_out[pos] = p.tags[base + e];
+      p.index_out[pos] = gbase + e;
+    }
+  } else if (tma) {
     if (tid == 0) {
       tma_store_2d(&maps.out[0], 0, T * NT, val_sa);
       tma_store_2d(&maps.out[1], 0, T * NT, val_sa + NT * 128);
@@ -1358,7 +1470,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
       if (e < nvalid) __stcs(p.out + base + e, s.val[slot_of(e)]);
     }
   }
-  if (PM) {
+  if (PM && !SC) {
 #pragma unroll
     for (int j = 0; j < W / 4 / NT; j++) {
       const int e = 4 * (j * NT + tid);
@@ -1554,13 +1666,12 @@ static int ctrl_blocks() {  // co-resident CTAs of the cooperative kernel
 
 static cudaError_t setup() {
   if (once_per_device(3)) {
-    cudaError_t e = cudaFuncSetAttribute(fz_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fz_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fz_main<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fz_main<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaError_t e = cudaSuccess;
+    for (const void* f : {(const void*)fz_main<true, false>, (const void*)fz_main<false, false>,
+                          (const void*)fz_main<true, true>, (const void*)fz_main<false, true>}) {
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
     uint8_t tab[UNM4_ENTRIES];
     for (int i = 0; i < UNM4_ENTRIES; i++) tab[i] = unm4_entry(i);
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_unm4, tab, sizeof tab);
@@ -1626,10 +1737,19 @@ static cudaError_t launch_back(fz::Params& p, const float* leaf_bbox, float* nod
   memset(&maps, 0, sizeof maps);
   p.use_tma = g_fz_tma && fz::make_maps(leaf_bbox, node_bbox, p.n, maps) ? 1 : 0;
   p.abl = g_fz_abl;
-  if (pm)
-    TB_LAUNCH(stream, "fz_main", (fz::fz_main<true><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p, maps)));
-  else
-    TB_LAUNCH(stream, "fz_main", (fz::fz_main<false><<<(unsigned)nt, fz::NT, sizeof(fz::Smem), stream>>>(p, maps)));
+  const unsigned g = (unsigned)nt;
+  const size_t sm = sizeof(fz::Smem);
+  if (p.scene) {
+    if (pm)
+      TB_LAUNCH(stream, "fz_main", (fz::fz_main<true, true><<<g, fz::NT, sm, stream>>>(p, maps)));
+    else
+      TB_LAUNCH(stream, "fz_main", (fz::fz_main<false, true><<<g, fz::NT, sm, stream>>>(p, maps)));
+  } else {
+    if (pm)
+      TB_LAUNCH(stream, "fz_main", (fz::fz_main<true, false><<<g, fz::NT, sm, stream>>>(p, maps)));
+    else
+      TB_LAUNCH(stream, "fz_main", (fz::fz_main<false, false><<<g, fz::NT, sm, stream>>>(p, maps)));
+  }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = dbg_sync(stream, "fz_main");
   if (e != cudaSuccess) return e;
@@ -1660,6 +1780,29 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
   e = launch_front(p, stream);
   if (e != cudaSuccess) return e;
   return launch_back(p, leaf_bbox, node_bbox, match != nullptr, stream);
+}
+
+// scene mode (fused stream compaction): the full stream in, the kept
+// elements' outputs at their compacted indices; *d_n_out = the kept count
+cudaError_t fused_scene_launch(const uint8_t* tags, const float* boxes, int64_t n, const uint8_t* h_keep_map,
+                               uint8_t* tags_out, int32_t* index_out, int32_t* match, int32_t* parent,
+                               float* node_bbox, int64_t* d_n_out, void* ws, cudaStream_t stream) {
+  if (n <= 0) return cudaMemsetAsync(d_n_out, 0, sizeof(int64_t), stream);
+  cudaError_t e = fz::setup();
+  if (e != cudaSuccess) return e;
+  fz::Params p = fz::make_params(tags, boxes, n, match, parent, node_bbox, ws);
+  p.scene = 1;
+  p.tags_out = tags_out;
+  p.index_out = index_out;
+  uint32_t kw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int b = 0; b < 256; b++)
+    if (h_keep_map[b]) kw[b >> 5] |= 1u << (b & 31);
+  e = cudaMemcpyAsync((void*)p.keepw, kw, sizeof kw, cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = launch_front(p, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_n_out, p.koff + p.ntiles, sizeof(int64_t), cudaMemcpyDeviceToDevice, stream);
+  if (e != cudaSuccess) return e;
+  return launch_back(p, boxes, node_bbox, match != nullptr, stream);
 }
 
 #include "fused_shard.cuh"
