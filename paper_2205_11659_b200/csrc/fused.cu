@@ -95,16 +95,22 @@ struct Params {
   int32_t* tcend;      // [ntiles] end of TC's pointer chain: -1 root, -2 - h imported height h
   int32_t* exc;        // [h0] shard: the close popping imported height h (-1: none)
   float4* exu;         // [h0] shard: its union over this chunk (the prefix before the close)
-  // scene mode (fused stream compaction): elements whose
-  // byte is not in the keep table are dropped -- null for the walk (no Bic,
-  // no box), no output; every output lands at the element's index in the
-  // compacted stream, and match / parent values are compacted indices
+  // scene mode (stream compaction fused into the loaders):
+  // the passes run on the COMPACTED stream -- tile T holds kept elements
+  // [T W, T W + W) -- whose tags and full-stream indices fz_reduce writes while
+  // it compacts; fz_main gathers the boxes through those indices.  n / ntiles
+  // are the full stream's (capacity); the kept count is on the device.
   int scene;
-  const uint32_t* keepw;  // [8] 256-bit keep table
-  int32_t* kcnt;       // [ntiles] kept elements per tile (fz_reduce)
-  int64_t* koff;       // [ntiles + 1] their exclusive prefix (fz_ctrl); koff[ntiles] = the total
-  uint8_t* tags_out;   // [n] compacted tags
-  int32_t* index_out;  // [n] index in the full stream of each compacted element
+  int keep03;              // the keep table is bytes 0-3 exactly (a compare)
+  const uint32_t* keepw;   // [8] 256-bit keep table
+  int64_t* nkp;            // the kept count
+  const uint8_t* tags_in;  // the full stream
+  const float4* boxes_in;  // its boxes
+  int64_t* tin;            // [ntiles + 1] full-stream index of kept element T W (n past the last)
+  int32_t* kcin;           // [ntiles] kept elements per full-stream tile
+  int64_t* kpin;           // [ntiles + 1] their exclusive prefix
+  uint8_t* tags_out;       // [n] the compacted tags
+  int32_t* index_out;      // [n] full-stream index of each kept element
 };
 constexpr int SHD = 64;
 // TMA descriptors of fz_main: per array (leaf boxes in, node boxes out) one 2D
@@ -121,8 +127,8 @@ constexpr int RMAX = 8;        // runs of the incoming stack kept per tile (more
 // workspace
 // ----------------------------------------------------------------------------
 struct Layout {
-  size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, shd, tce, kct, kof,
-      kpw, bytes;
+  size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, shd, tce, kpw, nk,
+      tin, kci, kpi, bytes;
   int64_t ntiles;
   explicit Layout(int64_t n, int h0 = 0) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -153,9 +159,11 @@ struct Layout {
     blk = o; o = al(o + 16 * MAXCTRL);
     blkmin = o; o = al(o + 4 * MAXCTRL);
     tce = o; o = al(o + 4 * (size_t)ntiles);
-    kct = o; o = al(o + 4 * (size_t)ntiles);
-    kof = o; o = al(o + 8 * ((size_t)ntiles + 1));
     kpw = o; o = al(o + 32);
+    nk = o; o = al(o + 8);
+    tin = o; o = al(o + 8 * ((size_t)ntiles + 1));
+    kci = o; o = al(o + 4 * (size_t)ntiles);
+    kpi = o; o = al(o + 8 * ((size_t)ntiles + 1));
     bytes = o;
   }
 };
@@ -200,9 +208,14 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.exc = nullptr;
   p.exu = nullptr;
   p.scene = 0;
+  p.keep03 = 0;
   p.keepw = (const uint32_t*)(b + L.kpw);
-  p.kcnt = (int32_t*)(b + L.kct);
-  p.koff = (int64_t*)(b + L.kof);
+  p.nkp = (int64_t*)(b + L.nk);
+  p.tags_in = nullptr;
+  p.boxes_in = nullptr;
+  p.tin = (int64_t*)(b + L.tin);
+  p.kcin = (int32_t*)(b + L.kci);
+  p.kpin = (int64_t*)(b + L.kpi);
   p.tags_out = nullptr;
   p.index_out = nullptr;
   return p;
@@ -227,7 +240,8 @@ __device__ __forceinline__ int select_bit32(uint32_t m, int j) {
   return pos + (j >= (int)(m & 1u) ? 1 : 0);
 }
 
-// scene mode: bit i = byte i of the 16 is kept (256-bit table, L1-cached)
+// ---- scene mode prologue: where each compacted tile starts in the full stream
+// bit i = byte i of the 16 is kept (256-bit table, L1-cached)
 __device__ __forceinline__ uint32_t keep16(const uint32_t* keepw, uint4 raw) {
   const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
   uint32_t m = 0;
@@ -238,8 +252,128 @@ __device__ __forceinline__ uint32_t keep16(const uint32_t* keepw, uint4 raw) {
   }
   return m;
 }
+// keep mask of the 64 full-stream elements [g, g + 64) (bits past n clear)
+__device__ __forceinline__ uint64_t keep64(const Params& p, int64_t g) {
+  uint64_t m = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int64_t h = g + 16 * q;
+    if (h >= p.n) break;
+    const uint4 raw = h + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags_in + h))
+                                     : load_tags16(p.tags_in, p.n, h, false);
+    const int64_t rem = p.n - h;
+    const uint32_t v = rem >= 16 ? 0xffffu : ((1u << rem) - 1u);
+    m |= (uint64_t)(keep16(p.keepw, raw) & v) << (16 * q);
+  }
+  return m;
+}
+// kept elements of each full-stream tile (one warp per tile)
+__global__ void __launch_bounds__(256) sc_count(Params p) {
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (u >= p.ntiles) return;
+  int c = __popcll(keep64(p, (int64_t)u * W + 64 * lane));
+  c = __reduce_add_sync(0xffffffffu, c);
+  if (lane == 0) p.kcin[u] = c;
+}
+// their exclusive prefix and the kept count: 1024 tiles per block (a block
+// scan), the block totals scanned by one block, then added back
+__device__ __forceinline__ long long block_scan_excl(long long v, long long& tot, long long* ws) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    long long t = ws[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, t, off);
+      if (lane >= off) t += y;
+    }
+    ws[lane] = t;
+  }
+  __syncthreads();
+  tot = ws[31];
+  const long long r = (warp ? ws[warp - 1] : 0) + x - v;
+  __syncthreads();
+  return r;
+}
+__global__ void __launch_bounds__(1024) sc_scan1(Params p, long long* bsum) {
+  __shared__ long long ws[32];
+  const int u = blockIdx.x * 1024 + threadIdx.x;
+  long long tot;
+  const long long ex = block_scan_excl(u < p.ntiles ? __ldcg(p.kcin + u) : 0, tot, ws);
+  if (u < p.ntiles) p.kpin[u] = ex;
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(1024) sc_scan2(Params p, long long* bsum, int nb) {
+  __shared__ long long ws[32];
+  long long tot;
+  const int i = threadIdx.x;  // nb <= 1024 (ntiles <= 2^20)
+  const long long ex = block_scan_excl(i < nb ? bsum[i] : 0, tot, ws);
+  if (i < nb) bsum[i] = ex;
+  if (i == 0) {
+    p.kpin[p.ntiles] = tot;
+    *p.nkp = tot;
+  }
+}
+__global__ void __launch_bounds__(1024) sc_scan3(Params p, const long long* bsum) {
+  const int u = blockIdx.x * 1024 + threadIdx.x;
+  if (u < p.ntiles) p.kpin[u] += bsum[blockIdx.x];
+}
+// tin[j] = full-stream index of kept element j W (n when j W >= the kept
+// count): the full-stream tile holding it (binary search of the prefix), then
+// its rank inside that tile (one warp per compacted tile)
+__global__ void __launch_bounds__(256) sc_ranges(Params p) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (j > p.ntiles) return;
+  const int64_t q = (int64_t)j * W, nk = __ldcg(p.nkp);
+  if (q >= nk) {
+    if (lane == 0) p.tin[j] = p.n;
+    return;
+  }
+  int lo = 0, hi = p.ntiles - 1;  // the last tile u with kpin[u] <= q
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldcg(p.kpin + mid) <= q) lo = mid;
+    else hi = mid - 1;
+  }
+  const int r = (int)(q - __ldcg(p.kpin + lo));
+  const uint64_t m = keep64(p, (int64_t)lo * W + 64 * lane);
+  const int c = __popcll(m);
+  int incl = c;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  const int ex = incl - c;
+  if (r >= ex && r < incl) {
+    const uint32_t lo32 = (uint32_t)m, hi32 = (uint32_t)(m >> 32);
+    const int k = r - ex, c0 = __popc(lo32);
+    int pos;
+    {
+      // select the k-th set bit of the lane's 64
+      uint32_t mm = k < c0 ? lo32 : hi32;
+      int kk = k < c0 ? k : k - c0, b = k < c0 ? 0 : 32;
+      for (int t = 0; t < kk; t++) mm &= mm - 1;
+      pos = b + __ffs(mm) - 1;
+    }
+    p.tin[j] = (int64_t)lo * W + 64 * lane + pos;
+  }
+}
 
 constexpr int RL = W / 32;  // 64 elements per lane
+// scene mode: per warp, the compacted tile's tags and full-stream indices
+constexpr size_t SC_WARP_BYTES = W;
+
+template <bool SC>
 __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   __shared__ uint8_t bic4[256];  // Bic of 4 elements: index = open nibble | close nibble << 4; value a | b << 4
   __shared__ __align__(16) uint8_t unm4[UNM4_ENTRIES];
@@ -257,28 +391,78 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   const int T = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (T >= p.ntiles) return;
   const int64_t base = (int64_t)T * W, lbase = base + (int64_t)lane * RL;
-  uint32_t om[2], cm[2], bk[2], km[2] = {0u, 0u};
+  uint8_t* ctag = nullptr;  // scene mode: the compacted tile (zero padded: leaves)
+  if (SC) {
+    extern __shared__ __align__(16) unsigned char sc_smem[];
+    ctag = sc_smem + (threadIdx.x >> 5) * SC_WARP_BYTES;
+    const int64_t nk = __ldcg(p.nkp);
+    const int len = (int)(nk - base < 0 ? 0 : (nk - base < W ? nk - base : W));
+    if (len == 0) {  // past the compacted stream: an empty tile
+      if (lane == 0) p.ctrl.agg[T] = make_int2(0, 0);
+      return;
+    }
+    // compact the full-stream range [tin[T], tin[T + 1]) -- exactly len kept
+    // elements -- 32 consecutive elements per step (one per lane, ballot
+    // ranks: consecutive shared-memory slots, no bank conflicts)
+    // (16 bytes per lane per load; sub-step b hands lane l the byte of element
+    // c0 + 32 b + l through shuffles)
+    const int64_t a = __ldcg(p.tin + T);
+    int co = 0;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t kt[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) kt[i] = __ldg(p.keepw + i);
+    for (int64_t c0 = a & ~int64_t(15); co < len; c0 += 512) {
+      const int64_t g16 = c0 + 16 * lane;
+      const uint4 raw = g16 + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags_in + g16))
+                                        : load_tags16(p.tags_in, p.n, g16, false);
+      const int bi = lane & 15;
+#pragma unroll
+      for (int b = 0; b < 16; b++) {
+        const int src = 2 * b + (lane >> 4);
+        const uint32_t w0 = __shfl_sync(0xffffffffu, raw.x, src), w1 = __shfl_sync(0xffffffffu, raw.y, src);
+        const uint32_t w2 = __shfl_sync(0xffffffffu, raw.z, src), w3 = __shfl_sync(0xffffffffu, raw.w, src);
+        const uint32_t wv = (bi & 8) ? ((bi & 4) ? w3 : w2) : ((bi & 4) ? w1 : w0);
+        const uint32_t byte = (wv >> (8 * (bi & 3))) & 255u;
+        const int64_t g = c0 + 32 * b + lane;
+        bool kept;
+        if (p.keep03) {
+          kept = byte < 4u;
+        } else {
+          uint32_t kw = kt[0];
+#pragma unroll
+          for (int i = 1; i < 8; i++) kw = (byte >> 5) == (uint32_t)i ? kt[i] : kw;
+          kept = (kw >> (byte & 31)) & 1u;
+        }
+        kept = kept && g >= a && g < p.n;
+        const uint32_t bal = __ballot_sync(0xffffffffu, kept);
+        const int k = co + __popc(bal & lt);
+        if (kept && k < len) {
+          ctag[k] = (uint8_t)byte;
+          p.tags_out[base + k] = (uint8_t)byte;
+          p.index_out[base + k] = (int32_t)g;
+        }
+        co += __popc(bal);
+      }
+    }
+    for (int e = len + lane; e < W; e += 32) ctag[e] = 0;
+    __syncwarp();  // ctag and this warp's index_out writes are visible to the warp
+  }
+  uint32_t om[2], cm[2], bk[2];
   {
     uint4 raw[4];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       const int64_t g = lbase + 16 * q;
-      raw[q] = g + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags + g)) : load_tags16(p.tags, p.n, g, false);
+      if (SC)
+        raw[q] = *reinterpret_cast<const uint4*>(ctag + lane * RL + 16 * q);
+      else
+        raw[q] = g + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags + g)) : load_tags16(p.tags, p.n, g, false);
     }
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       uint32_t o, c, b;
       classify16b(raw[q], o, c, b);
-      if (p.scene) {  // dropped elements: neither opens nor closes (and no leaves)
-        const int64_t g = lbase + 16 * q;
-        const int64_t rem = p.n - g;
-        const int nv = rem <= 0 ? 0 : (rem >= 16 ? 16 : (int)rem);
-        const uint32_t k = keep16(p.keepw, raw[q]) & (nv >= 16 ? 0xffffu : ((1u << nv) - 1u));
-        o &= k;
-        c &= k;
-        b &= k;
-        km[q >> 1] |= k << (16 * (q & 1));
-      }
       if (q & 1) {
         om[q >> 1] |= o << 16;
         cm[q >> 1] |= c << 16;
@@ -313,20 +497,6 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   if (lane == 0) ex = Bic{0, 0};
   if (lane == 31) sx = Bic{0, 0};
   if (lane == 0) p.ctrl.agg[T] = make_int2(tot.a, tot.b);
-  // scene mode: the lane's kept elements before it (a slice entry's index in
-  // the compacted stream is the tile's offset, added by fz_ctrl, + this)
-  int kex = 0;
-  if (p.scene) {
-    const int kc = __popc(km[0]) + __popc(km[1]);
-    int ki = kc;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, ki, off);
-      if (lane >= off) ki += y;
-    }
-    kex = ki - kc;
-    if (lane == 31) p.kcnt[T] = ki;
-  }
   // the lane's unmatched opens that survive to the tile end: its bottom s_l,
   // at tile-relative heights l + k, slice positions [l + a_T, l + a_T + s_l)
   const int l = ex.b - ex.a - lb.a;
@@ -368,8 +538,6 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
     const int ostart = __shfl_sync(0xffffffffu, start, L);
     const uint32_t o0 = __shfl_sync(0xffffffffu, sv0, L), o1 = __shfl_sync(0xffffffffu, sv1, L);
     const uint32_t b0 = __shfl_sync(0xffffffffu, bk[0], L), b1 = __shfl_sync(0xffffffffu, bk[1], L);
-    const uint32_t k0 = __shfl_sync(0xffffffffu, km[0], L), k1 = __shfl_sync(0xffffffffu, km[1], L);
-    const int kx = __shfl_sync(0xffffffffu, kex, L);
     const bool act = pos < tot.b;
     float4 v = bINF();
     uint32_t e = 0u, blend = 0u;
@@ -378,10 +546,8 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
       const int j = k < c0 ? select_bit32(o0, k) : 32 + select_bit32(o1, k - c0);
       blend = ((j < 32 ? b0 : b1) >> (j & 31)) & 1u;
       e = (uint32_t)(base + L * RL + j);
-      if (!blend) v = __ldg(p.boxes + e);
+      if (!blend) v = SC ? __ldg(p.boxes_in + __ldcg(p.index_out + e)) : __ldg(p.boxes + e);
       e += (uint32_t)p.goff;
-      if (p.scene)  // tile-local compacted index
-        e = (uint32_t)(kx + (j < 32 ? __popc(k0 & ((1u << j) - 1u)) : __popc(k0) + __popc(k1 & ((1u << (j - 32)) - 1u))));
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -527,13 +693,11 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   FZ_TRACE(0);
 
   // P0: Bic value and a-sum of the block's tiles
-  // s = Σa (pop offsets) + 2^32 Σkept (scene mode): both sums < 2^31
-  auto tile_agg = [&](int T) {
-    const int2 g = __ldcg(p.ctrl.agg + T);
-    return Agg{g.x, g.y, g.x + (p.scene ? (long long)__ldcg(p.kcnt + T) << 32 : 0ll)};
-  };
   Agg v{0, 0, 0};
-  for (int T = ta; T < tb; T++) v = agg_combine(v, tile_agg(T));
+  for (int T = ta; T < tb; T++) {
+    const int2 g = __ldcg(p.ctrl.agg + T);
+    v = agg_combine(v, Agg{g.x, g.y, g.x});
+  }
   Agg ex, tot;
   block_excl(v, ex, tot, sh);
   if (tid == 0) {
@@ -565,21 +729,19 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
     Agg cur = agg_combine(pre, ex);
     for (int T = ta; T < tb; T++) {
       const int2 g = __ldcg(p.ctrl.agg + T);
-      if (p.scene) p.koff[T] = cur.s >> 32;
       // one device: the height is the prefix's b (its a closes popped the root);
       // shard mode: h0 imported entries below, the prefix's a of them popped
       const int H = p.h0 ? p.h0 - cur.a + cur.b : cur.b;
       const int L = max(H - g.x, 0);
       p.ctrl.hstart[T] = H;
       p.ctrl.lw[T] = (uint32_t)L + 1u;
-      p.aoff[T] = cur.s & 0xffffffffll;
+      p.aoff[T] = cur.s;
       lmin = min(lmin, L);
-      cur = agg_combine(cur, tile_agg(T));
+      cur = agg_combine(cur, Agg{g.x, g.y, g.x});
     }
     if (tb == nt && ta < tb) {
       *p.ctrl.total = make_int2(cur.a, cur.b);
-      p.aoff[nt] = cur.s & 0xffffffffll;
-      if (p.scene) p.koff[nt] = cur.s >> 32;
+      p.aoff[nt] = cur.s;
     }
   }
   lmin = block_min(lmin, shm);
@@ -761,11 +923,6 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   for (int V = gt; V < nt; V += nthr) {
     p.tc[V] = __ldcg(accb[cb] + V);
     p.tcend[V] = __ldcg(ptrb[cb] + V);  // -1, or -2 - h: TC still lacks imported height h's context
-    if (p.scene) {  // slice entries: tile-local compacted index -> compacted index
-      const int bT = __ldcg(p.ctrl.agg + V).y;
-      const int ko = (int)__ldcg(p.koff + V);
-      for (int k = 0; k < bT; k++) p.slice_idx[(int64_t)V * W + k] += ko;
-    }
   }
   FZ_TRACE(7);
 }
@@ -876,8 +1033,6 @@ struct Smem {
   float4 wtu[NW];                   // warp unions
   float4 wmid[NW][NW];              // union of the warps strictly between
   Bic wtot[NW];
-  uint32_t kS[NT];                  // scene mode: kept elements of threads before t << 16 | t's kept mask
-  int kw[NW];
 };
 static_assert(sizeof(Smem) <= 56 * 1024, "four CTAs per SM");
 // rbuf addressed as val[RB0 + k * NT + t] (both arrays of float4 in one shared block)
@@ -982,7 +1137,12 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = blockIdx.x;
   const int64_t base = (int64_t)T * W;
-  const int nvalid = (int)(p.n - base < W ? p.n - base : W);
+  const int64_t nn = SC ? __ldg(p.nkp) : p.n;  // scene mode: the compacted stream's length
+  if (SC && base >= nn) {                       // a tile past it: no leaves
+    if (tid == 0) p.tu[0][T] = bEMPTY();
+    return;
+  }
+  const int nvalid = (int)(nn - base < W ? nn - base : W);
   const int gbase = p.goff + (int)base;  // global indices fit in int32 (n <= 2^31 - 1)
   const int tl0 = tid * K;      // tile-local index of the thread's first element
   const int gtb = gbase + tl0;
@@ -991,15 +1151,15 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   const int mb = mpad(tl0);                  // matchS index of element i = mb + i
 
   // ---- A. loads, register walk -------------------------------------------------
-  const uint4 raw = load_tags16(p.tags, p.n, base + tl0, nvalid == W);
+  const uint4 raw = load_tags16(p.tags, nn, base + tl0, nvalid == W);
   const int H = __ldg(p.ctrl.hstart + T);
   const int aT = __ldg(p.ctrl.agg + T).x;
   const int64_t poff = __ldg(p.aoff + T);  // pop records of this tile: [poff, poff + a_T)
   // the boxes of a full tile arrive by TMA (two 16 KB boxes, one per half of
   // the thread rows); the last, partial tile is copied by the threads
   const uint32_t val_sa = smem_u32(&s.val[0]), mbar = smem_u32(&s.mbar);
-  const bool tma = p.use_tma && nvalid == W && (val_sa & 1023u) == 0u;
-  if (tma) {
+  const bool tma = p.use_tma && nvalid == W && (val_sa & 1023u) == 0u;  // TMA store (and load, off scene mode)
+  if (tma && !SC) {
     if (tid == 0) {
       mbar_init(mbar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1007,6 +1167,15 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
       tma_load_2d(val_sa, &maps.in[0], 0, T * NT, mbar);
       tma_load_2d(val_sa + NT * 128, &maps.in[1], 0, T * NT, mbar);
     }
+  } else if (SC) {  // the kept elements' boxes, through their full-stream indices (all in flight)
+    int gi[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      const int e = j * NT + tid;
+      gi[j] = e < nvalid ? __ldg(p.index_out + base + e) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < K; j++) s.val[slot_of(j * NT + tid)] = gi[j] >= 0 ? __ldg(p.boxes_in + gi[j]) : bEMPTY();
   } else {
 #pragma unroll 1
     for (int j = 0; j < K; j++) {
@@ -1021,8 +1190,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   }
   const int nruns = __ldg(p.nruns + T);
   const int nv_t = nvalid - tl0;
-  const uint32_t valid = (nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u))) &
-                         (SC ? keep16(p.keepw, raw) : 0xffffu);  // scene: dropped elements are null
+  const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
   const Walk w = walk(raw, valid);
   const int a_t = __popc(w.ucm), b_t = __popc(w.S);
 
@@ -1030,29 +1198,6 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   if (tid < RMAX) cp_async_wait_all();
   Bic ex, sx, tot;
   block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, false);
-  int koffT = 0, kpt = 0;  // scene mode: compacted index of the tile's / the thread's first kept element
-  if (SC) {
-    koffT = (int)__ldg(p.koff + T);
-    const int kc = __popc(valid);
-    int ki = kc;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, ki, off);
-      if (lane >= off) ki += y;
-    }
-    if (lane == 31) s.kw[warp] = ki;
-    __syncthreads();
-    kpt = ki - kc;
-    for (int w2 = 0; w2 < warp; w2++) kpt += s.kw[w2];
-    s.kS[tid] = ((uint32_t)kpt << 16) | valid;
-  }
-  // scene mode: tile-local element -> its compacted index; a value (global
-  // index in the tile, or an earlier tile's compacted index, or -1) -> compacted
-  auto kpos = [&](int e) {
-    const uint32_t kw = s.kS[e >> 4];
-    return koffT + (int)(kw >> 16) + __popc(kw & ((1u << (e & 15)) - 1u) & 0xffffu);
-  };
-  auto conv = [&](int v) { return v < 0 ? -1 : (v >= gbase ? kpos(v - gbase) : v); };
   const int r_t = ex.b - ex.a;
   const int l_t = r_t - a_t;
   for (uint32_t q = w.S; q; q &= q - 1) s.matchS[mb + __ffs(q) - 1] = -1;  // closed by another thread / tile
@@ -1097,7 +1242,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
     else top_ref = r;
   }
   s.u.pj.link[tid] = lk;
-  if (tma) mbar_wait(mbar, 0);
+  if (tma && !SC) mbar_wait(mbar, 0);
   {
     float4 acc = bINF();
     for (uint32_t q = w.S; q; q &= q - 1) {
@@ -1224,7 +1369,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         if (si != -1) {
           gi = si & 0x7fffffff;
           xcm |= 1u << ci;
-          p.pop[poff + D] = make_int2(SC ? koffT + kpt + __popc(valid & ((1u << ci) - 1u)) : gtb + ci, rf);
+          p.pop[poff + D] = make_int2(gtb + ci, rf);
         } else {
           p.pop[poff + D] = make_int2(-1, -1);  // an imported slot below the global root (R3)
         }
@@ -1302,13 +1447,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         if (PM && !(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + pt;
         pv[jq] = par;
       }
-      if (PM && SC) {
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          const int i = 4 * q + jj;
-          if ((valid >> i) & 1u) p.parent[koffT + kpt + __popc(valid & ((1u << i) - 1u))] = conv(pv[jj]);
-        }
-      } else if (PM) {
+      if (PM) {
         if (nv_t >= 4 * q + 4) {
           __stcs(reinterpret_cast<int4*>(p.parent + base + tl0) + q, make_int4(pv[0], pv[1], pv[2], pv[3]));
         } else {
@@ -1446,18 +1585,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   __syncthreads();
 
   // ---- I. copy-out: node boxes by TMA (full tiles), match coalesced ---------
-  if (SC) {  // kept elements to their compacted indices
-#pragma unroll 1
-    for (int j = 0; j < K; j++) {
-      const int e = j * NT + tid;
-      if (e >= nvalid || !((s.kS[e >> 4] >> (e & 15)) & 1u)) continue;
-      const int pos = kpos(e);
-      __stcs(p.out + pos, s.val[slot_of(e)]);
-      if (PM) p.match[pos] = conv(s.matchS[mpad(e)]);
-      p.tags_out[pos] = p.tags[base + e];
-      p.index_out[pos] = gbase + e;
-    }
-  } else if (tma) {
+  if (tma) {
     if (tid == 0) {
       tma_store_2d(&maps.out[0], 0, T * NT, val_sa);
       tma_store_2d(&maps.out[1], 0, T * NT, val_sa + NT * 128);
@@ -1470,7 +1598,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
       if (e < nvalid) __stcs(p.out + base + e, s.val[slot_of(e)]);
     }
   }
-  if (PM && !SC) {
+  if (PM) {
 #pragma unroll
     for (int j = 0; j < W / 4 / NT; j++) {
       const int e = 4 * (j * NT + tid);
@@ -1672,6 +1800,8 @@ static cudaError_t setup() {
       if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
       if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fz_reduce<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * SC_WARP_BYTES));
     uint8_t tab[UNM4_ENTRIES];
     for (int i = 0; i < UNM4_ENTRIES; i++) tab[i] = unm4_entry(i);
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_unm4, tab, sizeof tab);
@@ -1713,7 +1843,19 @@ static cudaError_t dbg_sync(cudaStream_t s, const char* what) {
 // cooperative control kernel (tile scan, link owners, TC)
 static cudaError_t launch_front(fz::Params& p, cudaStream_t stream) {
   const int nt = p.ntiles;
-  TB_LAUNCH(stream, "fz_reduce", (fz::fz_reduce<<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
+  if (p.scene) {
+    TB_LAUNCH(stream, "sc_count", (fz::sc_count<<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
+    const int nb = (nt + 1023) / 1024;
+    long long* bsum = (long long*)p.blk;  // fz_ctrl's block aggregates: free until fz_ctrl
+    TB_LAUNCH(stream, "sc_scan", (fz::sc_scan1<<<nb, 1024, 0, stream>>>(p, bsum)));
+    TB_LAUNCH(stream, "sc_scan", (fz::sc_scan2<<<1, 1024, 0, stream>>>(p, bsum, nb)));
+    TB_LAUNCH(stream, "sc_scan", (fz::sc_scan3<<<nb, 1024, 0, stream>>>(p, bsum)));
+    TB_LAUNCH(stream, "sc_ranges", (fz::sc_ranges<<<(unsigned)((nt + 1 + 7) / 8), 256, 0, stream>>>(p)));
+    TB_LAUNCH(stream, "fz_reduce",
+              (fz::fz_reduce<true><<<(unsigned)((nt + 7) / 8), 256, 8 * fz::SC_WARP_BYTES, stream>>>(p)));
+  } else {
+    TB_LAUNCH(stream, "fz_reduce", (fz::fz_reduce<false><<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
+  }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = dbg_sync(stream, "fz_reduce");
   if (e != cudaSuccess) return e;
@@ -1782,26 +1924,29 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
   return launch_back(p, leaf_bbox, node_bbox, match != nullptr, stream);
 }
 
-// scene mode (fused stream compaction): the full stream in, the kept
-// elements' outputs at their compacted indices; *d_n_out = the kept count
+// scene mode (stream compaction fused into the loaders): the full stream in,
+// the kept elements' outputs at their compacted indices; *d_n_out = the kept count
 cudaError_t fused_scene_launch(const uint8_t* tags, const float* boxes, int64_t n, const uint8_t* h_keep_map,
                                uint8_t* tags_out, int32_t* index_out, int32_t* match, int32_t* parent,
                                float* node_bbox, int64_t* d_n_out, void* ws, cudaStream_t stream) {
   if (n <= 0) return cudaMemsetAsync(d_n_out, 0, sizeof(int64_t), stream);
   cudaError_t e = fz::setup();
   if (e != cudaSuccess) return e;
-  fz::Params p = fz::make_params(tags, boxes, n, match, parent, node_bbox, ws);
+  fz::Params p = fz::make_params(nullptr, boxes, n, match, parent, node_bbox, ws);
   p.scene = 1;
+  p.tags_in = tags;
+  p.boxes_in = (const float4*)boxes;
   p.tags_out = tags_out;
   p.index_out = index_out;
   uint32_t kw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int b = 0; b < 256; b++)
     if (h_keep_map[b]) kw[b >> 5] |= 1u << (b & 31);
+  p.keep03 = kw[0] == 0xfu && !(kw[1] | kw[2] | kw[3] | kw[4] | kw[5] | kw[6] | kw[7]);
   e = cudaMemcpyAsync((void*)p.keepw, kw, sizeof kw, cudaMemcpyHostToDevice, stream);
   if (e == cudaSuccess) e = launch_front(p, stream);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(d_n_out, p.koff + p.ntiles, sizeof(int64_t), cudaMemcpyDeviceToDevice, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_n_out, p.nkp, sizeof(int64_t), cudaMemcpyDeviceToDevice, stream);
   if (e != cudaSuccess) return e;
+  p.tags = tags_out;  // the main pass reads the compacted tags
   return launch_back(p, boxes, node_bbox, match != nullptr, stream);
 }
 
