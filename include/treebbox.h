@@ -166,10 +166,13 @@ int tree_bbox_matched_ws(const uint8_t *d_tags, const float *d_leaf_bbox, const 
  * paren_match_tree_bbox — the whole hot path in one device call: d_match and
  * d_parent as paren_match, d_node_bbox as tree_bbox_matched on them (same
  * arguments, layouts and error codes as those two; match / parent must not
- * overlap leaf_bbox either).  The box path's reduce pass (slice clips)
- * needs only tags and boxes, so it runs on a library side stream beside
- * paren_match and is joined into `stream` before the passes that read
- * match / parent.  Stream-ordered on `stream`; capturable in a CUDA graph.
+ * overlap leaf_bbox either).  One fused tile pass (csrc/fused.cu): a reduce
+ * pass (tile Bic values and slices with their clips), a
+ * cooperative control kernel (tile scan, link owners, tile contexts), the
+ * main pass (matching, clips and unions of each 2048-element tile; tags and
+ * boxes read once, match / parent / node_bbox written once) and a close pass
+ * for nodes that span tiles.  Stream-ordered on `stream`; capturable in a
+ * CUDA graph.
  * ------------------------------------------------------------------------ */
 int paren_match_tree_bbox(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, int32_t *d_match,
                           int32_t *d_parent, float *d_node_bbox, void *stream);
