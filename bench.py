@@ -156,9 +156,11 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def profile_traffic(config="C5"):
+    """DRAM bytes per launch of each kernel from the committed ncu launch list
+    of this config (profiles/traffic.json for C5, traffic_<config>.json else)."""
+    c = config.upper()
+    path = os.path.join(ROOT, "profiles", "traffic.json" if c == "C5" else f"traffic_{c}.json")
     try:
         with open(path) as f:
             return json.load(f)
@@ -393,7 +395,7 @@ def main():
     avg_ms = tot_ms / max(cnt, 1)
     kb = KERNEL_BYTES.get(dom, BYTES_PAIR)
     achieved = kb * n / (avg_ms / 1e3) / 1e9
-    traffic = profile_traffic().get(dom)
+    traffic = profile_traffic(args.config).get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "kernel_bytes_per_elem": kb, "kernel_ms": avg_ms,

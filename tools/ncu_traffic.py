@@ -12,11 +12,12 @@ import sys
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
         "nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3}
-OURS = ("fz_", "pm_", "tile_scan", "bbm_", "tt_", "bin_", "count_k", "scatter_k", "excl_scan", "scan_", "classify_bytes")
+OURS = ("fz_", "sh_", "sc_", "tf_", "pm_", "tile_scan", "bbm_", "tt_", "bin_", "count_k", "scatter_k", "excl_scan", "scan_", "classify_bytes")
 
 
 def main():
     rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
+    rows = rows[next(i for i, r in enumerate(rows) if "Kernel Name" in r):]  # skip the program's own output
     hdr = rows[0]
     ix = {h: i for i, h in enumerate(hdr)}
     per = collections.OrderedDict()
