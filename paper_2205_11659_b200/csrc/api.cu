@@ -132,6 +132,11 @@ int get_aux(AuxStreams** out) {
   return TB_OK;
 }
 
+// The fused single-device path (fused.cu) runs paren_match + tree_bbox from one
+// tile pass; tb_debug_use_fused(0) selects the earlier two-call path
+// (paren_match, then the boxes from its match / parent) for comparisons.
+static int g_use_fused = 1;
+
 int pm_checks(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent) {
   int r = check_n(n);
   if (r) return r;
@@ -208,6 +213,13 @@ int paren_match(const uint8_t* d_tags, int64_t n, int32_t* d_match, int32_t* d_p
   int r = pm_checks(d_tags, n, d_match, d_parent);
   if (r || n == 0) return r;
   void* ws = nullptr;
+  if (g_use_fused) {  // the fused tile pass without boxes (fz_match)
+    r = get_ws(stream, 14, tb::fused_match_workspace_bytes(n), &ws);
+    if (r) return r;
+    cudaError_t e = tb::fused_match_launch(d_tags, n, d_match, d_parent, ws, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "paren_match launch");
+    return TB_OK;
+  }
   const size_t need = tb::pm_workspace_bytes(n);
   r = get_ws(stream, 0, need, &ws);
   if (r) return r;
@@ -265,11 +277,6 @@ static int bbm_checks(const uint8_t* tags, const float* leaf, const int32_t* mat
     return fail(TB_ERR_ALIAS, "node_bbox overlaps an input");
   return TB_OK;
 }
-
-// The fused single-device path (fused.cu) runs paren_match + tree_bbox from one
-// tile pass; tb_debug_use_fused(0) selects the earlier two-call path
-// (paren_match, then the boxes from its match / parent) for comparisons.
-static int g_use_fused = 1;
 
 size_t tree_bbox_workspace_bytes(int64_t n) {
   if (n <= 0) return 0;

@@ -100,6 +100,7 @@ struct Params {
   // [T W, T W + W) -- whose tags and full-stream indices fz_reduce writes while
   // it compacts; fz_main gathers the boxes through those indices.  n / ntiles
   // are the full stream's (capacity); the kept count is on the device.
+  int nobox;              // matching only (fused_match_launch): no boxes, no contexts, no unions
   int scene;
   int keep03;              // the keep table is bytes 0-3 exactly (a compare)
   const uint32_t* keepw;   // [8] 256-bit keep table
@@ -130,7 +131,7 @@ struct Layout {
   size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, shd, tce, kpw, nk,
       tin, kci, kpi, bytes;
   int64_t ntiles;
-  explicit Layout(int64_t n, int h0 = 0) {
+  explicit Layout(int64_t n, int h0 = 0, bool nobox = false) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     ntiles = (n + W - 1) / W;
     const size_t cap = (size_t)ntiles * W + (size_t)h0;  // + the imported stack (shard mode)
@@ -141,8 +142,8 @@ struct Layout {
     ctrl = o; o = al(o + CtrlLayout(ntiles).bytes);
     aoff = o; o = al(o + 8 * ((size_t)ntiles + 1));
     sidx = o; o = al(o + 4 * cap);
-    sbox = o; o = al(o + 16 * cap);
-    ssu = o; o = al(o + 16 * cap);
+    sbox = o; o = al(o + (nobox ? 0 : 16 * cap));  // matching only: no slice boxes / unions
+    ssu = o; o = al(o + (nobox ? 0 : 16 * cap));
     pop = o; o = al(o + 8 * npop);
     int64_t m = ntiles;
     for (int k = 0; k < LV; k++) {
@@ -169,8 +170,8 @@ struct Layout {
 };
 
 static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, int32_t* match, int32_t* parent,
-                          float* out, void* ws, int h0 = 0, int goff = 0) {
-  const Layout L(n, h0);
+                          float* out, void* ws, int h0 = 0, int goff = 0, bool nobox = false) {
+  const Layout L(n, h0, nobox);
   char* b = (char*)ws;
   Params p;
   p.tags = tags;
@@ -207,6 +208,7 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.tcend = (int32_t*)(b + L.tce);
   p.exc = nullptr;
   p.exu = nullptr;
+  p.nobox = 0;
   p.scene = 0;
   p.keep03 = 0;
   p.keepw = (const uint32_t*)(b + L.kpw);
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
       const int j = k < c0 ? select_bit32(o0, k) : 32 + select_bit32(o1, k - c0);
       blend = ((j < 32 ? b0 : b1) >> (j & 31)) & 1u;
       e = (uint32_t)(base + L * RL + j);
-      if (!blend) v = SC ? __ldg(p.boxes_in + __ldcg(p.index_out + e)) : __ldg(p.boxes + e);
+      if (!blend && !p.nobox) v = SC ? __ldg(p.boxes_in + __ldcg(p.index_out + e)) : __ldg(p.boxes + e);
       e += (uint32_t)p.goff;
     }
 #pragma unroll
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
                         __shfl_sync(0xffffffffu, v.z, 31), __shfl_sync(0xffffffffu, v.w, 31));
     if (act) {
       p.slice_idx[base + pos] = (int)(e | (blend << 31));
-      p.slice_box[base + pos] = v;
+      if (!p.nobox) p.slice_box[base + pos] = v;
     }
   }
 }
@@ -837,7 +839,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
         }
       }
       float4 acc = bINF();
-      if (U >= 0) acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - ((int)__ldcg(p.ctrl.lw + U) - 1)));
+      if (U >= 0 && !p.nobox) acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - ((int)__ldcg(p.ctrl.lw + U) - 1)));
       p.pj_acc[T] = acc;
       p.pj_ptr[T] = U >= 0 || L < 1 ? U : -2 - (L - 1);  // no local owner: imported height L - 1
       p.pj_own[T] = U;
@@ -855,7 +857,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
       if (L >= 1) {
         int LU = 0;
         U = owner_search_cg(p.ctrl, T, L - 1, LU);
-        if (U >= 0) acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - LU));
+        if (U >= 0 && !p.nobox) acc = __ldcg(p.slice_box + (int64_t)U * W + (L - 1 - LU));
       }
       if (lane == 0) {
         p.pj_acc[T] = acc;
@@ -892,6 +894,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
     }
     p.nruns[T] = k;
   }
+  if (p.nobox) return;  // matching only: no tile contexts
   float4* accb[2] = {p.pj_acc, p.pj_acc + nt};
   int* ptrb[2] = {p.pj_ptr, p.pj_ptr + nt};
   int cb = 0;
@@ -1110,7 +1113,8 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
 // slice reference (owner tile * W + slice position) of the entry at height h
 // (>= 0) of the tile's incoming stack: the first run whose low-water mark is
 // <= h; past the stored runs, the walk along the link owners continues
-__device__ __forceinline__ int inc_ref(const Params& p, const Smem& s, int nruns, int h) {
+template <class S>
+__device__ __forceinline__ int inc_ref(const Params& p, const S& s, int nruns, int h) {
   const int nr = min(nruns, RMAX);
   for (int k = 0; k < nr; k++) {
     const int2 r = s.runs[k];
@@ -1617,6 +1621,205 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
 }
 
 // ----------------------------------------------------------------------------
+// fz_match: paren_match alone -- fz_main's matching phases
+// only (no boxes, contexts or unions): 15 KB of shared memory per tile instead
+// of 56, so four times the tiles per SM
+// ----------------------------------------------------------------------------
+struct SmemM {
+  int32_t matchS[W + W / K];
+  int lwin[NW][5][32];
+  int lwmin[NW];
+  int l[NT];
+  uint32_t uo[NT];
+  int link[NT];
+  int inc_idx[INCCAP];
+  int inc_ref[INCCAP];
+  int2 runs[RMAX];
+  Bic wtot[NW];
+};
+
+__global__ void __launch_bounds__(NT) fz_match(Params p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SmemM& s = *reinterpret_cast<SmemM*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockIdx.x;
+  const int64_t base = (int64_t)T * W;
+  const int nvalid = (int)(p.n - base < W ? p.n - base : W);
+  const int gbase = (int)base;
+  const int tl0 = tid * K;
+  const int gtb = gbase + tl0;
+  const int mb = mpad(tl0);
+  const uint4 raw = load_tags16(p.tags, p.n, base + tl0, nvalid == W);
+  const int H = __ldg(p.ctrl.hstart + T);
+  const int aT = __ldg(p.ctrl.agg + T).x;
+  const int64_t poff = __ldg(p.aoff + T);
+  if (tid < RMAX) {
+    cp_async8(smem_u32(&s.runs[tid]), p.runs + (int64_t)T * RMAX + tid);
+    cp_async_commit();
+  }
+  const int nruns = __ldg(p.nruns + T);
+  const int nv_t = nvalid - tl0;
+  const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
+  const Walk w = walk(raw, valid);
+  const int a_t = __popc(w.ucm);
+
+  // B. block Bic scan; thread low-water windows
+  if (tid < RMAX) cp_async_wait_all();
+  Bic ex, sx, tot;
+  block_bic_scans<NW>(Bic{a_t, __popc(w.S)}, s.wtot, ex, sx, tot, false);
+  const int r_t = ex.b - ex.a;
+  const int l_t = r_t - a_t;
+  for (uint32_t q = w.S; q; q &= q - 1) s.matchS[mb + __ffs(q) - 1] = -1;
+  int wl[5];
+  lane_windows(l_t, wl);
+#pragma unroll
+  for (int k = 0; k < 5; k++) s.lwin[warp][k][lane] = wl[k];
+  {
+    const int o = __shfl_sync(0xffffffffu, wl[4], 15);
+    if (lane == 31) s.lwmin[warp] = min(wl[4], o);
+  }
+  s.l[tid] = l_t;
+  s.uo[tid] = w.S;
+  __syncthreads();
+
+  // C. incoming entries (global index only); the thread's top entry and link
+  const int ninc = min(aT + 1, INCCAP);
+  for (int D = tid; D < ninc; D += NT) {
+    const int h = H - 1 - D;
+    if (h < 0) {
+      s.inc_idx[D] = -1;
+      s.inc_ref[D] = -1;
+    } else {
+      const int ref = inc_ref(p, s, nruns, h);
+      s.inc_ref[D] = ref;
+      cp_async4(smem_u32(&s.inc_idx[D]), p.slice_idx + ref);
+    }
+  }
+  cp_async_commit();
+  int top_ref = 0, lk = 0;
+#pragma unroll 1
+  for (int qq = 0; qq < 2; qq++) {
+    const int r = thread_ref<NW, K>(wl, l_t, w.S, qq ? l_t - 1 : r_t - 1, s.lwin, s.lwmin, s.l, s.uo);
+    if (qq) lk = r;
+    else top_ref = r;
+  }
+  s.link[tid] = lk;
+  cp_async_wait_all();
+  __syncthreads();
+  // D. the link's global index (the parent of the thread's outer elements after its last unmatched close)
+  int giLast = -1;
+  if (lk >= 0) {
+    giLast = gbase + lk;
+  } else {
+    const int D = -lk - 1;
+    if (H - 1 - D >= 0) {
+      const int si = D < INCCAP ? s.inc_idx[D] : __ldg(p.slice_idx + inc_ref(p, s, nruns, H - 1 - D));
+      giLast = si == -1 ? -1 : si & 0x7fffffff;
+    }
+  }
+  // E. the entries popped by the thread's unmatched closes
+  {
+    int ref = top_ref, d = 0;
+    uint32_t q = w.ucm;
+    if (d < a_t && ref >= 0) {
+      int V = ref >> LOGK, bp = ref & (K - 1);
+      uint32_t uV = s.uo[V];
+      while (true) {
+        const int e = (V << LOGK) | bp;
+        const int ci = __ffs(q) - 1;
+        q &= q - 1;
+        s.matchS[mb + ci] = gbase + e;
+        s.matchS[mpad(e)] = gtb + ci;
+        if (++d >= a_t) break;
+        const uint32_t below = uV & ((1u << bp) - 1u);
+        if (below) {
+          bp = 31 - __clz(below);
+        } else {
+          ref = s.link[V];
+          if (ref < 0) break;
+          V = ref >> LOGK;
+          bp = ref & (K - 1);
+          uV = s.uo[V];
+        }
+      }
+    }
+    for (; d < a_t; d++, ref--) {
+      const int ci = __ffs(q) - 1;
+      q &= q - 1;
+      const int D = -ref - 1;
+      int gi = -1;
+      if (H - 1 - D >= 0) {
+        const int rf = D < INCCAP ? s.inc_ref[D] : inc_ref(p, s, nruns, H - 1 - D);
+        const int si = D < INCCAP ? s.inc_idx[D] : __ldg(p.slice_idx + rf);
+        if (si != -1) {
+          gi = si & 0x7fffffff;
+          p.pop[poff + D] = make_int2(gtb + ci, rf);
+        } else {
+          p.pop[poff + D] = make_int2(-1, -1);
+        }
+      } else {
+        p.pop[poff + D] = make_int2(-1, -1);  // pops the root (R3)
+      }
+      s.matchS[mb + ci] = gi;
+    }
+  }
+  __syncthreads();
+  // F. parent of every element, match of the in-thread pairs and leaves
+#pragma unroll 1
+  for (int q = 0; q < K / 4; q++) {
+    const int i0 = 4 * q;
+    const uint32_t Lq = w.lm >> i0, Uq = w.ucm >> i0, Sq = w.S >> i0, Xq = w.ext >> i0;
+    const uint32_t pwq = (q < 2 ? w.plo : w.phi) >> (16 * (q & 1)), mwq = (q < 2 ? w.mlo : w.mhi) >> (16 * (q & 1));
+    int pv[4];
+#pragma unroll
+    for (int jq = 0; jq < 4; jq++) {
+      const int i = i0 + jq;
+      const bool isL = (Lq >> jq) & 1u, isU = (Uq >> jq) & 1u, isUO = (Sq >> jq) & 1u, isx = (Xq >> jq) & 1u;
+      const int pn = (int)((pwq >> (4 * jq)) & 15u);
+      const int pt = (int)((mwq >> (4 * jq)) & 15u);
+      const uint32_t nc = Uq >> jq;
+      const int j = nc ? i + __ffs(nc) - 1 : K - 1;
+      pv[jq] = isx ? (nc ? s.matchS[mb + j] : giLast) : gtb + pn;
+      if (!(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + pt;
+    }
+    if (nv_t >= 4 * q + 4) {
+      __stcs(reinterpret_cast<int4*>(p.parent + base + tl0) + q, make_int4(pv[0], pv[1], pv[2], pv[3]));
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++)
+        if (4 * q + jj < nv_t) p.parent[base + tl0 + 4 * q + jj] = pv[jj];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < W / 4 / NT; j++) {  // match out, coalesced
+    const int e = 4 * (j * NT + tid);
+    const int pe = mpad(e);
+    const int4 v4 = make_int4(s.matchS[pe], s.matchS[pe + 1], s.matchS[pe + 2], s.matchS[pe + 3]);
+    if (e + 4 <= nvalid) {
+      __stcs(reinterpret_cast<int4*>(p.match + base + e), v4);
+    } else {
+      if (e < nvalid) p.match[base + e] = v4.x;
+      if (e + 1 < nvalid) p.match[base + e + 1] = v4.y;
+      if (e + 2 < nvalid) p.match[base + e + 2] = v4.z;
+    }
+  }
+}
+
+// the opens of earlier tiles popped by this tile's closes: match[open] (one warp per tile)
+__global__ void __launch_bounds__(128) fz_close_m(Params p) {
+  const int lane = threadIdx.x & 31;
+  const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (T >= p.ntiles) return;
+  const int64_t poff = __ldg(p.aoff + T);
+  const int npop = (int)(__ldg(p.aoff + T + 1) - poff);
+  for (int j = lane; j < npop; j += 32) {
+    const int2 r = __ldcg(p.pop + poff + j);
+    if (r.x >= 0) p.match[__ldg(p.slice_idx + r.y) & 0x7fffffff] = r.x;
+  }
+}
+
+// ----------------------------------------------------------------------------
 // fz_hier: level k of the tile-union hierarchy (one warp per group of 32)
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) fz_hier(Params p, int k, int m /* nodes at level k - 1 */) {
@@ -1802,6 +2005,8 @@ static cudaError_t setup() {
     }
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fz_reduce<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * SC_WARP_BYTES));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fz_match, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemM));
     uint8_t tab[UNM4_ENTRIES];
     for (int i = 0; i < UNM4_ENTRIES; i++) tab[i] = unm4_entry(i);
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_unm4, tab, sizeof tab);
@@ -1828,6 +2033,7 @@ int fused_set_tma(int on) {
 }
 
 size_t fused_workspace_bytes(int64_t n) { return n > 0 ? fz::Layout(n).bytes : 0; }
+size_t fused_match_workspace_bytes(int64_t n) { return n > 0 ? fz::Layout(n, 0, true).bytes : 0; }
 int fused_tile_elems() { return fz::W; }
 
 // debug: TB_FZ_SYNC=1 synchronises after every launch and names the failing one
@@ -1922,6 +2128,27 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
   e = launch_front(p, stream);
   if (e != cudaSuccess) return e;
   return launch_back(p, leaf_bbox, node_bbox, match != nullptr, stream);
+}
+
+// paren_match alone by the fused machinery (no boxes): match and parent
+cudaError_t fused_match_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
+                               cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t e = fz::setup();
+  if (e != cudaSuccess) return e;
+  fz::Params p = fz::make_params(tags, nullptr, n, match, parent, nullptr, ws, 0, 0, true);
+  p.nobox = 1;
+  e = launch_front(p, stream);
+  if (e != cudaSuccess) return e;
+  const int nt = p.ntiles;
+  TB_LAUNCH(stream, "fz_match", (fz::fz_match<<<(unsigned)nt, fz::NT, sizeof(fz::SmemM), stream>>>(p)));
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = dbg_sync(stream, "fz_match");
+  if (e != cudaSuccess) return e;
+  TB_LAUNCH(stream, "fz_close", (fz::fz_close_m<<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = dbg_sync(stream, "fz_close_m");
+  return e;
 }
 
 // scene mode (stream compaction fused into the loaders): the full stream in,

@@ -87,6 +87,9 @@ cudaError_t fused_shard_phase3(int64_t n, int64_t goff, int cap, int G, int g, i
                                void* ws, const void* recv1, const void* recv2, cudaStream_t stream);
 int fused_shard_status(int64_t n, int cap, void* ws, cudaStream_t stream, cudaError_t* err);
 int fused_tile_elems();
+size_t fused_match_workspace_bytes(int64_t n);
+cudaError_t fused_match_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
+                               cudaStream_t stream);
 cudaError_t fused_scene_launch(const uint8_t* tags, const float* boxes, int64_t n, const uint8_t* h_keep_map,
                                uint8_t* tags_out, int32_t* index_out, int32_t* match, int32_t* parent,
                                float* node_bbox, int64_t* d_n_out, void* ws, cudaStream_t stream);
