@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(256) bin_fill_k(P p) {
 // only -- after culling few leaves remain -- instead of streaming all boxes
 // again; a list that overflowed falls back to the streaming fill.
 constexpr int SMB = 4096;
-constexpr unsigned GRID = 148 * 8;
 
 __device__ __forceinline__ void list_leaf(int32_t* cand, uint32_t* ncand, int64_t cap, int64_t e) {
   const unsigned act = __activemask();
@@ -166,7 +165,7 @@ cudaError_t bins_launch(const uint8_t* tags, const float* node_bbox, int64_t n, 
   uint32_t* ncand = reinterpret_cast<uint32_t*>(cursor + nb);
   int32_t* cand = cursor + nb + 4;
   const int64_t cap = std::min<int64_t>(g_cand_cap, std::max<int64_t>(n, 1));
-  const unsigned grid = bins::GRID;
+  const unsigned grid = (unsigned)(sm_count() * 8);
   cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)nb, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(ncand, 0, sizeof(uint32_t), stream);
   if (e == cudaSuccess && n > 0) {

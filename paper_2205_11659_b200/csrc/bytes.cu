@@ -40,7 +40,7 @@ cudaError_t classify_bytes_launch(const uint8_t* in, int64_t n, const uint8_t* c
   ClassMap cm;
   for (int i = 0; i < 256; i++) cm.m[i] = class_map[i];
   const int64_t nvec = (n >> 4) + 1;
-  const unsigned blocks = (unsigned)std::min<int64_t>((nvec + 255) / 256, 148 * 8);
+  const unsigned blocks = (unsigned)std::min<int64_t>((nvec + 255) / 256, sm_count() * 8);
   TB_LAUNCH(stream, "classify_bytes", (classify_bytes_k<<<blocks, 256, 0, stream>>>(in, n, cm, out)));
   return cudaGetLastError();
 }

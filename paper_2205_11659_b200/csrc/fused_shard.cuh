@@ -252,7 +252,7 @@ size_t fused_shard_slot1_bytes(int cap) { return fz::x1_bytes(cap); }
 size_t fused_shard_slot2_bytes(int cap) { return fz::x2_bytes(cap); }
 
 static int sh_grid(int64_t work, int per_block) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, 148 * 16));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((work + per_block - 1) / per_block, sm_count() * 16));
 }
 
 cudaError_t fused_shard_phase1(const uint8_t* tags, const float* leaf_bbox, int64_t n, int64_t goff, int cap,

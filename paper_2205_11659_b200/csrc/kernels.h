@@ -20,6 +20,7 @@ struct ShardInit {
 // One-time per-device setup (kernel attributes, occupancy-derived grid sizes):
 // `slot` names the setup, the bit of the current device says it is done.
 bool once_per_device(int slot);
+int sm_count();  // SMs of the current device (grid sizing: multiples of it)
 
 // Launch accounting / optional event timing around each kernel (prof.cu).
 void prof_begin(cudaStream_t s, const char* name, void** token);

@@ -53,6 +53,19 @@ void prof_end(cudaStream_t s, void* token) {
   delete r;
 }
 
+int sm_count() {  // streaming multiprocessors of the current device (cached per device)
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& c = cache[dev & 63];
+  if (c == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    c = v > 0 ? v : 1;
+  }
+  return c;
+}
+
 bool once_per_device(int slot) {
   static std::mutex mu;
   static uint64_t done[16] = {};  // [slot] bit d = done on device d (< 64)

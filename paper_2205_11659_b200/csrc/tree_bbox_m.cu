@@ -1174,7 +1174,7 @@ cudaError_t launch_range(const bbm::Params& p, cudaStream_t stream) {
 cudaError_t launch_rest(const bbm::Params& p, cudaStream_t stream) {
   cudaError_t err = launch_range(p, stream);
   if (err != cudaSuccess) return err;
-  TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<sm_count(), 256, 0, stream>>>(p)));
   return cudaGetLastError();
 }
 
@@ -1232,7 +1232,7 @@ cudaError_t bbm_end(const uint8_t* tags, const float* leaf_bbox, const int32_t* 
                     int64_t n, float* node_bbox, void* ws, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, nullptr, nullptr);
-  TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<148, 256, 0, stream>>>(p)));
+  TB_LAUNCH(stream, "bbm_final", (bbm::bbm_final<<<sm_count(), 256, 0, stream>>>(p)));
   return cudaGetLastError();
 }
 
@@ -1240,7 +1240,7 @@ cudaError_t bbm_patch_host_launch(const uint8_t* tags, const int32_t* match, int
                                   void* ws, float* host_mapped, int chunk_tiles, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   bbm::Params p = make_params(tags, nullptr, match, nullptr, n, const_cast<float*>(node_bbox), ws, nullptr, nullptr);
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p.ntiles + 7) / 8, 148 * 8));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((p.ntiles + 7) / 8, sm_count() * 8));
   TB_LAUNCH(stream, "bbm_patch_host", (bbm::bbm_patch_host<<<blocks, 256, 0, stream>>>(
                                           p, reinterpret_cast<float4*>(host_mapped), chunk_tiles)));
   return cudaGetLastError();
@@ -1312,7 +1312,7 @@ cudaError_t bbm_fixup_launch(const uint8_t* tags, const float* leaf_bbox, const 
                              const int* npops, int maxp, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   bbm::Params p = make_params(tags, leaf_bbox, match, parent, n, node_bbox, ws, sh, nullptr);
-  TB_LAUNCH(stream, "bbm_fixup", (bbm::bbm_fixup<<<148, 256, 0, stream>>>(p, hdr, G, g, allsuc, maxb, alltu,
+  TB_LAUNCH(stream, "bbm_fixup", (bbm::bbm_fixup<<<sm_count(), 256, 0, stream>>>(p, hdr, G, g, allsuc, maxb, alltu,
                                                                          allpops, npops, maxp)));
   return cudaGetLastError();
 }
