@@ -5,9 +5,10 @@
 Each case draws a size (1 .. ~400k, often near tile multiples), a tag mix
 (leaf / clip / blend / close probabilities, including close-heavy underflow
 mixes, deep chains and pure runs) and boxes, then checks bit-exact equality
-with the oracle for: paren_match_tree_bbox (the bench step), the virtual-shard
-protocol with a random shard count, and the chunked host pipeline with a
-random chunk size.  Prints one line per failure and a summary."""
+with the oracle for: paren_match_tree_bbox (the bench step), paren_match and
+tree_bbox alone, the round-1 virtual-shard box protocol and the sharded fused
+pass (random shard counts), the chunked host pipeline (random chunk size), the
+fused compaction (random commands inserted and dropped) and tree_fold.  Prints one line per failure and a summary."""
 import os
 import sys
 import time
@@ -78,10 +79,32 @@ def main():
         tb.paren_match_tree_bbox_host(t.pin_memory(), b.pin_memory(), hm, hp, ho)
         lib.tb_debug_host_chunk_shift(old)
         ok_h = np.array_equal(ho.numpy().view(np.uint32), ref) and np.array_equal(hm.numpy(), m_ref)
+        # paren_match alone (fz_match), tree_bbox alone, the sharded fused pass
+        m2, p2 = tb.paren_match(td)
+        ok_m = np.array_equal(m2.cpu().numpy(), m_ref) and np.array_equal(p2.cpu().numpy(), p_ref)
+        ok_t = np.array_equal(tb.tree_bbox(td, bd).cpu().numpy().view(np.uint32), ref)
+        gs = int(rng.integers(1, 17))
+        ms, ps, os_ = tb.pair_vshard(td, bd, gs, cap=n + 2)
+        ok_s = (np.array_equal(ms.cpu().numpy(), m_ref) and np.array_equal(ps.cpu().numpy(), p_ref)
+                and np.array_equal(os_.cpu().numpy().view(np.uint32), ref))
+        # the fused compaction: commands (bytes 4-15) inserted at random, dropped by the keep map
+        k = int(rng.integers(0, 2 * n + 1))
+        pos = np.sort(rng.integers(0, n + 1, size=k))
+        full = np.insert(t.numpy(), pos, rng.integers(4, 16, size=k).astype(np.uint8))
+        fb = np.insert(b.numpy(), pos, rng.normal(size=(k, 4)).astype(np.float32), axis=0)
+        tt, ii, mm, pp, oo, kk = tb.paren_match_tree_bbox_scene(torch.from_numpy(full).cuda(),
+                                                              torch.from_numpy(np.ascontiguousarray(fb)).cuda())
+        ok_c = (kk == n and np.array_equal(mm.cpu().numpy(), m_ref) and np.array_equal(pp.cpu().numpy(), p_ref)
+                and np.array_equal(oo.cpu().numpy().view(np.uint32), ref))
+        # tree_fold (2x2 matrices mod 2^32 up the tree)
+        x = rng.integers(0, 1 << 32, size=(n, 4), dtype=np.uint64).astype(np.uint32)
+        f = tb.tree_fold(td, torch.from_numpy(x.view(np.int32)).cuda(), torch.from_numpy(m_ref).cuda())
+        ok_f = np.array_equal(f.cpu().numpy().view(np.uint32), oracle.tree_fold(t.numpy(), x))
         cases += 1
-        if not (ok and ok_v and ok_h):
+        if not (ok and ok_v and ok_h and ok_m and ok_t and ok_s and ok_c and ok_f):
             fails += 1
-            print(f"FAIL n={n} fused={ok} vshard(G={g})={ok_v} host(shift={shift})={ok_h}", flush=True)
+            print(f"FAIL n={n} fused={ok} vshard(G={g})={ok_v} host(shift={shift})={ok_h} pm={ok_m} tb={ok_t} "
+                  f"shard(G={gs})={ok_s} scene={ok_c} fold={ok_f}", flush=True)
     print(f"fuzz: {cases} cases, {fails} failures")
     sys.exit(1 if fails else 0)
 
