@@ -24,7 +24,7 @@
 //              pointer jumping over threads, one forward walk that clips,
 //              unions and emits parent/match, a backward walk for the unions
 //              of opens closed in a later thread or tile; coalesced copy-out.
-//   fz_hier    32-ary hierarchy of tile unions.
+//   fz_hier    32-ary hierarchy of tile unions (one launch: the last block builds the upper levels).
 //   fz_close   closes of nodes opened in an earlier tile: tile prefix ∪ the
 //              open's tile suffix ∪ the whole tiles between (F4/F7); blend
 //              opens and match[open] receive the result; blend opens never
@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   if (tid == 0) {
     p.blk[bx] = make_int4(tot.a, tot.b, (int)(unsigned)(tot.s & 0xffffffffll), (int)(tot.s >> 32));
     if (bx == 0) {
-      p.flag[0] = p.flag[1] = p.flag[2] = 0;
+      p.flag[0] = p.flag[1] = p.flag[2] = p.flag[3] = 0;  // [3]: fz_hier's arrival counter
     }
   }
   grid.sync();
@@ -1822,14 +1822,38 @@ __global__ void __launch_bounds__(128) fz_close_m(Params p) {
 // ----------------------------------------------------------------------------
 // fz_hier: level k of the tile-union hierarchy (one warp per group of 32)
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) fz_hier(Params p, int k, int m /* nodes at level k - 1 */) {
-  const int lane = threadIdx.x & 31;
-  const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if ((g << 5) >= m) return;
-  const int c = (g << 5) + lane;
-  float4 v = c < m ? __ldcg(p.tu[k - 1] + c) : bEMPTY();
-  v = warp_unite_all(v);
-  if (lane == 0) p.tu[k][g] = v;
+// one launch: every block reduces its level-1 groups; the last block to finish
+// (arrival counter flag[3], zeroed by fz_ctrl) builds the upper levels
+__global__ void __launch_bounds__(256) fz_hier(Params p) {
+  __shared__ int last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int m = p.ntiles;  // nodes at level 0
+  {
+    const int g = blockIdx.x * 8 + warp;
+    if ((g << 5) < m) {
+      const int c = (g << 5) + lane;
+      const float4 v = warp_unite_all(c < m ? __ldcg(p.tu[0] + c) : bEMPTY());
+      if (lane == 0) p.tu[1][g] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(p.flag + 3, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  m = (m + 31) / 32;  // nodes at level 1
+  for (int k = 2; k < LV && m > 1; k++) {
+    const int groups = (m + 31) / 32;
+    for (int g = warp; g < groups; g += 8) {
+      const int c = (g << 5) + lane;
+      const float4 v = warp_unite_all(c < m ? __ldcg(p.tu[k - 1] + c) : bEMPTY());
+      if (lane == 0) p.tu[k][g] = v;
+    }
+    __threadfence_block();
+    __syncthreads();
+    m = groups;
+  }
 }
 
 // union over tiles [a, b] by one warp (a, b warp-uniform): per level of the
@@ -2101,13 +2125,11 @@ static cudaError_t launch_back(fz::Params& p, const float* leaf_bbox, float* nod
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = dbg_sync(stream, "fz_main");
   if (e != cudaSuccess) return e;
-  int m = nt;
-  for (int k = 1; k < fz::LV && m > 1; k++) {
-    const int groups = (m + 31) / 32;
-    TB_LAUNCH(stream, "fz_hier", (fz::fz_hier<<<(unsigned)((groups + 7) / 8), 256, 0, stream>>>(p, k, m)));
+  if (nt > 1) {
+    const int groups = (nt + 31) / 32;
+    TB_LAUNCH(stream, "fz_hier", (fz::fz_hier<<<(unsigned)((groups + 7) / 8), 256, 0, stream>>>(p)));
     e = dbg_sync(stream, "fz_hier");
     if (e != cudaSuccess) return e;
-    m = groups;
   }
   if (pm)
     TB_LAUNCH(stream, "fz_close", (fz::fz_close<true><<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
