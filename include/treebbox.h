@@ -301,10 +301,12 @@ int paren_match_tree_bbox_host(const uint8_t *h_tags, const float *h_leaf_bbox, 
  * NCCL all-gathers on `comm`, and each rank finishes locally; a close whose
  * open lies in an earlier chunk is reported to that chunk in a second small
  * all-gather.  `comm` is an ncclComm_t (from tb_comm_init).  Collective: all
- * ranks must call with their chunks.  paren_match_shard and
- * tree_bbox_matched_shard synchronise `stream` (their exchange sizes are read
- * on the host; tree_bbox_matched_shard takes at most 64 ranks);
- * paren_match_tree_bbox_shard (the bench step) does not.
+ * ranks must call with their chunks.  paren_match_tree_bbox_shard (the bench
+ * step) enqueues two fixed-size all-gathers and does not synchronise;
+ * paren_match_shard and tree_bbox_shard run the same protocol (matching alone
+ * / boxes alone) with a capacity from the largest chunk (an all-reduce) and
+ * check it, so they synchronise `stream`; tree_bbox_matched_shard (round 1's
+ * protocol, at most 64 ranks) synchronises too.
  * ------------------------------------------------------------------------ */
 #define TB_UNIQUE_ID_BYTES 128
 /* Rank 0 creates an id; broadcast its 128 bytes to the other ranks. */

@@ -481,19 +481,23 @@ def pair_vshard(tags: torch.Tensor, leaf_bbox: torch.Tensor, nshards: int, cap: 
     Returns (match, parent, node_bbox); match / parent are None when pm=False."""
     lib = load()
     _need_cuda(tags, "tags", torch.uint8)
-    _need_cuda(leaf_bbox, "leaf_bbox", torch.float32)
     n = tags.numel()
-    if leaf_bbox.shape != (n, 4):
-        raise ValueError("leaf_bbox must be (n, 4)")
+    if leaf_bbox is not None:  # None: the matching alone (paren_match_shard's protocol)
+        _need_cuda(leaf_bbox, "leaf_bbox", torch.float32)
+        if leaf_bbox.shape != (n, 4):
+            raise ValueError("leaf_bbox must be (n, 4)")
+    elif not pm:
+        raise ValueError("no outputs")
     if cap is None:
         cap = shard_default_cap((n + nshards - 1) // nshards + 16)  # chunk borders: multiples of 16
-    out = torch.empty_like(leaf_bbox)
+    out = torch.empty_like(leaf_bbox) if leaf_bbox is not None else None
     match = torch.empty(n, dtype=torch.int32, device=tags.device) if pm else None
     parent = torch.empty(n, dtype=torch.int32, device=tags.device) if pm else None
     with torch.cuda.device(tags.device):
-        _check(lib.tb_debug_pair_vshard(tags.data_ptr(), leaf_bbox.data_ptr(), n, nshards, int(cap),
-                                        match.data_ptr() if pm else None, parent.data_ptr() if pm else None,
-                                        out.data_ptr(), _stream(tags.device)))
+        _check(lib.tb_debug_pair_vshard(tags.data_ptr(), leaf_bbox.data_ptr() if out is not None else None, n,
+                                        nshards, int(cap), match.data_ptr() if pm else None,
+                                        parent.data_ptr() if pm else None, out.data_ptr() if out is not None else None,
+                                        _stream(tags.device)))
     return match, parent, out
 
 

@@ -765,12 +765,28 @@ int paren_match_shard(const uint8_t* d_tags, int64_t n_local, int64_t offset, in
   if (offset < 0 || offset + n_local > kMaxN) return fail(TB_ERR_ARG, "offset + n_local out of range");
   if (!comm) return fail(TB_ERR_ARG, "null communicator");
 #ifdef TB_WITH_NCCL
-  int nerr = 0;
-  cudaError_t e = tb::pm_nccl_shard(d_tags, n_local, offset, d_match, d_parent, (ncclComm_t)comm,
-                                    (cudaStream_t)stream, &nerr);
-  if (nerr) return fail(TB_ERR_NCCL, "NCCL error %d", nerr);
+  // the sharded fused pass without boxes (two fixed-size all-gathers); its
+  // capacity from the largest chunk (an all-reduce), then the status check
+  int nranks = 0;
+  if (ncclCommCount((ncclComm_t)comm, &nranks) != ncclSuccess) return fail(TB_ERR_NCCL, "ncclCommCount");
+  if (nranks > 256) return fail(TB_ERR_ARG, "paren_match_shard supports at most 256 ranks");
+  void* nmx = nullptr;
+  r = get_ws(stream, 11, 256, &nmx);
+  if (r) return r;
+  int64_t nl = n_local;
+  cudaError_t e = cudaMemcpyAsync(nmx, &nl, sizeof nl, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  if (e == cudaSuccess &&
+      ncclAllReduce(nmx, nmx, 1, ncclInt64, ncclMax, (ncclComm_t)comm, (cudaStream_t)stream) != ncclSuccess)
+    return fail(TB_ERR_NCCL, "ncclAllReduce");
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&nl, nmx, sizeof nl, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "paren_match_shard");
-  return TB_OK;
+  int nerr = 0;
+  e = tb::fz_nccl_shard(d_tags, nullptr, n_local, offset, (int)tb_shard_default_cap(nl), d_match, d_parent, nullptr,
+                        (ncclComm_t)comm, (cudaStream_t)stream, &nerr);
+  if (nerr) return fail(TB_ERR_NCCL, "NCCL error");
+  if (e != cudaSuccess) return cuda_fail(e, "paren_match_shard");
+  return tb_shard_status(stream);
 #else
   return fail(TB_ERR_NCCL, "built without NCCL");
 #endif
@@ -859,11 +875,16 @@ int tb_shard_status(void* stream) {
 int tb_debug_pair_vshard(const uint8_t* d_tags, const float* d_leaf_bbox, int64_t n, int nshards, int64_t cap,
                          int32_t* d_match, int32_t* d_parent, float* d_node_bbox, void* stream) {
   g_err[0] = 0;
-  int r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
-  if (r || n == 0) return r;
+  int r = 0;
+  if (d_leaf_bbox || d_node_bbox) {
+    r = bb_checks(d_tags, d_leaf_bbox, n, d_node_bbox);
+    if (r || n == 0) return r;
+  } else if (!d_match) {
+    return fail(TB_ERR_ARG, "no outputs");
+  }
   if (d_match || d_parent) {
     r = pm_checks(d_tags, n, d_match, d_parent);
-    if (r) return r;
+    if (r || n == 0) return r;
   }
   if (nshards < 1 || nshards > 256) return fail(TB_ERR_ARG, "bad shard count");
   if (cap < 1 || cap > kMaxN) return fail(TB_ERR_ARG, "cap out of range");

@@ -1645,7 +1645,7 @@ __global__ void __launch_bounds__(NT) fz_match(Params p) {
   const int T = blockIdx.x;
   const int64_t base = (int64_t)T * W;
   const int nvalid = (int)(p.n - base < W ? p.n - base : W);
-  const int gbase = (int)base;
+  const int gbase = p.goff + (int)base;  // shard mode: global indices
   const int tl0 = tid * K;
   const int gtb = gbase + tl0;
   const int mb = mpad(tl0);
@@ -1815,7 +1815,9 @@ __global__ void __launch_bounds__(128) fz_close_m(Params p) {
   const int npop = (int)(__ldg(p.aoff + T + 1) - poff);
   for (int j = lane; j < npop; j += 32) {
     const int2 r = __ldcg(p.pop + poff + j);
-    if (r.x >= 0) p.match[__ldg(p.slice_idx + r.y) & 0x7fffffff] = r.x;
+    if (r.x < 0) continue;
+    if (r.y >= p.vbase) p.exc[r.y - p.vbase] = r.x;  // an imported entry (shard mode): its chunk writes match
+    else p.match[(__ldg(p.slice_idx + r.y) & 0x7fffffff) - p.goff] = r.x;
   }
 }
 
@@ -2152,6 +2154,19 @@ cudaError_t fused_launch(const uint8_t* tags, const float* leaf_bbox, int64_t n,
   return launch_back(p, leaf_bbox, node_bbox, match != nullptr, stream);
 }
 
+// the matching main pass and its close pass (no boxes)
+static cudaError_t launch_back_match(fz::Params& p, cudaStream_t stream) {
+  const int nt = p.ntiles;
+  TB_LAUNCH(stream, "fz_match", (fz::fz_match<<<(unsigned)nt, fz::NT, sizeof(fz::SmemM), stream>>>(p)));
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = dbg_sync(stream, "fz_match");
+  if (e != cudaSuccess) return e;
+  TB_LAUNCH(stream, "fz_close", (fz::fz_close_m<<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = dbg_sync(stream, "fz_close_m");
+  return e;
+}
+
 // paren_match alone by the fused machinery (no boxes): match and parent
 cudaError_t fused_match_launch(const uint8_t* tags, int64_t n, int32_t* match, int32_t* parent, void* ws,
                                cudaStream_t stream) {
@@ -2162,15 +2177,7 @@ cudaError_t fused_match_launch(const uint8_t* tags, int64_t n, int32_t* match, i
   p.nobox = 1;
   e = launch_front(p, stream);
   if (e != cudaSuccess) return e;
-  const int nt = p.ntiles;
-  TB_LAUNCH(stream, "fz_match", (fz::fz_match<<<(unsigned)nt, fz::NT, sizeof(fz::SmemM), stream>>>(p)));
-  e = cudaGetLastError();
-  if (e == cudaSuccess) e = dbg_sync(stream, "fz_match");
-  if (e != cudaSuccess) return e;
-  TB_LAUNCH(stream, "fz_close", (fz::fz_close_m<<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
-  e = cudaGetLastError();
-  if (e == cudaSuccess) e = dbg_sync(stream, "fz_close_m");
-  return e;
+  return launch_back_match(p, stream);
 }
 
 // scene mode (stream compaction fused into the loaders): the full stream in,

@@ -59,8 +59,8 @@ __host__ __device__ inline X2 x2_view(char* slot, int cap) {
 // slice references of the final stack
 struct ShardLayout {
   size_t tab, tcc, svref, bytes;
-  ShardLayout(int64_t n, int cap) {
-    size_t o = al256(Layout(n, cap).bytes);
+  ShardLayout(int64_t n, int cap, bool nobox) {
+    size_t o = al256(Layout(n, cap, nobox).bytes);
     tab = o; o = al256(o + 16 * (size_t)GMAX);
     tcc = o; o = al256(o + 16 * (size_t)GMAX);
     svref = o; o = al256(o + 4 * (size_t)cap);
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) sh_export1(Params p, int cap, char* slot,
     if (lane == 0) {
       const int ref = U * W + (X - LU);
       x.idx[j] = __ldcg(p.slice_idx + ref);
-      x.lcc[j] = isect(__ldcg(p.slice_box + ref), __ldcg(p.tc + U));
+      x.lcc[j] = p.nobox ? bINF() : isect(__ldcg(p.slice_box + ref), __ldcg(p.tc + U));
       svref[j] = ref;
     }
   }
@@ -150,10 +150,12 @@ __global__ void __launch_bounds__(256) sh_compose(Params p, int g, int cap, cons
     int idx;
     const float4 c = imported_ctx(p, tab, tcc, g, recv1, cap, h, idx);
     p.slice_idx[p.vbase + h] = idx;
-    p.slice_box[p.vbase + h] = c;
     p.exc[h] = -1;
+    if (p.nobox) continue;
+    p.slice_box[p.vbase + h] = c;
     p.exu[h] = bEMPTY();
   }
+  if (p.nobox) return;  // matching only: no tile contexts
   const int ntv = (p.h0 + W - 1) / W;
   for (int j = gt; j < ntv; j += nthr) p.tc[p.ntiles + j] = bINF();
   for (int T = gt; T < p.ntiles; T += nthr) {
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(256) sh_compose(Params p, int g, int cap, cons
 // it to the chunk end)
 __global__ void __launch_bounds__(256) sh_export2(Params p, int cap, char* slot, const int32_t* svref) {
   const int lane = threadIdx.x & 31;
+  if (p.nobox) return;  // matching only: the recorded closes are all slot 2 carries
   X2 x = x2_view(slot, cap);
   const int2 tot = __ldcg(p.ctrl.total);
   const int nb = tot.y > cap || tot.x + 1 > p.h0 ? 0 : tot.y;
@@ -208,6 +211,7 @@ __global__ void __launch_bounds__(256) sh_fixup(Params p, int G, int g, int cap,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += nthr) {
     if (i < nA) {
       // A: this chunk's close of an imported entry (opened on chunk j)
+      if (p.nobox) continue;
       const int h = (int)i;
       const int c = mine2.exc[h];
       if (c < 0) continue;
@@ -228,10 +232,11 @@ __global__ void __launch_bounds__(256) sh_fixup(Params p, int G, int g, int cap,
       const int si = mine.idx[pos];
       const int o = (si & 0x7fffffff) - p.goff;
       if (PM) p.match[o] = c;
-      if (si < 0)  // a blend open takes its node's union
+      if (si < 0 && !p.nobox)  // a blend open takes its node's union
         p.out[o] = unite(unite(xk.exu[h], mine2.su[pos]), chunks_union(recv2, cap, g + 1, k - 1));
     } else {
       // C: final-stack opens no later chunk closes (R4): blend opens take the union to the end
+      if (p.nobox) continue;
       const int pos = (int)(i - nA - nB);
       const int X = tab[g].L + pos;
       int later = INT_MAX;
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(256) sh_fixup(Params p, int G, int g, int cap,
 }  // namespace fz
 
 // ---- host side of the sharded pass --------------------------------------------
-size_t fused_shard_workspace_bytes(int64_t n, int cap) { return fz::ShardLayout(n, cap).bytes; }
+size_t fused_shard_workspace_bytes(int64_t n, int cap, bool nobox) { return fz::ShardLayout(n, cap, nobox).bytes; }
 size_t fused_shard_slot1_bytes(int cap) { return fz::x1_bytes(cap); }
 size_t fused_shard_slot2_bytes(int cap) { return fz::x2_bytes(cap); }
 
@@ -260,10 +265,12 @@ cudaError_t fused_shard_phase1(const uint8_t* tags, const float* leaf_bbox, int6
   if (n <= 0) return cudaMemsetAsync(slot1, 0, 16, stream);  // header (0, 0): an empty chunk
   cudaError_t e = fz::setup();
   if (e != cudaSuccess) return e;
-  fz::Params p = fz::make_params(tags, leaf_bbox, n, nullptr, nullptr, nullptr, ws, cap, (int)goff);
+  const bool nobox = leaf_bbox == nullptr;  // paren_match alone
+  fz::Params p = fz::make_params(tags, leaf_bbox, n, nullptr, nullptr, nullptr, ws, cap, (int)goff, nobox);
+  p.nobox = nobox;
   e = launch_front(p, stream);
   if (e != cudaSuccess) return e;
-  const fz::ShardLayout SL(n, cap);
+  const fz::ShardLayout SL(n, cap, nobox);
   TB_LAUNCH(stream, "sh_export1",
             (fz::sh_export1<<<sh_grid(cap, 8), 256, 0, stream>>>(p, cap, (char*)slot1, (int32_t*)((char*)ws + SL.svref))));
   return cudaGetLastError();
@@ -272,10 +279,12 @@ cudaError_t fused_shard_phase1(const uint8_t* tags, const float* leaf_bbox, int6
 cudaError_t fused_shard_phase2(const uint8_t* tags, const float* leaf_bbox, int64_t n, int64_t goff, int cap, int G,
                                int g, int32_t* match, int32_t* parent, float* node_bbox, void* ws, const void* recv1,
                                void* slot2, cudaStream_t stream) {
-  const fz::ShardLayout SL(n > 0 ? n : 1, cap);
+  const bool nobox = leaf_bbox == nullptr;
+  const fz::ShardLayout SL(n > 0 ? n : 1, cap, nobox);
   cudaError_t e = fz::setup();
   if (e != cudaSuccess) return e;
-  fz::Params p = fz::make_params(tags, leaf_bbox, n > 0 ? n : 1, match, parent, node_bbox, ws, cap, (int)goff);
+  fz::Params p = fz::make_params(tags, leaf_bbox, n > 0 ? n : 1, match, parent, node_bbox, ws, cap, (int)goff, nobox);
+  p.nobox = nobox;
   fz::X2 x = fz::x2_view((char*)slot2, cap);
   p.exc = x.exc;
   p.exu = x.exu;
@@ -294,7 +303,7 @@ cudaError_t fused_shard_phase2(const uint8_t* tags, const float* leaf_bbox, int6
                 p, g, cap, (const char*)recv1, tab, tcc)));
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  e = launch_back(p, leaf_bbox, node_bbox, match != nullptr, stream);
+  e = nobox ? launch_back_match(p, stream) : launch_back(p, leaf_bbox, node_bbox, match != nullptr, stream);
   if (e != cudaSuccess) return e;
   TB_LAUNCH(stream, "sh_export2",
             (fz::sh_export2<<<sh_grid(cap, 8), 256, 0, stream>>>(p, cap, (char*)slot2,
@@ -305,8 +314,10 @@ cudaError_t fused_shard_phase2(const uint8_t* tags, const float* leaf_bbox, int6
 cudaError_t fused_shard_phase3(int64_t n, int64_t goff, int cap, int G, int g, int32_t* match, float* node_bbox,
                                void* ws, const void* recv1, const void* recv2, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;  // an empty chunk has no final stack and no closes
-  const fz::ShardLayout SL(n, cap);
-  fz::Params p = fz::make_params(nullptr, nullptr, n, match, nullptr, node_bbox, ws, cap, (int)goff);
+  const bool nobox = node_bbox == nullptr;
+  const fz::ShardLayout SL(n, cap, nobox);
+  fz::Params p = fz::make_params(nullptr, nullptr, n, match, nullptr, node_bbox, ws, cap, (int)goff, nobox);
+  p.nobox = nobox;
   auto* tab = (const fz::ChunkRow*)((char*)ws + SL.tab);
   const int64_t work = (int64_t)cap * (G - g) + cap;
   if (match)

@@ -76,7 +76,7 @@ int fused_set_abl(int mask);  // debug: skip fz_main phases (1 start stacks, 2 f
 // the fused pass over one chunk of a sharded stream (fused_shard.cuh): three
 // phases around two fixed-size exchanges of slot1 / slot2 (cap: the largest
 // Bic a + 1 and b of a chunk; equal on every rank)
-size_t fused_shard_workspace_bytes(int64_t n, int cap);
+size_t fused_shard_workspace_bytes(int64_t n, int cap, bool nobox);  // nobox: matching only (leaf_bbox null)
 size_t fused_shard_slot1_bytes(int cap);
 size_t fused_shard_slot2_bytes(int cap);
 cudaError_t fused_shard_phase1(const uint8_t* tags, const float* leaf_bbox, int64_t n, int64_t goff, int cap,

@@ -676,8 +676,8 @@ struct FzBufs {
   char* slot2 = nullptr;
   char* recv2 = nullptr;
 };
-cudaError_t fz_bufs(Scratch& sc, int64_t n, int cap, int G, int nws, FzBufs& b) {
-  const size_t wsb = fused_shard_workspace_bytes(std::max<int64_t>(n, 1), cap);
+cudaError_t fz_bufs(Scratch& sc, int64_t n, int cap, int G, int nws, bool nobox, FzBufs& b) {
+  const size_t wsb = fused_shard_workspace_bytes(std::max<int64_t>(n, 1), cap, nobox);
   const size_t s1 = fused_shard_slot1_bytes(cap), s2 = fused_shard_slot2_bytes(cap);
   cudaError_t e = sc.get(wsb * (size_t)nws, &b.ws);
   if (e == cudaSuccess) e = sc.get(s1, &b.slot1);
@@ -709,20 +709,21 @@ cudaError_t fz_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, 
   int64_t nmax = 0;
   for (int k = 0; k < G; k++) nmax = std::max(nmax, off(k + 1) - off(k));
   FzBufs b;
-  e = fz_bufs(sc, nmax, cap, G, G, b);
+  const bool nobox = leaf == nullptr;
+  e = fz_bufs(sc, nmax, cap, G, G, nobox, b);
   if (e != cudaSuccess) return e;
-  const size_t wsb = fused_shard_workspace_bytes(std::max<int64_t>(nmax, 1), cap);
+  const size_t wsb = fused_shard_workspace_bytes(std::max<int64_t>(nmax, 1), cap, nobox);
   const size_t s1 = fused_shard_slot1_bytes(cap), s2 = fused_shard_slot2_bytes(cap);
   for (int k = 0; k < G && e == cudaSuccess; k++)
-    e = fused_shard_phase1(tags + off(k), leaf + 4 * off(k), off(k + 1) - off(k), off(k), cap, b.ws + wsb * k,
-                           b.recv1 + s1 * k, s);
+    e = fused_shard_phase1(tags + off(k), leaf ? leaf + 4 * off(k) : nullptr, off(k + 1) - off(k), off(k), cap,
+                           b.ws + wsb * k, b.recv1 + s1 * k, s);
   for (int k = 0; k < G && e == cudaSuccess; k++)
-    e = fused_shard_phase2(tags + off(k), leaf + 4 * off(k), off(k + 1) - off(k), off(k), cap, G, k,
-                           match ? match + off(k) : nullptr, parent ? parent + off(k) : nullptr, out + 4 * off(k),
-                           b.ws + wsb * k, b.recv1, b.recv2 + s2 * k, s);
+    e = fused_shard_phase2(tags + off(k), leaf ? leaf + 4 * off(k) : nullptr, off(k + 1) - off(k), off(k), cap, G, k,
+                           match ? match + off(k) : nullptr, parent ? parent + off(k) : nullptr,
+                           out ? out + 4 * off(k) : nullptr, b.ws + wsb * k, b.recv1, b.recv2 + s2 * k, s);
   for (int k = 0; k < G && e == cudaSuccess; k++)
     e = fused_shard_phase3(off(k + 1) - off(k), off(k), cap, G, k, match ? match + off(k) : nullptr,
-                           out + 4 * off(k), b.ws + wsb * k, b.recv1, b.recv2, s);
+                           out ? out + 4 * off(k) : nullptr, b.ws + wsb * k, b.recv1, b.recv2, s);
   if (e == cudaSuccess && overflow) {
     cudaError_t e2 = cudaSuccess;
     *overflow = 0;
@@ -749,7 +750,7 @@ cudaError_t fz_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int
   cudaError_t e = sc.begin();
   if (e != cudaSuccess) return e;
   FzBufs b;
-  e = fz_bufs(sc, n, cap, G, 1, b);
+  e = fz_bufs(sc, n, cap, G, 1, leaf == nullptr, b);
   if (e != cudaSuccess) return e;
   auto nccl_ok = [&](ncclResult_t r) {
     ncclResult_t ar = ncclSuccess;

@@ -56,6 +56,9 @@ def check(t: torch.Tensor, Gs=(1, 2, 3, 5, 8), cap=None, seed=5, use_oracle=Fals
         same(o, o_ref, "node_bbox", n, G)
         _, _, o2 = tb.pair_vshard(tc, bc, G, cap=c, pm=False)
         same(o2, o_ref, "node_bbox (tree_bbox alone)", n, G)
+        m3, p3, _ = tb.pair_vshard(tc, None, G, cap=c)  # the matching alone (paren_match_shard)
+        same(p3, p_ref, "parent (matching alone)", n, G)
+        same(m3, m_ref, "match (matching alone)", n, G)
 
 
 def walk(n, seed, p_leaf=0.5, p_clip=0.75):

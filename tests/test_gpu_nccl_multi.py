@@ -48,11 +48,14 @@ def rank_main():
         ctx.paren_match_tree_bbox(tt, bb, m, p, o, cap=cap)
         ok = (np.array_equal(m.cpu().numpy(), m_ref[lo:hi]) and np.array_equal(p.cpu().numpy(), p_ref[lo:hi])
               and np.array_equal(o.cpu().numpy().view(np.uint32), o_ref[lo:hi]))
-        if cap is None:  # tree_bbox alone (the same protocol without match / parent)
+        if cap is None:  # tree_bbox alone and paren_match alone (the same protocol)
             o2 = torch.empty_like(o)
             ctx.tree_bbox(tt, bb, o2)
+            m2, p2 = torch.empty_like(m), torch.empty_like(p)
+            ctx.paren_match(tt, m2, p2)
             torch.cuda.synchronize()
             ok = ok and np.array_equal(o2.cpu().numpy().view(np.uint32), o_ref[lo:hi])
+            ok = ok and np.array_equal(m2.cpu().numpy(), m_ref[lo:hi]) and np.array_equal(p2.cpu().numpy(), p_ref[lo:hi])
         ctx.close()
         if not ok:
             fails.append(f"{name} rank {rank}/{world}")
