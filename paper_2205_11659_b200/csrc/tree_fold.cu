@@ -151,29 +151,34 @@ __global__ void __launch_bounds__(NT) tf_tile(Params p) {
   // outside the thread (parked in the close's slot until pass 2)
   M P = mid();
   {
-    M stk[K / 2 + 1];
+    // the innermost open in-thread node's product in a register (tp), the
+    // enclosing ones below it (stk, depth d - 1); every element runs the same
+    // predicated sequence: a leaf multiplies P and tp, an open of an in-thread
+    // node pushes, its close pops
+    M stk[K / 2];
+    M tp = mid();
     int d = 0;
 #pragma unroll
     for (int i = 0; i < K; i++) {
-      const int64_t g = gb + i;
-      if ((lm >> i) & 1u) {
-        const M v = s.xs[slot(tid, i)];
-        P = mul(P, v);
-        if (d > 0) stk[d - 1] = mul(stk[d - 1], v);
-      } else if ((om >> i) & 1u) {
-        if (mt[i] >= 0 && mt[i] < gb + K) stk[d++] = mid();  // closed in this thread
-      } else if ((cm >> i) & 1u) {
-        const int64_t o = mt[i];
-        if (o < 0) {
-          s.xs[slot(tid, i)] = mid();  // R3
-        } else if (o >= gb) {
-          const M u = stk[--d];
-          s.xs[slot(tid, i)] = u;
-          s.xs[slot(tid, (int)(o - gb))] = u;
-          if (d > 0) stk[d - 1] = mul(stk[d - 1], u);
-        } else {
-          s.xs[slot(tid, i)] = P;  // the thread prefix before the close (pass 2 completes it)
-        }
+      const bool isl = (lm >> i) & 1u, iso = (om >> i) & 1u, isc = (cm >> i) & 1u;
+      const int64_t o = mt[i];
+      const bool push = iso && o >= 0 && o < gb + K;  // an open closed in this thread
+      const bool pop = isc && o >= gb;                // the close of one
+      const M v = isl ? s.xs[slot(tid, i)] : mid();
+      P = mul(P, v);
+      const M tv = mul(tp, v);
+      if (push) {
+        if (d > 0) stk[d - 1] = tp;
+        d++;
+        tp = mid();
+      } else if (pop) {
+        s.xs[slot(tid, i)] = tv;
+        s.xs[slot(tid, (int)(o - gb))] = tv;
+        d--;
+        tp = d > 0 ? mul(stk[d - 1], tv) : mid();
+      } else {
+        tp = tv;
+        if (isc) s.xs[slot(tid, i)] = o < 0 ? mid() : P;  // R3; or the thread prefix before the close (pass 2)
       }
     }
   }
