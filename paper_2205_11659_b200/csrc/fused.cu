@@ -1438,11 +1438,10 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         float4 o = isB ? cpar : clipped;
         o = isC ? ((isU && par < 0) ? bEMPTY() : acc) : o;
         s.val[si] = o;
-        if (isO) {
-          // the enclosing accumulator: into the close's slot, or rbuf for an open left open
+        {  // an open saves the enclosing accumulator: into its close's slot, or rbuf when left open
           const int k = kq + __popc(Sq & ((1u << jq) - 1u));
           const int di = isUO ? RB0 + min(k, RCAP - 1) * NT + tid : sl(pt);
-          if (!isUO || k < RCAP) s.val[di] = acc;
+          if (isO && (!isUO || k < RCAP)) s.val[di] = acc;
         }
         if ((MBq >> jq) & 1u) s.val[spn] = acc;
         const float4 add = (isL || isMC) ? clipped : bEMPTY();
