@@ -677,7 +677,6 @@ int paren_match_tree_bbox_scene(const uint8_t* d_scene, const float* d_boxes, in
 int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }
 
 int tb_debug_fz_tma(int on) { return tb::fused_set_tma(on); }
-int tb_debug_fz_abl(int mask) { return tb::fused_set_abl(mask); }
 
 int tb_debug_fz_trace(void* dev_buf) {
   tb::fused_set_trace((uint64_t*)dev_buf);

@@ -84,7 +84,6 @@ struct Params {
   int chunk;           // fz_ctrl: tiles per block (multiple of 32)
   uint64_t* trace;     // optional (debug): fz_ctrl phase timestamps, block 0
   int use_tma;         // fz_main: full tiles move their boxes with TMA (tensor maps below)
-  int abl;             // debug (timing experiments only, results wrong): skip phases of fz_main
   // shard mode (fused_shard.cuh; all zero / null on one device): the chunk's
   // first element has global index goff; heights are offset by h0 and the
   // h0 entries below are the imported stack, a virtual slice at vbase
@@ -200,7 +199,6 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.chunk = 32;
   p.trace = nullptr;
   p.use_tma = 0;
-  p.abl = 0;
   p.goff = goff;
   p.h0 = h0;
   p.vbase = (int)(L.ntiles * W);
@@ -1312,14 +1310,10 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   //      the link, TL(t))
   uint32_t xcm = 0;  // closes popping an entry of an earlier tile
   uint32_t icm = 0;  // closes popping an open of an earlier thread of this tile
-#pragma unroll 1
-  for (int rep = 0; rep < ((p.abl & 64) ? 2 : 1); rep++) {
-    xcm = icm = 0;
+  {
     int ref = top_ref, d = 0, prevc = -1;
     uint32_t q = w.ucm;
     const uint32_t needm = w.ext & (w.lm | w.om);
-    if (p.abl & 1) d = a_t;
-    if (p.abl & 32) ref = -1;
     if (d < a_t && ref >= 0) {
       // the owner thread's unmatched-open mask stays in a register; shared
       // memory is read again only when the chain moves to another thread
@@ -1334,7 +1328,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         icm |= 1u << ci;
         s.matchS[mb + ci] = gbase + e;
         s.matchS[mpad(e)] = gtb + ci;
-        if ((seg & needm) && !(p.abl & 8)) s.val[sl(ci)] = isect(s.val[slot_of(e)], s.u.pj.acc[cbf][V]);
+        if (seg & needm) s.val[sl(ci)] = isect(s.val[slot_of(e)], s.u.pj.acc[cbf][V]);
         if (++d >= a_t) break;
         const uint32_t below = uV & ((1u << bp) - 1u);
         if (below) {
@@ -1350,7 +1344,6 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
     }
     // the rest are consecutive entries of the incoming stack (a chain that
     // leaves the tile never returns into it)
-    if (p.abl & 16) d = a_t;
     for (; d < a_t; d++, ref--) {
       const int ci = __ffs(q) - 1;
       q &= q - 1;
@@ -1402,7 +1395,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
     const float4 v15 = s.val[sl(K - 1)];
     if (!u15) s.val[sl(K - 1)] = TL;
 #pragma unroll 1
-    for (int q = 0; q < ((p.abl & 2) ? 0 : K / 4); q++) {
+    for (int q = 0; q < K / 4; q++) {
       // the masks shifted once per group: bit tests below use immediates
       const int i0 = 4 * q;
       const uint32_t Lq = w.lm >> i0, Bq = w.bm >> i0, Oq = w.om >> i0, Cq = w.cm >> i0, Uq = w.ucm >> i0;
@@ -1512,7 +1505,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   //      threads between in H2); otherwise a slice entry: su = R ∪ the threads
   //      after.  Closes of earlier tiles' nodes: the tile prefix before them
   //      into their pop records (fz_close ends them)
-  if (w.S && !(p.abl & 4)) {
+  if (w.S) {
     auto handle = [&](int i, int k, const float4& R) {
       const int mc = s.matchS[mb + i];
       if (mc >= 0) {
@@ -1575,7 +1568,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
 
   // ---- H2. closes of nodes opened in an earlier thread of the tile: add the
   //      threads between; a blend open receives the union
-  for (uint32_t q = (p.abl & 4) ? 0u : icm; q; q &= q - 1) {
+  for (uint32_t q = icm; q; q &= q - 1) {
     const int ci = __ffs(q) - 1;
     const int o = s.matchS[mb + ci] - gbase;
     const int to = o >> LOGK;
@@ -2045,12 +2038,6 @@ static cudaError_t setup() {
 static uint64_t* g_fz_trace = nullptr;  // debug hook (tb_debug_fz_trace)
 void fused_set_trace(uint64_t* dev) { g_fz_trace = dev; }
 static int g_fz_tma = 1;  // debug hook (tb_debug_fz_tma): 0 = the threads copy every tile
-static int g_fz_abl = 0;  // debug hook (tb_debug_fz_abl): phase-skipping timing experiments (wrong results)
-int fused_set_abl(int m) {
-  const int old = g_fz_abl;
-  if (m >= 0) g_fz_abl = m;
-  return old;
-}
 int fused_set_tma(int on) {
   const int old = g_fz_tma;
   if (on >= 0) g_fz_tma = on;
@@ -2109,7 +2096,6 @@ static cudaError_t launch_back(fz::Params& p, const float* leaf_bbox, float* nod
   fz::Maps maps;
   memset(&maps, 0, sizeof maps);
   p.use_tma = g_fz_tma && fz::make_maps(leaf_bbox, node_bbox, p.n, maps) ? 1 : 0;
-  p.abl = g_fz_abl;
   const unsigned g = (unsigned)nt;
   const size_t sm = sizeof(fz::Smem);
   if (p.scene) {
