@@ -1506,14 +1506,13 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   //      after.  Closes of earlier tiles' nodes: the tile prefix before them
   //      into their pop records (fz_close ends them)
   if (w.S) {
-    auto handle = [&](int i, int k, const float4& R) {
+    auto handle = [&](int i, int k, const float4& R) {  // predicated both ways (no branch)
       const int mc = s.matchS[mb + i];
-      if (mc >= 0) {
-        float4& cv = s.val[slot_of(mc - gbase)];
-        cv = unite(cv, R);
-      } else {
-        p.slice_su[base + l_t + k + aT] = unite(R, after);
-      }
+      const bool in_tile = mc >= 0;
+      float4& cv = s.val[slot_of(in_tile ? mc - gbase : 0)];
+      const float4 c0 = cv;
+      if (in_tile) cv = unite(c0, R);
+      if (!in_tile) p.slice_su[base + l_t + k + aT] = unite(R, after);
     };
     if (!ovf) {
       float4 R = acc;  // segment after the top open
