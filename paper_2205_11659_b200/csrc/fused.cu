@@ -1328,7 +1328,10 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         icm |= 1u << ci;
         s.matchS[mb + ci] = gbase + e;
         s.matchS[mpad(e)] = gtb + ci;
-        if (seg & needm) s.val[sl(ci)] = isect(s.val[slot_of(e)], s.u.pj.acc[cbf][V]);
+        {  // the context at depth d (loads unconditional, the store predicated)
+          const float4 cx = isect(s.val[slot_of(e)], s.u.pj.acc[cbf][V]);
+          if (seg & needm) s.val[sl(ci)] = cx;
+        }
         if (++d >= a_t) break;
         const uint32_t below = uV & ((1u << bp) - 1u);
         if (below) {
@@ -1357,7 +1360,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         if (D < INCCAP) {
           rf = s.u.pj.inc_ref[D];
           si = s.u.pj.inc_idx[D];
-          if (seg & needm) cx = isect(s.u.pj.inc_box[D], s.u.pj.inc_tc[D]);
+          cx = isect(s.u.pj.inc_box[D], s.u.pj.inc_tc[D]);
         } else {
           rf = inc_ref(p, s, nruns, H - 1 - D);
           si = __ldg(p.slice_idx + rf);
