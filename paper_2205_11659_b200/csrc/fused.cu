@@ -1461,8 +1461,9 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   const bool ovf = b_t > RCAP;
   float4 tu = acc;
   if (!ovf) {
-#pragma unroll 1
-    for (int k = 0; k < b_t; k++) tu = unite(tu, s.u.rbuf[k][tid]);
+#pragma unroll
+    for (int k = 0; k < RCAP; k++)  // a fixed trip count, predicated (no divergent loop)
+      if (k < b_t) tu = unite(tu, s.u.rbuf[k][tid]);
   } else {
 #pragma unroll 1
     for (int i = 0; i < K; i++)
