@@ -1202,7 +1202,9 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   block_bic_scans<NW>(Bic{a_t, b_t}, s.wtot, ex, sx, tot, false);
   const int r_t = ex.b - ex.a;
   const int l_t = r_t - a_t;
-  for (uint32_t q = w.S; q; q &= q - 1) s.matchS[mb + __ffs(q) - 1] = -1;  // closed by another thread / tile
+#pragma unroll
+  for (int i = 0; i < K; i++)  // closed by another thread / tile (a fixed predicated loop)
+    if ((w.S >> i) & 1u) s.matchS[mb + i] = -1;
   int wl[5];
   lane_windows(l_t, wl);
 #pragma unroll
