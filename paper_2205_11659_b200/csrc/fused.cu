@@ -1149,7 +1149,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   const int tl0 = tid * K;      // tile-local index of the thread's first element
   const int gtb = gbase + tl0;
   const int sb = (tid << 3) | (tid & 7);  // slot(tid, i) = ((i & 8) << 7) | (sb ^ (i & 7))
-  auto sl = [sb](int i) { return (sb ^ (i & 7)) | ((i << 7) & 1024); };
+  auto sl = [sb](int i) { return sb ^ ((i * 129) & 0x407); };  // (i & 7) | (i & 8) << 7, one IMAD + LOP3
   const int mb = mpad(tl0);                  // matchS index of element i = mb + i
 
   // ---- A. loads, register walk -------------------------------------------------
