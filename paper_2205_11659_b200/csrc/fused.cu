@@ -560,6 +560,7 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
     if (act) {
       p.slice_idx[base + pos] = (int)(e | (blend << 31));
       if (!p.nobox) p.slice_box[base + pos] = v;
+      else p.match[e - (uint32_t)p.goff] = -1;  // matching alone: a later tile writes the partner (fz_match E)
     }
   }
 }
@@ -1748,14 +1749,11 @@ __global__ void __launch_bounds__(NT) fz_match(Params p) {
       if (H - 1 - D >= 0) {
         const int rf = D < INCCAP ? s.inc_ref[D] : inc_ref(p, s, nruns, H - 1 - D);
         const int si = D < INCCAP ? s.inc_idx[D] : __ldg(p.slice_idx + rf);
-        if (si != -1) {
+        if (si != -1) {  // the open's match directly (its tile leaves that slot alone; fz_reduce wrote -1)
           gi = si & 0x7fffffff;
-          p.pop[poff + D] = make_int2(gtb + ci, rf);
-        } else {
-          p.pop[poff + D] = make_int2(-1, -1);
+          if (rf >= p.vbase) p.exc[rf - p.vbase] = gtb + ci;  // an imported entry (shard mode)
+          else p.match[gi - p.goff] = gtb + ci;
         }
-      } else {
-        p.pop[poff + D] = make_int2(-1, -1);  // pops the root (R3)
       }
       s.matchS[mb + ci] = gi;
     }
@@ -1789,34 +1787,24 @@ __global__ void __launch_bounds__(NT) fz_match(Params p) {
   }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < W / 4 / NT; j++) {  // match out, coalesced
+  for (int j = 0; j < W / 4 / NT; j++) {  // match out, coalesced; the tile's surviving opens are skipped
     const int e = 4 * (j * NT + tid);
     const int pe = mpad(e);
     const int4 v4 = make_int4(s.matchS[pe], s.matchS[pe + 1], s.matchS[pe + 2], s.matchS[pe + 3]);
-    if (e + 4 <= nvalid) {
+    // survivors: thread-unmatched opens no later thread of the tile closed (matchS still -1)
+    const uint32_t uo4 = (s.uo[e >> LOGK] >> (e & (K - 1))) & 15u;
+    const uint32_t sk = uo4 & ((v4.x < 0 ? 1u : 0u) | (v4.y < 0 ? 2u : 0u) | (v4.z < 0 ? 4u : 0u) | (v4.w < 0 ? 8u : 0u));
+    if (e + 4 <= nvalid && !sk) {
       __stcs(reinterpret_cast<int4*>(p.match + base + e), v4);
     } else {
-      if (e < nvalid) p.match[base + e] = v4.x;
-      if (e + 1 < nvalid) p.match[base + e + 1] = v4.y;
-      if (e + 2 < nvalid) p.match[base + e + 2] = v4.z;
+      if (e < nvalid && !(sk & 1u)) p.match[base + e] = v4.x;
+      if (e + 1 < nvalid && !(sk & 2u)) p.match[base + e + 1] = v4.y;
+      if (e + 2 < nvalid && !(sk & 4u)) p.match[base + e + 2] = v4.z;
+      if (e + 3 < nvalid && !(sk & 8u)) p.match[base + e + 3] = v4.w;
     }
   }
 }
 
-// the opens of earlier tiles popped by this tile's closes: match[open] (one warp per tile)
-__global__ void __launch_bounds__(128) fz_close_m(Params p) {
-  const int lane = threadIdx.x & 31;
-  const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (T >= p.ntiles) return;
-  const int64_t poff = __ldg(p.aoff + T);
-  const int npop = (int)(__ldg(p.aoff + T + 1) - poff);
-  for (int j = lane; j < npop; j += 32) {
-    const int2 r = __ldcg(p.pop + poff + j);
-    if (r.x < 0) continue;
-    if (r.y >= p.vbase) p.exc[r.y - p.vbase] = r.x;  // an imported entry (shard mode): its chunk writes match
-    else p.match[(__ldg(p.slice_idx + r.y) & 0x7fffffff) - p.goff] = r.x;
-  }
-}
 
 // ----------------------------------------------------------------------------
 // fz_hier: level k of the tile-union hierarchy (one warp per group of 32)
@@ -2151,9 +2139,6 @@ static cudaError_t launch_back_match(fz::Params& p, cudaStream_t stream) {
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = dbg_sync(stream, "fz_match");
   if (e != cudaSuccess) return e;
-  TB_LAUNCH(stream, "fz_close", (fz::fz_close_m<<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
-  e = cudaGetLastError();
-  if (e == cudaSuccess) e = dbg_sync(stream, "fz_close_m");
   return e;
 }
 

@@ -261,12 +261,13 @@ static int sh_grid(int64_t work, int per_block) {
 }
 
 cudaError_t fused_shard_phase1(const uint8_t* tags, const float* leaf_bbox, int64_t n, int64_t goff, int cap,
-                               void* ws, void* slot1, cudaStream_t stream) {
+                               int32_t* match, void* ws, void* slot1, cudaStream_t stream) {
   if (n <= 0) return cudaMemsetAsync(slot1, 0, 16, stream);  // header (0, 0): an empty chunk
   cudaError_t e = fz::setup();
   if (e != cudaSuccess) return e;
   const bool nobox = leaf_bbox == nullptr;  // paren_match alone
-  fz::Params p = fz::make_params(tags, leaf_bbox, n, nullptr, nullptr, nullptr, ws, cap, (int)goff, nobox);
+  // (the matching alone: fz_reduce marks the chunk's surviving opens in match)
+  fz::Params p = fz::make_params(tags, leaf_bbox, n, nobox ? match : nullptr, nullptr, nullptr, ws, cap, (int)goff, nobox);
   p.nobox = nobox;
   e = launch_front(p, stream);
   if (e != cudaSuccess) return e;

@@ -79,7 +79,7 @@ size_t fused_shard_workspace_bytes(int64_t n, int cap, bool nobox);  // nobox: m
 size_t fused_shard_slot1_bytes(int cap);
 size_t fused_shard_slot2_bytes(int cap);
 cudaError_t fused_shard_phase1(const uint8_t* tags, const float* leaf_bbox, int64_t n, int64_t goff, int cap,
-                               void* ws, void* slot1, cudaStream_t stream);
+                               int32_t* match, void* ws, void* slot1, cudaStream_t stream);
 cudaError_t fused_shard_phase2(const uint8_t* tags, const float* leaf_bbox, int64_t n, int64_t goff, int cap, int G,
                                int g, int32_t* match, int32_t* parent, float* node_bbox, void* ws, const void* recv1,
                                void* slot2, cudaStream_t stream);

@@ -716,7 +716,7 @@ cudaError_t fz_vshard(const uint8_t* tags, const float* leaf, int64_t n, int G, 
   const size_t s1 = fused_shard_slot1_bytes(cap), s2 = fused_shard_slot2_bytes(cap);
   for (int k = 0; k < G && e == cudaSuccess; k++)
     e = fused_shard_phase1(tags + off(k), leaf ? leaf + 4 * off(k) : nullptr, off(k + 1) - off(k), off(k), cap,
-                           b.ws + wsb * k, b.recv1 + s1 * k, s);
+                           match ? match + off(k) : nullptr, b.ws + wsb * k, b.recv1 + s1 * k, s);
   for (int k = 0; k < G && e == cudaSuccess; k++)
     e = fused_shard_phase2(tags + off(k), leaf ? leaf + 4 * off(k) : nullptr, off(k + 1) - off(k), off(k), cap, G, k,
                            match ? match + off(k) : nullptr, parent ? parent + off(k) : nullptr,
@@ -759,7 +759,7 @@ cudaError_t fz_nccl_shard(const uint8_t* tags, const float* leaf, int64_t n, int
     return !*nccl_err;
   };
   const size_t s1 = fused_shard_slot1_bytes(cap), s2 = fused_shard_slot2_bytes(cap);
-  e = fused_shard_phase1(tags, leaf, n, off, cap, b.ws, b.slot1, s);
+  e = fused_shard_phase1(tags, leaf, n, off, cap, match, b.ws, b.slot1, s);
   if (e != cudaSuccess || !nccl_ok(ncclAllGather(b.slot1, b.recv1, s1, ncclUint8, comm, s))) return e;
   e = fused_shard_phase2(tags, leaf, n, off, cap, G, g, match, parent, out, b.ws, b.recv1, b.slot2, s);
   if (e != cudaSuccess || !nccl_ok(ncclAllGather(b.slot2, b.recv2, s2, ncclUint8, comm, s))) return e;
