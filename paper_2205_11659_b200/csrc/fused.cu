@@ -935,11 +935,10 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
 struct Walk {
   uint32_t om, cm, bm, lm;  // opens, closes, blend opens, leaves (valid elements only)
   uint32_t S;               // opens still on the thread stack at its end (thread-unmatched)
-  uint32_t plo, phi;        // nibble i: in-thread parent of element i
-  uint32_t mlo, mhi;        // nibble i: in-thread partner of element i (matched opens and closes)
+  uint32_t plo, phi;        // nibble i: in-thread parent of element i (a matched close: its open)
+  uint32_t mlo, mhi;        // nibble i: in-thread close of open i (matched opens only)
   uint32_t ext;             // elements whose parent lies before the thread
   uint32_t ucm;             // closes with no in-thread open (they pop the stack at the thread start)
-  uint32_t mcb;             // closes whose (in-thread) open is a blend
 };
 
 // Fig. 1 over the thread's 16 elements with a bitmask stack (four
@@ -951,40 +950,29 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   w.cm &= valid;
   w.bm &= valid;
   w.lm = valid & ~(w.om | w.cm);
-  uint32_t S = 0, plo = 0, phi = 0, mlo = 0, mhi = 0, ext = 0, ucm = 0, mcb = 0;
+  uint32_t S = 0, plo = 0, phi = 0, mlo = 0, mhi = 0, ext = 0;
 #pragma unroll 1
   for (int q = 0; q < K / 4; q++) {
     const int i0 = 4 * q;
     const uint32_t oq = w.om >> i0, cq = w.cm >> i0;  // bit tests below use immediates
-    uint32_t gp = 0, gm = 0, gx = 0, gu = 0, gb = 0;   // the group's nibbles / bits
+    uint32_t gp = 0, gx = 0;                         // the group's nibbles / bits
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       const int i = i0 + j;
       const int top = 31 - __clz(S);  // -1 when the thread stack is empty
       gp |= (uint32_t)(top & 15) << (4 * j);
       gx |= S ? 0u : (1u << j);
-      const bool isc = (cq >> j) & 1u;
-      const bool pop = isc && S;
-      gu |= (isc && !S) ? (1u << j) : 0u;
-      gb |= (pop && ((w.bm >> top) & 1u)) ? (1u << j) : 0u;
-      // partner nibbles: the open's (at the pop) and the close's own
+      const bool pop = ((cq >> j) & 1u) && S;
+      // the open's partner nibble, written at the pop (a close's partner is its parent)
       const uint32_t pv = pop ? (uint32_t)i << (4 * (top & 7)) : 0u;
       mlo |= top < 8 ? pv : 0u;
       mhi |= top >= 8 ? pv : 0u;
-      gm |= pop ? (uint32_t)(top & 15) << (4 * j) : 0u;
       S = ((oq >> j) & 1u) ? (S | (1u << i)) : (pop ? (S ^ (1u << top)) : S);
     }
     const int sh = 16 * (q & 1);
-    if (q < 2) {
-      plo |= gp << sh;
-      mlo |= gm << sh;
-    } else {
-      phi |= gp << sh;
-      mhi |= gm << sh;
-    }
+    if (q < 2) plo |= gp << sh;
+    else phi |= gp << sh;
     ext |= gx << i0;
-    ucm |= gu << i0;
-    mcb |= gb << i0;
   }
   w.S = S;
   w.plo = plo;
@@ -992,8 +980,7 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   w.mlo = mlo;
   w.mhi = mhi;
   w.ext = ext;
-  w.ucm = ucm;
-  w.mcb = mcb;
+  w.ucm = w.cm & ext;  // closes met with an empty thread stack
   return w;
 }
 
@@ -1405,7 +1392,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
       // the masks shifted once per group: bit tests below use immediates
       const int i0 = 4 * q;
       const uint32_t Lq = w.lm >> i0, Bq = w.bm >> i0, Oq = w.om >> i0, Cq = w.cm >> i0, Uq = w.ucm >> i0;
-      const uint32_t Sq = w.S >> i0, Xq = w.ext >> i0, MBq = w.mcb >> i0;
+      const uint32_t Sq = w.S >> i0, Xq = w.ext >> i0;
       const uint32_t pwq = (q < 2 ? w.plo : w.phi) >> (16 * (q & 1)), mwq = (q < 2 ? w.mlo : w.mhi) >> (16 * (q & 1));
       const int kq = __popc(w.S & ((1u << i0) - 1u));      // thread-unmatched opens before the group
       const int sbq = ((q >> 1) << 10) | (sb ^ ((q & 1) << 2));  // slot of element i0 + jq = sbq ^ jq
@@ -1421,7 +1408,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         float4 v = s.val[si];
         if (jq == 3 && q == K / 4 - 1 && !isMC) v = v15;
         const int pn = (int)((pwq >> (4 * jq)) & 15u);
-        const int pt = (int)((mwq >> (4 * jq)) & 15u);
+        const int pt = isC ? pn : (int)((mwq >> (4 * jq)) & 15u);  // a close's partner is its parent
         const bool isx = (Xq >> jq) & 1u;
         const uint32_t nc = Uq >> jq;                        // unmatched closes at or after i
         const int j = nc ? i + __ffs(nc) - 1 : K - 1;        // the next one: c_d of element i's depth d (none: TL)
@@ -1442,7 +1429,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
           const int di = isUO ? RB0 + min(k, RCAP - 1) * NT + tid : sl(pt);
           if (isO && (!isUO || k < RCAP)) s.val[di] = acc;
         }
-        if ((MBq >> jq) & 1u) s.val[spn] = acc;
+        if (isMC && ((w.bm >> pn) & 1u)) s.val[spn] = acc;  // the close of an in-thread blend open
         const float4 add = (isL || isMC) ? clipped : bEMPTY();
         acc = unite(acc, add);
         acc = isO ? bEMPTY() : acc;
@@ -1771,7 +1758,7 @@ __global__ void __launch_bounds__(NT) fz_match(Params p) {
       const int i = i0 + jq;
       const bool isL = (Lq >> jq) & 1u, isU = (Uq >> jq) & 1u, isUO = (Sq >> jq) & 1u, isx = (Xq >> jq) & 1u;
       const int pn = (int)((pwq >> (4 * jq)) & 15u);
-      const int pt = (int)((mwq >> (4 * jq)) & 15u);
+      const int pt = ((w.cm >> i) & 1u) ? pn : (int)((mwq >> (4 * jq)) & 15u);  // a close's partner is its parent
       const uint32_t nc = Uq >> jq;
       const int j = nc ? i + __ffs(nc) - 1 : K - 1;
       pv[jq] = isx ? (nc ? s.matchS[mb + j] : giLast) : gtb + pn;
