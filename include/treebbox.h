@@ -86,18 +86,23 @@ int tb_release_workspaces(void);
  * d_match  : device int32[n] out.  Classical partner: matched opens and
  *            closes point at each other; leaves, opens never closed (R4) and
  *            closes with nothing to close (R3) get -1.
- * Computation: a reduce pass over the tags (each 4096-element tile's value
- * in the bicyclic monoid, and its stack slice), a scan of
- * the tile values (one CTA: start heights, low-water marks and their 32-ary
- * min hierarchy) and a finish pass (in-tile resolution, cross-tile lookup by
- * the suffix relation).  HBM traffic ~10 bytes/element (+ slices).
+ * Computation (the fused machinery without boxes, csrc/fused.cu): a reduce
+ * pass over the tags (each 2048-element tile's value in the bicyclic monoid,
+ * P:96-102, and its stack slice; the tile's surviving opens get
+ * match -1), a cooperative control kernel (the scan of the tile values,
+ * low-water marks and their 32-ary min hierarchy, link owners and incoming
+ * runs) and the matching pass (in-tile resolution, cross-tile lookup by the
+ * owner rule = the suffix relation; the closes of earlier tiles'
+ * opens write those opens' match).  HBM traffic ~10 bytes/element (+ slices).
  * ------------------------------------------------------------------------ */
 int paren_match(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *d_parent,
                 void *stream);
 
 size_t paren_match_workspace_bytes(int64_t n);
-/* d_workspace: device scratch of >= paren_match_workspace_bytes(n) bytes,
- * 256-byte aligned, not used concurrently by another call. */
+/* With caller workspace: round 1's three passes (a reduce over 4096-element
+ * tiles, a one-CTA scan of the tile values, a finish pass; csrc/paren_match.cu),
+ * same outputs.  d_workspace: device scratch of >= paren_match_workspace_bytes(n)
+ * bytes, 256-byte aligned, not used concurrently by another call. */
 int paren_match_ws(const uint8_t *d_tags, int64_t n, int32_t *d_match, int32_t *d_parent,
                    void *d_workspace, size_t workspace_bytes, void *stream);
 
@@ -134,7 +139,7 @@ int paren_match_bytes(const uint8_t *d_bytes, int64_t n, const uint8_t *h_class_
  * canonicalised (R9).
  * The matching structure is re-derived inside the same tile pass that
  * computes the boxes (the fused pass of paren_match_tree_bbox, without its
- * match / parent stores): ~34 bytes/element of HBM traffic (+ slices).
+ * match / parent stores): ~36 bytes/element of HBM traffic (+ slices).
  * ------------------------------------------------------------------------ */
 int tree_bbox(const uint8_t *d_tags, const float *d_leaf_bbox, int64_t n, float *d_node_bbox,
               void *stream);
