@@ -96,9 +96,10 @@ struct Params {
   float4* exu;         // [h0] shard: its union over this chunk (the prefix before the close)
   // scene mode (stream compaction fused into the loaders):
   // the passes run on the COMPACTED stream -- tile T holds kept elements
-  // [T W, T W + W) -- whose tags and full-stream indices fz_reduce writes while
-  // it compacts; fz_main gathers the boxes through those indices.  n / ntiles
-  // are the full stream's (capacity); the kept count is on the device.
+  // [T W, T W + W) -- whose tags and full-stream indices sc_compact writes (two
+  // of the outputs); fz_reduce / fz_main gather the boxes through those
+  // indices, so no box is compacted over HBM.  n / ntiles are the full
+  // stream's (capacity); the kept count is on the device.
   int nobox;              // matching only (fused_match_launch): no boxes, no contexts, no unions
   int scene;
   int keep03;              // the keep table is bytes 0-3 exactly (a compare)
@@ -106,7 +107,6 @@ struct Params {
   int64_t* nkp;            // the kept count
   const uint8_t* tags_in;  // the full stream
   const float4* boxes_in;  // its boxes
-  int64_t* tin;            // [ntiles + 1] full-stream index of kept element T W (n past the last)
   int32_t* kcin;           // [ntiles] kept elements per full-stream tile
   int64_t* kpin;           // [ntiles + 1] their exclusive prefix
   uint8_t* tags_out;       // [n] the compacted tags
@@ -128,7 +128,7 @@ constexpr int RMAX = 8;        // runs of the incoming stack kept per tile (more
 // ----------------------------------------------------------------------------
 struct Layout {
   size_t ctrl, aoff, sidx, sbox, ssu, pop, tu[LV], pja, pjp, pjo, tcs, rns, nrs, flag, blk, blkmin, shd, tce, kpw, nk,
-      tin, kci, kpi, bytes;
+      kci, kpi, bytes;
   int64_t ntiles;
   explicit Layout(int64_t n, int h0 = 0, bool nobox = false) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -161,7 +161,6 @@ struct Layout {
     tce = o; o = al(o + 4 * (size_t)ntiles);
     kpw = o; o = al(o + 32);
     nk = o; o = al(o + 8);
-    tin = o; o = al(o + 8 * ((size_t)ntiles + 1));
     kci = o; o = al(o + 4 * (size_t)ntiles);
     kpi = o; o = al(o + 8 * ((size_t)ntiles + 1));
     bytes = o;
@@ -213,7 +212,6 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.nkp = (int64_t*)(b + L.nk);
   p.tags_in = nullptr;
   p.boxes_in = nullptr;
-  p.tin = (int64_t*)(b + L.tin);
   p.kcin = (int32_t*)(b + L.kci);
   p.kpin = (int64_t*)(b + L.kpi);
   p.tags_out = nullptr;
@@ -326,52 +324,56 @@ __global__ void __launch_bounds__(1024) sc_scan3(Params p, const long long* bsum
   const int u = blockIdx.x * 1024 + threadIdx.x;
   if (u < p.ntiles) p.kpin[u] += bsum[blockIdx.x];
 }
-// tin[j] = full-stream index of kept element j W (n when j W >= the kept
-// count): the full-stream tile holding it (binary search of the prefix), then
-// its rank inside that tile (one warp per compacted tile)
-__global__ void __launch_bounds__(256) sc_ranges(Params p) {
+// the kept elements' tags and full-stream indices at their compacted positions
+// (one warp per full-stream tile from its prefix kpin; 32 consecutive elements
+// per ballot step -- coalesced stores -- with 16 bytes per lane per load
+// handed across by shuffles)
+__global__ void __launch_bounds__(256) sc_compact(Params p) {
   const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (j > p.ntiles) return;
-  const int64_t q = (int64_t)j * W, nk = __ldcg(p.nkp);
-  if (q >= nk) {
-    if (lane == 0) p.tin[j] = p.n;
-    return;
-  }
-  int lo = 0, hi = p.ntiles - 1;  // the last tile u with kpin[u] <= q
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldcg(p.kpin + mid) <= q) lo = mid;
-    else hi = mid - 1;
-  }
-  const int r = (int)(q - __ldcg(p.kpin + lo));
-  const uint64_t m = keep64(p, (int64_t)lo * W + 64 * lane);
-  const int c = __popcll(m);
-  int incl = c;
+  const int u = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (u >= p.ntiles) return;
+  const int64_t base = (int64_t)u * W;
+  int64_t co = __ldcg(p.kpin + u);
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t kt[8];
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += y;
-  }
-  const int ex = incl - c;
-  if (r >= ex && r < incl) {
-    const uint32_t lo32 = (uint32_t)m, hi32 = (uint32_t)(m >> 32);
-    const int k = r - ex, c0 = __popc(lo32);
-    int pos;
-    {
-      // select the k-th set bit of the lane's 64
-      uint32_t mm = k < c0 ? lo32 : hi32;
-      int kk = k < c0 ? k : k - c0, b = k < c0 ? 0 : 32;
-      for (int t = 0; t < kk; t++) mm &= mm - 1;
-      pos = b + __ffs(mm) - 1;
+  for (int i = 0; i < 8; i++) kt[i] = __ldg(p.keepw + i);
+  for (int c0 = 0; c0 < W && base + c0 < p.n; c0 += 512) {
+    const int64_t g16 = base + c0 + 16 * lane;
+    const uint4 raw = g16 + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags_in + g16))
+                                      : load_tags16(p.tags_in, p.n, g16, false);
+    const int bi = lane & 15;
+#pragma unroll
+    for (int b = 0; b < 16; b++) {
+      const int src = 2 * b + (lane >> 4);
+      const uint32_t w0 = __shfl_sync(0xffffffffu, raw.x, src), w1 = __shfl_sync(0xffffffffu, raw.y, src);
+      const uint32_t w2 = __shfl_sync(0xffffffffu, raw.z, src), w3 = __shfl_sync(0xffffffffu, raw.w, src);
+      const uint32_t wv = (bi & 8) ? ((bi & 4) ? w3 : w2) : ((bi & 4) ? w1 : w0);
+      const uint32_t byte = (wv >> (8 * (bi & 3))) & 255u;
+      const int64_t g = base + c0 + 32 * b + lane;
+      bool kept;
+      if (p.keep03) {
+        kept = byte < 4u;
+      } else {
+        uint32_t kw = kt[0];
+#pragma unroll
+        for (int i = 1; i < 8; i++) kw = (byte >> 5) == (uint32_t)i ? kt[i] : kw;
+        kept = (kw >> (byte & 31)) & 1u;
+      }
+      kept = kept && g < p.n;
+      const uint32_t bal = __ballot_sync(0xffffffffu, kept);
+      if (kept) {
+        const int64_t k = co + __popc(bal & lt);
+        p.tags_out[k] = (uint8_t)byte;
+        p.index_out[k] = (int32_t)g;
+      }
+      co += __popc(bal);
     }
-    p.tin[j] = (int64_t)lo * W + 64 * lane + pos;
   }
 }
 
 constexpr int RL = W / 32;  // 64 elements per lane
 // scene mode: per warp, the compacted tile's tags and full-stream indices
-constexpr size_t SC_WARP_BYTES = W;
 
 template <bool SC>
 __global__ void __launch_bounds__(256) fz_reduce(Params p) {
@@ -391,62 +393,12 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
   const int T = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (T >= p.ntiles) return;
   const int64_t base = (int64_t)T * W, lbase = base + (int64_t)lane * RL;
-  uint8_t* ctag = nullptr;  // scene mode: the compacted tile (zero padded: leaves)
-  if (SC) {
-    extern __shared__ __align__(16) unsigned char sc_smem[];
-    ctag = sc_smem + (threadIdx.x >> 5) * SC_WARP_BYTES;
-    const int64_t nk = __ldcg(p.nkp);
-    const int len = (int)(nk - base < 0 ? 0 : (nk - base < W ? nk - base : W));
-    if (len == 0) {  // past the compacted stream: an empty tile
-      if (lane == 0) p.ctrl.agg[T] = make_int2(0, 0);
-      return;
-    }
-    // compact the full-stream range [tin[T], tin[T + 1]) -- exactly len kept
-    // elements -- 32 consecutive elements per step (one per lane, ballot
-    // ranks: consecutive shared-memory slots, no bank conflicts)
-    // (16 bytes per lane per load; sub-step b hands lane l the byte of element
-    // c0 + 32 b + l through shuffles)
-    const int64_t a = __ldcg(p.tin + T);
-    int co = 0;
-    const uint32_t lt = (1u << lane) - 1u;
-    uint32_t kt[8];
-#pragma unroll
-    for (int i = 0; i < 8; i++) kt[i] = __ldg(p.keepw + i);
-    for (int64_t c0 = a & ~int64_t(15); co < len; c0 += 512) {
-      const int64_t g16 = c0 + 16 * lane;
-      const uint4 raw = g16 + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags_in + g16))
-                                        : load_tags16(p.tags_in, p.n, g16, false);
-      const int bi = lane & 15;
-#pragma unroll
-      for (int b = 0; b < 16; b++) {
-        const int src = 2 * b + (lane >> 4);
-        const uint32_t w0 = __shfl_sync(0xffffffffu, raw.x, src), w1 = __shfl_sync(0xffffffffu, raw.y, src);
-        const uint32_t w2 = __shfl_sync(0xffffffffu, raw.z, src), w3 = __shfl_sync(0xffffffffu, raw.w, src);
-        const uint32_t wv = (bi & 8) ? ((bi & 4) ? w3 : w2) : ((bi & 4) ? w1 : w0);
-        const uint32_t byte = (wv >> (8 * (bi & 3))) & 255u;
-        const int64_t g = c0 + 32 * b + lane;
-        bool kept;
-        if (p.keep03) {
-          kept = byte < 4u;
-        } else {
-          uint32_t kw = kt[0];
-#pragma unroll
-          for (int i = 1; i < 8; i++) kw = (byte >> 5) == (uint32_t)i ? kt[i] : kw;
-          kept = (kw >> (byte & 31)) & 1u;
-        }
-        kept = kept && g >= a && g < p.n;
-        const uint32_t bal = __ballot_sync(0xffffffffu, kept);
-        const int k = co + __popc(bal & lt);
-        if (kept && k < len) {
-          ctag[k] = (uint8_t)byte;
-          p.tags_out[base + k] = (uint8_t)byte;
-          p.index_out[base + k] = (int32_t)g;
-        }
-        co += __popc(bal);
-      }
-    }
-    for (int e = len + lane; e < W; e += 32) ctag[e] = 0;
-    __syncwarp();  // ctag and this warp's index_out writes are visible to the warp
+  // scene mode: the compacted stream (tags_out, written by sc_compact); its
+  // length is on the device, tiles past it are empty
+  const int64_t nn = SC ? __ldcg(p.nkp) : p.n;
+  if (SC && base >= nn) {
+    if (lane == 0) p.ctrl.agg[T] = make_int2(0, 0);
+    return;
   }
   uint32_t om[2], cm[2], bk[2];
   {
@@ -454,10 +406,7 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       const int64_t g = lbase + 16 * q;
-      if (SC)
-        raw[q] = *reinterpret_cast<const uint4*>(ctag + lane * RL + 16 * q);
-      else
-        raw[q] = g + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags + g)) : load_tags16(p.tags, p.n, g, false);
+      raw[q] = g + 16 <= nn ? __ldg(reinterpret_cast<const uint4*>(p.tags + g)) : load_tags16(p.tags, nn, g, false);
     }
 #pragma unroll
     for (int q = 0; q < 4; q++) {
@@ -546,7 +495,7 @@ __global__ void __launch_bounds__(256) fz_reduce(Params p) {
       const int j = k < c0 ? select_bit32(o0, k) : 32 + select_bit32(o1, k - c0);
       blend = ((j < 32 ? b0 : b1) >> (j & 31)) & 1u;
       e = (uint32_t)(base + L * RL + j);
-      if (!blend && !p.nobox) v = SC ? __ldg(p.boxes_in + __ldcg(p.index_out + e)) : __ldg(p.boxes + e);
+      if (!blend && !p.nobox) v = SC ? __ldg(p.boxes_in + __ldg(p.index_out + e)) : __ldg(p.boxes + e);
       e += (uint32_t)p.goff;
     }
 #pragma unroll
@@ -2002,8 +1951,6 @@ static cudaError_t setup() {
       if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fz_reduce<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * SC_WARP_BYTES));
-    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(fz_match, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemM));
     uint8_t tab[UNM4_ENTRIES];
     for (int i = 0; i < UNM4_ENTRIES; i++) tab[i] = unm4_entry(i);
@@ -2048,9 +1995,8 @@ static cudaError_t launch_front(fz::Params& p, cudaStream_t stream) {
     TB_LAUNCH(stream, "sc_scan", (fz::sc_scan1<<<nb, 1024, 0, stream>>>(p, bsum)));
     TB_LAUNCH(stream, "sc_scan", (fz::sc_scan2<<<1, 1024, 0, stream>>>(p, bsum, nb)));
     TB_LAUNCH(stream, "sc_scan", (fz::sc_scan3<<<nb, 1024, 0, stream>>>(p, bsum)));
-    TB_LAUNCH(stream, "sc_ranges", (fz::sc_ranges<<<(unsigned)((nt + 1 + 7) / 8), 256, 0, stream>>>(p)));
-    TB_LAUNCH(stream, "fz_reduce",
-              (fz::fz_reduce<true><<<(unsigned)((nt + 7) / 8), 256, 8 * fz::SC_WARP_BYTES, stream>>>(p)));
+    TB_LAUNCH(stream, "sc_compact", (fz::sc_compact<<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
+    TB_LAUNCH(stream, "fz_reduce", (fz::fz_reduce<true><<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
   } else {
     TB_LAUNCH(stream, "fz_reduce", (fz::fz_reduce<false><<<(unsigned)((nt + 7) / 8), 256, 0, stream>>>(p)));
   }
@@ -2150,7 +2096,7 @@ cudaError_t fused_scene_launch(const uint8_t* tags, const float* boxes, int64_t 
   if (n <= 0) return cudaMemsetAsync(d_n_out, 0, sizeof(int64_t), stream);
   cudaError_t e = fz::setup();
   if (e != cudaSuccess) return e;
-  fz::Params p = fz::make_params(nullptr, boxes, n, match, parent, node_bbox, ws);
+  fz::Params p = fz::make_params(tags_out, boxes, n, match, parent, node_bbox, ws);  // the passes read the compacted tags
   p.scene = 1;
   p.tags_in = tags;
   p.boxes_in = (const float4*)boxes;
@@ -2164,7 +2110,6 @@ cudaError_t fused_scene_launch(const uint8_t* tags, const float* boxes, int64_t 
   if (e == cudaSuccess) e = launch_front(p, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_n_out, p.nkp, sizeof(int64_t), cudaMemcpyDeviceToDevice, stream);
   if (e != cudaSuccess) return e;
-  p.tags = tags_out;  // the main pass reads the compacted tags
   return launch_back(p, boxes, node_bbox, match != nullptr, stream);
 }
 
