@@ -326,8 +326,7 @@ __global__ void __launch_bounds__(1024) sc_scan3(Params p, const long long* bsum
 }
 // the kept elements' tags and full-stream indices at their compacted positions
 // (one warp per full-stream tile from its prefix kpin; 32 consecutive elements
-// per ballot step -- coalesced stores -- with 16 bytes per lane per load
-// handed across by shuffles)
+// per ballot step -- coalesced loads and stores)
 __global__ void __launch_bounds__(256) sc_compact(Params p) {
   const int lane = threadIdx.x & 31;
   const int u = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -339,17 +338,15 @@ __global__ void __launch_bounds__(256) sc_compact(Params p) {
 #pragma unroll
   for (int i = 0; i < 8; i++) kt[i] = __ldg(p.keepw + i);
   for (int c0 = 0; c0 < W && base + c0 < p.n; c0 += 512) {
-    const int64_t g16 = base + c0 + 16 * lane;
-    const uint4 raw = g16 + 16 <= p.n ? __ldg(reinterpret_cast<const uint4*>(p.tags_in + g16))
-                                      : load_tags16(p.tags_in, p.n, g16, false);
-    const int bi = lane & 15;
+    uint32_t bytes[16];  // 16 coalesced byte loads in flight: lane l takes element c0 + 32 b + l
 #pragma unroll
     for (int b = 0; b < 16; b++) {
-      const int src = 2 * b + (lane >> 4);
-      const uint32_t w0 = __shfl_sync(0xffffffffu, raw.x, src), w1 = __shfl_sync(0xffffffffu, raw.y, src);
-      const uint32_t w2 = __shfl_sync(0xffffffffu, raw.z, src), w3 = __shfl_sync(0xffffffffu, raw.w, src);
-      const uint32_t wv = (bi & 8) ? ((bi & 4) ? w3 : w2) : ((bi & 4) ? w1 : w0);
-      const uint32_t byte = (wv >> (8 * (bi & 3))) & 255u;
+      const int64_t g = base + c0 + 32 * b + lane;
+      bytes[b] = g < p.n ? (uint32_t)__ldg(p.tags_in + g) : 255u;
+    }
+#pragma unroll
+    for (int b = 0; b < 16; b++) {
+      const uint32_t byte = bytes[b];
       const int64_t g = base + c0 + 32 * b + lane;
       bool kept;
       if (p.keep03) {
