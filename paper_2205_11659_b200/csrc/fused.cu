@@ -250,6 +250,12 @@ __device__ __forceinline__ uint32_t keep16(const uint32_t* keepw, uint4 raw) {
   }
   return m;
 }
+// bytes < 4 of 16 (the hierarchy tags; keep03): bit 6 of ((x >> 2) & 0x3f) + 0x3f
+// per byte is set iff x >= 4, gathered by one multiply per 8 bytes
+__device__ __forceinline__ uint32_t lt4_16(uint4 raw) {
+  auto hi4 = [](uint32_t x) { return ((((x >> 2) & 0x3f3f3f3fu) + 0x3f3f3f3fu) >> 6) & 0x01010101u; };
+  return ~top_bytes(gather8(hi4(raw.x), hi4(raw.y)), gather8(hi4(raw.z), hi4(raw.w))) & 0xffffu;
+}
 // keep mask of the 64 full-stream elements [g, g + 64) (bits past n clear)
 __device__ __forceinline__ uint64_t keep64(const Params& p, int64_t g) {
   uint64_t m = 0;
@@ -261,7 +267,7 @@ __device__ __forceinline__ uint64_t keep64(const Params& p, int64_t g) {
                                      : load_tags16(p.tags_in, p.n, h, false);
     const int64_t rem = p.n - h;
     const uint32_t v = rem >= 16 ? 0xffffu : ((1u << rem) - 1u);
-    m |= (uint64_t)(keep16(p.keepw, raw) & v) << (16 * q);
+    m |= (uint64_t)((p.keep03 ? lt4_16(raw) : keep16(p.keepw, raw)) & v) << (16 * q);
   }
   return m;
 }
@@ -632,7 +638,8 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   __shared__ int nun;
   __shared__ int unres[CMAX];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nt = p.ntiles, G = gridDim.x, bx = blockIdx.x;
+  // (scene mode: only the tiles of the compacted stream, whose length is on the device)
+  const int nt = p.scene ? (int)((__ldcg(p.nkp) + W - 1) / W) : p.ntiles, G = gridDim.x, bx = blockIdx.x;
   const int C = p.chunk;  // tiles per block, a multiple of 32 (level-1 groups stay inside a block)
   const int t0 = min(bx * C, nt), t1 = min(t0 + C, nt);
   const int per = (C + NTC - 1) / NTC;
@@ -1820,7 +1827,7 @@ template <bool PM>
 __global__ void __launch_bounds__(128) fz_close(Params p) {
   const int lane = threadIdx.x & 31;
   const int T = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (T >= p.ntiles) return;
+  if (T >= (p.scene ? (int)((__ldg(p.nkp) + W - 1) / W) : p.ntiles)) return;  // scene: past the compacted stream
   const int64_t poff = __ldg(p.aoff + T);
   const int npop = (int)(__ldg(p.aoff + T + 1) - poff);
   const int bT = __ldg(p.ctrl.agg + T).y;
