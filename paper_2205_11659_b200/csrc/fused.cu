@@ -11,24 +11,28 @@
 //              tile's unmatched opens): the tile's Bic value (§3) and
 //              its stack slice (§7.1: unmatched opens, ascending)
 //              with each entry's tile-local cumulative clip lc.
-//   tile_scan  start heights H_T, low-water marks L_T, the 32-ary low-water
-//              hierarchy (owner rule F1), offsets of the incoming lists.
-//   fz_ctrl    (cooperative) per tile: TC(T) = context of the stack entry just
-//              below its slice, by pointer jumping over tiles (F3 at tile
-//              level; replaces the paper's scan of partition top boxes,
-//              P:292); slice contexts lc ∩ TC; the tile's incoming list = the
-//              a_T + 1 top entries of the stack at its start (owner rule F1
-//              over the published slices = the suffix relation of P:131-138).
+//   fz_ctrl    (cooperative, one CTA per SM) the tile scan: start heights H_T,
+//              low-water marks L_T and their 32-ary hierarchy (owner rule F1),
+//              pop offsets; each tile's link owner and incoming stack as runs
+//              of one owner tile (the suffix relation of P:131-138); TC(T) =
+//              the context of the stack entry just below its slice, by
+//              pointer jumping over tiles (F11; replaces the paper's scan of
+//              partition top boxes).
 //   fz_main    one CTA per tile: register walk (Fig. 1 per thread), block Bic
 //              scan, thread-level owner lookups (F2), thread link contexts by
-//              pointer jumping over threads, one forward walk that clips,
-//              unions and emits parent/match, a backward walk for the unions
-//              of opens closed in a later thread or tile; coalesced copy-out.
-//   fz_hier    32-ary hierarchy of tile unions (one launch: the last block builds the upper levels).
+//              pointer jumping over threads, the start stacks' pops, one
+//              forward walk that clips, unions and emits parent/match, the
+//              suffix unions of opens closed in a later thread or tile, the
+//              cross-thread closes; TMA in and out.
+//   fz_hier    32-ary hierarchy of tile unions (one launch: the last block
+//              builds the upper levels).
 //   fz_close   closes of nodes opened in an earlier tile: tile prefix ∪ the
 //              open's tile suffix ∪ the whole tiles between (F4/F7); blend
 //              opens and match[open] receive the result; blend opens never
 //              closed (R4) get the union of everything after them.
+// Variants of the same kernels: the matching alone (fz_match, no boxes);
+// scene mode (sc_count / sc_scan / sc_compact in front: the passes run on the
+// compacted stream); shard mode (fused_shard.cuh: the imported stack above h0).
 #include <algorithm>
 #include <climits>
 #include <cstddef>
