@@ -465,6 +465,22 @@ def main():
                "api": ("paren_match_tree_bbox_host (pinned host buffers)" if shard is None else
                        "pinned H2D + ShardContext.paren_match_tree_bbox + D2H")}
 
+    # --- launch-bound configs (§8(d)): the same step replayed from a CUDA graph
+    graph = None
+    if shard is None and n <= (1 << 22):
+        s2 = torch.cuda.Stream(dev)
+        with torch.cuda.stream(s2):
+            for _ in range(3):
+                step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s2):
+            step()
+        torch.cuda.synchronize()
+        k = max(args.steps, 20)
+        gms = timed(g.replay, k) / k
+        graph = {"ms_per_step": gms, "value": n / (gms / 1e3) / 1e9, "unit": UNIT, "steps": k}
+
     # --- oracle on the host (rank 0, N = 1 only): one pinned thread, median of 3
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -485,6 +501,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
+            "graph": graph,
             "pair_bytes_per_elem": BYTES_PAIR,
             "pair_hbm_frac": BYTES_PAIR * n * world / (ms_per_step / 1e3) / 1e9 / (peak * world),
             "pair_frac_of_8TBs": BYTES_PAIR * n * world / (ms_per_step / 1e3) / 1e9 / (NOMINAL_GBS * world),
