@@ -105,6 +105,7 @@ struct Params {
   // indices, so no box is compacted over HBM.  n / ntiles are the full
   // stream's (capacity); the kept count is on the device.
   int nobox;              // matching only (fused_match_launch): no boxes, no contexts, no unions
+  int pf_tiles;           // fz_main: resident CTAs on the device (the L2 prefetch distance in tiles)
   int scene;
   int keep03;              // the keep table is bytes 0-3 exactly (a compare)
   const uint32_t* keepw;   // [8] 256-bit keep table
@@ -210,6 +211,7 @@ static Params make_params(const uint8_t* tags, const float* boxes, int64_t n, in
   p.exc = nullptr;
   p.exu = nullptr;
   p.nobox = 0;
+  p.pf_tiles = 0;
   p.scene = 0;
   p.keep03 = 0;
   p.keepw = (const uint32_t*)(b + L.kpw);
@@ -1099,6 +1101,10 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
 
   // ---- A. loads, register walk -------------------------------------------------
   const uint4 raw = load_tags16(p.tags, nn, base + tl0, nvalid == W);
+  if (tid < W / 128) {  // the tags of the tile that will take this CTA's place (about one residency later) into L2
+    const int64_t pf = base + (int64_t)p.pf_tiles * W + tid * 128;
+    if (pf < nn) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.tags + pf));
+  }
   const int H = __ldg(p.ctrl.hstart + T);
   const int aT = __ldg(p.ctrl.agg + T).x;
   const int64_t poff = __ldg(p.aoff + T);  // pop records of this tile: [poff, poff + a_T)
@@ -1942,6 +1948,19 @@ static bool make_maps(const float* boxes, float* out, int64_t n, Maps& m) {
   return true;
 }
 
+static int main_ctas() {  // resident CTAs of fz_main on the device (4 per SM: shared memory)
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& c = cache[dev & 63];
+  if (c == 0) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fz_main<true, false>, NT, sizeof(Smem));
+    c = sm_count() * std::max(occ, 1);
+  }
+  return c;
+}
+
 static int ctrl_blocks() {  // co-resident CTAs of the cooperative kernel
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
@@ -2030,6 +2049,7 @@ static cudaError_t launch_back(fz::Params& p, const float* leaf_bbox, float* nod
   fz::Maps maps;
   memset(&maps, 0, sizeof maps);
   p.use_tma = g_fz_tma && fz::make_maps(leaf_bbox, node_bbox, p.n, maps) ? 1 : 0;
+  p.pf_tiles = fz::main_ctas();
   const unsigned g = (unsigned)nt;
   const size_t sm = sizeof(fz::Smem);
   if (p.scene) {
