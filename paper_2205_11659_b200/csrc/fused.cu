@@ -1272,6 +1272,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
       // memory is read again only when the chain moves to another thread
       int V = ref >> LOGK, bp = ref & (K - 1);
       uint32_t uV = s.u.pj.uo[V];
+      float4 tV = s.u.pj.acc[cbf][V];
       while (true) {
         const int e = (V << LOGK) | bp;  // the entry at depth d: a tile-local open
         const int ci = __ffs(q) - 1;
@@ -1282,7 +1283,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         s.matchS[mb + ci] = gbase + e;
         s.matchS[mpad(e)] = gtb + ci;
         {  // the context at depth d (loads unconditional, the store predicated)
-          const float4 cx = isect(s.val[slot_of(e)], s.u.pj.acc[cbf][V]);
+          const float4 cx = isect(s.val[slot_of(e)], tV);
           if (seg & needm) s.val[sl(ci)] = cx;
         }
         if (++d >= a_t) break;
@@ -1295,6 +1296,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
           V = ref >> LOGK;
           bp = ref & (K - 1);
           uV = s.u.pj.uo[V];
+          tV = s.u.pj.acc[cbf][V];
         }
       }
     }
