@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Agg sh[NWC];
   __shared__ int shm[NWC];
-  __shared__ int mw[CLOG][CMAX];  // ANSV windows over the chunk (levels >= 1)
+  __shared__ __align__(16) int mw[CLOG][CMAX];  // ANSV windows over the chunk (levels >= 1); then P3's local jumps
   __shared__ int nun;
   __shared__ int unres[CMAX];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -822,6 +822,43 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
         p.pj_ptr[T] = U >= 0 || L < 1 ? U : -2 - (L - 1);
         p.pj_own[T] = U;
       }
+    }
+  }
+  if (local && !p.nobox) {
+    // pointer jumping inside the chunk first (block barriers, shared memory):
+    // the grid rounds of P4 then only follow pointers that leave the chunk
+    static_assert(sizeof(mw) >= 2 * CMAX * (sizeof(float4) + sizeof(int)), "local jump buffers");
+    float4* la = reinterpret_cast<float4*>(&mw[0][0]);
+    int* lp = reinterpret_cast<int*>(la + 2 * CMAX);
+    const int cn = t1 - t0;
+    __syncthreads();  // the chunk's pj values (this block's global writes) and mw dead
+    int more = 0;
+    for (int i = tid; i < cn; i += NTC) {
+      la[i] = __ldcg(p.pj_acc + t0 + i);
+      lp[i] = __ldcg(p.pj_ptr + t0 + i);
+      more |= lp[i] >= t0;
+    }
+    int cb = 0;
+    bool any = __syncthreads_or(more);
+    while (any) {
+      more = 0;
+      for (int i = tid; i < cn; i += NTC) {
+        float4 a = la[cb * CMAX + i];
+        int q = lp[cb * CMAX + i];
+        if (q >= t0) {
+          a = isect(a, la[cb * CMAX + q - t0]);
+          q = lp[cb * CMAX + q - t0];
+          more |= q >= t0;
+        }
+        la[(cb ^ 1) * CMAX + i] = a;
+        lp[(cb ^ 1) * CMAX + i] = q;
+      }
+      cb ^= 1;
+      any = __syncthreads_or(more);
+    }
+    for (int i = tid; i < cn; i += NTC) {
+      p.pj_acc[t0 + i] = la[cb * CMAX + i];
+      p.pj_ptr[t0 + i] = lp[cb * CMAX + i];
     }
   }
   grid.sync();
