@@ -804,6 +804,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
     }
     __syncthreads();
   }
+  FZ_TRACE(9);
   {
     // unresolved tiles (or every tile when the chunk is too long for shared memory)
     const int cnt = local ? nun : (t1 - t0);
@@ -824,6 +825,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
       }
     }
   }
+  FZ_TRACE(10);
   if (local && !p.nobox) {
     // pointer jumping inside the chunk first (block barriers, shared memory):
     // the grid rounds of P4 then only follow pointers that leave the chunk
@@ -889,6 +891,7 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
     }
     p.nruns[T] = k;
   }
+  FZ_TRACE(8);
   if (p.nobox) return;  // matching only: no tile contexts
   float4* accb[2] = {p.pj_acc, p.pj_acc + nt};
   int* ptrb[2] = {p.pj_ptr, p.pj_ptr + nt};

@@ -108,14 +108,16 @@ def timing(log2n=27):
         per = {k: round(v[1] / v[0], 4) for k, v in json.loads(buf.value.decode()).items()}
         res["fused" if fused else "two-call"] = {"ms": round(ms, 4), "Gelem/s": round(n / ms / 1e6, 2), "kernels": per}
     lib.tb_debug_use_fused(1)
-    tr = torch.zeros(8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(16, dtype=torch.int64, device=dev)
     lib.tb_debug_fz_trace(tr.data_ptr())
     tb.paren_match_tree_bbox(tags, boxes, match, parent, out)
     torch.cuda.synchronize()
     lib.tb_debug_fz_trace(None)
     t = tr.cpu().tolist()
     res["fz_ctrl_phases_us"] = {"P0": (t[1] - t[0]) / 1e3, "P1": (t[2] - t[1]) / 1e3, "P2": (t[3] - t[2]) / 1e3,
-                                "P3": (t[4] - t[3]) / 1e3, "P4": (t[5] - t[4]) / 1e3, "P5": (t[7] - t[5]) / 1e3,
+                                "P3": (t[4] - t[3]) / 1e3, "P3_ansv": (t[9] - t[3]) / 1e3,
+                                "P3_unres": (t[10] - t[9]) / 1e3, "P3_jump": (t[4] - t[10]) / 1e3,
+                                "P4": (t[5] - t[4]) / 1e3, "P4_runs": (t[8] - t[4]) / 1e3, "P5": (t[7] - t[5]) / 1e3,
                                 "rounds": t[6]}
     print(json.dumps(res, indent=1), flush=True)
 
