@@ -76,6 +76,7 @@ def load():
                 "tb_debug_use_fused": ([ctypes.c_int], ctypes.c_int),
                 "tb_debug_fz_trace": ([P], ctypes.c_int),
                 "tb_debug_fz_tma": ([ctypes.c_int], ctypes.c_int),
+                "tb_debug_fz_ctrl_blocks": ([ctypes.c_int], ctypes.c_int),
                 "tb_debug_bins_cap": ([I64], I64),
                 "tree_bbox_shard": ([P, P, I64, I64, P, P, P], ctypes.c_int),
                 "paren_match_tree_bbox_shard": ([P, P, I64, I64, I64, P, P, P, P, P], ctypes.c_int),

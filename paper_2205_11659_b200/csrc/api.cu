@@ -678,6 +678,10 @@ int tb_debug_bb_tile(void) { return tb::bbm_tile_elems(); }
 
 int tb_debug_fz_tma(int on) { return tb::fused_set_tma(on); }
 
+/* Debug: cap the fused control kernel's blocks at g (0 = the co-resident count); returns the old cap.
+ * Few blocks make long chunks: more than 1024 tiles per block takes the global owner-search path. */
+int tb_debug_fz_ctrl_blocks(int g) { return tb::fused_set_ctrl_blocks(g); }
+
 /* Debug: fz_ctrl phase timestamps (globaltimer ns, block 0) into dev_buf[0..10] (16 int64 slots); NULL turns it off. */
 int tb_debug_fz_trace(void* dev_buf) {
   tb::fused_set_trace((uint64_t*)dev_buf);

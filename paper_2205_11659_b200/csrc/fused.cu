@@ -2034,6 +2034,12 @@ static cudaError_t setup() {
 static uint64_t* g_fz_trace = nullptr;  // debug hook (tb_debug_fz_trace)
 void fused_set_trace(uint64_t* dev) { g_fz_trace = dev; }
 static int g_fz_tma = 1;  // debug hook (tb_debug_fz_tma): 0 = the threads copy every tile
+static int g_fz_ctrl_cap = 0;  // debug hook (tb_debug_fz_ctrl_blocks): at most this many fz_ctrl blocks (0: all)
+int fused_set_ctrl_blocks(int g) {
+  const int old = g_fz_ctrl_cap;
+  if (g >= 0) g_fz_ctrl_cap = g;
+  return old;
+}
 int fused_set_tma(int on) {
   const int old = g_fz_tma;
   if (on >= 0) g_fz_tma = on;
@@ -2074,7 +2080,8 @@ static cudaError_t launch_front(fz::Params& p, cudaStream_t stream) {
   if (e != cudaSuccess) return e;
   // enough blocks for the per-tile warps of P3 / P5, at most the co-resident
   // count; chunks of whole 32-tile groups
-  const int G = std::max(1, std::min((nt + 31) / 32, fz::ctrl_blocks()));
+  const int cbk = g_fz_ctrl_cap > 0 ? std::min(g_fz_ctrl_cap, fz::ctrl_blocks()) : fz::ctrl_blocks();
+  const int G = std::max(1, std::min((nt + 31) / 32, cbk));
   p.chunk = (((nt + G - 1) / G) + 31) & ~31;
   void* args[] = {(void*)&p};
   void* tok;

@@ -72,6 +72,7 @@ struct ShardOpen {
 size_t fused_workspace_bytes(int64_t n);
 void fused_set_trace(uint64_t* dev);  // debug: fz_ctrl phase timestamps (8 x u64 device buffer) or null
 int fused_set_tma(int on);
+int fused_set_ctrl_blocks(int g);
 // the fused pass over one chunk of a sharded stream (fused_shard.cuh): three
 // phases around two fixed-size exchanges of slot1 / slot2 (cap: the largest
 // Bic a + 1 and b of a chunk; equal on every rank)
