@@ -152,10 +152,11 @@ __global__ void __launch_bounds__(NT) tf_tile(Params p) {
   M P = mid();
   {
     // the innermost open in-thread node's product in a register (tp), the
-    // enclosing ones below it (stk, depth d - 1); every element runs the same
-    // predicated sequence: a leaf multiplies P and tp, an open of an in-thread
-    // node pushes, its close pops
-    M stk[K / 2];
+    // enclosing ones below it (entry j of thread t in dl[j][t]: the sparse
+    // table is built after the walk; the bank depends on t only); every element
+    // runs the same predicated sequence: a leaf multiplies P and tp, an open
+    // of an in-thread node pushes, its close pops
+    static_assert(DL >= K / 2, "the walk's stack lives in dl");
     M tp = mid();
     int d = 0;
 #pragma unroll
@@ -168,14 +169,14 @@ __global__ void __launch_bounds__(NT) tf_tile(Params p) {
       P = mul(P, v);
       const M tv = mul(tp, v);
       if (push) {
-        if (d > 0) stk[d - 1] = tp;
+        if (d > 0) s.dl[d - 1][tid] = tp;
         d++;
         tp = mid();
       } else if (pop) {
         s.xs[slot(tid, i)] = tv;
         s.xs[slot(tid, (int)(o - gb))] = tv;
         d--;
-        tp = d > 0 ? mul(stk[d - 1], tv) : mid();
+        tp = d > 0 ? mul(s.dl[d - 1][tid], tv) : mid();
       } else {
         tp = tv;
         if (isc) s.xs[slot(tid, i)] = o < 0 ? mid() : P;  // R3; or the thread prefix before the close (pass 2)
