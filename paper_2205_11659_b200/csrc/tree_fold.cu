@@ -273,38 +273,42 @@ __global__ void __launch_bounds__(NT) tf_tile(Params p) {
   }
 }
 
-__global__ void __launch_bounds__(256) tf_hier(Params p, int k, int m /* nodes at level k - 1 */) {
+__global__ void __launch_bounds__(256) tf_hier(const M* src, M* dst, int m /* nodes at level k - 1 */) {
   const int lane = threadIdx.x & 31;
   const int g = blockIdx.x * 8 + (threadIdx.x >> 5);
   if ((g << 5) >= m) return;
   const int c = (g << 5) + lane;
-  const M v = warp_prod(c < m ? __ldcg(p.tp[k - 1] + c) : mid());
-  if (lane == 0) p.tp[k][g] = v;
+  const M v = warp_prod(c < m ? __ldcg(src + c) : mid());
+  if (lane == 0) dst[g] = v;
 }
 
 // ordered product of tiles a .. b by one thread (a > b: identity): disjoint
 // pieces, a's partial group and b's partial group at each level
-__device__ M range_tiles(const Params& p, int a, int b) {
+__device__ __forceinline__ M range_tiles(const Params& p, int a, int b) {
   M left = mid(), right = mid();
-  for (int k = 0; k < LV && a <= b; k++) {
-    if ((a >> 5) == (b >> 5)) {
-      for (int i = a; i <= b; i++) left = mul(left, __ldcg(p.tp[k] + i));
-      a = b + 1;
-      break;
-    }
-    if (a & 31) {
-      for (int i = a; i <= (a | 31); i++) left = mul(left, __ldcg(p.tp[k] + i));
-      a = (a >> 5) + 1;
-    } else {
-      a >>= 5;
-    }
-    if ((b & 31) != 31) {
-      M r = mid();
-      for (int i = b & ~31; i <= b; i++) r = mul(r, __ldcg(p.tp[k] + i));
-      right = mul(r, right);
-      b = (b >> 5) - 1;
-    } else {
-      b >>= 5;
+#pragma unroll
+  for (int k = 0; k < LV; k++) {  // unrolled: p.tp[k] stays a parameter-space load
+    if (a <= b) {
+      const M* t = p.tp[k];
+      if ((a >> 5) == (b >> 5)) {
+        for (int i = a; i <= b; i++) left = mul(left, __ldcg(t + i));
+        a = b + 1;
+      } else {
+        if (a & 31) {
+          for (int i = a; i <= (a | 31); i++) left = mul(left, __ldcg(t + i));
+          a = (a >> 5) + 1;
+        } else {
+          a >>= 5;
+        }
+        if ((b & 31) != 31) {
+          M r = mid();
+          for (int i = b & ~31; i <= b; i++) r = mul(r, __ldcg(t + i));
+          right = mul(r, right);
+          b = (b >> 5) - 1;
+        } else {
+          b >>= 5;
+        }
+      }
     }
   }
   return mul(left, right);
@@ -377,7 +381,7 @@ cudaError_t tf_launch(const uint8_t* tags, const uint32_t* x, const int32_t* mat
   int m = nt;
   for (int k = 1; k < tf::LV && m > 1; k++) {
     const int groups = (m + 31) / 32;
-    TB_LAUNCH(stream, "tf_hier", (tf::tf_hier<<<(unsigned)((groups + 7) / 8), 256, 0, stream>>>(p, k, m)));
+    TB_LAUNCH(stream, "tf_hier", (tf::tf_hier<<<(unsigned)((groups + 7) / 8), 256, 0, stream>>>(p.tp[k - 1], p.tp[k], m)));
     m = groups;
   }
   TB_LAUNCH(stream, "tf_cross", (tf::tf_cross<<<(unsigned)((nt + 3) / 4), 128, 0, stream>>>(p)));
