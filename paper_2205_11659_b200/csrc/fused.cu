@@ -893,22 +893,24 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   }
   FZ_TRACE(8);
   if (p.nobox) return;  // matching only: no tile contexts
-  float4* accb[2] = {p.pj_acc, p.pj_acc + nt};
-  int* ptrb[2] = {p.pj_ptr, p.pj_ptr + nt};
+  // the two buffers of each array by selects (a runtime index into a pointer
+  // array would place it in local memory)
+  auto accb = [&](int b) { return b ? p.pj_acc + nt : p.pj_acc; };
+  auto ptrb = [&](int b) { return b ? p.pj_ptr + nt : p.pj_ptr; };
   int cb = 0;
   for (int round = 0; round < 64; round++) {
     if (gt == 0) p.flag[(round + 1) % 3] = 0;
     int any = 0;
     for (int V = gt; V < nt; V += nthr) {
-      float4 a = __ldcg(accb[cb] + V);
-      int q = __ldcg(ptrb[cb] + V);
+      float4 a = __ldcg(accb(cb) + V);
+      int q = __ldcg(ptrb(cb) + V);
       if (q >= 0) {
-        a = isect(a, __ldcg(accb[cb] + q));
-        q = __ldcg(ptrb[cb] + q);
+        a = isect(a, __ldcg(accb(cb) + q));
+        q = __ldcg(ptrb(cb) + q);
         any |= q >= 0;
       }
-      accb[cb ^ 1][V] = a;
-      ptrb[cb ^ 1][V] = q;
+      accb(cb ^ 1)[V] = a;
+      ptrb(cb ^ 1)[V] = q;
     }
     any = __syncthreads_or(any);
     if (any && tid == 0) atomicOr(p.flag + round % 3, 1);
@@ -922,8 +924,8 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   FZ_TRACE(5);
   // P5: TC for the main pass (slice context = lc ∩ TC of the slice's tile)
   for (int V = gt; V < nt; V += nthr) {
-    p.tc[V] = __ldcg(accb[cb] + V);
-    p.tcend[V] = __ldcg(ptrb[cb] + V);  // -1, or -2 - h: TC still lacks imported height h's context
+    p.tc[V] = __ldcg(accb(cb) + V);
+    p.tcend[V] = __ldcg(ptrb(cb) + V);  // -1, or -2 - h: TC still lacks imported height h's context
   }
   FZ_TRACE(7);
 }

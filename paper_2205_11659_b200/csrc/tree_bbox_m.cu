@@ -353,8 +353,9 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
   const int nt = p.ntiles, t0 = p.t0, t1 = p.t1;
   const int gt = (int)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
   const int nthr = (int)(gridDim.x * (int64_t)blockDim.x);
-  float4* acc[2] = {acc2, acc2 + nt};
-  int* ptr[2] = {ptr2, ptr2 + nt};
+  // the two buffers by selects (a runtime index into a pointer array would place it in local memory)
+  auto acc = [&](int b) { return b ? acc2 + nt : acc2; };
+  auto ptr = [&](int b) { return b ? ptr2 + nt : ptr2; };
   for (int V = t0 + gt; V < t1; V += nthr) {
     const int f = __ldg(p.link + V);  // the tile's first slice entry (local), -1: none
     const int X = f >= 0 ? __ldg(p.parent + (int64_t)V * TILE + f) : -1;  // its parent: global index
@@ -372,8 +373,8 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
     } else if (X >= 0) {
       a = ext_ctx(p, X);
     }
-    acc[0][V] = a;
-    ptr[0][V] = q;
+    acc(0)[V] = a;
+    ptr(0)[V] = q;
   }
   int cb = 0;
   for (int round = 0; round < 40; round++) {
@@ -381,15 +382,15 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
     grid.sync();
     int any = 0;
     for (int V = t0 + gt; V < t1; V += nthr) {
-      float4 a = __ldcg(acc[cb] + V);
-      int q = __ldcg(ptr[cb] + V);
+      float4 a = __ldcg(acc(cb) + V);
+      int q = __ldcg(ptr(cb) + V);
       if (q >= 0) {
-        a = isect(a, __ldcg(acc[cb] + q));
-        q = __ldcg(ptr[cb] + q);
+        a = isect(a, __ldcg(acc(cb) + q));
+        q = __ldcg(ptr(cb) + q);
         any |= q >= 0;
       }
-      acc[cb ^ 1][V] = a;
-      ptr[cb ^ 1][V] = q;
+      acc(cb ^ 1)[V] = a;
+      ptr(cb ^ 1)[V] = q;
     }
     any = __syncthreads_or(any);
     if (any && threadIdx.x == 0) atomicOr(flag + (round & 1), 1);
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(256) bbm_tc(Params p, float4* acc2, int* ptr2,
     grid.sync();
     if (__ldcg(flag + (round & 1)) == 0) break;
   }
-  for (int V = t0 + gt; V < t1; V += nthr) p.tc[V] = __ldcg(acc[cb] + V);
+  for (int V = t0 + gt; V < t1; V += nthr) p.tc[V] = __ldcg(acc(cb) + V);
 }
 
 // ----------------------------------------------------------------------------

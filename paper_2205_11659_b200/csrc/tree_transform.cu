@@ -127,12 +127,13 @@ __global__ void __launch_bounds__(256) tt_tc(Params p, Xf* acc2, int* ptr2, int*
   const int nt = p.ntiles;
   const int gt = (int)(blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
   const int nthr = (int)(gridDim.x * (int64_t)blockDim.x);
-  Xf* acc[2] = {acc2, acc2 + nt};
-  int* ptr[2] = {ptr2, ptr2 + nt};
+  // the two buffers by selects (a runtime index into a pointer array would place it in local memory)
+  auto acc = [&](int b) { return b ? acc2 + nt : acc2; };
+  auto ptr = [&](int b) { return b ? ptr2 + nt : ptr2; };
   for (int V = gt; V < nt; V += nthr) {
     const int X = __ldg(p.link + V);
-    acc[0][V] = X >= 0 ? p.lcg[X] : xf_id();
-    ptr[0][V] = X >= 0 ? X / TILE : -1;
+    acc(0)[V] = X >= 0 ? p.lcg[X] : xf_id();
+    ptr(0)[V] = X >= 0 ? X / TILE : -1;
   }
   int cb = 0;
   for (int round = 0; round < 40; round++) {
@@ -140,15 +141,15 @@ __global__ void __launch_bounds__(256) tt_tc(Params p, Xf* acc2, int* ptr2, int*
     grid.sync();
     int any = 0;
     for (int V = gt; V < nt; V += nthr) {
-      Xf a = acc[cb][V];
-      int q = __ldcg(ptr[cb] + V);
+      Xf a = acc(cb)[V];
+      int q = __ldcg(ptr(cb) + V);
       if (q >= 0) {
-        a = compose(acc[cb][q], a);  // the earlier context on the left
-        q = __ldcg(ptr[cb] + q);
+        a = compose(acc(cb)[q], a);  // the earlier context on the left
+        q = __ldcg(ptr(cb) + q);
         any |= q >= 0;
       }
-      acc[cb ^ 1][V] = a;
-      ptr[cb ^ 1][V] = q;
+      acc(cb ^ 1)[V] = a;
+      ptr(cb ^ 1)[V] = q;
     }
     any = __syncthreads_or(any);
     if (any && threadIdx.x == 0) atomicOr(flag + (round & 1), 1);
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(256) tt_tc(Params p, Xf* acc2, int* ptr2, int*
     grid.sync();
     if (__ldcg(flag + (round & 1)) == 0) break;
   }
-  for (int V = gt; V < nt; V += nthr) p.tc[V] = acc[cb][V];
+  for (int V = gt; V < nt; V += nthr) p.tc[V] = acc(cb)[V];
 }
 
 // Shared memory holds the tile's transforms as six float arrays (SoA); thread t's
