@@ -16,9 +16,10 @@ for r in csv.reader(out.splitlines()):
     if r[0] == "File Path": cur = r[1].split("/")[-1]; continue
     if r[0] == "Line No": idx = {n: i for i, n in enumerate(r)}; continue
     if idx and len(r) > 10 and r[2] == "-":
-        recs.append(dict(file=cur, line=r[0], src=r[1].strip(), instr=f(r[idx["Instructions Executed"]]),
-                         thr=f(r[idx["Thread Instructions Executed"]]), stall=f(r[idx["Warp Stall Sampling (All Samples)"]]),
-                         conf=f(r[idx["L1 Wavefronts Shared Excessive"]])))
+        col = lambda name: f(r[idx[name]]) if name in idx else 0.0  # absent when the kernel has no such traffic
+        recs.append(dict(file=cur, line=r[0], src=r[1].strip(), instr=col("Instructions Executed"),
+                         thr=col("Thread Instructions Executed"), stall=col("Warp Stall Sampling (All Samples)"),
+                         conf=col("L1 Wavefronts Shared Excessive")))
 ti = sum(x["instr"] for x in recs) or 1; ts = sum(x["stall"] for x in recs) or 1; tc = sum(x["conf"] for x in recs) or 1
 print(f"warp-instr {ti:.3g}  stall samples {ts:.3g}  excess shared wavefronts {tc:.3g}")
 for x in sorted(recs, key=lambda x: -x[key])[:top]:
