@@ -897,20 +897,41 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   // array would place it in local memory)
   auto accb = [&](int b) { return b ? p.pj_acc + nt : p.pj_acc; };
   auto ptrb = [&](int b) { return b ? p.pj_ptr + nt : p.pj_ptr; };
+  // at most one tile per thread (nt <= threads of the grid, n <= 3.1e8 on a
+  // B200): its value and pointer stay in registers across the rounds
+  const bool one = nt <= nthr;
+  float4 ra = bINF();
+  int rq = -1;
+  if (one && gt < nt) {
+    ra = __ldcg(accb(0) + gt);
+    rq = __ldcg(ptrb(0) + gt);
+  }
   int cb = 0;
   for (int round = 0; round < 64; round++) {
     if (gt == 0) p.flag[(round + 1) % 3] = 0;
     int any = 0;
-    for (int V = gt; V < nt; V += nthr) {
-      float4 a = __ldcg(accb(cb) + V);
-      int q = __ldcg(ptrb(cb) + V);
-      if (q >= 0) {
-        a = isect(a, __ldcg(accb(cb) + q));
-        q = __ldcg(ptrb(cb) + q);
-        any |= q >= 0;
+    if (one) {
+      if (rq >= 0) {
+        ra = isect(ra, __ldcg(accb(cb) + rq));
+        rq = __ldcg(ptrb(cb) + rq);
+        any = rq >= 0;
       }
-      accb(cb ^ 1)[V] = a;
-      ptrb(cb ^ 1)[V] = q;
+      if (gt < nt) {
+        accb(cb ^ 1)[gt] = ra;
+        ptrb(cb ^ 1)[gt] = rq;
+      }
+    } else {
+      for (int V = gt; V < nt; V += nthr) {
+        float4 a = __ldcg(accb(cb) + V);
+        int q = __ldcg(ptrb(cb) + V);
+        if (q >= 0) {
+          a = isect(a, __ldcg(accb(cb) + q));
+          q = __ldcg(ptrb(cb) + q);
+          any |= q >= 0;
+        }
+        accb(cb ^ 1)[V] = a;
+        ptrb(cb ^ 1)[V] = q;
+      }
     }
     any = __syncthreads_or(any);
     if (any && tid == 0) atomicOr(p.flag + round % 3, 1);
@@ -923,9 +944,16 @@ __global__ void __launch_bounds__(NTC, 1) fz_ctrl(Params p) {
   }
   FZ_TRACE(5);
   // P5: TC for the main pass (slice context = lc ∩ TC of the slice's tile)
-  for (int V = gt; V < nt; V += nthr) {
-    p.tc[V] = __ldcg(accb(cb) + V);
-    p.tcend[V] = __ldcg(ptrb(cb) + V);  // -1, or -2 - h: TC still lacks imported height h's context
+  if (one) {
+    if (gt < nt) {
+      p.tc[gt] = ra;
+      p.tcend[gt] = rq;  // -1, or -2 - h: TC still lacks imported height h's context
+    }
+  } else {
+    for (int V = gt; V < nt; V += nthr) {
+      p.tc[V] = __ldcg(accb(cb) + V);
+      p.tcend[V] = __ldcg(ptrb(cb) + V);
+    }
   }
   FZ_TRACE(7);
 }
