@@ -1013,6 +1013,46 @@ __device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
   return w;
 }
 
+// fz_match's walk: as walk(), but an in-thread open's match is stored at its
+// pop (mrow[i] = element i's match slot) instead of kept as a partner nibble,
+// and no blend mask (the matching alone has no boxes)
+__device__ __forceinline__ Walk walk_m(uint4 raw, uint32_t valid, int32_t* mrow, int gtb) {
+  Walk w;
+  classify16(raw, w.om, w.cm);
+  w.om &= valid;
+  w.cm &= valid;
+  w.bm = 0u;
+  w.lm = valid & ~(w.om | w.cm);
+  uint32_t S = 0, plo = 0, phi = 0, ext = 0;
+#pragma unroll 1
+  for (int q = 0; q < K / 4; q++) {
+    const int i0 = 4 * q;
+    const uint32_t oq = w.om >> i0, cq = w.cm >> i0;
+    uint32_t gp = 0, gx = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int i = i0 + j;
+      const int top = 31 - __clz(S);  // -1 when the thread stack is empty
+      gp |= (uint32_t)(top & 15) << (4 * j);
+      gx |= S ? 0u : (1u << j);
+      const bool pop = ((cq >> j) & 1u) && S;
+      if (pop) mrow[top] = gtb + i;
+      S = ((oq >> j) & 1u) ? (S | (1u << i)) : (pop ? (S ^ (1u << top)) : S);
+    }
+    const int sh = 16 * (q & 1);
+    if (q < 2) plo |= gp << sh;
+    else phi |= gp << sh;
+    ext |= gx << i0;
+  }
+  w.S = S;
+  w.plo = plo;
+  w.phi = phi;
+  w.mlo = w.mhi = 0u;
+  w.ext = ext;
+  w.ucm = w.cm & ext;
+  return w;
+}
+
 constexpr int RCAP = 7;      // segment unions kept per thread (more unmatched opens: recomputed in H1)
 constexpr int INCCAP = 192;  // incoming entries cached in shared memory (deeper ones: read from global)
 
@@ -1680,7 +1720,7 @@ __global__ void __launch_bounds__(NT) fz_match(Params p) {
   const int nruns = __ldg(p.nruns + T);
   const int nv_t = nvalid - tl0;
   const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
-  const Walk w = walk(raw, valid);
+  const Walk w = walk_m(raw, valid, s.matchS + mb, gtb);  // in-thread opens' matches stored here
   const int a_t = __popc(w.ucm);
 
   // B. block Bic scan; thread low-water windows
@@ -1786,18 +1826,18 @@ __global__ void __launch_bounds__(NT) fz_match(Params p) {
   for (int q = 0; q < K / 4; q++) {
     const int i0 = 4 * q;
     const uint32_t Lq = w.lm >> i0, Uq = w.ucm >> i0, Sq = w.S >> i0, Xq = w.ext >> i0;
-    const uint32_t pwq = (q < 2 ? w.plo : w.phi) >> (16 * (q & 1)), mwq = (q < 2 ? w.mlo : w.mhi) >> (16 * (q & 1));
+    const uint32_t pwq = (q < 2 ? w.plo : w.phi) >> (16 * (q & 1)), Oq = w.om >> i0;
     int pv[4];
 #pragma unroll
     for (int jq = 0; jq < 4; jq++) {
       const int i = i0 + jq;
       const bool isL = (Lq >> jq) & 1u, isU = (Uq >> jq) & 1u, isUO = (Sq >> jq) & 1u, isx = (Xq >> jq) & 1u;
       const int pn = (int)((pwq >> (4 * jq)) & 15u);
-      const int pt = ((w.cm >> i) & 1u) ? pn : (int)((mwq >> (4 * jq)) & 15u);  // a close's partner is its parent
+      const bool isO = (Oq >> jq) & 1u;  // an in-thread open's match was stored by the walk
       const uint32_t nc = Uq >> jq;
       const int j = nc ? i + __ffs(nc) - 1 : K - 1;
       pv[jq] = isx ? (nc ? s.matchS[mb + j] : giLast) : gtb + pn;
-      if (!(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + pt;
+      if (!(isUO || isU || isO)) s.matchS[mb + i] = isL ? -1 : gtb + pn;  // a close's partner is its parent
     }
     if (nv_t >= 4 * q + 4) {
       __stcs(reinterpret_cast<int4*>(p.parent + base + tl0) + q, make_int4(pv[0], pv[1], pv[2], pv[3]));
