@@ -965,63 +965,27 @@ struct Walk {
   uint32_t om, cm, bm, lm;  // opens, closes, blend opens, leaves (valid elements only)
   uint32_t S;               // opens still on the thread stack at its end (thread-unmatched)
   uint32_t plo, phi;        // nibble i: in-thread parent of element i (a matched close: its open)
-  uint32_t mlo, mhi;        // nibble i: in-thread close of open i (matched opens only)
   uint32_t ext;             // elements whose parent lies before the thread
   uint32_t ucm;             // closes with no in-thread open (they pop the stack at the thread start)
 };
 
 // Fig. 1 over the thread's 16 elements with a bitmask stack (four
-// groups of four elements: a rolled outer loop keeps the code small)
-__device__ __forceinline__ Walk walk(uint4 raw, uint32_t valid) {
+// groups of four elements: a rolled outer loop keeps the code small).  An
+// in-thread open's match is stored at its pop (mrow[i] = element i's match
+// slot: gtb + its close); BM: the blend-open mask too (fz_main; the matching
+// alone has no boxes)
+template <bool BM>
+__device__ __forceinline__ Walk walk_m(uint4 raw, uint32_t valid, int32_t* mrow, int gtb) {
   Walk w;
-  classify16b(raw, w.om, w.cm, w.bm);
+  if (BM) {
+    classify16b(raw, w.om, w.cm, w.bm);
+  } else {
+    classify16(raw, w.om, w.cm);
+    w.bm = 0u;
+  }
   w.om &= valid;
   w.cm &= valid;
   w.bm &= valid;
-  w.lm = valid & ~(w.om | w.cm);
-  uint32_t S = 0, plo = 0, phi = 0, mlo = 0, mhi = 0, ext = 0;
-#pragma unroll 1
-  for (int q = 0; q < K / 4; q++) {
-    const int i0 = 4 * q;
-    const uint32_t oq = w.om >> i0, cq = w.cm >> i0;  // bit tests below use immediates
-    uint32_t gp = 0, gx = 0;                         // the group's nibbles / bits
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int i = i0 + j;
-      const int top = 31 - __clz(S);  // -1 when the thread stack is empty
-      gp |= (uint32_t)(top & 15) << (4 * j);
-      gx |= S ? 0u : (1u << j);
-      const bool pop = ((cq >> j) & 1u) && S;
-      // the open's partner nibble, written at the pop (a close's partner is its parent)
-      const uint32_t pv = pop ? (uint32_t)i << (4 * (top & 7)) : 0u;
-      mlo |= top < 8 ? pv : 0u;
-      mhi |= top >= 8 ? pv : 0u;
-      S = ((oq >> j) & 1u) ? (S | (1u << i)) : (pop ? (S ^ (1u << top)) : S);
-    }
-    const int sh = 16 * (q & 1);
-    if (q < 2) plo |= gp << sh;
-    else phi |= gp << sh;
-    ext |= gx << i0;
-  }
-  w.S = S;
-  w.plo = plo;
-  w.phi = phi;
-  w.mlo = mlo;
-  w.mhi = mhi;
-  w.ext = ext;
-  w.ucm = w.cm & ext;  // closes met with an empty thread stack
-  return w;
-}
-
-// fz_match's walk: as walk(), but an in-thread open's match is stored at its
-// pop (mrow[i] = element i's match slot) instead of kept as a partner nibble,
-// and no blend mask (the matching alone has no boxes)
-__device__ __forceinline__ Walk walk_m(uint4 raw, uint32_t valid, int32_t* mrow, int gtb) {
-  Walk w;
-  classify16(raw, w.om, w.cm);
-  w.om &= valid;
-  w.cm &= valid;
-  w.bm = 0u;
   w.lm = valid & ~(w.om | w.cm);
   uint32_t S = 0, plo = 0, phi = 0, ext = 0;
 #pragma unroll 1
@@ -1047,7 +1011,6 @@ __device__ __forceinline__ Walk walk_m(uint4 raw, uint32_t valid, int32_t* mrow,
   w.S = S;
   w.plo = plo;
   w.phi = phi;
-  w.mlo = w.mhi = 0u;
   w.ext = ext;
   w.ucm = w.cm & ext;
   return w;
@@ -1254,7 +1217,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
   const int nruns = __ldg(p.nruns + T);
   const int nv_t = nvalid - tl0;
   const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
-  const Walk w = walk(raw, valid);
+  const Walk w = walk_m<true>(raw, valid, s.matchS + mb, gtb);  // an in-thread open's close: matchS[mb + i] - gtb
   const int a_t = __popc(w.ucm), b_t = __popc(w.S);
 
   // ---- B. block Bic scan: relative height at the thread start, low-water mark
@@ -1468,7 +1431,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
       const int i0 = 4 * q;
       const uint32_t Lq = w.lm >> i0, Bq = w.bm >> i0, Oq = w.om >> i0, Cq = w.cm >> i0, Uq = w.ucm >> i0;
       const uint32_t Sq = w.S >> i0, Xq = w.ext >> i0;
-      const uint32_t pwq = (q < 2 ? w.plo : w.phi) >> (16 * (q & 1)), mwq = (q < 2 ? w.mlo : w.mhi) >> (16 * (q & 1));
+      const uint32_t pwq = (q < 2 ? w.plo : w.phi) >> (16 * (q & 1));
       const int kq = __popc(w.S & ((1u << i0) - 1u));      // thread-unmatched opens before the group
       const int sbq = ((q >> 1) << 10) | (sb ^ ((q & 1) << 2));  // slot of element i0 + jq = sbq ^ jq
       int pv[4];
@@ -1483,7 +1446,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         float4 v = s.val[si];
         if (jq == 3 && q == K / 4 - 1 && !isMC) v = v15;
         const int pn = (int)((pwq >> (4 * jq)) & 15u);
-        const int pt = isC ? pn : (int)((mwq >> (4 * jq)) & 15u);  // a close's partner is its parent
+        const int pt = isC ? pn : s.matchS[mb + i] - gtb;  // a close's partner is its parent; an open's, from the walk
         const bool isx = (Xq >> jq) & 1u;
         const uint32_t nc = Uq >> jq;                        // unmatched closes at or after i
         const int j = nc ? i + __ffs(nc) - 1 : K - 1;        // the next one: c_d of element i's depth d (none: TL)
@@ -1508,7 +1471,7 @@ __global__ void __launch_bounds__(NT, FZ_MINB) fz_main(Params p, const __grid_co
         const float4 add = (isL || isMC) ? clipped : bEMPTY();
         acc = unite(acc, add);
         acc = isO ? bEMPTY() : acc;
-        if (PM && !(isUO || isU)) s.matchS[mb + i] = isL ? -1 : gtb + pt;
+        if (PM && !(isUO || isU || isO)) s.matchS[mb + i] = isL ? -1 : gtb + pt;  // in-thread opens: stored by the walk
         pv[jq] = par;
       }
       if (PM) {
@@ -1720,7 +1683,7 @@ __global__ void __launch_bounds__(NT) fz_match(Params p) {
   const int nruns = __ldg(p.nruns + T);
   const int nv_t = nvalid - tl0;
   const uint32_t valid = nv_t >= K ? 0xffffu : (nv_t <= 0 ? 0u : ((1u << nv_t) - 1u));
-  const Walk w = walk_m(raw, valid, s.matchS + mb, gtb);  // in-thread opens' matches stored here
+  const Walk w = walk_m<false>(raw, valid, s.matchS + mb, gtb);  // in-thread opens' matches stored here
   const int a_t = __popc(w.ucm);
 
   // B. block Bic scan; thread low-water windows
