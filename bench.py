@@ -114,6 +114,11 @@ class ClockSampler:
             return
         self.th = threading.Thread(target=self._read, daemon=True)
         self.th.start()
+        # the timed region starts once nvidia-smi is sampling (a short region
+        # would otherwise end before its first sample)
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+            time.sleep(0.01)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -122,7 +127,10 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        n0 = len(self.lines)
+        t0 = time.time()  # at least one sample at or after the end of the region
+        while len(self.lines) <= n0 and time.time() - t0 < 1.0 and self.proc.poll() is None:
+            time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
